@@ -1,0 +1,162 @@
+/*
+ * hx_b200.h -- C-ABI of the B200 (sm_100a) CKKS hot-path library libhx_b200.so.
+ *
+ * This is the device boundary below the C++ helix API (include/helix/): the
+ * GPU SlotBackend (helix::GpuLatticeBackend) and the linear-transform entry
+ * points call only these functions.  Plain pointers and sizes, no torch or
+ * C++ types.  Every entry point replaces a reference routine of
+ * /root/reference/proj (cited per function); the ones marked SPEC have no
+ * reference code (the lattice backend and kernels are missing from the
+ * reference tree, proj/CMakeLists.txt:20-26) and follow SPEC.md.
+ *
+ * Conventions (pinned):
+ *  - A poly is u64 [limbs][N]; limb k < n_q is chain prime q_k, limb
+ *    n_q + k is special prime p_k.  Residues in [0, q).  Batches are
+ *    contiguous: [batch][limbs][N].  Ciphertexts are [2][n_q][N] (c0, c1),
+ *    NTT domain (the reference's bit-reversed NttTables::forward layout).
+ *  - A switching key is [dnum_max][2][n_chain + K][N] over the full basis
+ *    (dnum_max = ceil(n_chain / alpha)); hx_key_words() gives its size.
+ *  - Rotation by k slots (left) uses Galois element g = 5^k mod 2N.
+ *  - All device pointers are device memory; `stream` is a cudaStream_t
+ *    (NULL = legacy default stream).  Calls are asynchronous on `stream`
+ *    unless stated otherwise and reentrant for distinct buffers.
+ *  - Errors: every int-returning call returns HX_OK (0) or an HX_ERR_*
+ *    code and records a message readable with hx_last_error() (thread-local).
+ *    There is no CPU fallback: without a usable sm_100 device every compute
+ *    call fails with HX_ERR_CUDA.
+ */
+#ifndef HX_B200_H
+#define HX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HX_OK 0
+#define HX_ERR_INVALID 1
+#define HX_ERR_CUDA 2
+#define HX_ERR_UNSUPPORTED 3
+
+typedef struct hx_ctx hx_ctx;
+
+const char* hx_last_error(void);
+const char* hx_version(void);
+
+/* ---- context ------------------------------------------------------------
+ * Replaces LatticeContext(const CkksParams&) (rns_poly.cpp:11-22) and the
+ * NttTables ctor (ntt.cpp:36-55): per-prime psi (reference root search,
+ * ntt.cpp:23-32), twiddle tables with Shoup companions, Barrett/Shoup
+ * constants, ModUp/ModDown/rescale basis-conversion constants.  Unlike the
+ * reference (one special prime, rns_poly.cpp:14-15) any K >= 1 special primes
+ * and digit size alpha >= 1 are accepted.  logn in [8, 16]. */
+hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64_t* special,
+                      int n_special, int alpha);
+void hx_ctx_destroy(hx_ctx* ctx);
+int hx_ctx_dnum(const hx_ctx* ctx, int n_q);
+uint64_t hx_ctx_psi(const hx_ctx* ctx, int prime_index);
+size_t hx_key_words(const hx_ctx* ctx);
+/* number of kernels this context has launched so far (bench evidence) */
+unsigned long long hx_ctx_launches(const hx_ctx* ctx);
+
+/* ---- memory / streams ---- */
+int hx_malloc(void** ptr, size_t bytes);
+int hx_free(void* ptr);
+int hx_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
+int hx_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
+int hx_stream_sync(void* stream);
+int hx_device_sync(void);
+
+/* ---- RNS arithmetic ------------------------------------------------------ */
+/* NttTables::forward / inverse per limb = LatticeContext::to_ntt / to_coeff
+ * (ntt.cpp:57-96, rns_poly.cpp:42-54), in place over [batch][n_q+n_p][N]. */
+int hx_ntt_fwd(hx_ctx* ctx, uint64_t* data, int batch, int n_q, int n_p, void* stream);
+int hx_ntt_inv(hx_ctx* ctx, uint64_t* data, int batch, int n_q, int n_p, void* stream);
+/* LatticeContext::add / sub / negate / mul / mul_acc (rns_poly.cpp:62-110) */
+int hx_add(hx_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int batch, int n_q,
+           int n_p, void* stream);
+int hx_sub(hx_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int batch, int n_q,
+           int n_p, void* stream);
+int hx_neg(hx_ctx* ctx, uint64_t* out, const uint64_t* a, int batch, int n_q, int n_p,
+           void* stream);
+int hx_mul(hx_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int batch, int n_q,
+           int n_p, void* stream);
+int hx_mul_acc(hx_ctx* ctx, uint64_t* acc, const uint64_t* a, const uint64_t* b, int batch,
+               int n_q, int n_p, void* stream);
+/* LatticeContext::automorphism (rns_poly.cpp:124-142), X -> X^g, applied in
+ * the NTT domain as a permutation. */
+int hx_automorphism(hx_ctx* ctx, uint64_t* out, const uint64_t* in, int batch, int n_q, int n_p,
+                    uint64_t galois, void* stream);
+/* LatticeContext::from_i64 (rns_poly.cpp:218-227): v is device int64 [batch][N] */
+int hx_from_i64(hx_ctx* ctx, uint64_t* out, const int64_t* v, int batch, int n_q, int n_p,
+                void* stream);
+/* LatticeContext::rescale_drop_last (rns_poly.cpp:144-162) on NTT-domain
+ * polys: in [batch][n_q][N] -> out [batch][n_q-1][N] (centred lift). */
+int hx_rescale(hx_ctx* ctx, uint64_t* out, const uint64_t* in, int batch, int n_q, void* stream);
+/* x mod q per limb for words < 2^64 (after an NCCL uint64 sum of partials) */
+int hx_reduce_mod_q(hx_ctx* ctx, uint64_t* data, int batch, int n_q, int n_p, void* stream);
+
+/* ---- hybrid key switching -------------------- */
+/* ModUp: c1 [batch][n_q][N] (NTT) -> digits [batch][dnum][n_q+K][N] (NTT) */
+int hx_modup(hx_ctx* ctx, uint64_t* digits, const uint64_t* c1, int batch, int n_q, void* stream);
+/* u [batch][2][n_q+K][N] = sum_d tau_g(D_d) (.) key_d ; galois 1 = none */
+int hx_ks_inner(hx_ctx* ctx, uint64_t* u, const uint64_t* digits, const uint64_t* key, int batch,
+                int n_q, uint64_t galois, void* stream);
+/* centred ModDown (K = 1: LatticeContext::moddown_special, rns_poly.cpp:164-180):
+ * u [polys][n_q+K][N] (NTT) -> out [polys][n_q][N] (NTT) */
+int hx_moddown(hx_ctx* ctx, uint64_t* out, const uint64_t* u, int polys, int n_q, void* stream);
+/* out [batch][2][n_q][N] with out0 + out1*s ~= in * s' (key for s') */
+int hx_keyswitch(hx_ctx* ctx, uint64_t* out, const uint64_t* in, const uint64_t* key, int batch,
+                 int n_q, void* stream);
+/* galois_rotate: out = (tau(c0) + u0, u1), u = KS(tau(c1)),
+ * ModUp hoisted before the automorphism.  in/out [batch][2][n_q][N]. */
+int hx_rotate(hx_ctx* ctx, uint64_t* out, const uint64_t* in, const uint64_t* key, int batch,
+              int n_q, uint64_t galois, void* stream);
+/* R rotations of each ciphertext sharing one ModUp.  keys: host array of R
+ * device key pointers; galois: host array of R elements.
+ * out [batch][R][2][n_q][N]. */
+int hx_rotate_hoisted(hx_ctx* ctx, uint64_t* out, const uint64_t* in,
+                      const uint64_t* const* keys, const uint64_t* galois, int R, int batch,
+                      int n_q, void* stream);
+/* tensor (LatticeContext::mul x4): a, b [batch][2][n_q][N] -> [batch][3][n_q][N] */
+int hx_tensor(hx_ctx* ctx, uint64_t* out3, const uint64_t* a, const uint64_t* b, int batch,
+              int n_q, void* stream);
+/* ct x ct with relinearisation: tensor + KS(d2) with the key for s^2 */
+int hx_mul_relin(hx_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b,
+                 const uint64_t* rlk, int batch, int n_q, void* stream);
+
+/* ---- BSGS linear transform ------------------------------ */
+/* inner [n2][2][n_q][N]: inner_j = sum_k diags[j*n1+k] (.) baby[k];
+ * baby [n1][2][n_q][N]; diags [n2*n1][diag_limbs][N] (first n_q limbs used). */
+int hx_bsgs_mac(hx_ctx* ctx, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,
+                int diag_limbs, int n1, int n2, int n_q, void* stream);
+
+/* ---- keys / encryption ------------------------ */
+/* ksk_d = (-a_d s + e_d + [P]_{q_i} s' on the chain limbs of digit d, a_d).
+ * s_full, sp_full [n_chain+K][N] NTT; a_full [dnum_max][n_chain+K][N];
+ * e [dnum_max][N] int64; all device. */
+int hx_keygen_ksk(hx_ctx* ctx, uint64_t* key, const uint64_t* s_full, const uint64_t* sp_full,
+                  const uint64_t* a_full, const int64_t* e, void* stream);
+/* ct = (m - a s + e, a), m/a [n_q][N] NTT, e [N] int64 (device) */
+int hx_encrypt_sk(hx_ctx* ctx, uint64_t* ct, const uint64_t* m, const uint64_t* s_full,
+                  const uint64_t* a, const int64_t* e, int n_q, void* stream);
+/* m = c0 + c1 s (NTT), ct [batch][2][n_q][N] -> m [batch][n_q][N] */
+int hx_decrypt(hx_ctx* ctx, uint64_t* m, const uint64_t* ct, const uint64_t* s_full, int batch,
+               int n_q, void* stream);
+
+/* ---- end-to-end entry points over HOST buffers ----------------------------
+ * The reference-facing calls a CPU caller makes: host (ideally pinned) input
+ * ciphertexts are copied in, processed with device-resident keys, and copied
+ * back, all on `stream`; the call returns after the result is in host memory. */
+int hx_rotate_host(hx_ctx* ctx, uint64_t* out_host, const uint64_t* in_host, const uint64_t* key,
+                   int batch, int n_q, uint64_t galois, void* stream);
+int hx_mul_relin_host(hx_ctx* ctx, uint64_t* out_host, const uint64_t* a_host,
+                      const uint64_t* b_host, const uint64_t* rlk, int batch, int n_q,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,56 @@
+// hx_internal.h -- host-side context and launcher prototypes shared by the
+// translation units of libhx_b200.so (not part of the public C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "hx_common.cuh"
+#include "hx_types.cuh"
+#include "hx_ntt.cuh"
+
+struct hx_ctx {
+  int logn = 0;
+  int n_chain = 0, n_special = 0, alpha = 1;
+  int device = 0;
+  std::vector<hx::u64> primes;  // chain then special
+  std::vector<hx::u64> psi;
+  // device memory
+  hx::PrimeConst* d_pc = nullptr;
+  ulonglong2* d_tw = nullptr;  // [n_total][2][N]
+  // ModUp constants: for each n_q in [1, n_chain] and digit d < dnum(n_q):
+  // qhinv [alpha] and conv [alpha][n_total]; offsets in units of SC.
+  hx::SC* d_modup = nullptr;
+  std::vector<std::vector<long long>> modup_qh_off, modup_cv_off;  // [n_q][d]
+  // ModDown constants
+  hx::SC* d_phinv = nullptr;   // [K]
+  hx::SC* d_pconv = nullptr;   // [K][n_chain]
+  hx::u64* d_pmodq = nullptr;  // [n_chain]
+  hx::SC* d_pinv = nullptr;    // [n_chain]
+  // Rescale constants: [l][i] for i < l
+  hx::SC* d_qlinv = nullptr;   // [n_chain][n_chain]
+  hx::u64* d_qlmod = nullptr;  // [n_chain][n_chain]
+  // launch counter (kernels issued through this context)
+  unsigned long long launches = 0;
+
+  int n_total() const { return n_chain + n_special; }
+  long long N() const { return 1ll << logn; }
+  int dnum(int n_q) const { return (n_q + alpha - 1) / alpha; }
+  int pidx(int k, int n_q) const { return k < n_q ? k : n_chain + (k - n_q); }
+};
+
+namespace hx {
+
+// limb table for an (n_q chain, n_p special) poly batch element with `stride`
+// limbs per element starting at limb offset `first`
+LimbTable make_table(const hx_ctx* c, int n_q, int n_p, int stride = -1, int first = 0);
+
+// NTT launchers (hx_ntt.cu)
+void ntt_forward(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
+void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
+
+void set_error(const std::string& msg);
+
+}  // namespace hx

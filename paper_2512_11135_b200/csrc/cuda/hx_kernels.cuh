@@ -1,0 +1,384 @@
+// hx_kernels.cuh -- device kernels other than the NTT (declared for the
+// launchers in hx_ops.cu).  Every kernel names the reference routine it
+// replaces.  Layout: u64 [batch][limbs][N], limb k of an (n_q, n_p) poly is
+// chain prime k for k < n_q, special prime k - n_q otherwise.
+#pragma once
+
+#include "hx_common.cuh"
+#include "hx_ntt.cuh"
+#include "hx_types.cuh"
+
+namespace hx {
+
+// ------------------------------------------------------------ elementwise
+enum class EwOp : int { Add = 0, Sub, Neg, Mul, MulAcc, Copy };
+
+struct EwArgs {
+  u64* out;
+  const u64* a;
+  const u64* b;
+  const PrimeConst* pc;
+  LimbTable lt;   // limbs of one batch element
+  int logn;
+  long long instances;
+};
+
+// add / sub / negate / mul / mul_acc (rns_poly.cpp:62-110), 2 words per thread
+template <EwOp OP>
+__global__ void ew_kernel(EwArgs A) {
+  const int per_limb = (1 << A.logn) / (2 * blockDim.x);
+  const long long inst = blockIdx.x / per_limb;
+  const int chunk = blockIdx.x % per_limb;
+  const long long b = inst / A.lt.count;
+  const int e = (int)(inst % A.lt.count);
+  const PrimeConst& P = A.pc[A.lt.prime[e]];
+  const u64 q = P.q;
+  const long long ofs = (b * A.lt.stride + A.lt.off[e]) * (1ll << A.logn) +
+                        2ll * (chunk * blockDim.x + threadIdx.x);
+  const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(A.a + ofs);
+  ulonglong2 y = make_ulonglong2(0, 0), r;
+  if (OP != EwOp::Neg && OP != EwOp::Copy) y = *reinterpret_cast<const ulonglong2*>(A.b + ofs);
+  if (OP == EwOp::Add) {
+    r.x = addmod(x.x, y.x, q);
+    r.y = addmod(x.y, y.y, q);
+  } else if (OP == EwOp::Sub) {
+    r.x = submod(x.x, y.x, q);
+    r.y = submod(x.y, y.y, q);
+  } else if (OP == EwOp::Neg) {
+    r.x = x.x ? q - x.x : 0;
+    r.y = x.y ? q - x.y : 0;
+  } else if (OP == EwOp::Mul) {
+    r.x = mulmod(x.x, y.x, P);
+    r.y = mulmod(x.y, y.y, P);
+  } else if (OP == EwOp::MulAcc) {
+    const ulonglong2 acc = *reinterpret_cast<const ulonglong2*>(A.out + ofs);
+    U128 z0{acc.x, 0}, z1{acc.y, 0};
+    mac128(z0, x.x, y.x);
+    mac128(z1, x.y, y.y);
+    r.x = reduce128(z0, P);
+    r.y = reduce128(z1, P);
+  } else {
+    r = x;
+  }
+  *reinterpret_cast<ulonglong2*>(A.out + ofs) = r;
+}
+
+// NTT-domain automorphism (rns_poly.cpp:124-142 restated as a permutation of
+// the bit-reversed evaluation vector): out[k] = in[perm_g(k)]
+__global__ void automorphism_kernel(EwArgs A, u32 g) {
+  const int per_limb = (1 << A.logn) / blockDim.x;
+  const long long inst = blockIdx.x / per_limb;
+  const int k = (blockIdx.x % per_limb) * blockDim.x + threadIdx.x;
+  const long long b = inst / A.lt.count;
+  const int e = (int)(inst % A.lt.count);
+  const long long base = (b * A.lt.stride + A.lt.off[e]) * (1ll << A.logn);
+  A.out[base + k] = __ldg(A.a + base + ntt_auto_index((u32)k, g, A.logn));
+}
+
+// from_i64 (rns_poly.cpp:218-227): small signed ints -> every limb.
+// v is [batch][N] int64; out [batch][limbs][N].
+__global__ void from_i64_kernel(u64* out, const long long* v, const PrimeConst* pc, LimbTable lt,
+                                int logn) {
+  const int per_limb = (1 << logn) / blockDim.x;
+  const long long inst = blockIdx.x / per_limb;
+  const int t = (blockIdx.x % per_limb) * blockDim.x + threadIdx.x;
+  const long long b = inst / lt.count;
+  const int e = (int)(inst % lt.count);
+  const u64 q = pc[lt.prime[e]].q;
+  const long long x = v[(b << logn) + t];
+  u64 r;
+  if (x >= 0) {
+    r = (u64)x % q;
+  } else {
+    const u64 m = (u64)(-x) % q;
+    r = m ? q - m : 0;
+  }
+  out[(b * lt.stride + lt.off[e]) * (1ll << logn) + t] = r;
+}
+
+// x mod q for values < 2^64 (after an NCCL uint64 sum of partial ciphertexts)
+__global__ void reduce_kernel(EwArgs A) {
+  const int per_limb = (1 << A.logn) / blockDim.x;
+  const long long inst = blockIdx.x / per_limb;
+  const int t = (blockIdx.x % per_limb) * blockDim.x + threadIdx.x;
+  const long long b = inst / A.lt.count;
+  const int e = (int)(inst % A.lt.count);
+  const PrimeConst& P = A.pc[A.lt.prime[e]];
+  const long long i = (b * A.lt.stride + A.lt.off[e]) * (1ll << A.logn) + t;
+  const u64 x = A.out[i];
+  A.out[i] = csub(x - mulhi64(x, P.onep) * P.q, P.q);
+}
+
+// ------------------------------------------------------------ key switching
+// ModUp basis conversion for one digit (non-centred FastBConv):
+//   x_i = [a_i * (Qhat_i)^-1]_{q_i},  y_j = sum_i x_i [Qhat_i]_{p_j}
+// coef: [batch][n_q][N] coefficient-domain c1; out: digit block
+// [batch][ext][N] (only non-digit limbs written, in coefficient domain)
+struct ModUpArgs {
+  const u64* coef;
+  u64* out;
+  const PrimeConst* pc;
+  const SC* qhinv;   // [alpha] for this digit
+  const SC* conv;    // [alpha][n_prime_total] indexed by prime index
+  int lo, cnt;       // digit limbs [lo, lo+cnt)
+  int n_q, n_chain, n_special, n_total;
+  long long out_stride;  // words between batch elements of out
+  int logn;
+};
+
+template <int MAXA>
+__global__ void modup_bconv_kernel(ModUpArgs A) {
+  const int N = 1 << A.logn;
+  const long long b = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const u64* cb = A.coef + b * (long long)A.n_q * N;
+  u64 x[MAXA];
+#pragma unroll
+  for (int i = 0; i < MAXA; ++i) {
+    if (i < A.cnt) {
+      const PrimeConst& P = A.pc[A.lo + i];
+      const SC c = A.qhinv[i];
+      x[i] = csub(shoup_lazy(cb[(long long)(A.lo + i) * N + t], c.w, c.wp, P.q), P.q);
+    }
+  }
+  u64* ob = A.out + b * A.out_stride;
+  const int ext = A.n_q + A.n_special;
+  for (int j = 0; j < ext; ++j) {
+    if (j >= A.lo && j < A.lo + A.cnt) continue;
+    const int pj = j < A.n_q ? j : A.n_chain + (j - A.n_q);
+    const PrimeConst& P = A.pc[pj];
+    u64 y = 0;
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) {
+      if (i < A.cnt) {
+        const SC c = A.conv[i * A.n_total + pj];
+        y = csub(y + shoup_lazy(x[i], c.w, c.wp, P.q), P.two_q);
+      }
+    }
+    ob[(long long)j * N + t] = csub(y, P.q);
+  }
+}
+
+// Key inner product with the NTT-domain automorphism folded into the digit
+// read: u_c[j][t] = sum_d D_d[j][perm_g(t)] * key_{d,c}[kl(j)][t]
+// (mul_acc, rns_poly.cpp:102-110, with lazy 128-bit accumulation).  The key
+// words of a (j, t) are held in registers and reused across the batch.
+struct InnerArgs {
+  const u64* digits;  // [batch][dnum][ext][N]
+  const u64* key;     // [dnum_max][2][full][N]
+  u64* u;             // [batch][2][ext][N]
+  const PrimeConst* pc;
+  int n_q, n_chain, n_special, dnum, batch;
+  u32 g;  // 1 = identity
+  int logn;
+};
+
+template <int MAXD>
+__global__ void ks_inner_kernel(InnerArgs A) {
+  const int N = 1 << A.logn;
+  const int ext = A.n_q + A.n_special, full = A.n_chain + A.n_special;
+  const int j = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int kl = j < A.n_q ? j : A.n_chain + (j - A.n_q);
+  const PrimeConst& P = A.pc[kl];
+  u64 k0[MAXD], k1[MAXD];
+#pragma unroll
+  for (int d = 0; d < MAXD; ++d) {
+    if (d < A.dnum) {
+      k0[d] = __ldg(A.key + (((long long)d * 2 + 0) * full + kl) * N + t);
+      k1[d] = __ldg(A.key + (((long long)d * 2 + 1) * full + kl) * N + t);
+    }
+  }
+  const int src = (A.g == 1) ? t : (int)ntt_auto_index((u32)t, A.g, A.logn);
+  for (int b = 0; b < A.batch; ++b) {
+    const u64* Db = A.digits + (long long)b * A.dnum * ext * N + (long long)j * N + src;
+    U128 z0{0, 0}, z1{0, 0};
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) {
+      if (d < A.dnum) {
+        const u64 v = __ldg(Db + (long long)d * ext * N);
+        mac128(z0, v, k0[d]);
+        mac128(z1, v, k1[d]);
+      }
+    }
+    u64* ub = A.u + (long long)b * 2 * ext * N + (long long)j * N + t;
+    ub[0] = reduce128(z0, P);
+    ub[(long long)ext * N] = reduce128(z1, P);
+  }
+}
+
+// ModDown basis conversion P -> Q (centred FastBConv; K = 1 is
+// moddown_special, rns_poly.cpp:164-180):
+//   x_k = [s_k * (P/p_k)^-1]_{p_k};  v_i = sum_k x_k [P/p_k]_{q_i} - #neg * [P]_{q_i}
+// sp: [bp][K][N] coefficient-domain special limbs; conv out: [bp][n_q][N]
+struct ModDownArgs {
+  const u64* sp;
+  u64* conv;
+  const PrimeConst* pc;
+  const SC* phinv;   // [K]
+  const SC* pconv;   // [K][n_chain]  ([P/p_k]_{q_i})
+  const u64* pmodq;  // [n_chain]     ([P]_{q_i})
+  int n_q, n_chain, n_special, logn;
+};
+
+template <int MAXK>
+__global__ void moddown_bconv_kernel(ModDownArgs A) {
+  const int N = 1 << A.logn;
+  const long long b = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  u64 x[MAXK];
+  int nneg = 0;
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k) {
+    if (k < A.n_special) {
+      const PrimeConst& P = A.pc[A.n_chain + k];
+      const SC c = A.phinv[k];
+      x[k] = csub(shoup_lazy(A.sp[(b * A.n_special + k) * N + t], c.w, c.wp, P.q), P.q);
+      nneg += x[k] > (P.q >> 1);
+    }
+  }
+  u64* cb = A.conv + b * (long long)A.n_q * N;
+  for (int i = 0; i < A.n_q; ++i) {
+    const PrimeConst& P = A.pc[i];
+    u64 v = 0;
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) {
+      if (k < A.n_special) {
+        const SC c = A.pconv[k * A.n_chain + i];
+        v = csub(v + shoup_lazy(x[k], c.w, c.wp, P.q), P.two_q);
+      }
+    }
+    v = csub(v, P.q);
+    const u64 pm = A.pmodq[i];
+    for (int m = 0; m < nneg; ++m) v = submod(v, pm, P.q);
+    cb[(long long)i * N + t] = v;
+  }
+}
+
+// out_i = (u_i - conv_i) * P^-1 mod q_i   (NTT domain), optionally
+// + tau_g(add)_i.  All strides in words between consecutive polys.
+struct CombineArgs {
+  const u64* u;
+  const u64* conv;
+  const u64* add;  // may be null
+  u64* out;
+  const PrimeConst* pc;
+  const SC* pinv;  // [n_chain]
+  int n_q;
+  long long u_stride, conv_stride, out_stride, add_stride;
+  u32 add_g;  // 1 = no automorphism on `add`
+  int logn;
+};
+
+__global__ void combine_kernel(CombineArgs A) {
+  const int N = 1 << A.logn;
+  const long long b = blockIdx.z;
+  const int i = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst& P = A.pc[i];
+  const SC c = A.pinv[i];
+  const u64 uu = A.u[b * A.u_stride + (long long)i * N + t];
+  const u64 cv = A.conv[b * A.conv_stride + (long long)i * N + t];
+  u64 r = csub(shoup_lazy(uu + P.q - cv, c.w, c.wp, P.q), P.q);
+  if (A.add) {
+    const int src = A.add_g == 1 ? t : (int)ntt_auto_index((u32)t, A.add_g, A.logn);
+    r = addmod(r, A.add[b * A.add_stride + (long long)i * N + src], P.q);
+  }
+  A.out[b * A.out_stride + (long long)i * N + t] = r;
+}
+
+// Rescale helper (rns_poly.cpp:144-162): from the coefficient-domain last limb
+// c, write [centred(c)]_{q_i} for every i < n_q - 1.
+struct RescaleArgs {
+  const u64* last;  // [bp][N]
+  u64* out;         // [bp][n_q-1][N]
+  const PrimeConst* pc;
+  const u64* qlmod;  // [n_q-1]: [q_l]_{q_i}
+  int n_q, logn;
+};
+
+__global__ void rescale_lift_kernel(RescaleArgs A) {
+  const int N = 1 << A.logn;
+  const long long b = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 ql = A.pc[A.n_q - 1].q;
+  const u64 c = A.last[b * N + t];
+  const bool neg = c > (ql >> 1);
+  for (int i = 0; i < A.n_q - 1; ++i) {
+    const PrimeConst& P = A.pc[i];
+    u64 r = csub(c - mulhi64(c, P.onep) * P.q, P.q);
+    if (neg) r = submod(r, A.qlmod[i], P.q);
+    A.out[(b * (A.n_q - 1) + i) * N + t] = r;
+  }
+}
+
+// Tensor (LatticeContext::mul x4, rns_poly.cpp:91-100):
+// d0 = a0 b0, d1 = a0 b1 + a1 b0, d2 = a1 b1.  a, b: [batch][2][n_q][N],
+// out: [batch][3][n_q][N]
+__global__ void tensor_kernel(u64* out, const u64* a, const u64* b, const PrimeConst* pc, int n_q,
+                              int logn) {
+  const int N = 1 << logn;
+  const long long bt = blockIdx.z;
+  const int i = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst& P = pc[i];
+  const long long L = (long long)n_q * N;
+  const u64* ab = a + bt * 2 * L + (long long)i * N + t;
+  const u64* bb = b + bt * 2 * L + (long long)i * N + t;
+  const u64 a0 = ab[0], a1 = ab[L], b0 = bb[0], b1 = bb[L];
+  U128 z{0, 0};
+  mac128(z, a0, b1);
+  mac128(z, a1, b0);
+  u64* ob = out + bt * 3 * L + (long long)i * N + t;
+  ob[0] = mulmod(a0, b0, P);
+  ob[L] = reduce128(z, P);
+  ob[2 * L] = mulmod(a1, b1, P);
+}
+
+// ------------------------------------------------------------ keys
+// ksk_d over the full basis: b = e - a s + [P]_{q_l} s' on chain limbs of digit d
+__global__ void keygen_kernel(u64* key, const u64* en, const u64* s_full, const u64* sp_full,
+                              const u64* a_full, const PrimeConst* pc, const u64* pmodq,
+                              int n_chain, int n_total, int alpha, int logn) {
+  const int N = 1 << logn;
+  const int d = blockIdx.z, l = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst& P = pc[l];
+  const long long li = (long long)l * N + t;
+  const u64 a = a_full[(long long)d * n_total * N + li];
+  const u64 as = mulmod(a, s_full[li], P);
+  u64 v = submod(en[(long long)d * n_total * N + li], as, P.q);
+  const int lo = d * alpha, hi = min(lo + alpha, n_chain);
+  if (l >= lo && l < hi) v = addmod(v, mulmod(pmodq[l], sp_full[li], P), P.q);
+  key[((long long)d * 2 + 0) * n_total * N + li] = v;
+  key[((long long)d * 2 + 1) * n_total * N + li] = a;
+}
+
+// ct = (m + e - a s, a)
+__global__ void encrypt_kernel(u64* ct, const u64* m, const u64* en, const u64* s_full,
+                               const u64* a, const PrimeConst* pc, int n_q, int logn) {
+  const int N = 1 << logn;
+  const int i = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst& P = pc[i];
+  const long long idx = (long long)i * N + t;
+  const u64 as = mulmod(a[idx], s_full[idx], P);
+  ct[idx] = submod(addmod(m[idx], en[idx], P.q), as, P.q);
+  ct[(long long)n_q * N + idx] = a[idx];
+}
+
+// m = c0 + c1 s
+__global__ void decrypt_kernel(u64* m, const u64* ct, const u64* s_full, const PrimeConst* pc,
+                               int n_q, int logn) {
+  const int N = 1 << logn;
+  const long long b = blockIdx.z;
+  const int i = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const PrimeConst& P = pc[i];
+  const long long L = (long long)n_q * N, idx = (long long)i * N + t;
+  U128 z{ct[b * 2 * L + idx], 0};
+  mac128(z, ct[b * 2 * L + L + idx], s_full[idx]);
+  m[b * L + idx] = reduce128(z, P);
+}
+
+}  // namespace hx

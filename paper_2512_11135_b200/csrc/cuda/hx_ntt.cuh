@@ -1,0 +1,258 @@
+// hx_ntt.cuh -- batched negacyclic NTT / INTT for sm_100a.
+//
+// Replaces NttTables::forward / inverse (reference ntt.cpp:57-96) and
+// LatticeContext::to_ntt / to_coeff (rns_poly.cpp:42-54).  Output is
+// bit-identical to the reference: forward leaves the bit-reversed layout
+// out[k] = a(psi^(2 brv(k) + 1)) with the reference's psi (ntt.cpp:23-32),
+// inverse restores natural order and applies N^-1.
+//
+// Structure: N = 2^logn is split as N1 x N2 (N1 = 2^a "high" bits, N2 = 2^b
+// "low" bits).  Forward runs two passes:
+//   COL pass  -- the first a stages: 2^a-point sub-transforms over the high
+//                bits, a CTA owns 16 adjacent columns (128-B coalesced rows);
+//   ROW pass  -- the last b stages on contiguous 2^b-element rows, a CTA
+//                owns 16 rows.
+// The inverse runs ROW then COL (Gentleman-Sande order).  Inside a pass each
+// thread holds 16 words in registers and performs radix-16 groups of 4 stages
+// (Harvey lazy butterflies, values in [0,4q) / [0,2q)); groups exchange data
+// through a 32 KB XOR-swizzled shared-memory tile.  Twiddles are the
+// reference tables (psi^brv(i), Shoup companion) packed as ulonglong2 and read
+// through the read-only path; the twiddle index of a butterfly whose lower
+// element has global index j and whose pair bit is beta is (N + j) >> (beta+1)
+// for both directions.
+#pragma once
+
+#include "hx_common.cuh"
+
+namespace hx {
+
+// One entry per limb a launch transforms.  Instance i of a batched launch is
+// (element b = i / count, entry e = i % count) at
+//   data + (b * stride + off[e]) * N,  prime index prime[e].
+constexpr int kMaxLimbEntries = 256;
+struct LimbTable {
+  int count;
+  int stride;  // limbs per batch element
+  unsigned short off[kMaxLimbEntries];
+  unsigned char prime[kMaxLimbEntries];
+};
+
+struct NttArgs {
+  u64* data;
+  const PrimeConst* pc;
+  LimbTable lt;
+  int logn;
+  long long instances;  // batch * lt.count
+};
+
+// Deposit free index f around the w group bits starting at bit lowbits.
+__device__ __forceinline__ int deposit(int f, int lowbits, int w) {
+  return (f & ((1 << lowbits) - 1)) | ((f >> lowbits) << (lowbits + w));
+}
+
+template <bool ROW>
+__device__ __forceinline__ int swz(int e) {
+  return ROW ? (e ^ ((e >> 4) & 15)) : e;
+}
+
+// One radix-2^W group over sub-bits [g0, g0+W) of the tile index.
+// x[r], r = (r_out << W) | r_in ; element e_r = base[r_out] | (r_in << lowbits).
+template <bool FWD, bool ROW, int S, int W>
+__device__ __forceinline__ void ntt_group(u64 (&x)[16], const int (&jb)[16 >> W], int g0,
+                                          int logn, const ulonglong2* __restrict__ tw,
+                                          const PrimeConst& P, bool last_stage_inv) {
+  constexpr int NO = 16 >> W;
+  const int logb = ROW ? 0 : (logn - S);  // j-bit of sub-bit 0
+  const u64 q = P.q, q2 = P.two_q;
+  const u64 N = 1ull << logn;
+#pragma unroll
+  for (int ii = 0; ii < W; ++ii) {
+    const int i = FWD ? (W - 1 - ii) : ii;  // register bit processed
+    const int beta = logb + g0 + i;         // global j-bit of the pair
+#pragma unroll
+    for (int ro = 0; ro < NO; ++ro) {
+#pragma unroll
+      for (int hp = 0; hp < (1 << (W - 1 - i)); ++hp) {
+        const int rb = (ro << W) | (hp << (i + 1));
+        // global index of element rb: jb[ro] + (hp << (i+1)) << (logb + g0)
+        const u64 j = (u64)jb[ro] + ((u64)(hp << (i + 1)) << (logb + g0));
+        const bool fin = (!FWD) && last_stage_inv && (beta == logn - 1);
+        ulonglong2 wt = make_ulonglong2(0, 0);
+        if (!fin) wt = __ldg(tw + ((N + j) >> (beta + 1)));
+#pragma unroll
+        for (int lp = 0; lp < (1 << i); ++lp) {
+          const int r0 = rb | lp, r1 = r0 | (1 << i);
+          const u64 X = x[r0], Y = x[r1];
+          if (FWD) {
+            const u64 Xr = csub(X, q2);
+            const u64 T = shoup_lazy(Y, wt.x, wt.y, q);
+            x[r0] = Xr + T;
+            x[r1] = Xr - T + q2;
+          } else if (fin) {
+            x[r0] = shoup_lazy(X + Y, P.ninv, P.ninvp, q);
+            x[r1] = shoup_lazy(X - Y + q2, P.w1n, P.w1np, q);
+          } else {
+            x[r0] = csub(X + Y, q2);
+            x[r1] = shoup_lazy(X - Y + q2, wt.x, wt.y, q);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Compute, for a group at sub-bits [g0, g0+W), the tile element base index
+// (r_in = 0) and the global j base for each r_out.
+template <bool ROW, int S, int OB, int W>
+__device__ __forceinline__ void group_index(int t, int g0, int logn, int tile,
+                                           int (&eb)[16 >> W], int (&jb)[16 >> W]) {
+  constexpr int T = (1 << (S + OB)) / 16;
+  const int subbase = ROW ? 0 : OB;
+  const int lowbits = subbase + g0;
+#pragma unroll
+  for (int ro = 0; ro < (16 >> W); ++ro) {
+    const int f = ro * T + t;
+    const int e = deposit(f, lowbits, W);
+    eb[ro] = e;
+    if (ROW) {
+      jb[ro] = (tile << (S + OB)) + e;
+    } else {
+      const int logb = logn - S;
+      jb[ro] = ((e >> OB) << logb) + (tile << OB) + (e & ((1 << OB) - 1));
+    }
+  }
+}
+
+template <bool ROW, int S, int OB>
+__device__ __forceinline__ long long tile_gofs(int e, int tile, int logn) {
+  if (ROW) return ((long long)tile << (S + OB)) + e;
+  const int logb = logn - S;
+  return ((long long)(e >> OB) << logb) + (tile << OB) + (e & ((1 << OB) - 1));
+}
+
+// Group schedule: forward processes sub-bits from the top (groups of 4, the
+// remainder last); inverse from the bottom (remainder first).
+template <int S>
+struct Sched {
+  static constexpr int R = S % 4;          // remainder width
+  static constexpr int G = S / 4;          // number of full groups
+};
+
+template <bool FWD, bool ROW, int S, int OB>
+__global__ void __launch_bounds__((1 << (S + OB)) / 16)
+    ntt_pass_kernel(NttArgs a) {
+  constexpr int TILE = 1 << (S + OB);
+  constexpr int T = TILE / 16;
+  __shared__ u64 sm[TILE];
+  const int t = threadIdx.x;
+  const int tiles = (1 << a.logn) / TILE;
+  const long long inst = blockIdx.x / tiles;
+  const int tile = blockIdx.x % tiles;
+  const int per = a.lt.count;
+  const long long bidx = inst / per;
+  const int ent = (int)(inst % per);
+  u64* base = a.data + ((long long)bidx * a.lt.stride + a.lt.off[ent]) * (1ll << a.logn);
+  const PrimeConst P = a.pc[a.lt.prime[ent]];
+  const ulonglong2* tw = FWD ? P.tw_fwd : P.tw_inv;
+  const u64 q = P.q;
+
+  u64 x[16];
+  constexpr int NG = Sched<S>::G + (Sched<S>::R ? 1 : 0);
+  // group g (in processing order) -> (g0, W)
+  // forward: full groups from the top, remainder (at bit 0) last
+  // inverse: remainder (at bit 0) first, then full groups upwards
+  bool first = true;
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    constexpr int Rm = Sched<S>::R;
+    int W, g0;
+    if (FWD) {
+      if (gi < Sched<S>::G) {
+        W = 4;
+        g0 = S - 4 * (gi + 1);
+      } else {
+        W = Rm;
+        g0 = 0;
+      }
+    } else {
+      if (Rm && gi == 0) {
+        W = Rm;
+        g0 = 0;
+      } else {
+        W = 4;
+        g0 = Rm + 4 * (gi - (Rm ? 1 : 0));
+      }
+    }
+    const bool lastg = (gi == NG - 1);
+    // W is a compile-time constant after unrolling; dispatch explicitly.
+#define HX_GROUP(WW)                                                                           \
+  {                                                                                            \
+    int eb[16 >> WW], jb[16 >> WW];                                                            \
+    group_index<ROW, S, OB, WW>(t, g0, a.logn, tile, eb, jb);                                  \
+    const int lowbits = (ROW ? 0 : OB) + g0;                                                   \
+    if (first) {                                                                               \
+      if (FWD || !ROW) {                                                                       \
+        /* direct coalesced global load */                                                     \
+        _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
+          const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                     \
+          x[r] = base[tile_gofs<ROW, S, OB>(e, tile, a.logn)];                                 \
+        }                                                                                      \
+      } else {                                                                                 \
+        /* inverse ROW pass: stage through smem for coalescing */                              \
+        _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
+          const int e = r * T + t;                                                             \
+          sm[swz<ROW>(e)] = base[tile_gofs<ROW, S, OB>(e, tile, a.logn)];                      \
+        }                                                                                      \
+        __syncthreads();                                                                       \
+        _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
+          const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                     \
+          x[r] = sm[swz<ROW>(e)];                                                              \
+        }                                                                                      \
+      }                                                                                        \
+    } else {                                                                                   \
+      _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                         \
+        const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                       \
+        x[r] = sm[swz<ROW>(e)];                                                                \
+      }                                                                                        \
+    }                                                                                          \
+    ntt_group<FWD, ROW, S, WW>(x, jb, g0, a.logn, tw, P, !ROW);                                 \
+    if (lastg) {                                                                               \
+      _Pragma("unroll") for (int r = 0; r < 16; ++r) x[r] =                                    \
+          (FWD ? (ROW ? reduce4(x[r], q, P.two_q) : x[r]) : (ROW ? x[r] : csub(x[r], q)));      \
+      if (FWD && ROW) {                                                                        \
+        /* stage through smem for a coalesced store */                                         \
+        __syncthreads();                                                                       \
+        _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
+          const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                     \
+          sm[swz<ROW>(e)] = x[r];                                                              \
+        }                                                                                      \
+        __syncthreads();                                                                       \
+        _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
+          const int e = r * T + t;                                                             \
+          base[tile_gofs<ROW, S, OB>(e, tile, a.logn)] = sm[swz<ROW>(e)];                      \
+        }                                                                                      \
+      } else {                                                                                 \
+        _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
+          const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                     \
+          base[tile_gofs<ROW, S, OB>(e, tile, a.logn)] = x[r];                                 \
+        }                                                                                      \
+      }                                                                                        \
+    } else {                                                                                   \
+      __syncthreads();                                                                         \
+      _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                         \
+        const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                       \
+        sm[swz<ROW>(e)] = x[r];                                                                \
+      }                                                                                        \
+      __syncthreads();                                                                         \
+    }                                                                                          \
+  }
+    if (W == 4) HX_GROUP(4)
+    else if (W == 3) HX_GROUP(3)
+    else if (W == 2) HX_GROUP(2)
+    else if (W == 1) HX_GROUP(1)
+#undef HX_GROUP
+    first = false;
+  }
+}
+
+}  // namespace hx

@@ -1,0 +1,888 @@
+// hx_ops.cu -- context construction, launchers and the C-ABI of libhx_b200.
+//
+// Host-side precomputation mirrors the reference constructors:
+//   psi search            ntt.cpp:23-32   (smallest g with (g^((q-1)/2N))^N = -1)
+//   twiddle tables        ntt.cpp:36-55   (psi^brv(i), psi^-brv(i), Shoup)
+//   rescale constants     rns_poly.cpp:144-162
+//   moddown constants     rns_poly.cpp:164-180 (generalised to K primes)
+// and the SPEC-only hybrid key-switch constants (ModUp FastBConv per digit).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/hx_b200.h"
+#include "hx_internal.h"
+#include "hx_kernels.cuh"
+
+using hx::LimbTable;
+using hx::PrimeConst;
+using hx::SC;
+using hx::u64;
+using u128 = unsigned __int128;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct HxError : std::runtime_error {
+  int code;
+  HxError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define HX_REQUIRE(cond, msg) \
+  do {                        \
+    if (!(cond)) throw HxError(HX_ERR_INVALID, msg); \
+  } while (0)
+
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw HxError(HX_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void launched(hx_ctx* c, const char* what, int n = 1) {
+  c->launches += n;
+  cuda_ok(cudaGetLastError(), what);
+}
+
+template <class F>
+int guarded(F f) {
+  try {
+    f();
+    return HX_OK;
+  } catch (const HxError& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return HX_ERR_INVALID;
+  }
+}
+
+// ---- host modular arithmetic (setup only) ----
+u64 hmul(u64 a, u64 b, u64 q) { return (u64)(((u128)a * b) % q); }
+u64 hpow(u64 a, u64 e, u64 q) {
+  u64 r = 1 % q, b = a % q;
+  while (e) {
+    if (e & 1) r = hmul(r, b, q);
+    b = hmul(b, b, q);
+    e >>= 1;
+  }
+  return r;
+}
+u64 hinv(u64 a, u64 q) { return hpow(a % q, q - 2, q); }
+u64 shoup(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+SC sc(u64 w, u64 q) { return SC{w % q, shoup(w % q, q)}; }
+u64 brv(u64 x, int bits) {
+  u64 r = 0;
+  for (int i = 0; i < bits; ++i) {
+    r = (r << 1) | (x & 1);
+    x >>= 1;
+  }
+  return r;
+}
+bool is_prime(u64 n) {
+  static const u64 sm[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  if (n < 2) return false;
+  for (u64 p : sm)
+    if (n % p == 0) return n == p;
+  u64 d = n - 1;
+  int r = 0;
+  while (!(d & 1)) {
+    d >>= 1;
+    ++r;
+  }
+  for (u64 a : sm) {
+    u64 x = hpow(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int i = 1; i < r; ++i) {
+      x = hmul(x, x, n);
+      if (x == n - 1) {
+        comp = false;
+        break;
+      }
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+// ntt.cpp:23-32
+u64 find_psi(u64 q, u64 n) {
+  const u64 order = 2 * n;
+  for (u64 g = 2; g < q; ++g) {
+    const u64 c = hpow(g, (q - 1) / order, q);
+    if (hpow(c, n, q) == q - 1) return c;
+  }
+  throw HxError(HX_ERR_INVALID, "no primitive 2N-th root");
+}
+
+// ---- stream-ordered scratch buffer ----
+struct DBuf {
+  u64* p = nullptr;
+  cudaStream_t s = nullptr;
+  DBuf(size_t words, cudaStream_t st) : s(st) {
+    if (words) cuda_ok(cudaMallocAsync((void**)&p, words * 8, st), "cudaMallocAsync");
+  }
+  ~DBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+};
+
+template <class T>
+T* upload(const std::vector<T>& v) {
+  T* d = nullptr;
+  if (v.empty()) return nullptr;
+  cuda_ok(cudaMalloc((void**)&d, v.size() * sizeof(T)), "cudaMalloc(const)");
+  cuda_ok(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  return d;
+}
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+void check_ctx(const hx_ctx* c) { HX_REQUIRE(c != nullptr, "null hx_ctx"); }
+void check_nq(const hx_ctx* c, int n_q) {
+  HX_REQUIRE(n_q >= 1 && n_q <= c->n_chain, "n_q out of range");
+}
+
+// strided 2-D device copy: rows of `width` words, pitches in words
+void copy2d(u64* dst, long long dpitch, const u64* src, long long spitch, long long width,
+            long long rows, cudaStream_t s) {
+  if (rows <= 0 || width <= 0) return;
+  cuda_ok(cudaMemcpy2DAsync(dst, dpitch * 8, src, spitch * 8, width * 8, rows,
+                            cudaMemcpyDeviceToDevice, s),
+          "cudaMemcpy2DAsync");
+}
+
+int ew_threads(const hx_ctx* c) { return (int)std::min<long long>(256, c->N() / 2); }
+int pt_threads(const hx_ctx* c) { return (int)std::min<long long>(256, c->N()); }
+
+template <hx::EwOp OP>
+void ew(hx_ctx* c, u64* out, const u64* a, const u64* b, long long batch, const LimbTable& lt,
+        cudaStream_t s) {
+  hx::EwArgs A{out, a, b, c->d_pc, lt, c->logn, batch * lt.count};
+  const int th = ew_threads(c);
+  const long long blocks = A.instances * (c->N() / (2 * th));
+  if (blocks <= 0) return;
+  hx::ew_kernel<OP><<<(unsigned)blocks, th, 0, s>>>(A);
+  launched(c, "ew_kernel");
+}
+
+void automorphism(hx_ctx* c, u64* out, const u64* in, long long batch, const LimbTable& lt,
+                  u64 g, cudaStream_t s) {
+  hx::EwArgs A{out, in, nullptr, c->d_pc, lt, c->logn, batch * lt.count};
+  const int th = pt_threads(c);
+  const long long blocks = A.instances * (c->N() / th);
+  if (blocks <= 0) return;
+  hx::automorphism_kernel<<<(unsigned)blocks, th, 0, s>>>(A, (hx::u32)g);
+  launched(c, "automorphism_kernel");
+}
+
+// ---- key-switch building blocks ----
+
+// c1: [batch] polys of n_q limbs at stride c1_stride words.
+void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long batch, int n_q,
+           cudaStream_t s) {
+  const long long N = c->N();
+  const int K = c->n_special, ext = n_q + K, dnum = c->dnum(n_q);
+  DBuf coef(batch * n_q * N, s);
+  copy2d(coef.p, n_q * N, c1, c1_stride, n_q * N, batch, s);
+  hx::ntt_inverse(c, coef.p, batch, hx::make_table(c, n_q, 0), s);
+  // basis conversion per digit (coefficient domain), own limbs copied (NTT)
+  LimbTable lt{};
+  lt.stride = dnum * ext;
+  lt.count = 0;
+  const long long out_stride = (long long)dnum * ext * N;
+  for (int d = 0; d < dnum; ++d) {
+    const int lo = d * c->alpha, cnt = std::min(c->alpha, n_q - lo);
+    hx::ModUpArgs A;
+    A.coef = coef.p;
+    A.out = digits + (long long)d * ext * N;
+    A.pc = c->d_pc;
+    A.qhinv = c->d_modup + c->modup_qh_off[n_q][d];
+    A.conv = c->d_modup + c->modup_cv_off[n_q][d];
+    A.lo = lo;
+    A.cnt = cnt;
+    A.n_q = n_q;
+    A.n_chain = c->n_chain;
+    A.n_special = K;
+    A.n_total = c->n_total();
+    A.out_stride = out_stride;
+    A.logn = c->logn;
+    const int th = pt_threads(c);
+    dim3 grid((unsigned)(N / th), (unsigned)batch);
+    if (c->alpha <= 1)
+      hx::modup_bconv_kernel<1><<<grid, th, 0, s>>>(A);
+    else if (c->alpha <= 2)
+      hx::modup_bconv_kernel<2><<<grid, th, 0, s>>>(A);
+    else if (c->alpha <= 4)
+      hx::modup_bconv_kernel<4><<<grid, th, 0, s>>>(A);
+    else
+      hx::modup_bconv_kernel<8><<<grid, th, 0, s>>>(A);
+    launched(c, "modup_bconv_kernel");
+    copy2d(digits + ((long long)d * ext + lo) * N, out_stride, c1 + (long long)lo * N, c1_stride,
+           (long long)cnt * N, batch, s);
+    for (int j = 0; j < ext; ++j) {
+      if (j >= lo && j < lo + cnt) continue;
+      HX_REQUIRE(lt.count < hx::kMaxLimbEntries, "modup: too many limbs for one launch");
+      lt.off[lt.count] = (unsigned short)(d * ext + j);
+      lt.prime[lt.count] = (unsigned char)c->pidx(j, n_q);
+      ++lt.count;
+    }
+  }
+  if (lt.count) hx::ntt_forward(c, digits, batch, lt, s);
+}
+
+void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long batch, int n_q,
+              u64 g, cudaStream_t s) {
+  hx::InnerArgs A;
+  A.digits = digits;
+  A.key = key;
+  A.u = u;
+  A.pc = c->d_pc;
+  A.n_q = n_q;
+  A.n_chain = c->n_chain;
+  A.n_special = c->n_special;
+  A.dnum = c->dnum(n_q);
+  A.batch = (int)batch;
+  A.g = (hx::u32)g;
+  A.logn = c->logn;
+  const int th = pt_threads(c);
+  dim3 grid((unsigned)(c->N() / th), (unsigned)(n_q + c->n_special));
+  if (A.dnum <= 4)
+    hx::ks_inner_kernel<4><<<grid, th, 0, s>>>(A);
+  else if (A.dnum <= 8)
+    hx::ks_inner_kernel<8><<<grid, th, 0, s>>>(A);
+  else if (A.dnum <= 16)
+    hx::ks_inner_kernel<16><<<grid, th, 0, s>>>(A);
+  else if (A.dnum <= 32)
+    hx::ks_inner_kernel<32><<<grid, th, 0, s>>>(A);
+  else
+    hx::ks_inner_kernel<64><<<grid, th, 0, s>>>(A);
+  launched(c, "ks_inner_kernel");
+}
+
+// Centred ModDown of `polys` PQ-basis polys u (stride u_stride words) into
+// out (stride out_stride words); optionally adds tau_g(add) (stride add_stride).
+void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long u_stride,
+             long long polys, int n_q, const u64* add, long long add_stride, u64 add_g,
+             cudaStream_t s) {
+  const long long N = c->N();
+  const int K = c->n_special;
+  DBuf sp(polys * K * N, s), conv(polys * n_q * N, s);
+  copy2d(sp.p, K * N, u + (long long)n_q * N, u_stride, K * N, polys, s);
+  hx::ntt_inverse(c, sp.p, polys, hx::make_table(c, 0, K), s);
+  hx::ModDownArgs M;
+  M.sp = sp.p;
+  M.conv = conv.p;
+  M.pc = c->d_pc;
+  M.phinv = c->d_phinv;
+  M.pconv = c->d_pconv;
+  M.pmodq = c->d_pmodq;
+  M.n_q = n_q;
+  M.n_chain = c->n_chain;
+  M.n_special = K;
+  M.logn = c->logn;
+  const int th = pt_threads(c);
+  dim3 grid((unsigned)(N / th), (unsigned)polys);
+  if (K <= 1)
+    hx::moddown_bconv_kernel<1><<<grid, th, 0, s>>>(M);
+  else if (K <= 4)
+    hx::moddown_bconv_kernel<4><<<grid, th, 0, s>>>(M);
+  else
+    hx::moddown_bconv_kernel<8><<<grid, th, 0, s>>>(M);
+  launched(c, "moddown_bconv_kernel");
+  hx::ntt_forward(c, conv.p, polys, hx::make_table(c, n_q, 0), s);
+  hx::CombineArgs C;
+  C.u = u;
+  C.conv = conv.p;
+  C.add = add;
+  C.out = out;
+  C.pc = c->d_pc;
+  C.pinv = c->d_pinv;
+  C.n_q = n_q;
+  C.u_stride = u_stride;
+  C.conv_stride = (long long)n_q * N;
+  C.out_stride = out_stride;
+  C.add_stride = add_stride;
+  C.add_g = (hx::u32)add_g;
+  C.logn = c->logn;
+  dim3 g3((unsigned)(N / th), (unsigned)n_q, (unsigned)polys);
+  hx::combine_kernel<<<g3, th, 0, s>>>(C);
+  launched(c, "combine_kernel");
+}
+
+void rescale(hx_ctx* c, u64* out, const u64* in, long long polys, int n_q, cudaStream_t s) {
+  const long long N = c->N();
+  DBuf last(polys * N, s), lift(polys * (n_q - 1) * N, s);
+  copy2d(last.p, N, in + (long long)(n_q - 1) * N, (long long)n_q * N, N, polys, s);
+  LimbTable lt{};
+  lt.count = 1;
+  lt.stride = 1;
+  lt.off[0] = 0;
+  lt.prime[0] = (unsigned char)(n_q - 1);
+  hx::ntt_inverse(c, last.p, polys, lt, s);
+  hx::RescaleArgs R;
+  R.last = last.p;
+  R.out = lift.p;
+  R.pc = c->d_pc;
+  R.qlmod = c->d_qlmod + (long long)(n_q - 1) * c->n_chain;
+  R.n_q = n_q;
+  R.logn = c->logn;
+  const int th = pt_threads(c);
+  hx::rescale_lift_kernel<<<dim3((unsigned)(N / th), (unsigned)polys), th, 0, s>>>(R);
+  launched(c, "rescale_lift_kernel");
+  hx::ntt_forward(c, lift.p, polys, hx::make_table(c, n_q - 1, 0), s);
+  hx::CombineArgs C;
+  C.u = in;
+  C.conv = lift.p;
+  C.add = nullptr;
+  C.out = out;
+  C.pc = c->d_pc;
+  C.pinv = c->d_qlinv + (long long)(n_q - 1) * c->n_chain;
+  C.n_q = n_q - 1;
+  C.u_stride = (long long)n_q * N;
+  C.conv_stride = (long long)(n_q - 1) * N;
+  C.out_stride = (long long)(n_q - 1) * N;
+  C.add_stride = 0;
+  C.add_g = 1;
+  C.logn = c->logn;
+  hx::combine_kernel<<<dim3((unsigned)(N / th), (unsigned)(n_q - 1), (unsigned)polys), th, 0, s>>>(C);
+  launched(c, "combine_kernel");
+}
+
+// rotation(s) from precomputed digits of `in` (batch cts [2][n_q]); writes
+// out + r-th slot with ct stride out_ct_stride words
+void rotate_from_digits(hx_ctx* c, u64* out, long long out_ct_stride, const u64* in,
+                        const u64* digits, const u64* key, long long batch, int n_q, u64 g,
+                        cudaStream_t s) {
+  const long long N = c->N();
+  const int ext = n_q + c->n_special;
+  DBuf U(batch * 2 * ext * N, s);
+  ks_inner(c, U.p, digits, key, batch, n_q, g, s);
+  // c0' = tau(c0) + ModDown(u0)
+  moddown(c, out, out_ct_stride, U.p, 2ll * ext * N, batch, n_q, in, 2ll * n_q * N, g, s);
+  // c1' = ModDown(u1)
+  moddown(c, out + (long long)n_q * N, out_ct_stride, U.p + (long long)ext * N, 2ll * ext * N,
+          batch, n_q, nullptr, 0, 1, s);
+}
+
+}  // namespace
+
+namespace hx {
+
+void set_error(const std::string& msg) { throw HxError(HX_ERR_UNSUPPORTED, msg); }
+
+LimbTable make_table(const hx_ctx* c, int n_q, int n_p, int stride, int first) {
+  LimbTable lt{};
+  lt.count = n_q + n_p;
+  lt.stride = stride < 0 ? lt.count : stride;
+  HX_REQUIRE(lt.count <= kMaxLimbEntries, "too many limbs");
+  for (int k = 0; k < lt.count; ++k) {
+    lt.off[k] = (unsigned short)(first + k);
+    lt.prime[k] = (unsigned char)c->pidx(k, n_q);
+  }
+  return lt;
+}
+
+}  // namespace hx
+
+// =============================================================================
+// C-ABI
+// =============================================================================
+extern "C" {
+
+const char* hx_last_error(void) { return g_last_error.c_str(); }
+const char* hx_version(void) { return "libhx_b200 0.1 (sm_100a)"; }
+
+hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64_t* special,
+                      int n_special, int alpha) {
+  hx_ctx* out = nullptr;
+  const int rc = guarded([&] {
+    HX_REQUIRE(logn >= 8 && logn <= 16, "logn must be in [8, 16]");
+    HX_REQUIRE(n_chain >= 1 && n_special >= 1 && n_chain + n_special <= hx::kMaxPrimes,
+               "prime counts out of range");
+    HX_REQUIRE(alpha >= 1 && alpha <= 8, "alpha must be in [1, 8]");
+    int ndev = 0;
+    cuda_ok(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    HX_REQUIRE(ndev > 0, "no CUDA device");
+    auto c = std::make_unique<hx_ctx>();
+    c->logn = logn;
+    c->n_chain = n_chain;
+    c->n_special = n_special;
+    c->alpha = alpha;
+    cuda_ok(cudaGetDevice(&c->device), "cudaGetDevice");
+    c->primes.assign(chain, chain + n_chain);
+    c->primes.insert(c->primes.end(), special, special + n_special);
+    const u64 N = 1ull << logn;
+    const int T = c->n_total();
+    for (int i = 0; i < T; ++i) {
+      const u64 q = c->primes[i];
+      HX_REQUIRE(q < (1ull << 62) && q % (2 * N) == 1 && is_prime(q),
+                 "modulus must be prime, < 2^62 and = 1 mod 2N");
+      for (int j = 0; j < i; ++j) HX_REQUIRE(c->primes[j] != q, "duplicate modulus");
+    }
+    // twiddles + per-prime constants
+    std::vector<ulonglong2> tw((size_t)T * 2 * N);
+    std::vector<PrimeConst> pc(T);
+    cuda_ok(cudaMalloc((void**)&c->d_tw, tw.size() * sizeof(ulonglong2)), "cudaMalloc(tw)");
+    for (int i = 0; i < T; ++i) {
+      const u64 q = c->primes[i];
+      const u64 psi = find_psi(q, N), psi_inv = hinv(psi, q);
+      c->psi.push_back(psi);
+      ulonglong2* f = tw.data() + (size_t)i * 2 * N;
+      ulonglong2* g = f + N;
+      u64 pw = 1, pwi = 1;
+      for (u64 e = 0; e < N; ++e) {
+        const u64 k = brv(e, logn);
+        f[k] = make_ulonglong2(pw, shoup(pw, q));
+        g[k] = make_ulonglong2(pwi, shoup(pwi, q));
+        pw = hmul(pw, psi, q);
+        pwi = hmul(pwi, psi_inv, q);
+      }
+      PrimeConst& P = pc[i];
+      P.q = q;
+      P.two_q = 2 * q;
+      P.r64 = (u64)(((u128)1 << 64) % q);
+      P.r64p = shoup(P.r64, q);
+      P.onep = (u64)(((u128)1 << 64) / q);
+      P.ninv = hinv(N % q, q);
+      P.ninvp = shoup(P.ninv, q);
+      P.w1n = hmul(g[1].x, P.ninv, q);
+      P.w1np = shoup(P.w1n, q);
+      P.tw_fwd = c->d_tw + (size_t)i * 2 * N;
+      P.tw_inv = c->d_tw + (size_t)i * 2 * N + N;
+    }
+    cuda_ok(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice),
+            "upload tw");
+    c->d_pc = upload(pc);
+    // ModUp constants per (n_q, digit)
+    std::vector<SC> mu;
+    c->modup_qh_off.assign(n_chain + 1, {});
+    c->modup_cv_off.assign(n_chain + 1, {});
+    for (int nq = 1; nq <= n_chain; ++nq) {
+      const int dn = c->dnum(nq);
+      for (int d = 0; d < dn; ++d) {
+        const int lo = d * alpha, cnt = std::min(alpha, nq - lo);
+        c->modup_qh_off[nq].push_back((long long)mu.size());
+        for (int i = lo; i < lo + cnt; ++i) {
+          const u64 q = c->primes[i];
+          u64 prod = 1;
+          for (int i2 = lo; i2 < lo + cnt; ++i2)
+            if (i2 != i) prod = hmul(prod, c->primes[i2] % q, q);
+          mu.push_back(sc(hinv(prod, q), q));
+        }
+        c->modup_cv_off[nq].push_back((long long)mu.size());
+        for (int i = lo; i < lo + cnt; ++i) {
+          for (int p = 0; p < T; ++p) {
+            const u64 m = c->primes[p];
+            u64 prod = 1;
+            for (int i2 = lo; i2 < lo + cnt; ++i2)
+              if (i2 != i) prod = hmul(prod, c->primes[i2] % m, m);
+            mu.push_back(sc(prod, m));
+          }
+        }
+      }
+    }
+    c->d_modup = upload(mu);
+    // ModDown constants
+    std::vector<SC> phinv(n_special), pconv((size_t)n_special * n_chain), pinv(n_chain);
+    std::vector<u64> pmodq(n_chain);
+    for (int k = 0; k < n_special; ++k) {
+      const u64 pk = c->primes[n_chain + k];
+      u64 prod = 1;
+      for (int k2 = 0; k2 < n_special; ++k2)
+        if (k2 != k) prod = hmul(prod, c->primes[n_chain + k2] % pk, pk);
+      phinv[k] = sc(hinv(prod, pk), pk);
+      for (int i = 0; i < n_chain; ++i) {
+        const u64 q = c->primes[i];
+        u64 pr = 1;
+        for (int k2 = 0; k2 < n_special; ++k2)
+          if (k2 != k) pr = hmul(pr, c->primes[n_chain + k2] % q, q);
+        pconv[(size_t)k * n_chain + i] = sc(pr, q);
+      }
+    }
+    for (int i = 0; i < n_chain; ++i) {
+      const u64 q = c->primes[i];
+      u64 P = 1;
+      for (int k = 0; k < n_special; ++k) P = hmul(P, c->primes[n_chain + k] % q, q);
+      pmodq[i] = P;
+      pinv[i] = sc(hinv(P, q), q);
+    }
+    c->d_phinv = upload(phinv);
+    c->d_pconv = upload(pconv);
+    c->d_pmodq = upload(pmodq);
+    c->d_pinv = upload(pinv);
+    // Rescale constants
+    std::vector<SC> qlinv((size_t)n_chain * n_chain, SC{0, 0});
+    std::vector<u64> qlmod((size_t)n_chain * n_chain, 0);
+    for (int l = 1; l < n_chain; ++l)
+      for (int i = 0; i < l; ++i) {
+        const u64 q = c->primes[i], ql = c->primes[l];
+        qlinv[(size_t)l * n_chain + i] = sc(hinv(ql % q, q), q);
+        qlmod[(size_t)l * n_chain + i] = ql % q;
+      }
+    c->d_qlinv = upload(qlinv);
+    c->d_qlmod = upload(qlmod);
+    out = c.release();
+  });
+  return rc == HX_OK ? out : nullptr;
+}
+
+void hx_ctx_destroy(hx_ctx* c) {
+  if (!c) return;
+  for (void* p : {(void*)c->d_pc, (void*)c->d_tw, (void*)c->d_modup, (void*)c->d_phinv,
+                  (void*)c->d_pconv, (void*)c->d_pmodq, (void*)c->d_pinv, (void*)c->d_qlinv,
+                  (void*)c->d_qlmod})
+    if (p) cudaFree(p);
+  delete c;
+}
+
+int hx_ctx_dnum(const hx_ctx* c, int n_q) { return c ? c->dnum(n_q) : -1; }
+uint64_t hx_ctx_psi(const hx_ctx* c, int i) {
+  return (c && i >= 0 && i < c->n_total()) ? c->psi[i] : 0;
+}
+size_t hx_key_words(const hx_ctx* c) {
+  return c ? (size_t)c->dnum(c->n_chain) * 2 * c->n_total() * c->N() : 0;
+}
+unsigned long long hx_ctx_launches(const hx_ctx* c) { return c ? c->launches : 0; }
+
+int hx_malloc(void** p, size_t bytes) {
+  return guarded([&] { cuda_ok(cudaMalloc(p, bytes), "cudaMalloc"); });
+}
+int hx_free(void* p) {
+  return guarded([&] { cuda_ok(cudaFree(p), "cudaFree"); });
+}
+int hx_memcpy_h2d(void* dst, const void* src, size_t bytes, void* s) {
+  return guarded(
+      [&] { cuda_ok(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, S(s)), "h2d"); });
+}
+int hx_memcpy_d2h(void* dst, const void* src, size_t bytes, void* s) {
+  return guarded(
+      [&] { cuda_ok(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, S(s)), "d2h"); });
+}
+int hx_stream_sync(void* s) {
+  return guarded([&] { cuda_ok(cudaStreamSynchronize(S(s)), "cudaStreamSynchronize"); });
+}
+int hx_device_sync(void) {
+  return guarded([&] { cuda_ok(cudaDeviceSynchronize(), "cudaDeviceSynchronize"); });
+}
+
+int hx_ntt_fwd(hx_ctx* c, uint64_t* data, int batch, int n_q, int n_p, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_REQUIRE(n_q >= 0 && n_q <= c->n_chain && n_p >= 0 && n_p <= c->n_special, "limbs");
+    hx::ntt_forward(c, (u64*)data, batch, hx::make_table(c, n_q, n_p), S(s));
+    cuda_ok(cudaGetLastError(), "ntt_forward");
+  });
+}
+
+int hx_ntt_inv(hx_ctx* c, uint64_t* data, int batch, int n_q, int n_p, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_REQUIRE(n_q >= 0 && n_q <= c->n_chain && n_p >= 0 && n_p <= c->n_special, "limbs");
+    hx::ntt_inverse(c, (u64*)data, batch, hx::make_table(c, n_q, n_p), S(s));
+    cuda_ok(cudaGetLastError(), "ntt_inverse");
+  });
+}
+
+#define HX_EW_ENTRY(NAME, OP)                                                                 \
+  int NAME(hx_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, int batch, int n_q, \
+           int n_p, void* s) {                                                                \
+    return guarded([&] {                                                                      \
+      check_ctx(c);                                                                           \
+      ew<OP>(c, (u64*)out, (const u64*)a, (const u64*)b, batch, hx::make_table(c, n_q, n_p),   \
+             S(s));                                                                           \
+    });                                                                                       \
+  }
+HX_EW_ENTRY(hx_add, hx::EwOp::Add)
+HX_EW_ENTRY(hx_sub, hx::EwOp::Sub)
+HX_EW_ENTRY(hx_mul, hx::EwOp::Mul)
+#undef HX_EW_ENTRY
+
+int hx_mul_acc(hx_ctx* c, uint64_t* acc, const uint64_t* a, const uint64_t* b, int batch, int n_q,
+               int n_p, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    ew<hx::EwOp::MulAcc>(c, (u64*)acc, (const u64*)a, (const u64*)b, batch,
+                         hx::make_table(c, n_q, n_p), S(s));
+  });
+}
+
+int hx_neg(hx_ctx* c, uint64_t* out, const uint64_t* a, int batch, int n_q, int n_p, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    ew<hx::EwOp::Neg>(c, (u64*)out, (const u64*)a, nullptr, batch, hx::make_table(c, n_q, n_p),
+                      S(s));
+  });
+}
+
+int hx_automorphism(hx_ctx* c, uint64_t* out, const uint64_t* in, int batch, int n_q, int n_p,
+                    uint64_t g, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element must be odd and < 2N");
+    HX_REQUIRE(out != in, "automorphism cannot run in place");
+    automorphism(c, (u64*)out, (const u64*)in, batch, hx::make_table(c, n_q, n_p), g, S(s));
+  });
+}
+
+int hx_from_i64(hx_ctx* c, uint64_t* out, const int64_t* v, int batch, int n_q, int n_p,
+                void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    const LimbTable lt = hx::make_table(c, n_q, n_p);
+    const int th = pt_threads(c);
+    const long long blocks = (long long)batch * lt.count * (c->N() / th);
+    if (blocks <= 0) return;
+    hx::from_i64_kernel<<<(unsigned)blocks, th, 0, S(s)>>>((u64*)out, (const long long*)v,
+                                                            c->d_pc, lt, c->logn);
+    launched(c, "from_i64_kernel");
+  });
+}
+
+int hx_reduce_mod_q(hx_ctx* c, uint64_t* data, int batch, int n_q, int n_p, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    hx::EwArgs A{(u64*)data, nullptr, nullptr, c->d_pc, hx::make_table(c, n_q, n_p), c->logn, 0};
+    A.instances = (long long)batch * A.lt.count;
+    const int th = pt_threads(c);
+    const long long blocks = A.instances * (c->N() / th);
+    if (blocks <= 0) return;
+    hx::reduce_kernel<<<(unsigned)blocks, th, 0, S(s)>>>(A);
+    launched(c, "reduce_kernel");
+  });
+}
+
+int hx_rescale(hx_ctx* c, uint64_t* out, const uint64_t* in, int batch, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    HX_REQUIRE(n_q >= 2, "rescale: no limb to drop");
+    rescale(c, (u64*)out, (const u64*)in, batch, n_q, S(s));
+  });
+}
+
+int hx_modup(hx_ctx* c, uint64_t* digits, const uint64_t* c1, int batch, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    modup(c, (u64*)digits, (const u64*)c1, (long long)n_q * c->N(), batch, n_q, S(s));
+  });
+}
+
+int hx_ks_inner(hx_ctx* c, uint64_t* u, const uint64_t* digits, const uint64_t* key, int batch,
+                int n_q, uint64_t g, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element must be odd and < 2N");
+    ks_inner(c, (u64*)u, (const u64*)digits, (const u64*)key, batch, n_q, g, S(s));
+  });
+}
+
+int hx_moddown(hx_ctx* c, uint64_t* out, const uint64_t* u, int polys, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    const long long N = c->N();
+    moddown(c, (u64*)out, (long long)n_q * N, (const u64*)u, (long long)(n_q + c->n_special) * N,
+            polys, n_q, nullptr, 0, 1, S(s));
+  });
+}
+
+int hx_keyswitch(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* key, int batch,
+                 int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    const long long N = c->N();
+    const int ext = n_q + c->n_special;
+    DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s)), U((long long)batch * 2 * ext * N, S(s));
+    modup(c, D.p, (const u64*)in, (long long)n_q * N, batch, n_q, S(s));
+    ks_inner(c, U.p, D.p, (const u64*)key, batch, n_q, 1, S(s));
+    moddown(c, (u64*)out, (long long)n_q * N, U.p, (long long)ext * N, 2ll * batch, n_q, nullptr,
+            0, 1, S(s));
+  });
+}
+
+int hx_rotate(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* key, int batch,
+              int n_q, uint64_t g, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element must be odd and < 2N");
+    HX_REQUIRE(out != in, "rotate cannot run in place");
+    const long long N = c->N();
+    const int ext = n_q + c->n_special;
+    DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s));
+    modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s));
+    rotate_from_digits(c, (u64*)out, 2ll * n_q * N, (const u64*)in, D.p, (const u64*)key, batch,
+                       n_q, g, S(s));
+  });
+}
+
+int hx_rotate_hoisted(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* const* keys,
+                      const uint64_t* galois, int R, int batch, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    HX_REQUIRE(R >= 1, "R >= 1");
+    const long long N = c->N();
+    const int ext = n_q + c->n_special;
+    DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s));
+    modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s));
+    for (int r = 0; r < R; ++r) {
+      HX_REQUIRE((galois[r] & 1) && galois[r] < 2 * (u64)N, "galois element");
+      rotate_from_digits(c, (u64*)out + (long long)r * 2 * n_q * N, (long long)R * 2 * n_q * N,
+                         (const u64*)in, D.p, (const u64*)keys[r], batch, n_q, galois[r], S(s));
+    }
+  });
+}
+
+int hx_tensor(hx_ctx* c, uint64_t* out3, const uint64_t* a, const uint64_t* b, int batch, int n_q,
+              void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    const int th = pt_threads(c);
+    hx::tensor_kernel<<<dim3((unsigned)(c->N() / th), (unsigned)n_q, (unsigned)batch), th, 0,
+                        S(s)>>>((u64*)out3, (const u64*)a, (const u64*)b, c->d_pc, n_q, c->logn);
+    launched(c, "tensor_kernel");
+  });
+}
+
+int hx_mul_relin(hx_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b,
+                 const uint64_t* rlk, int batch, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    const long long N = c->N(), L = (long long)n_q * N;
+    const int ext = n_q + c->n_special;
+    DBuf d3((long long)batch * 3 * L, S(s)), D((long long)batch * c->dnum(n_q) * ext * N, S(s)),
+        U((long long)batch * 2 * ext * N, S(s));
+    const int th = pt_threads(c);
+    hx::tensor_kernel<<<dim3((unsigned)(N / th), (unsigned)n_q, (unsigned)batch), th, 0, S(s)>>>(
+        d3.p, (const u64*)a, (const u64*)b, c->d_pc, n_q, c->logn);
+    launched(c, "tensor_kernel");
+    modup(c, D.p, d3.p + 2 * L, 3 * L, batch, n_q, S(s));
+    ks_inner(c, U.p, D.p, (const u64*)rlk, batch, n_q, 1, S(s));
+    moddown(c, (u64*)out, 2 * L, U.p, 2ll * ext * N, batch, n_q, d3.p, 3 * L, 1, S(s));
+    moddown(c, (u64*)out + L, 2 * L, U.p + (long long)ext * N, 2ll * ext * N, batch, n_q,
+            d3.p + L, 3 * L, 1, S(s));
+  });
+}
+
+int hx_bsgs_mac(hx_ctx* c, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,
+                int diag_limbs, int n1, int n2, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    HX_REQUIRE(n1 >= 1 && n1 <= 64 && n2 >= 1 && diag_limbs >= n_q, "bsgs_mac: bad shape");
+    hx::MacArgs A;
+    A.inner = (u64*)inner;
+    A.baby = (const u64*)baby;
+    A.diags = (const u64*)diags;
+    A.pc = c->d_pc;
+    A.n1 = n1;
+    A.n2 = n2;
+    A.n_q = n_q;
+    A.logn = c->logn;
+    A.diag_stride = (long long)diag_limbs * c->N();
+    hx::launch_bsgs_mac(A, c->N(), S(s));
+    launched(c, "bsgs_mac_kernel");
+  });
+}
+
+int hx_keygen_ksk(hx_ctx* c, uint64_t* key, const uint64_t* s_full, const uint64_t* sp_full,
+                  const uint64_t* a_full, const int64_t* e, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    const long long N = c->N();
+    const int T = c->n_total(), dn = c->dnum(c->n_chain);
+    DBuf en((long long)dn * T * N, S(s));
+    const LimbTable lt = hx::make_table(c, c->n_chain, c->n_special);
+    const int th = pt_threads(c);
+    hx::from_i64_kernel<<<(unsigned)((long long)dn * T * (N / th)), th, 0, S(s)>>>(
+        en.p, (const long long*)e, c->d_pc, lt, c->logn);
+    launched(c, "from_i64_kernel");
+    hx::ntt_forward(c, en.p, dn, lt, S(s));
+    hx::keygen_kernel<<<dim3((unsigned)(N / th), (unsigned)T, (unsigned)dn), th, 0, S(s)>>>(
+        (u64*)key, en.p, (const u64*)s_full, (const u64*)sp_full, (const u64*)a_full, c->d_pc,
+        c->d_pmodq, c->n_chain, T, c->alpha, c->logn);
+    launched(c, "keygen_kernel");
+  });
+}
+
+int hx_encrypt_sk(hx_ctx* c, uint64_t* ct, const uint64_t* m, const uint64_t* s_full,
+                  const uint64_t* a, const int64_t* e, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    const long long N = c->N();
+    DBuf en((long long)n_q * N, S(s));
+    const LimbTable lt = hx::make_table(c, n_q, 0);
+    const int th = pt_threads(c);
+    hx::from_i64_kernel<<<(unsigned)((long long)n_q * (N / th)), th, 0, S(s)>>>(
+        en.p, (const long long*)e, c->d_pc, lt, c->logn);
+    launched(c, "from_i64_kernel");
+    hx::ntt_forward(c, en.p, 1, lt, S(s));
+    hx::encrypt_kernel<<<dim3((unsigned)(N / th), (unsigned)n_q), th, 0, S(s)>>>(
+        (u64*)ct, (const u64*)m, en.p, (const u64*)s_full, (const u64*)a, c->d_pc, n_q, c->logn);
+    launched(c, "encrypt_kernel");
+  });
+}
+
+int hx_decrypt(hx_ctx* c, uint64_t* m, const uint64_t* ct, const uint64_t* s_full, int batch,
+               int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    const int th = pt_threads(c);
+    hx::decrypt_kernel<<<dim3((unsigned)(c->N() / th), (unsigned)n_q, (unsigned)batch), th, 0,
+                         S(s)>>>((u64*)m, (const u64*)ct, (const u64*)s_full, c->d_pc, n_q,
+                                 c->logn);
+    launched(c, "decrypt_kernel");
+  });
+}
+
+int hx_rotate_host(hx_ctx* c, uint64_t* out_host, const uint64_t* in_host, const uint64_t* key,
+                   int batch, int n_q, uint64_t g, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    const long long words = (long long)batch * 2 * n_q * c->N();
+    DBuf din(words, S(s)), dout(words, S(s));
+    cuda_ok(cudaMemcpyAsync(din.p, in_host, words * 8, cudaMemcpyHostToDevice, S(s)), "h2d");
+    const int rc = hx_rotate(c, (uint64_t*)dout.p, (const uint64_t*)din.p, key, batch, n_q, g, s);
+    if (rc != HX_OK) throw HxError(rc, g_last_error);
+    cuda_ok(cudaMemcpyAsync(out_host, dout.p, words * 8, cudaMemcpyDeviceToHost, S(s)), "d2h");
+    cuda_ok(cudaStreamSynchronize(S(s)), "sync");
+  });
+}
+
+int hx_mul_relin_host(hx_ctx* c, uint64_t* out_host, const uint64_t* a_host,
+                      const uint64_t* b_host, const uint64_t* rlk, int batch, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    const long long words = (long long)batch * 2 * n_q * c->N();
+    DBuf da(words, S(s)), db(words, S(s)), dout(words, S(s));
+    cuda_ok(cudaMemcpyAsync(da.p, a_host, words * 8, cudaMemcpyHostToDevice, S(s)), "h2d");
+    cuda_ok(cudaMemcpyAsync(db.p, b_host, words * 8, cudaMemcpyHostToDevice, S(s)), "h2d");
+    const int rc = hx_mul_relin(c, (uint64_t*)dout.p, (const uint64_t*)da.p,
+                                (const uint64_t*)db.p, rlk, batch, n_q, s);
+    if (rc != HX_OK) throw HxError(rc, g_last_error);
+    cuda_ok(cudaMemcpyAsync(out_host, dout.p, words * 8, cudaMemcpyDeviceToHost, S(s)), "d2h");
+    cuda_ok(cudaStreamSynchronize(S(s)), "sync");
+  });
+}
+
+}  // extern "C"

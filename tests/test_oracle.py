@@ -1,0 +1,188 @@
+"""CPU tests: pin the C oracle against the reference's own code.
+
+1. tests/golden/ref_n1024.npz (generated from oracle/_ref = the reference's
+   compiled primitives, tests/golden/make_golden.py) -- always run.
+2. Live comparison with oracle/_ref at config-1 size when it is built.
+3. SPEC known answers and BASELINE prime shapes.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from configs import config1, config2
+from oracle_bindings import (
+    Oracle,
+    Ref,
+    find_ntt_primes,
+    galois_elt,
+    gaussian,
+    oracle_lib,
+    ptr,
+    ref_available,
+    ternary,
+    uniform_limbs,
+)
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "ref_n1024.npz")
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return np.load(GOLD)
+
+
+@pytest.fixture(scope="module")
+def gorc(gold):
+    return Oracle(int(gold["logn"]), [int(x) for x in gold["chain"]], [int(x) for x in gold["special"]], 1)
+
+
+def test_golden_psi_and_ntt(gold, gorc):
+    for i in range(4):
+        assert gorc.psi(i) == int(gold["psi"][i])
+    x = gold["ntt_in"]
+    assert np.array_equal(gorc.ntt_fwd(x, 3, 1), gold["ntt_fwd"])
+    assert np.array_equal(gorc.ntt_inv(x, 3, 1), gold["ntt_inv"])
+
+
+def test_golden_ring_ops(gold, gorc):
+    a = gold["auto_in"]
+    for g, exp in zip(gold["auto_g"], gold["auto_out"]):
+        assert np.array_equal(gorc.automorphism_coeff(a, 3, 0, int(g)), exp)
+        # NTT-domain permutation form agrees with the coefficient-domain map
+        fa = gorc.ntt_fwd(a, 3)
+        assert np.array_equal(gorc.ntt_inv(gorc.automorphism_ntt(fa, 3, 0, int(g)), 3), exp)
+    assert np.array_equal(gorc.rescale_coeff(a, 3), gold["rescale_out"])
+    assert np.array_equal(gorc.moddown_coeff(gold["moddown_in"], 3), gold["moddown_out"])
+    assert np.array_equal(gorc.mul_acc(gold["mac_acc"], gold["mac_a"], gold["mac_b"], 3), gold["mac_out"])
+    fa = gorc.ntt_fwd(gold["mac_a"], 3)
+    fb = gorc.ntt_fwd(gold["mac_b"], 3)
+    assert np.array_equal(gorc.ntt_inv(gorc.binop("hxo_mul", fa, fb, 3), 3), gold["ring_mul_out"])
+
+
+def test_golden_keyswitch(gold, gorc):
+    out = gorc.rotate(gold["ks_ct"], gold["ks_key"], 3, int(gold["ks_g"]))
+    assert np.array_equal(out, gold["ks_out"])
+
+
+def test_golden_encoder_roundtrip(gold):
+    # the reference encoder's output decodes back to m (< 1e-4)
+    m = gold["enc_m"]
+    assert np.abs(gold["dec_out"][: len(m)] - m).max() < 1e-4
+    assert np.abs(gold["dec_out"][len(m):]).max() < 1e-4
+
+
+def test_spec_ring_known_answers():
+    """identity, X * X^(N-1) = -1, N=16/q=97 vs schoolbook."""
+    L = oracle_lib()
+    q, n, logn = 97, 16, 4
+    psi = L.hxo_find_psi(q, n)
+    assert psi != 0
+    rng = np.random.default_rng(0)
+
+    def ring_mul(a, b):
+        fa, fb = a.copy(), b.copy()
+        L.hxo_ntt_forward_limb(q, psi, logn, ptr(fa))
+        L.hxo_ntt_forward_limb(q, psi, logn, ptr(fb))
+        fc = np.array([(int(x) * int(y)) % q for x, y in zip(fa, fb)], dtype=np.uint64)
+        L.hxo_ntt_inverse_limb(q, psi, logn, ptr(fc))
+        return fc
+
+    one = np.zeros(n, dtype=np.uint64)
+    one[0] = 1
+    b = rng.integers(0, q, n, dtype=np.uint64)
+    assert np.array_equal(ring_mul(one, b), b)
+    x = np.zeros(n, dtype=np.uint64)
+    x[1] = 1
+    xn1 = np.zeros(n, dtype=np.uint64)
+    xn1[n - 1] = 1
+    minus1 = np.zeros(n, dtype=np.uint64)
+    minus1[0] = q - 1
+    assert np.array_equal(ring_mul(x, xn1), minus1)
+    for _ in range(5):
+        a = rng.integers(0, q, n, dtype=np.uint64)
+        b = rng.integers(0, q, n, dtype=np.uint64)
+        sb = np.zeros(n, dtype=np.uint64)
+        L.hxo_schoolbook_negacyclic(q, n, ptr(a), ptr(b), ptr(sb))
+        assert np.array_equal(ring_mul(a, b), sb)
+
+
+def test_baseline_prime_shapes():
+    """config-1 and config-2 primes from find_ntt_primes."""
+    c1 = config1(13)
+    assert c1["chain"] == [549756026881, 549756174337, 549756239873]
+    assert c1["special"] == [562949954093057]
+    c2 = config2(16, 24)
+    assert c2["chain"][0] == 576460752308273153
+    assert c2["special"] == [576460752315482113, 576460752319021057, 576460752319414273]
+    assert len(c2["chain"]) == 24 and all(q.bit_length() == 40 for q in c2["chain"][1:])
+
+
+def _centred_max(a, b, q):
+    d = (a.astype(object) - b.astype(object)) % q
+    d = np.where(d > q // 2, d - q, d)
+    return int(np.abs(d).max())
+
+
+@pytest.mark.parametrize("logn,n_chain", [(11, 24), (12, 8)])
+def test_oracle_hybrid_ks_decrypts(logn, n_chain):
+    """K=3 / alpha=3 hybrid KS: rotations and relinearisation decrypt correctly
+    at every level (the builder's restatement has no reference code)."""
+    p = config2(logn, n_chain)
+    orc = Oracle(p["logn"], p["chain"], p["special"], 3)
+    nq, K, n = len(p["chain"]), 3, 1 << logn
+    rng = np.random.default_rng(3)
+    s_full = orc.ntt_fwd(orc.from_i64(ternary(rng, n), nq, K), nq, K)
+    g = galois_elt(5, n)
+    dn = orc.dnum(nq)
+    key = orc.keygen_ksk(s_full, orc.automorphism_ntt(s_full, nq, K, g),
+                         uniform_limbs(rng, p["chain"] + p["special"], n, (dn,)),
+                         np.stack([gaussian(rng, n) for _ in range(dn)]))
+    m = rng.integers(-(2**10), 2**10, n).astype(np.int64)
+    ct = orc.encrypt_sk(orc.ntt_fwd(orc.from_i64(m, nq), nq), s_full,
+                        uniform_limbs(rng, p["chain"], n), gaussian(rng, n), nq)
+    for lvl in (nq, max(2, nq // 2), 1):
+        c = np.ascontiguousarray(ct[:, :lvl])
+        rot = orc.rotate(c, key, lvl, g)
+        dec = orc.ntt_inv(orc.decrypt(rot, s_full, lvl), lvl)
+        ref = orc.automorphism_coeff(orc.from_i64(m, lvl), lvl, 0, g)
+        assert _centred_max(dec[0], ref[0], p["chain"][0]) < 2**12
+    s2 = orc.binop("hxo_mul", s_full, s_full, nq, K)
+    rlk = orc.keygen_ksk(s_full, s2, uniform_limbs(rng, p["chain"] + p["special"], n, (dn,)),
+                         np.stack([gaussian(rng, n) for _ in range(dn)]))
+    pr = orc.mul_relin(ct, ct, rlk, nq)
+    dec = orc.ntt_inv(orc.decrypt(pr, s_full, nq), nq)
+    mm = orc.ntt_fwd(orc.from_i64(m, nq), nq)
+    exp = orc.ntt_inv(orc.binop("hxo_mul", mm, mm, nq), nq)
+    assert _centred_max(dec[1], exp[1], p["chain"][1]) < 2**30
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built (needs /root/reference)")
+def test_live_reference_config1():
+    """Oracle vs the reference's compiled primitives at full config-1 size."""
+    p = config1(13)
+    orc = Oracle(p["logn"], p["chain"], p["special"], 1)
+    ref = Ref(p["logn"], p["chain"], p["special"], 1)
+    n, primes = 1 << 13, p["chain"] + p["special"]
+    rng = np.random.default_rng(4)
+    x = uniform_limbs(rng, primes, n)
+    fx = orc.ntt_fwd(x, 3, 1)
+    for i in range(4):
+        assert np.array_equal(fx[i], ref.ntt_fwd(i, x[i]))
+    a = x[:3].copy()
+    for k in (1, 7, 2047):
+        g = galois_elt(k, n)
+        o = np.zeros_like(a)
+        ref.L.ref_lc_automorphism(ref.h, ptr(a), ptr(o), 3, 0, g)
+        assert np.array_equal(orc.automorphism_coeff(a, 3, 0, g), o)
+    o = np.zeros((3, n), dtype=np.uint64)
+    ref.L.ref_lc_moddown(ref.h, ptr(x), ptr(o), 3)
+    assert np.array_equal(orc.moddown_coeff(x, 3), o)
+    s_full = orc.ntt_fwd(orc.from_i64(ternary(rng, n), 3, 1), 3, 1)
+    g = galois_elt(3, n)
+    key = orc.keygen_ksk(s_full, orc.automorphism_ntt(s_full, 3, 1, g),
+                         uniform_limbs(rng, primes, n, (3,)), np.stack([gaussian(rng, n) for _ in range(3)]))
+    ct = uniform_limbs(rng, p["chain"], n, (2,))
+    o = np.zeros_like(ct)
+    ref.L.ref_rotate(ref.h, ptr(ct), ptr(key), ptr(o), 3, g)
+    assert np.array_equal(orc.rotate(ct, key, 3, g), o)
