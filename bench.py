@@ -1,0 +1,406 @@
+#!/usr/bin/env python3
+"""bench.py -- key-switches/s at N=2^16 on B200 (BASELINE.json configs[1]).
+
+Workload ("step"): one single-rotation key switch (hx_rotate = ModUp ->
+key inner product -> ModDown -> + tau(c0)) over a batch of 256 ciphertexts,
+N = 2^16, 24 chain primes (1 x 60-bit + 23 x 40-bit) + 3 special primes,
+alpha = 3 (dnum = 8), one rotation key shared by the batch, ciphertext
+coefficients uniform mod each prime (synthetic, seeded).  value = key
+switches per second over all ranks (weak scaling: every rank owns its own
+256-ciphertext batch; the primitive does not shard, so N > 1 runs replicas).
+
+Also reported (extras): limb-NTTs/s, HMult+relin/s and the 32-rotation
+hoisted batch, each on the same shapes.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+LOGN = 16
+N = 1 << LOGN
+N_CHAIN = 24
+BATCH = 256
+ALPHA = 3
+HOIST_R = 32
+HOIST_CHUNK = 8
+
+
+def primes():
+    """config-2 primes: reference find_ntt_primes (modmath.hpp:138-152)."""
+    # a self-contained restatement (bench must not depend on the oracle for
+    # the product path): first primes = 1 mod 2N at or above the starts.
+    def is_prime(n):
+        if n < 2:
+            return False
+        small = [2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37]
+        for p in small:
+            if n % p == 0:
+                return n == p
+        d, r = n - 1, 0
+        while d % 2 == 0:
+            d //= 2
+            r += 1
+        for a in small:
+            x = pow(a, d, n)
+            if x in (1, n - 1):
+                continue
+            for _ in range(r - 1):
+                x = x * x % n
+                if x == n - 1:
+                    break
+            else:
+                return False
+        return True
+
+    def find(start, count, two_n, exclude=()):
+        out, p = [], ((start + two_n - 1) // two_n) * two_n + 1
+        while len(out) < count:
+            if p not in exclude and is_prime(p):
+                out.append(p)
+            p += two_n
+        return out
+
+    two_n = 2 * N
+    q0 = find(1 << 59, 1, two_n)
+    rest = find(1 << 39, N_CHAIN - 1, two_n)
+    sp = find(1 << 59, 3, two_n, exclude=q0)
+    return q0 + rest, sp
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = self.rows
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ helpers
+def rand_limbs(torch, gen, ps, lead, device):
+    """uniform residues, shape lead + (len(ps), N), int64 holding u64."""
+    out = torch.empty(tuple(lead) + (len(ps), N), dtype=torch.int64, device=device)
+    for k, q in enumerate(ps):
+        out[..., k, :] = torch.randint(0, q, tuple(lead) + (N,), generator=gen, device=device,
+                                       dtype=torch.int64)
+    return out
+
+
+def make_key(torch, ctx, gen, chain, special, sprime_galois, device):
+    """A real switching key from a ternary secret (keygen on the GPU)."""
+    nq, K = len(chain), len(special)
+    s = torch.randint(-1, 2, (N,), generator=gen, device=device, dtype=torch.int64)
+    s_full = torch.empty((nq + K, N), dtype=torch.int64, device=device)
+    ctx.from_i64(s_full, s, 1, nq, K)
+    ctx.ntt_fwd(s_full, 1, nq, K)
+    sp = torch.empty_like(s_full)
+    if sprime_galois == 0:  # relinearisation key: s' = s^2
+        ctx.binop("mul", sp, s_full, s_full, 1, nq, K)
+    else:
+        ctx.automorphism(sp, s_full, 1, nq, K, sprime_galois)
+    dn = ctx.dnum(nq)
+    a = rand_limbs(torch, gen, chain + special, (dn,), device)
+    e = torch.round(torch.randn((dn, N), generator=gen, device=device) * 3.2).to(torch.int64)
+    key = torch.empty(ctx.key_words(), dtype=torch.int64, device=device)
+    ctx.keygen_ksk(key, s_full, sp, a, e)
+    return key
+
+
+def time_loop(torch, fn, steps, warmup, stream):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(steps):
+        fn()
+    t1.record()
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / 1e3  # seconds
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ CPU arms
+def cpu_reference_ks(samples: int, threads: int):
+    """The reference's own primitives (oracle/_ref: NttTables, Modulus with the
+    Barrett fix) composed into the SPEC key switch, timed on host cores."""
+    import numpy as np
+
+    from oracle_bindings import Oracle, Ref, galois_elt, ptr, ref_available, uniform_limbs
+
+    chain, special = primes()
+    rng = np.random.default_rng(1)
+    kind = "reference" if ref_available() else "port"
+    key = uniform_limbs(rng, chain + special, N, ((N_CHAIN + ALPHA - 1) // ALPHA, 2))
+    ct = uniform_limbs(rng, chain, N, (2,))
+    out = np.zeros_like(ct)
+    g = galois_elt(1, N)
+    if kind == "reference":
+        r = Ref(LOGN, chain, special, ALPHA)
+        r.L.ref_set_threads(r.h, threads)
+        run = lambda: r.L.ref_rotate(r.h, ptr(ct), ptr(key), ptr(out), N_CHAIN, g)  # noqa: E731
+    else:
+        from oracle_bindings import oracle_lib
+
+        o = Oracle(LOGN, chain, special, ALPHA)
+        oracle_lib().hxo_set_threads(threads)
+        run = lambda: o.rotate(ct, key, N_CHAIN, g)  # noqa: E731
+    run()  # warm
+    t = time.perf_counter()
+    for _ in range(samples):
+        run()
+    dt = time.perf_counter() - t
+    return samples / dt, kind, dt
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    per_step = 1
+    t_total, vals = 0.0, []
+    kind = "port"
+    for i in range(args.warmup + args.steps):
+        v, kind, dt = cpu_reference_ks(per_step, threads)
+        if i >= args.warmup:
+            vals.append(v)
+            t_total += dt
+    value = args.steps * per_step / t_total
+    line = {
+        "impl": "reference", "metric": "key-switches/s (N=2^16, 24+3 primes, dnum=8)",
+        "value": value, "unit": "KS/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": "config2 single-rotation KS (bounded sample: 1 ciphertext per step)",
+                   "batch_per_step": per_step, "N": N, "chain_primes": N_CHAIN, "special_primes": 3,
+                   "alpha": ALPHA},
+        "cpu_baseline": {"value": value, "unit": "KS/s", "cores": threads, "kind": kind,
+                         "sample": f"{args.steps} x 1 ciphertext rotation key switch"},
+        "e2e": {"value": value, "unit": "KS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2512_11135_b200 import Context
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    chain, special = primes()
+    ctx = Context(LOGN, chain, special, ALPHA)
+    stream = torch.cuda.current_stream().cuda_stream
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(20251211 * 10 + 2 + rank)
+    nq, K = N_CHAIN, len(special)
+    g1 = pow(5, 1, 2 * N)
+    key = make_key(torch, ctx, gen, chain, special, g1, dev)
+    cts = rand_limbs(torch, gen, chain, (BATCH, 2), dev)
+    out = torch.empty_like(cts)
+    torch.cuda.synchronize()
+
+    def step():
+        ctx.rotate(out, cts, key, BATCH, nq, g1, stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- headline: timed region ----
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    l0 = ctx.launches()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        step()
+    t1.record()
+    barrier()
+    launches = ctx.launches() - l0
+    clocks = sampler.stop()
+    secs = t0.elapsed_time(t1) / 1e3
+    if world > 1:
+        tt = torch.tensor([secs], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        secs = float(tt.item())
+    ks_total = BATCH * args.steps * world
+    value = ks_total / secs
+
+    # ---- roofline of the dominant kernel family (the NTT) ----
+    # algorithmic bytes per limb-NTT = read + write one limb = 2 N 8 B.
+    # One KS at 24 limbs runs 24 INTT (ModUp) + 8*24 NTT (ModUp) + 2*3 INTT +
+    # 2*24 NTT (ModDown) = 270 limb transforms.
+    hbm_peak, peak_kind = peaks()
+    ntt_buf = rand_limbs(torch, gen, chain, (BATCH, 2), dev)
+    ntt_secs = time_loop(torch, lambda: ctx.ntt_fwd(ntt_buf, 2 * BATCH, nq, 0, stream), 3, 1, stream)
+    ntt_limbs = 2 * BATCH * nq
+    ntt_launch_s = ntt_secs / 3 / 2  # two pass kernels per transform
+    ntt_bytes_per_launch = ntt_limbs * 2 * N * 8
+    ntt_achieved = ntt_bytes_per_launch / ntt_launch_s / 1e9
+    roofline = {"kernel": "ntt_pass_kernel (fwd, COL+ROW passes)", "bound": "hbm",
+                "achieved": ntt_achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ntt_achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": ntt_bytes_per_launch,
+                "note": "NTT is integer-issue bound on CUDA cores (DESIGN.md §5); HBM frac shown "
+                        "per the contract"}
+
+    extras = {"limb_ntt_per_s": ntt_limbs / (ntt_secs / 3)}
+    if not args.no_extras:
+        # HMult + relin over the batch
+        rlk = make_key(torch, ctx, gen, chain, special, 0, dev)
+        b2 = rand_limbs(torch, gen, chain, (BATCH, 2), dev)
+        hm = time_loop(torch, lambda: ctx.mul_relin(out, cts, b2, rlk, BATCH, nq, stream), 2, 1, stream)
+        extras["hmult_relin_per_s"] = BATCH * 2 / hm
+        del b2
+        # 32-rotation hoisted batch, in chunks of HOIST_CHUNK ciphertexts
+        gs = [pow(5, k, 2 * N) for k in range(1, HOIST_R + 1)]
+        keys = [key] * HOIST_R  # one resident key reused (key bytes identical in size)
+        hout = torch.empty((HOIST_CHUNK, HOIST_R, 2, nq, N), dtype=torch.int64, device=dev)
+
+        def hoist():
+            for c0 in range(0, BATCH, HOIST_CHUNK):
+                ctx.rotate_hoisted(hout, cts[c0:c0 + HOIST_CHUNK], keys, gs, HOIST_CHUNK, nq, stream)
+
+        hs = time_loop(torch, hoist, 1, 1, stream)
+        extras["hoisted32_ks_per_s"] = BATCH * HOIST_R / hs
+        del hout
+
+    # ---- e2e through the host-buffer C-ABI entry point ----
+    hin = torch.empty(cts.shape, dtype=torch.int64, pin_memory=True)
+    hin.copy_(cts.cpu())
+    hout_h = torch.empty_like(hin, pin_memory=True)
+    e2e_steps = max(1, min(args.steps, 3))
+    ctx.rotate_host(hout_h.data_ptr(), hin.data_ptr(), key, BATCH, nq, g1, stream)  # warm
+    barrier()
+    te = time.perf_counter()
+    for _ in range(e2e_steps):
+        ctx.rotate_host(hout_h.data_ptr(), hin.data_ptr(), key, BATCH, nq, g1, stream)
+    barrier()
+    e2e_secs = time.perf_counter() - te
+    if world > 1:
+        tt = torch.tensor([e2e_secs], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_secs = float(tt.item())
+    ct_bytes = BATCH * 2 * nq * N * 8
+    e2e = {"value": BATCH * e2e_steps * world / e2e_secs, "unit": "KS/s",
+           "h2d_bytes_per_step": ct_bytes, "d2h_bytes_per_step": ct_bytes,
+           "api": "hx_rotate_host (pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        samples = 4
+        v, kind, dt = cpu_reference_ks(samples, os.cpu_count() or 1)
+        cpu = {"value": v, "unit": "KS/s", "cores": os.cpu_count(), "kind": kind,
+               "sample": f"{samples} single-rotation key switches of 1 ciphertext ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": "key-switches/s (N=2^16, 24+3 primes, dnum=8)", "value": value, "unit": "KS/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded uniform residues, GPU keygen)",
+            "config": {"workload": "config2 single-rotation KS, batch 256 ciphertexts per GPU",
+                       "N": N, "chain_primes": nq, "special_primes": K, "alpha": ALPHA,
+                       "batch_per_gpu": BATCH, "parallelism": f"replicas x{world}",
+                       "l2": "inputs larger than L2 (6.4 GB of ciphertexts per step)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks, "extras": extras,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

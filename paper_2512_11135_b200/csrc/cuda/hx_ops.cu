@@ -419,6 +419,13 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
     c->n_special = n_special;
     c->alpha = alpha;
     cuda_ok(cudaGetDevice(&c->device), "cudaGetDevice");
+    // keep stream-ordered scratch (ModUp digits, ModDown temporaries) cached
+    // in the device pool instead of returning it to the OS at every sync
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+      unsigned long long thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     c->primes.assign(chain, chain + n_chain);
     c->primes.insert(c->primes.end(), special, special + n_special);
     const u64 N = 1ull << logn;

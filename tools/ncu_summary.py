@@ -1,0 +1,68 @@
+"""Summarise ncu outputs for profiles/ (run here, no GPU needed).
+
+  python tools/ncu_summary.py launches <launches.csv>   per-kernel share of device time
+  python tools/ncu_summary.py full <report.ncu-rep>      key metrics per captured launch
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+UNIT = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h = rows[hi]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    tot, cnt = collections.defaultdict(float), collections.Counter()
+    for r in rows[hi + 1:]:
+        if len(r) <= vi or not r[vi]:
+            continue
+        us = float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
+        name = r[ki].split("(")[0].replace("void ", "")[:60]
+        tot[name] += us
+        cnt[name] += 1
+    T = sum(tot.values())
+    print(f"| kernel | launches | total ms | share | avg us |\n|---|---|---|---|---|")
+    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+        print(f"| `{k}` | {cnt[k]} | {v/1e3:.2f} | {100*v/T:.1f}% | {v/cnt[k]:.1f} |")
+    print(f"\ntotal device time {T/1e3:.2f} ms over {sum(cnt.values())} launches")
+
+
+METRICS = [
+    ("gpu__time_duration.sum", "time"),
+    ("dram__bytes_read.sum", "dram rd"),
+    ("dram__bytes_write.sum", "dram wr"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram %"),
+    ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", "fmaheavy %"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "alu %"),
+    ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy %"),
+    ("launch__registers_per_thread", "regs"),
+    ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem conflicts"),
+    ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall lsb"),
+]
+
+
+def full(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    idx = {n: i for i, n in enumerate(h)}
+    print("| kernel | " + " | ".join(m[1] for m in METRICS) + " |")
+    print("|---" * (len(METRICS) + 1) + "|")
+    for r in rows[2:]:
+        cells = [r[idx["Kernel Name"]].split("(")[0].replace("void ", "")[:45]]
+        for m, _ in METRICS:
+            v = r[idx[m]] if m in idx else "-"
+            u = units[idx[m]] if m in idx else ""
+            cells.append(f"{v} {u}".strip())
+        print("| " + " | ".join(cells) + " |")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])

@@ -1,0 +1,54 @@
+"""Small launch sequences for ncu captures (one GPU, after a plain run exits 0).
+
+  python tools/prof.py ks [batch]     one hx_rotate over `batch` ciphertexts (N=2^16, 24+3 primes)
+  python tools/prof.py ntt [batch]    forward + inverse NTT over batch x 2 x 24 limbs
+  python tools/prof.py mac [n1] [n2]  one BSGS MAC launch (24 limbs)
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2512_11135_b200 import Context  # noqa: E402
+
+
+def main():
+    mode = sys.argv[1] if len(sys.argv) > 1 else "ks"
+    chain, special = bench.primes()
+    ctx = Context(bench.LOGN, chain, special, bench.ALPHA)
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1)
+    nq, N = len(chain), bench.N
+    if mode == "ks":
+        B = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+        g = pow(5, 1, 2 * N)
+        key = bench.make_key(torch, ctx, gen, chain, special, g, dev)
+        cts = bench.rand_limbs(torch, gen, chain, (B, 2), dev)
+        out = torch.empty_like(cts)
+        for _ in range(2):
+            ctx.rotate(out, cts, key, B, nq, g)
+    elif mode == "ntt":
+        B = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+        x = bench.rand_limbs(torch, gen, chain, (B, 2), dev)
+        for _ in range(2):
+            ctx.ntt_fwd(x, 2 * B, nq, 0)
+            ctx.ntt_inv(x, 2 * B, nq, 0)
+    elif mode == "mac":
+        n1 = int(sys.argv[2]) if len(sys.argv) > 2 else 32
+        n2 = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+        baby = bench.rand_limbs(torch, gen, chain, (n1, 2), dev)
+        diags = bench.rand_limbs(torch, gen, chain, (n1 * n2,), dev)
+        inner = torch.empty((n2, 2, nq, N), dtype=torch.int64, device=dev)
+        for _ in range(2):
+            ctx.bsgs_mac(inner, baby, diags, nq, n1, n2, nq)
+    torch.cuda.synchronize()
+    print("ok", mode, ctx.launches())
+
+
+if __name__ == "__main__":
+    main()
