@@ -1,22 +1,33 @@
 # Build for libhx_b200.so (sm_100a CUDA kernels + C-ABI), the helix C++ host
-# library and the CPU oracle.  `make` = everything buildable here (nvcc
-# cross-compiles sm_100a without a GPU).
+# library libhelix_b200.so above it, the CPU oracle and the C++ test driver.
+# `make` = everything buildable here (nvcc cross-compiles sm_100a without a GPU).
 NVCC      ?= nvcc
 CXX       ?= g++
+CUDA_HOME ?= /usr/local/cuda
+JSON_DIR  ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O2 --expt-relaxed-constexpr
+CXXFLAGS  := -std=c++20 -O2 -fPIC -Wall -Wextra -Wno-unused-parameter -Iinclude -I$(CUDA_HOME)/include -I$(JSON_DIR)
 PKG       := paper_2512_11135_b200
 CU_DIR    := $(PKG)/csrc/cuda
+HOST_DIR  := $(PKG)/csrc/host
 CU_SRCS   := $(CU_DIR)/hx_ntt.cu $(CU_DIR)/hx_ops.cu $(CU_DIR)/hx_bsgs.cu
 CU_HDRS   := $(wildcard $(CU_DIR)/*.cuh) $(CU_DIR)/hx_internal.h include/hx_b200.h
+HOST_SRCS := $(HOST_DIR)/params.cpp $(HOST_DIR)/encoder.cpp $(HOST_DIR)/gpu_backend.cpp \
+             $(HOST_DIR)/packing.cpp $(HOST_DIR)/linalg.cpp $(HOST_DIR)/helix_c.cpp
+HOST_HDRS := $(wildcard include/helix/*.hpp) include/helix_c.h include/hx_b200.h
 BUILD     := build
 CU_OBJS   := $(patsubst $(CU_DIR)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
+HOST_OBJS := $(patsubst $(HOST_DIR)/%.cpp,$(BUILD)/host_%.o,$(HOST_SRCS))
 LIB       := $(PKG)/libhx_b200.so
+HLIB      := $(PKG)/libhelix_b200.so
+TESTBIN   := $(BUILD)/test_linalg_clear
 
-.PHONY: all lib oracle ref clean
-all: lib oracle
+.PHONY: all lib host oracle ref testbin clean
+all: lib host oracle testbin
 
 lib: $(LIB)
+host: $(HLIB)
 
 $(BUILD)/%.o: $(CU_DIR)/%.cu $(CU_HDRS)
 	@mkdir -p $(BUILD)
@@ -25,6 +36,25 @@ $(BUILD)/%.o: $(CU_DIR)/%.cu $(CU_HDRS)
 $(LIB): $(CU_OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -lcudart
 
+$(BUILD)/host_%.o: $(HOST_DIR)/%.cpp $(HOST_HDRS)
+	@mkdir -p $(BUILD)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(HLIB): $(HOST_OBJS) $(LIB)
+	$(CXX) -shared -o $@ $(HOST_OBJS) -L$(PKG) -lhx_b200 -L$(CUDA_HOME)/lib64 -lcudart \
+	  -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,$(CUDA_HOME)/lib64
+
+# C++ test driver: the SPEC linear-algebra kernels on the cleartext oracle
+# backend (oracle/clear_backend.cpp) -- counts, levels, scales, results.
+$(TESTBIN): tests/cpp/test_linalg_clear.cpp oracle/clear_backend.cpp oracle/clear_backend.hpp \
+            $(HOST_DIR)/packing.cpp $(HOST_DIR)/params.cpp $(HOST_DIR)/linalg.cpp $(HOST_HDRS)
+	@mkdir -p $(BUILD)
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -Ioracle -I$(JSON_DIR) -DHELIX_NO_GPU \
+	  tests/cpp/test_linalg_clear.cpp oracle/clear_backend.cpp $(HOST_DIR)/packing.cpp \
+	  $(HOST_DIR)/params.cpp $(HOST_DIR)/linalg.cpp -o $@
+
+testbin: $(TESTBIN)
+
 oracle:
 	$(MAKE) -C oracle all
 
@@ -32,5 +62,5 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -rf $(BUILD) $(LIB)
+	rm -rf $(BUILD) $(LIB) $(HLIB)
 	$(MAKE) -C oracle clean

@@ -156,7 +156,10 @@ def make_key(torch, ctx, gen, chain, special, sprime_galois, device):
     a = rand_limbs(torch, gen, chain + special, (dn,), device)
     e = torch.round(torch.randn((dn, N), generator=gen, device=device) * 3.2).to(torch.int64)
     key = torch.empty(ctx.key_words(), dtype=torch.int64, device=device)
-    ctx.keygen_ksk(key, s_full, sp, a, e)
+    if sprime_galois == 0:
+        ctx.keygen_ksk(key, s_full, sp, a, e)
+    else:  # rotation layout (tau^-1 applied), as hx_rotate expects
+        ctx.keygen_rotation(key, s_full, sprime_galois, a, e)
     return key
 
 

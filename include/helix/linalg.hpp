@@ -1,0 +1,70 @@
+// helix/linalg.hpp -- encrypted linear-algebra entry points (
+// the reference's src/kernels.cpp is listed in proj/CMakeLists.txt:22 but
+// absent).  Written against SlotOps only, so they run on any backend; on the
+// B200 backend (GpuLatticeBackend) matvec_bsgs dispatches to the fused device
+// pipeline (hoisted baby steps, one streaming diagonal-MAC launch, batched
+// giant-step rotations) while recording exactly the same OpTrace counts.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "helix/backend.hpp"
+#include "helix/packing.hpp"
+
+namespace helix {
+
+// SPEC.md:353-356
+struct KernelReport {
+  std::uint64_t rotations = 0, pt_muls = 0, ct_muls = 0, adds = 0;
+  int levels_consumed = 0;
+  Scale output_scale;
+  std::string to_json() const;
+};
+
+// Plaintext payloads of a PackedMatrix encoded at one level (encode once,
+// apply many times).  Diagonal layouts are encoded at scale q_level so that
+// the kernel's final rescale restores the input scale.
+struct EncodedMatrix {
+  PackedMatrix meta;  // layout / dims (payload vectors dropped)
+  int level = 0;
+  std::vector<Plaintext> pts;  // null payload = zero
+};
+
+EncodedMatrix encode_matrix(SlotOps& ops, const PackedMatrix& M, int level);
+
+// log2(span) rotate-adds at strides stride * 2^i
+Ciphertext rotate_and_sum(SlotOps& ops, const Ciphertext& ct, std::size_t span, std::size_t stride,
+                          KernelReport* report = nullptr);
+
+// Matrix-vector products; x replicated at period d (packing.hpp).  One output
+// ciphertext per row block (one for a single-block matrix).
+struct MatvecResult {
+  std::vector<Ciphertext> outputs;
+  KernelReport report;
+};
+MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x);
+MatvecResult matvec_diag(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x);
+// packed-row method: y in the first R slots; 2 levels
+MatvecResult matvec_row(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x);
+
+// SPEC signatures (single output block)
+std::pair<Ciphertext, KernelReport> matvec_bsgs(SlotOps& ops, const PackedMatrix& M, const Ciphertext& x,
+                                                const BsgsPlan& plan);
+std::pair<Ciphertext, KernelReport> matvec_diag(SlotOps& ops, const PackedMatrix& M, const Ciphertext& x);
+std::pair<Ciphertext, KernelReport> matvec_row(SlotOps& ops, const PackedMatrix& M, const Ciphertext& x);
+
+// ct-ct matmul of row-major d x d operands: 2d pt-muls,
+// d ct-muls, 2d(1 + log2 d) - 2 rotations, 2 levels.
+std::pair<Ciphertext, KernelReport> matmul_ctct(SlotOps& ops, const Ciphertext& A, const Ciphertext& B,
+                                                int d);
+
+// rotation amounts each method needs
+std::vector<std::int64_t> bsgs_rotations(const BsgsPlan& plan);
+std::vector<std::int64_t> diag_rotations(int d);
+std::vector<std::int64_t> row_rotations(const PackedMatrix& M);
+std::vector<std::int64_t> matmul_rotations(int d, std::size_t slots);
+
+}  // namespace helix

@@ -1,0 +1,94 @@
+/*
+ * helix_c.h -- C-ABI over the helix C++ host API (include/helix/ headers) as
+ * implemented on B200 by libhelix_b200.so (GpuLatticeBackend + linalg).
+ *
+ * This is the reference-facing plugin boundary for non-C++ callers (the
+ * ctypes stubs in INTEGRATION.md, the tests and bench.py): it exposes
+ * exactly the SlotBackend / SPEC kernel entry points of the reference,
+ *   SlotBackend::{encrypt, decrypt, generate_rotation_keys, rotate, add, mul,
+ *                 mul_plain, rescale}            backend.hpp:90-138
+ *   matvec_row / matvec_diag / matvec_bsgs
+ *   matmul_ctct
+ *   rotate_and_sum
+ *   OpTrace::to_json                             trace.cpp:24-32
+ * with host double vectors in and out; ciphertexts stay in HBM behind
+ * opaque handles.  Errors: NULL / negative return + hxc_last_error().
+ */
+#ifndef HELIX_C_H
+#define HELIX_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hxc_backend hxc_backend;
+typedef struct hxc_ct hxc_ct;
+typedef struct hxc_mat hxc_mat;
+
+typedef struct {
+  uint64_t rotations, pt_muls, ct_muls, adds;
+  int64_t levels_consumed;
+  double output_scale_log2;
+} hxc_report;
+
+enum { HXC_ROW = 0, HXC_DIAG = 1, HXC_BSGS = 2 };
+
+const char* hxc_last_error(void);
+
+/* CkksParams JSON (reference params.cpp:53-96 keys + "alpha") */
+hxc_backend* hxc_backend_create(const char* params_json, uint64_t seed);
+void hxc_backend_destroy(hxc_backend* b);
+int64_t hxc_slots(hxc_backend* b);
+int hxc_max_level(hxc_backend* b);
+/* the underlying hx_ctx* (libhx_b200 C-ABI) for device-level pipelines */
+void* hxc_device_context(hxc_backend* b);
+int hxc_gen_rotation_keys(hxc_backend* b, const int64_t* amounts, int count);
+
+/* encode(m, level, Delta) + encrypt; m has len <= slots entries (zero-padded) */
+hxc_ct* hxc_encrypt(hxc_backend* b, const double* m, int len, int level);
+/* decrypt + decode: writes slots() doubles */
+int hxc_decrypt(hxc_backend* b, const hxc_ct* ct, double* out);
+void hxc_ct_free(hxc_ct* ct);
+int hxc_ct_level(const hxc_ct* ct);
+double hxc_ct_scale_log2(const hxc_ct* ct);
+/* device pointer to the ciphertext words [2][level+1][N] */
+uint64_t* hxc_ct_device_ptr(const hxc_ct* ct);
+
+hxc_ct* hxc_add(hxc_backend* b, const hxc_ct* x, const hxc_ct* y);
+hxc_ct* hxc_mul(hxc_backend* b, const hxc_ct* x, const hxc_ct* y);
+/* x (.) encode(m, x.level, scale_log2 == 0 ? q_level : 2^scale_log2) */
+hxc_ct* hxc_mul_plain(hxc_backend* b, const hxc_ct* x, const double* m, int len);
+hxc_ct* hxc_rotate(hxc_backend* b, const hxc_ct* x, int64_t k);
+hxc_ct* hxc_rescale(hxc_backend* b, const hxc_ct* x);
+hxc_ct* hxc_mod_down(hxc_backend* b, const hxc_ct* x, int level);
+hxc_ct* hxc_rotate_and_sum(hxc_backend* b, const hxc_ct* x, int64_t span, int64_t stride,
+                           hxc_report* rep);
+
+/* Pack (method HXC_ROW / HXC_DIAG / HXC_BSGS, default BSGS plan) and encode a
+ * rows x cols row-major matrix at `level` (encoding is not part of a matvec). */
+hxc_mat* hxc_matrix_prepare(hxc_backend* b, int method, const double* A, int rows, int cols,
+                            int level);
+void hxc_matrix_free(hxc_mat* m);
+/* d, n1, n2, row_blocks, nonzero payloads */
+int hxc_matrix_info(const hxc_mat* m, int* d, int* n1, int* n2, int* blocks, int* nonzero);
+/* rotation amounts the method needs; returns the count (writes <= cap) */
+int hxc_matrix_rotations(const hxc_mat* m, int64_t* out, int cap);
+/* y = M x; writes up to cap output handles (one per row block); returns count */
+int hxc_matvec(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, int cap,
+               hxc_report* rep);
+/* ct-ct matmul of row-major d x d operands */
+hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_report* rep);
+int hxc_matmul_rotations(int d, int64_t* out, int cap);
+
+/* OpTrace JSON (canonical names ct_add ... bootstrap); returns length */
+int hxc_trace_json(hxc_backend* b, char* buf, int cap);
+void hxc_trace_reset(hxc_backend* b);
+int hxc_sync(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -111,15 +111,24 @@ int hx_moddown(hx_ctx* ctx, uint64_t* out, const uint64_t* u, int polys, int n_q
 int hx_keyswitch(hx_ctx* ctx, uint64_t* out, const uint64_t* in, const uint64_t* key, int batch,
                  int n_q, void* stream);
 /* galois_rotate: out = (tau(c0) + u0, u1), u = KS(tau(c1)),
- * ModUp hoisted before the automorphism.  in/out [batch][2][n_q][N]. */
+ * ModUp hoisted before the automorphism.  in/out [batch][2][n_q][N].
+ * `key` must be in ROTATION LAYOUT (hx_ksk_to_rotation_layout /
+ * hx_keygen_rotation): the automorphism is applied once to the output instead
+ * of to every ModUp digit; results are bit-identical to the standard-layout
+ * definition. */
 int hx_rotate(hx_ctx* ctx, uint64_t* out, const uint64_t* in, const uint64_t* key, int batch,
               int n_q, uint64_t galois, void* stream);
 /* R rotations of each ciphertext sharing one ModUp.  keys: host array of R
- * device key pointers; galois: host array of R elements.
+ * device key pointers (rotation layout); galois: host array of R elements.
  * out [batch][R][2][n_q][N]. */
 int hx_rotate_hoisted(hx_ctx* ctx, uint64_t* out, const uint64_t* in,
                       const uint64_t* const* keys, const uint64_t* galois, int R, int batch,
                       int n_q, void* stream);
+/* batch of independent rotations with per-element keys (BSGS giant steps):
+ * element b of in [batch][2][n_q][N] is rotated by galois[b] with keys[b]
+ * (rotation layout); one batched ModUp. */
+int hx_rotate_multi(hx_ctx* ctx, uint64_t* out, const uint64_t* in, const uint64_t* const* keys,
+                    const uint64_t* galois, int batch, int n_q, void* stream);
 /* tensor (LatticeContext::mul x4): a, b [batch][2][n_q][N] -> [batch][3][n_q][N] */
 int hx_tensor(hx_ctx* ctx, uint64_t* out3, const uint64_t* a, const uint64_t* b, int batch,
               int n_q, void* stream);
@@ -139,6 +148,13 @@ int hx_bsgs_mac(hx_ctx* ctx, uint64_t* inner, const uint64_t* baby, const uint64
  * e [dnum_max][N] int64; all device. */
 int hx_keygen_ksk(hx_ctx* ctx, uint64_t* key, const uint64_t* s_full, const uint64_t* sp_full,
                   const uint64_t* a_full, const int64_t* e, void* stream);
+/* rotation-layout key for galois element g from a standard-layout key:
+ * out = tau_{g^-1}(in) limb-wise (out != in) */
+int hx_ksk_to_rotation_layout(hx_ctx* ctx, uint64_t* out, const uint64_t* in, uint64_t galois,
+                              void* stream);
+/* rotation key for tau_g (s' = tau_g(s)) directly in rotation layout */
+int hx_keygen_rotation(hx_ctx* ctx, uint64_t* key, const uint64_t* s_full, uint64_t galois,
+                       const uint64_t* a_full, const int64_t* e, void* stream);
 /* ct = (m - a s + e, a), m/a [n_q][N] NTT, e [N] int64 (device) */
 int hx_encrypt_sk(hx_ctx* ctx, uint64_t* ct, const uint64_t* m, const uint64_t* s_full,
                   const uint64_t* a, const int64_t* e, int n_q, void* stream);

@@ -75,6 +75,19 @@ __global__ void automorphism_kernel(EwArgs A, u32 g) {
   A.out[base + k] = __ldg(A.a + base + ntt_auto_index((u32)k, g, A.logn));
 }
 
+// out[b][l][t] = in[b][l][perm_g(t)] with independent batch strides (words):
+// the output-side automorphism of the rotation pipeline and the key-layout
+// conversion (tau_{g^-1}) of rotation keys.
+__global__ void permute_kernel(u64* out, long long out_stride, const u64* in, long long in_stride,
+                               u32 g, int logn) {
+  const long long N = 1ll << logn;
+  const long long b = blockIdx.z;
+  const int l = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int src = g == 1 ? t : (int)ntt_auto_index((u32)t, g, logn);
+  out[b * out_stride + l * N + t] = __ldg(in + b * in_stride + l * N + src);
+}
+
 // from_i64 (rns_poly.cpp:218-227): small signed ints -> every limb.
 // v is [batch][N] int64; out [batch][limbs][N].
 __global__ void from_i64_kernel(u64* out, const long long* v, const PrimeConst* pc, LimbTable lt,

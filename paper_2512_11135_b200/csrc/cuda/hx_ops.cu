@@ -358,20 +358,42 @@ void rescale(hx_ctx* c, u64* out, const u64* in, long long polys, int n_q, cudaS
   launched(c, "combine_kernel");
 }
 
-// rotation(s) from precomputed digits of `in` (batch cts [2][n_q]); writes
-// out + r-th slot with ct stride out_ct_stride words
+void permute(hx_ctx* c, u64* out, long long out_stride, const u64* in, long long in_stride,
+             int limbs, long long batch, u64 g, cudaStream_t s) {
+  const int th = pt_threads(c);
+  hx::permute_kernel<<<dim3((unsigned)(c->N() / th), (unsigned)limbs, (unsigned)batch), th, 0, s>>>(
+      out, out_stride, in, in_stride, (hx::u32)g, c->logn);
+  launched(c, "permute_kernel");
+}
+
+u64 galois_inverse(u64 g, u64 two_n) {
+  // g odd, 2N a power of two: g^-1 = g^(N/2 - 1) (the unit group has exponent N/2)
+  u64 r = 1, b = g % two_n, e = two_n / 4 - 1;
+  while (e) {
+    if (e & 1) r = (u64)(((u128)r * b) % two_n);
+    b = (u64)(((u128)b * b) % two_n);
+    e >>= 1;
+  }
+  return r;
+}
+
+// Rotation(s) from precomputed digits of `in` (batch cts [2][n_q]) with a
+// rotation-layout key K' = tau^-1(K):
+//   U' = sum_d D_d (.) K'_d,  W = (c0 + ModDown(U'_0), ModDown(U'_1)),
+//   out = tau_g(W)
+// which equals (tau(c0) + ModDown(sum_d tau(D_d) (.) K_d), ...) bit for bit
+// because the centred ModDown commutes with tau.
 void rotate_from_digits(hx_ctx* c, u64* out, long long out_ct_stride, const u64* in,
-                        const u64* digits, const u64* key, long long batch, int n_q, u64 g,
+                        const u64* digits, const u64* key_rot, long long batch, int n_q, u64 g,
                         cudaStream_t s) {
   const long long N = c->N();
   const int ext = n_q + c->n_special;
-  DBuf U(batch * 2 * ext * N, s);
-  ks_inner(c, U.p, digits, key, batch, n_q, g, s);
-  // c0' = tau(c0) + ModDown(u0)
-  moddown(c, out, out_ct_stride, U.p, 2ll * ext * N, batch, n_q, in, 2ll * n_q * N, g, s);
-  // c1' = ModDown(u1)
-  moddown(c, out + (long long)n_q * N, out_ct_stride, U.p + (long long)ext * N, 2ll * ext * N,
+  DBuf U(batch * 2 * ext * N, s), W(batch * 2 * n_q * N, s);
+  ks_inner(c, U.p, digits, key_rot, batch, n_q, 1, s);
+  moddown(c, W.p, 2ll * n_q * N, U.p, 2ll * ext * N, batch, n_q, in, 2ll * n_q * N, 1, s);
+  moddown(c, W.p + (long long)n_q * N, 2ll * n_q * N, U.p + (long long)ext * N, 2ll * ext * N,
           batch, n_q, nullptr, 0, 1, s);
+  permute(c, out, out_ct_stride, W.p, 2ll * n_q * N, 2 * n_q, batch, g, s);
 }
 
 }  // namespace
@@ -754,6 +776,24 @@ int hx_rotate_hoisted(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
   });
 }
 
+int hx_rotate_multi(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* const* keys,
+                    const uint64_t* galois, int batch, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    const long long N = c->N(), ct = 2ll * n_q * N;
+    const int ext = n_q + c->n_special;
+    const long long dstride = (long long)c->dnum(n_q) * ext * N;
+    for (int b = 0; b < batch; ++b)
+      HX_REQUIRE((galois[b] & 1) && galois[b] < 2 * (u64)N, "galois element");
+    DBuf D((long long)batch * dstride, S(s));
+    modup(c, D.p, (const u64*)in + (long long)n_q * N, ct, batch, n_q, S(s));
+    for (int b = 0; b < batch; ++b)
+      rotate_from_digits(c, (u64*)out + b * ct, ct, (const u64*)in + b * ct, D.p + b * dstride,
+                         (const u64*)keys[b], 1, n_q, galois[b], S(s));
+  });
+}
+
 int hx_tensor(hx_ctx* c, uint64_t* out3, const uint64_t* a, const uint64_t* b, int batch, int n_q,
               void* s) {
   return guarded([&] {
@@ -825,6 +865,33 @@ int hx_keygen_ksk(hx_ctx* c, uint64_t* key, const uint64_t* s_full, const uint64
         (u64*)key, en.p, (const u64*)s_full, (const u64*)sp_full, (const u64*)a_full, c->d_pc,
         c->d_pmodq, c->n_chain, T, c->alpha, c->logn);
     launched(c, "keygen_kernel");
+  });
+}
+
+int hx_ksk_to_rotation_layout(hx_ctx* c, uint64_t* out, const uint64_t* in, uint64_t g,
+                              void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element must be odd and < 2N");
+    HX_REQUIRE(out != in, "key layout conversion cannot run in place");
+    const int limbs = c->dnum(c->n_chain) * 2 * c->n_total();
+    permute(c, (u64*)out, 0, (const u64*)in, 0, limbs, 1, galois_inverse(g, 2 * c->N()), S(s));
+  });
+}
+
+int hx_keygen_rotation(hx_ctx* c, uint64_t* key, const uint64_t* s_full, uint64_t g,
+                       const uint64_t* a_full, const int64_t* e, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element must be odd and < 2N");
+    const long long N = c->N();
+    const int T = c->n_total();
+    DBuf sp((long long)T * N, S(s)), std_key((long long)hx_key_words(c), S(s));
+    permute(c, sp.p, 0, (const u64*)s_full, 0, T, 1, g, S(s));  // s' = tau_g(s)
+    int rc = hx_keygen_ksk(c, (uint64_t*)std_key.p, s_full, (const uint64_t*)sp.p, a_full, e, s);
+    if (rc != HX_OK) throw HxError(rc, g_last_error);
+    rc = hx_ksk_to_rotation_layout(c, key, (const uint64_t*)std_key.p, g, s);
+    if (rc != HX_OK) throw HxError(rc, g_last_error);
   });
 }
 

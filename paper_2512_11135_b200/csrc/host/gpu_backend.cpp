@@ -1,0 +1,622 @@
+// gpu_backend.cpp -- helix::GpuLatticeBackend over libhx_b200 (see header).
+//
+// Bookkeeping mirrors reference_backend.cpp:63-139 (level/scale checks,
+// trace records, rotation-key checks); the arithmetic is the lattice backend
+// of SPEC.md:143-245 with hybrid key switching.  Randomness: xoshiro256**
+// seeded by splitmix64 (secret key ternary, uniform `a`, centred-binomial
+// errors with k = 21, sigma ~ 3.24 ~ the spec's 3.2).  INSECURE TOY
+// PARAMETERS: requires params.insecure_toy.
+#include "helix/gpu_backend.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "hx_b200.h"
+
+namespace helix {
+
+namespace {
+using u64 = std::uint64_t;
+
+void ck(int rc, const char* what) {
+  if (rc != HX_OK) throw std::runtime_error(std::string(what) + ": " + hx_last_error());
+}
+void cuda_ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+u64 splitmix(u64& x) {
+  u64 z = (x += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+u64 rotl(u64 x, int k) { return (x << k) | (x >> (64 - k)); }
+}  // namespace
+
+// xoshiro256**
+std::uint64_t GpuLatticeBackend::next_u64() {
+  const u64 r = rotl(rng_[1] * 5, 7) * 9;
+  const u64 t = rng_[1] << 17;
+  rng_[2] ^= rng_[0];
+  rng_[3] ^= rng_[1];
+  rng_[1] ^= rng_[2];
+  rng_[0] ^= rng_[3];
+  rng_[2] ^= t;
+  rng_[3] = rotl(rng_[3], 45);
+  return r;
+}
+
+// ------------------------------------------------------------- DeviceBuffer
+DeviceBuffer::DeviceBuffer(std::size_t w) : words(w) {
+  if (w) cuda_ck(cudaMallocAsync((void**)&ptr, w * 8, nullptr), "cudaMallocAsync");
+}
+DeviceBuffer::~DeviceBuffer() {
+  if (ptr) cudaFreeAsync(ptr, nullptr);
+}
+
+static std::shared_ptr<DeviceBuffer> dev(std::size_t words) {
+  return std::make_shared<DeviceBuffer>(words);
+}
+
+// ------------------------------------------------------------- construction
+GpuLatticeBackend::GpuLatticeBackend(CkksParams params, std::uint64_t seed)
+    : params_(std::move(params)), enc_(params_) {
+  params_.validate();
+  if (!params_.insecure_toy)
+    throw std::invalid_argument("GpuLatticeBackend: parameters must set insecure_toy (toy CKKS)");
+  if (params_.special_primes.empty())
+    throw std::invalid_argument("GpuLatticeBackend: at least one special prime required");
+  int logn = 0;
+  while ((1ull << logn) < params_.ring_degree) ++logn;
+  ctx_ = hx_ctx_create(logn, params_.moduli.data(), (int)params_.moduli.size(),
+                       params_.special_primes.data(), (int)params_.special_primes.size(),
+                       params_.digit_size);
+  if (!ctx_) throw std::runtime_error(std::string("hx_ctx_create: ") + hx_last_error());
+  u64 sm = seed;
+  for (auto& w : rng_) w = splitmix(sm);
+  const std::size_t N = params_.ring_degree;
+  const int nc = (int)params_.moduli.size(), K = (int)params_.special_primes.size();
+  // secret key: ternary, NTT form over the full basis
+  std::vector<std::int64_t> s(N);
+  for (auto& c : s) {
+    u64 r;
+    do r = next_u64() & 3;
+    while (r == 3);
+    c = (std::int64_t)r - 1;
+  }
+  DeviceBuffer sv(N);
+  cuda_ck(cudaMemcpyAsync(sv.ptr, s.data(), N * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
+  s_full_ = dev((std::size_t)(nc + K) * N);
+  ck(hx_from_i64(ctx_, s_full_->ptr, (const int64_t*)sv.ptr, 1, nc, K, nullptr), "from_i64");
+  ck(hx_ntt_fwd(ctx_, s_full_->ptr, 1, nc, K, nullptr), "ntt");
+  // relinearisation key (s' = s^2)
+  auto s2 = dev((std::size_t)(nc + K) * N);
+  ck(hx_mul(ctx_, s2->ptr, s_full_->ptr, s_full_->ptr, 1, nc, K, nullptr), "mul");
+  rlk_ = make_key(s2, 0);
+  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+}
+
+GpuLatticeBackend::~GpuLatticeBackend() {
+  rot_keys_.clear();
+  rlk_.reset();
+  s_full_.reset();
+  cudaStreamSynchronize(nullptr);
+  hx_ctx_destroy(ctx_);
+}
+
+void GpuLatticeBackend::sample_uniform(std::vector<u64>& out, int lc, int ls, int copies) {
+  const std::size_t N = params_.ring_degree;
+  out.resize((std::size_t)copies * (lc + ls) * N);
+  auto next = [&]() { return next_u64(); };
+  std::size_t o = 0;
+  for (int c = 0; c < copies; ++c)
+    for (int l = 0; l < lc + ls; ++l) {
+      const u64 q = l < lc ? params_.moduli[l] : params_.special_primes[l - lc];
+      int bits = 64 - __builtin_clzll(q);
+      const u64 mask = bits >= 64 ? ~0ull : ((1ull << bits) - 1);
+      for (std::size_t t = 0; t < N; ++t) {
+        u64 v;
+        do v = next() & mask;
+        while (v >= q);
+        out[o++] = v;
+      }
+    }
+}
+
+void GpuLatticeBackend::sample_error(std::vector<std::int64_t>& out, int copies) {
+  const std::size_t N = params_.ring_degree;
+  out.resize((std::size_t)copies * N);
+  for (auto& e : out) {
+    const u64 r = next_u64();
+    // centred binomial, k = 21: popcount(21 bits) - popcount(21 bits)
+    e = (std::int64_t)__builtin_popcountll(r & 0x1fffff) - (std::int64_t)__builtin_popcountll((r >> 21) & 0x1fffff);
+  }
+}
+
+std::shared_ptr<DeviceBuffer> GpuLatticeBackend::make_key(const std::shared_ptr<DeviceBuffer>& sp,
+                                                          std::uint64_t g) {
+  const int nc = (int)params_.moduli.size(), K = (int)params_.special_primes.size();
+  const int dn = hx_ctx_dnum(ctx_, nc);
+  std::vector<u64> a;
+  std::vector<std::int64_t> e;
+  sample_uniform(a, nc, K, dn);
+  sample_error(e, dn);
+  DeviceBuffer da(a.size()), de(e.size());
+  cuda_ck(cudaMemcpyAsync(da.ptr, a.data(), a.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
+  cuda_ck(cudaMemcpyAsync(de.ptr, e.data(), e.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
+  auto key = dev(hx_key_words(ctx_));
+  if (g == 0)
+    ck(hx_keygen_ksk(ctx_, key->ptr, s_full_->ptr, sp->ptr, da.ptr, (const int64_t*)de.ptr, nullptr), "keygen");
+  else
+    ck(hx_keygen_rotation(ctx_, key->ptr, s_full_->ptr, g, da.ptr, (const int64_t*)de.ptr, nullptr),
+       "keygen_rotation");
+  cuda_ck(cudaStreamSynchronize(nullptr), "sync");  // host a/e vectors die here
+  return key;
+}
+
+std::uint64_t GpuLatticeBackend::galois(std::int64_t r) const {
+  const u64 two_n = 2 * params_.ring_degree;
+  u64 g = 1, b = 5;
+  for (u64 e = (u64)r; e; e >>= 1) {
+    if (e & 1) g = g * b % two_n;
+    b = b * b % two_n;
+  }
+  return g;
+}
+
+void GpuLatticeBackend::generate_rotation_keys(std::span<const std::int64_t> amounts) {
+  const auto n = (std::int64_t)slots();
+  for (std::int64_t a : amounts) {
+    const std::int64_t r = detail::reduce_amount(a, n);
+    rot_set_.insert(r);
+    if (r == 0 || rot_keys_.count(r)) continue;
+    rot_keys_[r] = make_key(nullptr, galois(r));
+  }
+}
+
+const std::uint64_t* GpuLatticeBackend::rotation_key(std::int64_t r) const {
+  auto it = rot_keys_.find(r);
+  return it == rot_keys_.end() ? nullptr : it->second->ptr;
+}
+
+const GpuCiphertext& GpuLatticeBackend::payload(const Ciphertext& ct) {
+  auto* p = dynamic_cast<const GpuCiphertext*>(ct.payload.get());
+  if (!p) throw std::invalid_argument("ciphertext does not belong to the GPU backend");
+  return *p;
+}
+const GpuPlaintext& GpuLatticeBackend::payload(const Plaintext& pt) {
+  auto* p = dynamic_cast<const GpuPlaintext*>(pt.payload.get());
+  if (!p) throw std::invalid_argument("plaintext does not belong to the GPU backend");
+  return *p;
+}
+
+Ciphertext GpuLatticeBackend::wrap(std::shared_ptr<DeviceBuffer> buf, std::size_t offset, int level,
+                                   const Scale& scale) const {
+  auto p = std::make_shared<GpuCiphertext>();
+  p->buf = std::move(buf);
+  p->offset = offset;
+  p->n_q = level + 1;
+  Ciphertext ct;
+  ct.payload = std::move(p);
+  ct.level = level;
+  ct.scale = scale;
+  ct.slot_count = slots();
+  ct.id = next_handle_id();
+  return ct;
+}
+
+// ------------------------------------------------------------- encode / decode
+Plaintext GpuLatticeBackend::encode(std::span<const double> m, int level, const Scale& scale) {
+  if (m.size() > slots()) throw std::invalid_argument("encode: vector longer than slot count");
+  if (!scale.is_positive()) throw std::invalid_argument("encode: non-positive scale");
+  if (level < 0 || level > params_.max_level) throw std::invalid_argument("encode: level out of range");
+  const auto coeffs = enc_.encode_coeffs(m, level, scale.to_double());
+  const std::size_t N = params_.ring_degree;
+  DeviceBuffer dc(N);
+  cuda_ck(cudaMemcpyAsync(dc.ptr, coeffs.data(), N * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
+  auto buf = dev((std::size_t)nq(level) * N);
+  ck(hx_from_i64(ctx_, buf->ptr, (const int64_t*)dc.ptr, 1, nq(level), 0, nullptr), "from_i64");
+  ck(hx_ntt_fwd(ctx_, buf->ptr, 1, nq(level), 0, nullptr), "ntt");
+  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+  auto p = std::make_shared<GpuPlaintext>();
+  p->buf = buf;
+  p->n_q = nq(level);
+  Plaintext pt;
+  pt.payload = p;
+  pt.level = level;
+  pt.scale = scale;
+  pt.slot_count = slots();
+  return pt;
+}
+
+std::vector<Plaintext> GpuLatticeBackend::encode_many(const std::vector<std::vector<double>>& msgs,
+                                                      int level, const Scale& scale) {
+  if (level < 0 || level > params_.max_level) throw std::invalid_argument("encode: level out of range");
+  const std::size_t N = params_.ring_degree;
+  const int n = nq(level);
+  std::size_t nz = 0;
+  for (const auto& m : msgs) nz += !m.empty();
+  std::vector<Plaintext> out(msgs.size());
+  if (nz == 0) return out;
+  auto buf = dev(nz * n * N);
+  std::vector<std::int64_t> coeffs(nz * N);
+  std::size_t idx = 0;
+  for (const auto& m : msgs) {
+    if (m.empty()) continue;
+    const auto c = enc_.encode_coeffs(m, level, scale.to_double());
+    std::memcpy(coeffs.data() + idx * N, c.data(), N * 8);
+    ++idx;
+  }
+  DeviceBuffer dc(coeffs.size());
+  cuda_ck(cudaMemcpyAsync(dc.ptr, coeffs.data(), coeffs.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
+  ck(hx_from_i64(ctx_, buf->ptr, (const int64_t*)dc.ptr, (int)nz, n, 0, nullptr), "from_i64");
+  ck(hx_ntt_fwd(ctx_, buf->ptr, (int)nz, n, 0, nullptr), "ntt");
+  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+  idx = 0;
+  for (std::size_t i = 0; i < msgs.size(); ++i) {
+    Plaintext& pt = out[i];
+    pt.level = level;
+    pt.scale = scale;
+    pt.slot_count = slots();
+    if (msgs[i].empty()) continue;
+    auto p = std::make_shared<GpuPlaintext>();
+    p->buf = buf;
+    p->offset = idx * n * N;
+    p->n_q = n;
+    pt.payload = p;
+    ++idx;
+  }
+  return out;
+}
+
+std::vector<double> GpuLatticeBackend::decode(const Plaintext& pt) {
+  const std::size_t N = params_.ring_degree;
+  const int n = nq(pt.level);
+  if (!pt.payload) return std::vector<double>(slots(), 0.0);
+  const auto& p = payload(pt);
+  DeviceBuffer tmp((std::size_t)n * N);
+  cuda_ck(cudaMemcpyAsync(tmp.ptr, p.data(), (std::size_t)n * N * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
+  ck(hx_ntt_inv(ctx_, tmp.ptr, 1, n, 0, nullptr), "intt");
+  std::vector<u64> limbs((std::size_t)n * N);
+  cuda_ck(cudaMemcpyAsync(limbs.data(), tmp.ptr, limbs.size() * 8, cudaMemcpyDeviceToHost, nullptr), "d2h");
+  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+  return enc_.decode_coeffs(limbs, n, pt.scale.to_double());
+}
+
+// ------------------------------------------------------------- encrypt / decrypt
+Ciphertext GpuLatticeBackend::encrypt(const Plaintext& pt) {
+  const std::size_t N = params_.ring_degree;
+  const int n = nq(pt.level);
+  std::vector<u64> a;
+  std::vector<std::int64_t> e;
+  sample_uniform(a, n, 0, 1);
+  sample_error(e, 1);
+  DeviceBuffer da(a.size()), de(e.size());
+  cuda_ck(cudaMemcpyAsync(da.ptr, a.data(), a.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
+  cuda_ck(cudaMemcpyAsync(de.ptr, e.data(), e.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
+  std::shared_ptr<DeviceBuffer> zero;
+  const u64* m;
+  if (pt.payload) {
+    m = payload(pt).data();
+  } else {
+    zero = dev((std::size_t)n * N);
+    cuda_ck(cudaMemsetAsync(zero->ptr, 0, (std::size_t)n * N * 8, nullptr), "memset");
+    m = zero->ptr;
+  }
+  auto buf = dev((std::size_t)2 * n * N);
+  ck(hx_encrypt_sk(ctx_, buf->ptr, m, s_full_->ptr, da.ptr, (const int64_t*)de.ptr, n, nullptr), "encrypt");
+  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+  return wrap(buf, 0, pt.level, pt.scale);
+}
+
+std::vector<double> GpuLatticeBackend::decrypt(const Ciphertext& ct) {
+  const std::size_t N = params_.ring_degree;
+  const int n = nq(ct.level);
+  auto buf = dev((std::size_t)n * N);
+  ck(hx_decrypt(ctx_, buf->ptr, payload(ct).data(), s_full_->ptr, 1, n, nullptr), "decrypt");
+  auto p = std::make_shared<GpuPlaintext>();
+  p->buf = buf;
+  p->n_q = n;
+  Plaintext pt;
+  pt.payload = p;
+  pt.level = ct.level;
+  pt.scale = ct.scale;
+  pt.slot_count = slots();
+  return decode(pt);
+}
+
+// ------------------------------------------------------------- SlotOps
+Ciphertext GpuLatticeBackend::add(const Ciphertext& a, const Ciphertext& b) {
+  detail::require_same_level(a.level, b.level, "add");
+  detail::require_same_scale(a.scale, b.scale, "add");
+  const int n = nq(a.level);
+  auto buf = dev((std::size_t)2 * n * params_.ring_degree);
+  ck(hx_add(ctx_, buf->ptr, payload(a).data(), payload(b).data(), 2, n, 0, nullptr), "add");
+  trace_.record(OpKind::CtAdd, a.level);
+  return wrap(buf, 0, a.level, a.scale);
+}
+
+Ciphertext GpuLatticeBackend::add_plain(const Ciphertext& a, const Plaintext& b) {
+  detail::require_same_level(a.level, b.level, "add_plain");
+  detail::require_same_scale(a.scale, b.scale, "add_plain");
+  const std::size_t N = params_.ring_degree;
+  const int n = nq(a.level);
+  auto buf = dev((std::size_t)2 * n * N);
+  const u64* ad = payload(a).data();
+  if (b.payload)
+    ck(hx_add(ctx_, buf->ptr, ad, payload(b).data(), 1, n, 0, nullptr), "add");
+  else
+    cuda_ck(cudaMemcpyAsync(buf->ptr, ad, (std::size_t)n * N * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
+  cuda_ck(cudaMemcpyAsync(buf->ptr + (std::size_t)n * N, ad + (std::size_t)n * N, (std::size_t)n * N * 8,
+                          cudaMemcpyDeviceToDevice, nullptr), "d2d");
+  trace_.record(OpKind::PtAdd, a.level);
+  return wrap(buf, 0, a.level, a.scale);
+}
+
+Ciphertext GpuLatticeBackend::mul(const Ciphertext& a, const Ciphertext& b) {
+  detail::require_same_level(a.level, b.level, "mul");
+  if (a.level < 1) throw LevelUnderflowError("mul: no level left for a following rescale");
+  const int n = nq(a.level);
+  auto buf = dev((std::size_t)2 * n * params_.ring_degree);
+  ck(hx_mul_relin(ctx_, buf->ptr, payload(a).data(), payload(b).data(), rlk_->ptr, 1, n, nullptr), "mul_relin");
+  trace_.record(OpKind::CtMul, a.level);
+  return wrap(buf, 0, a.level, a.scale * b.scale);
+}
+
+Ciphertext GpuLatticeBackend::mul_plain(const Ciphertext& a, const Plaintext& b) {
+  detail::require_same_level(a.level, b.level, "mul_plain");
+  if (a.level < 1) throw LevelUnderflowError("mul_plain: no level left for a following rescale");
+  const std::size_t N = params_.ring_degree;
+  const int n = nq(a.level);
+  auto buf = dev((std::size_t)2 * n * N);
+  if (!b.payload) {
+    cuda_ck(cudaMemsetAsync(buf->ptr, 0, (std::size_t)2 * n * N * 8, nullptr), "memset");
+  } else {
+    const u64* ad = payload(a).data();
+    const u64* bd = payload(b).data();
+    ck(hx_mul(ctx_, buf->ptr, ad, bd, 1, n, 0, nullptr), "mul");
+    ck(hx_mul(ctx_, buf->ptr + (std::size_t)n * N, ad + (std::size_t)n * N, bd, 1, n, 0, nullptr), "mul");
+  }
+  trace_.record(OpKind::PtMul, a.level);
+  return wrap(buf, 0, a.level, a.scale * b.scale);
+}
+
+Ciphertext GpuLatticeBackend::rotate(const Ciphertext& a, std::int64_t k) {
+  const auto n = (std::int64_t)slots();
+  const std::int64_t r = detail::reduce_amount(k, n);
+  const std::size_t N = params_.ring_degree;
+  const int nqv = nq(a.level);
+  if (r == 0) {
+    auto buf = dev((std::size_t)2 * nqv * N);
+    cuda_ck(cudaMemcpyAsync(buf->ptr, payload(a).data(), (std::size_t)2 * nqv * N * 8,
+                            cudaMemcpyDeviceToDevice, nullptr), "d2d");
+    return wrap(buf, 0, a.level, a.scale);
+  }
+  const u64* key = rotation_key(r);
+  if (!rot_set_.contains(r) || !key) throw MissingRotationKeyError("rotate: no key for amount " + std::to_string(r));
+  auto buf = dev((std::size_t)2 * nqv * N);
+  ck(hx_rotate(ctx_, buf->ptr, payload(a).data(), key, 1, nqv, galois(r), nullptr), "rotate");
+  trace_.record(OpKind::Rotate, a.level);
+  return wrap(buf, 0, a.level, a.scale);
+}
+
+Ciphertext GpuLatticeBackend::rescale(const Ciphertext& a) {
+  if (a.level < 1) throw LevelUnderflowError("rescale: no levels remain");
+  if (!(a.scale.log2() > params_.delta().log2()))
+    throw std::invalid_argument("rescale: scale not above Delta (no multiplication preceded)");
+  const int n = nq(a.level);
+  auto buf = dev((std::size_t)2 * (n - 1) * params_.ring_degree);
+  ck(hx_rescale(ctx_, buf->ptr, payload(a).data(), 2, n, nullptr), "rescale");
+  trace_.record(OpKind::Rescale, a.level);
+  return wrap(buf, 0, a.level - 1, a.scale / Scale::prime(modulus_at(a.level)));
+}
+
+Ciphertext GpuLatticeBackend::mod_down(const Ciphertext& a, int target) {
+  if (target > a.level) throw std::invalid_argument("mod_down: target level above current level");
+  if (target < 0) throw std::invalid_argument("mod_down: negative target level");
+  const std::size_t N = params_.ring_degree;
+  const int n = nq(a.level), t = nq(target);
+  auto buf = dev((std::size_t)2 * t * N);
+  cuda_ck(cudaMemcpy2DAsync(buf->ptr, (std::size_t)t * N * 8, payload(a).data(), (std::size_t)n * N * 8,
+                            (std::size_t)t * N * 8, 2, cudaMemcpyDeviceToDevice, nullptr),
+          "memcpy2d");
+  if (target != a.level) trace_.record(OpKind::ModDown, a.level);
+  return wrap(buf, 0, target, a.scale);
+}
+
+Ciphertext GpuLatticeBackend::bootstrap(const Ciphertext& a) {
+  if (!params_.mock_bootstrap)
+    throw std::runtime_error("bootstrap: only the insecure mock refresh is implemented (mock_bootstrap=false)");
+  trace_.record(OpKind::Bootstrap, a.level);
+  const auto v = decrypt(a);
+  return encrypt(encode(v, params_.l_boot(), params_.delta()));
+}
+
+// ------------------------------------------------------------- fused pipelines
+std::vector<Ciphertext> GpuLatticeBackend::rotate_many(const Ciphertext& a,
+                                                       std::span<const std::int64_t> amounts) {
+  const auto n = (std::int64_t)slots();
+  const std::size_t N = params_.ring_degree;
+  const int nqv = nq(a.level);
+  const std::size_t ctw = (std::size_t)2 * nqv * N;
+  std::vector<const u64*> keys;
+  std::vector<u64> gs;
+  std::vector<std::size_t> which;
+  for (std::size_t i = 0; i < amounts.size(); ++i) {
+    const std::int64_t r = detail::reduce_amount(amounts[i], n);
+    if (r == 0) continue;
+    const u64* key = rotation_key(r);
+    if (!rot_set_.contains(r) || !key) throw MissingRotationKeyError("rotate: no key for amount " + std::to_string(r));
+    keys.push_back(key);
+    gs.push_back(galois(r));
+    which.push_back(i);
+  }
+  auto buf = dev(amounts.size() * ctw);
+  if (!keys.empty()) {
+    // hoisted outputs land contiguously; identity rotations are copied after
+    auto tmp = dev(keys.size() * ctw);
+    ck(hx_rotate_hoisted(ctx_, tmp->ptr, payload(a).data(), keys.data(), gs.data(), (int)keys.size(), 1,
+                         nqv, nullptr), "rotate_hoisted");
+    for (std::size_t j = 0; j < which.size(); ++j)
+      cuda_ck(cudaMemcpyAsync(buf->ptr + which[j] * ctw, tmp->ptr + j * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
+                              nullptr), "d2d");
+    trace_.record(OpKind::Rotate, a.level, keys.size());
+  }
+  std::vector<Ciphertext> out;
+  for (std::size_t i = 0; i < amounts.size(); ++i) {
+    if (detail::reduce_amount(amounts[i], n) == 0)
+      cuda_ck(cudaMemcpyAsync(buf->ptr + i * ctw, payload(a).data(), ctw * 8, cudaMemcpyDeviceToDevice, nullptr),
+              "d2d");
+    out.push_back(wrap(buf, i * ctw, a.level, a.scale));
+  }
+  return out;
+}
+
+Ciphertext GpuLatticeBackend::bsgs_block(const std::vector<Ciphertext>& baby,
+                                         const std::vector<Plaintext>& diags, int n1, int n2) {
+  if ((int)baby.size() < n1 || (int)diags.size() < n1 * n2) throw std::invalid_argument("bsgs_block: shape");
+  const Ciphertext& x = baby[0];
+  const int level = x.level, nqv = nq(level);
+  const std::size_t N = params_.ring_degree, ctw = (std::size_t)2 * nqv * N, ptw = (std::size_t)nqv * N;
+  const auto n = (std::int64_t)slots();
+  // baby steps contiguous [n1][2][n_q][N]
+  std::shared_ptr<DeviceBuffer> bb;
+  const u64* baby_ptr = nullptr;
+  {
+    const auto& p0 = payload(baby[0]);
+    bool contiguous = true;
+    for (int k = 1; k < n1 && contiguous; ++k) {
+      const auto& pk = payload(baby[k]);
+      contiguous = pk.buf == p0.buf && pk.offset == p0.offset + k * ctw;
+    }
+    if (contiguous) {
+      baby_ptr = p0.data();
+    } else {
+      bb = dev(n1 * ctw);
+      for (int k = 0; k < n1; ++k)
+        cuda_ck(cudaMemcpyAsync(bb->ptr + k * ctw, payload(baby[k]).data(), ctw * 8, cudaMemcpyDeviceToDevice,
+                                nullptr), "d2d");
+      baby_ptr = bb->ptr;
+    }
+  }
+  // diagonals: gather the non-zero ones of each giant group, MAC per group
+  // (a group of all-zero diagonals contributes nothing and is skipped)
+  Scale dscale;
+  bool have_scale = false;
+  auto inner = dev((std::size_t)n2 * ctw);
+  std::vector<int> live;
+  std::uint64_t ptmuls = 0, adds = 0;
+  bool all_contig = true;
+  {
+    const GpuPlaintext* p0 = diags[0].payload ? &payload(diags[0]) : nullptr;
+    for (std::size_t i = 0; i < (std::size_t)n1 * n2 && all_contig; ++i) {
+      if (!diags[i].payload || !p0) {
+        all_contig = false;
+        break;
+      }
+      const auto& pi = payload(diags[i]);
+      all_contig = pi.buf == p0->buf && pi.offset == p0->offset + i * ptw && diags[i].level == level &&
+                   diags[i].scale == diags[0].scale;
+    }
+    if (all_contig) {
+      dscale = diags[0].scale;
+      have_scale = true;
+      ck(hx_bsgs_mac(ctx_, inner->ptr, baby_ptr, p0->data(), nqv, n1, n2, nqv, nullptr), "bsgs_mac");
+      ptmuls = (std::uint64_t)n1 * n2;
+      adds = (std::uint64_t)(n1 - 1) * n2;
+      for (int j = 0; j < n2; ++j) live.push_back(j);
+    }
+  }
+  for (int j = 0; j < n2 && !all_contig; ++j) {
+    std::vector<int> ks;
+    for (int k = 0; k < n1; ++k) {
+      const Plaintext& pt = diags[(std::size_t)j * n1 + k];
+      if (!pt.payload) continue;
+      if (pt.level != level) throw LevelMismatchError("bsgs_block: diagonal level mismatch");
+      if (!have_scale) {
+        dscale = pt.scale;
+        have_scale = true;
+      } else if (pt.scale != dscale) {
+        throw ScaleMismatchError("bsgs_block: diagonal scales differ");
+      }
+      ks.push_back(k);
+    }
+    if (ks.empty()) continue;
+    ptmuls += ks.size();
+    adds += ks.size() - 1;
+    // contiguous run of this group's diagonals (the common case: encode_many)?
+    const auto& p0 = payload(diags[(std::size_t)j * n1 + ks[0]]);
+    bool dense_contig = (int)ks.size() == n1;
+    for (int k = 1; k < n1 && dense_contig; ++k) {
+      const auto& pk = payload(diags[(std::size_t)j * n1 + k]);
+      dense_contig = pk.buf == p0.buf && pk.offset == p0.offset + k * ptw;
+    }
+    if (dense_contig) {
+      ck(hx_bsgs_mac(ctx_, inner->ptr + j * ctw, baby_ptr, p0.data(), nqv, n1, 1, nqv, nullptr), "bsgs_mac");
+    } else {
+      // sparse group: gather its diagonals and the matching baby steps
+      DeviceBuffer dg(ks.size() * ptw), bs(ks.size() * ctw);
+      for (std::size_t i = 0; i < ks.size(); ++i) {
+        cuda_ck(cudaMemcpyAsync(dg.ptr + i * ptw, payload(diags[(std::size_t)j * n1 + ks[i]]).data(), ptw * 8,
+                                cudaMemcpyDeviceToDevice, nullptr), "d2d");
+        cuda_ck(cudaMemcpyAsync(bs.ptr + i * ctw, baby_ptr + ks[i] * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
+                                nullptr), "d2d");
+      }
+      ck(hx_bsgs_mac(ctx_, inner->ptr + j * ctw, bs.ptr, dg.ptr, nqv, (int)ks.size(), 1, nqv, nullptr),
+         "bsgs_mac");
+    }
+    live.push_back(j);
+  }
+  if (live.empty()) throw std::invalid_argument("bsgs_block: all diagonals are zero");
+  trace_.record(OpKind::PtMul, level, ptmuls);
+  if (adds) trace_.record(OpKind::CtAdd, level, adds);
+  const Scale out_scale = x.scale * dscale;
+  // giant steps: rotate every live group j >= 1 by n1 j (one batched ModUp)
+  std::vector<const u64*> keys;
+  std::vector<u64> gs;
+  std::vector<int> rot_j;
+  for (int j : live) {
+    if (j == 0) continue;
+    const std::int64_t r = detail::reduce_amount((std::int64_t)n1 * j, n);
+    if (r == 0) continue;
+    const u64* key = rotation_key(r);
+    if (!rot_set_.contains(r) || !key) throw MissingRotationKeyError("rotate: no key for amount " + std::to_string(r));
+    keys.push_back(key);
+    gs.push_back(galois(r));
+    rot_j.push_back(j);
+  }
+  std::shared_ptr<DeviceBuffer> rotated;
+  if (!keys.empty()) {
+    DeviceBuffer src(keys.size() * ctw);
+    for (std::size_t i = 0; i < rot_j.size(); ++i)
+      cuda_ck(cudaMemcpyAsync(src.ptr + i * ctw, inner->ptr + rot_j[i] * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
+                              nullptr), "d2d");
+    rotated = dev(keys.size() * ctw);
+    ck(hx_rotate_multi(ctx_, rotated->ptr, src.ptr, keys.data(), gs.data(), (int)keys.size(), nqv, nullptr),
+       "rotate_multi");
+    trace_.record(OpKind::Rotate, level, keys.size());
+  }
+  // accumulate: acc = sum of live groups (rotated where j >= 1)
+  auto acc = dev(ctw);
+  std::size_t ri = 0;
+  bool first = true;
+  for (int j : live) {
+    const u64* term = (j == 0 || rot_j.empty() || ri >= rot_j.size() || rot_j[ri] != j)
+                          ? inner->ptr + j * ctw
+                          : rotated->ptr + (ri++) * ctw;
+    if (first) {
+      cuda_ck(cudaMemcpyAsync(acc->ptr, term, ctw * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
+      first = false;
+    } else {
+      ck(hx_add(ctx_, acc->ptr, acc->ptr, term, 2, nqv, 0, nullptr), "add");
+    }
+  }
+  if (live.size() > 1) trace_.record(OpKind::CtAdd, level, live.size() - 1);
+  return wrap(acc, 0, level, out_scale);
+}
+
+}  // namespace helix

@@ -1,0 +1,203 @@
+// helix_c.cpp -- C-ABI over GpuLatticeBackend + linalg (include/helix_c.h).
+#include "helix_c.h"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "helix/gpu_backend.hpp"
+#include "helix/linalg.hpp"
+
+using namespace helix;
+
+struct hxc_backend {
+  std::unique_ptr<GpuLatticeBackend> b;
+};
+struct hxc_ct {
+  Ciphertext c;
+};
+struct hxc_mat {
+  EncodedMatrix m;
+  int method;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class T, class F>
+T guard(T fail, F f) {
+  try {
+    return f();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return fail;
+  }
+}
+
+hxc_ct* wrap(Ciphertext c) { return new hxc_ct{std::move(c)}; }
+
+void fill(hxc_report* r, const KernelReport& k) {
+  if (!r) return;
+  r->rotations = k.rotations;
+  r->pt_muls = k.pt_muls;
+  r->ct_muls = k.ct_muls;
+  r->adds = k.adds;
+  r->levels_consumed = k.levels_consumed;
+  r->output_scale_log2 = k.output_scale.log2();
+}
+}  // namespace
+
+extern "C" {
+
+const char* hxc_last_error(void) { return g_err.c_str(); }
+
+hxc_backend* hxc_backend_create(const char* json, uint64_t seed) {
+  return guard<hxc_backend*>(nullptr, [&] {
+    auto p = CkksParams::from_json(json);
+    auto* h = new hxc_backend;
+    h->b = std::make_unique<GpuLatticeBackend>(p, seed);
+    return h;
+  });
+}
+
+void hxc_backend_destroy(hxc_backend* b) { delete b; }
+int64_t hxc_slots(hxc_backend* b) { return (int64_t)b->b->slots(); }
+int hxc_max_level(hxc_backend* b) { return b->b->params().max_level; }
+void* hxc_device_context(hxc_backend* b) { return b->b->device_context(); }
+
+int hxc_gen_rotation_keys(hxc_backend* b, const int64_t* a, int n) {
+  return guard(-1, [&] {
+    b->b->generate_rotation_keys(std::span<const std::int64_t>(a, n));
+    return 0;
+  });
+}
+
+hxc_ct* hxc_encrypt(hxc_backend* b, const double* m, int len, int level) {
+  return guard<hxc_ct*>(nullptr, [&] {
+    auto& be = *b->b;
+    return wrap(be.encrypt(be.encode(std::span<const double>(m, len), level, be.params().delta())));
+  });
+}
+
+int hxc_decrypt(hxc_backend* b, const hxc_ct* ct, double* out) {
+  return guard(-1, [&] {
+    const auto v = b->b->decrypt(ct->c);
+    std::memcpy(out, v.data(), v.size() * sizeof(double));
+    return 0;
+  });
+}
+
+void hxc_ct_free(hxc_ct* ct) { delete ct; }
+int hxc_ct_level(const hxc_ct* ct) { return ct->c.level; }
+double hxc_ct_scale_log2(const hxc_ct* ct) { return ct->c.scale.log2(); }
+uint64_t* hxc_ct_device_ptr(const hxc_ct* ct) { return GpuLatticeBackend::payload(ct->c).data(); }
+
+hxc_ct* hxc_add(hxc_backend* b, const hxc_ct* x, const hxc_ct* y) {
+  return guard<hxc_ct*>(nullptr, [&] { return wrap(b->b->add(x->c, y->c)); });
+}
+hxc_ct* hxc_mul(hxc_backend* b, const hxc_ct* x, const hxc_ct* y) {
+  return guard<hxc_ct*>(nullptr, [&] { return wrap(b->b->mul(x->c, y->c)); });
+}
+hxc_ct* hxc_mul_plain(hxc_backend* b, const hxc_ct* x, const double* m, int len) {
+  return guard<hxc_ct*>(nullptr, [&] {
+    auto& be = *b->b;
+    const auto pt = be.encode(std::span<const double>(m, len), x->c.level, Scale::prime(be.modulus_at(x->c.level)));
+    return wrap(be.mul_plain(x->c, pt));
+  });
+}
+hxc_ct* hxc_rotate(hxc_backend* b, const hxc_ct* x, int64_t k) {
+  return guard<hxc_ct*>(nullptr, [&] { return wrap(b->b->rotate(x->c, k)); });
+}
+hxc_ct* hxc_rescale(hxc_backend* b, const hxc_ct* x) {
+  return guard<hxc_ct*>(nullptr, [&] { return wrap(b->b->rescale(x->c)); });
+}
+hxc_ct* hxc_mod_down(hxc_backend* b, const hxc_ct* x, int level) {
+  return guard<hxc_ct*>(nullptr, [&] { return wrap(b->b->mod_down(x->c, level)); });
+}
+hxc_ct* hxc_rotate_and_sum(hxc_backend* b, const hxc_ct* x, int64_t span, int64_t stride, hxc_report* rep) {
+  return guard<hxc_ct*>(nullptr, [&] {
+    KernelReport k;
+    auto c = rotate_and_sum(*b->b, x->c, (std::size_t)span, (std::size_t)stride, &k);
+    fill(rep, k);
+    return wrap(c);
+  });
+}
+
+hxc_mat* hxc_matrix_prepare(hxc_backend* b, int method, const double* A, int rows, int cols, int level) {
+  return guard<hxc_mat*>(nullptr, [&] {
+    Matrix M(rows, cols);
+    std::memcpy(M.data.data(), A, sizeof(double) * (std::size_t)rows * cols);
+    const std::size_t n = b->b->slots();
+    PackedMatrix P = method == HXC_ROW ? pack_rows(M, n) : method == HXC_DIAG ? pack_diagonals(M, n) : pack_bsgs(M, n);
+    auto* h = new hxc_mat;
+    h->method = method;
+    h->m = encode_matrix(*b->b, P, level);
+    return h;
+  });
+}
+
+void hxc_matrix_free(hxc_mat* m) { delete m; }
+
+int hxc_matrix_info(const hxc_mat* m, int* d, int* n1, int* n2, int* blocks, int* nonzero) {
+  if (d) *d = m->m.meta.d;
+  if (n1) *n1 = m->m.meta.plan.n1;
+  if (n2) *n2 = m->m.meta.plan.n2;
+  if (blocks) *blocks = m->m.meta.row_blocks;
+  if (nonzero) {
+    int c = 0;
+    for (const auto& p : m->m.pts) c += p.payload != nullptr;
+    *nonzero = c;
+  }
+  return 0;
+}
+
+int hxc_matrix_rotations(const hxc_mat* m, int64_t* out, int cap) {
+  std::vector<std::int64_t> r = m->method == HXC_ROW    ? row_rotations(m->m.meta)
+                                : m->method == HXC_DIAG ? diag_rotations(m->m.meta.d)
+                                                        : bsgs_rotations(m->m.meta.plan);
+  for (int i = 0; i < (int)r.size() && i < cap; ++i) out[i] = r[i];
+  return (int)r.size();
+}
+
+int hxc_matvec(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, int cap, hxc_report* rep) {
+  return guard(-1, [&] {
+    MatvecResult r = m->method == HXC_ROW    ? matvec_row(*b->b, m->m, x->c)
+                     : m->method == HXC_DIAG ? matvec_diag(*b->b, m->m, x->c)
+                                             : matvec_bsgs(*b->b, m->m, x->c);
+    fill(rep, r.report);
+    int k = 0;
+    for (; k < (int)r.outputs.size() && k < cap; ++k) out[k] = wrap(r.outputs[k]);
+    return (int)r.outputs.size();
+  });
+}
+
+hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_report* rep) {
+  return guard<hxc_ct*>(nullptr, [&] {
+    auto r = matmul_ctct(*b->b, A->c, B->c, d);
+    fill(rep, r.second);
+    return wrap(r.first);
+  });
+}
+
+int hxc_matmul_rotations(int d, int64_t* out, int cap) {
+  const auto r = matmul_rotations(d, 0);
+  for (int i = 0; i < (int)r.size() && i < cap; ++i) out[i] = r[i];
+  return (int)r.size();
+}
+
+int hxc_trace_json(hxc_backend* b, char* buf, int cap) {
+  const auto s = b->b->trace().to_json();
+  if (buf && cap > 0) {
+    std::strncpy(buf, s.c_str(), cap - 1);
+    buf[cap - 1] = 0;
+  }
+  return (int)s.size();
+}
+
+void hxc_trace_reset(hxc_backend* b) { b->b->trace().reset(); }
+
+int hxc_sync(void) { return cudaDeviceSynchronize() == cudaSuccess ? 0 : -1; }
+
+}  // extern "C"

@@ -1,0 +1,309 @@
+// linalg.cpp -- encrypted linear algebra over SlotOps.
+#include "helix/linalg.hpp"
+
+#include <map>
+#include <optional>
+#include <sstream>
+
+#ifndef HELIX_NO_GPU
+#include "helix/gpu_backend.hpp"
+#endif
+
+namespace helix {
+
+namespace {
+
+int ilog2(std::size_t v) {
+  int l = 0;
+  while ((std::size_t(1) << l) < v) ++l;
+  return l;
+}
+
+KernelReport report_since(OpTrace& t, const TraceSnapshot& s, int in_level, const Ciphertext& out) {
+  KernelReport r;
+  r.rotations = s.delta(t, OpKind::Rotate);
+  r.pt_muls = s.delta(t, OpKind::PtMul);
+  r.ct_muls = s.delta(t, OpKind::CtMul);
+  r.adds = s.delta(t, OpKind::CtAdd) + s.delta(t, OpKind::PtAdd);
+  r.levels_consumed = in_level - out.level;
+  r.output_scale = out.scale;
+  return r;
+}
+
+Ciphertext add_opt(SlotOps& ops, std::optional<Ciphertext>& acc, const Ciphertext& t) {
+  acc = acc ? ops.add(*acc, t) : t;
+  return *acc;
+}
+
+void require_matvec_input(const EncodedMatrix& M, const Ciphertext& x, Layout want) {
+  if (M.meta.layout != want) throw std::invalid_argument("matvec: wrong matrix layout");
+  detail::require_same_level(x.level, M.level, "matvec");
+  if (x.level < 1) throw LevelUnderflowError("matvec: level budget < 1");
+}
+
+}  // namespace
+
+std::string KernelReport::to_json() const {
+  std::ostringstream o;
+  o << "{\"rotations\": " << rotations << ", \"pt_muls\": " << pt_muls << ", \"ct_muls\": " << ct_muls
+    << ", \"adds\": " << adds << ", \"levels_consumed\": " << levels_consumed << ", \"output_scale_log2\": "
+    << output_scale.log2() << "}";
+  return o.str();
+}
+
+EncodedMatrix encode_matrix(SlotOps& ops, const PackedMatrix& M, int level) {
+  EncodedMatrix E;
+  E.meta = M;
+  E.meta.payloads.clear();
+  E.level = level;
+  if (M.layout == Layout::RowMajor) throw std::invalid_argument("encode_matrix: RowMajor operands are ciphertexts");
+  const Scale s = Scale::prime(ops.modulus_at(level));
+#ifndef HELIX_NO_GPU
+  if (auto* g = dynamic_cast<GpuLatticeBackend*>(&ops)) {
+    E.pts = g->encode_many(M.payloads, level, s);
+    return E;
+  }
+#endif
+  {
+    for (const auto& p : M.payloads) {
+      if (p.empty()) {
+        Plaintext z;
+        z.level = level;
+        z.scale = s;
+        z.slot_count = ops.slots();
+        E.pts.push_back(z);
+      } else {
+        E.pts.push_back(ops.encode(p, level, s));
+      }
+    }
+  }
+  return E;
+}
+
+Ciphertext rotate_and_sum(SlotOps& ops, const Ciphertext& ct, std::size_t span, std::size_t stride,
+                          KernelReport* report) {
+  if (span == 0 || (span & (span - 1))) throw std::invalid_argument("rotate_and_sum: span must be a power of two");
+  const auto snap = TraceSnapshot::take(ops.trace());
+  Ciphertext acc = ct;
+  for (std::size_t s = 1; s < span; s <<= 1) acc = ops.add(acc, ops.rotate(acc, (std::int64_t)(stride * s)));
+  if (report) *report = report_since(ops.trace(), snap, ct.level, acc);
+  return acc;
+}
+
+// ------------------------------------------------------------------- BSGS
+MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x) {
+  require_matvec_input(M, x, Layout::BsgsDiagonal);
+  const auto snap = TraceSnapshot::take(ops.trace());
+  const int d = M.meta.d, n1 = M.meta.plan.n1, n2 = M.meta.plan.n2;
+  MatvecResult R;
+#ifndef HELIX_NO_GPU
+  auto* gpu = dynamic_cast<GpuLatticeBackend*>(&ops);
+#else
+  SlotOps* gpu = nullptr;
+#endif
+  // baby steps Rot(x, k), k < n1, shared by every row block
+  std::vector<Ciphertext> baby;
+#ifndef HELIX_NO_GPU
+  if (gpu) {
+    std::vector<std::int64_t> ks(n1);
+    for (int k = 0; k < n1; ++k) ks[k] = k;
+    baby = gpu->rotate_many(x, ks);  // one ModUp for all n1 - 1 rotations
+  } else
+#endif
+  {
+    baby.push_back(x);
+    for (int k = 1; k < n1; ++k) baby.push_back(ops.rotate(x, k));
+  }
+  for (int b = 0; b < M.meta.row_blocks; ++b) {
+    const std::vector<Plaintext> diags(M.pts.begin() + (std::ptrdiff_t)b * d,
+                                       M.pts.begin() + (std::ptrdiff_t)(b + 1) * d);
+    Ciphertext acc;
+#ifndef HELIX_NO_GPU
+    if (gpu) {
+      acc = gpu->bsgs_block(baby, diags, n1, n2);
+    } else
+#endif
+    {
+      std::optional<Ciphertext> sum;
+      for (int j = 0; j < n2; ++j) {
+        std::optional<Ciphertext> inner;
+        for (int k = 0; k < n1; ++k) {
+          const Plaintext& pt = diags[(std::size_t)j * n1 + k];
+          if (!pt.payload) continue;
+          add_opt(ops, inner, ops.mul_plain(baby[k], pt));
+        }
+        if (!inner) continue;
+        add_opt(ops, sum, j ? ops.rotate(*inner, (std::int64_t)n1 * j) : *inner);
+      }
+      if (!sum) throw std::invalid_argument("matvec_bsgs: block has no non-zero diagonal");
+      acc = *sum;
+    }
+    R.outputs.push_back(ops.rescale(acc));
+  }
+  R.report = report_since(ops.trace(), snap, x.level, R.outputs.front());
+  return R;
+}
+
+// ------------------------------------------------------------------- diagonal
+MatvecResult matvec_diag(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x) {
+  require_matvec_input(M, x, Layout::Diagonal);
+  const auto snap = TraceSnapshot::take(ops.trace());
+  const int d = M.meta.d;
+  std::vector<bool> need(d, false);
+  for (int b = 0; b < M.meta.row_blocks; ++b)
+    for (int i = 0; i < d; ++i) need[i] = need[i] || M.pts[(std::size_t)b * d + i].payload != nullptr;
+  std::map<int, Ciphertext> rot;
+#ifndef HELIX_NO_GPU
+  if (auto* gpu = dynamic_cast<GpuLatticeBackend*>(&ops)) {
+    std::vector<std::int64_t> ks;
+    for (int i = 0; i < d; ++i)
+      if (need[i]) ks.push_back(i);
+    const auto r = gpu->rotate_many(x, ks);
+    for (std::size_t j = 0; j < ks.size(); ++j) rot.emplace((int)ks[j], r[j]);
+  } else
+#endif
+  {
+    for (int i = 0; i < d; ++i)
+      if (need[i]) rot.emplace(i, i ? ops.rotate(x, i) : x);
+  }
+  MatvecResult R;
+  for (int b = 0; b < M.meta.row_blocks; ++b) {
+    std::optional<Ciphertext> acc;
+    for (int i = 0; i < d; ++i) {
+      const Plaintext& pt = M.pts[(std::size_t)b * d + i];
+      if (pt.payload) add_opt(ops, acc, ops.mul_plain(rot.at(i), pt));
+    }
+    if (!acc) throw std::invalid_argument("matvec_diag: block has no non-zero diagonal");
+    R.outputs.push_back(ops.rescale(*acc));
+  }
+  R.report = report_since(ops.trace(), snap, x.level, R.outputs.front());
+  return R;
+}
+
+// ------------------------------------------------------------------- packed rows
+// Per payload g: t = rescale(x (.) rows_g); rotate_and_sum(t, pad_cols, 1)
+// leaves row r's dot product in slots [r pc, (r+1) pc).  Assembly
+// (SPEC.md:422): mask slot r pc (second level), rotate left by
+// r pc - (g p + r) so it lands in slot g p + r, sum, rescale.
+MatvecResult matvec_row(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x) {
+  if (M.meta.layout != Layout::PackedRow) throw std::invalid_argument("matvec_row: wrong layout");
+  detail::require_same_level(x.level, M.level, "matvec_row");
+  if (x.level < 2) throw LevelUnderflowError("matvec_row: level budget < 2");
+  const auto snap = TraceSnapshot::take(ops.trace());
+  const int pc = M.meta.pad_cols, p = M.meta.rows_per_payload, R = M.meta.rows;
+  const std::size_t n = ops.slots();
+  const int lvl1 = x.level - 1;
+  const Scale mscale = Scale::prime(ops.modulus_at(lvl1));
+  std::map<int, Plaintext> masks;
+  std::optional<Ciphertext> acc;
+  for (std::size_t g = 0; g < M.pts.size(); ++g) {
+    Ciphertext t = ops.rescale(ops.mul_plain(x, M.pts[g]));
+    t = rotate_and_sum(ops, t, (std::size_t)pc, 1);
+    for (int r = 0; r < p; ++r) {
+      const int row = (int)g * p + r;
+      if (row >= R) break;
+      auto it = masks.find(r);
+      if (it == masks.end()) {
+        std::vector<double> m(n, 0.0);
+        m[(std::size_t)r * pc] = 1.0;
+        it = masks.emplace(r, ops.encode(m, lvl1, mscale)).first;
+      }
+      Ciphertext u = ops.mul_plain(t, it->second);
+      const std::int64_t shift = (std::int64_t)r * pc - row;
+      if (detail::reduce_amount(shift, (std::int64_t)n) != 0) u = ops.rotate(u, shift);
+      add_opt(ops, acc, u);
+    }
+  }
+  MatvecResult Rz;
+  Rz.outputs.push_back(ops.rescale(*acc));
+  Rz.report = report_since(ops.trace(), snap, x.level, Rz.outputs.front());
+  return Rz;
+}
+
+// ------------------------------------------------------------------- SPEC forms
+static std::pair<Ciphertext, KernelReport> single(MatvecResult r) {
+  if (r.outputs.size() != 1) throw std::invalid_argument("matvec: matrix has several row blocks; use the EncodedMatrix form");
+  return {r.outputs.front(), r.report};
+}
+
+std::pair<Ciphertext, KernelReport> matvec_bsgs(SlotOps& ops, const PackedMatrix& M, const Ciphertext& x,
+                                                const BsgsPlan& plan) {
+  if (plan.n1 != M.plan.n1 || plan.n2 != M.plan.n2) throw std::invalid_argument("matvec_bsgs: plan mismatch");
+  return single(matvec_bsgs(ops, encode_matrix(ops, M, x.level), x));
+}
+std::pair<Ciphertext, KernelReport> matvec_diag(SlotOps& ops, const PackedMatrix& M, const Ciphertext& x) {
+  return single(matvec_diag(ops, encode_matrix(ops, M, x.level), x));
+}
+std::pair<Ciphertext, KernelReport> matvec_row(SlotOps& ops, const PackedMatrix& M, const Ciphertext& x) {
+  return single(matvec_row(ops, encode_matrix(ops, M, x.level), x));
+}
+
+// ------------------------------------------------------------------- matmul
+std::pair<Ciphertext, KernelReport> matmul_ctct(SlotOps& ops, const Ciphertext& A, const Ciphertext& B,
+                                                int d) {
+  if (d < 1 || (d & (d - 1))) throw std::invalid_argument("matmul_ctct: d must be a power of two");
+  const std::size_t n = ops.slots();
+  if ((std::size_t)d * d > n) throw std::invalid_argument("matmul_ctct: d^2 > n");
+  detail::require_same_level(A.level, B.level, "matmul_ctct");
+  if (A.level < 2) throw LevelUnderflowError("matmul_ctct: requires a multiplicative level of 2");
+  const auto snap = TraceSnapshot::take(ops.trace());
+  const int lv = A.level, lg = ilog2((std::size_t)d);
+  // A's column mask at scale q_l (A_col keeps Delta); B's row mask at scale
+  // q_l q_{l-1} / Delta so that the ct-ct product has scale Delta q_{l-1} and
+  // the final rescale by q_{l-1} restores exactly Delta (SPEC.md:417 invariant)
+  const Scale ms = Scale::prime(ops.modulus_at(lv));
+  const Scale ms_b = ms * Scale::prime(ops.modulus_at(lv - 1)) / ops.params().delta();
+  std::optional<Ciphertext> C;
+  for (int j = 0; j < d; ++j) {
+    const Plaintext cm = ops.encode(make_mask(MaskKind::ColumnExtractor, j, d, n), lv, ms);
+    const Plaintext rm = ops.encode(make_mask(MaskKind::RowExtractor, j, d, n), lv, ms_b);
+    Ciphertext a = ops.rescale(ops.mul_plain(A, cm));
+    Ciphertext b = ops.rescale(ops.mul_plain(B, rm));
+    if (j) {
+      a = ops.rotate(a, j);                      // column j -> column 0
+      b = ops.rotate(b, (std::int64_t)d * j);    // row j -> row 0
+    }
+    for (int i = 0; i < lg; ++i) a = ops.add(a, ops.rotate(a, -(std::int64_t(1) << i)));
+    for (int i = 0; i < lg; ++i) b = ops.add(b, ops.rotate(b, -((std::int64_t)d << i)));
+    add_opt(ops, C, ops.mul(a, b));
+  }
+  const Ciphertext out = ops.rescale(*C);
+  return {out, report_since(ops.trace(), snap, A.level, out)};
+}
+
+// ------------------------------------------------------------------- keys
+std::vector<std::int64_t> bsgs_rotations(const BsgsPlan& plan) {
+  std::vector<std::int64_t> r;
+  for (int k = 1; k < plan.n1; ++k) r.push_back(k);
+  for (int j = 1; j < plan.n2; ++j) r.push_back((std::int64_t)plan.n1 * j);
+  return r;
+}
+std::vector<std::int64_t> diag_rotations(int d) {
+  std::vector<std::int64_t> r;
+  for (int i = 1; i < d; ++i) r.push_back(i);
+  return r;
+}
+std::vector<std::int64_t> row_rotations(const PackedMatrix& M) {
+  std::vector<std::int64_t> r;
+  for (int s = 1; s < M.pad_cols; s <<= 1) r.push_back(s);
+  const int p = M.rows_per_payload;
+  for (int row = 0; row < M.rows; ++row) {
+    const std::int64_t shift = (std::int64_t)(row % p) * M.pad_cols - row;
+    if (shift) r.push_back(shift);
+  }
+  return r;
+}
+std::vector<std::int64_t> matmul_rotations(int d, std::size_t) {
+  std::vector<std::int64_t> r;
+  for (int s = 1; s < d; s <<= 1) {
+    r.push_back(-s);
+    r.push_back(-(std::int64_t)d * s);
+  }
+  for (int j = 1; j < d; ++j) {
+    r.push_back(j);
+    r.push_back((std::int64_t)d * j);
+  }
+  return r;
+}
+
+}  // namespace helix

@@ -69,6 +69,8 @@ def lib() -> C.CDLL:
         "hx_bsgs_mac": [v, v, v, v, i32, i32, i32, i32, v],
         "hx_keygen_ksk": [v, v, v, v, v, v, v],
         "hx_encrypt_sk": [v, v, v, v, v, v, i32, v],
+        "hx_ksk_to_rotation_layout": [v, v, v, u64, v],
+        "hx_keygen_rotation": [v, v, v, u64, v, v, v],
         "hx_decrypt": [v, v, v, v, i32, i32, v],
         "hx_rotate_host": [v, v, v, v, i32, i32, u64, v],
         "hx_mul_relin_host": [v, v, v, v, v, i32, i32, v],
@@ -217,6 +219,22 @@ class Context:
     def keygen_ksk(self, key, s_full, sp_full, a_full, e, stream=None):
         _check(self.L.hx_keygen_ksk(self.h, _p(key), _p(s_full), _p(sp_full), _p(a_full), _p(e),
                                     _stream(stream)), "hx_keygen_ksk")
+
+    def ksk_to_rotation_layout(self, out, key, g, stream=None):
+        _check(self.L.hx_ksk_to_rotation_layout(self.h, _p(out), _p(key), g, _stream(stream)),
+               "hx_ksk_to_rotation_layout")
+
+    def rotation_key(self, key, g, stream=None):
+        """new tensor: a standard-layout key converted to rotation layout"""
+        import torch
+
+        out = torch.empty_like(key)
+        self.ksk_to_rotation_layout(out, key, g, stream)
+        return out
+
+    def keygen_rotation(self, key, s_full, g, a_full, e, stream=None):
+        _check(self.L.hx_keygen_rotation(self.h, _p(key), _p(s_full), g, _p(a_full), _p(e), _stream(stream)),
+               "hx_keygen_rotation")
 
     def encrypt_sk(self, ct, m, s_full, a, e, n_q, stream=None):
         _check(self.L.hx_encrypt_sk(self.h, _p(ct), _p(m), _p(s_full), _p(a), _p(e), n_q, _stream(stream)),

@@ -226,7 +226,7 @@ def test_rotate_parity_and_decrypt(cfg):
         cts.append(orc.encrypt_sk(m_ntt, s_full, uniform_limbs(rng, p["chain"], orc.n), gaussian(rng, orc.n), nq))
     ct = np.stack(cts)
     out = empty(batch, 2, nq, orc.n)
-    ctx.rotate(out, dev(ct), dev(key), batch, nq, g)
+    ctx.rotate(out, dev(ct), ctx.rotation_key(dev(key), g), batch, nq, g)
     got = host(out)
     for b in range(batch):
         exp = orc.rotate(ct[b], key, nq, g)
@@ -255,7 +255,7 @@ def test_keyswitch_and_hoisted_parity(cfg):
     ctx.keyswitch(out, dev(ct[1]), dev(keys[0]), 1, nq)
     assert np.array_equal(host(out), orc.keyswitch(ct[1], keys[0], nq))
     # hoisted batch
-    dkeys = [dev(k) for k in keys]
+    dkeys = [ctx.rotation_key(dev(k), g) for k, g in zip(keys, gs)]
     outh = empty(1, len(gs), 2, nq, orc.n)
     ctx.rotate_hoisted(outh, dev(ct), dkeys, gs, 1, nq)
     exp = orc.rotate_hoisted(ct, keys, gs, nq)
@@ -328,6 +328,29 @@ def test_keygen_encrypt_decrypt_parity(cfg):
     assert np.array_equal(host(mo)[0], orc.decrypt(exp, s_full, nq))
 
 
+@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+def test_keygen_rotation_layout(cfg):
+    """hx_keygen_rotation == hx_ksk_to_rotation_layout(standard keygen of tau_g(s))."""
+    import torch
+
+    p, ctx, orc = env(cfg)
+    rng = np.random.default_rng(13)
+    nq, K = len(p["chain"]), len(p["special"])
+    s_full = secret(p, orc, rng)
+    g = galois_elt(11, orc.n)
+    dn = orc.dnum(nq)
+    a = uniform_limbs(rng, p["chain"] + p["special"], orc.n, (dn,))
+    e = np.stack([gaussian(rng, orc.n) for _ in range(dn)])
+    std = orc.keygen_ksk(s_full, orc.automorphism_ntt(s_full, nq, K, g), a, e)
+    key = empty(ctx.key_words())
+    ctx.keygen_rotation(key, dev(s_full), g, dev(a), torch.from_numpy(e).cuda())
+    assert np.array_equal(host(key), host(ctx.rotation_key(dev(std), g)).reshape(-1))
+    # and the rotation layout is tau_{g^-1} of the standard layout, limb-wise
+    ginv = pow(g, -1, 2 * orc.n)
+    exp = orc.automorphism_ntt(std.reshape(dn * 2 * (nq + K), orc.n), dn * 2 * (nq + K), 0, ginv)
+    assert np.array_equal(host(key).reshape(-1, orc.n), exp)
+
+
 def test_host_entry_points():
     """hx_rotate_host / hx_mul_relin_host (host buffers in, host buffers out)."""
     import torch
@@ -340,7 +363,7 @@ def test_host_entry_points():
     key, _, _ = keyset(p, orc, rng, s_full, orc.automorphism_ntt(s_full, nq, K, g))
     ct = uniform_limbs(rng, p["chain"], orc.n, (2, 2))
     out = np.zeros_like(ct)
-    ctx.rotate_host(out.ctypes.data, ct.ctypes.data, dev(key), 2, nq, g)
+    ctx.rotate_host(out.ctypes.data, ct.ctypes.data, ctx.rotation_key(dev(key), g), 2, nq, g)
     for b in range(2):
         assert np.array_equal(out[b], orc.rotate(ct[b], key, nq, g))
     s2 = orc.binop("hxo_mul", s_full, s_full, nq, K)
