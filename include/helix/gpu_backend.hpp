@@ -106,9 +106,12 @@ class GpuLatticeBackend final : public SlotBackend {
                   const Scale& scale) const;
   // device word pointer of the rotation-layout key for amount k (mod n), or null
   const std::uint64_t* rotation_key(std::int64_t amount_mod_n) const;
+  // secret key s over the full basis (NTT) and the relinearisation key --
+  // exported for the parity tests (the oracle recomputes with the same words)
+  const std::uint64_t* secret_key_words() const { return s_full_->ptr; }
+  const std::uint64_t* relin_key_words() const { return rlk_->ptr; }
 
  private:
-  std::shared_ptr<DeviceBuffer> secret_poly_full() const { return s_full_; }
   std::uint64_t galois(std::int64_t amount_mod_n) const;
   std::uint64_t next_u64();
   void sample_uniform(std::vector<std::uint64_t>& out, int limbs_chain, int limbs_special, int copies);

@@ -83,6 +83,19 @@ int hxc_matvec(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, 
 hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_report* rep);
 int hxc_matmul_rotations(int d, int64_t* out, int cap);
 
+/* ---- raw device words, for the bit-exact parity tests ----
+ * secret key [n_chain+K][N] (NTT), relinearisation key (standard layout),
+ * rotation key for amount k (rotation layout, NULL if absent), payload i of an
+ * encoded matrix [level+1][N] (NULL for an all-zero payload) */
+const uint64_t* hxc_secret_key_ptr(hxc_backend* b);
+const uint64_t* hxc_relin_key_ptr(hxc_backend* b);
+const uint64_t* hxc_rotation_key_ptr(hxc_backend* b, int64_t k);
+const uint64_t* hxc_matrix_payload_ptr(const hxc_mat* m, int i);
+int hxc_matrix_payload_count(const hxc_mat* m);
+/* host-only: CkksEncoder::encode_coeffs for a CkksParams JSON (no device) */
+int hxc_encode_coeffs(const char* params_json, const double* m, int len, int level, double scale,
+                      int64_t* out);
+
 /* OpTrace JSON (canonical names ct_add ... bootstrap); returns length */
 int hxc_trace_json(hxc_backend* b, char* buf, int cap);
 void hxc_trace_reset(hxc_backend* b);

@@ -187,6 +187,26 @@ int hxc_matmul_rotations(int d, int64_t* out, int cap) {
   return (int)r.size();
 }
 
+const uint64_t* hxc_secret_key_ptr(hxc_backend* b) { return b->b->secret_key_words(); }
+const uint64_t* hxc_relin_key_ptr(hxc_backend* b) { return b->b->relin_key_words(); }
+const uint64_t* hxc_rotation_key_ptr(hxc_backend* b, int64_t k) {
+  return b->b->rotation_key(detail::reduce_amount(k, (std::int64_t)b->b->slots()));
+}
+const uint64_t* hxc_matrix_payload_ptr(const hxc_mat* m, int i) {
+  if (i < 0 || i >= (int)m->m.pts.size() || !m->m.pts[i].payload) return nullptr;
+  return GpuLatticeBackend::payload(m->m.pts[i]).data();
+}
+int hxc_matrix_payload_count(const hxc_mat* m) { return (int)m->m.pts.size(); }
+
+int hxc_encode_coeffs(const char* json, const double* m, int len, int level, double scale, int64_t* out) {
+  return guard(-1, [&] {
+    const CkksEncoder enc(CkksParams::from_json(json));
+    const auto c = enc.encode_coeffs(std::span<const double>(m, len), level, scale);
+    std::memcpy(out, c.data(), c.size() * 8);
+    return 0;
+  });
+}
+
 int hxc_trace_json(hxc_backend* b, char* buf, int cap) {
   const auto s = b->b->trace().to_json();
   if (buf && cap > 0) {

@@ -266,6 +266,30 @@ def test_keyswitch_and_hoisted_parity(cfg):
 
 
 @pytest.mark.parametrize("cfg", ["c1", "c2s"])
+def test_rotate_multi_parity(cfg):
+    """hx_rotate_multi: per-element keys / galois elements, one batched ModUp"""
+    import ctypes as C
+
+    p, ctx, orc = env(cfg)
+    rng = np.random.default_rng(14)
+    nq, K = len(p["chain"]), len(p["special"])
+    s_full = secret(p, orc, rng)
+    ks = [3, 8, 40]
+    gs = [galois_elt(k, orc.n) for k in ks]
+    keys = [keyset(p, orc, rng, s_full, orc.automorphism_ntt(s_full, nq, K, g))[0] for g in gs]
+    dkeys = [ctx.rotation_key(dev(k), g) for k, g in zip(keys, gs)]
+    cts = uniform_limbs(rng, p["chain"], orc.n, (3, 2))
+    out = empty(3, 2, nq, orc.n)
+    kp = (C.c_void_p * 3)(*[k.data_ptr() for k in dkeys])
+    ga = (C.c_uint64 * 3)(*gs)
+    ctx.L.hx_rotate_multi.argtypes = [C.c_void_p] * 4 + [C.POINTER(C.c_uint64), C.c_int, C.c_int, C.c_void_p]
+    assert ctx.L.hx_rotate_multi(ctx.h, out.data_ptr(), dev(cts).data_ptr(), kp, ga, 3, nq, None) == 0
+    got = host(out)
+    for b in range(3):
+        assert np.array_equal(got[b], orc.rotate(cts[b], keys[b], nq, gs[b])), b
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2s"])
 def test_tensor_and_mul_relin_parity(cfg):
     p, ctx, orc = env(cfg)
     rng = np.random.default_rng(9)
