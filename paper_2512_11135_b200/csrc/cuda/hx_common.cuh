@@ -31,6 +31,13 @@ struct PrimeConst {
   u64 w1np;
   const ulonglong2* tw_fwd;  // (psi^brv(i), shoup) i in [0, N)
   const ulonglong2* tw_inv;  // (psi^-brv(i), shoup)
+  // FP64 butterfly path (q < 2^47 only; null otherwise)
+  bool f64;
+  double qd, qinv_d;         // q, 1/q
+  double ninv_d, ninv_q;     // N^-1, N^-1 / q
+  double w1n_d, w1n_q;       // last-stage twiddle * N^-1, / q
+  const double* twf_fwd;     // w as double (w / q formed in-kernel)
+  const double* twf_inv;
 };
 
 // ---------------------------------------------------------------- arithmetic

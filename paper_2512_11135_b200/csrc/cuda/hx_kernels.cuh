@@ -203,20 +203,36 @@ __global__ void ks_inner_kernel(InnerArgs A) {
     }
   }
   const int src = (A.g == 1) ? t : (int)ntt_auto_index((u32)t, A.g, A.logn);
-  for (int b = 0; b < A.batch; ++b) {
-    const u64* Db = A.digits + (long long)b * A.dnum * ext * N + (long long)j * N + src;
-    U128 z0{0, 0}, z1{0, 0};
+  // this CTA's slice of the batch (blockIdx.z); BB ciphertexts per iteration
+  // so 8 x BB independent digit loads are in flight per thread
+  constexpr int BB = MAXD <= 8 ? 4 : 1;
+  const int per = (A.batch + gridDim.z - 1) / gridDim.z;
+  const int b_lo = blockIdx.z * per, b_hi = min(A.batch, b_lo + per);
+  const long long dstride = (long long)A.dnum * ext * N;
+  for (int b0 = b_lo; b0 < b_hi; b0 += BB) {
+    u64 v[BB][MAXD];
 #pragma unroll
-    for (int d = 0; d < MAXD; ++d) {
-      if (d < A.dnum) {
-        const u64 v = __ldg(Db + (long long)d * ext * N);
-        mac128(z0, v, k0[d]);
-        mac128(z1, v, k1[d]);
-      }
+    for (int bb = 0; bb < BB; ++bb) {
+      const u64* Db = A.digits + (long long)(b0 + bb) * dstride + (long long)j * N + src;
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d)
+        v[bb][d] = (d < A.dnum && b0 + bb < b_hi) ? __ldcs(Db + (long long)d * ext * N) : 0ull;
     }
-    u64* ub = A.u + (long long)b * 2 * ext * N + (long long)j * N + t;
-    ub[0] = reduce128(z0, P);
-    ub[(long long)ext * N] = reduce128(z1, P);
+#pragma unroll
+    for (int bb = 0; bb < BB; ++bb) {
+      if (b0 + bb >= b_hi) break;
+      U128 z0{0, 0}, z1{0, 0};
+#pragma unroll
+      for (int d = 0; d < MAXD; ++d) {
+        if (d < A.dnum) {
+          mac128(z0, v[bb][d], k0[d]);
+          mac128(z1, v[bb][d], k1[d]);
+        }
+      }
+      u64* ub = A.u + (long long)(b0 + bb) * 2 * ext * N + (long long)j * N + t;
+      ub[0] = reduce128(z0, P);
+      ub[(long long)ext * N] = reduce128(z1, P);
+    }
   }
 }
 

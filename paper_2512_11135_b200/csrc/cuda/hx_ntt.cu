@@ -1,11 +1,19 @@
 // hx_ntt.cu -- NTT pass instantiations and launchers (see hx_ntt.cuh).
+//
+// A launch's limb table is split by prime class: primes q < 2^47 run the
+// FP64-pipe butterflies, wider primes (the 60-bit q_0 and special primes of
+// config 2, the 50-bit special of config 1) the integer Shoup butterflies.
+// Both classes are issued on the same stream in pass order, so every limb
+// sees its COL pass before its ROW pass (forward) and vice versa (inverse).
+#include <cstdlib>
+
 #include "hx_internal.h"
 
 namespace hx {
 
 namespace {
 
-template <bool FWD, bool ROW, int S>
+template <bool FWD, bool ROW, int S, bool F64>
 void launch_pass(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
   constexpr int OB = 4;
   constexpr int TILE = 1 << (S + OB);
@@ -18,19 +26,26 @@ void launch_pass(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cud
   const long long tiles = c->N() / TILE;
   const long long blocks = a.instances * tiles;
   if (blocks <= 0) return;
-  ntt_pass_kernel<FWD, ROW, S, OB><<<(unsigned)blocks, TILE / 16, 0, s>>>(a);
+  constexpr int smem = ntt_smem_bytes<ROW, S, OB, F64>();
+  static bool configured = false;  // opt in to > 48 KB once per instantiation
+  if (!configured) {
+    cudaFuncSetAttribute(ntt_pass_kernel<FWD, ROW, S, OB, F64>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  ntt_pass_kernel<FWD, ROW, S, OB, F64><<<(unsigned)blocks, TILE / 16, smem, s>>>(a);
   ++c->launches;
 }
 
-template <bool FWD, bool ROW>
+template <bool FWD, bool ROW, bool F64>
 void dispatch(hx_ctx* c, int S, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
   switch (S) {
-    case 3: launch_pass<FWD, ROW, 3>(c, data, batch, lt, s); break;
-    case 4: launch_pass<FWD, ROW, 4>(c, data, batch, lt, s); break;
-    case 5: launch_pass<FWD, ROW, 5>(c, data, batch, lt, s); break;
-    case 6: launch_pass<FWD, ROW, 6>(c, data, batch, lt, s); break;
-    case 7: launch_pass<FWD, ROW, 7>(c, data, batch, lt, s); break;
-    case 8: launch_pass<FWD, ROW, 8>(c, data, batch, lt, s); break;
+    case 3: launch_pass<FWD, ROW, 3, F64>(c, data, batch, lt, s); break;
+    case 4: launch_pass<FWD, ROW, 4, F64>(c, data, batch, lt, s); break;
+    case 5: launch_pass<FWD, ROW, 5, F64>(c, data, batch, lt, s); break;
+    case 6: launch_pass<FWD, ROW, 6, F64>(c, data, batch, lt, s); break;
+    case 7: launch_pass<FWD, ROW, 7, F64>(c, data, batch, lt, s); break;
+    case 8: launch_pass<FWD, ROW, 8, F64>(c, data, batch, lt, s); break;
     default: set_error("ntt: unsupported sub-transform size");
   }
 }
@@ -38,18 +53,38 @@ void dispatch(hx_ctx* c, int S, u64* data, long long batch, const LimbTable& lt,
 // N = 2^a (column / high bits) x 2^b (row / low bits), a = ceil(logn/2)
 inline int split_a(int logn) { return (logn + 1) / 2; }
 
+void split(const hx_ctx* c, const LimbTable& lt, LimbTable& ti, LimbTable& tf) {
+  ti = LimbTable{};
+  tf = LimbTable{};
+  ti.stride = tf.stride = lt.stride;
+  for (int e = 0; e < lt.count; ++e) {
+    LimbTable& t = c->f64[lt.prime[e]] ? tf : ti;
+    t.off[t.count] = lt.off[e];
+    t.prime[t.count] = lt.prime[e];
+    ++t.count;
+  }
+}
+
 }  // namespace
 
 void ntt_forward(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
   const int a = split_a(c->logn), b = c->logn - a;
-  dispatch<true, false>(c, a, data, batch, lt, s);  // first a stages (COL)
-  dispatch<true, true>(c, b, data, batch, lt, s);   // last b stages (ROW)
+  LimbTable ti, tf;
+  split(c, lt, ti, tf);
+  if (ti.count) dispatch<true, false, false>(c, a, data, batch, ti, s);  // first a stages (COL)
+  if (tf.count) dispatch<true, false, true>(c, a, data, batch, tf, s);
+  if (ti.count) dispatch<true, true, false>(c, b, data, batch, ti, s);   // last b stages (ROW)
+  if (tf.count) dispatch<true, true, true>(c, b, data, batch, tf, s);
 }
 
 void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
   const int a = split_a(c->logn), b = c->logn - a;
-  dispatch<false, true>(c, b, data, batch, lt, s);   // low-bit stages (ROW)
-  dispatch<false, false>(c, a, data, batch, lt, s);  // high-bit stages (COL), x N^-1
+  LimbTable ti, tf;
+  split(c, lt, ti, tf);
+  if (ti.count) dispatch<false, true, false>(c, b, data, batch, ti, s);   // low-bit stages (ROW)
+  if (tf.count) dispatch<false, true, true>(c, b, data, batch, tf, s);
+  if (ti.count) dispatch<false, false, false>(c, a, data, batch, ti, s);  // high-bit stages (COL), x N^-1
+  if (tf.count) dispatch<false, false, true>(c, a, data, batch, tf, s);
 }
 
 }  // namespace hx

@@ -101,6 +101,111 @@ __device__ __forceinline__ void ntt_group(u64 (&x)[16], const int (&jb)[16 >> W]
   }
 }
 
+// ---------------------------------------------------------------- FP64 path
+// For primes q < 2^47 the butterflies run on the FP64 pipe (B200: DFMA at 64
+// lanes/clk/SM, twice the IMAD.WIDE rate, and a separate pipe from the
+// integer multiplier).  Values are integers held exactly in doubles, lazily in
+// a signed range; the modular product is exact:
+//   h = fl(y w), l = y w - h (one FMA, exact), qf = rint(y (w/q)) (one FMA
+//   against the 1.5*2^52 rounding constant), r = h - qf q (one FMA, exact),
+//   y w mod q == r + l  with |r + l| < q.
+// Forward (CT) values grow by < q per stage (< 17 q after 16 stages); inverse
+// (GS) values are re-centred (|v| <= q/2) at the start of every register
+// group.  The last pass normalises to [0, q) and converts back to u64, so the
+// output is bit-identical to the integer path and to the reference.
+constexpr double kRound = 6755399441055744.0;  // 1.5 * 2^52
+constexpr double kTwo52 = 4503599627370496.0;
+
+__device__ __forceinline__ double mulmod_f64(double y, double w, double wq, double q) {
+  const double h = __dmul_rn(y, w);
+  const double l = __fma_rn(y, w, -h);
+  const double qf = __dsub_rn(__fma_rn(y, wq, kRound), kRound);
+  const double r = __fma_rn(-qf, q, h);
+  return __dadd_rn(r, l);
+}
+
+// centre v into [-q/2 - eps, q/2 + eps]
+__device__ __forceinline__ double centre_f64(double v, double q, double qinv) {
+  const double qf = __dsub_rn(__fma_rn(v, qinv, kRound), kRound);
+  return __fma_rn(-qf, q, v);
+}
+
+__device__ __forceinline__ u64 u64_to_f64bits(u64 x) {  // x < 2^52 -> bits of (double)x
+  return (u64)__double_as_longlong(__dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), kTwo52));
+}
+
+__device__ __forceinline__ u64 f64bits_to_residue(u64 bits, double q, double qinv) {  // -> [0, q)
+  double r = centre_f64(__longlong_as_double((long long)bits), q, qinv);
+  r = r < 0.0 ? __dadd_rn(r, q) : r;
+  return (u64)__double_as_longlong(__dadd_rn(r, kTwo52)) & 0xFFFFFFFFFFFFFull;
+}
+
+// ROW-pass twiddles of a tile staged in shared memory: for pair bit beta < S
+// the tile's twiddle indices are contiguous, (N >> (beta+1)) + row0 2^(S-beta-1)
+// + [0, OTH 2^(S-beta-1)); they are stored back to back, stage beta at offset
+// OTH (2^S - 2^(S-beta)).  This turns the per-butterfly distinct twiddle
+// loads of the last stages into one coalesced bulk load per tile.
+template <int S, int OB>
+__device__ __forceinline__ int row_tw_offset(int beta) {
+  return (1 << OB) * ((1 << S) - (1 << (S - beta)));
+}
+
+template <bool FWD, bool ROW, int S, int OB, int W>
+__device__ __forceinline__ void ntt_group_f64(u64 (&x)[16], const int (&jb)[16 >> W], int g0, int logn,
+                                              const double* __restrict__ tw, const double* sm_tw,
+                                              const PrimeConst& P, bool last_stage_inv) {
+  constexpr int NO = 16 >> W;
+  const int logb = ROW ? 0 : (logn - S);
+  const double q = P.qd;
+  const u64 N = 1ull << logn;
+  double v[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    v[r] = __longlong_as_double((long long)x[r]);
+    if (!FWD) v[r] = centre_f64(v[r], q, P.qinv_d);
+  }
+#pragma unroll
+  for (int ii = 0; ii < W; ++ii) {
+    const int i = FWD ? (W - 1 - ii) : ii;
+    const int beta = logb + g0 + i;
+#pragma unroll
+    for (int ro = 0; ro < NO; ++ro) {
+#pragma unroll
+      for (int hp = 0; hp < (1 << (W - 1 - i)); ++hp) {
+        const int rb = (ro << W) | (hp << (i + 1));
+        const u64 j = (u64)jb[ro] + ((u64)(hp << (i + 1)) << (logb + g0));
+        const bool fin = (!FWD) && last_stage_inv && (beta == logn - 1);
+        double2 wt = make_double2(0.0, 0.0);
+        if (!fin) {
+          if (ROW)
+            wt.x = sm_tw[row_tw_offset<S, OB>(beta) + (int)((j & ((1u << (S + OB)) - 1)) >> (beta + 1))];
+          else
+            wt.x = __ldg(tw + ((N + j) >> (beta + 1)));
+          wt.y = __dmul_rn(wt.x, P.qinv_d);  // w / q (relative error <= 2^-52)
+        }
+#pragma unroll
+        for (int lp = 0; lp < (1 << i); ++lp) {
+          const int r0 = rb | lp, r1 = r0 | (1 << i);
+          const double X = v[r0], Y = v[r1];
+          if (FWD) {
+            const double T = mulmod_f64(Y, wt.x, wt.y, q);
+            v[r0] = __dadd_rn(X, T);
+            v[r1] = __dsub_rn(X, T);
+          } else if (fin) {
+            v[r0] = mulmod_f64(__dadd_rn(X, Y), P.ninv_d, P.ninv_q, q);
+            v[r1] = mulmod_f64(__dsub_rn(X, Y), P.w1n_d, P.w1n_q, q);
+          } else {
+            v[r0] = __dadd_rn(X, Y);
+            v[r1] = mulmod_f64(__dsub_rn(X, Y), wt.x, wt.y, q);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r) x[r] = (u64)__double_as_longlong(v[r]);
+}
+
 // Compute, for a group at sub-bits [g0, g0+W), the tile element base index
 // (r_in = 0) and the global j base for each r_out.
 template <bool ROW, int S, int OB, int W>
@@ -138,12 +243,19 @@ struct Sched {
   static constexpr int G = S / 4;          // number of full groups
 };
 
-template <bool FWD, bool ROW, int S, int OB>
+// dynamic shared memory of a pass kernel (bytes)
+template <bool ROW, int S, int OB, bool F64>
+constexpr int ntt_smem_bytes() {
+  return 8 * ((1 << (S + OB)) + ((ROW && F64) ? (1 << OB) * ((1 << S) - 1) : 0));
+}
+
+template <bool FWD, bool ROW, int S, int OB, bool F64>
 __global__ void __launch_bounds__((1 << (S + OB)) / 16)
     ntt_pass_kernel(NttArgs a) {
   constexpr int TILE = 1 << (S + OB);
   constexpr int T = TILE / 16;
-  __shared__ u64 sm[TILE];
+  extern __shared__ u64 dyn_smem[];  // [TILE] data tile, then [kTw] staged twiddles
+  u64* sm = dyn_smem;
   const int t = threadIdx.x;
   const int tiles = (1 << a.logn) / TILE;
   const long long inst = blockIdx.x / tiles;
@@ -154,7 +266,24 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16)
   u64* base = a.data + ((long long)bidx * a.lt.stride + a.lt.off[ent]) * (1ll << a.logn);
   const PrimeConst P = a.pc[a.lt.prime[ent]];
   const ulonglong2* tw = FWD ? P.tw_fwd : P.tw_inv;
+  const double* twf = FWD ? P.twf_fwd : P.twf_inv;
   const u64 q = P.q;
+  // first pass of the transform reads residues, last pass writes residues
+  constexpr bool kFirstPass = FWD ? !ROW : ROW;
+  constexpr bool kLastPass = !kFirstPass;
+  // FP64 ROW pass: stage the tile's twiddles (all S stages) in shared memory
+  double* sm_tw = reinterpret_cast<double*>(dyn_smem + TILE);
+  if (ROW && F64) {
+    const long long row0 = (long long)tile << OB;
+#pragma unroll 1
+    for (int beta = 0; beta < S; ++beta) {
+      const int cnt = (1 << OB) << (S - beta - 1);
+      const double* src = twf + ((1ll << a.logn) >> (beta + 1)) + (row0 << (S - beta - 1));
+      double* dst = sm_tw + row_tw_offset<S, OB>(beta);
+      for (int k = t; k < cnt; k += T) dst[k] = __ldg(src + k);
+    }
+    __syncthreads();
+  }
 
   u64 x[16];
   constexpr int NG = Sched<S>::G + (Sched<S>::R ? 1 : 0);
@@ -215,10 +344,23 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16)
         x[r] = sm[swz<ROW>(e)];                                                                \
       }                                                                                        \
     }                                                                                          \
-    ntt_group<FWD, ROW, S, WW>(x, jb, g0, a.logn, tw, P, !ROW);                                 \
+    if (F64 && kFirstPass && first) {                                                          \
+      _Pragma("unroll") for (int r = 0; r < 16; ++r) x[r] = u64_to_f64bits(x[r]);              \
+    }                                                                                          \
+    if (F64)                                                                                   \
+      ntt_group_f64<FWD, ROW, S, OB, WW>(x, jb, g0, a.logn, twf, sm_tw, P, !ROW);              \
+    else                                                                                       \
+      ntt_group<FWD, ROW, S, WW>(x, jb, g0, a.logn, tw, P, !ROW);                              \
     if (lastg) {                                                                               \
-      _Pragma("unroll") for (int r = 0; r < 16; ++r) x[r] =                                    \
-          (FWD ? (ROW ? reduce4(x[r], q, P.two_q) : x[r]) : (ROW ? x[r] : csub(x[r], q)));      \
+      if (F64) {                                                                               \
+        if (kLastPass) {                                                                       \
+          _Pragma("unroll") for (int r = 0; r < 16; ++r) x[r] =                                \
+              f64bits_to_residue(x[r], P.qd, P.qinv_d);                                        \
+        }                                                                                      \
+      } else {                                                                                 \
+        _Pragma("unroll") for (int r = 0; r < 16; ++r) x[r] =                                  \
+            (FWD ? (ROW ? reduce4(x[r], q, P.two_q) : x[r]) : (ROW ? x[r] : csub(x[r], q)));    \
+      }                                                                                        \
       if (FWD && ROW) {                                                                        \
         /* stage through smem for a coalesced store */                                         \
         __syncthreads();                                                                       \

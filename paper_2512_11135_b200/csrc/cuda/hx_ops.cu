@@ -255,7 +255,10 @@ void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long ba
   A.g = (hx::u32)g;
   A.logn = c->logn;
   const int th = pt_threads(c);
-  dim3 grid((unsigned)(c->N() / th), (unsigned)(n_q + c->n_special));
+  // split the batch over blockIdx.z: more CTAs in flight, key words re-read
+  // from L2/HBM only once per slice
+  const unsigned zs = (unsigned)std::max<long long>(1, std::min<long long>(batch / 16, 8));
+  dim3 grid((unsigned)(c->N() / th), (unsigned)(n_q + c->n_special), zs);
   if (A.dnum <= 4)
     hx::ks_inner_kernel<4><<<grid, th, 0, s>>>(A);
   else if (A.dnum <= 8)
@@ -396,6 +399,65 @@ void rotate_from_digits(hx_ctx* c, u64* out, long long out_ct_stride, const u64*
   permute(c, out, out_ct_stride, W.p, 2ll * n_q * N, 2 * n_q, batch, g, s);
 }
 
+// Host-buffer round trip, pipelined: the batch is cut into chunks; chunk i's
+// host->device copy (stream h), compute (stream s) and device->host copy
+// (stream d) overlap with chunks i-1 / i+1 on double-buffered device slots.
+// Host buffers should be pinned for the copies to run asynchronously.
+template <class F>
+void pipelined_host(hx_ctx* c, int batch, std::vector<const uint64_t*> in_host,
+                    std::vector<long long> in_words, uint64_t* out_host, long long out_words,
+                    cudaStream_t s, F compute) {
+  const int chunk = std::max(1, std::min(batch, 32));
+  const int nchunks = (batch + chunk - 1) / chunk;
+  cudaStream_t h = nullptr, d = nullptr;
+  cuda_ok(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking), "stream");
+  cuda_ok(cudaStreamCreateWithFlags(&d, cudaStreamNonBlocking), "stream");
+  cudaEvent_t ev_in[2], ev_cmp[2], ev_out[2];
+  for (int k = 0; k < 2; ++k) {
+    cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_cmp[k], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming);
+  }
+  std::vector<u64*> din[2];
+  u64* dout[2] = {nullptr, nullptr};
+  for (int k = 0; k < 2 && k < nchunks; ++k) {
+    for (long long w : in_words) {
+      u64* p = nullptr;
+      cuda_ok(cudaMalloc((void**)&p, (size_t)w * chunk * 8), "cudaMalloc(chunk)");
+      din[k].push_back(p);
+    }
+    cuda_ok(cudaMalloc((void**)&dout[k], (size_t)out_words * chunk * 8), "cudaMalloc(chunk)");
+  }
+  cuda_ok(cudaStreamSynchronize(s), "sync");
+  for (int i = 0; i < nchunks; ++i) {
+    const int k = i & 1, b0 = i * chunk, n = std::min(chunk, batch - b0);
+    if (i >= 2) cuda_ok(cudaStreamWaitEvent(h, ev_cmp[k], 0), "wait");
+    for (std::size_t a = 0; a < in_host.size(); ++a)
+      cuda_ok(cudaMemcpyAsync(din[k][a], in_host[a] + (long long)b0 * in_words[a], (size_t)n * in_words[a] * 8,
+                              cudaMemcpyHostToDevice, h), "h2d");
+    cudaEventRecord(ev_in[k], h);
+    cuda_ok(cudaStreamWaitEvent(s, ev_in[k], 0), "wait");
+    if (i >= 2) cuda_ok(cudaStreamWaitEvent(s, ev_out[k], 0), "wait");
+    compute(dout[k], din[k], n, s);
+    cudaEventRecord(ev_cmp[k], s);
+    cuda_ok(cudaStreamWaitEvent(d, ev_cmp[k], 0), "wait");
+    cuda_ok(cudaMemcpyAsync(out_host + (long long)b0 * out_words, dout[k], (size_t)n * out_words * 8,
+                            cudaMemcpyDeviceToHost, d), "d2h");
+    cudaEventRecord(ev_out[k], d);
+  }
+  cuda_ok(cudaStreamSynchronize(d), "sync");
+  cuda_ok(cudaStreamSynchronize(s), "sync");
+  for (int k = 0; k < 2; ++k) {
+    for (u64* p : din[k]) cudaFree(p);
+    if (dout[k]) cudaFree(dout[k]);
+    cudaEventDestroy(ev_in[k]);
+    cudaEventDestroy(ev_cmp[k]);
+    cudaEventDestroy(ev_out[k]);
+  }
+  cudaStreamDestroy(h);
+  cudaStreamDestroy(d);
+}
+
 }  // namespace
 
 namespace hx {
@@ -460,8 +522,12 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
     }
     // twiddles + per-prime constants
     std::vector<ulonglong2> tw((size_t)T * 2 * N);
+    std::vector<double> twf((size_t)T * 2 * N, 0.0);
     std::vector<PrimeConst> pc(T);
+    const char* force_int = std::getenv("HX_NTT_INT");
+    c->allow_f64 = !(force_int && force_int[0] == '1');
     cuda_ok(cudaMalloc((void**)&c->d_tw, tw.size() * sizeof(ulonglong2)), "cudaMalloc(tw)");
+    cuda_ok(cudaMalloc((void**)&c->d_twf, twf.size() * sizeof(double)), "cudaMalloc(twf)");
     for (int i = 0; i < T; ++i) {
       const u64 q = c->primes[i];
       const u64 psi = find_psi(q, N), psi_inv = hinv(psi, q);
@@ -488,9 +554,26 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
       P.w1np = shoup(P.w1n, q);
       P.tw_fwd = c->d_tw + (size_t)i * 2 * N;
       P.tw_inv = c->d_tw + (size_t)i * 2 * N + N;
+      // FP64 butterfly path for q < 2^47 (exactness bounds in hx_ntt.cuh)
+      P.f64 = c->allow_f64 && q < (1ull << 47);
+      c->f64.push_back(P.f64 ? 1 : 0);
+      const double qd = (double)q;
+      P.qd = qd;
+      P.qinv_d = 1.0 / qd;
+      P.ninv_d = (double)P.ninv;
+      P.ninv_q = (double)P.ninv / qd;
+      P.w1n_d = (double)P.w1n;
+      P.w1n_q = (double)P.w1n / qd;
+      double* ff = twf.data() + (size_t)i * 2 * N;
+      if (P.f64)
+        for (u64 k = 0; k < 2 * N; ++k) ff[k] = (double)(k < N ? f[k] : g[k - N]).x;
+      P.twf_fwd = c->d_twf + (size_t)i * 2 * N;
+      P.twf_inv = c->d_twf + (size_t)i * 2 * N + N;
     }
     cuda_ok(cudaMemcpy(c->d_tw, tw.data(), tw.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice),
             "upload tw");
+    cuda_ok(cudaMemcpy(c->d_twf, twf.data(), twf.size() * sizeof(double), cudaMemcpyHostToDevice),
+            "upload twf");
     c->d_pc = upload(pc);
     // ModUp constants per (n_q, digit)
     std::vector<SC> mu;
@@ -567,7 +650,7 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
 
 void hx_ctx_destroy(hx_ctx* c) {
   if (!c) return;
-  for (void* p : {(void*)c->d_pc, (void*)c->d_tw, (void*)c->d_modup, (void*)c->d_phinv,
+  for (void* p : {(void*)c->d_pc, (void*)c->d_tw, (void*)c->d_twf, (void*)c->d_modup, (void*)c->d_phinv,
                   (void*)c->d_pconv, (void*)c->d_pmodq, (void*)c->d_pinv, (void*)c->d_qlinv,
                   (void*)c->d_qlmod})
     if (p) cudaFree(p);
@@ -932,13 +1015,12 @@ int hx_rotate_host(hx_ctx* c, uint64_t* out_host, const uint64_t* in_host, const
   return guarded([&] {
     check_ctx(c);
     check_nq(c, n_q);
-    const long long words = (long long)batch * 2 * n_q * c->N();
-    DBuf din(words, S(s)), dout(words, S(s));
-    cuda_ok(cudaMemcpyAsync(din.p, in_host, words * 8, cudaMemcpyHostToDevice, S(s)), "h2d");
-    const int rc = hx_rotate(c, (uint64_t*)dout.p, (const uint64_t*)din.p, key, batch, n_q, g, s);
-    if (rc != HX_OK) throw HxError(rc, g_last_error);
-    cuda_ok(cudaMemcpyAsync(out_host, dout.p, words * 8, cudaMemcpyDeviceToHost, S(s)), "d2h");
-    cuda_ok(cudaStreamSynchronize(S(s)), "sync");
+    const long long ct = 2ll * n_q * c->N();
+    pipelined_host(c, batch, {in_host}, {ct}, out_host, ct, S(s),
+                   [&](u64* out, const std::vector<u64*>& in, int n, cudaStream_t st) {
+                     const int rc = hx_rotate(c, (uint64_t*)out, (const uint64_t*)in[0], key, n, n_q, g, st);
+                     if (rc != HX_OK) throw HxError(rc, g_last_error);
+                   });
   });
 }
 
@@ -947,15 +1029,13 @@ int hx_mul_relin_host(hx_ctx* c, uint64_t* out_host, const uint64_t* a_host,
   return guarded([&] {
     check_ctx(c);
     check_nq(c, n_q);
-    const long long words = (long long)batch * 2 * n_q * c->N();
-    DBuf da(words, S(s)), db(words, S(s)), dout(words, S(s));
-    cuda_ok(cudaMemcpyAsync(da.p, a_host, words * 8, cudaMemcpyHostToDevice, S(s)), "h2d");
-    cuda_ok(cudaMemcpyAsync(db.p, b_host, words * 8, cudaMemcpyHostToDevice, S(s)), "h2d");
-    const int rc = hx_mul_relin(c, (uint64_t*)dout.p, (const uint64_t*)da.p,
-                                (const uint64_t*)db.p, rlk, batch, n_q, s);
-    if (rc != HX_OK) throw HxError(rc, g_last_error);
-    cuda_ok(cudaMemcpyAsync(out_host, dout.p, words * 8, cudaMemcpyDeviceToHost, S(s)), "d2h");
-    cuda_ok(cudaStreamSynchronize(S(s)), "sync");
+    const long long ct = 2ll * n_q * c->N();
+    pipelined_host(c, batch, {a_host, b_host}, {ct, ct}, out_host, ct, S(s),
+                   [&](u64* out, const std::vector<u64*>& in, int n, cudaStream_t st) {
+                     const int rc = hx_mul_relin(c, (uint64_t*)out, (const uint64_t*)in[0],
+                                                 (const uint64_t*)in[1], rlk, n, n_q, st);
+                     if (rc != HX_OK) throw HxError(rc, g_last_error);
+                   });
   });
 }
 
