@@ -249,6 +249,56 @@ def run_reference_arm(args):
     return 0
 
 
+def ffn_bsgs_bench(torch, chain, special, args, iters=3):
+    """BASELINE configs[2]: FFN up-projection W1 (768 x 3072, N(0, 0.02^2)) as a
+    BSGS linear transform at N=2^16 / 24+3 primes through the helix C-ABI
+    (hxc_matvec): d = 1024, 3 row blocks, n1 = n2 = 32, one token per
+    ciphertext (T = 1), plus the 90%-diagonal-pruned variant."""
+    import numpy as np
+
+    from paper_2512_11135_b200.helix import BSGS, Backend, params_json
+
+    rng = np.random.default_rng(20251211 * 10 + 3)
+    be = Backend(params_json(LOGN, chain, special, ALPHA, 40), seed=3)
+    out = {}
+    W1 = rng.normal(0.0, 0.02, (768, 3072))
+    x = rng.uniform(-1, 1, 768)
+    xs = np.tile(np.concatenate([x, np.zeros(256)]), be.slots // 1024)
+    lvl = be.max_level
+    for name, prune in (("ffn_w1", False), ("ffn_w1_pruned90", True)):
+        M = W1.T.copy()  # y = x W1  ->  M = W1^T (3072 out x 768 in)
+        if prune:  # zero 90% of the generalized diagonals of every 1024 x 1024 block
+            for b in range(3):
+                for i in rng.choice(1024, 922, replace=False):
+                    r = np.arange(1024)
+                    c = (i + r) % 1024
+                    keep = c < 768
+                    M[b * 1024 + r[keep], c[keep]] = 0.0
+        t0 = time.perf_counter()
+        mat = be.prepare(BSGS, M, lvl)
+        be.gen_rotation_keys(mat.rotations())
+        prep = time.perf_counter() - t0
+        ct = be.encrypt(xs, lvl)
+        outs, rep = be.matvec(mat, ct)  # warm-up + correctness
+        y = np.concatenate([be.decrypt(o)[:1024] for o in outs])
+        err = float(np.abs(y - M @ x).max())
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            outs, rep = be.matvec(mat, ct)
+        e1.record()
+        torch.cuda.synchronize()
+        secs = e0.elapsed_time(e1) / 1e3 / iters
+        info = mat.info()
+        out[name] = {"matvec_per_s": 1.0 / secs, "ms_per_matvec": 1e3 * secs, "max_abs_err": err,
+                     "rotations": rep["rotations"], "pt_muls": rep["pt_muls"], "nonzero_diagonals": info["nonzero"],
+                     "diag_bytes": info["nonzero"] * 24 * N * 8, "prepare_s": prep}
+        del mat, outs, ct
+    be.close()
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -258,6 +308,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-ffn", action="store_true", help="skip the config-3 BSGS matvec extra")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -379,6 +430,11 @@ def main():
     e2e = {"value": BATCH * e2e_steps * world / e2e_secs, "unit": "KS/s",
            "h2d_bytes_per_step": ct_bytes, "d2h_bytes_per_step": ct_bytes,
            "api": "hx_rotate_host (pinned host buffers)"}
+
+    if not args.no_extras and not args.no_ffn:
+        del hin, hout_h, out, ntt_buf
+        torch.cuda.empty_cache()
+        extras.update(ffn_bsgs_bench(torch, chain, special, args))
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

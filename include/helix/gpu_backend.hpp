@@ -96,6 +96,12 @@ class GpuLatticeBackend final : public SlotBackend {
   // linalg.cpp's generic matvec_bsgs.
   Ciphertext bsgs_block(const std::vector<Ciphertext>& baby, const std::vector<Plaintext>& diags,
                         int n1, int n2);
+  // All row blocks of a tiled matrix at once (diags: blocks x n1 n2 payloads):
+  // per-block MAC launches write inner sums in [n2][blocks] order, then giant
+  // step j of every block is rotated with one read of key n1 j
+  // (hx_rotate_grouped) and summed in one pass.  Same trace as per-block.
+  std::vector<Ciphertext> bsgs_blocks(const std::vector<Ciphertext>& baby,
+                                      const std::vector<Plaintext>& diags, int n1, int n2, int blocks);
 
   // ---- raw access ----
   hx_ctx* device_context() const { return ctx_; }

@@ -129,6 +129,12 @@ int hx_rotate_hoisted(hx_ctx* ctx, uint64_t* out, const uint64_t* in,
  * (rotation layout); one batched ModUp. */
 int hx_rotate_multi(hx_ctx* ctx, uint64_t* out, const uint64_t* in, const uint64_t* const* keys,
                     const uint64_t* galois, int batch, int n_q, void* stream);
+/* rotations grouped by key: in [R][E][2][n_q][N]; ciphertexts r*E .. r*E+E-1
+ * are rotated by galois[r] with keys[r] (rotation layout), each key word read
+ * once for its E ciphertexts (BSGS giant step j of every row block).
+ * out [R][E][2][n_q][N]. */
+int hx_rotate_grouped(hx_ctx* ctx, uint64_t* out, const uint64_t* in, const uint64_t* const* keys,
+                      const uint64_t* galois, int R, int E, int n_q, void* stream);
 /* tensor (LatticeContext::mul x4): a, b [batch][2][n_q][N] -> [batch][3][n_q][N] */
 int hx_tensor(hx_ctx* ctx, uint64_t* out3, const uint64_t* a, const uint64_t* b, int batch,
               int n_q, void* stream);
@@ -139,6 +145,15 @@ int hx_mul_relin(hx_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* 
 /* ---- BSGS linear transform ------------------------------ */
 /* inner [n2][2][n_q][N]: inner_j = sum_k diags[j*n1+k] (.) baby[k];
  * baby [n1][2][n_q][N]; diags [n2*n1][diag_limbs][N] (first n_q limbs used). */
+/* as hx_bsgs_mac with inner_j written at inner + j * inner_jstride words (e.g.
+ * [n2][blocks][2][n_q][N] so the giant steps of all row blocks are grouped) */
+int hx_bsgs_mac_ex(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, const uint64_t* baby,
+                   const uint64_t* diags, int diag_limbs, int n1, int n2, int n_q, void* stream);
+/* out[p] = sum_{r < terms} in[r * term_stride + p * in_poly_stride] (mod q per
+ * limb) for polys p of n_q limbs -- the giant-step sum */
+int hx_sum_strided(hx_ctx* ctx, uint64_t* out, const uint64_t* in, int terms, long long term_stride,
+                   int polys, long long in_poly_stride, long long out_poly_stride, int n_q,
+                   void* stream);
 int hx_bsgs_mac(hx_ctx* ctx, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,
                 int diag_limbs, int n1, int n2, int n_q, void* stream);
 

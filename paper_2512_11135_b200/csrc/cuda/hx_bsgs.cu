@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(TT) bsgs_mac_kernel(MacArgs A) {
       mac128(z0, d, smb[(2 * k) * TT + tid]);
       mac128(z1, d, smb[(2 * k + 1) * TT + tid]);
     }
-    u64* o = A.inner + (2ll * j) * L + i * N + t;
+    u64* o = A.inner + (long long)j * A.out_jstride + i * N + t;
     o[0] = reduce128(z0, P);
     o[L] = reduce128(z1, P);
   }
@@ -66,6 +66,23 @@ void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s) {
   (void)tt;
   dim3 grid((unsigned)(N / TT), (unsigned)A.n_q);
   bsgs_mac_kernel<TT><<<grid, TT, smem, s>>>(A);
+}
+
+// out[p][i][t] = sum_r in[r][p][i][t] mod q_i
+__global__ void sum_kernel(SumArgs A) {
+  const long long N = 1ll << A.logn;
+  const int p = blockIdx.z, i = blockIdx.y;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 q = A.pc[i].q;
+  const u64* src = A.in + p * A.in_poly_stride + i * N + t;
+  u64 acc = 0;
+  for (int r = 0; r < A.terms; ++r) acc = addmod(acc, __ldcs(src + r * A.term_stride), q);
+  A.out[p * A.out_poly_stride + i * N + t] = acc;
+}
+
+void launch_sum(const SumArgs& A, int polys, long long N, cudaStream_t s) {
+  const int th = (int)(N < 256 ? N : 256);
+  sum_kernel<<<dim3((unsigned)(N / th), (unsigned)A.n_q, (unsigned)polys), th, 0, s>>>(A);
 }
 
 }  // namespace hx

@@ -88,6 +88,26 @@ __global__ void permute_kernel(u64* out, long long out_stride, const u64* in, lo
   out[b * out_stride + l * N + t] = __ldg(in + b * in_stride + l * N + src);
 }
 
+// Several permutations in one launch: group r (blockIdx.z / per) applies
+// galois element g[r] to `per` elements (blockIdx.z % per); element (r, e) is
+// read at in + (r per + e) in_stride and written at out + r out_rstride +
+// e out_estride.
+struct PermuteMulti {
+  u32 g[64];
+  long long in_stride, out_rstride, out_estride;
+  int per, logn;
+};
+__global__ void permute_multi_kernel(u64* out, const u64* in, PermuteMulti P) {
+  const long long N = 1ll << P.logn;
+  const int r = blockIdx.z / P.per, e = blockIdx.z % P.per;
+  const int l = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const u32 g = P.g[r];
+  const int src = g == 1 ? t : (int)ntt_auto_index((u32)t, g, P.logn);
+  out[r * P.out_rstride + e * P.out_estride + l * N + t] =
+      __ldg(in + ((long long)r * P.per + e) * P.in_stride + l * N + src);
+}
+
 // from_i64 (rns_poly.cpp:218-227): small signed ints -> every limb.
 // v is [batch][N] int64; out [batch][limbs][N].
 __global__ void from_i64_kernel(u64* out, const long long* v, const PrimeConst* pc, LimbTable lt,
@@ -176,44 +196,57 @@ __global__ void modup_bconv_kernel(ModUpArgs A) {
 // read: u_c[j][t] = sum_d D_d[j][perm_g(t)] * key_{d,c}[kl(j)][t]
 // (mul_acc, rns_poly.cpp:102-110, with lazy 128-bit accumulation).  The key
 // words of a (j, t) are held in registers and reused across the batch.
+// Several keys per launch, E = `batch` elements per key.  shared = 1: every
+// key applies to the same digit elements 0..E-1 (hoisted rotations of a
+// batch); shared = 0: key r applies to its own digit elements r E .. r E + E-1
+// (independent rotations grouped by key, e.g. the BSGS giant step j of every
+// row block).  Output element (r, e) at u + (r E + e) 2 ext N.
+// blockIdx.z = r * slices + element slice.
+constexpr int kMaxKeys = 64;
 struct InnerArgs {
-  const u64* digits;  // [batch][dnum][ext][N]
-  const u64* key;     // [dnum_max][2][full][N]
-  u64* u;             // [batch][2][ext][N]
+  const u64* digits;  // [elements][dnum][ext][N]
+  const u64* keys[kMaxKeys];  // [dnum_max][2][full][N] each
+  int n_keys, shared, slices;
+  u64* u;             // [n_keys][E][2][ext][N]
   const PrimeConst* pc;
   int n_q, n_chain, n_special, dnum, batch;
-  u32 g;  // 1 = identity
+  u32 g;  // 1 = identity (input-side automorphism of the digits)
   int logn;
 };
 
 template <int MAXD>
-__global__ void ks_inner_kernel(InnerArgs A) {
+__global__ void __launch_bounds__(256, 2) ks_inner_kernel(InnerArgs A) {
   const int N = 1 << A.logn;
   const int ext = A.n_q + A.n_special, full = A.n_chain + A.n_special;
   const int j = blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int kl = j < A.n_q ? j : A.n_chain + (j - A.n_q);
+  const int r = blockIdx.z / A.slices, slice = blockIdx.z % A.slices;
+  const u64* key = A.keys[r];
+  const int E = A.batch;
   const PrimeConst& P = A.pc[kl];
   u64 k0[MAXD], k1[MAXD];
 #pragma unroll
   for (int d = 0; d < MAXD; ++d) {
     if (d < A.dnum) {
-      k0[d] = __ldg(A.key + (((long long)d * 2 + 0) * full + kl) * N + t);
-      k1[d] = __ldg(A.key + (((long long)d * 2 + 1) * full + kl) * N + t);
+      k0[d] = __ldg(key + (((long long)d * 2 + 0) * full + kl) * N + t);
+      k1[d] = __ldg(key + (((long long)d * 2 + 1) * full + kl) * N + t);
     }
   }
   const int src = (A.g == 1) ? t : (int)ntt_auto_index((u32)t, A.g, A.logn);
-  // this CTA's slice of the batch (blockIdx.z); BB ciphertexts per iteration
-  // so 8 x BB independent digit loads are in flight per thread
-  constexpr int BB = MAXD <= 8 ? 4 : 1;
-  const int per = (A.batch + gridDim.z - 1) / gridDim.z;
-  const int b_lo = blockIdx.z * per, b_hi = min(A.batch, b_lo + per);
+  // this CTA's slice of the elements; BB ciphertexts per iteration so that
+  // 8 x BB independent digit loads are in flight per thread
+  constexpr int BB = MAXD <= 8 ? 2 : 1;
+  const int per = (E + A.slices - 1) / A.slices;
+  const int b_lo = slice * per, b_hi = min(E, b_lo + per);
   const long long dstride = (long long)A.dnum * ext * N;
+  const long long ebase = A.shared ? 0 : (long long)r * E;  // digit element of e = 0
+  u64* ubase = A.u + (long long)r * E * 2 * ext * N;
   for (int b0 = b_lo; b0 < b_hi; b0 += BB) {
     u64 v[BB][MAXD];
 #pragma unroll
     for (int bb = 0; bb < BB; ++bb) {
-      const u64* Db = A.digits + (long long)(b0 + bb) * dstride + (long long)j * N + src;
+      const u64* Db = A.digits + (ebase + b0 + bb) * dstride + (long long)j * N + src;
 #pragma unroll
       for (int d = 0; d < MAXD; ++d)
         v[bb][d] = (d < A.dnum && b0 + bb < b_hi) ? __ldcs(Db + (long long)d * ext * N) : 0ull;
@@ -229,7 +262,7 @@ __global__ void ks_inner_kernel(InnerArgs A) {
           mac128(z1, v[bb][d], k1[d]);
         }
       }
-      u64* ub = A.u + (long long)(b0 + bb) * 2 * ext * N + (long long)j * N + t;
+      u64* ub = ubase + (long long)(b0 + bb) * 2 * ext * N + (long long)j * N + t;
       ub[0] = reduce128(z0, P);
       ub[(long long)ext * N] = reduce128(z1, P);
     }
@@ -295,6 +328,9 @@ struct CombineArgs {
   const SC* pinv;  // [n_chain]
   int n_q;
   long long u_stride, conv_stride, out_stride, add_stride;
+  // `add` applies to polys b with b % add_every == 0; its element is
+  // (b / add_every) % add_period (add_period 0: no wrap)
+  long long add_every, add_period;
   u32 add_g;  // 1 = no automorphism on `add`
   int logn;
 };
@@ -302,6 +338,9 @@ struct CombineArgs {
 __global__ void combine_kernel(CombineArgs A) {
   const int N = 1 << A.logn;
   const long long b = blockIdx.z;
+  long long ba = b / A.add_every;
+  if (A.add_period) ba %= A.add_period;
+  const bool do_add = A.add && (b % A.add_every) == 0;
   const int i = blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const PrimeConst& P = A.pc[i];
@@ -309,9 +348,9 @@ __global__ void combine_kernel(CombineArgs A) {
   const u64 uu = A.u[b * A.u_stride + (long long)i * N + t];
   const u64 cv = A.conv[b * A.conv_stride + (long long)i * N + t];
   u64 r = csub(shoup_lazy(uu + P.q - cv, c.w, c.wp, P.q), P.q);
-  if (A.add) {
+  if (do_add) {
     const int src = A.add_g == 1 ? t : (int)ntt_auto_index((u32)t, A.add_g, A.logn);
-    r = addmod(r, A.add[b * A.add_stride + (long long)i * N + src], P.q);
+    r = addmod(r, A.add[ba * A.add_stride + (long long)i * N + src], P.q);
   }
   A.out[b * A.out_stride + (long long)i * N + t] = r;
 }

@@ -240,11 +240,19 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
   if (lt.count) hx::ntt_forward(c, digits, batch, lt, s);
 }
 
-void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long batch, int n_q,
-              u64 g, cudaStream_t s) {
+// Key inner products for R keys, E elements per key, one launch:
+//   shared: keys[r] applies to digit elements 0..E-1 (hoisting);
+//   !shared: keys[r] applies to digit elements r E .. r E + E - 1.
+// Output element (r, e) at u + (r E + e) 2 ext N.
+void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<const u64*>& keys,
+                    bool shared, long long E, int n_q, u64 g, cudaStream_t s) {
+  HX_REQUIRE(!keys.empty() && (int)keys.size() <= hx::kMaxKeys, "ks_inner: 1..64 keys per launch");
   hx::InnerArgs A;
   A.digits = digits;
-  A.key = key;
+  for (std::size_t r = 0; r < keys.size(); ++r) A.keys[r] = keys[r];
+  A.n_keys = (int)keys.size();
+  A.shared = shared ? 1 : 0;
+  const long long batch = E;
   A.u = u;
   A.pc = c->d_pc;
   A.n_q = n_q;
@@ -255,10 +263,10 @@ void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long ba
   A.g = (hx::u32)g;
   A.logn = c->logn;
   const int th = pt_threads(c);
-  // split the batch over blockIdx.z: more CTAs in flight, key words re-read
-  // from L2/HBM only once per slice
-  const unsigned zs = (unsigned)std::max<long long>(1, std::min<long long>(batch / 16, 8));
-  dim3 grid((unsigned)(c->N() / th), (unsigned)(n_q + c->n_special), zs);
+  // split each key's elements over slices: more CTAs in flight, the key words
+  // of a (limb, coefficient) are re-read only once per slice
+  A.slices = (int)std::max<long long>(1, std::min<long long>(E / 16, 8));
+  dim3 grid((unsigned)(c->N() / th), (unsigned)(n_q + c->n_special), (unsigned)(A.n_keys * A.slices));
   if (A.dnum <= 4)
     hx::ks_inner_kernel<4><<<grid, th, 0, s>>>(A);
   else if (A.dnum <= 8)
@@ -272,11 +280,17 @@ void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long ba
   launched(c, "ks_inner_kernel");
 }
 
+void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long batch, int n_q,
+              u64 g, cudaStream_t s) {
+  ks_inner_multi(c, u, digits, {key}, true, batch, n_q, g, s);
+}
+
 // Centred ModDown of `polys` PQ-basis polys u (stride u_stride words) into
-// out (stride out_stride words); optionally adds tau_g(add) (stride add_stride).
+// out (stride out_stride words).  Optionally adds tau_g(add) to the polys with
+// index % add_every == 0, using add element (index / add_every) % add_period.
 void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long u_stride,
              long long polys, int n_q, const u64* add, long long add_stride, u64 add_g,
-             cudaStream_t s) {
+             cudaStream_t s, long long add_every = 1, long long add_period = 0) {
   const long long N = c->N();
   const int K = c->n_special;
   DBuf sp(polys * K * N, s), conv(polys * n_q * N, s);
@@ -315,6 +329,8 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
   C.conv_stride = (long long)n_q * N;
   C.out_stride = out_stride;
   C.add_stride = add_stride;
+  C.add_every = add_every;
+  C.add_period = add_period;
   C.add_g = (hx::u32)add_g;
   C.logn = c->logn;
   dim3 g3((unsigned)(N / th), (unsigned)n_q, (unsigned)polys);
@@ -355,6 +371,8 @@ void rescale(hx_ctx* c, u64* out, const u64* in, long long polys, int n_q, cudaS
   C.conv_stride = (long long)(n_q - 1) * N;
   C.out_stride = (long long)(n_q - 1) * N;
   C.add_stride = 0;
+  C.add_every = 1;
+  C.add_period = 0;
   C.add_g = 1;
   C.logn = c->logn;
   hx::combine_kernel<<<dim3((unsigned)(N / th), (unsigned)(n_q - 1), (unsigned)polys), th, 0, s>>>(C);
@@ -380,23 +398,49 @@ u64 galois_inverse(u64 g, u64 two_n) {
   return r;
 }
 
-// Rotation(s) from precomputed digits of `in` (batch cts [2][n_q]) with a
-// rotation-layout key K' = tau^-1(K):
-//   U' = sum_d D_d (.) K'_d,  W = (c0 + ModDown(U'_0), ModDown(U'_1)),
-//   out = tau_g(W)
-// which equals (tau(c0) + ModDown(sum_d tau(D_d) (.) K_d), ...) bit for bit
-// because the centred ModDown commutes with tau.
-void rotate_from_digits(hx_ctx* c, u64* out, long long out_ct_stride, const u64* in,
-                        const u64* digits, const u64* key_rot, long long batch, int n_q, u64 g,
-                        cudaStream_t s) {
-  const long long N = c->N();
+// Rotations from precomputed ModUp digits with rotation-layout keys
+// K' = tau^-1(K):  U' = sum_d D_d (.) K'_d,  W = (c0 + ModDown(U'_0),
+// ModDown(U'_1)),  out = tau_g(W) -- bit-identical to (tau(c0) +
+// ModDown(sum_d tau(D_d) (.) K_d), ...) because the centred ModDown commutes
+// with tau.  R keys at once, E ciphertexts per key:
+//   shared (hoisting): every key applies to input cts 0..E-1;
+//     output ct (e, r) at out + (e R + r) ct.
+//   !shared (independent rotations grouped by key, e.g. the BSGS giant step j
+//     of every row block): key r applies to input cts r E .. r E + E - 1;
+//     output (r, e) at out + (r E + e) ct.
+// One inner-product launch, one ModDown (both ciphertext polys of every
+// output), one permutation launch (per 64 keys).
+void rotate_batch_from_digits(hx_ctx* c, u64* out, const u64* in, const u64* digits,
+                              const std::vector<const u64*>& keys, const std::vector<u64>& galois,
+                              bool shared, long long E, int n_q, cudaStream_t s) {
+  const long long N = c->N(), ct = 2ll * n_q * N;
   const int ext = n_q + c->n_special;
-  DBuf U(batch * 2 * ext * N, s), W(batch * 2 * n_q * N, s);
-  ks_inner(c, U.p, digits, key_rot, batch, n_q, 1, s);
-  moddown(c, W.p, 2ll * n_q * N, U.p, 2ll * ext * N, batch, n_q, in, 2ll * n_q * N, 1, s);
-  moddown(c, W.p + (long long)n_q * N, 2ll * n_q * N, U.p + (long long)ext * N, 2ll * ext * N,
-          batch, n_q, nullptr, 0, 1, s);
-  permute(c, out, out_ct_stride, W.p, 2ll * n_q * N, 2 * n_q, batch, g, s);
+  const long long R = (long long)keys.size();
+  const long long dstride = (long long)c->dnum(n_q) * ext * N;
+  DBuf U(R * E * 2 * ext * N, s), W(R * E * ct, s);
+  for (long long r0 = 0; r0 < R; r0 += hx::kMaxKeys) {
+    const long long nr = std::min<long long>(hx::kMaxKeys, R - r0);
+    const std::vector<const u64*> kk(keys.begin() + r0, keys.begin() + r0 + nr);
+    const u64* dg = shared ? digits : digits + r0 * E * dstride;
+    ks_inner_multi(c, U.p + r0 * E * 2 * ext * N, dg, kk, shared, E, n_q, 1, s);
+  }
+  // polys p = (r E + e) 2 + c; the c0 polys add input ct (shared ? e : r E + e)
+  moddown(c, W.p, (long long)n_q * N, U.p, (long long)ext * N, R * E * 2, n_q, in, ct, 1, s, 2,
+          shared ? E : 0);
+  const int th = pt_threads(c);
+  for (long long r0 = 0; r0 < R; r0 += 64) {
+    const long long nr = std::min<long long>(64, R - r0);
+    hx::PermuteMulti P;
+    for (long long r = 0; r < nr; ++r) P.g[r] = (hx::u32)galois[r0 + r];
+    P.in_stride = ct;
+    P.per = (int)E;
+    P.logn = c->logn;
+    P.out_rstride = shared ? ct : E * ct;
+    P.out_estride = shared ? R * ct : ct;
+    hx::permute_multi_kernel<<<dim3((unsigned)(N / th), (unsigned)(2 * n_q), (unsigned)(nr * E)), th, 0,
+                               s>>>(out + r0 * P.out_rstride, W.p + r0 * E * ct, P);
+    launched(c, "permute_multi_kernel");
+  }
 }
 
 // Host-buffer round trip, pipelined: the batch is cut into chunks; chunk i's
@@ -836,8 +880,8 @@ int hx_rotate(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* key,
     const int ext = n_q + c->n_special;
     DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s));
     modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s));
-    rotate_from_digits(c, (u64*)out, 2ll * n_q * N, (const u64*)in, D.p, (const u64*)key, batch,
-                       n_q, g, S(s));
+    rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, {(const u64*)key}, {g}, true, batch,
+                             n_q, S(s));
   });
 }
 
@@ -851,11 +895,14 @@ int hx_rotate_hoisted(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
     const int ext = n_q + c->n_special;
     DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s));
     modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s));
+    std::vector<const u64*> kk;
+    std::vector<u64> gg;
     for (int r = 0; r < R; ++r) {
       HX_REQUIRE((galois[r] & 1) && galois[r] < 2 * (u64)N, "galois element");
-      rotate_from_digits(c, (u64*)out + (long long)r * 2 * n_q * N, (long long)R * 2 * n_q * N,
-                         (const u64*)in, D.p, (const u64*)keys[r], batch, n_q, galois[r], S(s));
+      kk.push_back((const u64*)keys[r]);
+      gg.push_back(galois[r]);
     }
+    rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, kk, gg, true, batch, n_q, S(s));
   });
 }
 
@@ -871,9 +918,34 @@ int hx_rotate_multi(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t
       HX_REQUIRE((galois[b] & 1) && galois[b] < 2 * (u64)N, "galois element");
     DBuf D((long long)batch * dstride, S(s));
     modup(c, D.p, (const u64*)in + (long long)n_q * N, ct, batch, n_q, S(s));
-    for (int b = 0; b < batch; ++b)
-      rotate_from_digits(c, (u64*)out + b * ct, ct, (const u64*)in + b * ct, D.p + b * dstride,
-                         (const u64*)keys[b], 1, n_q, galois[b], S(s));
+    std::vector<const u64*> kk;
+    std::vector<u64> gg;
+    for (int b = 0; b < batch; ++b) {
+      kk.push_back((const u64*)keys[b]);
+      gg.push_back((u64)galois[b]);
+    }
+    rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, kk, gg, false, 1, n_q, S(s));
+  });
+}
+
+int hx_rotate_grouped(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* const* keys,
+                      const uint64_t* galois, int R, int E, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    HX_REQUIRE(R >= 1 && E >= 1, "R, E >= 1");
+    const long long N = c->N(), ct = 2ll * n_q * N;
+    const int ext = n_q + c->n_special;
+    std::vector<const u64*> kk;
+    std::vector<u64> gg;
+    for (int r = 0; r < R; ++r) {
+      HX_REQUIRE((galois[r] & 1) && galois[r] < 2 * (u64)N, "galois element");
+      kk.push_back((const u64*)keys[r]);
+      gg.push_back((u64)galois[r]);
+    }
+    DBuf D((long long)R * E * c->dnum(n_q) * ext * N, S(s));
+    modup(c, D.p, (const u64*)in + (long long)n_q * N, ct, (long long)R * E, n_q, S(s));
+    rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, kk, gg, false, E, n_q, S(s));
   });
 }
 
@@ -910,8 +982,8 @@ int hx_mul_relin(hx_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b,
   });
 }
 
-int hx_bsgs_mac(hx_ctx* c, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,
-                int diag_limbs, int n1, int n2, int n_q, void* s) {
+int hx_bsgs_mac_ex(hx_ctx* c, uint64_t* inner, long long inner_jstride, const uint64_t* baby,
+                   const uint64_t* diags, int diag_limbs, int n1, int n2, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
     check_nq(c, n_q);
@@ -926,8 +998,35 @@ int hx_bsgs_mac(hx_ctx* c, uint64_t* inner, const uint64_t* baby, const uint64_t
     A.n_q = n_q;
     A.logn = c->logn;
     A.diag_stride = (long long)diag_limbs * c->N();
+    A.out_jstride = inner_jstride;
     hx::launch_bsgs_mac(A, c->N(), S(s));
     launched(c, "bsgs_mac_kernel");
+  });
+}
+
+int hx_bsgs_mac(hx_ctx* c, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,
+                int diag_limbs, int n1, int n2, int n_q, void* s) {
+  return hx_bsgs_mac_ex(c, inner, 2ll * n_q * (c ? c->N() : 0), baby, diags, diag_limbs, n1, n2, n_q, s);
+}
+
+int hx_sum_strided(hx_ctx* c, uint64_t* out, const uint64_t* in, int terms, long long term_stride,
+                   int polys, long long in_poly_stride, long long out_poly_stride, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    HX_REQUIRE(terms >= 1 && polys >= 1, "sum: terms, polys >= 1");
+    hx::SumArgs A;
+    A.out = (u64*)out;
+    A.in = (const u64*)in;
+    A.pc = c->d_pc;
+    A.terms = terms;
+    A.n_q = n_q;
+    A.logn = c->logn;
+    A.term_stride = term_stride;
+    A.in_poly_stride = in_poly_stride;
+    A.out_poly_stride = out_poly_stride;
+    hx::launch_sum(A, polys, c->N(), S(s));
+    launched(c, "sum_kernel");
   });
 }
 

@@ -23,7 +23,19 @@ struct MacArgs {
   const PrimeConst* pc;
   int n1, n2, n_q, logn;
   long long diag_stride;  // words between consecutive diagonals
+  long long out_jstride;  // words between inner_j and inner_{j+1} (2 n_q N when packed)
 };
+
+// out = sum_{r < terms} in + r * term_stride, per (poly, limb) of `polys`
+// polys of n_q limbs (ciphertext sums of the BSGS giant steps)
+struct SumArgs {
+  u64* out;
+  const u64* in;
+  const PrimeConst* pc;
+  int terms, n_q, logn;
+  long long term_stride, in_poly_stride, out_poly_stride;
+};
+void launch_sum(const SumArgs& A, int polys, long long N, cudaStream_t s);
 
 void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s);
 

@@ -12,8 +12,11 @@
 
 #include <algorithm>
 #include <cstring>
+#include <exception>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 #include "hx_b200.h"
 
@@ -244,13 +247,30 @@ std::vector<Plaintext> GpuLatticeBackend::encode_many(const std::vector<std::vec
   if (nz == 0) return out;
   auto buf = dev(nz * n * N);
   std::vector<std::int64_t> coeffs(nz * N);
+  std::vector<std::size_t> src;  // non-empty message indices
+  for (std::size_t i = 0; i < msgs.size(); ++i)
+    if (!msgs[i].empty()) src.push_back(i);
+  // host FFT encodes are independent: spread them over the host cores
+  const unsigned hw = std::max(1u, std::min(std::thread::hardware_concurrency(), 32u));
+  const std::size_t nt = std::min<std::size_t>(hw, src.size());
+  std::vector<std::thread> pool;
+  std::exception_ptr err;
+  std::mutex err_mu;
+  for (std::size_t w = 0; w < nt; ++w)
+    pool.emplace_back([&, w] {
+      try {
+        for (std::size_t k = w; k < src.size(); k += nt) {
+          const auto c = enc_.encode_coeffs(msgs[src[k]], level, scale.to_double());
+          std::memcpy(coeffs.data() + k * N, c.data(), N * 8);
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> g(err_mu);
+        err = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
   std::size_t idx = 0;
-  for (const auto& m : msgs) {
-    if (m.empty()) continue;
-    const auto c = enc_.encode_coeffs(m, level, scale.to_double());
-    std::memcpy(coeffs.data() + idx * N, c.data(), N * 8);
-    ++idx;
-  }
   DeviceBuffer dc(coeffs.size());
   cuda_ck(cudaMemcpyAsync(dc.ptr, coeffs.data(), coeffs.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
   ck(hx_from_i64(ctx_, buf->ptr, (const int64_t*)dc.ptr, (int)nz, n, 0, nullptr), "from_i64");
@@ -478,10 +498,18 @@ std::vector<Ciphertext> GpuLatticeBackend::rotate_many(const Ciphertext& a,
 
 Ciphertext GpuLatticeBackend::bsgs_block(const std::vector<Ciphertext>& baby,
                                          const std::vector<Plaintext>& diags, int n1, int n2) {
-  if ((int)baby.size() < n1 || (int)diags.size() < n1 * n2) throw std::invalid_argument("bsgs_block: shape");
+  return bsgs_blocks(baby, diags, n1, n2, 1).front();
+}
+
+std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphertext>& baby,
+                                                       const std::vector<Plaintext>& diags, int n1, int n2,
+                                                       int blocks) {
+  if ((int)baby.size() < n1 || (long long)diags.size() < (long long)n1 * n2 * blocks)
+    throw std::invalid_argument("bsgs_blocks: shape");
   const Ciphertext& x = baby[0];
   const int level = x.level, nqv = nq(level);
   const std::size_t N = params_.ring_degree, ctw = (std::size_t)2 * nqv * N, ptw = (std::size_t)nqv * N;
+  const std::size_t d = (std::size_t)n1 * n2;
   const auto n = (std::int64_t)slots();
   // baby steps contiguous [n1][2][n_q][N]
   std::shared_ptr<DeviceBuffer> bb;
@@ -503,120 +531,136 @@ Ciphertext GpuLatticeBackend::bsgs_block(const std::vector<Ciphertext>& baby,
       baby_ptr = bb->ptr;
     }
   }
-  // diagonals: gather the non-zero ones of each giant group, MAC per group
-  // (a group of all-zero diagonals contributes nothing and is skipped)
+  // inner sums, layout [n2][blocks][2][n_q][N] so giant step j of every block
+  // is one contiguous group (one key read for all blocks); dead groups stay 0
+  const std::size_t jstride = (std::size_t)blocks * ctw;
+  auto inner = dev((std::size_t)n2 * jstride);
+  cuda_ck(cudaMemsetAsync(inner->ptr, 0, inner->words * 8, nullptr), "memset");
   Scale dscale;
   bool have_scale = false;
-  auto inner = dev((std::size_t)n2 * ctw);
-  std::vector<int> live;
-  std::uint64_t ptmuls = 0, adds = 0;
-  bool all_contig = true;
-  {
-    const GpuPlaintext* p0 = diags[0].payload ? &payload(diags[0]) : nullptr;
-    for (std::size_t i = 0; i < (std::size_t)n1 * n2 && all_contig; ++i) {
-      if (!diags[i].payload || !p0) {
+  std::vector<std::vector<char>> live(blocks, std::vector<char>(n2, 0));
+  for (int b = 0; b < blocks; ++b) {
+    const Plaintext* D = diags.data() + (std::size_t)b * d;
+    std::uint64_t ptmuls = 0, adds = 0;
+    // fast path: the whole block dense and contiguous (encode_many) -> one MAC launch
+    bool all_contig = D[0].payload != nullptr;
+    const GpuPlaintext* p0 = all_contig ? &payload(D[0]) : nullptr;
+    for (std::size_t i = 0; i < d && all_contig; ++i) {
+      if (!D[i].payload) {
         all_contig = false;
         break;
       }
-      const auto& pi = payload(diags[i]);
-      all_contig = pi.buf == p0->buf && pi.offset == p0->offset + i * ptw && diags[i].level == level &&
-                   diags[i].scale == diags[0].scale;
+      const auto& pi = payload(D[i]);
+      all_contig = pi.buf == p0->buf && pi.offset == p0->offset + i * ptw && D[i].level == level &&
+                   D[i].scale == D[0].scale;
     }
     if (all_contig) {
-      dscale = diags[0].scale;
+      if (have_scale && D[0].scale != dscale) throw ScaleMismatchError("bsgs: diagonal scales differ");
+      dscale = D[0].scale;
       have_scale = true;
-      ck(hx_bsgs_mac(ctx_, inner->ptr, baby_ptr, p0->data(), nqv, n1, n2, nqv, nullptr), "bsgs_mac");
-      ptmuls = (std::uint64_t)n1 * n2;
-      adds = (std::uint64_t)(n1 - 1) * n2;
-      for (int j = 0; j < n2; ++j) live.push_back(j);
-    }
-  }
-  for (int j = 0; j < n2 && !all_contig; ++j) {
-    std::vector<int> ks;
-    for (int k = 0; k < n1; ++k) {
-      const Plaintext& pt = diags[(std::size_t)j * n1 + k];
-      if (!pt.payload) continue;
-      if (pt.level != level) throw LevelMismatchError("bsgs_block: diagonal level mismatch");
-      if (!have_scale) {
-        dscale = pt.scale;
-        have_scale = true;
-      } else if (pt.scale != dscale) {
-        throw ScaleMismatchError("bsgs_block: diagonal scales differ");
-      }
-      ks.push_back(k);
-    }
-    if (ks.empty()) continue;
-    ptmuls += ks.size();
-    adds += ks.size() - 1;
-    // contiguous run of this group's diagonals (the common case: encode_many)?
-    const auto& p0 = payload(diags[(std::size_t)j * n1 + ks[0]]);
-    bool dense_contig = (int)ks.size() == n1;
-    for (int k = 1; k < n1 && dense_contig; ++k) {
-      const auto& pk = payload(diags[(std::size_t)j * n1 + k]);
-      dense_contig = pk.buf == p0.buf && pk.offset == p0.offset + k * ptw;
-    }
-    if (dense_contig) {
-      ck(hx_bsgs_mac(ctx_, inner->ptr + j * ctw, baby_ptr, p0.data(), nqv, n1, 1, nqv, nullptr), "bsgs_mac");
-    } else {
-      // sparse group: gather its diagonals and the matching baby steps
-      DeviceBuffer dg(ks.size() * ptw), bs(ks.size() * ctw);
-      for (std::size_t i = 0; i < ks.size(); ++i) {
-        cuda_ck(cudaMemcpyAsync(dg.ptr + i * ptw, payload(diags[(std::size_t)j * n1 + ks[i]]).data(), ptw * 8,
-                                cudaMemcpyDeviceToDevice, nullptr), "d2d");
-        cuda_ck(cudaMemcpyAsync(bs.ptr + i * ctw, baby_ptr + ks[i] * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
-                                nullptr), "d2d");
-      }
-      ck(hx_bsgs_mac(ctx_, inner->ptr + j * ctw, bs.ptr, dg.ptr, nqv, (int)ks.size(), 1, nqv, nullptr),
+      ck(hx_bsgs_mac_ex(ctx_, inner->ptr + b * ctw, (long long)jstride, baby_ptr, p0->data(), nqv, n1, n2, nqv,
+                        nullptr),
          "bsgs_mac");
+      ptmuls = d;
+      adds = (std::uint64_t)(n1 - 1) * n2;
+      for (int j = 0; j < n2; ++j) live[b][j] = 1;
+    } else {
+      for (int j = 0; j < n2; ++j) {
+        std::vector<int> ks;
+        for (int k = 0; k < n1; ++k) {
+          const Plaintext& pt = D[(std::size_t)j * n1 + k];
+          if (!pt.payload) continue;
+          if (pt.level != level) throw LevelMismatchError("bsgs: diagonal level mismatch");
+          if (!have_scale) {
+            dscale = pt.scale;
+            have_scale = true;
+          } else if (pt.scale != dscale) {
+            throw ScaleMismatchError("bsgs: diagonal scales differ");
+          }
+          ks.push_back(k);
+        }
+        if (ks.empty()) continue;
+        ptmuls += ks.size();
+        adds += ks.size() - 1;
+        u64* dst = inner->ptr + j * jstride + b * ctw;
+        const auto& q0 = payload(D[(std::size_t)j * n1 + ks[0]]);
+        bool dense = (int)ks.size() == n1;
+        for (int k = 1; k < n1 && dense; ++k) {
+          const auto& pk = payload(D[(std::size_t)j * n1 + k]);
+          dense = pk.buf == q0.buf && pk.offset == q0.offset + k * ptw;
+        }
+        if (dense) {
+          ck(hx_bsgs_mac_ex(ctx_, dst, (long long)ctw, baby_ptr, q0.data(), nqv, n1, 1, nqv, nullptr), "bsgs_mac");
+        } else {  // sparse group: gather its diagonals and the matching baby steps
+          DeviceBuffer dg(ks.size() * ptw), bs(ks.size() * ctw);
+          for (std::size_t i = 0; i < ks.size(); ++i) {
+            cuda_ck(cudaMemcpyAsync(dg.ptr + i * ptw, payload(D[(std::size_t)j * n1 + ks[i]]).data(), ptw * 8,
+                                    cudaMemcpyDeviceToDevice, nullptr), "d2d");
+            cuda_ck(cudaMemcpyAsync(bs.ptr + i * ctw, baby_ptr + ks[i] * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
+                                    nullptr), "d2d");
+          }
+          ck(hx_bsgs_mac_ex(ctx_, dst, (long long)ctw, bs.ptr, dg.ptr, nqv, (int)ks.size(), 1, nqv, nullptr),
+             "bsgs_mac");
+        }
+        live[b][j] = 1;
+      }
     }
-    live.push_back(j);
+    bool any = false;
+    for (int j = 0; j < n2; ++j) any |= live[b][j] != 0;
+    if (!any) throw std::invalid_argument("matvec_bsgs: block has no non-zero diagonal");
+    trace_.record(OpKind::PtMul, level, ptmuls);
+    if (adds) trace_.record(OpKind::CtAdd, level, adds);
   }
-  if (live.empty()) throw std::invalid_argument("bsgs_block: all diagonals are zero");
-  trace_.record(OpKind::PtMul, level, ptmuls);
-  if (adds) trace_.record(OpKind::CtAdd, level, adds);
   const Scale out_scale = x.scale * dscale;
-  // giant steps: rotate every live group j >= 1 by n1 j (one batched ModUp)
+  // giant steps j >= 1: rotate group j of every block by n1 j with one key
   std::vector<const u64*> keys;
   std::vector<u64> gs;
-  std::vector<int> rot_j;
-  for (int j : live) {
-    if (j == 0) continue;
+  std::vector<int> J;
+  for (int j = 1; j < n2; ++j) {
+    bool any = false;
+    for (int b = 0; b < blocks; ++b) any |= live[b][j] != 0;
+    if (!any) continue;
     const std::int64_t r = detail::reduce_amount((std::int64_t)n1 * j, n);
-    if (r == 0) continue;
     const u64* key = rotation_key(r);
     if (!rot_set_.contains(r) || !key) throw MissingRotationKeyError("rotate: no key for amount " + std::to_string(r));
     keys.push_back(key);
     gs.push_back(galois(r));
-    rot_j.push_back(j);
+    J.push_back(j);
   }
-  std::shared_ptr<DeviceBuffer> rotated;
-  if (!keys.empty()) {
-    DeviceBuffer src(keys.size() * ctw);
-    for (std::size_t i = 0; i < rot_j.size(); ++i)
-      cuda_ck(cudaMemcpyAsync(src.ptr + i * ctw, inner->ptr + rot_j[i] * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
-                              nullptr), "d2d");
-    rotated = dev(keys.size() * ctw);
-    ck(hx_rotate_multi(ctx_, rotated->ptr, src.ptr, keys.data(), gs.data(), (int)keys.size(), nqv, nullptr),
-       "rotate_multi");
-    trace_.record(OpKind::Rotate, level, keys.size());
-  }
-  // accumulate: acc = sum of live groups (rotated where j >= 1)
-  auto acc = dev(ctw);
-  std::size_t ri = 0;
-  bool first = true;
-  for (int j : live) {
-    const u64* term = (j == 0 || rot_j.empty() || ri >= rot_j.size() || rot_j[ri] != j)
-                          ? inner->ptr + j * ctw
-                          : rotated->ptr + (ri++) * ctw;
-    if (first) {
-      cuda_ck(cudaMemcpyAsync(acc->ptr, term, ctw * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
-      first = false;
-    } else {
-      ck(hx_add(ctx_, acc->ptr, acc->ptr, term, 2, nqv, 0, nullptr), "add");
+  auto out = dev((std::size_t)blocks * ctw);
+  if (!J.empty()) {
+    std::shared_ptr<DeviceBuffer> src;
+    const u64* srcp = inner->ptr + jstride;  // groups 1..n2-1 are contiguous
+    if ((int)J.size() != n2 - 1) {
+      src = dev(J.size() * jstride);
+      for (std::size_t i = 0; i < J.size(); ++i)
+        cuda_ck(cudaMemcpyAsync(src->ptr + i * jstride, inner->ptr + J[i] * jstride, jstride * 8,
+                                cudaMemcpyDeviceToDevice, nullptr), "d2d");
+      srcp = src->ptr;
     }
+    auto rotated = dev(J.size() * jstride);
+    ck(hx_rotate_grouped(ctx_, rotated->ptr, srcp, keys.data(), gs.data(), (int)J.size(), blocks, nqv, nullptr),
+       "rotate_grouped");
+    // y_b = inner_0,b + sum_j Rot(inner_j,b): rotated terms summed in one pass
+    ck(hx_sum_strided(ctx_, out->ptr, rotated->ptr, (int)J.size(), (long long)jstride, 2 * blocks,
+                      (long long)ptw, (long long)ptw, nqv, nullptr),
+       "sum");
+    ck(hx_add(ctx_, out->ptr, out->ptr, inner->ptr, 2 * blocks, nqv, 0, nullptr), "add");
+  } else {
+    cuda_ck(cudaMemcpyAsync(out->ptr, inner->ptr, jstride * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
   }
-  if (live.size() > 1) trace_.record(OpKind::CtAdd, level, live.size() - 1);
-  return wrap(acc, 0, level, out_scale);
+  std::vector<Ciphertext> res;
+  for (int b = 0; b < blocks; ++b) {
+    std::uint64_t nl = 0, nr = 0;
+    for (int j = 0; j < n2; ++j) {
+      nl += live[b][j] != 0;
+      nr += (j > 0 && live[b][j] != 0);
+    }
+    if (nr) trace_.record(OpKind::Rotate, level, nr);
+    if (nl > 1) trace_.record(OpKind::CtAdd, level, nl - 1);
+    res.push_back(wrap(out, (std::size_t)b * ctw, level, out_scale));
+  }
+  return res;
 }
 
 }  // namespace helix

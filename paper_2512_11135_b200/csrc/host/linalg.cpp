@@ -98,8 +98,6 @@ MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext&
   MatvecResult R;
 #ifndef HELIX_NO_GPU
   auto* gpu = dynamic_cast<GpuLatticeBackend*>(&ops);
-#else
-  SlotOps* gpu = nullptr;
 #endif
   // baby steps Rot(x, k), k < n1, shared by every row block
   std::vector<Ciphertext> baby;
@@ -114,15 +112,18 @@ MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext&
     baby.push_back(x);
     for (int k = 1; k < n1; ++k) baby.push_back(ops.rotate(x, k));
   }
+#ifndef HELIX_NO_GPU
+  if (gpu) {
+    for (const auto& acc : gpu->bsgs_blocks(baby, M.pts, n1, n2, M.meta.row_blocks))
+      R.outputs.push_back(ops.rescale(acc));
+    R.report = report_since(ops.trace(), snap, x.level, R.outputs.front());
+    return R;
+  }
+#endif
   for (int b = 0; b < M.meta.row_blocks; ++b) {
     const std::vector<Plaintext> diags(M.pts.begin() + (std::ptrdiff_t)b * d,
                                        M.pts.begin() + (std::ptrdiff_t)(b + 1) * d);
     Ciphertext acc;
-#ifndef HELIX_NO_GPU
-    if (gpu) {
-      acc = gpu->bsgs_block(baby, diags, n1, n2);
-    } else
-#endif
     {
       std::optional<Ciphertext> sum;
       for (int j = 0; j < n2; ++j) {

@@ -50,5 +50,30 @@ def main():
     print("ok", mode, ctx.launches())
 
 
+
+
+def ffn(prune=False):
+    """one config-3 W1 BSGS matvec (after a warm-up matvec) through the helix C-ABI"""
+    import numpy as np
+
+    from paper_2512_11135_b200.helix import BSGS, Backend, params_json
+
+    chain, special = bench.primes()
+    be = Backend(params_json(bench.LOGN, chain, special, bench.ALPHA, 40), seed=3)
+    rng = np.random.default_rng(3)
+    M = rng.normal(0, 0.02, (3072, 768))
+    mat = be.prepare(BSGS, M, be.max_level)
+    be.gen_rotation_keys(mat.rotations())
+    x = np.tile(np.concatenate([rng.uniform(-1, 1, 768), np.zeros(256)]), be.slots // 1024)
+    ct = be.encrypt(x)
+    for _ in range(2):
+        outs, rep = be.matvec(mat, ct)
+    torch.cuda.synchronize()
+    print("ok ffn", rep)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "ffn":
+        ffn()
+    else:
+        main()
