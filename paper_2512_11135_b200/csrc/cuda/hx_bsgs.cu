@@ -17,7 +17,7 @@ template <int TT>
 __global__ void __launch_bounds__(TT) bsgs_mac_kernel(MacArgs A) {
   extern __shared__ u64 smb[];  // [n1][2][TT]
   const long long N = 1ll << A.logn;
-  const int i = blockIdx.y;
+  const int i = A.limbs ? A.limbs[blockIdx.y] : blockIdx.y;
   const int tid = threadIdx.x;
   const long long t = (long long)blockIdx.x * TT + tid;
   const PrimeConst& P = A.pc[i];
@@ -32,6 +32,19 @@ __global__ void __launch_bounds__(TT) bsgs_mac_kernel(MacArgs A) {
     U128 z0{0, 0}, z1{0, 0};
     const u64* dj = dg + (long long)j * A.n1 * A.diag_stride;
     int k = 0;
+    // 16 independent diagonal loads in flight per thread (the CTA count per SM
+    // is bounded by the baby tile in shared memory, so memory-level
+    // parallelism has to come from each thread)
+    for (; k + 16 <= A.n1; k += 16) {
+      u64 d[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) d[u] = __ldcs(dj + (long long)(k + u) * A.diag_stride);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        mac128(z0, d[u], smb[(2 * (k + u)) * TT + tid]);
+        mac128(z1, d[u], smb[(2 * (k + u) + 1) * TT + tid]);
+      }
+    }
     for (; k + 8 <= A.n1; k += 8) {
       u64 d[8];
 #pragma unroll
@@ -53,19 +66,203 @@ __global__ void __launch_bounds__(TT) bsgs_mac_kernel(MacArgs A) {
   }
 }
 
-void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s) {
+// ---------------------------------------------------------------------------
+// FP64 k-split MAC for limbs with q < 2^43 (B200's full-rate FP64 pipe).
+//
+// Operands are canonical residues x, y < q; split at 20 bits,
+// x = x1 2^20 + x0 (x1 < q / 2^20, x0 < 2^20), and
+//   sum_k x_k y_k = S11 2^40 + S10 2^20 + S00,
+//   S11 = sum x1 y1 < n1 q^2 / 2^40,  S10 = sum (x1 y0 + x0 y1) < 2 n1 q,
+//   S00 = sum x0 y0 < n1 2^40,
+// all integers below 2^52 for q < 2^43 and n1 <= 64, so every FMA and the
+// cross-warp sums are exact in doubles.  A CTA is
+// 8 warps x 32 coefficients of one limb: warp w owns baby steps
+// k in [w KPT, (w+1) KPT) in registers (split into doubles once), streams its
+// diagonal words (evict-first, next giant step prefetched), and the 8 warps'
+// partial sums are combined through shared memory (double-buffered, one
+// barrier per giant step); the combine is one exact modular reduction per
+// output word.  Bit-identical to the integer kernel.
+constexpr int kMacWarps = 8;
+
+__device__ __forceinline__ void split20(u64 v, double& hi, double& lo) {
+  hi = __dsub_rn(__longlong_as_double((long long)((v >> 20) | 0x4330000000000000ull)), kTwo52);
+  lo = __dsub_rn(__longlong_as_double((long long)((v & 0xFFFFFull) | 0x4330000000000000ull)), kTwo52);
+}
+
+template <int KPT>
+__global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_f64_kernel(MacArgs A, const int* limbs) {
+  __shared__ double part[2][kMacWarps][2][3][32];  // [buf][warp][poly][S11,S10,S00][lane]
+  const long long N = 1ll << A.logn;
+  const int i = limbs[blockIdx.y];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t = (long long)blockIdx.x * 32 + lane;
+  const PrimeConst& P = A.pc[i];
+  const long long L = (long long)A.n_q * N;
+  // baby words of this warp's k slice, split into 20-bit halves
+  double bh[KPT][2], bl[KPT][2];
+#pragma unroll
+  for (int kk = 0; kk < KPT; ++kk) {
+    const int k = w * KPT + kk;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) split20(A.baby[(2ll * k + c) * L + i * N + t], bh[kk][c], bl[kk][c]);
+  }
+  const u64* dg = A.diags + i * N + t + (long long)(w * KPT) * A.diag_stride;
+  u64 dn[KPT];
+#pragma unroll
+  for (int kk = 0; kk < KPT; ++kk) dn[kk] = __ldcs(dg + (long long)kk * A.diag_stride);
+  // 2^40 mod q and 2^20 mod q for the final combine
+  const double r20 = (double)((1ull << 20) % P.q);
+  const double r40 = (double)((1ull << 40) % P.q);
+  for (int j = 0; j < A.n2; ++j) {
+    u64 d[KPT];
+#pragma unroll
+    for (int kk = 0; kk < KPT; ++kk) d[kk] = dn[kk];
+    if (j + 1 < A.n2) {
+      const u64* dj = dg + (long long)(j + 1) * A.n1 * A.diag_stride;
+#pragma unroll
+      for (int kk = 0; kk < KPT; ++kk) dn[kk] = __ldcs(dj + (long long)kk * A.diag_stride);
+    }
+    double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+    for (int kk = 0; kk < KPT; ++kk) {
+      double xh, xl;
+      split20(d[kk], xh, xl);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        s[c][0] = __fma_rn(xh, bh[kk][c], s[c][0]);
+        s[c][1] = __fma_rn(xh, bl[kk][c], s[c][1]);
+        s[c][1] = __fma_rn(xl, bh[kk][c], s[c][1]);
+        s[c][2] = __fma_rn(xl, bl[kk][c], s[c][2]);
+      }
+    }
+    const int buf = j & 1;
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) part[buf][w][c][m][lane] = s[c][m];
+    __syncthreads();
+    if (threadIdx.x < 64) {  // warps 0-1: (poly c, lane) reductions
+      const int c = threadIdx.x >> 5;
+      double S[3] = {0, 0, 0};
+#pragma unroll
+      for (int ww = 0; ww < kMacWarps; ++ww)
+#pragma unroll
+        for (int m = 0; m < 3; ++m) S[m] = __dadd_rn(S[m], part[buf][ww][c][m][lane]);
+      // S11 2^40 + S10 2^20 + S00 mod q (each S exact, < 2^52)
+      const double v = __dadd_rn(__dadd_rn(mulmod_f64(S[0], r40, __dmul_rn(r40, P.qinv_d), P.qd),
+                                           mulmod_f64(S[1], r20, __dmul_rn(r20, P.qinv_d), P.qd)),
+                                 centre_f64(S[2], P.qd, P.qinv_d));
+      A.inner[(long long)j * A.out_jstride + c * L + i * N + t] =
+          f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);
+    }
+  }
+}
+
+// Integer twin of the k-split kernel for the wide primes (q >= 2^43, e.g. the
+// 60-bit q_0): same CTA shape and double-buffered cross-warp combine, 128-bit
+// lazy accumulators (products < 2^120, n1 <= 64 terms), one reduction per output.
+template <int KPT>
+__global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_int_kernel(MacArgs A, const int* limbs) {
+  __shared__ u64 part[2][kMacWarps][2][2][32];  // [buf][warp][poly][lo,hi][lane]
+  const long long N = 1ll << A.logn;
+  const int i = limbs[blockIdx.y];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t = (long long)blockIdx.x * 32 + lane;
+  const PrimeConst& P = A.pc[i];
+  const long long L = (long long)A.n_q * N;
+  u64 b[KPT][2];
+#pragma unroll
+  for (int kk = 0; kk < KPT; ++kk) {
+    const int k = w * KPT + kk;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) b[kk][c] = A.baby[(2ll * k + c) * L + i * N + t];
+  }
+  const u64* dg = A.diags + i * N + t + (long long)(w * KPT) * A.diag_stride;
+  u64 dn[KPT];
+#pragma unroll
+  for (int kk = 0; kk < KPT; ++kk) dn[kk] = __ldcs(dg + (long long)kk * A.diag_stride);
+  for (int j = 0; j < A.n2; ++j) {
+    u64 d[KPT];
+#pragma unroll
+    for (int kk = 0; kk < KPT; ++kk) d[kk] = dn[kk];
+    if (j + 1 < A.n2) {
+      const u64* dj = dg + (long long)(j + 1) * A.n1 * A.diag_stride;
+#pragma unroll
+      for (int kk = 0; kk < KPT; ++kk) dn[kk] = __ldcs(dj + (long long)kk * A.diag_stride);
+    }
+    U128 z[2] = {{0, 0}, {0, 0}};
+#pragma unroll
+    for (int kk = 0; kk < KPT; ++kk)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) mac128(z[c], d[kk], b[kk][c]);
+    const int buf = j & 1;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      part[buf][w][c][0][lane] = z[c].lo;
+      part[buf][w][c][1][lane] = z[c].hi;
+    }
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      const int c = threadIdx.x >> 5;
+      U128 S{0, 0};
+#pragma unroll
+      for (int ww = 0; ww < kMacWarps; ++ww) {
+        asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;"
+            : "+l"(S.lo), "+l"(S.hi)
+            : "l"(part[buf][ww][c][0][lane]), "l"(part[buf][ww][c][1][lane]));
+      }
+      A.inner[(long long)j * A.out_jstride + c * L + i * N + t] = reduce128(S, P);
+    }
+  }
+}
+
+namespace {
+template <class K>
+void set_max_smem(K kernel, int bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+}  // namespace
+
+void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s, const int* d_f64_limbs, int n_f64,
+                     const int* d_int_limbs, int n_int) {
   constexpr int TT = 128;
-  const int tt = (int)(N < TT ? N : TT);
-  const size_t smem = (size_t)A.n1 * 2 * TT * sizeof(u64);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(bsgs_mac_kernel<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         64 * 2 * TT * (int)sizeof(u64));
+    set_max_smem(bsgs_mac_kernel<TT>, 64 * 2 * TT * (int)sizeof(u64));
     configured = true;
   }
-  (void)tt;
-  dim3 grid((unsigned)(N / TT), (unsigned)A.n_q);
-  bsgs_mac_kernel<TT><<<grid, TT, smem, s>>>(A);
+  const int kpt = A.n1 / kMacWarps;
+  const bool f64_ok = n_f64 > 0 && N >= 32 && A.n1 % kMacWarps == 0 && (kpt == 1 || kpt == 2 || kpt == 4 || kpt == 8);
+  if (f64_ok) {
+    dim3 grid((unsigned)(N / 32), (unsigned)n_f64);
+    switch (kpt) {
+      case 1: bsgs_mac_f64_kernel<1><<<grid, 32 * kMacWarps, 0, s>>>(A, d_f64_limbs); break;
+      case 2: bsgs_mac_f64_kernel<2><<<grid, 32 * kMacWarps, 0, s>>>(A, d_f64_limbs); break;
+      case 4: bsgs_mac_f64_kernel<4><<<grid, 32 * kMacWarps, 0, s>>>(A, d_f64_limbs); break;
+      case 8: bsgs_mac_f64_kernel<8><<<grid, 32 * kMacWarps, 0, s>>>(A, d_f64_limbs); break;
+    }
+  }
+  // integer k-split kernel for the wide primes
+  if (f64_ok && n_int > 0) {
+    dim3 grid((unsigned)(N / 32), (unsigned)n_int);
+    switch (kpt) {
+      case 1: bsgs_mac_int_kernel<1><<<grid, 32 * kMacWarps, 0, s>>>(A, d_int_limbs); break;
+      case 2: bsgs_mac_int_kernel<2><<<grid, 32 * kMacWarps, 0, s>>>(A, d_int_limbs); break;
+      case 4: bsgs_mac_int_kernel<4><<<grid, 32 * kMacWarps, 0, s>>>(A, d_int_limbs); break;
+      case 8: bsgs_mac_int_kernel<8><<<grid, 32 * kMacWarps, 0, s>>>(A, d_int_limbs); break;
+    }
+    return;
+  }
+  // generic smem-tile kernel (n1 not a multiple of 8, tiny N): all limbs
+  const int* il = nullptr;
+  const int ni = A.n_q;
+  if (ni > 0) {
+    const size_t smem = (size_t)A.n1 * 2 * TT * sizeof(u64);
+    MacArgs B = A;
+    B.limbs = il;
+    dim3 grid((unsigned)(N / TT), (unsigned)ni);
+    bsgs_mac_kernel<TT><<<grid, TT, smem, s>>>(B);
+  }
 }
 
 // out[p][i][t] = sum_r in[r][p][i][t] mod q_i

@@ -23,6 +23,9 @@ struct hx_ctx {
   double* d_twf = nullptr;     // FP64-path twiddles [n_total][2][N] (w as double)
   std::vector<char> f64;       // prime index -> NTT on the FP64 pipe (q < 2^47)
   bool allow_f64 = true;       // HX_NTT_INT=1 forces the integer path (A/B tests)
+  // BSGS MAC limb lists per n_q: [n_q][2][n_chain] ints (FP64 list, integer list)
+  int* d_maclimbs = nullptr;
+  std::vector<int> mac_nf64, mac_nint;
   // ModUp constants: for each n_q in [1, n_chain] and digit d < dnum(n_q):
   // qhinv [alpha] and conv [alpha][n_total]; offsets in units of SC.
   hx::SC* d_modup = nullptr;

@@ -165,13 +165,30 @@ __global__ void modup_bconv_kernel(ModUpArgs A) {
   const long long b = blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const u64* cb = A.coef + b * (long long)A.n_q * N;
+  // FP64 pipe when every source prime of the digit and the target prime are
+  // < 2^47 (exact double arithmetic, hx_ntt.cuh); integer Shoup otherwise
+  bool src_f64 = true;
+#pragma unroll
+  for (int i = 0; i < MAXA; ++i)
+    if (i < A.cnt) src_f64 = src_f64 && A.pc[A.lo + i].f64;
   u64 x[MAXA];
+  double xd[MAXA];
 #pragma unroll
   for (int i = 0; i < MAXA; ++i) {
     if (i < A.cnt) {
       const PrimeConst& P = A.pc[A.lo + i];
       const SC c = A.qhinv[i];
-      x[i] = csub(shoup_lazy(cb[(long long)(A.lo + i) * N + t], c.w, c.wp, P.q), P.q);
+      const u64 a = cb[(long long)(A.lo + i) * N + t];
+      if (src_f64) {
+        const double w = __longlong_as_double((long long)u64_to_f64bits(c.w));
+        const double v = mulmod_f64(__longlong_as_double((long long)u64_to_f64bits(a)), w,
+                                    __dmul_rn(w, P.qinv_d), P.qd);
+        x[i] = f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);  // canonical [0, q)
+        xd[i] = __longlong_as_double((long long)u64_to_f64bits(x[i]));
+      } else {
+        x[i] = csub(shoup_lazy(a, c.w, c.wp, P.q), P.q);
+        xd[i] = 0.0;
+      }
     }
   }
   u64* ob = A.out + b * A.out_stride;
@@ -180,15 +197,27 @@ __global__ void modup_bconv_kernel(ModUpArgs A) {
     if (j >= A.lo && j < A.lo + A.cnt) continue;
     const int pj = j < A.n_q ? j : A.n_chain + (j - A.n_q);
     const PrimeConst& P = A.pc[pj];
-    u64 y = 0;
+    if (src_f64 && P.f64) {
+      double acc = 0.0;  // |acc| < cnt q: exact
 #pragma unroll
-    for (int i = 0; i < MAXA; ++i) {
-      if (i < A.cnt) {
-        const SC c = A.conv[i * A.n_total + pj];
-        y = csub(y + shoup_lazy(x[i], c.w, c.wp, P.q), P.two_q);
+      for (int i = 0; i < MAXA; ++i) {
+        if (i < A.cnt) {
+          const double w = __longlong_as_double((long long)u64_to_f64bits(A.conv[i * A.n_total + pj].w));
+          acc = __dadd_rn(acc, mulmod_f64(xd[i], w, __dmul_rn(w, P.qinv_d), P.qd));
+        }
       }
+      ob[(long long)j * N + t] = f64bits_to_residue((u64)__double_as_longlong(acc), P.qd, P.qinv_d);
+    } else {
+      u64 y = 0;
+#pragma unroll
+      for (int i = 0; i < MAXA; ++i) {
+        if (i < A.cnt) {
+          const SC c = A.conv[i * A.n_total + pj];
+          y = csub(y + shoup_lazy(x[i], c.w, c.wp, P.q), P.two_q);
+        }
+      }
+      ob[(long long)j * N + t] = csub(y, P.q);
     }
-    ob[(long long)j * N + t] = csub(y, P.q);
   }
 }
 

@@ -687,6 +687,21 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
       }
     c->d_qlinv = upload(qlinv);
     c->d_qlmod = upload(qlmod);
+    // BSGS MAC limb classes: FP64 k-split kernel for q < 2^43, integer otherwise
+    std::vector<int> ml((size_t)(n_chain + 1) * 2 * n_chain, 0);
+    c->mac_nf64.assign(n_chain + 1, 0);
+    c->mac_nint.assign(n_chain + 1, 0);
+    for (int nq = 1; nq <= n_chain; ++nq) {
+      int* f = ml.data() + (size_t)nq * 2 * n_chain;
+      int* g = f + n_chain;
+      for (int i = 0; i < nq; ++i) {
+        if (c->allow_f64 && c->primes[i] < (1ull << 43))
+          f[c->mac_nf64[nq]++] = i;
+        else
+          g[c->mac_nint[nq]++] = i;
+      }
+    }
+    c->d_maclimbs = upload(ml);
     out = c.release();
   });
   return rc == HX_OK ? out : nullptr;
@@ -696,7 +711,7 @@ void hx_ctx_destroy(hx_ctx* c) {
   if (!c) return;
   for (void* p : {(void*)c->d_pc, (void*)c->d_tw, (void*)c->d_twf, (void*)c->d_modup, (void*)c->d_phinv,
                   (void*)c->d_pconv, (void*)c->d_pmodq, (void*)c->d_pinv, (void*)c->d_qlinv,
-                  (void*)c->d_qlmod})
+                  (void*)c->d_qlmod, (void*)c->d_maclimbs})
     if (p) cudaFree(p);
   delete c;
 }
@@ -999,8 +1014,10 @@ int hx_bsgs_mac_ex(hx_ctx* c, uint64_t* inner, long long inner_jstride, const ui
     A.logn = c->logn;
     A.diag_stride = (long long)diag_limbs * c->N();
     A.out_jstride = inner_jstride;
-    hx::launch_bsgs_mac(A, c->N(), S(s));
-    launched(c, "bsgs_mac_kernel");
+    A.limbs = nullptr;
+    const int* lists = c->d_maclimbs + (size_t)n_q * 2 * c->n_chain;
+    hx::launch_bsgs_mac(A, c->N(), S(s), lists, c->mac_nf64[n_q], lists + c->n_chain, c->mac_nint[n_q]);
+    launched(c, "bsgs_mac_kernel", 2);
   });
 }
 

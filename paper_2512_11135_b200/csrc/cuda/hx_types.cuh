@@ -24,6 +24,7 @@ struct MacArgs {
   int n1, n2, n_q, logn;
   long long diag_stride;  // words between consecutive diagonals
   long long out_jstride;  // words between inner_j and inner_{j+1} (2 n_q N when packed)
+  const int* limbs;       // device limb list for blockIdx.y (null: identity)
 };
 
 // out = sum_{r < terms} in + r * term_stride, per (poly, limb) of `polys`
@@ -37,6 +38,9 @@ struct SumArgs {
 };
 void launch_sum(const SumArgs& A, int polys, long long N, cudaStream_t s);
 
-void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s);
+// d_f64_limbs / d_int_limbs: device lists of the limbs (of 0..n_q-1) whose
+// primes take the FP64 k-split kernel (q < 2^43) / the integer kernel
+void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s, const int* d_f64_limbs, int n_f64,
+                     const int* d_int_limbs, int n_int);
 
 }  // namespace hx
