@@ -110,9 +110,6 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_f64_kernel(MacArgs A,
   u64 dn[KPT];
 #pragma unroll
   for (int kk = 0; kk < KPT; ++kk) dn[kk] = __ldcs(dg + (long long)kk * A.diag_stride);
-  // 2^40 mod q and 2^20 mod q for the final combine
-  const double r20 = (double)((1ull << 20) % P.q);
-  const double r40 = (double)((1ull << 40) % P.q);
   for (int j = 0; j < A.n2; ++j) {
     u64 d[KPT];
 #pragma unroll
@@ -149,8 +146,8 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_f64_kernel(MacArgs A,
 #pragma unroll
         for (int m = 0; m < 3; ++m) S[m] = __dadd_rn(S[m], part[buf][ww][c][m][lane]);
       // S11 2^40 + S10 2^20 + S00 mod q (each S exact, < 2^52)
-      const double v = __dadd_rn(__dadd_rn(mulmod_f64(S[0], r40, __dmul_rn(r40, P.qinv_d), P.qd),
-                                           mulmod_f64(S[1], r20, __dmul_rn(r20, P.qinv_d), P.qd)),
+      const double v = __dadd_rn(__dadd_rn(mulmod_f64(S[0], P.r40_d, P.r40_q, P.qd),
+                                           mulmod_f64(S[1], P.r20_d, P.r20_q, P.qd)),
                                  centre_f64(S[2], P.qd, P.qinv_d));
       A.inner[(long long)j * A.out_jstride + c * L + i * N + t] =
           f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);

@@ -36,6 +36,8 @@ struct PrimeConst {
   double qd, qinv_d;         // q, 1/q
   double ninv_d, ninv_q;     // N^-1, N^-1 / q
   double w1n_d, w1n_q;       // last-stage twiddle * N^-1, / q
+  double r20_d, r20_q;       // 2^20 mod q (and / q): 20-bit split MAC combine
+  double r40_d, r40_q;       // 2^40 mod q
   const double* twf_fwd;     // w as double (w / q formed in-kernel)
   const double* twf_inv;
 };

@@ -26,6 +26,9 @@ struct hx_ctx {
   // BSGS MAC limb lists per n_q: [n_q][2][n_chain] ints (FP64 list, integer list)
   int* d_maclimbs = nullptr;
   std::vector<int> mac_nf64, mac_nint;
+  // key inner-product limb lists over the n_q + K limbs: [n_q][2][n_total]
+  int* d_kslimbs = nullptr;
+  std::vector<int> ks_nf64, ks_nint;
   // ModUp constants: for each n_q in [1, n_chain] and digit d < dnum(n_q):
   // qhinv [alpha] and conv [alpha][n_total]; offsets in units of SC.
   hx::SC* d_modup = nullptr;

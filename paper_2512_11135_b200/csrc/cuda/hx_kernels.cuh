@@ -243,11 +243,77 @@ struct InnerArgs {
   int logn;
 };
 
+// FP64 variant for limbs with q < 2^43: the key words are split once into
+// 20-bit halves held as doubles, every digit word is split on load, and the
+// dnum-term inner product is accumulated exactly as S11 2^40 + S10 2^20 + S00
+// (see the BSGS MAC in hx_bsgs.cu for the bounds) on the FP64 pipe; one exact
+// modular combine per output word.  `limbs` lists the limbs j of this class.
+__device__ __forceinline__ void split20_d(u64 v, double& hi, double& lo) {
+  hi = __dsub_rn(__longlong_as_double((long long)((v >> 20) | 0x4330000000000000ull)), kTwo52);
+  lo = __dsub_rn(__longlong_as_double((long long)((v & 0xFFFFFull) | 0x4330000000000000ull)), kTwo52);
+}
+
+__device__ __forceinline__ u64 combine_split(const double (&s)[3], const PrimeConst& P) {
+  const double v = __dadd_rn(__dadd_rn(mulmod_f64(s[0], P.r40_d, P.r40_q, P.qd),
+                                       mulmod_f64(s[1], P.r20_d, P.r20_q, P.qd)),
+                             centre_f64(s[2], P.qd, P.qinv_d));
+  return f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);
+}
+
 template <int MAXD>
-__global__ void __launch_bounds__(256, 2) ks_inner_kernel(InnerArgs A) {
+__global__ void __launch_bounds__(256, 2) ks_inner_f64_kernel(InnerArgs A, const int* limbs) {
   const int N = 1 << A.logn;
   const int ext = A.n_q + A.n_special, full = A.n_chain + A.n_special;
-  const int j = blockIdx.y;
+  const int j = limbs[blockIdx.y];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int kl = j < A.n_q ? j : A.n_chain + (j - A.n_q);
+  const int r = blockIdx.z / A.slices, slice = blockIdx.z % A.slices;
+  const u64* key = A.keys[r];
+  const int E = A.batch;
+  const PrimeConst& P = A.pc[kl];
+  double kh[MAXD][2], klo[MAXD][2];
+#pragma unroll
+  for (int d = 0; d < MAXD; ++d)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const u64 kw = d < A.dnum ? __ldg(key + (((long long)d * 2 + c) * full + kl) * N + t) : 0ull;
+      split20_d(kw, kh[d][c], klo[d][c]);
+    }
+  const int src = (A.g == 1) ? t : (int)ntt_auto_index((u32)t, A.g, A.logn);
+  const int per = (E + A.slices - 1) / A.slices;
+  const int b_lo = slice * per, b_hi = min(E, b_lo + per);
+  const long long dstride = (long long)A.dnum * ext * N;
+  const long long ebase = A.shared ? 0 : (long long)r * E;
+  u64* ubase = A.u + (long long)r * E * 2 * ext * N;
+  for (int b = b_lo; b < b_hi; ++b) {
+    const u64* Db = A.digits + (ebase + b) * dstride + (long long)j * N + src;
+    u64 v[MAXD];
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) v[d] = d < A.dnum ? __ldcs(Db + (long long)d * ext * N) : 0ull;
+    double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) {
+      double xh, xl;
+      split20_d(v[d], xh, xl);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        s[c][0] = __fma_rn(xh, kh[d][c], s[c][0]);
+        s[c][1] = __fma_rn(xh, klo[d][c], s[c][1]);
+        s[c][1] = __fma_rn(xl, kh[d][c], s[c][1]);
+        s[c][2] = __fma_rn(xl, klo[d][c], s[c][2]);
+      }
+    }
+    u64* ub = ubase + (long long)b * 2 * ext * N + (long long)j * N + t;
+    ub[0] = combine_split(s[0], P);
+    ub[(long long)ext * N] = combine_split(s[1], P);
+  }
+}
+
+template <int MAXD>
+__global__ void __launch_bounds__(256, 2) ks_inner_kernel(InnerArgs A, const int* limbs) {
+  const int N = 1 << A.logn;
+  const int ext = A.n_q + A.n_special, full = A.n_chain + A.n_special;
+  const int j = limbs ? limbs[blockIdx.y] : blockIdx.y;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int kl = j < A.n_q ? j : A.n_chain + (j - A.n_q);
   const int r = blockIdx.z / A.slices, slice = blockIdx.z % A.slices;

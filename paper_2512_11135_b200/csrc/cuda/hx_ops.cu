@@ -266,18 +266,35 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
   // split each key's elements over slices: more CTAs in flight, the key words
   // of a (limb, coefficient) are re-read only once per slice
   A.slices = (int)std::max<long long>(1, std::min<long long>(E / 16, 8));
-  dim3 grid((unsigned)(c->N() / th), (unsigned)(n_q + c->n_special), (unsigned)(A.n_keys * A.slices));
-  if (A.dnum <= 4)
-    hx::ks_inner_kernel<4><<<grid, th, 0, s>>>(A);
-  else if (A.dnum <= 8)
-    hx::ks_inner_kernel<8><<<grid, th, 0, s>>>(A);
-  else if (A.dnum <= 16)
-    hx::ks_inner_kernel<16><<<grid, th, 0, s>>>(A);
-  else if (A.dnum <= 32)
-    hx::ks_inner_kernel<32><<<grid, th, 0, s>>>(A);
-  else
-    hx::ks_inner_kernel<64><<<grid, th, 0, s>>>(A);
-  launched(c, "ks_inner_kernel");
+  const unsigned gz = (unsigned)(A.n_keys * A.slices);
+  // limbs with q < 2^43 take the FP64 split-MAC kernel (dnum <= 8), the rest
+  // (60-bit q_0 and special primes) the 128-bit integer kernel
+  const int* lists = c->d_kslimbs + (size_t)n_q * 2 * c->n_total();
+  const int nf = A.dnum <= 8 ? c->ks_nf64[n_q] : 0;
+  const int ni = A.dnum <= 8 ? c->ks_nint[n_q] : n_q + c->n_special;
+  const int* il = A.dnum <= 8 ? lists + c->n_total() : nullptr;
+  if (nf > 0) {
+    dim3 grid((unsigned)(c->N() / th), (unsigned)nf, gz);
+    if (A.dnum <= 4)
+      hx::ks_inner_f64_kernel<4><<<grid, th, 0, s>>>(A, lists);
+    else
+      hx::ks_inner_f64_kernel<8><<<grid, th, 0, s>>>(A, lists);
+    launched(c, "ks_inner_f64_kernel");
+  }
+  if (ni > 0) {
+    dim3 grid((unsigned)(c->N() / th), (unsigned)ni, gz);
+    if (A.dnum <= 4)
+      hx::ks_inner_kernel<4><<<grid, th, 0, s>>>(A, il);
+    else if (A.dnum <= 8)
+      hx::ks_inner_kernel<8><<<grid, th, 0, s>>>(A, il);
+    else if (A.dnum <= 16)
+      hx::ks_inner_kernel<16><<<grid, th, 0, s>>>(A, il);
+    else if (A.dnum <= 32)
+      hx::ks_inner_kernel<32><<<grid, th, 0, s>>>(A, il);
+    else
+      hx::ks_inner_kernel<64><<<grid, th, 0, s>>>(A, il);
+    launched(c, "ks_inner_kernel");
+  }
 }
 
 void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long batch, int n_q,
@@ -608,6 +625,10 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
       P.ninv_q = (double)P.ninv / qd;
       P.w1n_d = (double)P.w1n;
       P.w1n_q = (double)P.w1n / qd;
+      P.r20_d = (double)((1ull << 20) % q);
+      P.r20_q = P.r20_d / qd;
+      P.r40_d = (double)((1ull << 40) % q);
+      P.r40_q = P.r40_d / qd;
       double* ff = twf.data() + (size_t)i * 2 * N;
       if (P.f64)
         for (u64 k = 0; k < 2 * N; ++k) ff[k] = (double)(k < N ? f[k] : g[k - N]).x;
@@ -702,6 +723,20 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
       }
     }
     c->d_maclimbs = upload(ml);
+    std::vector<int> kl((size_t)(n_chain + 1) * 2 * T, 0);
+    c->ks_nf64.assign(n_chain + 1, 0);
+    c->ks_nint.assign(n_chain + 1, 0);
+    for (int nq = 1; nq <= n_chain; ++nq) {
+      int* f = kl.data() + (size_t)nq * 2 * T;
+      int* g = f + T;
+      for (int j = 0; j < nq + n_special; ++j) {
+        if (c->allow_f64 && c->primes[c->pidx(j, nq)] < (1ull << 43))
+          f[c->ks_nf64[nq]++] = j;
+        else
+          g[c->ks_nint[nq]++] = j;
+      }
+    }
+    c->d_kslimbs = upload(kl);
     out = c.release();
   });
   return rc == HX_OK ? out : nullptr;
@@ -711,7 +746,7 @@ void hx_ctx_destroy(hx_ctx* c) {
   if (!c) return;
   for (void* p : {(void*)c->d_pc, (void*)c->d_tw, (void*)c->d_twf, (void*)c->d_modup, (void*)c->d_phinv,
                   (void*)c->d_pconv, (void*)c->d_pmodq, (void*)c->d_pinv, (void*)c->d_qlinv,
-                  (void*)c->d_qlmod, (void*)c->d_maclimbs})
+                  (void*)c->d_qlmod, (void*)c->d_maclimbs, (void*)c->d_kslimbs})
     if (p) cudaFree(p);
   delete c;
 }

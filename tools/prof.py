@@ -101,9 +101,63 @@ def mactime(n1=32, n2=32):
     print(f"bsgs_mac n1={n1} n2={n2}: {ms:.3f} ms  diag {gb:.2f} GB  {gb / ms:.2f} TB/s")
 
 
+def timed(fn, iters=5):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def mactime(n1=32, n2=32):
+    chain, special = bench.primes()
+    ctx = Context(bench.LOGN, chain, special, bench.ALPHA)
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1)
+    nq, N = len(chain), bench.N
+    baby = bench.rand_limbs(torch, gen, chain, (n1, 2), dev)
+    diags = bench.rand_limbs(torch, gen, chain, (n1 * n2,), dev)
+    inner = torch.empty((n2, 2, nq, N), dtype=torch.int64, device=dev)
+    ms = timed(lambda: ctx.bsgs_mac(inner, baby, diags, nq, n1, n2, nq))
+    gb = n1 * n2 * nq * N * 8 / 1e9
+    print(f"bsgs_mac n1={n1} n2={n2}: {ms:.3f} ms  diag {gb:.2f} GB  {gb / ms:.2f} TB/s")
+
+
+def ffnloop(iters=8):
+    import time
+
+    import numpy as np
+
+    from paper_2512_11135_b200.helix import BSGS, Backend, params_json
+
+    chain, special = bench.primes()
+    be = Backend(params_json(bench.LOGN, chain, special, bench.ALPHA, 40), seed=3)
+    rng = np.random.default_rng(3)
+    M = rng.normal(0, 0.02, (3072, 768))
+    t0 = time.perf_counter()
+    mat = be.prepare(BSGS, M, be.max_level)
+    be.gen_rotation_keys(mat.rotations())
+    print("prepare", time.perf_counter() - t0, flush=True)
+    x = np.tile(np.concatenate([rng.uniform(-1, 1, 768), np.zeros(256)]), be.slots // 1024)
+    ct = be.encrypt(x)
+    for it in range(iters):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        outs, rep = be.matvec(mat, ct)
+        torch.cuda.synchronize()
+        print(f"matvec {it}: {1e3 * (time.perf_counter() - t):.1f} ms", flush=True)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "ffn":
         ffn()
+    elif len(sys.argv) > 1 and sys.argv[1] == "ffnloop":
+        ffnloop()
     elif len(sys.argv) > 1 and sys.argv[1] == "mactime":
         mactime(*[int(a) for a in sys.argv[2:4]])
     else:
