@@ -100,8 +100,11 @@ class GpuLatticeBackend final : public SlotBackend {
   // per-block MAC launches write inner sums in [n2][blocks] order, then giant
   // step j of every block is rotated with one read of key n1 j
   // (hx_rotate_grouped) and summed in one pass.  Same trace as per-block.
+  // allow_empty: a block without live diagonals yields a zero ciphertext
+  // (giant-step shards, linalg.hpp BsgsShard) instead of an error.
   std::vector<Ciphertext> bsgs_blocks(const std::vector<Ciphertext>& baby,
-                                      const std::vector<Plaintext>& diags, int n1, int n2, int blocks);
+                                      const std::vector<Plaintext>& diags, int n1, int n2, int blocks,
+                                      bool allow_empty = false);
 
   // ---- raw access ----
   hx_ctx* device_context() const { return ctx_; }

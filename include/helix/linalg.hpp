@@ -35,6 +35,20 @@ struct EncodedMatrix {
 
 EncodedMatrix encode_matrix(SlotOps& ops, const PackedMatrix& M, int level);
 
+// Giant-step shard of a BSGS transform (multi-GPU): only the
+// diagonals of giant groups j in [giant_begin, giant_end) are encoded /
+// applied; `rescale = false` returns the pre-rescale partial sum so that the
+// shards' partials can be added exactly (NCCL uint64 sum + hx_reduce_mod_q)
+// before the single final rescale.
+struct BsgsShard {
+  int giant_begin = 0;
+  int giant_end = -1;  // -1: n2
+  bool rescale = true;
+};
+EncodedMatrix encode_matrix(SlotOps& ops, const PackedMatrix& M, int level, const BsgsShard& shard);
+// the shard of giant groups owned by `rank` of `world` (contiguous split)
+BsgsShard bsgs_shard(const BsgsPlan& plan, int rank, int world);
+
 // log2(span) rotate-adds at strides stride * 2^i
 Ciphertext rotate_and_sum(SlotOps& ops, const Ciphertext& ct, std::size_t span, std::size_t stride,
                           KernelReport* report = nullptr);
@@ -46,6 +60,7 @@ struct MatvecResult {
   KernelReport report;
 };
 MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x);
+MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x, const BsgsShard& shard);
 MatvecResult matvec_diag(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x);
 // packed-row method: y in the first R slots; 2 levels
 MatvecResult matvec_row(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x);

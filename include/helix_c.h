@@ -79,6 +79,19 @@ int hxc_matrix_rotations(const hxc_mat* m, int64_t* out, int cap);
 /* y = M x; writes up to cap output handles (one per row block); returns count */
 int hxc_matvec(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, int cap,
                hxc_report* rep);
+/* ---- giant-step sharding of BSGS (multi-GPU, one process per GPU) ----
+ * rank r of world G encodes only its giant groups (helix::bsgs_shard) and
+ * returns PRE-RESCALE partial outputs; the caller sums the partial words of all
+ * ranks (e.g. NCCL all-reduce of int64 = wrapping uint64 sum), reduces mod q
+ * (hx_reduce_mod_q), wraps the words (hxc_ct_like) and rescales once. */
+hxc_mat* hxc_matrix_prepare_shard(hxc_backend* b, const double* A, int rows, int cols, int level,
+                                  int rank, int world);
+int hxc_matvec_shard(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, int cap,
+                     hxc_report* rep);
+/* a new ciphertext with the level / scale of `like` and words copied from the
+ * device buffer `words` ([2][level+1][N]) */
+hxc_ct* hxc_ct_like(hxc_backend* b, const hxc_ct* like, const uint64_t* words);
+
 /* ct-ct matmul of row-major d x d operands */
 hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_report* rep);
 int hxc_matmul_rotations(int d, int64_t* out, int cap);

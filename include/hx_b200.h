@@ -66,6 +66,7 @@ int hx_malloc(void** ptr, size_t bytes);
 int hx_free(void* ptr);
 int hx_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream);
 int hx_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream);
+int hx_memcpy_d2d(void* dst, const void* src, size_t bytes, void* stream);
 int hx_stream_sync(void* stream);
 int hx_device_sync(void);
 

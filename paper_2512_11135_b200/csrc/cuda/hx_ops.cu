@@ -774,6 +774,10 @@ int hx_memcpy_d2h(void* dst, const void* src, size_t bytes, void* s) {
   return guarded(
       [&] { cuda_ok(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, S(s)), "d2h"); });
 }
+int hx_memcpy_d2d(void* dst, const void* src, size_t bytes, void* s) {
+  return guarded(
+      [&] { cuda_ok(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, S(s)), "d2d"); });
+}
 int hx_stream_sync(void* s) {
   return guarded([&] { cuda_ok(cudaStreamSynchronize(S(s)), "cudaStreamSynchronize"); });
 }

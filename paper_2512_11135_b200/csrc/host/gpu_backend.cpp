@@ -503,7 +503,7 @@ Ciphertext GpuLatticeBackend::bsgs_block(const std::vector<Ciphertext>& baby,
 
 std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphertext>& baby,
                                                        const std::vector<Plaintext>& diags, int n1, int n2,
-                                                       int blocks) {
+                                                       int blocks, bool allow_empty) {
   if ((int)baby.size() < n1 || (long long)diags.size() < (long long)n1 * n2 * blocks)
     throw std::invalid_argument("bsgs_blocks: shape");
   const Ciphertext& x = baby[0];
@@ -607,10 +607,11 @@ std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphert
     }
     bool any = false;
     for (int j = 0; j < n2; ++j) any |= live[b][j] != 0;
-    if (!any) throw std::invalid_argument("matvec_bsgs: block has no non-zero diagonal");
-    trace_.record(OpKind::PtMul, level, ptmuls);
+    if (!any && !allow_empty) throw std::invalid_argument("matvec_bsgs: block has no non-zero diagonal");
+    if (ptmuls) trace_.record(OpKind::PtMul, level, ptmuls);
     if (adds) trace_.record(OpKind::CtAdd, level, adds);
   }
+  if (!have_scale) dscale = Scale::prime(modulus_at(level));  // empty shard: the diagonal scale
   const Scale out_scale = x.scale * dscale;
   // giant steps j >= 1: rotate group j of every block by n1 j with one key
   std::vector<const u64*> keys;

@@ -21,6 +21,7 @@ struct hxc_ct {
 struct hxc_mat {
   EncodedMatrix m;
   int method;
+  BsgsShard shard;
 };
 
 namespace {
@@ -170,6 +171,42 @@ int hxc_matvec(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, 
     int k = 0;
     for (; k < (int)r.outputs.size() && k < cap; ++k) out[k] = wrap(r.outputs[k]);
     return (int)r.outputs.size();
+  });
+}
+
+hxc_mat* hxc_matrix_prepare_shard(hxc_backend* b, const double* A, int rows, int cols, int level, int rank,
+                                  int world) {
+  return guard<hxc_mat*>(nullptr, [&] {
+    Matrix M(rows, cols);
+    std::memcpy(M.data.data(), A, sizeof(double) * (std::size_t)rows * cols);
+    const PackedMatrix P = pack_bsgs(M, b->b->slots());
+    auto* h = new hxc_mat;
+    h->method = HXC_BSGS;
+    h->shard = bsgs_shard(P.plan, rank, world);
+    h->m = encode_matrix(*b->b, P, level, h->shard);
+    return h;
+  });
+}
+
+int hxc_matvec_shard(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, int cap, hxc_report* rep) {
+  return guard(-1, [&] {
+    BsgsShard s = m->shard;
+    s.rescale = false;
+    MatvecResult r = matvec_bsgs(*b->b, m->m, x->c, s);
+    fill(rep, r.report);
+    int k = 0;
+    for (; k < (int)r.outputs.size() && k < cap; ++k) out[k] = wrap(r.outputs[k]);
+    return (int)r.outputs.size();
+  });
+}
+
+hxc_ct* hxc_ct_like(hxc_backend* b, const hxc_ct* like, const uint64_t* words) {
+  return guard<hxc_ct*>(nullptr, [&] {
+    const std::size_t w = (std::size_t)2 * (like->c.level + 1) * b->b->params().ring_degree;
+    auto buf = std::make_shared<DeviceBuffer>(w);
+    if (cudaMemcpyAsync(buf->ptr, words, w * 8, cudaMemcpyDeviceToDevice, nullptr) != cudaSuccess)
+      throw std::runtime_error("hxc_ct_like: copy failed");
+    return wrap(b->b->wrap(buf, 0, like->c.level, like->c.scale));
   });
 }
 

@@ -92,9 +92,49 @@ Ciphertext rotate_and_sum(SlotOps& ops, const Ciphertext& ct, std::size_t span, 
 
 // ------------------------------------------------------------------- BSGS
 MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x) {
-  require_matvec_input(M, x, Layout::BsgsDiagonal);
+  return matvec_bsgs(ops, M, x, BsgsShard{});
+}
+
+BsgsShard bsgs_shard(const BsgsPlan& plan, int rank, int world) {
+  if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bsgs_shard: bad rank/world");
+  BsgsShard s;
+  s.giant_begin = (int)((long long)plan.n2 * rank / world);
+  s.giant_end = (int)((long long)plan.n2 * (rank + 1) / world);
+  s.rescale = world == 1;
+  return s;
+}
+
+EncodedMatrix encode_matrix(SlotOps& ops, const PackedMatrix& M, int level, const BsgsShard& shard) {
+  if (M.layout != Layout::BsgsDiagonal) throw std::invalid_argument("encode_matrix: shards apply to BSGS layouts");
+  PackedMatrix S = M;
+  const int n1 = M.plan.n1, ge = shard.giant_end < 0 ? M.plan.n2 : shard.giant_end;
+  for (int b = 0; b < M.row_blocks; ++b)
+    for (int i = 0; i < M.d; ++i) {
+      const int j = i / n1;
+      if (j < shard.giant_begin || j >= ge) S.payloads[(std::size_t)b * M.d + i].clear();
+    }
+  return encode_matrix(ops, S, level);
+}
+
+MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& Min, const Ciphertext& x, const BsgsShard& shard) {
+  require_matvec_input(Min, x, Layout::BsgsDiagonal);
   const auto snap = TraceSnapshot::take(ops.trace());
-  const int d = M.meta.d, n1 = M.meta.plan.n1, n2 = M.meta.plan.n2;
+  const int d = Min.meta.d, n1 = Min.meta.plan.n1, n2 = Min.meta.plan.n2;
+  const int gb = shard.giant_begin, ge = shard.giant_end < 0 ? n2 : shard.giant_end;
+  const bool sharded = gb > 0 || ge < n2;
+  // groups outside the shard are treated as zero
+  EncodedMatrix Msh;
+  if (sharded) {
+    Msh.meta = Min.meta;
+    Msh.level = Min.level;
+    Msh.pts = Min.pts;
+    for (std::size_t i = 0; i < Msh.pts.size(); ++i) {
+      const int j = (int)(i % (std::size_t)d) / n1;
+      if (j < gb || j >= ge) Msh.pts[i].payload.reset();
+    }
+  }
+  const EncodedMatrix& M = sharded ? Msh : Min;
+  auto finish = [&](const Ciphertext& acc) { return shard.rescale ? ops.rescale(acc) : acc; };
   MatvecResult R;
 #ifndef HELIX_NO_GPU
   auto* gpu = dynamic_cast<GpuLatticeBackend*>(&ops);
@@ -114,8 +154,8 @@ MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext&
   }
 #ifndef HELIX_NO_GPU
   if (gpu) {
-    for (const auto& acc : gpu->bsgs_blocks(baby, M.pts, n1, n2, M.meta.row_blocks))
-      R.outputs.push_back(ops.rescale(acc));
+    for (const auto& acc : gpu->bsgs_blocks(baby, M.pts, n1, n2, M.meta.row_blocks, sharded))
+      R.outputs.push_back(finish(acc));
     R.report = report_since(ops.trace(), snap, x.level, R.outputs.front());
     return R;
   }
@@ -139,7 +179,7 @@ MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext&
       if (!sum) throw std::invalid_argument("matvec_bsgs: block has no non-zero diagonal");
       acc = *sum;
     }
-    R.outputs.push_back(ops.rescale(acc));
+    R.outputs.push_back(finish(acc));
   }
   R.report = report_since(ops.trace(), snap, x.level, R.outputs.front());
   return R;

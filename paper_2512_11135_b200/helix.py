@@ -64,6 +64,9 @@ def lib():
         "hxc_matrix_rotations": (i32, [v, C.POINTER(C.c_int64), i32]),
         "hxc_matvec": (i32, [v, v, v, C.POINTER(v), i32, rp]),
         "hxc_matmul": (v, [v, v, v, i32, rp]),
+        "hxc_matrix_prepare_shard": (v, [v, f64p, i32, i32, i32, i32, i32]),
+        "hxc_matvec_shard": (i32, [v, v, v, C.POINTER(v), i32, rp]),
+        "hxc_ct_like": (v, [v, v, v]),
         "hxc_matmul_rotations": (i32, [i32, C.POINTER(C.c_int64), i32]),
         "hxc_secret_key_ptr": (v, [v]),
         "hxc_relin_key_ptr": (v, [v]),
@@ -237,6 +240,24 @@ class Backend:
         if k < 0:
             raise _err()
         return [Ct(self, outs[i]) for i in range(k)], r.as_dict()
+
+    def prepare_shard(self, A, level, rank, world):
+        """BSGS matrix restricted to this rank's giant groups (helix::bsgs_shard)"""
+        A = np.ascontiguousarray(A, dtype=np.float64)
+        return Mat(self, self.L.hxc_matrix_prepare_shard(self.h, A.ctypes.data_as(C.POINTER(C.c_double)),
+                                                         A.shape[0], A.shape[1], level, rank, world), BSGS)
+
+    def matvec_shard(self, mat, x):
+        """pre-rescale partial outputs of this rank's giant groups"""
+        r = Report()
+        outs = (C.c_void_p * 64)()
+        k = self.L.hxc_matvec_shard(self.h, mat.h, x.h, outs, 64, C.byref(r))
+        if k < 0:
+            raise _err()
+        return [Ct(self, outs[i]) for i in range(k)], r.as_dict()
+
+    def ct_like(self, like, words_ptr):
+        return Ct(self, self.L.hxc_ct_like(self.h, like.h, words_ptr))
 
     def matmul(self, A, B, d):
         r = Report()

@@ -74,6 +74,8 @@ def lib() -> C.CDLL:
         "hx_decrypt": [v, v, v, v, i32, i32, v],
         "hx_rotate_host": [v, v, v, v, i32, i32, u64, v],
         "hx_mul_relin_host": [v, v, v, v, v, i32, i32, v],
+        "hx_memcpy_d2d": [v, v, C.c_size_t, v],
+        "hx_memcpy_d2h": [v, v, C.c_size_t, v],
         "hx_stream_sync": [v],
         "hx_device_sync": [],
     }

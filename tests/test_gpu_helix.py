@@ -194,3 +194,50 @@ def test_matmul_ctct(d):
     assert rep["levels_consumed"] == 2 and abs(rep["output_scale_log2"] - 40) < 1e-12
     out = be.decrypt(c)[: d * d].reshape(d, d)
     assert np.abs(out - A @ Bm).max() < 1e-3 * d
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_giant_step_shards_bit_exact(world):
+    """the G rank shards of a multi-block BSGS matvec (each rank
+    its giant groups, pre-rescale partials), summed as int64 words (what the
+    NCCL all-reduce does), reduced mod q on the device (hx_reduce_mod_q) and
+    rescaled once, equal the single-GPU matvec word for word.  The ranks run
+    one after another on this GPU; nothing waits on another rank."""
+    import torch
+
+    from paper_2512_11135_b200.helix import BSGS
+    from paper_2512_11135_b200.shard import gather_words, reduce_partials, shard_range
+
+    p, be = backend("c2s")
+    N = 1 << p["logn"]
+    rng = np.random.default_rng(40 + world)
+    A = rng.normal(0, 0.02, (512, 256))
+    x = rng.uniform(-1, 1, 256)
+    lvl = 6
+    nq = lvl + 1
+    M = be.prepare(BSGS, A, lvl)
+    be.gen_rotation_keys(M.rotations())
+    ct = be.encrypt(np.tile(x, be.slots // 256), lvl)
+    ref, rep_full = be.matvec(M, ct)
+    n2 = M.info()["n2"]
+    total = None
+    rots = 0
+    for r in range(world):
+        Ms = be.prepare_shard(A, lvl, r, world)
+        gb, ge = shard_range(n2, r, world)
+        parts, rep = be.matvec_shard(Ms, ct)
+        assert len(parts) == 2 and rep["levels_consumed"] == 0
+        rots += rep["rotations"] - (M.info()["n1"] - 1)  # baby steps are replicated per rank
+        w = gather_words(parts, nq, N, torch)
+        total = w if total is None else total + w  # int64 wrap == u64 sum
+        like = parts
+    torch.cuda.synchronize()
+    reduce_partials(be.device_context(), total, 2, nq, lambda t: None)
+    outs = [be.rescale(be.ct_like(like[i], total[i].data_ptr())) for i in range(2)]
+    for i in range(2):
+        got = d2h(outs[i].device_ptr(), 2 * lvl * N)
+        exp = d2h(ref[i].device_ptr(), 2 * lvl * N)
+        assert np.array_equal(got, exp)
+    assert rots == rep_full["rotations"] - (M.info()["n1"] - 1)
+    y = np.concatenate([be.decrypt(o)[:256] for o in outs])
+    assert np.abs(y - A @ x).max() < 1e-5
