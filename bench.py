@@ -104,6 +104,12 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def wait_first(self, timeout: float = 5.0):
+        t = time.time()
+        while self.proc is not None and not self.rows and time.time() - t < timeout:
+            time.sleep(0.05)
+        time.sleep(0.3)
+
     def _read(self):
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
@@ -348,19 +354,24 @@ def main():
         torch.cuda.synchronize()
 
     # ---- headline: timed region ----
+    # nvidia-smi's start-up stalls the device for ~0.2-0.5 s: start the clock
+    # sampler first and let it produce samples before the warm-up ends
+    sampler = ClockSampler(local)
+    sampler.start()
+    sampler.wait_first()
     for _ in range(args.warmup):
         step()
     barrier()
-    sampler = ClockSampler(local)
-    sampler.start()
+    sampler.rows.clear()  # clocks of the timed region only
     l0 = ctx.launches()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    t0, t1 = evs[0], evs[-1]
     t0.record()
-    for _ in range(args.steps):
+    for k in range(args.steps):
         step()
-    t1.record()
+        evs[k + 1].record()
     barrier()
+    print("step ms:", [round(evs[k].elapsed_time(evs[k + 1]), 2) for k in range(args.steps)], file=sys.stderr)
     launches = ctx.launches() - l0
     clocks = sampler.stop()
     secs = t0.elapsed_time(t1) / 1e3

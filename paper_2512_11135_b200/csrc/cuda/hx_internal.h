@@ -11,7 +11,25 @@
 #include "hx_types.cuh"
 #include "hx_ntt.cuh"
 
+// Scratch arena of a context: one device block handed out as a LIFO stack to
+// the scoped temporaries of the C-ABI calls (DBuf), so the steady state makes
+// no allocator calls at all (mapping fresh pool memory costs ~0.1 s per
+// 5 GB and would land inside timed steps).  Requests that do not fit fall
+// back to the stream-ordered pool and raise the high-water mark; the block is
+// regrown to the mark when the stack is next empty.  Stream safety: the arena
+// follows one stream at a time; a call on another stream first waits for the
+// previous stream's work (event), so reuse never races.
+struct HxArena {
+  char* base = nullptr;
+  size_t cap = 0, top = 0, high = 0;
+  int depth = 0;
+  cudaStream_t stream = nullptr;
+  bool stream_set = false;
+  cudaEvent_t ev = nullptr;
+};
+
 struct hx_ctx {
+  HxArena arena;
   int logn = 0;
   int n_chain = 0, n_special = 0, alpha = 1;
   int device = 0;

@@ -428,6 +428,13 @@ struct CombineArgs {
   long long add_every, add_period;
   u32 add_g;  // 1 = no automorphism on `add`
   int logn;
+  // Fused output automorphism (rotations): when perm != 0, poly b is poly
+  // (b & 1) of ciphertext q = b / 2 = r per + e, and the result is written
+  // permuted, out[r rstride + e estride + (b & 1) n_q N + i N + t] =
+  // result[tau_{pg[r]}(t)] (u, conv and add gathered at the same source).
+  int perm, per;
+  long long out_rstride, out_estride;
+  u32 pg[64];
 };
 
 __global__ void combine_kernel(CombineArgs A) {
@@ -440,14 +447,23 @@ __global__ void combine_kernel(CombineArgs A) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const PrimeConst& P = A.pc[i];
   const SC c = A.pinv[i];
-  const u64 uu = A.u[b * A.u_stride + (long long)i * N + t];
-  const u64 cv = A.conv[b * A.conv_stride + (long long)i * N + t];
+  int src = t;
+  long long ob = b * A.out_stride;
+  if (A.perm) {
+    const long long q = b >> 1;
+    const long long rr = q / A.per, e = q % A.per;
+    const u32 g = A.pg[rr];
+    if (g != 1) src = (int)ntt_auto_index((u32)t, g, A.logn);
+    ob = rr * A.out_rstride + e * A.out_estride + (b & 1) * (long long)A.n_q * N;
+  }
+  const u64 uu = __ldg(A.u + b * A.u_stride + (long long)i * N + src);
+  const u64 cv = __ldg(A.conv + b * A.conv_stride + (long long)i * N + src);
   u64 r = csub(shoup_lazy(uu + P.q - cv, c.w, c.wp, P.q), P.q);
   if (do_add) {
-    const int src = A.add_g == 1 ? t : (int)ntt_auto_index((u32)t, A.add_g, A.logn);
-    r = addmod(r, A.add[ba * A.add_stride + (long long)i * N + src], P.q);
+    const int asrc = A.perm ? src : (A.add_g == 1 ? t : (int)ntt_auto_index((u32)t, A.add_g, A.logn));
+    r = addmod(r, __ldg(A.add + ba * A.add_stride + (long long)i * N + asrc), P.q);
   }
-  A.out[b * A.out_stride + (long long)i * N + t] = r;
+  A.out[ob + (long long)i * N + t] = r;
 }
 
 // Rescale helper (rns_poly.cpp:144-162): from the coefficient-domain last limb

@@ -145,10 +145,14 @@ __device__ __forceinline__ u64 f64bits_to_residue(u64 bits, double q, double qin
 // + [0, OTH 2^(S-beta-1)); they are stored back to back, stage beta at offset
 // OTH (2^S - 2^(S-beta)).  This turns the per-butterfly distinct twiddle
 // loads of the last stages into one coalesced bulk load per tile.
+// Each segment is padded with one double per 16 (index k stored at
+// k + k / 16): the last register group reads twiddles at a lane stride of
+// 2^(3 - beta) doubles, which without padding is a 16-way bank conflict.
 template <int S, int OB>
 __device__ __forceinline__ int row_tw_offset(int beta) {
-  return (1 << OB) * ((1 << S) - (1 << (S - beta)));
+  return 17 * ((1 << OB) * ((1 << S) - (1 << (S - beta)))) / 16;
 }
+__device__ __forceinline__ int row_tw_pad(int k) { return k + (k >> 4); }
 
 template <bool FWD, bool ROW, int S, int OB, int W>
 __device__ __forceinline__ void ntt_group_f64(u64 (&x)[16], const int (&jb)[16 >> W], int g0, int logn,
@@ -178,7 +182,7 @@ __device__ __forceinline__ void ntt_group_f64(u64 (&x)[16], const int (&jb)[16 >
         double2 wt = make_double2(0.0, 0.0);
         if (!fin) {
           if (ROW)
-            wt.x = sm_tw[row_tw_offset<S, OB>(beta) + (int)((j & ((1u << (S + OB)) - 1)) >> (beta + 1))];
+            wt.x = sm_tw[row_tw_offset<S, OB>(beta) + row_tw_pad((int)((j & ((1u << (S + OB)) - 1)) >> (beta + 1)))];
           else
             wt.x = __ldg(tw + ((N + j) >> (beta + 1)));
           wt.y = __dmul_rn(wt.x, P.qinv_d);  // w / q (relative error <= 2^-52)
@@ -246,7 +250,7 @@ struct Sched {
 // dynamic shared memory of a pass kernel (bytes)
 template <bool ROW, int S, int OB, bool F64>
 constexpr int ntt_smem_bytes() {
-  return 8 * ((1 << (S + OB)) + ((ROW && F64) ? (1 << OB) * ((1 << S) - 1) : 0));
+  return 8 * ((1 << (S + OB)) + ((ROW && F64) ? 17 * (1 << OB) * ((1 << S) - 1) / 16 + 16 : 0));
 }
 
 template <bool FWD, bool ROW, int S, int OB, bool F64>
@@ -274,15 +278,24 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16)
   // FP64 ROW pass: stage the tile's twiddles (all S stages) in shared memory
   double* sm_tw = reinterpret_cast<double*>(dyn_smem + TILE);
   if (ROW && F64) {
+    // all S stages' twiddles of the tile (255 x 2^OB doubles) with 8-byte
+    // cp.async (LDGSTS): every thread has all its copies in flight at once and
+    // they overlap the first group's data loads; waited for before group 0.
+    constexpr int kTw = (1 << OB) * ((1 << S) - 1);
     const long long row0 = (long long)tile << OB;
-#pragma unroll 1
-    for (int beta = 0; beta < S; ++beta) {
-      const int cnt = (1 << OB) << (S - beta - 1);
-      const double* src = twf + ((1ll << a.logn) >> (beta + 1)) + (row0 << (S - beta - 1));
-      double* dst = sm_tw + row_tw_offset<S, OB>(beta);
-      for (int k = t; k < cnt; k += T) dst[k] = __ldg(src + k);
+#pragma unroll
+    for (int i = 0; i < (kTw + T - 1) / T; ++i) {
+      const int m = t + i * T;  // flat index, stage beta owns [2^(S+OB) - 2^(S+OB-beta), 2^(S+OB) - 2^(S+OB-beta-1))
+      if (m < kTw) {
+        const int beta = (S + OB - 1) - (31 - __clz((TILE - 1) - m));
+        const int seg = TILE - (TILE >> beta);
+        const int k = m - seg;
+        const double* src = twf + ((1ll << a.logn) >> (beta + 1)) + (row0 << (S - beta - 1)) + k;
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(sm_tw + 17 * seg / 16 + row_tw_pad(k));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src) : "memory");
+      }
     }
-    __syncthreads();
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
 
   u64 x[16];
@@ -343,6 +356,10 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16)
         const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                       \
         x[r] = sm[swz<ROW>(e)];                                                                \
       }                                                                                        \
+    }                                                                                          \
+    if (ROW && F64 && first) {                                                                 \
+      asm volatile("cp.async.wait_all;\n" ::: "memory");                                     \
+      __syncthreads();                                                                         \
     }                                                                                          \
     if (F64 && kFirstPass && first) {                                                          \
       _Pragma("unroll") for (int r = 0; r < 16; ++r) x[r] = u64_to_f64bits(x[r]);              \

@@ -15,6 +15,9 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "../../../include/hx_b200.h"
 #include "hx_internal.h"
@@ -123,14 +126,50 @@ u64 find_psi(u64 q, u64 n) {
 }
 
 // ---- stream-ordered scratch buffer ----
+// Scoped device temporary: from the context arena (HxArena, hx_internal.h)
+// when a context is given, else from the stream-ordered pool.
 struct DBuf {
   u64* p = nullptr;
   cudaStream_t s = nullptr;
-  DBuf(size_t words, cudaStream_t st) : s(st) {
-    if (words) cuda_ok(cudaMallocAsync((void**)&p, words * 8, st), "cudaMallocAsync");
+  hx_ctx* c = nullptr;
+  size_t bytes = 0;
+  bool from_arena = false;
+  DBuf(size_t words, cudaStream_t st, hx_ctx* ctx = nullptr) : s(st), c(ctx), bytes(((words * 8) + 255) & ~size_t(255)) {
+    if (!words) return;
+    if (c) {
+      HxArena& A = c->arena;
+      if (A.stream_set && A.stream != st) {  // hand the arena over to stream st
+        if (!A.ev) cuda_ok(cudaEventCreateWithFlags(&A.ev, cudaEventDisableTiming), "event");
+        cuda_ok(cudaEventRecord(A.ev, A.stream), "event record");
+        cuda_ok(cudaStreamWaitEvent(st, A.ev, 0), "stream wait");
+      }
+      A.stream = st;
+      A.stream_set = true;
+      if (A.depth == 0 && A.high > A.cap) {  // regrow to the high-water mark
+        if (A.base) cuda_ok(cudaFreeAsync(A.base, st), "cudaFreeAsync(arena)");
+        A.base = nullptr;
+        cuda_ok(cudaMallocAsync((void**)&A.base, A.high, st), "cudaMallocAsync(arena)");
+        A.cap = A.high;
+      }
+      A.depth++;
+      A.high = std::max(A.high, A.top + bytes);
+      if (A.base && A.top + bytes <= A.cap) {
+        p = (u64*)(A.base + A.top);
+        A.top += bytes;
+        from_arena = true;
+        return;
+      }
+      A.top += bytes;  // keeps the LIFO accounting; memory from the pool
+    }
+    cuda_ok(cudaMallocAsync((void**)&p, words * 8, st), "cudaMallocAsync");
   }
   ~DBuf() {
-    if (p) cudaFreeAsync(p, s);
+    if (!p) return;
+    if (c) {
+      c->arena.top -= bytes;
+      c->arena.depth--;
+    }
+    if (!from_arena) cudaFreeAsync(p, s);
   }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
@@ -192,7 +231,7 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
            cudaStream_t s) {
   const long long N = c->N();
   const int K = c->n_special, ext = n_q + K, dnum = c->dnum(n_q);
-  DBuf coef(batch * n_q * N, s);
+  DBuf coef(batch * n_q * N, s, c);
   copy2d(coef.p, n_q * N, c1, c1_stride, n_q * N, batch, s);
   hx::ntt_inverse(c, coef.p, batch, hx::make_table(c, n_q, 0), s);
   // basis conversion per digit (coefficient domain), own limbs copied (NTT)
@@ -305,12 +344,21 @@ void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long ba
 // Centred ModDown of `polys` PQ-basis polys u (stride u_stride words) into
 // out (stride out_stride words).  Optionally adds tau_g(add) to the polys with
 // index % add_every == 0, using add element (index / add_every) % add_period.
+// Output permutation fused into the ModDown combine (rotations): see
+// CombineArgs::perm.  g[r] for the r-th group of `per` ciphertexts.
+struct OutPerm {
+  std::vector<u64> g;
+  int per = 1;
+  long long rstride = 0, estride = 0;
+};
+
 void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long u_stride,
              long long polys, int n_q, const u64* add, long long add_stride, u64 add_g,
-             cudaStream_t s, long long add_every = 1, long long add_period = 0) {
+             cudaStream_t s, long long add_every = 1, long long add_period = 0,
+             const OutPerm* perm = nullptr) {
   const long long N = c->N();
   const int K = c->n_special;
-  DBuf sp(polys * K * N, s), conv(polys * n_q * N, s);
+  DBuf sp(polys * K * N, s, c), conv(polys * n_q * N, s, c);
   copy2d(sp.p, K * N, u + (long long)n_q * N, u_stride, K * N, polys, s);
   hx::ntt_inverse(c, sp.p, polys, hx::make_table(c, 0, K), s);
   hx::ModDownArgs M;
@@ -350,6 +398,15 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
   C.add_period = add_period;
   C.add_g = (hx::u32)add_g;
   C.logn = c->logn;
+  C.perm = 0;
+  if (perm) {
+    HX_REQUIRE(perm->g.size() <= 64 && add_g == 1 && add_every == 2, "fused output permutation");
+    C.perm = 1;
+    C.per = perm->per;
+    C.out_rstride = perm->rstride;
+    C.out_estride = perm->estride;
+    for (std::size_t r = 0; r < perm->g.size(); ++r) C.pg[r] = (hx::u32)perm->g[r];
+  }
   dim3 g3((unsigned)(N / th), (unsigned)n_q, (unsigned)polys);
   hx::combine_kernel<<<g3, th, 0, s>>>(C);
   launched(c, "combine_kernel");
@@ -357,7 +414,7 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
 
 void rescale(hx_ctx* c, u64* out, const u64* in, long long polys, int n_q, cudaStream_t s) {
   const long long N = c->N();
-  DBuf last(polys * N, s), lift(polys * (n_q - 1) * N, s);
+  DBuf last(polys * N, s, c), lift(polys * (n_q - 1) * N, s, c);
   copy2d(last.p, N, in + (long long)(n_q - 1) * N, (long long)n_q * N, N, polys, s);
   LimbTable lt{};
   lt.count = 1;
@@ -434,29 +491,25 @@ void rotate_batch_from_digits(hx_ctx* c, u64* out, const u64* in, const u64* dig
   const int ext = n_q + c->n_special;
   const long long R = (long long)keys.size();
   const long long dstride = (long long)c->dnum(n_q) * ext * N;
-  DBuf U(R * E * 2 * ext * N, s), W(R * E * ct, s);
+  DBuf U(R * E * 2 * ext * N, s, c);
   for (long long r0 = 0; r0 < R; r0 += hx::kMaxKeys) {
     const long long nr = std::min<long long>(hx::kMaxKeys, R - r0);
     const std::vector<const u64*> kk(keys.begin() + r0, keys.begin() + r0 + nr);
     const u64* dg = shared ? digits : digits + r0 * E * dstride;
     ks_inner_multi(c, U.p + r0 * E * 2 * ext * N, dg, kk, shared, E, n_q, 1, s);
   }
-  // polys p = (r E + e) 2 + c; the c0 polys add input ct (shared ? e : r E + e)
-  moddown(c, W.p, (long long)n_q * N, U.p, (long long)ext * N, R * E * 2, n_q, in, ct, 1, s, 2,
-          shared ? E : 0);
-  const int th = pt_threads(c);
+  // polys p = (r E + e) 2 + c; the c0 polys add input ct (shared ? e : r E + e);
+  // the output automorphism tau_{g_r} is fused into the combine (64 keys per call)
+  const long long out_rstride = shared ? ct : E * ct, out_estride = shared ? R * ct : ct;
   for (long long r0 = 0; r0 < R; r0 += 64) {
     const long long nr = std::min<long long>(64, R - r0);
-    hx::PermuteMulti P;
-    for (long long r = 0; r < nr; ++r) P.g[r] = (hx::u32)galois[r0 + r];
-    P.in_stride = ct;
+    OutPerm P;
+    P.g.assign(galois.begin() + r0, galois.begin() + r0 + nr);
     P.per = (int)E;
-    P.logn = c->logn;
-    P.out_rstride = shared ? ct : E * ct;
-    P.out_estride = shared ? R * ct : ct;
-    hx::permute_multi_kernel<<<dim3((unsigned)(N / th), (unsigned)(2 * n_q), (unsigned)(nr * E)), th, 0,
-                               s>>>(out + r0 * P.out_rstride, W.p + r0 * E * ct, P);
-    launched(c, "permute_multi_kernel");
+    P.rstride = out_rstride;
+    P.estride = out_estride;
+    moddown(c, out + r0 * out_rstride, (long long)n_q * N, U.p + r0 * E * 2 * ext * N, (long long)ext * N,
+            nr * E * 2, n_q, shared ? in : in + r0 * E * ct, ct, 1, s, 2, shared ? E : 0, &P);
   }
 }
 
@@ -479,15 +532,17 @@ void pipelined_host(hx_ctx* c, int batch, std::vector<const uint64_t*> in_host,
     cudaEventCreateWithFlags(&ev_cmp[k], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming);
   }
+  // double-buffered chunk slots from the context arena (released in reverse order)
+  std::vector<std::unique_ptr<DBuf>> slots;
   std::vector<u64*> din[2];
   u64* dout[2] = {nullptr, nullptr};
   for (int k = 0; k < 2 && k < nchunks; ++k) {
     for (long long w : in_words) {
-      u64* p = nullptr;
-      cuda_ok(cudaMalloc((void**)&p, (size_t)w * chunk * 8), "cudaMalloc(chunk)");
-      din[k].push_back(p);
+      slots.push_back(std::make_unique<DBuf>((size_t)w * chunk, s, c));
+      din[k].push_back(slots.back()->p);
     }
-    cuda_ok(cudaMalloc((void**)&dout[k], (size_t)out_words * chunk * 8), "cudaMalloc(chunk)");
+    slots.push_back(std::make_unique<DBuf>((size_t)out_words * chunk, s, c));
+    dout[k] = slots.back()->p;
   }
   cuda_ok(cudaStreamSynchronize(s), "sync");
   for (int i = 0; i < nchunks; ++i) {
@@ -509,14 +564,13 @@ void pipelined_host(hx_ctx* c, int batch, std::vector<const uint64_t*> in_host,
   cuda_ok(cudaStreamSynchronize(d), "sync");
   cuda_ok(cudaStreamSynchronize(s), "sync");
   for (int k = 0; k < 2; ++k) {
-    for (u64* p : din[k]) cudaFree(p);
-    if (dout[k]) cudaFree(dout[k]);
     cudaEventDestroy(ev_in[k]);
     cudaEventDestroy(ev_cmp[k]);
     cudaEventDestroy(ev_out[k]);
   }
   cudaStreamDestroy(h);
   cudaStreamDestroy(d);
+  while (!slots.empty()) slots.pop_back();
 }
 
 }  // namespace
@@ -748,6 +802,12 @@ void hx_ctx_destroy(hx_ctx* c) {
                   (void*)c->d_pconv, (void*)c->d_pmodq, (void*)c->d_pinv, (void*)c->d_qlinv,
                   (void*)c->d_qlmod, (void*)c->d_maclimbs, (void*)c->d_kslimbs})
     if (p) cudaFree(p);
+  if (c->arena.base) {
+    cudaStreamSynchronize(c->arena.stream);
+    cudaFreeAsync(c->arena.base, c->arena.stream);
+    cudaStreamSynchronize(c->arena.stream);
+  }
+  if (c->arena.ev) cudaEventDestroy(c->arena.ev);
   delete c;
 }
 
@@ -915,7 +975,7 @@ int hx_keyswitch(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* k
     check_nq(c, n_q);
     const long long N = c->N();
     const int ext = n_q + c->n_special;
-    DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s)), U((long long)batch * 2 * ext * N, S(s));
+    DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s), c), U((long long)batch * 2 * ext * N, S(s), c);
     modup(c, D.p, (const u64*)in, (long long)n_q * N, batch, n_q, S(s));
     ks_inner(c, U.p, D.p, (const u64*)key, batch, n_q, 1, S(s));
     moddown(c, (u64*)out, (long long)n_q * N, U.p, (long long)ext * N, 2ll * batch, n_q, nullptr,
@@ -932,7 +992,7 @@ int hx_rotate(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* key,
     HX_REQUIRE(out != in, "rotate cannot run in place");
     const long long N = c->N();
     const int ext = n_q + c->n_special;
-    DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s));
+    DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s), c);
     modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s));
     rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, {(const u64*)key}, {g}, true, batch,
                              n_q, S(s));
@@ -947,7 +1007,7 @@ int hx_rotate_hoisted(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
     HX_REQUIRE(R >= 1, "R >= 1");
     const long long N = c->N();
     const int ext = n_q + c->n_special;
-    DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s));
+    DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s), c);
     modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s));
     std::vector<const u64*> kk;
     std::vector<u64> gg;
@@ -970,7 +1030,7 @@ int hx_rotate_multi(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t
     const long long dstride = (long long)c->dnum(n_q) * ext * N;
     for (int b = 0; b < batch; ++b)
       HX_REQUIRE((galois[b] & 1) && galois[b] < 2 * (u64)N, "galois element");
-    DBuf D((long long)batch * dstride, S(s));
+    DBuf D((long long)batch * dstride, S(s), c);
     modup(c, D.p, (const u64*)in + (long long)n_q * N, ct, batch, n_q, S(s));
     std::vector<const u64*> kk;
     std::vector<u64> gg;
@@ -997,7 +1057,7 @@ int hx_rotate_grouped(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
       kk.push_back((const u64*)keys[r]);
       gg.push_back((u64)galois[r]);
     }
-    DBuf D((long long)R * E * c->dnum(n_q) * ext * N, S(s));
+    DBuf D((long long)R * E * c->dnum(n_q) * ext * N, S(s), c);
     modup(c, D.p, (const u64*)in + (long long)n_q * N, ct, (long long)R * E, n_q, S(s));
     rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, kk, gg, false, E, n_q, S(s));
   });
@@ -1092,7 +1152,7 @@ int hx_keygen_ksk(hx_ctx* c, uint64_t* key, const uint64_t* s_full, const uint64
     check_ctx(c);
     const long long N = c->N();
     const int T = c->n_total(), dn = c->dnum(c->n_chain);
-    DBuf en((long long)dn * T * N, S(s));
+    DBuf en((long long)dn * T * N, S(s), c);
     const LimbTable lt = hx::make_table(c, c->n_chain, c->n_special);
     const int th = pt_threads(c);
     hx::from_i64_kernel<<<(unsigned)((long long)dn * T * (N / th)), th, 0, S(s)>>>(
@@ -1124,7 +1184,7 @@ int hx_keygen_rotation(hx_ctx* c, uint64_t* key, const uint64_t* s_full, uint64_
     HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element must be odd and < 2N");
     const long long N = c->N();
     const int T = c->n_total();
-    DBuf sp((long long)T * N, S(s)), std_key((long long)hx_key_words(c), S(s));
+    DBuf sp((long long)T * N, S(s), c), std_key((long long)hx_key_words(c), S(s), c);
     permute(c, sp.p, 0, (const u64*)s_full, 0, T, 1, g, S(s));  // s' = tau_g(s)
     int rc = hx_keygen_ksk(c, (uint64_t*)std_key.p, s_full, (const uint64_t*)sp.p, a_full, e, s);
     if (rc != HX_OK) throw HxError(rc, g_last_error);
@@ -1139,7 +1199,7 @@ int hx_encrypt_sk(hx_ctx* c, uint64_t* ct, const uint64_t* m, const uint64_t* s_
     check_ctx(c);
     check_nq(c, n_q);
     const long long N = c->N();
-    DBuf en((long long)n_q * N, S(s));
+    DBuf en((long long)n_q * N, S(s), c);
     const LimbTable lt = hx::make_table(c, n_q, 0);
     const int th = pt_threads(c);
     hx::from_i64_kernel<<<(unsigned)((long long)n_q * (N / th)), th, 0, S(s)>>>(

@@ -54,6 +54,40 @@ __global__ void k_iadd3(unsigned* out, unsigned a, unsigned b) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
 }
 
+// half the warps on the FP64 pipe, half on 32-bit IMAD / IMAD.WIDE: if the
+// pipes are independent the mixed kernel takes ~half the single-pipe time.
+template <int KIND>
+__global__ void k_mix(unsigned long long* out, double a, double b, unsigned ia) {
+  if ((threadIdx.x >> 5) & 1) {
+    double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < ITERS; ++i) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = __double_as_longlong(x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7);
+  } else if (KIND == 0) {
+    unsigned x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < ITERS; ++i) {
+      x0 = x0 * ia + 7; x1 = x1 * ia + 7; x2 = x2 * ia + 7; x3 = x3 * ia + 7;
+      x4 = x4 * ia + 7; x5 = x5 * ia + 7; x6 = x6 * ia + 7; x7 = x7 * ia + 7;
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  } else {
+    unsigned long long x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < ITERS; ++i) {
+      x0 = (unsigned long long)(unsigned)x0 * ia + (x0 >> 32);
+      x1 = (unsigned long long)(unsigned)x1 * ia + (x1 >> 32);
+      x2 = (unsigned long long)(unsigned)x2 * ia + (x2 >> 32);
+      x3 = (unsigned long long)(unsigned)x3 * ia + (x3 >> 32);
+      x4 = (unsigned long long)(unsigned)x4 * ia + (x4 >> 32);
+      x5 = (unsigned long long)(unsigned)x5 * ia + (x5 >> 32);
+      x6 = (unsigned long long)(unsigned)x6 * ia + (x6 >> 32);
+      x7 = (unsigned long long)(unsigned)x7 * ia + (x7 >> 32);
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  }
+}
+
 template <class F>
 float timeit(F f) {
   cudaEvent_t a, b;
@@ -86,6 +120,9 @@ int main() {
   report("IMAD.WIDE.U32 (+shift/add)", timeit([&] { k_imad_wide<<<blocks, threads>>>((unsigned long long*)buf, 2654435761u); }), 1);
   report("IMAD (32-bit)", timeit([&] { k_imad<<<blocks, threads>>>((unsigned*)buf, 2654435761u, 7); }), 1);
   report("IADD3+LOP3", timeit([&] { k_iadd3<<<blocks, threads>>>((unsigned*)buf, 3, 7); }), 1);
+  // mixed: each half does the same per-thread work as above, so 'lanes' counts all lanes
+  report("MIX DFMA | IMAD", timeit([&] { k_mix<0><<<blocks, threads>>>((unsigned long long*)buf, 1.0000001, 1e-9, 2654435761u); }), 1);
+  report("MIX DFMA | IMAD.WIDE", timeit([&] { k_mix<1><<<blocks, threads>>>((unsigned long long*)buf, 1.0000001, 1e-9, 2654435761u); }), 1);
   cudaDeviceSynchronize();
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;

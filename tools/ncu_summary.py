@@ -12,13 +12,22 @@ import sys
 UNIT = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 
 
-def launches(path):
+def launches(path, after=None, seq=False):
+    """after: only launches following the last launch whose name starts with it"""
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
     tot, cnt = collections.defaultdict(float), collections.Counter()
-    for r in rows[hi + 1:]:
+    body = rows[hi + 1:]
+    if after:
+        last = max(i for i, r in enumerate(body) if len(r) > ki and r[ki].replace("void ", "").startswith(after))
+        body = body[last + 1:]
+    if seq:
+        for r in body:
+            if len(r) > vi and r[vi]:
+                print(f"{float(r[vi].replace(',', '')) * UNIT.get(r[ui], 1.0):10.1f} us  {r[ki][:90]}  grid={r[h.index('Grid Size')]}")
+    for r in body:
         if len(r) <= vi or not r[vi]:
             continue
         us = float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
@@ -65,4 +74,7 @@ def full(path):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None, "--seq" in sys.argv)
+    else:
+        full(sys.argv[2])

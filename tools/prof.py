@@ -101,33 +101,6 @@ def mactime(n1=32, n2=32):
     print(f"bsgs_mac n1={n1} n2={n2}: {ms:.3f} ms  diag {gb:.2f} GB  {gb / ms:.2f} TB/s")
 
 
-def timed(fn, iters=5):
-    fn()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(iters):
-        fn()
-    e1.record()
-    torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / iters
-
-
-def mactime(n1=32, n2=32):
-    chain, special = bench.primes()
-    ctx = Context(bench.LOGN, chain, special, bench.ALPHA)
-    dev = torch.device("cuda", 0)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1)
-    nq, N = len(chain), bench.N
-    baby = bench.rand_limbs(torch, gen, chain, (n1, 2), dev)
-    diags = bench.rand_limbs(torch, gen, chain, (n1 * n2,), dev)
-    inner = torch.empty((n2, 2, nq, N), dtype=torch.int64, device=dev)
-    ms = timed(lambda: ctx.bsgs_mac(inner, baby, diags, nq, n1, n2, nq))
-    gb = n1 * n2 * nq * N * 8 / 1e9
-    print(f"bsgs_mac n1={n1} n2={n2}: {ms:.3f} ms  diag {gb:.2f} GB  {gb / ms:.2f} TB/s")
-
-
 def ffnloop(iters=8):
     import time
 
