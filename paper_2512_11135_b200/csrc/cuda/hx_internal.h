@@ -10,6 +10,7 @@
 #include "hx_common.cuh"
 #include "hx_types.cuh"
 #include "hx_ntt.cuh"
+#include "hx_modup.cuh"
 
 // Scratch arena of a context: one device block handed out as a LIFO stack to
 // the scoped temporaries of the C-ABI calls (DBuf), so the steady state makes
@@ -51,6 +52,12 @@ struct hx_ctx {
   // qhinv [alpha] and conv [alpha][n_total]; offsets in units of SC.
   hx::SC* d_modup = nullptr;
   std::vector<std::vector<long long>> modup_qh_off, modup_cv_off;  // [n_q][d]
+  // fused ModUp: BconvC table offsets [n_q][d]; target lists [n_q][d] into
+  // d_tlist (FP64-class limbs first, then integer-class)
+  hx::BconvC* d_bconv = nullptr;
+  int* d_tlist = nullptr;
+  std::vector<std::vector<long long>> bc_off;
+  std::vector<std::vector<int>> tl_off, tl_cnt, tl_icnt;
   // ModDown constants
   hx::SC* d_phinv = nullptr;   // [K]
   hx::SC* d_pconv = nullptr;   // [K][n_chain]
@@ -77,6 +84,9 @@ LimbTable make_table(const hx_ctx* c, int n_q, int n_p, int stride = -1, int fir
 // NTT launchers (hx_ntt.cu)
 void ntt_forward(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
 void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
+// forward ROW pass only (the COL pass done by a fused producer, hx_modup.cuh)
+void ntt_forward_rows(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
+int ntt_split_a(int logn);
 
 void set_error(const std::string& msg);
 

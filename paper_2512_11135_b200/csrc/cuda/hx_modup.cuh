@@ -1,0 +1,236 @@
+// hx_modup.cuh -- ModUp basis conversion fused into the first (COL) pass of
+// the forward NTT of the extended limbs.
+//
+// Replaces, for every digit d of c1 (coefficient domain after the INTT),
+//   bconv -> [P_d]-basis limb j (coefficient domain)      (FastBConv, non-centred:
+//            the hybrid ModUp of the reference's keyswitch, rns_poly.cpp:182-216)
+//   NTT COL pass on limb j                                 (ntt.cpp:57-74, first stages)
+// with one kernel: a CTA owns one COL tile (2^OB adjacent columns x 2^S rows)
+// of one digit of one ciphertext.  It loads the digit's alpha source limbs of
+// the tile once, forms x_i = [a_i (Qhat_i)^-1]_{q_i} into shared memory, then
+// loops over the digit's target limbs of one prime class: the conversion of a
+// target word is computed straight into the butterfly registers, the COL
+// stages run, and the tile is stored.  The extended limbs therefore never
+// exist in HBM in the coefficient domain (saves one write + one read of
+// 8 x 24 limbs per ciphertext at config 2) and the conversion's FP64 work
+// overlaps the NTT's.  The ROW pass of those limbs is the ordinary ROW launch.
+//
+// Exactness: FP64-class targets (p < 2^47): x_i < 2^47 sources enter as exact
+// doubles, the 60-bit q_0 source as x = xh 2^30 + xl (two exact doubles, the
+// constant [2^30 Qhat_i]_p precomputed), each product by mulmod_f64 (exact),
+// the sum kept lazily in (-(alpha+1) p, (alpha+1) p): the forward FP64 NTT
+// grows values by < p per stage, so |v| < (alpha + 1 + logn) p < 2^52.  Integer
+// targets (60-bit q_0 and special primes): Shoup products, sum in [0, 2p).
+#pragma once
+
+#include "hx_common.cuh"
+#include "hx_ntt.cuh"
+#include "hx_types.cuh"
+
+namespace hx {
+
+// conversion constant of (source limb i of the digit, target limb j):
+// w = [Qhat_i]_{p_j}; FP64 form (w, w / p), (w30, w30 / p) with w30 = [2^30 w]_p;
+// integer form (w, Shoup w').
+struct BconvC {
+  double w, wq, w30, w30q;
+  u64 sw, swp;
+};
+
+constexpr int kMaxDigits = 64;
+
+struct ModUpColArgs {
+  const u64* coef;        // [batch][n_q][N] coefficient-domain c1
+  u64* out;               // [batch][dnum][ext][N] extended digits
+  const PrimeConst* pc;
+  const SC* qhinv;        // per digit at qh_off[d]: [alpha]
+  const BconvC* bc;       // per digit at bc_off[d]: [ext][alpha]
+  const int* tlist;       // per digit at toff[d]: tcnt[d] target limbs j (this class)
+  long long qh_off[kMaxDigits], bc_off[kMaxDigits];
+  // per digit: tcnt[d] FP64-class targets (conversion + COL pass) followed by
+  // icnt[d] integer-class targets (conversion only, coefficient domain out)
+  int toff[kMaxDigits], tcnt[kMaxDigits], icnt[kMaxDigits];
+  int alpha, n_q, n_chain, ext, dnum, logn;
+};
+
+// bconv of one tile word (sources at src[i * stride]) into the working
+// representation of the target class
+template <bool F64, int MAXA>
+__device__ __forceinline__ u64 bconv_word(const u64* src, int stride, int cnt, const bool (&sf64)[MAXA],
+                                          const BconvC* C, const PrimeConst& P) {
+  if (F64) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) {
+      if (i < cnt) {
+        const u64 v = src[i * stride];
+        if (sf64[i]) {
+          acc = __dadd_rn(acc, mulmod_f64(__longlong_as_double((long long)v), C[i].w, C[i].wq, P.qd));
+        } else {  // 60-bit source: x = xh 2^30 + xl
+          const double xh = __dsub_rn(__longlong_as_double((long long)((v >> 30) | 0x4330000000000000ull)), kTwo52);
+          const double xl =
+              __dsub_rn(__longlong_as_double((long long)((v & 0x3FFFFFFFull) | 0x4330000000000000ull)), kTwo52);
+          acc = __dadd_rn(acc, mulmod_f64(xh, C[i].w30, C[i].w30q, P.qd));
+          acc = __dadd_rn(acc, mulmod_f64(xl, C[i].w, C[i].wq, P.qd));
+        }
+      }
+    }
+    return (u64)__double_as_longlong(acc);
+  } else {
+    u64 y = 0;
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) {
+      if (i < cnt) {
+        u64 v = src[i * stride];
+        if (sf64[i])  // exact double -> integer
+          v = (u64)__double_as_longlong(__dadd_rn(__longlong_as_double((long long)v), kTwo52)) & 0xFFFFFFFFFFFFFull;
+        y = csub(y + shoup_lazy(v, C[i].sw, C[i].swp, P.q), P.two_q);
+      }
+    }
+    return y;
+  }
+}
+
+// one target limb of the tile: conversion into registers, forward COL stages,
+// store (FP64 or integer butterflies by the target's prime class)
+template <int S, int OB, bool F64, int MAXA>
+__device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, const bool (&sf64)[MAXA],
+                                             const BconvC (&C)[MAXA], const PrimeConst& P, u64* base,
+                                             int tile, int logn) {
+  constexpr int TILE = 1 << (S + OB);
+  constexpr int NG = Sched<S>::G + (Sched<S>::R ? 1 : 0);
+  const int t = threadIdx.x;
+  const ulonglong2* tw = P.tw_fwd;
+  const double* twf = P.twf_fwd;
+  u64 x[16];
+  // forward COL schedule: full groups from the top, the remainder at bit 0 last
+#pragma unroll
+  for (int gi = 0; gi < NG; ++gi) {
+    int W, g0;
+    if (gi < Sched<S>::G) {
+      W = 4;
+      g0 = S - 4 * (gi + 1);
+    } else {
+      W = Sched<S>::R;
+      g0 = 0;
+    }
+    const bool firstg = gi == 0, lastg = gi == NG - 1;
+#define HX_MGROUP(WW)                                                                        \
+  {                                                                                          \
+    int eb[16 >> WW], jb[16 >> WW];                                                          \
+    group_index<false, S, OB, WW>(t, g0, logn, tile, eb, jb);                                \
+    const int lowbits = OB + g0;                                                             \
+    _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                         \
+      const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                       \
+      x[r] = firstg ? bconv_word<F64, MAXA>(src + e, TILE, cnt, sf64, C, P) : sm[e];         \
+    }                                                                                        \
+    if (F64)                                                                                 \
+      ntt_group_f64<true, false, S, OB, WW>(x, jb, g0, logn, twf, nullptr, P, false);         \
+    else                                                                                     \
+      ntt_group<true, false, S, WW>(x, jb, g0, logn, tw, P, false);                          \
+    if (lastg) {                                                                             \
+      _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
+        const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                     \
+        base[tile_gofs<false, S, OB>(e, tile, logn)] = x[r];                                 \
+      }                                                                                      \
+    } else {                                                                                 \
+      __syncthreads();                                                                       \
+      _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
+        const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                     \
+        sm[e] = x[r];                                                                        \
+      }                                                                                      \
+      __syncthreads();                                                                       \
+    }                                                                                        \
+  }
+    if (W == 4) HX_MGROUP(4)
+    else if (W == 3) HX_MGROUP(3)
+    else if (W == 2) HX_MGROUP(2)
+    else if (W == 1) HX_MGROUP(1)
+#undef HX_MGROUP
+  }
+}
+
+// One launch per ModUp.  FP64-class targets: conversion + COL pass (the ROW
+// pass follows as an ordinary launch).  Integer-class targets (the 60-bit
+// q_0 / special primes, at most alpha + 1 of the ~27 limbs): conversion only,
+// written in the coefficient domain for an ordinary integer NTT -- their
+// 64-bit Shoup butterflies need more registers and latency hiding than this
+// kernel's occupancy (3 CTAs of 128 threads per SM) gives them.
+template <int S, int OB, int MAXA>
+__global__ void __launch_bounds__((1 << (S + OB)) / 16, 3) modup_col_kernel(ModUpColArgs A) {
+  constexpr int TILE = 1 << (S + OB);
+  constexpr int T = TILE / 16;
+  extern __shared__ u64 dyn_smem[];
+  u64* sm = dyn_smem;            // [TILE] group exchange
+  u64* src = dyn_smem + TILE;    // [alpha][TILE] x_i of the tile
+  const int t = threadIdx.x;
+  const int tile = blockIdx.x, d = blockIdx.y;
+  const long long b = blockIdx.z;
+  const int logn = A.logn;
+  const long long N = 1ll << logn;
+  const int lo = d * A.alpha, cnt = min(A.alpha, A.n_q - lo);
+  const int nt = A.tcnt[d], ni = A.icnt[d];
+  if (nt + ni == 0) return;
+
+  // ---- sources: x_i = [a_i Qhat_i^-1]_{q_i} (canonical); FP64-class sources
+  // stored as double bits, the wide ones as integers
+  bool sf64[MAXA];
+  const u64* cb = A.coef + b * (long long)A.n_q * N;
+#pragma unroll
+  for (int i = 0; i < MAXA; ++i) {
+    sf64[i] = false;
+    if (i < cnt) {
+      const PrimeConst& Q = A.pc[lo + i];
+      sf64[i] = Q.f64;
+      const SC h = A.qhinv[A.qh_off[d] + i];
+      const u64* ci = cb + (long long)(lo + i) * N;
+      u64 a[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) a[r] = __ldcs(ci + tile_gofs<false, S, OB>(r * T + t, tile, logn));
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        u64 x = csub(shoup_lazy(a[r], h.w, h.wp, Q.q), Q.q);
+        if (sf64[i]) x = u64_to_f64bits(x);
+        src[i * TILE + r * T + t] = x;
+      }
+    }
+  }
+  __syncthreads();
+
+  const int* tl = A.tlist + A.toff[d];
+  const BconvC* bcd = A.bc + A.bc_off[d];
+  u64* dout = A.out + (b * A.dnum + d) * (long long)A.ext * N;
+#pragma unroll 1
+  for (int k = 0; k < nt; ++k) {
+    const int j = tl[k];
+    const int pj = j < A.n_q ? j : A.n_chain + (j - A.n_q);
+    const PrimeConst P = A.pc[pj];
+    BconvC C[MAXA];
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i)
+      if (i < cnt) C[i] = bcd[(long long)j * A.alpha + i];
+    u64* base = dout + (long long)j * N;
+    __syncthreads();  // the previous target's last exchange reads are done
+    modup_target<S, OB, true, MAXA>(src, sm, cnt, sf64, C, P, base, tile, logn);
+  }
+#pragma unroll 1
+  for (int k = nt; k < nt + ni; ++k) {
+    const int j = tl[k];
+    const int pj = j < A.n_q ? j : A.n_chain + (j - A.n_q);
+    const PrimeConst& P = A.pc[pj];
+    BconvC C[MAXA];
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i)
+      if (i < cnt) C[i] = bcd[(long long)j * A.alpha + i];
+    u64* base = dout + (long long)j * N;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int e = r * T + t;
+      base[tile_gofs<false, S, OB>(e, tile, logn)] = csub(bconv_word<false, MAXA>(src + e, TILE, cnt, sf64, C, P), P.q);
+    }
+  }
+}
+
+inline int modup_col_smem_bytes(int S, int OB, int alpha) { return 8 * (1 << (S + OB)) * (1 + alpha); }
+
+}  // namespace hx

@@ -5,6 +5,7 @@
 // config 2, the 50-bit special of config 1) the integer Shoup butterflies.
 // Both classes are issued on the same stream in pass order, so every limb
 // sees its COL pass before its ROW pass (forward) and vice versa (inverse).
+#include <algorithm>
 #include <cstdlib>
 
 #include "hx_internal.h"
@@ -23,6 +24,8 @@ void launch_pass(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cud
   a.lt = lt;
   a.logn = c->logn;
   a.instances = batch * lt.count;
+  a.batch = batch;
+  a.bper = 1;
   const long long tiles = c->N() / TILE;
   const long long blocks = a.instances * tiles;
   if (blocks <= 0) return;
@@ -76,6 +79,16 @@ void ntt_forward(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cud
   if (ti.count) dispatch<true, true, false>(c, b, data, batch, ti, s);   // last b stages (ROW)
   if (tf.count) dispatch<true, true, true>(c, b, data, batch, tf, s);
 }
+
+void ntt_forward_rows(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
+  const int a = split_a(c->logn), b = c->logn - a;
+  LimbTable ti, tf;
+  split(c, lt, ti, tf);
+  if (ti.count) dispatch<true, true, false>(c, b, data, batch, ti, s);
+  if (tf.count) dispatch<true, true, true>(c, b, data, batch, tf, s);
+}
+
+int ntt_split_a(int logn) { return split_a(logn); }
 
 void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
   const int a = split_a(c->logn), b = c->logn - a;

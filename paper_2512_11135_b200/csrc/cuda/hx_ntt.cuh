@@ -43,6 +43,8 @@ struct NttArgs {
   LimbTable lt;
   int logn;
   long long instances;  // batch * lt.count
+  long long batch;      // batch elements
+  int bper;             // batch elements per CTA (the grid is pairs x chunks)
 };
 
 // Deposit free index f around the w group bits starting at bit lowbits.
@@ -124,6 +126,17 @@ __device__ __forceinline__ double mulmod_f64(double y, double w, double wq, doub
   return __dadd_rn(r, l);
 }
 
+// Same product without a per-twiddle w / q: the quotient is taken from the
+// rounded product, qf = rint(h / q) (|h / q - qf| <= 1/2 + 2^-7 for
+// y w < 2^99), so r = h - qf q is exact in one FMA and |r + l| < q as before.
+__device__ __forceinline__ double mulmod_f64h(double y, double w, double qinv, double q) {
+  const double h = __dmul_rn(y, w);
+  const double l = __fma_rn(y, w, -h);
+  const double qf = __dsub_rn(__fma_rn(h, qinv, kRound), kRound);
+  const double r = __fma_rn(-qf, q, h);
+  return __dadd_rn(r, l);
+}
+
 // centre v into [-q/2 - eps, q/2 + eps]
 __device__ __forceinline__ double centre_f64(double v, double q, double qinv) {
   const double qf = __dsub_rn(__fma_rn(v, qinv, kRound), kRound);
@@ -179,20 +192,19 @@ __device__ __forceinline__ void ntt_group_f64(u64 (&x)[16], const int (&jb)[16 >
         const int rb = (ro << W) | (hp << (i + 1));
         const u64 j = (u64)jb[ro] + ((u64)(hp << (i + 1)) << (logb + g0));
         const bool fin = (!FWD) && last_stage_inv && (beta == logn - 1);
-        double2 wt = make_double2(0.0, 0.0);
+        double wt = 0.0;
         if (!fin) {
           if (ROW)
-            wt.x = sm_tw[row_tw_offset<S, OB>(beta) + row_tw_pad((int)((j & ((1u << (S + OB)) - 1)) >> (beta + 1)))];
+            wt = sm_tw[row_tw_offset<S, OB>(beta) + row_tw_pad((int)((j & ((1u << (S + OB)) - 1)) >> (beta + 1)))];
           else
-            wt.x = __ldg(tw + ((N + j) >> (beta + 1)));
-          wt.y = __dmul_rn(wt.x, P.qinv_d);  // w / q (relative error <= 2^-52)
+            wt = __ldg(tw + ((N + j) >> (beta + 1)));
         }
 #pragma unroll
         for (int lp = 0; lp < (1 << i); ++lp) {
           const int r0 = rb | lp, r1 = r0 | (1 << i);
           const double X = v[r0], Y = v[r1];
           if (FWD) {
-            const double T = mulmod_f64(Y, wt.x, wt.y, q);
+            const double T = mulmod_f64h(Y, wt, P.qinv_d, q);
             v[r0] = __dadd_rn(X, T);
             v[r1] = __dsub_rn(X, T);
           } else if (fin) {
@@ -200,7 +212,7 @@ __device__ __forceinline__ void ntt_group_f64(u64 (&x)[16], const int (&jb)[16 >
             v[r1] = mulmod_f64(__dsub_rn(X, Y), P.w1n_d, P.w1n_q, q);
           } else {
             v[r0] = __dadd_rn(X, Y);
-            v[r1] = mulmod_f64(__dsub_rn(X, Y), wt.x, wt.y, q);
+            v[r1] = mulmod_f64h(__dsub_rn(X, Y), wt, P.qinv_d, q);
           }
         }
       }

@@ -22,6 +22,7 @@
 #include "../../../include/hx_b200.h"
 #include "hx_internal.h"
 #include "hx_kernels.cuh"
+#include "hx_modup.cuh"
 
 using hx::LimbTable;
 using hx::PrimeConst;
@@ -226,6 +227,48 @@ void automorphism(hx_ctx* c, u64* out, const u64* in, long long batch, const Lim
 
 // ---- key-switch building blocks ----
 
+// ---- fused ModUp bconv + forward COL pass (hx_modup.cuh) ----
+template <int S, int MAXA>
+void launch_modup_col_t(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, cudaStream_t s) {
+  constexpr int OB = 3, TILE = 1 << (S + OB);
+  auto kern = hx::modup_col_kernel<S, OB, MAXA>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * TILE * (1 + MAXA));
+    configured = true;
+  }
+  dim3 grid((unsigned)(c->N() / TILE), (unsigned)A.dnum, (unsigned)batch);
+  kern<<<grid, TILE / 16, hx::modup_col_smem_bytes(S, OB, c->alpha), s>>>(A);
+  launched(c, "modup_col_kernel");
+}
+
+template <int S>
+bool launch_modup_col_a(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, cudaStream_t s) {
+  switch (c->alpha) {
+    case 1: launch_modup_col_t<S, 1>(c, A, batch, s); return true;
+    case 2: launch_modup_col_t<S, 2>(c, A, batch, s); return true;
+    case 3: launch_modup_col_t<S, 3>(c, A, batch, s); return true;
+    case 4: launch_modup_col_t<S, 4>(c, A, batch, s); return true;
+    default: return false;
+  }
+}
+
+bool launch_modup_col(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, cudaStream_t s) {
+  switch (hx::ntt_split_a(c->logn)) {
+    case 5: return launch_modup_col_a<5>(c, A, batch, s);
+    case 6: return launch_modup_col_a<6>(c, A, batch, s);
+    case 7: return launch_modup_col_a<7>(c, A, batch, s);
+    case 8: return launch_modup_col_a<8>(c, A, batch, s);
+    default: return false;
+  }
+}
+
+bool modup_fused_ok(const hx_ctx* c, int n_q) {
+  static const bool off = getenv("HX_MODUP_UNFUSED") != nullptr;
+  const int a = hx::ntt_split_a(c->logn);
+  return !off && a >= 5 && a <= 8 && c->alpha <= 4 && c->dnum(n_q) <= hx::kMaxDigits;
+}
+
 // c1: [batch] polys of n_q limbs at stride c1_stride words.
 void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long batch, int n_q,
            cudaStream_t s) {
@@ -234,6 +277,59 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
   DBuf coef(batch * n_q * N, s, c);
   copy2d(coef.p, n_q * N, c1, c1_stride, n_q * N, batch, s);
   hx::ntt_inverse(c, coef.p, batch, hx::make_table(c, n_q, 0), s);
+  if (modup_fused_ok(c, n_q)) {
+    // conversion fused into the COL pass (one launch per prime class), the
+    // digits' own limbs copied from the NTT-domain input, then the ROW pass
+    hx::ModUpColArgs A{};
+    A.coef = coef.p;
+    A.out = digits;
+    A.pc = c->d_pc;
+    A.qhinv = c->d_modup;
+    A.bc = c->d_bconv;
+    A.tlist = c->d_tlist;
+    A.alpha = c->alpha;
+    A.n_q = n_q;
+    A.n_chain = c->n_chain;
+    A.ext = ext;
+    A.dnum = dnum;
+    A.logn = c->logn;
+    LimbTable lt{};
+    lt.stride = dnum * ext;
+    for (int d = 0; d < dnum; ++d) {
+      A.qh_off[d] = c->modup_qh_off[n_q][d];
+      A.bc_off[d] = c->bc_off[n_q][d];
+      const int lo = d * c->alpha, cnt = std::min(c->alpha, n_q - lo);
+      copy2d(digits + ((long long)d * ext + lo) * N, (long long)dnum * ext * N, c1 + (long long)lo * N, c1_stride,
+             (long long)cnt * N, batch, s);
+      for (int j = 0; j < ext; ++j) {
+        if (j >= lo && j < lo + cnt) continue;
+        HX_REQUIRE(lt.count < hx::kMaxLimbEntries, "modup: too many limbs for one launch");
+        lt.off[lt.count] = (unsigned short)(d * ext + j);
+        lt.prime[lt.count] = (unsigned char)c->pidx(j, n_q);
+        ++lt.count;
+      }
+    }
+    int total = 0;
+    for (int d = 0; d < dnum; ++d) {
+      A.toff[d] = c->tl_off[n_q][d];
+      A.tcnt[d] = c->tl_cnt[n_q][d];
+      A.icnt[d] = c->tl_icnt[n_q][d];
+      total += A.tcnt[d] + A.icnt[d];
+    }
+    if (total) HX_REQUIRE(launch_modup_col(c, A, batch, s), "modup: fused path unavailable");
+    // integer-class limbs: full forward NTT; FP64-class limbs: ROW pass only
+    LimbTable li{}, lf{};
+    li.stride = lf.stride = lt.stride;
+    for (int e = 0; e < lt.count; ++e) {
+      LimbTable& x = c->f64[lt.prime[e]] ? lf : li;
+      x.off[x.count] = lt.off[e];
+      x.prime[x.count] = lt.prime[e];
+      ++x.count;
+    }
+    if (li.count) hx::ntt_forward(c, digits, batch, li, s);
+    if (lf.count) hx::ntt_forward_rows(c, digits, batch, lf, s);
+    return;
+  }
   // basis conversion per digit (coefficient domain), own limbs copied (NTT)
   LimbTable lt{};
   lt.stride = dnum * ext;
@@ -723,6 +819,58 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
       }
     }
     c->d_modup = upload(mu);
+    // Fused ModUp (hx_modup.cuh): conversion constants per (n_q, digit) as
+    // [ext][alpha] BconvC and per-class target limb lists per (n_q, digit)
+    {
+      std::vector<hx::BconvC> bc;
+      std::vector<int> tl;
+      c->bc_off.assign(n_chain + 1, {});
+      c->tl_off.assign(n_chain + 1, {});
+      c->tl_cnt.assign(n_chain + 1, {});
+      c->tl_icnt.assign(n_chain + 1, {});
+      for (int nq = 1; nq <= n_chain; ++nq) {
+        const int dn = c->dnum(nq), ext = nq + n_special;
+        for (int d = 0; d < dn; ++d) {
+          const int lo = d * alpha, cnt = std::min(alpha, nq - lo);
+          c->bc_off[nq].push_back((long long)bc.size());
+          for (int j = 0; j < ext; ++j) {
+            const int pj = c->pidx(j, nq);
+            const u64 m = c->primes[pj];
+            for (int ii = 0; ii < alpha; ++ii) {
+              hx::BconvC e{};
+              if (ii < cnt) {
+                const int i = lo + ii;
+                u64 prod = 1;
+                for (int i2 = lo; i2 < lo + cnt; ++i2)
+                  if (i2 != i) prod = hmul(prod, c->primes[i2] % m, m);
+                const SC w = sc(prod, m);
+                const u64 w30 = hmul(prod, (1ull << 30) % m, m);
+                e.w = (double)prod;
+                e.wq = (double)prod / (double)m;
+                e.w30 = (double)w30;
+                e.w30q = (double)w30 / (double)m;
+                e.sw = w.w;
+                e.swp = w.wp;
+              }
+              bc.push_back(e);
+            }
+          }
+          c->tl_off[nq].push_back((int)tl.size());
+          for (int cls = 0; cls < 2; ++cls) {  // FP64-class targets first, then integer ones
+            int n = 0;
+            for (int j = 0; j < ext; ++j) {
+              if (j >= lo && j < lo + cnt) continue;
+              if ((c->f64[c->pidx(j, nq)] != 0) != (cls == 0)) continue;
+              tl.push_back(j);
+              ++n;
+            }
+            (cls == 0 ? c->tl_cnt : c->tl_icnt)[nq].push_back(n);
+          }
+        }
+      }
+      c->d_bconv = upload(bc);
+      c->d_tlist = upload(tl);
+    }
     // ModDown constants
     std::vector<SC> phinv(n_special), pconv((size_t)n_special * n_chain), pinv(n_chain);
     std::vector<u64> pmodq(n_chain);
@@ -800,7 +948,8 @@ void hx_ctx_destroy(hx_ctx* c) {
   if (!c) return;
   for (void* p : {(void*)c->d_pc, (void*)c->d_tw, (void*)c->d_twf, (void*)c->d_modup, (void*)c->d_phinv,
                   (void*)c->d_pconv, (void*)c->d_pmodq, (void*)c->d_pinv, (void*)c->d_qlinv,
-                  (void*)c->d_qlmod, (void*)c->d_maclimbs, (void*)c->d_kslimbs})
+                  (void*)c->d_qlmod, (void*)c->d_maclimbs, (void*)c->d_kslimbs, (void*)c->d_bconv,
+                  (void*)c->d_tlist})
     if (p) cudaFree(p);
   if (c->arena.base) {
     cudaStreamSynchronize(c->arena.stream);

@@ -101,6 +101,24 @@ def mactime(n1=32, n2=32):
     print(f"bsgs_mac n1={n1} n2={n2}: {ms:.3f} ms  diag {gb:.2f} GB  {gb / ms:.2f} TB/s")
 
 
+def nttscale():
+    """forward-NTT limb throughput vs batch (L2-resident small batches vs HBM-sized)"""
+    chain, special = bench.primes()
+    ctx = Context(bench.LOGN, chain, special, bench.ALPHA)
+    dev = torch.device("cuda", 0)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1)
+    nq = len(chain)
+    for B in (1, 2, 4, 16, 64, 256):
+        x = bench.rand_limbs(torch, gen, chain, (B, 2), dev)
+        reps = max(1, 256 // B)
+        ms = timed(lambda: [ctx.ntt_fwd(x, 2 * B, nq, 0) for _ in range(reps)], iters=3) / reps
+        limbs = 2 * B * nq
+        print(f"B={B:4d} limbs={limbs:6d} MB={limbs * bench.N * 8 / 1e6:8.1f}  {ms * 1e3:9.1f} us  "
+              f"{limbs / ms * 1e3 / 1e6:.3f} M limb/s", flush=True)
+        del x
+
+
 def ffnloop(iters=8):
     import time
 
@@ -131,6 +149,8 @@ if __name__ == "__main__":
         ffn()
     elif len(sys.argv) > 1 and sys.argv[1] == "ffnloop":
         ffnloop()
+    elif len(sys.argv) > 1 and sys.argv[1] == "nttscale":
+        nttscale()
     elif len(sys.argv) > 1 and sys.argv[1] == "mactime":
         mactime(*[int(a) for a in sys.argv[2:4]])
     else:
