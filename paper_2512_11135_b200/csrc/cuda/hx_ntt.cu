@@ -10,13 +10,17 @@
 
 #include "hx_internal.h"
 
+#ifndef HX_NTT_OB
+#define HX_NTT_OB 3
+#endif
+
 namespace hx {
 
 namespace {
 
 template <bool FWD, bool ROW, int S, bool F64>
 void launch_pass(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
-  constexpr int OB = 4;
+  constexpr int OB = HX_NTT_OB;
   constexpr int TILE = 1 << (S + OB);
   NttArgs a;
   a.data = data;

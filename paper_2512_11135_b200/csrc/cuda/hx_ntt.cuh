@@ -175,6 +175,29 @@ __device__ __forceinline__ void ntt_group_f64(u64 (&x)[16], const int (&jb)[16 >
   const int logb = ROW ? 0 : (logn - S);
   const double q = P.qd;
   const u64 N = 1ull << logn;
+  // every twiddle of the group is fetched up front (all loads in flight
+  // together, 32-bit indices) instead of one dependent load per stage
+  double wts[W][8];
+#pragma unroll
+  for (int i = 0; i < W; ++i) {
+    const int beta = logb + g0 + i;
+#pragma unroll
+    for (int ro = 0; ro < NO; ++ro) {
+#pragma unroll
+      for (int hp = 0; hp < (1 << (W - 1 - i)); ++hp) {
+        const unsigned j = (unsigned)jb[ro] + ((unsigned)(hp << (i + 1)) << (logb + g0));
+        const bool fin = (!FWD) && last_stage_inv && (beta == logn - 1);
+        double wt = 0.0;
+        if (!fin) {
+          if (ROW)
+            wt = sm_tw[row_tw_offset<S, OB>(beta) + row_tw_pad((int)((j & ((1u << (S + OB)) - 1)) >> (beta + 1)))];
+          else
+            wt = __ldg(tw + (((unsigned)N + j) >> (beta + 1)));
+        }
+        wts[i][ro * (1 << (W - 1 - i)) + hp] = wt;
+      }
+    }
+  }
   double v[16];
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
@@ -190,15 +213,8 @@ __device__ __forceinline__ void ntt_group_f64(u64 (&x)[16], const int (&jb)[16 >
 #pragma unroll
       for (int hp = 0; hp < (1 << (W - 1 - i)); ++hp) {
         const int rb = (ro << W) | (hp << (i + 1));
-        const u64 j = (u64)jb[ro] + ((u64)(hp << (i + 1)) << (logb + g0));
         const bool fin = (!FWD) && last_stage_inv && (beta == logn - 1);
-        double wt = 0.0;
-        if (!fin) {
-          if (ROW)
-            wt = sm_tw[row_tw_offset<S, OB>(beta) + row_tw_pad((int)((j & ((1u << (S + OB)) - 1)) >> (beta + 1)))];
-          else
-            wt = __ldg(tw + ((N + j) >> (beta + 1)));
-        }
+        const double wt = wts[i][ro * (1 << (W - 1 - i)) + hp];
 #pragma unroll
         for (int lp = 0; lp < (1 << i); ++lp) {
           const int r0 = rb | lp, r1 = r0 | (1 << i);
