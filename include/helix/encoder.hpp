@@ -38,6 +38,19 @@ class CkksEncoder {
   };
   Embedding embed_real(std::span<const double> m) const;
 
+  // Tables of the device encoder (hx_encoder_create, include/hx_b200.h), all
+  // computed here on the host with the same libm calls and recurrences as
+  // encode_coeffs so the device result is bit-identical:
+  //   perm[i]     = slot j whose value lands at position i after the FFT's bit
+  //                 reversal, | 1<<31 when it is the conjugate mirror;
+  //   stage_tw    = for len = 2, 4, ..., N the len/2 inverse-FFT twiddles
+  //                 (w_0 = 1, w_{j+1} = w_j * wn), interleaved re/im;
+  //   zeta        = zeta^t, t < N, interleaved re/im.
+  void device_tables(std::vector<std::int32_t>& perm, std::vector<double>& stage_tw,
+                     std::vector<double>& zeta) const;
+  // log2(Q_level / 2): the capacity bound of encode_coeffs
+  double capacity_log2(int level) const;
+
   std::size_t slot_count() const { return n_slots_; }
   std::size_t ring_degree() const { return n_; }
 

@@ -24,6 +24,7 @@
 #include "helix/encoder.hpp"
 
 struct hx_ctx;
+struct hx_encoder;
 
 namespace helix {
 
@@ -128,12 +129,16 @@ class GpuLatticeBackend final : public SlotBackend {
   std::shared_ptr<DeviceBuffer> make_key(const std::shared_ptr<DeviceBuffer>& sprime_or_null,
                                          std::uint64_t galois_elt);
   int nq(int level) const { return level + 1; }
+  // device encoder (hx_encode): n messages -> NTT-domain plaintext words at out
+  void encode_device(const std::vector<const std::vector<double>*>& msgs, int level, const Scale& scale,
+                     std::uint64_t* out);
 
   CkksParams params_;
   CkksEncoder enc_;
   OpTrace trace_;
   RotationKeySet rot_set_;
   hx_ctx* ctx_ = nullptr;
+  hx_encoder* henc_ = nullptr;  // created on first encode
   std::uint64_t rng_[4];
   std::shared_ptr<DeviceBuffer> s_full_;  // [n_chain + K][N], NTT
   std::shared_ptr<DeviceBuffer> rlk_;     // relinearisation key (standard layout)

@@ -106,6 +106,10 @@ const uint64_t* hxc_rotation_key_ptr(hxc_backend* b, int64_t k);
 const uint64_t* hxc_matrix_payload_ptr(const hxc_mat* m, int i);
 int hxc_matrix_payload_count(const hxc_mat* m);
 /* host-only: CkksEncoder::encode_coeffs for a CkksParams JSON (no device) */
+/* device encode (GpuLatticeBackend::encode: hx_encode + RNS lift + NTT) of m at
+ * `level` with a raw double scale; out: host [level+1][N] NTT-domain words.
+ * -1 with hxc_last_error() on error (std::overflow_error text on capacity). */
+int hxc_encode_words(hxc_backend* b, const double* m, int len, int level, double scale, uint64_t* out);
 int hxc_encode_coeffs(const char* params_json, const double* m, int len, int level, double scale,
                       int64_t* out);
 

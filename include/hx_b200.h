@@ -39,6 +39,7 @@ extern "C" {
 #define HX_ERR_INVALID 1
 #define HX_ERR_CUDA 2
 #define HX_ERR_UNSUPPORTED 3
+#define HX_ERR_OVERFLOW 4  /* encode: a coefficient exceeds the level's capacity */
 
 typedef struct hx_ctx hx_ctx;
 
@@ -187,6 +188,21 @@ int hx_rotate_host(hx_ctx* ctx, uint64_t* out_host, const uint64_t* in_host, con
 int hx_mul_relin_host(hx_ctx* ctx, uint64_t* out_host, const uint64_t* a_host,
                       const uint64_t* b_host, const uint64_t* rlk, int batch, int n_q,
                       void* stream);
+
+/* ---- CKKS encoder on the device ----
+ * Replaces CkksEncoder::encode (reference encoder.cpp:69-117) for batches of
+ * real slot vectors: int64 coefficients bit-identical to the host encoder.
+ * Tables come from the host (helix::CkksEncoder::device_tables): perm [N]
+ * int32, stage_tw [N-1] complex (re, im interleaved), zeta [N] complex. */
+typedef struct hx_encoder hx_encoder;
+hx_encoder* hx_encoder_create(hx_ctx* ctx, const int32_t* perm, const double* stage_tw, const double* zeta);
+void hx_encoder_destroy(hx_encoder* enc);
+/* coeffs (device) [batch][N] int64 <- round(scale * embed^-1(m_b)), m (device)
+ * [batch] vectors of len_m <= N/2 doubles at stride m_stride (zero padded).
+ * HX_ERR_OVERFLOW when some |coefficient| >= 2^62 or log2(|c| + 1) >= cap_log2
+ * (log2(Q_level / 2), CkksEncoder::capacity_log2).  Synchronises `stream`. */
+int hx_encode(hx_encoder* enc, int64_t* coeffs, const double* m, int len_m, long long m_stride, int batch,
+              double scale, double cap_log2, void* stream);
 
 #ifdef __cplusplus
 }

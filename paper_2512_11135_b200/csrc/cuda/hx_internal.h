@@ -89,5 +89,7 @@ void ntt_forward_rows(hx_ctx* c, u64* data, long long batch, const LimbTable& lt
 int ntt_split_a(int logn);
 
 void set_error(const std::string& msg);
+// record `msg` as hx_last_error() and return `code` (C-ABI entry points outside hx_ops.cu)
+int fail(int code, const std::string& msg);
 
 }  // namespace hx

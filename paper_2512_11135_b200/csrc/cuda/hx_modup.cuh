@@ -157,7 +157,7 @@ __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, c
 // 64-bit Shoup butterflies need more registers and latency hiding than this
 // kernel's occupancy (3 CTAs of 128 threads per SM) gives them.
 template <int S, int OB, int MAXA>
-__global__ void __launch_bounds__((1 << (S + OB)) / 16, 3) modup_col_kernel(ModUpColArgs A) {
+__global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup_col_kernel(ModUpColArgs A) {
   constexpr int TILE = 1 << (S + OB);
   constexpr int T = TILE / 16;
   extern __shared__ u64 dyn_smem[];

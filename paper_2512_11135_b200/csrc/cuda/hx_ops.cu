@@ -674,6 +674,10 @@ void pipelined_host(hx_ctx* c, int batch, std::vector<const uint64_t*> in_host,
 namespace hx {
 
 void set_error(const std::string& msg) { throw HxError(HX_ERR_UNSUPPORTED, msg); }
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
 
 LimbTable make_table(const hx_ctx* c, int n_q, int n_p, int stride, int first) {
   LimbTable lt{};

@@ -108,6 +108,7 @@ GpuLatticeBackend::~GpuLatticeBackend() {
   rlk_.reset();
   s_full_.reset();
   cudaStreamSynchronize(nullptr);
+  hx_encoder_destroy(henc_);
   hx_ctx_destroy(ctx_);
 }
 
@@ -213,18 +214,53 @@ Ciphertext GpuLatticeBackend::wrap(std::shared_ptr<DeviceBuffer> buf, std::size_
 }
 
 // ------------------------------------------------------------- encode / decode
+// Encoding runs on the device (hx_encode, bit-identical to CkksEncoder::
+// encode_coeffs), then the RNS lift and NTT; messages go in chunks of 1024.
+void GpuLatticeBackend::encode_device(const std::vector<const std::vector<double>*>& msgs, int level,
+                                      const Scale& scale, std::uint64_t* out) {
+  if (!scale.is_positive()) throw std::invalid_argument("encode: non-positive scale");
+  if (level < 0 || level > params_.max_level) throw std::invalid_argument("encode: level out of range");
+  const std::size_t N = params_.ring_degree, S = slots();
+  for (const auto* m : msgs)
+    if (m->size() > S) throw std::invalid_argument("encode: vector longer than slot count");
+  if (!henc_) {
+    std::vector<std::int32_t> perm;
+    std::vector<double> tw, zeta;
+    enc_.device_tables(perm, tw, zeta);
+    henc_ = hx_encoder_create(ctx_, perm.data(), tw.data(), zeta.data());
+    if (!henc_) throw std::runtime_error("hx_encoder_create failed");
+  }
+  const int n = nq(level);
+  const double cap = enc_.capacity_log2(level);
+  const std::size_t chunk = std::min<std::size_t>(msgs.size(), 1024);
+  std::size_t width = 1;
+  for (const auto* m : msgs) width = std::max(width, m->size());
+  std::vector<double> host(chunk * width);
+  DeviceBuffer dm(chunk * width), dc(chunk * N);
+  for (std::size_t c0 = 0; c0 < msgs.size(); c0 += chunk) {
+    const std::size_t k = std::min(chunk, msgs.size() - c0);
+    std::fill(host.begin(), host.end(), 0.0);
+    for (std::size_t i = 0; i < k; ++i)
+      std::memcpy(host.data() + i * width, msgs[c0 + i]->data(), msgs[c0 + i]->size() * 8);
+    cuda_ck(cudaMemcpy(dm.ptr, host.data(), k * width * 8, cudaMemcpyHostToDevice), "h2d");
+    const int rc = hx_encode(henc_, (int64_t*)dc.ptr, (const double*)dm.ptr, (int)width, (long long)width, (int)k,
+                             scale.to_double(), cap, nullptr);
+    if (rc == HX_ERR_OVERFLOW) throw std::overflow_error(hx_last_error());
+    ck(rc, "encode");
+    std::uint64_t* o = out + c0 * n * N;
+    ck(hx_from_i64(ctx_, o, (const int64_t*)dc.ptr, (int)k, n, 0, nullptr), "from_i64");
+    ck(hx_ntt_fwd(ctx_, o, (int)k, n, 0, nullptr), "ntt");
+  }
+  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+}
+
 Plaintext GpuLatticeBackend::encode(std::span<const double> m, int level, const Scale& scale) {
   if (m.size() > slots()) throw std::invalid_argument("encode: vector longer than slot count");
   if (!scale.is_positive()) throw std::invalid_argument("encode: non-positive scale");
   if (level < 0 || level > params_.max_level) throw std::invalid_argument("encode: level out of range");
-  const auto coeffs = enc_.encode_coeffs(m, level, scale.to_double());
-  const std::size_t N = params_.ring_degree;
-  DeviceBuffer dc(N);
-  cuda_ck(cudaMemcpyAsync(dc.ptr, coeffs.data(), N * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
-  auto buf = dev((std::size_t)nq(level) * N);
-  ck(hx_from_i64(ctx_, buf->ptr, (const int64_t*)dc.ptr, 1, nq(level), 0, nullptr), "from_i64");
-  ck(hx_ntt_fwd(ctx_, buf->ptr, 1, nq(level), 0, nullptr), "ntt");
-  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+  const std::vector<double> v(m.begin(), m.end());
+  auto buf = dev((std::size_t)nq(level) * params_.ring_degree);
+  encode_device({&v}, level, scale, buf->ptr);
   auto p = std::make_shared<GpuPlaintext>();
   p->buf = buf;
   p->n_q = nq(level);
@@ -241,53 +277,26 @@ std::vector<Plaintext> GpuLatticeBackend::encode_many(const std::vector<std::vec
   if (level < 0 || level > params_.max_level) throw std::invalid_argument("encode: level out of range");
   const std::size_t N = params_.ring_degree;
   const int n = nq(level);
-  std::size_t nz = 0;
-  for (const auto& m : msgs) nz += !m.empty();
+  std::vector<const std::vector<double>*> src;  // non-empty messages
+  for (const auto& m : msgs)
+    if (!m.empty()) src.push_back(&m);
   std::vector<Plaintext> out(msgs.size());
-  if (nz == 0) return out;
-  auto buf = dev(nz * n * N);
-  std::vector<std::int64_t> coeffs(nz * N);
-  std::vector<std::size_t> src;  // non-empty message indices
-  for (std::size_t i = 0; i < msgs.size(); ++i)
-    if (!msgs[i].empty()) src.push_back(i);
-  // host FFT encodes are independent: spread them over the host cores
-  const unsigned hw = std::max(1u, std::min(std::thread::hardware_concurrency(), 32u));
-  const std::size_t nt = std::min<std::size_t>(hw, src.size());
-  std::vector<std::thread> pool;
-  std::exception_ptr err;
-  std::mutex err_mu;
-  for (std::size_t w = 0; w < nt; ++w)
-    pool.emplace_back([&, w] {
-      try {
-        for (std::size_t k = w; k < src.size(); k += nt) {
-          const auto c = enc_.encode_coeffs(msgs[src[k]], level, scale.to_double());
-          std::memcpy(coeffs.data() + k * N, c.data(), N * 8);
-        }
-      } catch (...) {
-        std::lock_guard<std::mutex> g(err_mu);
-        err = std::current_exception();
-      }
-    });
-  for (auto& th : pool) th.join();
-  if (err) std::rethrow_exception(err);
-  std::size_t idx = 0;
-  DeviceBuffer dc(coeffs.size());
-  cuda_ck(cudaMemcpyAsync(dc.ptr, coeffs.data(), coeffs.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
-  ck(hx_from_i64(ctx_, buf->ptr, (const int64_t*)dc.ptr, (int)nz, n, 0, nullptr), "from_i64");
-  ck(hx_ntt_fwd(ctx_, buf->ptr, (int)nz, n, 0, nullptr), "ntt");
-  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
-  idx = 0;
-  for (std::size_t i = 0; i < msgs.size(); ++i) {
-    Plaintext& pt = out[i];
+  for (auto& pt : out) {
     pt.level = level;
     pt.scale = scale;
     pt.slot_count = slots();
+  }
+  if (src.empty()) return out;
+  auto buf = dev(src.size() * n * N);
+  encode_device(src, level, scale, buf->ptr);
+  std::size_t idx = 0;
+  for (std::size_t i = 0; i < msgs.size(); ++i) {
     if (msgs[i].empty()) continue;
     auto p = std::make_shared<GpuPlaintext>();
     p->buf = buf;
     p->offset = idx * n * N;
     p->n_q = n;
-    pt.payload = p;
+    out[i].payload = p;
     ++idx;
   }
   return out;

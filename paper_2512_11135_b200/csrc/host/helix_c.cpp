@@ -235,6 +235,17 @@ const uint64_t* hxc_matrix_payload_ptr(const hxc_mat* m, int i) {
 }
 int hxc_matrix_payload_count(const hxc_mat* m) { return (int)m->m.pts.size(); }
 
+int hxc_encode_words(hxc_backend* b, const double* m, int len, int level, double scale, uint64_t* out) {
+  return guard(-1, [&] {
+    auto& be = *b->b;
+    const auto pt = be.encode(std::span<const double>(m, len), level, Scale::raw(scale));
+    const std::size_t w = (std::size_t)(level + 1) * be.params().ring_degree;
+    if (cudaMemcpy(out, GpuLatticeBackend::payload(pt).data(), w * 8, cudaMemcpyDeviceToHost) != cudaSuccess)
+      throw std::runtime_error("hxc_encode_words: copy failed");
+    return 0;
+  });
+}
+
 int hxc_encode_coeffs(const char* json, const double* m, int len, int level, double scale, int64_t* out) {
   return guard(-1, [&] {
     const CkksEncoder enc(CkksParams::from_json(json));

@@ -74,6 +74,7 @@ def lib():
         "hxc_matrix_payload_ptr": (v, [v, i32]),
         "hxc_matrix_payload_count": (i32, [v]),
         "hxc_encode_coeffs": (i32, [C.c_char_p, f64p, i32, i32, C.c_double, C.POINTER(C.c_int64)]),
+        "hxc_encode_words": (i32, [v, f64p, i32, i32, C.c_double, C.POINTER(C.c_uint64)]),
         "hxc_trace_json": (i32, [v, C.c_char_p, i32]),
         "hxc_trace_reset": (None, [v]),
         "hxc_sync": (i32, []),
@@ -171,6 +172,7 @@ class Backend:
 
     def __init__(self, pjson: str, seed: int = 1):
         self.L = lib()
+        self.pjson = pjson
         self.h = self.L.hxc_backend_create(pjson.encode(), seed)
         if not self.h:
             raise _err()
@@ -271,6 +273,15 @@ class Backend:
         arr = (C.c_int64 * cnt)()
         L.hxc_matmul_rotations(d, arr, cnt)
         return list(arr)
+
+    def encode_words(self, m, level, scale):
+        """device encode -> host [level+1][N] NTT-domain words"""
+        a, ap = _dp(m)
+        n = json.loads(self.pjson)["N"]
+        out = np.zeros((level + 1) * n, dtype=np.uint64)
+        if self.L.hxc_encode_words(self.h, ap, len(a), level, scale, out.ctypes.data_as(C.POINTER(C.c_uint64))) != 0:
+            raise _err()
+        return out.reshape(level + 1, n)
 
     def trace(self):
         buf = C.create_string_buffer(4096)
