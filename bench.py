@@ -25,6 +25,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
@@ -255,39 +257,52 @@ def run_reference_arm(args):
     return 0
 
 
-def ffn_bsgs_bench(torch, chain, special, args, iters=5):
-    """BASELINE configs[2]: FFN up-projection W1 (768 x 3072, N(0, 0.02^2)) as a
-    BSGS linear transform at N=2^16 / 24+3 primes through the helix C-ABI
-    (hxc_matvec): d = 1024, 3 row blocks, n1 = n2 = 32, one token per
-    ciphertext (T = 1), plus the 90%-diagonal-pruned variant."""
-    import numpy as np
+def _prune_diagonals(M, d, rng, frac=0.9):
+    """zero `frac` of the generalized diagonals of every d x d row block (seeded)"""
+    rows, cols = M.shape
+    for b in range((rows + d - 1) // d):
+        for i in rng.choice(d, int(round(frac * d)), replace=False):
+            r = np.arange(d)
+            c = (i + r) % d
+            keep = (c < cols) & (b * d + r < rows)
+            M[b * d + r[keep], c[keep]] = 0.0
+    return M
 
+
+def ffn_bsgs_bench(torch, chain, special, args, iters=5):
+    """BASELINE configs[2]: FFN up-projection W1 (768 x 3072) and down-projection
+    W2 (3072 x 768), N(0, 0.02^2), as BSGS linear transforms at N=2^16 / 24+3
+    primes through the helix C-ABI (hxc_matvec): W1 d = 1024, 3 row blocks,
+    n1 = n2 = 32; W2 d = 4096, 1 block, n1 = n2 = 64; one token per ciphertext
+    (T = 1), plus the 90%-diagonal-pruned variants.  Diagonals are encoded on
+    the device (hx_encode); prepare_s is encode + rotation-key generation."""
     from paper_2512_11135_b200.helix import BSGS, Backend, params_json
 
     rng = np.random.default_rng(20251211 * 10 + 3)
     be = Backend(params_json(LOGN, chain, special, ALPHA, 40), seed=3)
     out = {}
     W1 = rng.normal(0.0, 0.02, (768, 3072))
-    x = rng.uniform(-1, 1, 768)
-    xs = np.tile(np.concatenate([x, np.zeros(256)]), be.slots // 1024)
+    W2 = rng.normal(0.0, 0.02, (3072, 768))
     lvl = be.max_level
-    for name, prune in (("ffn_w1", False), ("ffn_w1_pruned90", True)):
-        M = W1.T.copy()  # y = x W1  ->  M = W1^T (3072 out x 768 in)
-        if prune:  # zero 90% of the generalized diagonals of every 1024 x 1024 block
-            for b in range(3):
-                for i in rng.choice(1024, 922, replace=False):
-                    r = np.arange(1024)
-                    c = (i + r) % 1024
-                    keep = c < 768
-                    M[b * 1024 + r[keep], c[keep]] = 0.0
+    prune_rng = np.random.default_rng(20251211 * 10 + 3 + 200)
+    jobs = [("ffn_w1", W1.T.copy(), 1024, False), ("ffn_w1_pruned90", W1.T.copy(), 1024, True)]
+    if not getattr(args, "no_w2", False):
+        jobs += [("ffn_w2", W2.T.copy(), 4096, False), ("ffn_w2_pruned90", W2.T.copy(), 4096, True)]
+    for name, M, d, prune in jobs:  # y = x W  ->  M = W^T (out x in)
+        if prune:
+            M = _prune_diagonals(M, d, prune_rng)
+        x = rng.uniform(-1, 1, M.shape[1])
+        xs = np.tile(np.concatenate([x, np.zeros(d - M.shape[1])]), be.slots // d)
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         mat = be.prepare(BSGS, M, lvl)
         be.gen_rotation_keys(mat.rotations())
+        torch.cuda.synchronize()
         prep = time.perf_counter() - t0
         ct = be.encrypt(xs, lvl)
-        for _ in range(3):  # warm-up (stream-ordered pool growth, first-launch setup) + correctness
+        for _ in range(3):  # warm-up (pool growth, first-launch setup) + correctness
             outs, rep = be.matvec(mat, ct)
-        y = np.concatenate([be.decrypt(o)[:1024] for o in outs])
+        y = np.concatenate([be.decrypt(o)[:d] for o in outs])[:M.shape[0]]
         err = float(np.abs(y - M @ x).max())
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -299,11 +314,48 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5):
         secs = e0.elapsed_time(e1) / 1e3 / iters
         info = mat.info()
         out[name] = {"matvec_per_s": 1.0 / secs, "ms_per_matvec": 1e3 * secs, "max_abs_err": err,
+                     "d": d, "n1": info["n1"], "n2": info["n2"], "row_blocks": info["blocks"],
                      "rotations": rep["rotations"], "pt_muls": rep["pt_muls"], "nonzero_diagonals": info["nonzero"],
                      "diag_bytes": info["nonzero"] * 24 * N * 8, "prepare_s": prep}
         del mat, outs, ct
+        torch.cuda.synchronize()
     be.close()
     return out
+
+
+def matmul_bench(torch, chain, special, d=128, n_q=4, iters=2):
+    """BASELINE configs[3]: ct x ct matmul Q K^T of one head (128 x 64 padded to
+    d = 128, N(0, 1)) through hxc_matmul (SPEC square-padded schedule), at a
+    4-limb level of the config-2 chain (q0 + 3 x 40-bit, K = 3 specials)."""
+    from paper_2512_11135_b200.helix import Backend, params_json
+
+    rng = np.random.default_rng(20251211 * 10 + 4)
+    be = Backend(params_json(LOGN, chain[:n_q], special, ALPHA, 40), seed=4)
+    Q = np.zeros((d, d))
+    Kt = np.zeros((d, d))
+    Q[:, :64] = rng.normal(0, 1, (128, 64))
+    Kt[:64, :] = rng.normal(0, 1, (128, 64)).T
+    t0 = time.perf_counter()
+    rots = Backend.matmul_rotations(d)
+    be.gen_rotation_keys(rots)
+    torch.cuda.synchronize()
+    prep = time.perf_counter() - t0
+    ca, cb = be.encrypt(Q.reshape(-1) / 8), be.encrypt(Kt.reshape(-1) / 8)
+    c, rep = be.matmul(ca, cb, d)  # warm-up + correctness
+    got = be.decrypt(c)[: d * d].reshape(d, d)
+    err = float(np.abs(got - (Q / 8) @ (Kt / 8)).max())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        c, rep = be.matmul(ca, cb, d)
+    e1.record()
+    torch.cuda.synchronize()
+    secs = e0.elapsed_time(e1) / 1e3 / iters
+    be.close()
+    return {"matmul_d128": {"matmul_per_s": 1.0 / secs, "ms_per_matmul": 1e3 * secs, "max_abs_err": err,
+                            "level_limbs": n_q, "rotations": rep["rotations"], "ct_muls": rep["ct_muls"],
+                            "pt_muls": rep["pt_muls"], "distinct_keys": len(rots), "keygen_s": prep}}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -315,7 +367,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extras", action="store_true")
-    ap.add_argument("--no-ffn", action="store_true", help="skip the config-3 BSGS matvec extra")
+    ap.add_argument("--no-ffn", action="store_true", help="skip the config-3/4 BSGS and matmul extras")
+    ap.add_argument("--no-w2", action="store_true", help="skip the W2 (d = 4096) FFN extras")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -447,6 +500,11 @@ def main():
         del hin, hout_h, out, ntt_buf
         torch.cuda.empty_cache()
         extras.update(ffn_bsgs_bench(torch, chain, special, args))
+        torch.cuda.empty_cache()
+        try:
+            extras.update(matmul_bench(torch, chain, special))
+        except Exception as exc:  # reported, never fatal for the headline line
+            extras["matmul_d128"] = {"error": str(exc)[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -160,6 +160,12 @@ int hx_bsgs_mac(hx_ctx* ctx, uint64_t* inner, const uint64_t* baby, const uint64
                 int diag_limbs, int n1, int n2, int n_q, void* stream);
 
 /* ---- keys / encryption ------------------------ */
+/* Device samplers (counter-based: splitmix64 of (seed, index)), used for key
+ * material so that key generation needs no host RNG stream or H2D copy:
+ * out [copies][n_c + n_s][N] uniform in [0, q) per limb (128-bit multiply-high
+ * reduction, bias < 2^-64); e [count] centred binomial (k = 21) int64. */
+int hx_sample_uniform(hx_ctx* ctx, uint64_t* out, int n_c, int n_s, int copies, uint64_t seed, void* stream);
+int hx_sample_cbd(hx_ctx* ctx, int64_t* e, long long count, uint64_t seed, void* stream);
 /* ksk_d = (-a_d s + e_d + [P]_{q_i} s' on the chain limbs of digit d, a_d).
  * s_full, sp_full [n_chain+K][N] NTT; a_full [dnum_max][n_chain+K][N];
  * e [dnum_max][N] int64; all device. */

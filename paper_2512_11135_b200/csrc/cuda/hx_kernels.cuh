@@ -516,6 +516,37 @@ __global__ void tensor_kernel(u64* out, const u64* a, const u64* b, const PrimeC
 
 // ------------------------------------------------------------ keys
 // ksk_d over the full basis: b = e - a s + [P]_{q_l} s' on chain limbs of digit d
+// ------------------------------------------------------------ samplers
+__device__ __forceinline__ u64 splitmix64(u64 x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// out [copies][limbs][N]: uniform mod the limb's prime, floor(r q / 2^128)
+// over 128 random bits r
+__global__ void sample_uniform_kernel(u64* out, const PrimeConst* pc, LimbTable lt, int logn, u64 seed) {
+  const long long N = 1ll << logn;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // word index
+  const long long limb = i >> logn;
+  const u64 q = pc[lt.prime[limb % lt.count]].q;
+  const u64 r0 = splitmix64(seed ^ splitmix64(2 * (u64)i));
+  const u64 r1 = splitmix64(seed ^ splitmix64(2 * (u64)i + 1));
+  const u64 t = mulhi64(r1, q);                    // floor(r1 q / 2^64)
+  const u64 lo = r0 * q, hi = mulhi64(r0, q);      // r0 q
+  const u64 sum = lo + t;
+  out[i] = hi + (sum < lo ? 1 : 0);                // floor((r0 2^64 + r1) q / 2^128)
+  (void)N;
+}
+
+__global__ void sample_cbd_kernel(long long* e, long long count, u64 seed) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const u64 r = splitmix64(seed ^ splitmix64((u64)i ^ 0xA5A5A5A5A5A5A5A5ull));
+  e[i] = (long long)__popcll(r & 0x1fffffull) - (long long)__popcll((r >> 21) & 0x1fffffull);
+}
+
 __global__ void keygen_kernel(u64* key, const u64* en, const u64* s_full, const u64* sp_full,
                               const u64* a_full, const PrimeConst* pc, const u64* pmodq,
                               int n_chain, int n_total, int alpha, int logn) {

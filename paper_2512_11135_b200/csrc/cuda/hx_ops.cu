@@ -1299,6 +1299,28 @@ int hx_sum_strided(hx_ctx* c, uint64_t* out, const uint64_t* in, int terms, long
   });
 }
 
+int hx_sample_uniform(hx_ctx* c, uint64_t* out, int n_c, int n_s, int copies, uint64_t seed, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_REQUIRE(n_c >= 0 && n_c <= c->n_chain && n_s >= 0 && n_s <= c->n_special && copies >= 0, "sample_uniform");
+    const long long words = (long long)copies * (n_c + n_s) * c->N();
+    if (!words) return;
+    const LimbTable lt = hx::make_table(c, n_c, n_s);
+    hx::sample_uniform_kernel<<<(unsigned)(words / 256), 256, 0, S(s)>>>((u64*)out, c->d_pc, lt, c->logn, seed);
+    launched(c, "sample_uniform_kernel");
+  });
+}
+
+int hx_sample_cbd(hx_ctx* c, int64_t* e, long long count, uint64_t seed, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_REQUIRE(count >= 0, "sample_cbd");
+    if (!count) return;
+    hx::sample_cbd_kernel<<<(unsigned)((count + 255) / 256), 256, 0, S(s)>>>((long long*)e, count, seed);
+    launched(c, "sample_cbd_kernel");
+  });
+}
+
 int hx_keygen_ksk(hx_ctx* c, uint64_t* key, const uint64_t* s_full, const uint64_t* sp_full,
                   const uint64_t* a_full, const int64_t* e, void* s) {
   return guarded([&] {

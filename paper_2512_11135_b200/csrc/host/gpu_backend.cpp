@@ -145,20 +145,18 @@ std::shared_ptr<DeviceBuffer> GpuLatticeBackend::make_key(const std::shared_ptr<
                                                           std::uint64_t g) {
   const int nc = (int)params_.moduli.size(), K = (int)params_.special_primes.size();
   const int dn = hx_ctx_dnum(ctx_, nc);
-  std::vector<u64> a;
-  std::vector<std::int64_t> e;
-  sample_uniform(a, nc, K, dn);
-  sample_error(e, dn);
-  DeviceBuffer da(a.size()), de(e.size());
-  cuda_ck(cudaMemcpyAsync(da.ptr, a.data(), a.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
-  cuda_ck(cudaMemcpyAsync(de.ptr, e.data(), e.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
+  // key material sampled on the device from two seeds of the backend's stream
+  const std::size_t N = params_.ring_degree;
+  DeviceBuffer da((std::size_t)dn * (nc + K) * N), de((std::size_t)dn * N);
+  ck(hx_sample_uniform(ctx_, da.ptr, nc, K, dn, next_u64(), nullptr), "sample_uniform");
+  ck(hx_sample_cbd(ctx_, (int64_t*)de.ptr, (long long)dn * N, next_u64(), nullptr), "sample_cbd");
   auto key = dev(hx_key_words(ctx_));
   if (g == 0)
     ck(hx_keygen_ksk(ctx_, key->ptr, s_full_->ptr, sp->ptr, da.ptr, (const int64_t*)de.ptr, nullptr), "keygen");
   else
     ck(hx_keygen_rotation(ctx_, key->ptr, s_full_->ptr, g, da.ptr, (const int64_t*)de.ptr, nullptr),
        "keygen_rotation");
-  cuda_ck(cudaStreamSynchronize(nullptr), "sync");  // host a/e vectors die here
+  cuda_ck(cudaStreamSynchronize(nullptr), "sync");  // da / de die here
   return key;
 }
 

@@ -3,6 +3,9 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -131,10 +134,18 @@ hxc_mat* hxc_matrix_prepare(hxc_backend* b, int method, const double* A, int row
     Matrix M(rows, cols);
     std::memcpy(M.data.data(), A, sizeof(double) * (std::size_t)rows * cols);
     const std::size_t n = b->b->slots();
+    static const bool trace = getenv("HX_PREP_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     PackedMatrix P = method == HXC_ROW ? pack_rows(M, n) : method == HXC_DIAG ? pack_diagonals(M, n) : pack_bsgs(M, n);
+    const auto t1 = std::chrono::steady_clock::now();
     auto* h = new hxc_mat;
     h->method = method;
     h->m = encode_matrix(*b->b, P, level);
+    if (trace) {
+      const auto t2 = std::chrono::steady_clock::now();
+      fprintf(stderr, "[prep] pack %.3f s, encode %.3f s\n", std::chrono::duration<double>(t1 - t0).count(),
+              std::chrono::duration<double>(t2 - t1).count());
+    }
     return h;
   });
 }

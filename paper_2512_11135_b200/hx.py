@@ -68,6 +68,8 @@ def lib() -> C.CDLL:
         "hx_mul_relin": [v, v, v, v, v, i32, i32, v],
         "hx_bsgs_mac": [v, v, v, v, i32, i32, i32, i32, v],
         "hx_keygen_ksk": [v, v, v, v, v, v, v],
+        "hx_sample_uniform": [v, v, i32, i32, i32, C.c_uint64, v],
+        "hx_sample_cbd": [v, v, C.c_longlong, C.c_uint64, v],
         "hx_encrypt_sk": [v, v, v, v, v, v, i32, v],
         "hx_ksk_to_rotation_layout": [v, v, v, u64, v],
         "hx_keygen_rotation": [v, v, v, u64, v, v, v],
@@ -233,6 +235,12 @@ class Context:
         out = torch.empty_like(key)
         self.ksk_to_rotation_layout(out, key, g, stream)
         return out
+
+    def sample_uniform(self, out, n_c, n_s, copies, seed, stream=None):
+        _check(self.L.hx_sample_uniform(self.h, _p(out), n_c, n_s, copies, seed, _stream(stream)), "hx_sample_uniform")
+
+    def sample_cbd(self, e, count, seed, stream=None):
+        _check(self.L.hx_sample_cbd(self.h, _p(e), count, seed, _stream(stream)), "hx_sample_cbd")
 
     def keygen_rotation(self, key, s_full, g, a_full, e, stream=None):
         _check(self.L.hx_keygen_rotation(self.h, _p(key), _p(s_full), g, _p(a_full), _p(e), _stream(stream)),

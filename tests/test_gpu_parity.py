@@ -407,3 +407,26 @@ def test_errors_are_loud():
         ctx.rescale(empty(1, orc.n), empty(1, orc.n), 1, 1)  # no limb to drop
     with pytest.raises(HxError):
         ctx.automorphism(empty(1, orc.n), empty(1, orc.n), 1, 1, 0, 4)  # even galois element
+
+
+def test_device_samplers():
+    """key-material samplers: uniform residues below each limb's prime with
+    uniform-looking moments, centred binomial errors in [-21, 21] with the
+    k = 21 variance; distinct seeds give distinct streams."""
+    p, ctx, orc = env("c2s")
+    nq, K, N = len(p["chain"]), len(p["special"]), 1 << p["logn"]
+    out = empty(2, nq + K, N)
+    ctx.sample_uniform(out, nq, K, 2, 1234)
+    u = host(out).view(np.uint64)
+    primes = np.array(p["chain"] + p["special"], dtype=np.uint64)
+    assert (u < primes[None, :, None]).all()
+    frac = u.astype(np.float64) / primes[None, :, None].astype(np.float64)
+    assert abs(frac.mean() - 0.5) < 0.01 and abs(frac.var() - 1 / 12) < 0.005
+    e = empty(4 * N)
+    ctx.sample_cbd(e, 4 * N, 99)
+    ev = host(e).view(np.int64)
+    assert ev.min() >= -21 and ev.max() <= 21
+    assert abs(ev.mean()) < 0.1 and abs(ev.var() - 10.5) < 0.5
+    out2 = empty(2, nq + K, N)
+    ctx.sample_uniform(out2, nq, K, 2, 1235)
+    assert not np.array_equal(host(out2), host(out))
