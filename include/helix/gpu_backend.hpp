@@ -107,6 +107,14 @@ class GpuLatticeBackend final : public SlotBackend {
                                       const std::vector<Plaintext>& diags, int n1, int n2, int blocks,
                                       bool allow_empty = false);
 
+  // ct x ct matmul (linalg.hpp matmul_ctct) with every step
+  // batched over the d column / row extractions: 2 encode_many of the masks,
+  // one mask product + rescale launch per operand, one multi-key rotation
+  // (Rot_j / Rot_dj), log2(d) rounds of one shared-key rotation + add per
+  // operand, d ct-ct products + relinearisation in one launch, one strided sum
+  // and the final rescale.  Same trace records as the SlotOps form.
+  Ciphertext matmul(const Ciphertext& A, const Ciphertext& B, int d);
+
   // ---- raw access ----
   hx_ctx* device_context() const { return ctx_; }
   const CkksEncoder& encoder() const { return enc_; }
@@ -139,6 +147,8 @@ class GpuLatticeBackend final : public SlotBackend {
   RotationKeySet rot_set_;
   hx_ctx* ctx_ = nullptr;
   hx_encoder* henc_ = nullptr;  // created on first encode
+  // matmul extraction masks per (d, level): immutable plaintexts, encoded once
+  std::map<std::pair<int, int>, std::pair<std::vector<Plaintext>, std::vector<Plaintext>>> matmul_masks_;
   std::uint64_t rng_[4];
   std::shared_ptr<DeviceBuffer> s_full_;  // [n_chain + K][N], NTT
   std::shared_ptr<DeviceBuffer> rlk_;     // relinearisation key (standard layout)

@@ -7,6 +7,7 @@
 // errors with k = 21, sigma ~ 3.24 ~ the spec's 3.2).  INSECURE TOY
 // PARAMETERS: requires params.insecure_toy.
 #include "helix/gpu_backend.hpp"
+#include "helix/packing.hpp"
 
 #include <cuda_runtime.h>
 
@@ -501,6 +502,90 @@ std::vector<Ciphertext> GpuLatticeBackend::rotate_many(const Ciphertext& a,
     out.push_back(wrap(buf, i * ctw, a.level, a.scale));
   }
   return out;
+}
+
+Ciphertext GpuLatticeBackend::matmul(const Ciphertext& A, const Ciphertext& B, int d) {
+  const std::size_t N = params_.ring_degree, n = slots();
+  detail::require_same_level(A.level, B.level, "matmul_ctct");
+  if (A.level < 2) throw LevelUnderflowError("matmul_ctct: requires a multiplicative level of 2");
+  const int lv = A.level, nqa = nq(lv), nqb = nqa - 1, lg = __builtin_ctz((unsigned)d);
+  const std::size_t cw = (std::size_t)2 * nqa * N, cwb = (std::size_t)2 * nqb * N;
+  const Scale ms = Scale::prime(modulus_at(lv));
+  const Scale ms_b = ms * Scale::prime(modulus_at(lv - 1)) / params_.delta();
+  const auto need = [&](std::int64_t k) {
+    const std::int64_t r = detail::reduce_amount(k, (std::int64_t)n);
+    const u64* key = rotation_key(r);
+    if (!rot_set_.contains(r) || !key) throw MissingRotationKeyError("rotate: no key for amount " + std::to_string(r));
+    return std::pair<const u64*, u64>{key, galois(r)};
+  };
+  // masks, each twice ([j][poly]) so one elementwise launch covers both polys;
+  // encoded once per (d, level) and cached (plaintexts are immutable)
+  auto it = matmul_masks_.find({d, lv});
+  if (it == matmul_masks_.end()) {
+    std::vector<std::vector<double>> cmv, rmv;
+    for (int j = 0; j < d; ++j) {
+      auto c = make_mask(MaskKind::ColumnExtractor, j, d, n);
+      auto r = make_mask(MaskKind::RowExtractor, j, d, n);
+      cmv.push_back(c);
+      cmv.push_back(std::move(c));
+      rmv.push_back(r);
+      rmv.push_back(std::move(r));
+    }
+    it = matmul_masks_.emplace(std::make_pair(d, lv), std::make_pair(encode_many(cmv, lv, ms), encode_many(rmv, lv, ms_b)))
+             .first;
+  }
+  const auto& cm = it->second.first;
+  const auto& rm = it->second.second;
+  // operand replicas [j][2][nqa][N] and the masked / rescaled / rotated sets
+  auto rep = dev((std::size_t)d * cw), prod = dev((std::size_t)d * cw);
+  auto sa = dev((std::size_t)d * cwb), sb = dev((std::size_t)d * cwb), tmp = dev((std::size_t)d * cwb);
+  const auto side = [&](const Ciphertext& X, const std::vector<Plaintext>& masks, const std::shared_ptr<DeviceBuffer>& out,
+                        std::int64_t unit) {
+    for (int j = 0; j < d; ++j)
+      cuda_ck(cudaMemcpyAsync(rep->ptr + j * cw, payload(X).data(), cw * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
+    const u64* mk = payload(masks[0]).data();  // encode_many: contiguous [2d][nqa][N]
+    ck(hx_mul(ctx_, prod->ptr, rep->ptr, mk, 2 * d, nqa, 0, nullptr), "mul");
+    ck(hx_rescale(ctx_, out->ptr, prod->ptr, 2 * d, nqa, nullptr), "rescale");
+    // element j -> Rot_{unit j}, j >= 1 (element 0 stays)
+    std::vector<const u64*> keys;
+    std::vector<u64> gal;
+    for (int j = 1; j < d; ++j) {
+      const auto kg = need(unit * j);
+      keys.push_back(kg.first);
+      gal.push_back(kg.second);
+    }
+    if (d > 1) {
+      ck(hx_rotate_multi(ctx_, tmp->ptr, out->ptr + cwb, keys.data(), gal.data(), d - 1, nqb, nullptr), "rotate_multi");
+      cuda_ck(cudaMemcpyAsync(out->ptr + cwb, tmp->ptr, (std::size_t)(d - 1) * cwb * 8, cudaMemcpyDeviceToDevice,
+                              nullptr), "d2d");
+    }
+    // replicate: x += Rot_{-unit 2^i}(x), i < log2 d, for all d at once
+    for (int i = 0; i < lg; ++i) {
+      const auto kg = need(-(unit << i));
+      ck(hx_rotate(ctx_, tmp->ptr, out->ptr, kg.first, d, nqb, kg.second, nullptr), "rotate");
+      ck(hx_add(ctx_, out->ptr, out->ptr, tmp->ptr, 2 * d, nqb, 0, nullptr), "add");
+    }
+  };
+  side(A, cm, sa, 1);
+  side(B, rm, sb, d);
+  // d ct-ct products + relinearisation, summed over j, one rescale
+  ck(hx_mul_relin(ctx_, tmp->ptr, sa->ptr, sb->ptr, rlk_->ptr, d, nqb, nullptr), "mul_relin");
+  auto acc = dev(cwb);
+  ck(hx_sum_strided(ctx_, acc->ptr, tmp->ptr, d, (long long)cwb, 2, (long long)nqb * N, (long long)nqb * N, nqb, nullptr),
+     "sum");
+  auto outb = dev((std::size_t)2 * (nqb - 1) * N);
+  ck(hx_rescale(ctx_, outb->ptr, acc->ptr, 2, nqb, nullptr), "rescale");
+  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+  // trace: exactly the SlotOps schedule of linalg.cpp matmul_ctct
+  trace_.record(OpKind::PtMul, lv, 2 * d);
+  trace_.record(OpKind::Rescale, lv, 2 * d);
+  trace_.record(OpKind::Rotate, lv - 1, 2 * (d - 1) + 2 * (std::size_t)d * lg);
+  trace_.record(OpKind::CtAdd, lv - 1, 2 * (std::size_t)d * lg + (d - 1));
+  trace_.record(OpKind::CtMul, lv - 1, d);
+  trace_.record(OpKind::Rescale, lv - 1);
+  const Scale s_a = A.scale * ms / Scale::prime(modulus_at(lv));
+  const Scale s_b = B.scale * ms_b / Scale::prime(modulus_at(lv));
+  return wrap(outb, 0, lv - 2, s_a * s_b / Scale::prime(modulus_at(lv - 1)));
 }
 
 Ciphertext GpuLatticeBackend::bsgs_block(const std::vector<Ciphertext>& baby,

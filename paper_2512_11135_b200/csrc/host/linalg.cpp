@@ -288,6 +288,12 @@ std::pair<Ciphertext, KernelReport> matmul_ctct(SlotOps& ops, const Ciphertext& 
   detail::require_same_level(A.level, B.level, "matmul_ctct");
   if (A.level < 2) throw LevelUnderflowError("matmul_ctct: requires a multiplicative level of 2");
   const auto snap = TraceSnapshot::take(ops.trace());
+#ifndef HELIX_NO_GPU
+  if (auto* g = dynamic_cast<GpuLatticeBackend*>(&ops)) {  // batched device pipeline
+    const Ciphertext out = g->matmul(A, B, d);
+    return {out, report_since(ops.trace(), snap, A.level, out)};
+  }
+#endif
   const int lv = A.level, lg = ilog2((std::size_t)d);
   // A's column mask at scale q_l (A_col keeps Delta); B's row mask at scale
   // q_l q_{l-1} / Delta so that the ct-ct product has scale Delta q_{l-1} and
