@@ -122,7 +122,7 @@ __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, c
     const int lowbits = OB + g0;                                                             \
     _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                         \
       const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                       \
-      x[r] = firstg ? bconv_word<F64, MAXA>(src + e, TILE, cnt, sf64, C, P) : sm[e];         \
+      x[r] = firstg ? bconv_word<F64, MAXA>(src + e, TILE, cnt, sf64, C, P) : sm[swz<false>(e)]; \
     }                                                                                        \
     if (F64)                                                                                 \
       ntt_group_f64<true, false, S, OB, WW>(x, jb, g0, logn, twf, nullptr, P, false);         \
@@ -137,7 +137,7 @@ __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, c
       __syncthreads();                                                                       \
       _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
         const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                     \
-        sm[e] = x[r];                                                                        \
+        sm[swz<false>(e)] = x[r];                                                            \
       }                                                                                      \
       __syncthreads();                                                                       \
     }                                                                                        \

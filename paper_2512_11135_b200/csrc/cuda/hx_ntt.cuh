@@ -52,9 +52,14 @@ __device__ __forceinline__ int deposit(int f, int lowbits, int w) {
   return (f & ((1 << lowbits) - 1)) | ((f >> lowbits) << (lowbits + w));
 }
 
+// Shared-memory tile swizzles (u64 words: bank pair = e mod 16).  ROW tiles:
+// XOR the low 4 bits with the row index.  COL tiles of 8 columns: the last
+// group's lanes read 8 consecutive words then jump 128 words, so word bit 3 is
+// flipped by bit 7 -- lanes 0-15 then cover all 16 bank pairs (2 wavefronts per
+// 8-byte warp access, the minimum).
 template <bool ROW>
 __device__ __forceinline__ int swz(int e) {
-  return ROW ? (e ^ ((e >> 4) & 15)) : e;
+  return ROW ? (e ^ ((e >> 4) & 15)) : (e ^ (((e >> 7) & 1) << 3));
 }
 
 // One radix-2^W group over sub-bits [g0, g0+W) of the tile index.
