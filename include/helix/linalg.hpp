@@ -53,6 +53,13 @@ BsgsShard bsgs_shard(const BsgsPlan& plan, int rank, int world);
 Ciphertext rotate_and_sum(SlotOps& ops, const Ciphertext& ct, std::size_t span, std::size_t stride,
                           KernelReport* report = nullptr);
 
+// Rotation count the kernel records for a DENSE rows x cols matrix at `slots`
+// slots, from the packing alone (no ciphertext work): the counters-only form
+// of SPEC acceptance criterion 4.  Row: groups log2(pad_cols) +
+// rows with a nonzero assembly shift; diag: d - 1; BSGS: (n1 - 1) +
+// blocks (n2 - 1).
+std::int64_t predicted_rotations(Layout layout, int rows, int cols, std::size_t slots);
+
 // Matrix-vector products; x replicated at period d (packing.hpp).  One output
 // ciphertext per row block (one for a single-block matrix).
 struct MatvecResult {

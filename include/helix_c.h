@@ -94,6 +94,9 @@ hxc_ct* hxc_ct_like(hxc_backend* b, const hxc_ct* like, const uint64_t* words);
 
 /* ct-ct matmul of row-major d x d operands */
 hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_report* rep);
+/* rotation count a dense rows x cols matvec records at `slots` slots (counters
+ * only, no device work; helix::predicted_rotations; SPEC criterion 4) */
+long long hxc_predicted_rotations(int method, int rows, int cols, int64_t slots);
 int hxc_matmul_rotations(int d, int64_t* out, int cap);
 
 /* ---- raw device words, for the bit-exact parity tests ----

@@ -229,6 +229,13 @@ hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_
   });
 }
 
+long long hxc_predicted_rotations(int method, int rows, int cols, int64_t slots) {
+  return guard<long long>(-1, [&] {
+    const Layout l = method == HXC_ROW ? Layout::PackedRow : method == HXC_DIAG ? Layout::Diagonal : Layout::BsgsDiagonal;
+    return (long long)predicted_rotations(l, rows, cols, (std::size_t)slots);
+  });
+}
+
 int hxc_matmul_rotations(int d, int64_t* out, int cap) {
   const auto r = matmul_rotations(d, 0);
   for (int i = 0; i < (int)r.size() && i < cap; ++i) out[i] = r[i];

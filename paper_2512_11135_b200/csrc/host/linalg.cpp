@@ -318,6 +318,33 @@ std::pair<Ciphertext, KernelReport> matmul_ctct(SlotOps& ops, const Ciphertext& 
   return {out, report_since(ops.trace(), snap, A.level, out)};
 }
 
+std::int64_t predicted_rotations(Layout layout, int rows, int cols, std::size_t slots) {
+  if (rows < 1 || cols < 1) throw std::invalid_argument("predicted_rotations: empty matrix");
+  int pc = 1;
+  while (pc < cols) pc <<= 1;
+  if ((std::size_t)pc > slots) throw std::invalid_argument("predicted_rotations: input dimension exceeds the slot count");
+  const int lg = ilog2((std::size_t)pc);
+  switch (layout) {
+    case Layout::PackedRow: {
+      const int p = std::max(1, std::min((int)(slots / pc), rows));
+      const std::int64_t groups = (rows + p - 1) / p;
+      std::int64_t r = groups * lg;
+      for (int row = 0; row < rows; ++row)
+        if (detail::reduce_amount((std::int64_t)(row % p) * pc - row, (std::int64_t)slots) != 0) ++r;
+      return r;
+    }
+    case Layout::Diagonal:
+      return pc - 1;
+    case Layout::BsgsDiagonal: {
+      const BsgsPlan plan = BsgsPlan::for_dim(pc);
+      const std::int64_t blocks = (rows + pc - 1) / pc;
+      return (plan.n1 - 1) + blocks * (plan.n2 - 1);
+    }
+    default:
+      throw std::invalid_argument("predicted_rotations: not a matvec layout");
+  }
+}
+
 // ------------------------------------------------------------------- keys
 std::vector<std::int64_t> bsgs_rotations(const BsgsPlan& plan) {
   std::vector<std::int64_t> r;

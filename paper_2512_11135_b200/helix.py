@@ -68,6 +68,7 @@ def lib():
         "hxc_matvec_shard": (i32, [v, v, v, C.POINTER(v), i32, rp]),
         "hxc_ct_like": (v, [v, v, v]),
         "hxc_matmul_rotations": (i32, [i32, C.POINTER(C.c_int64), i32]),
+        "hxc_predicted_rotations": (C.c_longlong, [i32, i32, i32, i64]),
         "hxc_secret_key_ptr": (v, [v]),
         "hxc_relin_key_ptr": (v, [v]),
         "hxc_rotation_key_ptr": (v, [v, i64]),
@@ -100,6 +101,14 @@ def params_json(logn, chain, special, alpha, delta_log2=40, **kw):
          "special_primes": list(special), "backend": "lattice", "insecure_toy": True, "alpha": alpha}
     d.update(kw)
     return json.dumps(d)
+
+
+def predicted_rotations(method: int, rows: int, cols: int, slots: int) -> int:
+    """host-only helix::predicted_rotations (no device needed)"""
+    r = lib().hxc_predicted_rotations(method, rows, cols, slots)
+    if r < 0:
+        raise _err()
+    return r
 
 
 def encode_coeffs(pjson: str, m, level: int, scale: float) -> np.ndarray:
