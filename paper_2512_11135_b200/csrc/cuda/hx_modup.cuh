@@ -55,7 +55,16 @@ struct ModUpColArgs {
 
 // bconv of one tile word (sources at src[i * stride]) into the working
 // representation of the target class
-template <bool F64, int MAXA>
+// Source-class modes (fixed per digit, so a CTA runs one straight-line body and
+// the instruction cache holds one variant): 0 every source limb < 2^47,
+// 1 source 0 is the wide q_0 and the rest < 2^47 (config 2's digit 0),
+// 2 any mix (runtime test per source).
+template <int SRC, int MAXA>
+__device__ __forceinline__ bool src_is_f64(const bool (&sf64)[MAXA], int i) {
+  return SRC == 0 ? true : SRC == 1 ? (i != 0) : sf64[i];
+}
+
+template <bool F64, int MAXA, int SRC = 2>
 __device__ __forceinline__ u64 bconv_word(const u64* src, int stride, int cnt, const bool (&sf64)[MAXA],
                                           const BconvC* C, const PrimeConst& P) {
   if (F64) {
@@ -64,7 +73,7 @@ __device__ __forceinline__ u64 bconv_word(const u64* src, int stride, int cnt, c
     for (int i = 0; i < MAXA; ++i) {
       if (i < cnt) {
         const u64 v = src[i * stride];
-        if (sf64[i]) {
+        if (src_is_f64<SRC, MAXA>(sf64, i)) {
           acc = __dadd_rn(acc, mulmod_f64(__longlong_as_double((long long)v), C[i].w, C[i].wq, P.qd));
         } else {  // 60-bit source: x = xh 2^30 + xl
           const double xh = __dsub_rn(__longlong_as_double((long long)((v >> 30) | 0x4330000000000000ull)), kTwo52);
@@ -93,7 +102,7 @@ __device__ __forceinline__ u64 bconv_word(const u64* src, int stride, int cnt, c
 
 // one target limb of the tile: conversion into registers, forward COL stages,
 // store (FP64 or integer butterflies by the target's prime class)
-template <int S, int OB, bool F64, int MAXA>
+template <int S, int OB, bool F64, int MAXA, int SRC>
 __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, const bool (&sf64)[MAXA],
                                              const BconvC (&C)[MAXA], const PrimeConst& P, u64* base,
                                              int tile, int logn) {
@@ -122,7 +131,7 @@ __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, c
     const int lowbits = OB + g0;                                                             \
     _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                         \
       const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                       \
-      x[r] = firstg ? bconv_word<F64, MAXA>(src + e, TILE, cnt, sf64, C, P) : sm[swz<false>(e)]; \
+      x[r] = firstg ? bconv_word<F64, MAXA, SRC>(src + e, TILE, cnt, sf64, C, P) : sm[swz<false>(e)]; \
     }                                                                                        \
     if (F64)                                                                                 \
       ntt_group_f64<true, false, S, OB, WW>(x, jb, g0, logn, twf, nullptr, P, false);         \
@@ -196,6 +205,17 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
     }
   }
   __syncthreads();
+  int mode = 0;  // source-class mode of this digit (see src_is_f64)
+  {
+    bool all = true, first_only = cnt > 0 && !sf64[0];
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i)
+      if (i < cnt) {
+        all = all && sf64[i];
+        if (i > 0) first_only = first_only && sf64[i];
+      }
+    mode = all ? 0 : first_only ? 1 : 2;
+  }
 
   const int* tl = A.tlist + A.toff[d];
   const BconvC* bcd = A.bc + A.bc_off[d];
@@ -211,7 +231,12 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
       if (i < cnt) C[i] = bcd[(long long)j * A.alpha + i];
     u64* base = dout + (long long)j * N;
     __syncthreads();  // the previous target's last exchange reads are done
-    modup_target<S, OB, true, MAXA>(src, sm, cnt, sf64, C, P, base, tile, logn);
+    if (mode == 0)
+      modup_target<S, OB, true, MAXA, 0>(src, sm, cnt, sf64, C, P, base, tile, logn);
+    else if (mode == 1)
+      modup_target<S, OB, true, MAXA, 1>(src, sm, cnt, sf64, C, P, base, tile, logn);
+    else
+      modup_target<S, OB, true, MAXA, 2>(src, sm, cnt, sf64, C, P, base, tile, logn);
   }
 #pragma unroll 1
   for (int k = nt; k < nt + ni; ++k) {
