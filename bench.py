@@ -269,7 +269,7 @@ def _prune_diagonals(M, d, rng, frac=0.9):
     return M
 
 
-def ffn_bsgs_bench(torch, chain, special, args, iters=5):
+def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=16, chunk=8):
     """BASELINE configs[2]: FFN up-projection W1 (768 x 3072) and down-projection
     W2 (3072 x 768), N(0, 0.02^2), as BSGS linear transforms at N=2^16 / 24+3
     primes through the helix C-ABI (hxc_matvec): W1 d = 1024, 3 row blocks,
@@ -317,7 +317,28 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5):
                      "d": d, "n1": info["n1"], "n2": info["n2"], "row_blocks": info["blocks"],
                      "rotations": rep["rotations"], "pt_muls": rep["pt_muls"], "nonzero_diagonals": info["nonzero"],
                      "diag_bytes": info["nonzero"] * 24 * N * 8, "prepare_s": prep}
-        del mat, outs, ct
+        del outs
+        if not prune and tokens > 0:
+            # T tokens through the same matrix, key switches batched over a chunk
+            # of `chunk` tokens (hxc_matvec_tokens); per-token throughput
+            xt = [be.encrypt(np.tile(np.concatenate([rng.uniform(-1, 1, M.shape[1]), np.zeros(d - M.shape[1])]),
+                                     be.slots // d), lvl) for _ in range(chunk)]
+            outs_t, _ = be.matvec_tokens(mat, xt)  # warm-up
+            del outs_t
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(tokens // chunk):
+                outs_t, rep_t = be.matvec_tokens(mat, xt)
+                del outs_t
+            e1.record()
+            torch.cuda.synchronize()
+            tsecs = e0.elapsed_time(e1) / 1e3
+            done = (tokens // chunk) * chunk
+            out[name + f"_tokens{done}"] = {"tokens_per_s": done / tsecs, "ms_per_token": 1e3 * tsecs / done,
+                                            "tokens": done, "chunk": chunk,
+                                            "rotations_per_token": rep_t["rotations"]}
+            del xt
+        del mat, ct
         torch.cuda.synchronize()
     be.close()
     return out

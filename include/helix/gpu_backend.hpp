@@ -106,6 +106,17 @@ class GpuLatticeBackend final : public SlotBackend {
   std::vector<Ciphertext> bsgs_blocks(const std::vector<Ciphertext>& baby,
                                       const std::vector<Plaintext>& diags, int n1, int n2, int blocks,
                                       bool allow_empty = false);
+  // Token batch (SURVEY §8(d) config 3, T tokens through one matrix): baby
+  // sets of T ciphertexts, MACs per (token, block), and giant step j of every
+  // (token, block) pair rotated with ONE read of key n1 j (hx_rotate_grouped
+  // over T x blocks elements).  Outputs [token][block]; trace = T single runs.
+  std::vector<std::vector<Ciphertext>> bsgs_blocks_tokens(const std::vector<std::vector<Ciphertext>>& babies,
+                                                          const std::vector<Plaintext>& diags, int n1, int n2,
+                                                          int blocks, bool allow_empty = false);
+  // hoisted rotations of T ciphertexts in one launch sequence (ModUp of all
+  // T, then every amount): out[t][i] = Rot(xs[t], amounts[i])
+  std::vector<std::vector<Ciphertext>> rotate_many_tokens(const std::vector<Ciphertext>& xs,
+                                                          std::span<const std::int64_t> amounts);
 
   // ct x ct matmul (linalg.hpp matmul_ctct) with every step
   // batched over the d column / row extractions: 2 encode_many of the masks,

@@ -68,6 +68,11 @@ struct MatvecResult {
 };
 MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x);
 MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x, const BsgsShard& shard);
+// T input ciphertexts (tokens) through one BSGS matrix; on the GPU backend the
+// key switches of all tokens are batched (hoisted baby steps over T inputs,
+// giant steps grouped by key over T x blocks).  Same outputs and trace as T
+// separate matvec_bsgs calls.
+std::vector<MatvecResult> matvec_bsgs_tokens(SlotOps& ops, const EncodedMatrix& M, const std::vector<Ciphertext>& xs);
 MatvecResult matvec_diag(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x);
 // packed-row method: y in the first R slots; 2 levels
 MatvecResult matvec_row(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x);

@@ -79,6 +79,12 @@ int hxc_matrix_rotations(const hxc_mat* m, int64_t* out, int cap);
 /* y = M x; writes up to cap output handles (one per row block); returns count */
 int hxc_matvec(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, int cap,
                hxc_report* rep);
+/* T ciphertexts (tokens) through one BSGS matrix with every key switch batched
+ * over the tokens (helix::matvec_bsgs_tokens); out receives T x blocks handles
+ * token-major; returns that count (or -1); rep = per-token counters. */
+int hxc_matvec_tokens(hxc_backend* b, const hxc_mat* m, const hxc_ct* const* xs, int T, hxc_ct** out, int cap,
+                      hxc_report* rep);
+
 /* ---- giant-step sharding of BSGS (multi-GPU, one process per GPU) ----
  * rank r of world G encodes only its giant groups (helix::bsgs_shard) and
  * returns PRE-RESCALE partial outputs; the caller sums the partial words of all

@@ -1210,9 +1210,19 @@ int hx_rotate_grouped(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
       kk.push_back((const u64*)keys[r]);
       gg.push_back((u64)galois[r]);
     }
-    DBuf D((long long)R * E * c->dnum(n_q) * ext * N, S(s), c);
-    modup(c, D.p, (const u64*)in + (long long)n_q * N, ct, (long long)R * E, n_q, S(s));
-    rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, kk, gg, false, E, n_q, S(s));
+    // keys in chunks so the ModUp digits + inner products of a chunk stay
+    // within ~16 GB (T tokens x blocks elements per key multiply them)
+    const long long per_key = (long long)E * (c->dnum(n_q) + 2) * ext * N * 8;
+    const int Rc = (int)std::max(1ll, std::min<long long>(R, (16ll << 30) / per_key));
+    for (int r0 = 0; r0 < R; r0 += Rc) {
+      const int nr = std::min(Rc, R - r0);
+      const u64* ip = (const u64*)in + (long long)r0 * E * ct;
+      DBuf D((long long)nr * E * c->dnum(n_q) * ext * N, S(s), c);
+      modup(c, D.p, ip + (long long)n_q * N, ct, (long long)nr * E, n_q, S(s));
+      const std::vector<const u64*> kc(kk.begin() + r0, kk.begin() + r0 + nr);
+      const std::vector<u64> gc(gg.begin() + r0, gg.begin() + r0 + nr);
+      rotate_batch_from_digits(c, (u64*)out + (long long)r0 * E * ct, ip, D.p, kc, gc, false, E, n_q, S(s));
+    }
   });
 }
 

@@ -596,36 +596,50 @@ Ciphertext GpuLatticeBackend::bsgs_block(const std::vector<Ciphertext>& baby,
 std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphertext>& baby,
                                                        const std::vector<Plaintext>& diags, int n1, int n2,
                                                        int blocks, bool allow_empty) {
-  if ((int)baby.size() < n1 || (long long)diags.size() < (long long)n1 * n2 * blocks)
-    throw std::invalid_argument("bsgs_blocks: shape");
-  const Ciphertext& x = baby[0];
+  return bsgs_blocks_tokens({baby}, diags, n1, n2, blocks, allow_empty).front();
+}
+
+std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
+    const std::vector<std::vector<Ciphertext>>& babies, const std::vector<Plaintext>& diags, int n1, int n2,
+    int blocks, bool allow_empty) {
+  const int T = (int)babies.size();
+  if (T < 1) throw std::invalid_argument("bsgs_blocks: no tokens");
+  for (const auto& bb : babies)
+    if ((int)bb.size() < n1) throw std::invalid_argument("bsgs_blocks: shape");
+  if ((long long)diags.size() < (long long)n1 * n2 * blocks) throw std::invalid_argument("bsgs_blocks: shape");
+  const Ciphertext& x = babies[0][0];
   const int level = x.level, nqv = nq(level);
   const std::size_t N = params_.ring_degree, ctw = (std::size_t)2 * nqv * N, ptw = (std::size_t)nqv * N;
   const std::size_t d = (std::size_t)n1 * n2;
   const auto n = (std::int64_t)slots();
-  // baby steps contiguous [n1][2][n_q][N]
-  std::shared_ptr<DeviceBuffer> bb;
-  const u64* baby_ptr = nullptr;
-  {
-    const auto& p0 = payload(baby[0]);
+  for (const auto& bb : babies)
+    if (bb[0].level != level || bb[0].scale != x.scale) throw LevelMismatchError("bsgs: token level/scale mismatch");
+  // baby steps of token t contiguous [n1][2][n_q][N]
+  std::vector<std::shared_ptr<DeviceBuffer>> keep;
+  std::vector<const u64*> baby_ptr(T);
+  for (int t = 0; t < T; ++t) {
+    const auto& p0 = payload(babies[t][0]);
     bool contiguous = true;
     for (int k = 1; k < n1 && contiguous; ++k) {
-      const auto& pk = payload(baby[k]);
+      const auto& pk = payload(babies[t][k]);
       contiguous = pk.buf == p0.buf && pk.offset == p0.offset + k * ctw;
     }
     if (contiguous) {
-      baby_ptr = p0.data();
+      baby_ptr[t] = p0.data();
     } else {
-      bb = dev(n1 * ctw);
+      auto bb = dev(n1 * ctw);
       for (int k = 0; k < n1; ++k)
-        cuda_ck(cudaMemcpyAsync(bb->ptr + k * ctw, payload(baby[k]).data(), ctw * 8, cudaMemcpyDeviceToDevice,
+        cuda_ck(cudaMemcpyAsync(bb->ptr + k * ctw, payload(babies[t][k]).data(), ctw * 8, cudaMemcpyDeviceToDevice,
                                 nullptr), "d2d");
-      baby_ptr = bb->ptr;
+      baby_ptr[t] = bb->ptr;
+      keep.push_back(bb);
     }
   }
-  // inner sums, layout [n2][blocks][2][n_q][N] so giant step j of every block
-  // is one contiguous group (one key read for all blocks); dead groups stay 0
-  const std::size_t jstride = (std::size_t)blocks * ctw;
+  // inner sums, layout [n2][T][blocks][2][n_q][N]: giant step j of every
+  // (token, block) is one contiguous group (one key read for all of them);
+  // dead groups stay 0
+  const int E = T * blocks;
+  const std::size_t jstride = (std::size_t)E * ctw;
   auto inner = dev((std::size_t)n2 * jstride);
   cuda_ck(cudaMemsetAsync(inner->ptr, 0, inner->words * 8, nullptr), "memset");
   Scale dscale;
@@ -634,7 +648,7 @@ std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphert
   for (int b = 0; b < blocks; ++b) {
     const Plaintext* D = diags.data() + (std::size_t)b * d;
     std::uint64_t ptmuls = 0, adds = 0;
-    // fast path: the whole block dense and contiguous (encode_many) -> one MAC launch
+    // fast path: the whole block dense and contiguous (encode_many) -> one MAC launch per token
     bool all_contig = D[0].payload != nullptr;
     const GpuPlaintext* p0 = all_contig ? &payload(D[0]) : nullptr;
     for (std::size_t i = 0; i < d && all_contig; ++i) {
@@ -650,9 +664,10 @@ std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphert
       if (have_scale && D[0].scale != dscale) throw ScaleMismatchError("bsgs: diagonal scales differ");
       dscale = D[0].scale;
       have_scale = true;
-      ck(hx_bsgs_mac_ex(ctx_, inner->ptr + b * ctw, (long long)jstride, baby_ptr, p0->data(), nqv, n1, n2, nqv,
-                        nullptr),
-         "bsgs_mac");
+      for (int t = 0; t < T; ++t)
+        ck(hx_bsgs_mac_ex(ctx_, inner->ptr + ((std::size_t)t * blocks + b) * ctw, (long long)jstride, baby_ptr[t],
+                          p0->data(), nqv, n1, n2, nqv, nullptr),
+           "bsgs_mac");
       ptmuls = d;
       adds = (std::uint64_t)(n1 - 1) * n2;
       for (int j = 0; j < n2; ++j) live[b][j] = 1;
@@ -674,25 +689,32 @@ std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphert
         if (ks.empty()) continue;
         ptmuls += ks.size();
         adds += ks.size() - 1;
-        u64* dst = inner->ptr + j * jstride + b * ctw;
         const auto& q0 = payload(D[(std::size_t)j * n1 + ks[0]]);
         bool dense = (int)ks.size() == n1;
         for (int k = 1; k < n1 && dense; ++k) {
           const auto& pk = payload(D[(std::size_t)j * n1 + k]);
           dense = pk.buf == q0.buf && pk.offset == q0.offset + k * ptw;
         }
-        if (dense) {
-          ck(hx_bsgs_mac_ex(ctx_, dst, (long long)ctw, baby_ptr, q0.data(), nqv, n1, 1, nqv, nullptr), "bsgs_mac");
-        } else {  // sparse group: gather its diagonals and the matching baby steps
-          DeviceBuffer dg(ks.size() * ptw), bs(ks.size() * ctw);
-          for (std::size_t i = 0; i < ks.size(); ++i) {
-            cuda_ck(cudaMemcpyAsync(dg.ptr + i * ptw, payload(D[(std::size_t)j * n1 + ks[i]]).data(), ptw * 8,
+        std::unique_ptr<DeviceBuffer> dg;
+        if (!dense) {  // sparse group: gather its diagonals once for all tokens
+          dg = std::make_unique<DeviceBuffer>(ks.size() * ptw);
+          for (std::size_t i = 0; i < ks.size(); ++i)
+            cuda_ck(cudaMemcpyAsync(dg->ptr + i * ptw, payload(D[(std::size_t)j * n1 + ks[i]]).data(), ptw * 8,
                                     cudaMemcpyDeviceToDevice, nullptr), "d2d");
-            cuda_ck(cudaMemcpyAsync(bs.ptr + i * ctw, baby_ptr + ks[i] * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
-                                    nullptr), "d2d");
+        }
+        for (int t = 0; t < T; ++t) {
+          u64* dst = inner->ptr + j * jstride + ((std::size_t)t * blocks + b) * ctw;
+          if (dense) {
+            ck(hx_bsgs_mac_ex(ctx_, dst, (long long)ctw, baby_ptr[t], q0.data(), nqv, n1, 1, nqv, nullptr),
+               "bsgs_mac");
+          } else {  // ... and the matching baby steps of the token
+            DeviceBuffer bs(ks.size() * ctw);
+            for (std::size_t i = 0; i < ks.size(); ++i)
+              cuda_ck(cudaMemcpyAsync(bs.ptr + i * ctw, baby_ptr[t] + ks[i] * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
+                                      nullptr), "d2d");
+            ck(hx_bsgs_mac_ex(ctx_, dst, (long long)ctw, bs.ptr, dg->ptr, nqv, (int)ks.size(), 1, nqv, nullptr),
+               "bsgs_mac");
           }
-          ck(hx_bsgs_mac_ex(ctx_, dst, (long long)ctw, bs.ptr, dg.ptr, nqv, (int)ks.size(), 1, nqv, nullptr),
-             "bsgs_mac");
         }
         live[b][j] = 1;
       }
@@ -700,12 +722,12 @@ std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphert
     bool any = false;
     for (int j = 0; j < n2; ++j) any |= live[b][j] != 0;
     if (!any && !allow_empty) throw std::invalid_argument("matvec_bsgs: block has no non-zero diagonal");
-    if (ptmuls) trace_.record(OpKind::PtMul, level, ptmuls);
-    if (adds) trace_.record(OpKind::CtAdd, level, adds);
+    if (ptmuls) trace_.record(OpKind::PtMul, level, ptmuls * T);
+    if (adds) trace_.record(OpKind::CtAdd, level, adds * T);
   }
   if (!have_scale) dscale = Scale::prime(modulus_at(level));  // empty shard: the diagonal scale
   const Scale out_scale = x.scale * dscale;
-  // giant steps j >= 1: rotate group j of every block by n1 j with one key
+  // giant steps j >= 1: rotate group j of every (token, block) by n1 j with one key
   std::vector<const u64*> keys;
   std::vector<u64> gs;
   std::vector<int> J;
@@ -720,7 +742,7 @@ std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphert
     gs.push_back(galois(r));
     J.push_back(j);
   }
-  auto out = dev((std::size_t)blocks * ctw);
+  auto out = dev((std::size_t)E * ctw);
   if (!J.empty()) {
     std::shared_ptr<DeviceBuffer> src;
     const u64* srcp = inner->ptr + jstride;  // groups 1..n2-1 are contiguous
@@ -732,28 +754,91 @@ std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphert
       srcp = src->ptr;
     }
     auto rotated = dev(J.size() * jstride);
-    ck(hx_rotate_grouped(ctx_, rotated->ptr, srcp, keys.data(), gs.data(), (int)J.size(), blocks, nqv, nullptr),
+    ck(hx_rotate_grouped(ctx_, rotated->ptr, srcp, keys.data(), gs.data(), (int)J.size(), E, nqv, nullptr),
        "rotate_grouped");
-    // y_b = inner_0,b + sum_j Rot(inner_j,b): rotated terms summed in one pass
-    ck(hx_sum_strided(ctx_, out->ptr, rotated->ptr, (int)J.size(), (long long)jstride, 2 * blocks,
-                      (long long)ptw, (long long)ptw, nqv, nullptr),
+    // y = inner_0 + sum_j Rot(inner_j): rotated terms summed in one pass
+    ck(hx_sum_strided(ctx_, out->ptr, rotated->ptr, (int)J.size(), (long long)jstride, 2 * E, (long long)ptw,
+                      (long long)ptw, nqv, nullptr),
        "sum");
-    ck(hx_add(ctx_, out->ptr, out->ptr, inner->ptr, 2 * blocks, nqv, 0, nullptr), "add");
+    ck(hx_add(ctx_, out->ptr, out->ptr, inner->ptr, 2 * E, nqv, 0, nullptr), "add");
   } else {
     cuda_ck(cudaMemcpyAsync(out->ptr, inner->ptr, jstride * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
   }
-  std::vector<Ciphertext> res;
+  std::vector<std::vector<Ciphertext>> res(T);
   for (int b = 0; b < blocks; ++b) {
     std::uint64_t nl = 0, nr = 0;
     for (int j = 0; j < n2; ++j) {
       nl += live[b][j] != 0;
       nr += (j > 0 && live[b][j] != 0);
     }
-    if (nr) trace_.record(OpKind::Rotate, level, nr);
-    if (nl > 1) trace_.record(OpKind::CtAdd, level, nl - 1);
-    res.push_back(wrap(out, (std::size_t)b * ctw, level, out_scale));
+    if (nr) trace_.record(OpKind::Rotate, level, nr * T);
+    if (nl > 1) trace_.record(OpKind::CtAdd, level, (nl - 1) * T);
   }
+  for (int t = 0; t < T; ++t)
+    for (int b = 0; b < blocks; ++b)
+      res[t].push_back(wrap(out, ((std::size_t)t * blocks + b) * ctw, level, out_scale));
   return res;
+}
+
+std::vector<std::vector<Ciphertext>> GpuLatticeBackend::rotate_many_tokens(const std::vector<Ciphertext>& xs,
+                                                                           std::span<const std::int64_t> amounts) {
+  const int T = (int)xs.size();
+  if (T < 1) throw std::invalid_argument("rotate_many: no ciphertexts");
+  const auto n = (std::int64_t)slots();
+  const std::size_t N = params_.ring_degree;
+  const int level = xs[0].level, nqv = nq(level);
+  const std::size_t ctw = (std::size_t)2 * nqv * N;
+  const std::size_t R = amounts.size();
+  // inputs contiguous [T][ct]
+  auto in = dev((std::size_t)T * ctw);
+  for (int t = 0; t < T; ++t) {
+    if (xs[t].level != level) throw LevelMismatchError("rotate_many: token level mismatch");
+    cuda_ck(cudaMemcpyAsync(in->ptr + t * ctw, payload(xs[t]).data(), ctw * 8, cudaMemcpyDeviceToDevice, nullptr),
+            "d2d");
+  }
+  std::vector<const u64*> keys;
+  std::vector<u64> gs;
+  std::vector<std::size_t> which;
+  for (std::size_t i = 0; i < R; ++i) {
+    const std::int64_t r = detail::reduce_amount(amounts[i], n);
+    if (r == 0) continue;
+    const u64* key = rotation_key(r);
+    if (!rot_set_.contains(r) || !key) throw MissingRotationKeyError("rotate: no key for amount " + std::to_string(r));
+    keys.push_back(key);
+    gs.push_back(galois(r));
+    which.push_back(i);
+  }
+  // out [T][R][ct]: hoisted rotations land at [t][1 + ...] when amounts[0] == 0
+  auto buf = dev((std::size_t)T * R * ctw);
+  if (!keys.empty()) {
+    const bool lead_identity = detail::reduce_amount(amounts[0], n) == 0 && which.size() == R - 1;
+    if (lead_identity) {  // BSGS baby steps: write rotations straight after the identity slot
+      auto tmp = dev((std::size_t)T * keys.size() * ctw);
+      ck(hx_rotate_hoisted(ctx_, tmp->ptr, in->ptr, keys.data(), gs.data(), (int)keys.size(), T, nqv, nullptr),
+         "rotate_hoisted");
+      cuda_ck(cudaMemcpy2DAsync(buf->ptr + ctw, R * ctw * 8, tmp->ptr, keys.size() * ctw * 8, keys.size() * ctw * 8,
+                                T, cudaMemcpyDeviceToDevice, nullptr),
+              "memcpy2d");
+    } else {
+      auto tmp = dev((std::size_t)T * keys.size() * ctw);
+      ck(hx_rotate_hoisted(ctx_, tmp->ptr, in->ptr, keys.data(), gs.data(), (int)keys.size(), T, nqv, nullptr),
+         "rotate_hoisted");
+      for (int t = 0; t < T; ++t)
+        for (std::size_t j = 0; j < which.size(); ++j)
+          cuda_ck(cudaMemcpyAsync(buf->ptr + (t * R + which[j]) * ctw, tmp->ptr + (t * keys.size() + j) * ctw, ctw * 8,
+                                  cudaMemcpyDeviceToDevice, nullptr), "d2d");
+    }
+    trace_.record(OpKind::Rotate, level, keys.size() * T);
+  }
+  std::vector<std::vector<Ciphertext>> out(T);
+  for (int t = 0; t < T; ++t)
+    for (std::size_t i = 0; i < R; ++i) {
+      if (detail::reduce_amount(amounts[i], n) == 0)
+        cuda_ck(cudaMemcpyAsync(buf->ptr + (t * R + i) * ctw, in->ptr + t * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
+                                nullptr), "d2d");
+      out[t].push_back(wrap(buf, (t * R + i) * ctw, level, xs[t].scale));
+    }
+  return out;
 }
 
 }  // namespace helix

@@ -185,6 +185,24 @@ int hxc_matvec(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, 
   });
 }
 
+int hxc_matvec_tokens(hxc_backend* b, const hxc_mat* m, const hxc_ct* const* xs, int T, hxc_ct** out, int cap,
+                      hxc_report* rep) {
+  return guard(-1, [&] {
+    if (m->method != HXC_BSGS) throw std::invalid_argument("hxc_matvec_tokens: BSGS matrices only");
+    std::vector<Ciphertext> in;
+    for (int t = 0; t < T; ++t) in.push_back(xs[t]->c);
+    const auto rs = matvec_bsgs_tokens(*b->b, m->m, in);
+    int k = 0;
+    for (const auto& r : rs)
+      for (const auto& c : r.outputs) {
+        if (k < cap) out[k] = wrap(c);
+        ++k;
+      }
+    if (!rs.empty()) fill(rep, rs.front().report);
+    return k;
+  });
+}
+
 hxc_mat* hxc_matrix_prepare_shard(hxc_backend* b, const double* A, int rows, int cols, int level, int rank,
                                   int world) {
   return guard<hxc_mat*>(nullptr, [&] {

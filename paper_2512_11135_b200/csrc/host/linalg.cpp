@@ -185,6 +185,38 @@ MatvecResult matvec_bsgs(SlotOps& ops, const EncodedMatrix& Min, const Ciphertex
   return R;
 }
 
+std::vector<MatvecResult> matvec_bsgs_tokens(SlotOps& ops, const EncodedMatrix& M, const std::vector<Ciphertext>& xs) {
+  std::vector<MatvecResult> out;
+  if (xs.empty()) return out;
+#ifndef HELIX_NO_GPU
+  if (auto* gpu = dynamic_cast<GpuLatticeBackend*>(&ops)) {
+    for (const auto& x : xs) require_matvec_input(M, x, Layout::BsgsDiagonal);
+    const int n1 = M.meta.plan.n1, n2 = M.meta.plan.n2;
+    std::vector<std::int64_t> ks(n1);
+    for (int k = 0; k < n1; ++k) ks[k] = k;
+    const auto snap = TraceSnapshot::take(ops.trace());
+    const auto babies = gpu->rotate_many_tokens(xs, ks);
+    const auto accs = gpu->bsgs_blocks_tokens(babies, M.pts, n1, n2, M.meta.row_blocks);
+    for (const auto& per : accs) {
+      MatvecResult R;
+      for (const auto& a : per) R.outputs.push_back(ops.rescale(a));
+      out.push_back(std::move(R));
+    }
+    // the batch's counters, reported per token (identical for every token)
+    KernelReport rep = report_since(ops.trace(), snap, xs[0].level, out[0].outputs.front());
+    const auto T = (std::uint64_t)xs.size();
+    rep.rotations /= T;
+    rep.pt_muls /= T;
+    rep.ct_muls /= T;
+    rep.adds /= T;
+    for (auto& r : out) r.report = rep;
+    return out;
+  }
+#endif
+  for (const auto& x : xs) out.push_back(matvec_bsgs(ops, M, x));
+  return out;
+}
+
 // ------------------------------------------------------------------- diagonal
 MatvecResult matvec_diag(SlotOps& ops, const EncodedMatrix& M, const Ciphertext& x) {
   require_matvec_input(M, x, Layout::Diagonal);

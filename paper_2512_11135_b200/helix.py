@@ -65,6 +65,7 @@ def lib():
         "hxc_matvec": (i32, [v, v, v, C.POINTER(v), i32, rp]),
         "hxc_matmul": (v, [v, v, v, i32, rp]),
         "hxc_matrix_prepare_shard": (v, [v, f64p, i32, i32, i32, i32, i32]),
+        "hxc_matvec_tokens": (i32, [v, v, C.POINTER(v), i32, C.POINTER(v), i32, rp]),
         "hxc_matvec_shard": (i32, [v, v, v, C.POINTER(v), i32, rp]),
         "hxc_ct_like": (v, [v, v, v]),
         "hxc_matmul_rotations": (i32, [i32, C.POINTER(C.c_int64), i32]),
@@ -251,6 +252,20 @@ class Backend:
         if k < 0:
             raise _err()
         return [Ct(self, outs[i]) for i in range(k)], r.as_dict()
+
+    def matvec_tokens(self, mat, xs):
+        """T ciphertexts through one BSGS matrix, key switches batched over tokens;
+        returns ([[Ct per block] per token], per-token report)"""
+        r = Report()
+        T = len(xs)
+        blocks = mat.info()["blocks"]
+        arr = (C.c_void_p * T)(*[x.h for x in xs])
+        outs = (C.c_void_p * (T * blocks))()
+        k = self.L.hxc_matvec_tokens(self.h, mat.h, arr, T, outs, T * blocks, C.byref(r))
+        if k < 0:
+            raise _err()
+        cts = [Ct(self, outs[i]) for i in range(k)]
+        return [cts[t * blocks:(t + 1) * blocks] for t in range(T)], r.as_dict()
 
     def prepare_shard(self, A, level, rank, world):
         """BSGS matrix restricted to this rank's giant groups (helix::bsgs_shard)"""

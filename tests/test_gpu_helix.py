@@ -241,3 +241,32 @@ def test_giant_step_shards_bit_exact(world):
     assert rots == rep_full["rotations"] - (M.info()["n1"] - 1)
     y = np.concatenate([be.decrypt(o)[:256] for o in outs])
     assert np.abs(y - A @ x).max() < 1e-5
+
+
+@pytest.mark.parametrize("name,shape", [("c1", (64, 64)), ("c2s", (512, 256))])
+def test_bsgs_token_batch_matches_single(name, shape):
+    """config 3 token batching (helix::matvec_bsgs_tokens): T ciphertexts
+    through one matrix with the key switches batched over tokens give the
+    same words as T separate matvecs, and per-token counters."""
+    from paper_2512_11135_b200.helix import BSGS
+
+    p, be = backend(name)
+    N = 1 << p["logn"]
+    rows, cols = shape
+    rng = np.random.default_rng(rows + 5)
+    A = rng.normal(0, 0.05, (rows, cols))
+    lvl = be.max_level
+    M = be.prepare(BSGS, A, lvl)
+    be.gen_rotation_keys(M.rotations())
+    xs = [rng.uniform(-1, 1, cols) for _ in range(3)]
+    cts = [be.encrypt(np.tile(x, be.slots // cols), lvl) for x in xs]
+    outs_t, rep_t = be.matvec_tokens(M, cts)
+    nq = lvl  # output level lvl - 1
+    for t, ct in enumerate(cts):
+        outs_1, rep_1 = be.matvec(M, ct)
+        assert rep_t == rep_1
+        assert len(outs_t[t]) == len(outs_1)
+        for a, b in zip(outs_t[t], outs_1):
+            assert np.array_equal(d2h(a.device_ptr(), 2 * nq * N), d2h(b.device_ptr(), 2 * nq * N))
+        y = np.concatenate([be.decrypt(o)[:cols] for o in outs_t[t]])[:rows]
+        assert np.abs(y - A @ xs[t]).max() < 1e-5
