@@ -617,22 +617,30 @@ template <class F>
 void pipelined_host(hx_ctx* c, int batch, std::vector<const uint64_t*> in_host,
                     std::vector<long long> in_words, uint64_t* out_host, long long out_words,
                     cudaStream_t s, F compute) {
-  const int chunk = std::max(1, std::min(batch, 32));
+  // chunks of 8 ciphertexts in a ring of 3 device slots: H2D of chunk i + 2,
+  // compute of i + 1 and D2H of i run at once, and pipeline fill / drain is one
+  // small chunk (PCIe, ~55 GB/s each way, is the bound of this path)
+  static const int chunk_env = [] {
+    const char* e = getenv("HX_PIPE_CHUNK");
+    return e ? atoi(e) : 0;
+  }();
+  constexpr int NS = 3;
+  const int chunk = std::max(1, std::min(batch, chunk_env > 0 ? chunk_env : 8));
   const int nchunks = (batch + chunk - 1) / chunk;
   cudaStream_t h = nullptr, d = nullptr;
   cuda_ok(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking), "stream");
   cuda_ok(cudaStreamCreateWithFlags(&d, cudaStreamNonBlocking), "stream");
-  cudaEvent_t ev_in[2], ev_cmp[2], ev_out[2];
-  for (int k = 0; k < 2; ++k) {
+  cudaEvent_t ev_in[NS], ev_cmp[NS], ev_out[NS];
+  for (int k = 0; k < NS; ++k) {
     cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_cmp[k], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming);
   }
-  // double-buffered chunk slots from the context arena (released in reverse order)
+  // chunk slots from the context arena (released in reverse order)
   std::vector<std::unique_ptr<DBuf>> slots;
-  std::vector<u64*> din[2];
-  u64* dout[2] = {nullptr, nullptr};
-  for (int k = 0; k < 2 && k < nchunks; ++k) {
+  std::vector<u64*> din[NS];
+  u64* dout[NS] = {};
+  for (int k = 0; k < NS && k < nchunks; ++k) {
     for (long long w : in_words) {
       slots.push_back(std::make_unique<DBuf>((size_t)w * chunk, s, c));
       din[k].push_back(slots.back()->p);
@@ -642,14 +650,14 @@ void pipelined_host(hx_ctx* c, int batch, std::vector<const uint64_t*> in_host,
   }
   cuda_ok(cudaStreamSynchronize(s), "sync");
   for (int i = 0; i < nchunks; ++i) {
-    const int k = i & 1, b0 = i * chunk, n = std::min(chunk, batch - b0);
-    if (i >= 2) cuda_ok(cudaStreamWaitEvent(h, ev_cmp[k], 0), "wait");
+    const int k = i % NS, b0 = i * chunk, n = std::min(chunk, batch - b0);
+    if (i >= NS) cuda_ok(cudaStreamWaitEvent(h, ev_cmp[k], 0), "wait");  // input slot consumed
     for (std::size_t a = 0; a < in_host.size(); ++a)
       cuda_ok(cudaMemcpyAsync(din[k][a], in_host[a] + (long long)b0 * in_words[a], (size_t)n * in_words[a] * 8,
                               cudaMemcpyHostToDevice, h), "h2d");
     cudaEventRecord(ev_in[k], h);
     cuda_ok(cudaStreamWaitEvent(s, ev_in[k], 0), "wait");
-    if (i >= 2) cuda_ok(cudaStreamWaitEvent(s, ev_out[k], 0), "wait");
+    if (i >= NS) cuda_ok(cudaStreamWaitEvent(s, ev_out[k], 0), "wait");  // output slot drained
     compute(dout[k], din[k], n, s);
     cudaEventRecord(ev_cmp[k], s);
     cuda_ok(cudaStreamWaitEvent(d, ev_cmp[k], 0), "wait");
@@ -659,7 +667,7 @@ void pipelined_host(hx_ctx* c, int batch, std::vector<const uint64_t*> in_host,
   }
   cuda_ok(cudaStreamSynchronize(d), "sync");
   cuda_ok(cudaStreamSynchronize(s), "sync");
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < NS; ++k) {
     cudaEventDestroy(ev_in[k]);
     cudaEventDestroy(ev_cmp[k]);
     cudaEventDestroy(ev_out[k]);
