@@ -323,8 +323,9 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=16, chunk=8):
             # of `chunk` tokens (hxc_matvec_tokens); per-token throughput
             xt = [be.encrypt(np.tile(np.concatenate([rng.uniform(-1, 1, M.shape[1]), np.zeros(d - M.shape[1])]),
                                      be.slots // d), lvl) for _ in range(chunk)]
-            outs_t, _ = be.matvec_tokens(mat, xt)  # warm-up
-            del outs_t
+            for _ in range(2):  # warm-up (arena high-water mark, pool growth)
+                outs_t, _ = be.matvec_tokens(mat, xt)
+                del outs_t
             torch.cuda.synchronize()
             e0.record()
             for _ in range(tokens // chunk):
@@ -513,9 +514,24 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_secs = float(tt.item())
     ct_bytes = BATCH * 2 * nq * N * 8
+    # the interconnect bound of this path: H2D and D2H of the step's bytes at the
+    # measured full-duplex pinned copy rate
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    dscratch = torch.empty_like(cts)
+    torch.cuda.synchronize()
+    td = time.perf_counter()
+    with torch.cuda.stream(s1):
+        dscratch.copy_(hin, non_blocking=True)
+    with torch.cuda.stream(s2):
+        hout_h.copy_(cts, non_blocking=True)
+    torch.cuda.synchronize()
+    duplex = ct_bytes / (time.perf_counter() - td)
+    del dscratch
     e2e = {"value": BATCH * e2e_steps * world / e2e_secs, "unit": "KS/s",
            "h2d_bytes_per_step": ct_bytes, "d2h_bytes_per_step": ct_bytes,
-           "api": "hx_rotate_host (pinned host buffers)"}
+           "api": "hx_rotate_host (pinned host buffers)",
+           "pcie_duplex_gbps_each_way": duplex / 1e9,
+           "pcie_bound_ks_per_s": BATCH * world * duplex / ct_bytes}
 
     if not args.no_extras and not args.no_ffn:
         del hin, hout_h, out, ntt_buf

@@ -156,6 +156,13 @@ int hx_bsgs_mac_ex(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, const 
 int hx_sum_strided(hx_ctx* ctx, uint64_t* out, const uint64_t* in, int terms, long long term_stride,
                    int polys, long long in_poly_stride, long long out_poly_stride, int n_q,
                    void* stream);
+/* token batch: `tokens` baby sets at baby + t baby_tstride words, inner sums at
+ * inner + t inner_tstride; one launch, the blocks of one (coefficient tile,
+ * limb) for all tokens run back to back so each diagonal word is read from
+ * HBM once (L2 for the other tokens) -- config 3 with T tokens per matrix */
+int hx_bsgs_mac_tokens(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, long long inner_tstride,
+                       const uint64_t* baby, long long baby_tstride, const uint64_t* diags, int diag_limbs, int n1,
+                       int n2, int n_q, int tokens, void* stream);
 int hx_bsgs_mac(hx_ctx* ctx, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,
                 int diag_limbs, int n1, int n2, int n_q, void* stream);
 

@@ -19,12 +19,15 @@ __global__ void __launch_bounds__(TT) bsgs_mac_kernel(MacArgs A) {
   const long long N = 1ll << A.logn;
   const int i = A.limbs ? A.limbs[blockIdx.y] : blockIdx.y;
   const int tid = threadIdx.x;
-  const long long t = (long long)blockIdx.x * TT + tid;
+  const int tok = blockIdx.x % A.tokens;
+  const long long t = (long long)(blockIdx.x / A.tokens) * TT + tid;
+  const u64* baby = A.baby + tok * A.baby_tstride;
+  u64* inner = A.inner + tok * A.inner_tstride;
   const PrimeConst& P = A.pc[i];
   const long long L = (long long)A.n_q * N;
   for (int k = 0; k < A.n1; ++k) {
-    smb[(2 * k) * TT + tid] = A.baby[(2ll * k) * L + i * N + t];
-    smb[(2 * k + 1) * TT + tid] = A.baby[(2ll * k + 1) * L + i * N + t];
+    smb[(2 * k) * TT + tid] = baby[(2ll * k) * L + i * N + t];
+    smb[(2 * k + 1) * TT + tid] = baby[(2ll * k + 1) * L + i * N + t];
   }
   __syncthreads();
   const u64* dg = A.diags + i * N + t;
@@ -60,7 +63,7 @@ __global__ void __launch_bounds__(TT) bsgs_mac_kernel(MacArgs A) {
       mac128(z0, d, smb[(2 * k) * TT + tid]);
       mac128(z1, d, smb[(2 * k + 1) * TT + tid]);
     }
-    u64* o = A.inner + (long long)j * A.out_jstride + i * N + t;
+    u64* o = inner + (long long)j * A.out_jstride + i * N + t;
     o[0] = reduce128(z0, P);
     o[L] = reduce128(z1, P);
   }
@@ -95,7 +98,10 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_f64_kernel(MacArgs A,
   const long long N = 1ll << A.logn;
   const int i = limbs[blockIdx.y];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long t = (long long)blockIdx.x * 32 + lane;
+  const int tok = blockIdx.x % A.tokens;
+  const long long t = (long long)(blockIdx.x / A.tokens) * 32 + lane;
+  const u64* baby = A.baby + tok * A.baby_tstride;
+  u64* inner = A.inner + tok * A.inner_tstride;
   const PrimeConst& P = A.pc[i];
   const long long L = (long long)A.n_q * N;
   // baby words of this warp's k slice, split into 20-bit halves
@@ -104,7 +110,7 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_f64_kernel(MacArgs A,
   for (int kk = 0; kk < KPT; ++kk) {
     const int k = w * KPT + kk;
 #pragma unroll
-    for (int c = 0; c < 2; ++c) split20(A.baby[(2ll * k + c) * L + i * N + t], bh[kk][c], bl[kk][c]);
+    for (int c = 0; c < 2; ++c) split20(baby[(2ll * k + c) * L + i * N + t], bh[kk][c], bl[kk][c]);
   }
   const u64* dg = A.diags + i * N + t + (long long)(w * KPT) * A.diag_stride;
   u64 dn[KPT];
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_f64_kernel(MacArgs A,
       const double v = __dadd_rn(__dadd_rn(mulmod_f64(S[0], P.r40_d, P.r40_q, P.qd),
                                            mulmod_f64(S[1], P.r20_d, P.r20_q, P.qd)),
                                  centre_f64(S[2], P.qd, P.qinv_d));
-      A.inner[(long long)j * A.out_jstride + c * L + i * N + t] =
+      inner[(long long)j * A.out_jstride + c * L + i * N + t] =
           f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);
     }
   }
@@ -164,7 +170,10 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_int_kernel(MacArgs A,
   const long long N = 1ll << A.logn;
   const int i = limbs[blockIdx.y];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long t = (long long)blockIdx.x * 32 + lane;
+  const int tok = blockIdx.x % A.tokens;
+  const long long t = (long long)(blockIdx.x / A.tokens) * 32 + lane;
+  const u64* baby = A.baby + tok * A.baby_tstride;
+  u64* inner = A.inner + tok * A.inner_tstride;
   const PrimeConst& P = A.pc[i];
   const long long L = (long long)A.n_q * N;
   u64 b[KPT][2];
@@ -172,7 +181,7 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_int_kernel(MacArgs A,
   for (int kk = 0; kk < KPT; ++kk) {
     const int k = w * KPT + kk;
 #pragma unroll
-    for (int c = 0; c < 2; ++c) b[kk][c] = A.baby[(2ll * k + c) * L + i * N + t];
+    for (int c = 0; c < 2; ++c) b[kk][c] = baby[(2ll * k + c) * L + i * N + t];
   }
   const u64* dg = A.diags + i * N + t + (long long)(w * KPT) * A.diag_stride;
   u64 dn[KPT];
@@ -208,7 +217,7 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_int_kernel(MacArgs A,
             : "+l"(S.lo), "+l"(S.hi)
             : "l"(part[buf][ww][c][0][lane]), "l"(part[buf][ww][c][1][lane]));
       }
-      A.inner[(long long)j * A.out_jstride + c * L + i * N + t] = reduce128(S, P);
+      inner[(long long)j * A.out_jstride + c * L + i * N + t] = reduce128(S, P);
     }
   }
 }
@@ -231,7 +240,7 @@ void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s, const int* d
   const int kpt = A.n1 / kMacWarps;
   const bool f64_ok = n_f64 > 0 && N >= 32 && A.n1 % kMacWarps == 0 && (kpt == 1 || kpt == 2 || kpt == 4 || kpt == 8);
   if (f64_ok) {
-    dim3 grid((unsigned)(N / 32), (unsigned)n_f64);
+    dim3 grid((unsigned)(N / 32 * A.tokens), (unsigned)n_f64);
     switch (kpt) {
       case 1: bsgs_mac_f64_kernel<1><<<grid, 32 * kMacWarps, 0, s>>>(A, d_f64_limbs); break;
       case 2: bsgs_mac_f64_kernel<2><<<grid, 32 * kMacWarps, 0, s>>>(A, d_f64_limbs); break;
@@ -241,7 +250,7 @@ void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s, const int* d
   }
   // integer k-split kernel for the wide primes
   if (f64_ok && n_int > 0) {
-    dim3 grid((unsigned)(N / 32), (unsigned)n_int);
+    dim3 grid((unsigned)(N / 32 * A.tokens), (unsigned)n_int);
     switch (kpt) {
       case 1: bsgs_mac_int_kernel<1><<<grid, 32 * kMacWarps, 0, s>>>(A, d_int_limbs); break;
       case 2: bsgs_mac_int_kernel<2><<<grid, 32 * kMacWarps, 0, s>>>(A, d_int_limbs); break;
@@ -257,7 +266,7 @@ void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s, const int* d
     const size_t smem = (size_t)A.n1 * 2 * TT * sizeof(u64);
     MacArgs B = A;
     B.limbs = il;
-    dim3 grid((unsigned)(N / TT), (unsigned)ni);
+    dim3 grid((unsigned)(N / TT * A.tokens), (unsigned)ni);
     bsgs_mac_kernel<TT><<<grid, TT, smem, s>>>(B);
   }
 }

@@ -1267,12 +1267,14 @@ int hx_mul_relin(hx_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b,
   });
 }
 
-int hx_bsgs_mac_ex(hx_ctx* c, uint64_t* inner, long long inner_jstride, const uint64_t* baby,
-                   const uint64_t* diags, int diag_limbs, int n1, int n2, int n_q, void* s) {
+int hx_bsgs_mac_tokens(hx_ctx* c, uint64_t* inner, long long inner_jstride, long long inner_tstride,
+                       const uint64_t* baby, long long baby_tstride, const uint64_t* diags, int diag_limbs, int n1,
+                       int n2, int n_q, int tokens, void* s) {
   return guarded([&] {
     check_ctx(c);
     check_nq(c, n_q);
-    HX_REQUIRE(n1 >= 1 && n1 <= 64 && n2 >= 1 && diag_limbs >= n_q, "bsgs_mac: bad shape");
+    HX_REQUIRE(n1 >= 1 && n1 <= 64 && n2 >= 1 && diag_limbs >= n_q && tokens >= 1, "bsgs_mac: bad shape");
+    HX_REQUIRE((long long)tokens * (c->N() / 32) < (1ll << 31), "bsgs_mac: too many tokens");
     hx::MacArgs A;
     A.inner = (u64*)inner;
     A.baby = (const u64*)baby;
@@ -1285,10 +1287,18 @@ int hx_bsgs_mac_ex(hx_ctx* c, uint64_t* inner, long long inner_jstride, const ui
     A.diag_stride = (long long)diag_limbs * c->N();
     A.out_jstride = inner_jstride;
     A.limbs = nullptr;
+    A.tokens = tokens;
+    A.baby_tstride = baby_tstride;
+    A.inner_tstride = inner_tstride;
     const int* lists = c->d_maclimbs + (size_t)n_q * 2 * c->n_chain;
     hx::launch_bsgs_mac(A, c->N(), S(s), lists, c->mac_nf64[n_q], lists + c->n_chain, c->mac_nint[n_q]);
     launched(c, "bsgs_mac_kernel", 2);
   });
+}
+
+int hx_bsgs_mac_ex(hx_ctx* c, uint64_t* inner, long long inner_jstride, const uint64_t* baby,
+                   const uint64_t* diags, int diag_limbs, int n1, int n2, int n_q, void* s) {
+  return hx_bsgs_mac_tokens(c, inner, inner_jstride, 0, baby, 0, diags, diag_limbs, n1, n2, n_q, 1, s);
 }
 
 int hx_bsgs_mac(hx_ctx* c, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,

@@ -25,6 +25,12 @@ struct MacArgs {
   long long diag_stride;  // words between consecutive diagonals
   long long out_jstride;  // words between inner_j and inner_{j+1} (2 n_q N when packed)
   const int* limbs;       // device limb list for blockIdx.y (null: identity)
+  // token batch: `tokens` baby sets at baby + t baby_tstride, inner sums at
+  // inner + t inner_tstride; the token index varies fastest along blockIdx.x
+  // (blocks of one coefficient tile and limb run back to back, so every
+  // diagonal word comes from HBM once and from L2 for the other tokens)
+  int tokens;
+  long long baby_tstride, inner_tstride;
 };
 
 // out = sum_{r < terms} in + r * term_stride, per (poly, limb) of `polys`

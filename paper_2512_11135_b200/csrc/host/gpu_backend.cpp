@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -664,10 +665,24 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       if (have_scale && D[0].scale != dscale) throw ScaleMismatchError("bsgs: diagonal scales differ");
       dscale = D[0].scale;
       have_scale = true;
-      for (int t = 0; t < T; ++t)
-        ck(hx_bsgs_mac_ex(ctx_, inner->ptr + ((std::size_t)t * blocks + b) * ctw, (long long)jstride, baby_ptr[t],
-                          p0->data(), nqv, n1, n2, nqv, nullptr),
+      // one launch over the tokens when their baby sets sit at a uniform stride
+      static const bool tok_mac = [] {
+        const char* e = getenv("HX_MAC_TOKENS");
+        return !e || atoi(e) != 0;
+      }();
+      bool uniform = tok_mac;
+      const long long bstride = T > 1 ? (long long)(baby_ptr[1] - baby_ptr[0]) : 0;
+      for (int t = 1; t < T && uniform; ++t) uniform = (long long)(baby_ptr[t] - baby_ptr[t - 1]) == bstride;
+      if (uniform) {
+        ck(hx_bsgs_mac_tokens(ctx_, inner->ptr + (std::size_t)b * ctw, (long long)jstride, (long long)(blocks * ctw),
+                              baby_ptr[0], bstride, p0->data(), nqv, n1, n2, nqv, T, nullptr),
            "bsgs_mac");
+      } else {
+        for (int t = 0; t < T; ++t)
+          ck(hx_bsgs_mac_ex(ctx_, inner->ptr + ((std::size_t)t * blocks + b) * ctw, (long long)jstride, baby_ptr[t],
+                            p0->data(), nqv, n1, n2, nqv, nullptr),
+             "bsgs_mac");
+      }
       ptmuls = d;
       adds = (std::uint64_t)(n1 - 1) * n2;
       for (int j = 0; j < n2; ++j) live[b][j] = 1;
