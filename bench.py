@@ -534,7 +534,9 @@ def main():
            "pcie_bound_ks_per_s": BATCH * world * duplex / ct_bytes}
 
     if not args.no_extras and not args.no_ffn:
-        del hin, hout_h, out, ntt_buf
+        del hin, hout_h, out, ntt_buf, cts
+        torch.cuda.synchronize()
+        ctx.trim()  # the headline's ~50 GB scratch arena is not needed by the extras
         torch.cuda.empty_cache()
         extras.update(ffn_bsgs_bench(torch, chain, special, args))
         torch.cuda.empty_cache()

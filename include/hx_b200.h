@@ -59,6 +59,9 @@ void hx_ctx_destroy(hx_ctx* ctx);
 int hx_ctx_dnum(const hx_ctx* ctx, int n_q);
 uint64_t hx_ctx_psi(const hx_ctx* ctx, int prime_index);
 size_t hx_key_words(const hx_ctx* ctx);
+/* release the context's scratch arena (the high-water mark of its calls) and
+ * the device pool's idle memory; the next call regrows it */
+int hx_ctx_trim(hx_ctx* ctx);
 /* number of kernels this context has launched so far (bench evidence) */
 unsigned long long hx_ctx_launches(const hx_ctx* ctx);
 

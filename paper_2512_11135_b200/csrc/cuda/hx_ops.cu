@@ -147,10 +147,17 @@ struct DBuf {
       A.stream = st;
       A.stream_set = true;
       if (A.depth == 0 && A.high > A.cap) {  // regrow to the high-water mark
-        if (A.base) cuda_ok(cudaFreeAsync(A.base, st), "cudaFreeAsync(arena)");
+        // the arena is a plain cudaMalloc block outside the stream-ordered pool:
+        // freeing it returns the memory to the device at once (the pool keeps
+        // what it frees), and the pool's cached blocks stay untouched
+        if (A.base) {
+          cuda_ok(cudaStreamSynchronize(st), "sync");
+          cuda_ok(cudaFree(A.base), "cudaFree(arena)");
+        }
         A.base = nullptr;
-        cuda_ok(cudaMallocAsync((void**)&A.base, A.high, st), "cudaMallocAsync(arena)");
+        cuda_ok(cudaMalloc((void**)&A.base, A.high), "cudaMalloc(arena)");
         A.cap = A.high;
+        if (getenv("HX_ALLOC_TRACE")) fprintf(stderr, "[hx] arena regrown to %.2f GB\n", A.cap * 1e-9);
       }
       A.depth++;
       A.high = std::max(A.high, A.top + bytes);
@@ -964,12 +971,25 @@ void hx_ctx_destroy(hx_ctx* c) {
                   (void*)c->d_tlist})
     if (p) cudaFree(p);
   if (c->arena.base) {
-    cudaStreamSynchronize(c->arena.stream);
-    cudaFreeAsync(c->arena.base, c->arena.stream);
-    cudaStreamSynchronize(c->arena.stream);
+    cudaDeviceSynchronize();
+    cudaFree(c->arena.base);
   }
   if (c->arena.ev) cudaEventDestroy(c->arena.ev);
   delete c;
+}
+
+int hx_ctx_trim(hx_ctx* c) {
+  return guarded([&] {
+    check_ctx(c);
+    HxArena& A = c->arena;
+    HX_REQUIRE(A.depth == 0, "hx_ctx_trim: scratch in use");
+    cuda_ok(cudaDeviceSynchronize(), "sync");
+    if (A.base) cuda_ok(cudaFree(A.base), "cudaFree(arena)");
+    A.base = nullptr;
+    A.cap = A.high = A.top = 0;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  });
 }
 
 int hx_ctx_dnum(const hx_ctx* c, int n_q) { return c ? c->dnum(n_q) : -1; }

@@ -69,6 +69,7 @@ def lib() -> C.CDLL:
         "hx_bsgs_mac": [v, v, v, v, i32, i32, i32, i32, v],
         "hx_keygen_ksk": [v, v, v, v, v, v, v],
         "hx_sample_uniform": [v, v, i32, i32, i32, C.c_uint64, v],
+        "hx_ctx_trim": [v],
         "hx_sample_cbd": [v, v, C.c_longlong, C.c_uint64, v],
         "hx_encrypt_sk": [v, v, v, v, v, v, i32, v],
         "hx_ksk_to_rotation_layout": [v, v, v, u64, v],
@@ -235,6 +236,10 @@ class Context:
         out = torch.empty_like(key)
         self.ksk_to_rotation_layout(out, key, g, stream)
         return out
+
+    def trim(self):
+        """release the context's scratch arena and the pool's idle memory"""
+        _check(self.L.hx_ctx_trim(self.h), "hx_ctx_trim")
 
     def sample_uniform(self, out, n_c, n_s, copies, seed, stream=None):
         _check(self.L.hx_sample_uniform(self.h, _p(out), n_c, n_s, copies, seed, _stream(stream)), "hx_sample_uniform")
