@@ -241,6 +241,12 @@ struct InnerArgs {
   int n_q, n_chain, n_special, dnum, batch;
   u32 g;  // 1 = identity (input-side automorphism of the digits)
   int logn;
+  // own limbs: when c1 is set, digit d's own chain limbs j in [d alpha,
+  // d alpha + alpha) are read from the ModUp input c1 (element stride
+  // c1_stride words) -- ModUp then skips copying them into the digit buffer
+  const u64* c1;
+  long long c1_stride;
+  int alpha;
 };
 
 // FP64 variant for limbs with q < 2^43: the key words are split once into
@@ -285,11 +291,14 @@ __global__ void __launch_bounds__(256, 2) ks_inner_f64_kernel(InnerArgs A, const
   const long long dstride = (long long)A.dnum * ext * N;
   const long long ebase = A.shared ? 0 : (long long)r * E;
   u64* ubase = A.u + (long long)r * E * 2 * ext * N;
+  const int down = (A.c1 && j < A.n_q) ? j / A.alpha : -1;  // digit owning limb j
   for (int b = b_lo; b < b_hi; ++b) {
     const u64* Db = A.digits + (ebase + b) * dstride + (long long)j * N + src;
+    const u64* Cb = down >= 0 ? A.c1 + (ebase + b) * A.c1_stride + (long long)j * N + src : nullptr;
     u64 v[MAXD];
 #pragma unroll
-    for (int d = 0; d < MAXD; ++d) v[d] = d < A.dnum ? __ldcs(Db + (long long)d * ext * N) : 0ull;
+    for (int d = 0; d < MAXD; ++d)
+      v[d] = d < A.dnum ? __ldcs(d == down ? Cb : Db + (long long)d * ext * N) : 0ull;
     double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll
     for (int d = 0; d < MAXD; ++d) {
@@ -337,14 +346,16 @@ __global__ void __launch_bounds__(256, 2) ks_inner_kernel(InnerArgs A, const int
   const long long dstride = (long long)A.dnum * ext * N;
   const long long ebase = A.shared ? 0 : (long long)r * E;  // digit element of e = 0
   u64* ubase = A.u + (long long)r * E * 2 * ext * N;
+  const int down = (A.c1 && j < A.n_q) ? j / A.alpha : -1;  // digit owning limb j
   for (int b0 = b_lo; b0 < b_hi; b0 += BB) {
     u64 v[BB][MAXD];
 #pragma unroll
     for (int bb = 0; bb < BB; ++bb) {
       const u64* Db = A.digits + (ebase + b0 + bb) * dstride + (long long)j * N + src;
+      const u64* Cb = down >= 0 ? A.c1 + (ebase + b0 + bb) * A.c1_stride + (long long)j * N + src : nullptr;
 #pragma unroll
       for (int d = 0; d < MAXD; ++d)
-        v[bb][d] = (d < A.dnum && b0 + bb < b_hi) ? __ldcs(Db + (long long)d * ext * N) : 0ull;
+        v[bb][d] = (d < A.dnum && b0 + bb < b_hi) ? __ldcs(d == down ? Cb : Db + (long long)d * ext * N) : 0ull;
     }
 #pragma unroll
     for (int bb = 0; bb < BB; ++bb) {

@@ -277,8 +277,10 @@ bool modup_fused_ok(const hx_ctx* c, int n_q) {
 }
 
 // c1: [batch] polys of n_q limbs at stride c1_stride words.
+// copy_own = false: the digits' own limbs are left out of `digits` (the key
+// inner product reads them from c1, InnerArgs::c1)
 void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long batch, int n_q,
-           cudaStream_t s) {
+           cudaStream_t s, bool copy_own = true) {
   const long long N = c->N();
   const int K = c->n_special, ext = n_q + K, dnum = c->dnum(n_q);
   DBuf coef(batch * n_q * N, s, c);
@@ -306,8 +308,9 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
       A.qh_off[d] = c->modup_qh_off[n_q][d];
       A.bc_off[d] = c->bc_off[n_q][d];
       const int lo = d * c->alpha, cnt = std::min(c->alpha, n_q - lo);
-      copy2d(digits + ((long long)d * ext + lo) * N, (long long)dnum * ext * N, c1 + (long long)lo * N, c1_stride,
-             (long long)cnt * N, batch, s);
+      if (copy_own)
+        copy2d(digits + ((long long)d * ext + lo) * N, (long long)dnum * ext * N, c1 + (long long)lo * N, c1_stride,
+               (long long)cnt * N, batch, s);
       for (int j = 0; j < ext; ++j) {
         if (j >= lo && j < lo + cnt) continue;
         HX_REQUIRE(lt.count < hx::kMaxLimbEntries, "modup: too many limbs for one launch");
@@ -387,7 +390,8 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
 //   !shared: keys[r] applies to digit elements r E .. r E + E - 1.
 // Output element (r, e) at u + (r E + e) 2 ext N.
 void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<const u64*>& keys,
-                    bool shared, long long E, int n_q, u64 g, cudaStream_t s) {
+                    bool shared, long long E, int n_q, u64 g, cudaStream_t s, const u64* c1 = nullptr,
+                    long long c1_stride = 0) {
   HX_REQUIRE(!keys.empty() && (int)keys.size() <= hx::kMaxKeys, "ks_inner: 1..64 keys per launch");
   hx::InnerArgs A;
   A.digits = digits;
@@ -404,6 +408,9 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
   A.batch = (int)batch;
   A.g = (hx::u32)g;
   A.logn = c->logn;
+  A.c1 = c1;
+  A.c1_stride = c1_stride;
+  A.alpha = c->alpha;
   const int th = pt_threads(c);
   // split each key's elements over slices: more CTAs in flight, the key words
   // of a (limb, coefficient) are re-read only once per slice
@@ -440,8 +447,8 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
 }
 
 void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long batch, int n_q,
-              u64 g, cudaStream_t s) {
-  ks_inner_multi(c, u, digits, {key}, true, batch, n_q, g, s);
+              u64 g, cudaStream_t s, const u64* c1 = nullptr, long long c1_stride = 0) {
+  ks_inner_multi(c, u, digits, {key}, true, batch, n_q, g, s, c1, c1_stride);
 }
 
 // Centred ModDown of `polys` PQ-basis polys u (stride u_stride words) into
@@ -599,7 +606,8 @@ void rotate_batch_from_digits(hx_ctx* c, u64* out, const u64* in, const u64* dig
     const long long nr = std::min<long long>(hx::kMaxKeys, R - r0);
     const std::vector<const u64*> kk(keys.begin() + r0, keys.begin() + r0 + nr);
     const u64* dg = shared ? digits : digits + r0 * E * dstride;
-    ks_inner_multi(c, U.p + r0 * E * 2 * ext * N, dg, kk, shared, E, n_q, 1, s);
+    const u64* c1 = (shared ? in : in + r0 * E * ct) + (long long)n_q * N;  // own limbs (not copied by ModUp)
+    ks_inner_multi(c, U.p + r0 * E * 2 * ext * N, dg, kk, shared, E, n_q, 1, s, c1, ct);
   }
   // polys p = (r E + e) 2 + c; the c0 polys add input ct (shared ? e : r E + e);
   // the output automorphism tau_{g_r} is fused into the combine (64 keys per call)
@@ -1157,8 +1165,8 @@ int hx_keyswitch(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* k
     const long long N = c->N();
     const int ext = n_q + c->n_special;
     DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s), c), U((long long)batch * 2 * ext * N, S(s), c);
-    modup(c, D.p, (const u64*)in, (long long)n_q * N, batch, n_q, S(s));
-    ks_inner(c, U.p, D.p, (const u64*)key, batch, n_q, 1, S(s));
+    modup(c, D.p, (const u64*)in, (long long)n_q * N, batch, n_q, S(s), false);
+    ks_inner(c, U.p, D.p, (const u64*)key, batch, n_q, 1, S(s), (const u64*)in, (long long)n_q * N);
     moddown(c, (u64*)out, (long long)n_q * N, U.p, (long long)ext * N, 2ll * batch, n_q, nullptr,
             0, 1, S(s));
   });
@@ -1174,7 +1182,7 @@ int hx_rotate(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* key,
     const long long N = c->N();
     const int ext = n_q + c->n_special;
     DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s), c);
-    modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s));
+    modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s), false);
     rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, {(const u64*)key}, {g}, true, batch,
                              n_q, S(s));
   });
@@ -1189,7 +1197,7 @@ int hx_rotate_hoisted(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
     const long long N = c->N();
     const int ext = n_q + c->n_special;
     DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s), c);
-    modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s));
+    modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s), false);
     std::vector<const u64*> kk;
     std::vector<u64> gg;
     for (int r = 0; r < R; ++r) {
@@ -1212,7 +1220,7 @@ int hx_rotate_multi(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t
     for (int b = 0; b < batch; ++b)
       HX_REQUIRE((galois[b] & 1) && galois[b] < 2 * (u64)N, "galois element");
     DBuf D((long long)batch * dstride, S(s), c);
-    modup(c, D.p, (const u64*)in + (long long)n_q * N, ct, batch, n_q, S(s));
+    modup(c, D.p, (const u64*)in + (long long)n_q * N, ct, batch, n_q, S(s), false);
     std::vector<const u64*> kk;
     std::vector<u64> gg;
     for (int b = 0; b < batch; ++b) {
@@ -1246,7 +1254,7 @@ int hx_rotate_grouped(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
       const int nr = std::min(Rc, R - r0);
       const u64* ip = (const u64*)in + (long long)r0 * E * ct;
       DBuf D((long long)nr * E * c->dnum(n_q) * ext * N, S(s), c);
-      modup(c, D.p, ip + (long long)n_q * N, ct, (long long)nr * E, n_q, S(s));
+      modup(c, D.p, ip + (long long)n_q * N, ct, (long long)nr * E, n_q, S(s), false);
       const std::vector<const u64*> kc(kk.begin() + r0, kk.begin() + r0 + nr);
       const std::vector<u64> gc(gg.begin() + r0, gg.begin() + r0 + nr);
       rotate_batch_from_digits(c, (u64*)out + (long long)r0 * E * ct, ip, D.p, kc, gc, false, E, n_q, S(s));
@@ -1273,14 +1281,14 @@ int hx_mul_relin(hx_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b,
     check_nq(c, n_q);
     const long long N = c->N(), L = (long long)n_q * N;
     const int ext = n_q + c->n_special;
-    DBuf d3((long long)batch * 3 * L, S(s)), D((long long)batch * c->dnum(n_q) * ext * N, S(s)),
-        U((long long)batch * 2 * ext * N, S(s));
+    DBuf d3((long long)batch * 3 * L, S(s), c), D((long long)batch * c->dnum(n_q) * ext * N, S(s), c),
+        U((long long)batch * 2 * ext * N, S(s), c);
     const int th = pt_threads(c);
     hx::tensor_kernel<<<dim3((unsigned)(N / th), (unsigned)n_q, (unsigned)batch), th, 0, S(s)>>>(
         d3.p, (const u64*)a, (const u64*)b, c->d_pc, n_q, c->logn);
     launched(c, "tensor_kernel");
-    modup(c, D.p, d3.p + 2 * L, 3 * L, batch, n_q, S(s));
-    ks_inner(c, U.p, D.p, (const u64*)rlk, batch, n_q, 1, S(s));
+    modup(c, D.p, d3.p + 2 * L, 3 * L, batch, n_q, S(s), false);
+    ks_inner(c, U.p, D.p, (const u64*)rlk, batch, n_q, 1, S(s), d3.p + 2 * L, 3 * L);
     moddown(c, (u64*)out, 2 * L, U.p, 2ll * ext * N, batch, n_q, d3.p, 3 * L, 1, S(s));
     moddown(c, (u64*)out + L, 2 * L, U.p + (long long)ext * N, 2ll * ext * N, batch, n_q,
             d3.p + L, 3 * L, 1, S(s));
