@@ -345,6 +345,56 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=16, chunk=8):
     return out
 
 
+def sharded_bsgs_bench(torch, dist, chain, special, rank, world, rows=11008, cols=4096, iters=3):
+    """BASELINE configs[4]: W (11008 x 4096, N(0, 0.02^2)) x (4096, U[-1,1],
+    replicated 8x over the slots) as a BSGS matvec (d = 4096, 3 row blocks,
+    12288 diagonals) sharded over the ranks by giant step:
+    rank r encodes and keys only its giant groups' diagonals, computes the baby
+    steps locally, and the pre-rescale partials are summed with one NCCL
+    all-reduce (int64 words = exact u64 sum), reduced mod q and rescaled once
+    (paper_2512_11135_b200/shard.py).  Time = max over ranks."""
+    from paper_2512_11135_b200.helix import Backend, params_json
+    from paper_2512_11135_b200.shard import sharded_matvec
+
+    rng = np.random.default_rng(20251211 * 10 + 5)
+    be = Backend(params_json(LOGN, chain, special, ALPHA, 40), seed=5)  # same seed: same keys on every rank
+    W = rng.normal(0.0, 0.02, (rows, cols))
+    x = rng.uniform(-1, 1, cols)
+    lvl = be.max_level
+    t0 = time.perf_counter()
+    M = be.prepare_shard(W, lvl, rank, world)
+    be.gen_rotation_keys(M.rotations())
+    torch.cuda.synchronize()
+    prep = time.perf_counter() - t0
+    ct = be.encrypt(np.tile(x, be.slots // cols), lvl)
+    allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else (lambda t: None)
+    outs, rep = sharded_matvec(be, M, ct, lvl + 1, N, allreduce, torch)  # warm-up + correctness
+    y = np.concatenate([be.decrypt(o)[:cols] for o in outs])[:rows]
+    err = float(np.abs(y - W @ x).max())
+    del outs
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(iters):
+        outs, rep = sharded_matvec(be, M, ct, lvl + 1, N, allreduce, torch)
+        del outs
+    e1.record()
+    torch.cuda.synchronize()
+    secs = e0.elapsed_time(e1) / 1e3 / iters
+    if world > 1:
+        tt = torch.tensor([secs], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        secs = float(tt.item())
+    info = M.info()
+    be.close()
+    return {"sharded_bsgs_config5": {"matvec_per_s": 1.0 / secs, "ms_per_matvec": 1e3 * secs, "max_abs_err": err,
+                                     "gpus": world, "rows": rows, "cols": cols, "d": info["d"],
+                                     "row_blocks": info["blocks"], "local_nonzero_diagonals": info["nonzero"],
+                                     "rotations_local": rep["rotations"], "prepare_s": prep}}
+
+
 def matmul_bench(torch, chain, special, d=128, n_q=4, iters=2):
     """BASELINE configs[3]: ct x ct matmul Q K^T of one head (128 x 64 padded to
     d = 128, N(0, 1)) through hxc_matmul (SPEC square-padded schedule), at a
@@ -544,6 +594,12 @@ def main():
             extras.update(matmul_bench(torch, chain, special))
         except Exception as exc:  # reported, never fatal for the headline line
             extras["matmul_d128"] = {"error": str(exc)[:200]}
+        if world > 1:  # config 5 needs >= 2 GPUs of memory (183 GB of diagonals + keys)
+            torch.cuda.empty_cache()
+            try:
+                extras.update(sharded_bsgs_bench(torch, dist, chain, special, rank, world))
+            except Exception as exc:
+                extras["sharded_bsgs_config5"] = {"error": str(exc)[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
