@@ -11,6 +11,7 @@
 
 using namespace hx;
 
+template <bool XCH>
 __global__ void __launch_bounds__(128) k_groups(u64* out, const PrimeConst* pc, int reps, int logn) {
   const PrimeConst P = pc[0];
   u64 x[16];
@@ -18,8 +19,17 @@ __global__ void __launch_bounds__(128) k_groups(u64* out, const PrimeConst* pc, 
   for (int r = 0; r < 16; ++r) x[r] = u64_to_f64bits((threadIdx.x * 16 + r) % 1000003);
   int eb[1], jb[1];
   group_index<false, 8, 3, 4>(threadIdx.x, 4, logn, blockIdx.x & 31, eb, jb);
+  __shared__ u64 sm[2048];
   for (int it = 0; it < reps; ++it) {
     ntt_group_f64<true, false, 8, 3, 4>(x, jb, 4, logn, P.twf_fwd, nullptr, P, false);
+    if (XCH) {  // the pass kernels' group exchange: sync, 16 STS, sync, 16 LDS (transposed)
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) sm[swz<false>(r * 128 + threadIdx.x)] = x[r];
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) x[r] = sm[swz<false>((threadIdx.x & 7) | ((threadIdx.x >> 3) << 7) | (r << 3))];
+    }
 #pragma unroll
     for (int r = 0; r < 16; ++r) {  // keep values bounded (as the pass's normalisation would)
       double v = __longlong_as_double((long long)x[r]);
@@ -56,22 +66,25 @@ int main() {
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   u64* out;
   cudaMalloc(&out, (size_t)sms * 64 * 128 * 8);
-  for (int ctas : {2, 4, 7, 12}) {
+  for (int xch = 0; xch < 2; ++xch)
+  for (int ctas : {4, 7, 12}) {
     const int reps = 200, blocks = sms * ctas;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    k_groups<<<blocks, 128>>>(out, dpc, reps, logn);
+    auto kk = xch ? k_groups<true> : k_groups<false>;
+    kk<<<blocks, 128>>>(out, dpc, reps, logn);
     cudaEventRecord(a);
-    k_groups<<<blocks, 128>>>(out, dpc, reps, logn);
+    kk<<<blocks, 128>>>(out, dpc, reps, logn);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
     cudaEventElapsedTime(&ms, a, b);
     const double bfly = (double)blocks * 128 * reps * 32;  // 4 stages x 8 butterflies per thread per group
     const double fp64_ops = bfly * 8 + (double)blocks * 128 * reps * 16 * 2;  // + centring
-    printf("CTAs/SM %2d: %.3f ms  %.2f Gbfly/s  FP64 %.1f lanes/clk/SM\n", ctas, ms, bfly / ms / 1e6,
+    printf("xch %d CTAs/SM %2d: %.3f ms  %.2f Gbfly/s  FP64 %.1f lanes/clk/SM\n", xch, ctas, ms, bfly / ms / 1e6,
            fp64_ops / (ms * 1e-3) / sms / (clk * 1e3));
+    (void)0;
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
