@@ -44,6 +44,13 @@ struct HxError : std::runtime_error {
     if (!(cond)) throw HxError(HX_ERR_INVALID, msg); \
   } while (0)
 
+// element counts: negative is an error, zero a no-op (no zero-sized launches)
+#define HX_COUNT(n)                                   \
+  do {                                                \
+    HX_REQUIRE((n) >= 0, "negative element count");   \
+    if ((n) == 0) return;                              \
+  } while (0)
+
 void cuda_ok(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     throw HxError(HX_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -1037,7 +1044,8 @@ int hx_device_sync(void) {
 int hx_ntt_fwd(hx_ctx* c, uint64_t* data, int batch, int n_q, int n_p, void* s) {
   return guarded([&] {
     check_ctx(c);
-    HX_REQUIRE(n_q >= 0 && n_q <= c->n_chain && n_p >= 0 && n_p <= c->n_special, "limbs");
+    HX_COUNT(batch);
+    HX_REQUIRE(n_q >= 0 && n_q <= c->n_chain && n_p >= 0 && n_p <= c->n_special && n_q + n_p >= 1, "limbs");
     hx::ntt_forward(c, (u64*)data, batch, hx::make_table(c, n_q, n_p), S(s));
     cuda_ok(cudaGetLastError(), "ntt_forward");
   });
@@ -1046,7 +1054,8 @@ int hx_ntt_fwd(hx_ctx* c, uint64_t* data, int batch, int n_q, int n_p, void* s) 
 int hx_ntt_inv(hx_ctx* c, uint64_t* data, int batch, int n_q, int n_p, void* s) {
   return guarded([&] {
     check_ctx(c);
-    HX_REQUIRE(n_q >= 0 && n_q <= c->n_chain && n_p >= 0 && n_p <= c->n_special, "limbs");
+    HX_COUNT(batch);
+    HX_REQUIRE(n_q >= 0 && n_q <= c->n_chain && n_p >= 0 && n_p <= c->n_special && n_q + n_p >= 1, "limbs");
     hx::ntt_inverse(c, (u64*)data, batch, hx::make_table(c, n_q, n_p), S(s));
     cuda_ok(cudaGetLastError(), "ntt_inverse");
   });
@@ -1057,6 +1066,7 @@ int hx_ntt_inv(hx_ctx* c, uint64_t* data, int batch, int n_q, int n_p, void* s) 
            int n_p, void* s) {                                                                \
     return guarded([&] {                                                                      \
       check_ctx(c);                                                                           \
+      HX_COUNT(batch);                                                                        \
       ew<OP>(c, (u64*)out, (const u64*)a, (const u64*)b, batch, hx::make_table(c, n_q, n_p),   \
              S(s));                                                                           \
     });                                                                                       \
@@ -1070,6 +1080,7 @@ int hx_mul_acc(hx_ctx* c, uint64_t* acc, const uint64_t* a, const uint64_t* b, i
                int n_p, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     ew<hx::EwOp::MulAcc>(c, (u64*)acc, (const u64*)a, (const u64*)b, batch,
                          hx::make_table(c, n_q, n_p), S(s));
   });
@@ -1078,6 +1089,7 @@ int hx_mul_acc(hx_ctx* c, uint64_t* acc, const uint64_t* a, const uint64_t* b, i
 int hx_neg(hx_ctx* c, uint64_t* out, const uint64_t* a, int batch, int n_q, int n_p, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     ew<hx::EwOp::Neg>(c, (u64*)out, (const u64*)a, nullptr, batch, hx::make_table(c, n_q, n_p),
                       S(s));
   });
@@ -1087,6 +1099,7 @@ int hx_automorphism(hx_ctx* c, uint64_t* out, const uint64_t* in, int batch, int
                     uint64_t g, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element must be odd and < 2N");
     HX_REQUIRE(out != in, "automorphism cannot run in place");
     automorphism(c, (u64*)out, (const u64*)in, batch, hx::make_table(c, n_q, n_p), g, S(s));
@@ -1097,6 +1110,7 @@ int hx_from_i64(hx_ctx* c, uint64_t* out, const int64_t* v, int batch, int n_q, 
                 void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     const LimbTable lt = hx::make_table(c, n_q, n_p);
     const int th = pt_threads(c);
     const long long blocks = (long long)batch * lt.count * (c->N() / th);
@@ -1110,6 +1124,7 @@ int hx_from_i64(hx_ctx* c, uint64_t* out, const int64_t* v, int batch, int n_q, 
 int hx_reduce_mod_q(hx_ctx* c, uint64_t* data, int batch, int n_q, int n_p, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     hx::EwArgs A{(u64*)data, nullptr, nullptr, c->d_pc, hx::make_table(c, n_q, n_p), c->logn, 0};
     A.instances = (long long)batch * A.lt.count;
     const int th = pt_threads(c);
@@ -1123,6 +1138,7 @@ int hx_reduce_mod_q(hx_ctx* c, uint64_t* data, int batch, int n_q, int n_p, void
 int hx_rescale(hx_ctx* c, uint64_t* out, const uint64_t* in, int batch, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     HX_REQUIRE(n_q >= 2, "rescale: no limb to drop");
     rescale(c, (u64*)out, (const u64*)in, batch, n_q, S(s));
@@ -1132,6 +1148,7 @@ int hx_rescale(hx_ctx* c, uint64_t* out, const uint64_t* in, int batch, int n_q,
 int hx_modup(hx_ctx* c, uint64_t* digits, const uint64_t* c1, int batch, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     modup(c, (u64*)digits, (const u64*)c1, (long long)n_q * c->N(), batch, n_q, S(s));
   });
@@ -1141,6 +1158,7 @@ int hx_ks_inner(hx_ctx* c, uint64_t* u, const uint64_t* digits, const uint64_t* 
                 int n_q, uint64_t g, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element must be odd and < 2N");
     ks_inner(c, (u64*)u, (const u64*)digits, (const u64*)key, batch, n_q, g, S(s));
@@ -1150,6 +1168,7 @@ int hx_ks_inner(hx_ctx* c, uint64_t* u, const uint64_t* digits, const uint64_t* 
 int hx_moddown(hx_ctx* c, uint64_t* out, const uint64_t* u, int polys, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(polys);
     check_nq(c, n_q);
     const long long N = c->N();
     moddown(c, (u64*)out, (long long)n_q * N, (const u64*)u, (long long)(n_q + c->n_special) * N,
@@ -1161,6 +1180,7 @@ int hx_keyswitch(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* k
                  int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     const long long N = c->N();
     const int ext = n_q + c->n_special;
@@ -1176,6 +1196,7 @@ int hx_rotate(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* key,
               int n_q, uint64_t g, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element must be odd and < 2N");
     HX_REQUIRE(out != in, "rotate cannot run in place");
@@ -1192,6 +1213,7 @@ int hx_rotate_hoisted(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
                       const uint64_t* galois, int R, int batch, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     HX_REQUIRE(R >= 1, "R >= 1");
     const long long N = c->N();
@@ -1213,6 +1235,7 @@ int hx_rotate_multi(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t
                     const uint64_t* galois, int batch, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     const long long N = c->N(), ct = 2ll * n_q * N;
     const int ext = n_q + c->n_special;
@@ -1235,6 +1258,8 @@ int hx_rotate_grouped(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
                       const uint64_t* galois, int R, int E, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(R);
+    HX_COUNT(E);
     check_nq(c, n_q);
     HX_REQUIRE(R >= 1 && E >= 1, "R, E >= 1");
     const long long N = c->N(), ct = 2ll * n_q * N;
@@ -1266,6 +1291,7 @@ int hx_tensor(hx_ctx* c, uint64_t* out3, const uint64_t* a, const uint64_t* b, i
               void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     const int th = pt_threads(c);
     hx::tensor_kernel<<<dim3((unsigned)(c->N() / th), (unsigned)n_q, (unsigned)batch), th, 0,
@@ -1278,6 +1304,7 @@ int hx_mul_relin(hx_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b,
                  const uint64_t* rlk, int batch, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     const long long N = c->N(), L = (long long)n_q * N;
     const int ext = n_q + c->n_special;
@@ -1338,6 +1365,7 @@ int hx_sum_strided(hx_ctx* c, uint64_t* out, const uint64_t* in, int terms, long
                    int polys, long long in_poly_stride, long long out_poly_stride, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(polys);
     check_nq(c, n_q);
     HX_REQUIRE(terms >= 1 && polys >= 1, "sum: terms, polys >= 1");
     hx::SumArgs A;
@@ -1358,6 +1386,7 @@ int hx_sum_strided(hx_ctx* c, uint64_t* out, const uint64_t* in, int terms, long
 int hx_sample_uniform(hx_ctx* c, uint64_t* out, int n_c, int n_s, int copies, uint64_t seed, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(copies);
     HX_REQUIRE(n_c >= 0 && n_c <= c->n_chain && n_s >= 0 && n_s <= c->n_special && copies >= 0, "sample_uniform");
     const long long words = (long long)copies * (n_c + n_s) * c->N();
     if (!words) return;
@@ -1370,6 +1399,7 @@ int hx_sample_uniform(hx_ctx* c, uint64_t* out, int n_c, int n_s, int copies, ui
 int hx_sample_cbd(hx_ctx* c, int64_t* e, long long count, uint64_t seed, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(count);
     HX_REQUIRE(count >= 0, "sample_cbd");
     if (!count) return;
     hx::sample_cbd_kernel<<<(unsigned)((count + 255) / 256), 256, 0, S(s)>>>((long long*)e, count, seed);
@@ -1447,6 +1477,7 @@ int hx_decrypt(hx_ctx* c, uint64_t* m, const uint64_t* ct, const uint64_t* s_ful
                int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     const int th = pt_threads(c);
     hx::decrypt_kernel<<<dim3((unsigned)(c->N() / th), (unsigned)n_q, (unsigned)batch), th, 0,
@@ -1460,6 +1491,7 @@ int hx_rotate_host(hx_ctx* c, uint64_t* out_host, const uint64_t* in_host, const
                    int batch, int n_q, uint64_t g, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     const long long ct = 2ll * n_q * c->N();
     pipelined_host(c, batch, {in_host}, {ct}, out_host, ct, S(s),
@@ -1474,6 +1506,7 @@ int hx_mul_relin_host(hx_ctx* c, uint64_t* out_host, const uint64_t* a_host,
                       const uint64_t* b_host, const uint64_t* rlk, int batch, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
+    HX_COUNT(batch);
     check_nq(c, n_q);
     const long long ct = 2ll * n_q * c->N();
     pipelined_host(c, batch, {a_host, b_host}, {ct, ct}, out_host, ct, S(s),

@@ -1,0 +1,131 @@
+"""Edge cases of the device C-ABI (include/hx_b200.h): empty batches are
+no-ops, malformed shapes and Galois elements fail with HX_ERR_INVALID and a
+message (never a silent result or a CUDA launch error), ragged matrices
+(last row block partially filled, rectangular wider than tall) and the
+largest supported BSGS shape at N = 2^12 stay exact, and rotations by
+multiples of the slot count need no key (reference_backend.cpp:106)."""
+import numpy as np
+import pytest
+
+from configs import config2
+
+pytestmark = pytest.mark.gpu
+
+
+def _ctx():
+    import torch  # noqa: F401
+
+    from paper_2512_11135_b200 import Context
+
+    p = config2(12, 24)
+    return p, Context(p["logn"], p["chain"], p["special"], p["alpha"])
+
+
+def _empty(*shape):
+    import torch
+
+    return torch.zeros(shape, dtype=torch.int64, device="cuda")
+
+
+def test_empty_batches_are_noops():
+    p, ctx = _ctx()
+    nq, N = len(p["chain"]), 1 << p["logn"]
+    x = _empty(1, 2, nq, N)
+    y = _empty(1, 2, nq, N)
+    key = _empty(ctx.dnum(nq), 2, nq + len(p["special"]), N)
+    ctx.ntt_fwd(x, 0, nq)
+    ctx.ntt_inv(x, 0, nq)
+    ctx.binop("add", x, x, x, 0, nq)
+    ctx.reduce_mod_q(x, 0, nq)
+    ctx.rotate(y, x, key, 0, nq, 5)
+    ctx.mul_relin(y, x, x, key, 0, nq)
+    import torch
+
+    torch.cuda.synchronize()
+    assert int(x.abs().sum()) == 0 and int(y.abs().sum()) == 0
+
+
+def test_invalid_arguments_fail_loudly():
+    from paper_2512_11135_b200.hx import HxError
+
+    p, ctx = _ctx()
+    nq, N = len(p["chain"]), 1 << p["logn"]
+    x = _empty(1, 2, nq, N)
+    y = _empty(1, 2, nq, N)
+    key = _empty(ctx.dnum(nq), 2, nq + len(p["special"]), N)
+    cases = {
+        "too many limbs": lambda: ctx.ntt_fwd(x, 1, nq + 1),
+        "zero limbs": lambda: ctx.ntt_fwd(x, 1, 0),
+        "negative batch": lambda: ctx.ntt_fwd(x, -1, nq),
+        "even galois": lambda: ctx.rotate(y, x, key, 1, nq, 4),
+        "galois out of range": lambda: ctx.rotate(y, x, key, 1, nq, 2 * N + 1),
+        "in place rotate": lambda: ctx.rotate(x, x, key, 1, nq, 5),
+        "no hoisted rotations": lambda: ctx.rotate_hoisted(y, x, [], [], 1, nq),
+    }
+    silent = []
+    for name, f in cases.items():
+        try:
+            f()
+            silent.append(name)
+        except HxError as e:
+            assert str(e)  # a message, not a bare code
+    assert not silent, f"accepted silently: {silent}"
+
+
+def test_ragged_matrices_and_zero_rotation():
+    from test_gpu_helix import backend
+
+    from paper_2512_11135_b200.helix import BSGS, DIAG, ROW
+
+    p, be = backend("c2s")
+    rng = np.random.default_rng(77)
+    n = be.slots
+    lvl = be.max_level
+    for rows, cols in ((300, 256), (5, 256), (256, 100), (1, 1)):
+        A = rng.normal(0, 0.1, (rows, cols))
+        x = rng.uniform(-1, 1, cols)
+        d = 1 << max(0, (cols - 1).bit_length())
+        for meth in (BSGS, DIAG, ROW):
+            M = be.prepare(meth, A, lvl)
+            be.gen_rotation_keys(M.rotations())
+            v = np.zeros(d)
+            v[:cols] = x
+            ct = be.encrypt(np.tile(v, n // d), lvl)
+            outs, rep = be.matvec(M, ct)
+            if meth == ROW:
+                y = be.decrypt(outs[0])[:rows]
+            else:
+                y = np.concatenate([be.decrypt(o)[:d] for o in outs])[:rows]
+            assert np.abs(y - A @ x).max() < 1e-5, (rows, cols, meth)
+    v = rng.uniform(-1, 1, n)
+    ct = be.encrypt(v)
+    for k in (0, n, -n, 2 * n):  # identity rotations: no key needed
+        assert np.abs(be.decrypt(be.rotate(ct, k)) - v).max() < 1e-5
+
+
+def test_largest_bsgs_shape_at_n4096():
+    """d = 2048 = the slot count at N = 2^12 (n1 = 64, n2 = 32): the widest
+    diagonal count the MAC kernel accepts (n1 <= 64), 90 %-pruned to keep
+    the host encode short."""
+    from test_gpu_helix import backend
+
+    from paper_2512_11135_b200.helix import BSGS
+
+    p, be = backend("c2s")
+    n = be.slots
+    rng = np.random.default_rng(5)
+    d = n
+    A = np.zeros((d, d))
+    live = rng.choice(d, d // 10, replace=False)
+    r = np.arange(d)
+    for i in live:
+        A[r, (r + i) % d] = rng.normal(0, 0.05, d)
+    x = rng.uniform(-1, 1, d)
+    lvl = 4
+    M = be.prepare(BSGS, A, lvl)
+    info = M.info()
+    assert info["n1"] * info["n2"] == d and info["nonzero"] == len(live)
+    be.gen_rotation_keys(M.rotations())
+    ct = be.encrypt(x, lvl)
+    outs, rep = be.matvec(M, ct)
+    assert np.abs(be.decrypt(outs[0]) - A @ x).max() < 1e-4
