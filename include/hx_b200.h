@@ -165,7 +165,10 @@ int hx_sum_strided(hx_ctx* ctx, uint64_t* out, const uint64_t* in, int terms, lo
  * HBM once (L2 for the other tokens) -- config 3 with T tokens per matrix */
 int hx_bsgs_mac_tokens(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, long long inner_tstride,
                        const uint64_t* baby, long long baby_tstride, const uint64_t* diags, int diag_limbs, int n1,
-                       int n2, int n_q, int tokens, void* stream);
+                       int n2, int n_q, int tokens, int diag_jstride, void* stream);
+/* (diag_jstride: diagonals between giant groups j and j + 1; 0 = n1.  A block
+ * with more than 64 baby steps is multiplied in chunks of <= 64 of them, each
+ * chunk a launch with n1 = chunk and diag_jstride = the block's n1.) */
 int hx_bsgs_mac(hx_ctx* ctx, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,
                 int diag_limbs, int n1, int n2, int n_q, void* stream);
 

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(TT) bsgs_mac_kernel(MacArgs A) {
   const u64* dg = A.diags + i * N + t;
   for (int j = 0; j < A.n2; ++j) {
     U128 z0{0, 0}, z1{0, 0};
-    const u64* dj = dg + (long long)j * A.n1 * A.diag_stride;
+    const u64* dj = dg + (long long)j * A.diag_jstride * A.diag_stride;
     int k = 0;
     // 16 independent diagonal loads in flight per thread (the CTA count per SM
     // is bounded by the baby tile in shared memory, so memory-level
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_f64_kernel(MacArgs A,
 #pragma unroll
     for (int kk = 0; kk < KPT; ++kk) d[kk] = dn[kk];
     if (j + 1 < A.n2) {
-      const u64* dj = dg + (long long)(j + 1) * A.n1 * A.diag_stride;
+      const u64* dj = dg + (long long)(j + 1) * A.diag_jstride * A.diag_stride;
 #pragma unroll
       for (int kk = 0; kk < KPT; ++kk) dn[kk] = __ldcs(dj + (long long)kk * A.diag_stride);
     }
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_int_kernel(MacArgs A,
 #pragma unroll
     for (int kk = 0; kk < KPT; ++kk) d[kk] = dn[kk];
     if (j + 1 < A.n2) {
-      const u64* dj = dg + (long long)(j + 1) * A.n1 * A.diag_stride;
+      const u64* dj = dg + (long long)(j + 1) * A.diag_jstride * A.diag_stride;
 #pragma unroll
       for (int kk = 0; kk < KPT; ++kk) dn[kk] = __ldcs(dj + (long long)kk * A.diag_stride);
     }

@@ -1324,7 +1324,7 @@ int hx_mul_relin(hx_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b,
 
 int hx_bsgs_mac_tokens(hx_ctx* c, uint64_t* inner, long long inner_jstride, long long inner_tstride,
                        const uint64_t* baby, long long baby_tstride, const uint64_t* diags, int diag_limbs, int n1,
-                       int n2, int n_q, int tokens, void* s) {
+                       int n2, int n_q, int tokens, int diag_jstride, void* s) {
   return guarded([&] {
     check_ctx(c);
     check_nq(c, n_q);
@@ -1345,6 +1345,8 @@ int hx_bsgs_mac_tokens(hx_ctx* c, uint64_t* inner, long long inner_jstride, long
     A.tokens = tokens;
     A.baby_tstride = baby_tstride;
     A.inner_tstride = inner_tstride;
+    HX_REQUIRE(diag_jstride == 0 || diag_jstride >= n1, "bsgs_mac: diag_jstride < n1");
+    A.diag_jstride = diag_jstride ? diag_jstride : n1;
     const int* lists = c->d_maclimbs + (size_t)n_q * 2 * c->n_chain;
     hx::launch_bsgs_mac(A, c->N(), S(s), lists, c->mac_nf64[n_q], lists + c->n_chain, c->mac_nint[n_q]);
     launched(c, "bsgs_mac_kernel", 2);
@@ -1353,7 +1355,7 @@ int hx_bsgs_mac_tokens(hx_ctx* c, uint64_t* inner, long long inner_jstride, long
 
 int hx_bsgs_mac_ex(hx_ctx* c, uint64_t* inner, long long inner_jstride, const uint64_t* baby,
                    const uint64_t* diags, int diag_limbs, int n1, int n2, int n_q, void* s) {
-  return hx_bsgs_mac_tokens(c, inner, inner_jstride, 0, baby, 0, diags, diag_limbs, n1, n2, n_q, 1, s);
+  return hx_bsgs_mac_tokens(c, inner, inner_jstride, 0, baby, 0, diags, diag_limbs, n1, n2, n_q, 1, 0, s);
 }
 
 int hx_bsgs_mac(hx_ctx* c, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,

@@ -31,6 +31,9 @@ struct MacArgs {
   // diagonal word comes from HBM once and from L2 for the other tokens)
   int tokens;
   long long baby_tstride, inner_tstride;
+  // diagonals between giant groups j and j+1 (n1 for a whole block; larger when
+  // the baby steps of a block are processed in chunks of at most 64)
+  int diag_jstride;
 };
 
 // out = sum_{r < terms} in + r * term_stride, per (poly, limb) of `polys`

@@ -600,6 +600,31 @@ std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphert
   return bsgs_blocks_tokens({baby}, diags, n1, n2, blocks, allow_empty).front();
 }
 
+// inner[off + j jstride + t tstride] = sum_{k < n1} diag[j dj + k] (.) baby_t,k
+// for T tokens at a uniform baby stride.  n1 > 64 (the MAC kernels' limit) is
+// split into chunks of 64 baby steps; chunks >= 1 go to a zeroed copy of the
+// whole inner buffer (inner_polys polys) that is then added into it.
+static void mac_chunked(hx_ctx* ctx, std::uint64_t* inner, std::size_t inner_polys, std::size_t off,
+                        long long jstride, long long tstride, const std::uint64_t* baby, long long btstride,
+                        std::size_t ctw, const std::uint64_t* diags, std::size_t ptw, int nqv, int n1, int n2, int dj,
+                        int T) {
+  constexpr int kMax = 64;
+  std::unique_ptr<DeviceBuffer> tmp;
+  for (int k0 = 0; k0 < n1; k0 += kMax) {
+    const int kc = std::min(kMax, n1 - k0);
+    std::uint64_t* dst = inner;
+    if (k0) {
+      if (!tmp) tmp = std::make_unique<DeviceBuffer>(inner_polys * ptw);
+      cuda_ck(cudaMemsetAsync(tmp->ptr, 0, inner_polys * ptw * 8, nullptr), "memset");
+      dst = tmp->ptr;
+    }
+    ck(hx_bsgs_mac_tokens(ctx, dst + off, jstride, tstride, baby + (std::size_t)k0 * ctw, btstride,
+                          diags + (std::size_t)k0 * ptw, nqv, kc, n2, nqv, T, dj, nullptr),
+       "bsgs_mac");
+    if (k0) ck(hx_add(ctx, inner, inner, dst, (int)inner_polys, nqv, 0, nullptr), "add");
+  }
+}
+
 std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
     const std::vector<std::vector<Ciphertext>>& babies, const std::vector<Plaintext>& diags, int n1, int n2,
     int blocks, bool allow_empty) {
@@ -642,6 +667,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
   const int E = T * blocks;
   const std::size_t jstride = (std::size_t)E * ctw;
   auto inner = dev((std::size_t)n2 * jstride);
+  const std::size_t inner_polys = (std::size_t)n2 * E * 2;
   cuda_ck(cudaMemsetAsync(inner->ptr, 0, inner->words * 8, nullptr), "memset");
   Scale dscale;
   bool have_scale = false;
@@ -674,14 +700,12 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       const long long bstride = T > 1 ? (long long)(baby_ptr[1] - baby_ptr[0]) : 0;
       for (int t = 1; t < T && uniform; ++t) uniform = (long long)(baby_ptr[t] - baby_ptr[t - 1]) == bstride;
       if (uniform) {
-        ck(hx_bsgs_mac_tokens(ctx_, inner->ptr + (std::size_t)b * ctw, (long long)jstride, (long long)(blocks * ctw),
-                              baby_ptr[0], bstride, p0->data(), nqv, n1, n2, nqv, T, nullptr),
-           "bsgs_mac");
+        mac_chunked(ctx_, inner->ptr, inner_polys, (std::size_t)b * ctw, (long long)jstride, (long long)(blocks * ctw),
+                    baby_ptr[0], bstride, ctw, p0->data(), ptw, nqv, n1, n2, n1, T);
       } else {
         for (int t = 0; t < T; ++t)
-          ck(hx_bsgs_mac_ex(ctx_, inner->ptr + ((std::size_t)t * blocks + b) * ctw, (long long)jstride, baby_ptr[t],
-                            p0->data(), nqv, n1, n2, nqv, nullptr),
-             "bsgs_mac");
+          mac_chunked(ctx_, inner->ptr, inner_polys, ((std::size_t)t * blocks + b) * ctw, (long long)jstride, 0,
+                      baby_ptr[t], 0, ctw, p0->data(), ptw, nqv, n1, n2, n1, 1);
       }
       ptmuls = d;
       adds = (std::uint64_t)(n1 - 1) * n2;
@@ -718,17 +742,17 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
                                     cudaMemcpyDeviceToDevice, nullptr), "d2d");
         }
         for (int t = 0; t < T; ++t) {
-          u64* dst = inner->ptr + j * jstride + ((std::size_t)t * blocks + b) * ctw;
+          const std::size_t off = j * jstride + ((std::size_t)t * blocks + b) * ctw;
           if (dense) {
-            ck(hx_bsgs_mac_ex(ctx_, dst, (long long)ctw, baby_ptr[t], q0.data(), nqv, n1, 1, nqv, nullptr),
-               "bsgs_mac");
+            mac_chunked(ctx_, inner->ptr, inner_polys, off, (long long)ctw, 0, baby_ptr[t], 0, ctw, q0.data(), ptw,
+                        nqv, n1, 1, n1, 1);
           } else {  // ... and the matching baby steps of the token
             DeviceBuffer bs(ks.size() * ctw);
             for (std::size_t i = 0; i < ks.size(); ++i)
               cuda_ck(cudaMemcpyAsync(bs.ptr + i * ctw, baby_ptr[t] + ks[i] * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
                                       nullptr), "d2d");
-            ck(hx_bsgs_mac_ex(ctx_, dst, (long long)ctw, bs.ptr, dg->ptr, nqv, (int)ks.size(), 1, nqv, nullptr),
-               "bsgs_mac");
+            mac_chunked(ctx_, inner->ptr, inner_polys, off, (long long)ctw, 0, bs.ptr, 0, ctw, dg->ptr, ptw, nqv,
+                        (int)ks.size(), 1, (int)ks.size(), 1);
           }
         }
         live[b][j] = 1;

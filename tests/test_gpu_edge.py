@@ -129,3 +129,33 @@ def test_largest_bsgs_shape_at_n4096():
     ct = be.encrypt(x, lvl)
     outs, rep = be.matvec(M, ct)
     assert np.abs(be.decrypt(outs[0]) - A @ x).max() < 1e-4
+
+
+def test_bsgs_more_than_64_baby_steps():
+    """d = 8192 at N = 2^14 (BsgsPlan n1 = 128, n2 = 64): the MAC runs in
+    chunks of 64 baby steps (mac_chunked); dense and 90 %-pruned."""
+    from configs import config1
+
+    from paper_2512_11135_b200.helix import BSGS, Backend, params_json
+
+    p = config1(14)
+    be = Backend(params_json(p["logn"], p["chain"], p["special"], p["alpha"], 40), seed=3)
+    d = be.slots
+    rng = np.random.default_rng(8192)
+    A = rng.normal(0, 0.01, (d, d))
+    x = rng.uniform(-1, 1, d)
+    for prune in (False, True):
+        B = A.copy()
+        if prune:
+            r = np.arange(d)
+            for i in rng.choice(d, d - d // 10, replace=False):
+                B[r, (r + i) % d] = 0.0
+        M = be.prepare(BSGS, B, be.max_level)
+        info = M.info()
+        assert info["n1"] == 128 and info["n2"] == 64
+        be.gen_rotation_keys(M.rotations())
+        ct = be.encrypt(x)
+        outs, rep = be.matvec(M, ct)
+        assert np.abs(be.decrypt(outs[0]) - B @ x).max() < 1e-4
+        assert rep["rotations"] == 127 + 63 or prune
+    be.close()
