@@ -133,7 +133,10 @@ class GpuLatticeBackend final : public SlotBackend {
   static const GpuPlaintext& payload(const Plaintext& pt);
   Ciphertext wrap(std::shared_ptr<DeviceBuffer> buf, std::size_t offset, int level,
                   const Scale& scale) const;
-  // device word pointer of the rotation-layout key for amount k (mod n), or null
+  // full [dnum][2][full][N] words of a compressed key (rotation_key /
+  // relin_key_words pointers) into device memory `full` -- for oracles
+  void expand_key(const std::uint64_t* ckey, std::uint64_t* full) const;
+  // device word pointer of the (compressed) rotation-layout key for amount k (mod n), or null
   const std::uint64_t* rotation_key(std::int64_t amount_mod_n) const;
   // secret key s over the full basis (NTT) and the relinearisation key --
   // exported for the parity tests (the oracle recomputes with the same words)

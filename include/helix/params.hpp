@@ -25,6 +25,11 @@ struct CkksParams {
   BackendKind backend = BackendKind::Reference;
   bool mock_bootstrap = true;
   bool insecure_toy = false;
+  // GPU backend: store key-switching keys compressed (b halves only, the
+  // uniform halves regenerated from a seed in the inner product; half the key
+  // memory, slower key switches on B200 -- DESIGN.md 5).  Not part of the
+  // reference's parameter set (an extension key of this implementation).
+  bool compress_keys = false;
   int bootstrap_level = -1;  // L_boot, -1 = L
   int digit_size = 1;        // alpha (hybrid key switching), new
 

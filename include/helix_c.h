@@ -112,6 +112,10 @@ int hxc_matmul_rotations(int d, int64_t* out, int cap);
 const uint64_t* hxc_secret_key_ptr(hxc_backend* b);
 const uint64_t* hxc_relin_key_ptr(hxc_backend* b);
 const uint64_t* hxc_rotation_key_ptr(hxc_backend* b, int64_t k);
+/* the backend stores compressed keys (hx_keygen_*_c): full [dnum][2][n_chain+K][N]
+ * words of a key pointer (hxc_rotation_key_ptr / hxc_relin_key_ptr) into
+ * device memory full_dev (hx_key_words words) */
+int hxc_key_expand(hxc_backend* b, const uint64_t* ckey, uint64_t* full_dev);
 const uint64_t* hxc_matrix_payload_ptr(const hxc_mat* m, int i);
 int hxc_matrix_payload_count(const hxc_mat* m);
 /* host-only: CkksEncoder::encode_coeffs for a CkksParams JSON (no device) */

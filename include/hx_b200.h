@@ -188,6 +188,21 @@ int hx_keygen_ksk(hx_ctx* ctx, uint64_t* key, const uint64_t* s_full, const uint
  * out = tau_{g^-1}(in) limb-wise (out != in) */
 int hx_ksk_to_rotation_layout(hx_ctx* ctx, uint64_t* out, const uint64_t* in, uint64_t galois,
                               void* stream);
+/* ---- compressed keys (seeded key compression) ----
+ * Only the b half of every digit is stored ([dnum_max][n_chain+K][N] words,
+ * hx_ckey_words: half of hx_key_words); the uniform half a is the counter
+ * stream of `seed` (hx_sample_uniform) and is regenerated inside the key
+ * inner product.  The context remembers (seed, layout) per compressed key
+ * pointer: pass the pointer wherever a key is taken (hx_rotate*, hx_keyswitch,
+ * hx_mul_relin, hx_ks_inner); hx_key_release forgets it before it is freed.
+ * hx_key_expand writes the full key (e.g. for an oracle). */
+size_t hx_ckey_words(const hx_ctx* ctx);
+int hx_keygen_ksk_c(hx_ctx* ctx, uint64_t* ckey, const uint64_t* s_full, const uint64_t* sp_full, uint64_t seed,
+                    const int64_t* e, void* stream);
+int hx_keygen_rotation_c(hx_ctx* ctx, uint64_t* ckey, const uint64_t* s_full, uint64_t galois, uint64_t seed,
+                         const int64_t* e, void* stream);
+int hx_key_expand(hx_ctx* ctx, uint64_t* full, const uint64_t* ckey, void* stream);
+int hx_key_release(hx_ctx* ctx, const uint64_t* ckey);
 /* rotation key for tau_g (s' = tau_g(s)) directly in rotation layout */
 int hx_keygen_rotation(hx_ctx* ctx, uint64_t* key, const uint64_t* s_full, uint64_t galois,
                        const uint64_t* a_full, const int64_t* e, void* stream);

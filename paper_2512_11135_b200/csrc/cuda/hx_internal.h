@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "hx_common.cuh"
@@ -29,8 +30,15 @@ struct HxArena {
   cudaEvent_t ev = nullptr;
 };
 
+struct hx_ckey {
+  hx::u64 seed;
+  hx::u32 kg;  // layout permutation of the uniform half: g^-1 (rotation layout) or 1
+};
+
 struct hx_ctx {
   HxArena arena;
+  // compressed keys created by this context (b half only; see hx_keygen_*_c)
+  std::unordered_map<const void*, hx_ckey> ckeys;
   int logn = 0;
   int n_chain = 0, n_special = 0, alpha = 1;
   int device = 0;

@@ -10,6 +10,23 @@
 
 namespace hx {
 
+// counter-based uniform residue: word i of stream `seed`, floor(r q / 2^128)
+// over 128 hashed bits r (bias < 2^-64).  hx_sample_uniform writes these;
+// compressed keys (hx_keygen_*_c) regenerate their uniform half from them.
+__device__ __forceinline__ u64 splitmix64(u64 x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ u64 uniform_word(u64 seed, u64 i, u64 q) {
+  const u64 r0 = splitmix64(seed ^ splitmix64(2 * i));
+  const u64 r1 = splitmix64(seed ^ splitmix64(2 * i + 1));
+  const u64 t = mulhi64(r1, q);                // floor(r1 q / 2^64)
+  const u64 lo = r0 * q, hi = mulhi64(r0, q);  // r0 q
+  return hi + ((lo + t) < lo ? 1 : 0);         // floor((r0 2^64 + r1) q / 2^128)
+}
+
 // ------------------------------------------------------------ elementwise
 enum class EwOp : int { Add = 0, Sub, Neg, Mul, MulAcc, Copy };
 
@@ -247,6 +264,13 @@ struct InnerArgs {
   const u64* c1;
   long long c1_stride;
   int alpha;
+  // compressed keys (hx_keygen_*_c): bit r of cmask set -> keys[r] holds only
+  // the b half, [dnum_max][full][N]; the uniform half is regenerated:
+  // a[d][kl][t] = uniform_word(kseed[r], (d full + kl) N + tau(t)), tau the
+  // key's layout permutation (kg[r] = g^-1 for rotation layout, 1 standard)
+  unsigned long long cmask;
+  u64 kseed[kMaxKeys];
+  u32 kg[kMaxKeys];
 };
 
 // FP64 variant for limbs with q < 2^43: the key words are split once into
@@ -277,12 +301,17 @@ __global__ void __launch_bounds__(256, 2) ks_inner_f64_kernel(InnerArgs A, const
   const u64* key = A.keys[r];
   const int E = A.batch;
   const PrimeConst& P = A.pc[kl];
+  const bool comp = (A.cmask >> r) & 1ull;
+  const u64 ta = (!comp || A.kg[r] <= 1) ? (u64)t : (u64)ntt_auto_index((u32)t, A.kg[r], A.logn);
   double kh[MAXD][2], klo[MAXD][2];
 #pragma unroll
   for (int d = 0; d < MAXD; ++d)
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
-      const u64 kw = d < A.dnum ? __ldg(key + (((long long)d * 2 + c) * full + kl) * N + t) : 0ull;
+      u64 kw = 0;
+      if (d < A.dnum) kw = comp ? (c == 0 ? __ldg(key + ((long long)d * full + kl) * N + t)
+                                           : uniform_word(A.kseed[r], ((u64)d * full + kl) * N + ta, P.q))
+                                : __ldg(key + (((long long)d * 2 + c) * full + kl) * N + t);
       split20_d(kw, kh[d][c], klo[d][c]);
     }
   const int src = (A.g == 1) ? t : (int)ntt_auto_index((u32)t, A.g, A.logn);
@@ -329,12 +358,19 @@ __global__ void __launch_bounds__(256, 2) ks_inner_kernel(InnerArgs A, const int
   const u64* key = A.keys[r];
   const int E = A.batch;
   const PrimeConst& P = A.pc[kl];
+  const bool comp = (A.cmask >> r) & 1ull;
+  const u64 ta = (!comp || A.kg[r] <= 1) ? (u64)t : (u64)ntt_auto_index((u32)t, A.kg[r], A.logn);
   u64 k0[MAXD], k1[MAXD];
 #pragma unroll
   for (int d = 0; d < MAXD; ++d) {
     if (d < A.dnum) {
-      k0[d] = __ldg(key + (((long long)d * 2 + 0) * full + kl) * N + t);
-      k1[d] = __ldg(key + (((long long)d * 2 + 1) * full + kl) * N + t);
+      if (comp) {
+        k0[d] = __ldg(key + ((long long)d * full + kl) * N + t);
+        k1[d] = uniform_word(A.kseed[r], ((u64)d * full + kl) * N + ta, P.q);
+      } else {
+        k0[d] = __ldg(key + (((long long)d * 2 + 0) * full + kl) * N + t);
+        k1[d] = __ldg(key + (((long long)d * 2 + 1) * full + kl) * N + t);
+      }
     }
   }
   const int src = (A.g == 1) ? t : (int)ntt_auto_index((u32)t, A.g, A.logn);
@@ -528,12 +564,6 @@ __global__ void tensor_kernel(u64* out, const u64* a, const u64* b, const PrimeC
 // ------------------------------------------------------------ keys
 // ksk_d over the full basis: b = e - a s + [P]_{q_l} s' on chain limbs of digit d
 // ------------------------------------------------------------ samplers
-__device__ __forceinline__ u64 splitmix64(u64 x) {
-  x += 0x9E3779B97F4A7C15ull;
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  return x ^ (x >> 31);
-}
 
 // out [copies][limbs][N]: uniform mod the limb's prime, floor(r q / 2^128)
 // over 128 random bits r
@@ -542,13 +572,19 @@ __global__ void sample_uniform_kernel(u64* out, const PrimeConst* pc, LimbTable 
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // word index
   const long long limb = i >> logn;
   const u64 q = pc[lt.prime[limb % lt.count]].q;
-  const u64 r0 = splitmix64(seed ^ splitmix64(2 * (u64)i));
-  const u64 r1 = splitmix64(seed ^ splitmix64(2 * (u64)i + 1));
-  const u64 t = mulhi64(r1, q);                    // floor(r1 q / 2^64)
-  const u64 lo = r0 * q, hi = mulhi64(r0, q);      // r0 q
-  const u64 sum = lo + t;
-  out[i] = hi + (sum < lo ? 1 : 0);                // floor((r0 2^64 + r1) q / 2^128)
+  out[i] = uniform_word(seed, (u64)i, q);
   (void)N;
+}
+
+// full key words from a compressed key: out[d][0] = b[d], out[d][1] = a[d]
+__global__ void key_expand_kernel(u64* out, const u64* ckey, const PrimeConst* pc, int full, int logn, u64 seed,
+                                  u32 kg) {
+  const long long N = 1ll << logn;
+  const int d = blockIdx.z, kl = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const u64 ta = kg <= 1 ? (u64)t : (u64)ntt_auto_index((u32)t, kg, logn);
+  out[(((long long)d * 2 + 0) * full + kl) * N + t] = ckey[((long long)d * full + kl) * N + t];
+  out[(((long long)d * 2 + 1) * full + kl) * N + t] = uniform_word(seed, ((u64)d * full + kl) * N + ta, pc[kl].q);
 }
 
 __global__ void sample_cbd_kernel(long long* e, long long count, u64 seed) {

@@ -402,7 +402,18 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
   HX_REQUIRE(!keys.empty() && (int)keys.size() <= hx::kMaxKeys, "ks_inner: 1..64 keys per launch");
   hx::InnerArgs A;
   A.digits = digits;
-  for (std::size_t r = 0; r < keys.size(); ++r) A.keys[r] = keys[r];
+  A.cmask = 0;
+  for (std::size_t r = 0; r < keys.size(); ++r) {
+    A.keys[r] = keys[r];
+    const auto it = c->ckeys.find(keys[r]);
+    A.kseed[r] = 0;
+    A.kg[r] = 1;
+    if (it != c->ckeys.end()) {
+      A.cmask |= 1ull << r;
+      A.kseed[r] = it->second.seed;
+      A.kg[r] = it->second.kg;
+    }
+  }
   A.n_keys = (int)keys.size();
   A.shared = shared ? 1 : 0;
   const long long batch = E;
@@ -1426,6 +1437,67 @@ int hx_keygen_ksk(hx_ctx* c, uint64_t* key, const uint64_t* s_full, const uint64
         (u64*)key, en.p, (const u64*)s_full, (const u64*)sp_full, (const u64*)a_full, c->d_pc,
         c->d_pmodq, c->n_chain, T, c->alpha, c->logn);
     launched(c, "keygen_kernel");
+  });
+}
+
+size_t hx_ckey_words(const hx_ctx* c) {
+  return c ? (size_t)c->dnum(c->n_chain) * c->n_total() * c->N() : 0;
+}
+
+// b half of a full key [dnum][2][full][N] -> compressed [dnum][full][N]
+static void take_b(hx_ctx* c, u64* ckey, const u64* full, cudaStream_t s) {
+  const long long w = (long long)c->n_total() * c->N();
+  copy2d(ckey, w, full, 2 * w, w, c->dnum(c->n_chain), s);
+}
+
+int hx_keygen_ksk_c(hx_ctx* c, uint64_t* ckey, const uint64_t* s_full, const uint64_t* sp_full, uint64_t seed,
+                    const int64_t* e, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    const int dn = c->dnum(c->n_chain);
+    DBuf a((long long)dn * c->n_total() * c->N(), S(s), c), full((long long)hx_key_words(c), S(s), c);
+    int rc = hx_sample_uniform(c, (uint64_t*)a.p, c->n_chain, c->n_special, dn, seed, s);
+    if (rc == HX_OK) rc = hx_keygen_ksk(c, (uint64_t*)full.p, s_full, sp_full, (const uint64_t*)a.p, e, s);
+    if (rc != HX_OK) throw HxError(rc, g_last_error);
+    take_b(c, (u64*)ckey, full.p, S(s));
+    c->ckeys[ckey] = hx_ckey{seed, 1u};
+  });
+}
+
+int hx_keygen_rotation_c(hx_ctx* c, uint64_t* ckey, const uint64_t* s_full, uint64_t g, uint64_t seed,
+                         const int64_t* e, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element must be odd and < 2N");
+    const int dn = c->dnum(c->n_chain);
+    DBuf a((long long)dn * c->n_total() * c->N(), S(s), c), full((long long)hx_key_words(c), S(s), c);
+    int rc = hx_sample_uniform(c, (uint64_t*)a.p, c->n_chain, c->n_special, dn, seed, s);
+    if (rc == HX_OK) rc = hx_keygen_rotation(c, (uint64_t*)full.p, s_full, g, (const uint64_t*)a.p, e, s);
+    if (rc != HX_OK) throw HxError(rc, g_last_error);
+    // rotation layout: full = tau_{g^-1}(standard), its uniform half is the
+    // seed's stream read at ntt_auto_index(t, g^-1)
+    take_b(c, (u64*)ckey, full.p, S(s));
+    c->ckeys[ckey] = hx_ckey{seed, (hx::u32)galois_inverse(g, 2 * (u64)c->N())};
+  });
+}
+
+int hx_key_expand(hx_ctx* c, uint64_t* full, const uint64_t* ckey, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    const auto it = c->ckeys.find(ckey);
+    HX_REQUIRE(it != c->ckeys.end(), "hx_key_expand: not a compressed key of this context");
+    const int th = pt_threads(c);
+    hx::key_expand_kernel<<<dim3((unsigned)(c->N() / th), (unsigned)c->n_total(), (unsigned)c->dnum(c->n_chain)), th, 0,
+                            S(s)>>>((u64*)full, (const u64*)ckey, c->d_pc, c->n_total(), c->logn, it->second.seed,
+                                    it->second.kg);
+    launched(c, "key_expand_kernel");
+  });
+}
+
+int hx_key_release(hx_ctx* c, const uint64_t* ckey) {
+  return guarded([&] {
+    check_ctx(c);
+    c->ckeys.erase(ckey);
   });
 }
 

@@ -111,7 +111,7 @@ GpuLatticeBackend::~GpuLatticeBackend() {
   s_full_.reset();
   cudaStreamSynchronize(nullptr);
   hx_encoder_destroy(henc_);
-  hx_ctx_destroy(ctx_);
+  hx_ctx_destroy(ctx_);  // forgets the compressed keys with the context
 }
 
 void GpuLatticeBackend::sample_uniform(std::vector<u64>& out, int lc, int ls, int copies) {
@@ -145,21 +145,46 @@ void GpuLatticeBackend::sample_error(std::vector<std::int64_t>& out, int copies)
 
 std::shared_ptr<DeviceBuffer> GpuLatticeBackend::make_key(const std::shared_ptr<DeviceBuffer>& sp,
                                                           std::uint64_t g) {
-  const int nc = (int)params_.moduli.size(), K = (int)params_.special_primes.size();
+  // Key material from two seeds of the backend's stream: the uniform halves
+  // are the counter stream of the first (hx_sample_uniform), the CBD errors of
+  // the second.  compress_keys: store only the b halves and
+  // regenerate the uniform halves inside the key inner product (half the key
+  // bytes; the same key words either way).
+  const int nc = (int)params_.moduli.size();
   const int dn = hx_ctx_dnum(ctx_, nc);
-  // key material sampled on the device from two seeds of the backend's stream
   const std::size_t N = params_.ring_degree;
-  DeviceBuffer da((std::size_t)dn * (nc + K) * N), de((std::size_t)dn * N);
-  ck(hx_sample_uniform(ctx_, da.ptr, nc, K, dn, next_u64(), nullptr), "sample_uniform");
+  DeviceBuffer de((std::size_t)dn * N);
+  const std::uint64_t seed = next_u64();
   ck(hx_sample_cbd(ctx_, (int64_t*)de.ptr, (long long)dn * N, next_u64(), nullptr), "sample_cbd");
-  auto key = dev(hx_key_words(ctx_));
-  if (g == 0)
-    ck(hx_keygen_ksk(ctx_, key->ptr, s_full_->ptr, sp->ptr, da.ptr, (const int64_t*)de.ptr, nullptr), "keygen");
-  else
-    ck(hx_keygen_rotation(ctx_, key->ptr, s_full_->ptr, g, da.ptr, (const int64_t*)de.ptr, nullptr),
-       "keygen_rotation");
+  std::shared_ptr<DeviceBuffer> key;
+  if (params_.compress_keys) {
+    key = dev(hx_ckey_words(ctx_));
+    if (g == 0)
+      ck(hx_keygen_ksk_c(ctx_, key->ptr, s_full_->ptr, sp->ptr, seed, (const int64_t*)de.ptr, nullptr), "keygen");
+    else
+      ck(hx_keygen_rotation_c(ctx_, key->ptr, s_full_->ptr, g, seed, (const int64_t*)de.ptr, nullptr),
+         "keygen_rotation");
+  } else {  // full keys: the same words, the uniform halves materialised
+    const int K = (int)params_.special_primes.size();
+    DeviceBuffer da((std::size_t)dn * (nc + K) * N);
+    ck(hx_sample_uniform(ctx_, da.ptr, nc, K, dn, seed, nullptr), "sample_uniform");
+    key = dev(hx_key_words(ctx_));
+    if (g == 0)
+      ck(hx_keygen_ksk(ctx_, key->ptr, s_full_->ptr, sp->ptr, da.ptr, (const int64_t*)de.ptr, nullptr), "keygen");
+    else
+      ck(hx_keygen_rotation(ctx_, key->ptr, s_full_->ptr, g, da.ptr, (const int64_t*)de.ptr, nullptr),
+         "keygen_rotation");
+  }
   cuda_ck(cudaStreamSynchronize(nullptr), "sync");  // da / de die here
   return key;
+}
+
+void GpuLatticeBackend::expand_key(const std::uint64_t* key, std::uint64_t* full) const {
+  if (params_.compress_keys)
+    ck(hx_key_expand(ctx_, full, key, nullptr), "key_expand");
+  else
+    cuda_ck(cudaMemcpyAsync(full, key, hx_key_words(ctx_) * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
+  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
 }
 
 std::uint64_t GpuLatticeBackend::galois(std::int64_t r) const {

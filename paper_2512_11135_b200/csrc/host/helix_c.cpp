@@ -265,6 +265,13 @@ const uint64_t* hxc_relin_key_ptr(hxc_backend* b) { return b->b->relin_key_words
 const uint64_t* hxc_rotation_key_ptr(hxc_backend* b, int64_t k) {
   return b->b->rotation_key(detail::reduce_amount(k, (std::int64_t)b->b->slots()));
 }
+int hxc_key_expand(hxc_backend* b, const uint64_t* ckey, uint64_t* full_dev) {
+  return guard(-1, [&] {
+    b->b->expand_key(ckey, full_dev);
+    return 0;
+  });
+}
+
 const uint64_t* hxc_matrix_payload_ptr(const hxc_mat* m, int i) {
   if (i < 0 || i >= (int)m->m.pts.size() || !m->m.pts[i].payload) return nullptr;
   return GpuLatticeBackend::payload(m->m.pts[i]).data();

@@ -73,6 +73,7 @@ def lib():
         "hxc_secret_key_ptr": (v, [v]),
         "hxc_relin_key_ptr": (v, [v]),
         "hxc_rotation_key_ptr": (v, [v, i64]),
+        "hxc_key_expand": (i32, [v, v, v]),
         "hxc_matrix_payload_ptr": (v, [v, i32]),
         "hxc_matrix_payload_count": (i32, [v]),
         "hxc_encode_coeffs": (i32, [C.c_char_p, f64p, i32, i32, C.c_double, C.POINTER(C.c_int64)]),
@@ -325,4 +326,10 @@ class Backend:
         return self.L.hxc_relin_key_ptr(self.h)
 
     def rotation_key_ptr(self, k):
+        """device pointer of the compressed rotation key (b halves only)"""
         return self.L.hxc_rotation_key_ptr(self.h, k)
+
+    def expand_key(self, ckey_ptr, full_dev_ptr):
+        """full [dnum][2][n_chain+K][N] key words of a compressed key into device memory"""
+        if self.L.hxc_key_expand(self.h, ckey_ptr, full_dev_ptr) != 0:
+            raise _err()

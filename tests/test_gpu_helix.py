@@ -22,11 +22,14 @@ _cache = {}
 
 
 def backend(name):
+    """c1 / c2s; a "+ck" suffix selects compressed key storage (compress_keys)"""
     from paper_2512_11135_b200.helix import Backend, params_json
 
     if name not in _cache:
-        p = config1(13) if name == "c1" else config2(12, 24)
-        be = Backend(params_json(p["logn"], p["chain"], p["special"], p["alpha"], 40), seed=7)
+        base = name.split("+")[0]
+        p = config1(13) if base == "c1" else config2(12, 24)
+        extra = {"compress_keys": True} if name.endswith("+ck") else {}
+        be = Backend(params_json(p["logn"], p["chain"], p["special"], p["alpha"], 40, **extra), seed=7)
         _cache[name] = (p, be)
     return _cache[name]
 
@@ -109,12 +112,14 @@ def test_config1_matvec_64x64(method):
     assert abs(rep["output_scale_log2"] - 40.0) < 1e-12
 
 
-def test_bsgs_matvec_bit_exact_vs_oracle():
+@pytest.mark.parametrize("keys", ["full", "compressed"])
+def test_bsgs_matvec_bit_exact_vs_oracle(keys):
     """The fused BSGS pipeline (hoisted baby steps, streaming MAC, batched giant
-    rotations, rescale) reproduces the oracle's ciphertext word for word."""
+    rotations, rescale) reproduces the oracle's ciphertext word for word, with
+    full and with compressed (seeded) key storage."""
     from paper_2512_11135_b200.helix import BSGS
 
-    p, be = backend("c1")
+    p, be = backend("c1" if keys == "full" else "c1+ck")
     n, N, nq, K = be.slots, 1 << p["logn"], 3, 1
     orc = Oracle(p["logn"], p["chain"], p["special"], 1)
     rng = np.random.default_rng(5)
@@ -132,8 +137,12 @@ def test_bsgs_matvec_bit_exact_vs_oracle():
     kw = orc.dnum(nq) * 2 * (nq + K) * N
 
     def std_key(k):
+        import torch
+
         g = galois_elt(k, N)
-        rot = d2h(be.rotation_key_ptr(k), kw).reshape(-1, N)
+        full = torch.empty(kw, dtype=torch.int64, device="cuda")
+        be.expand_key(be.rotation_key_ptr(k), full.data_ptr())  # the backend stores compressed keys
+        rot = d2h(full.data_ptr(), kw).reshape(-1, N)
         # rotation layout = tau_{g^-1}(standard)  =>  standard = tau_g(rotation layout)
         return np.ascontiguousarray(orc.automorphism_ntt(rot, rot.shape[0], 0, g).reshape(orc.dnum(nq), 2, nq + K, N))
 

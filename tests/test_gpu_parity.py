@@ -430,3 +430,48 @@ def test_device_samplers():
     out2 = empty(2, nq + K, N)
     ctx.sample_uniform(out2, nq, K, 2, 1235)
     assert not np.array_equal(host(out2), host(out))
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+def test_compressed_keys(cfg):
+    """SURVEY 8(f)-2 seeded key compression: a compressed key (b halves only,
+    the uniform halves regenerated from the seed inside the inner product)
+    expands to exactly the full key made from hx_sample_uniform(seed), and a
+    rotation / key switch with it gives the same words as with the full key."""
+    p, ctx, orc = env(cfg)
+    import torch
+
+    from paper_2512_11135_b200.hx import lib
+
+    nq, K, N = len(p["chain"]), len(p["special"]), 1 << p["logn"]
+    rng = np.random.default_rng(91)
+    s_full = dev(secret(p, orc, rng))
+    dn = orc.dnum(len(p["chain"]))
+    e = dev(np.ascontiguousarray(np.stack([gaussian(rng, N) for _ in range(dn)]).astype(np.int64)))
+    L = lib()
+    import ctypes as C
+
+    L.hx_ckey_words.restype = C.c_size_t
+    L.hx_ckey_words.argtypes = [C.c_void_p]
+    for fn in ("hx_keygen_rotation_c",):
+        getattr(L, fn).argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]
+    L.hx_key_expand.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.hx_key_release.argtypes = [C.c_void_p, C.c_void_p]
+    seed, g = 0x1234ABCD, galois_elt(3, N)
+    ck = torch.empty(int(L.hx_ckey_words(ctx.h)), dtype=torch.int64, device="cuda")
+    assert L.hx_keygen_rotation_c(ctx.h, ck.data_ptr(), s_full.data_ptr(), g, seed, e.data_ptr(), None) == 0
+    full_c = torch.empty(ctx.key_words(), dtype=torch.int64, device="cuda")
+    assert L.hx_key_expand(ctx.h, full_c.data_ptr(), ck.data_ptr(), None) == 0
+    # the same key from explicit uniform words of the same seed
+    a = empty(dn, nq + K, N)
+    ctx.sample_uniform(a, nq, K, dn, seed)
+    full = torch.empty(ctx.key_words(), dtype=torch.int64, device="cuda")
+    ctx.keygen_rotation(full, s_full, g, a, e)
+    assert np.array_equal(host(full_c), host(full))
+    # rotations with the compressed and the full key agree word for word
+    ct = dev(uniform_limbs(rng, p["chain"], N, (2, 2)))
+    o1, o2 = empty(2, 2, nq, N), empty(2, 2, nq, N)
+    ctx.rotate(o1, ct, ck, 2, nq, g)
+    ctx.rotate(o2, ct, full, 2, nq, g)
+    assert np.array_equal(host(o1), host(o2))
+    assert L.hx_key_release(ctx.h, ck.data_ptr()) == 0
