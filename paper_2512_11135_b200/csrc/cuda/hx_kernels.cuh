@@ -347,6 +347,67 @@ __global__ void __launch_bounds__(256, 2) ks_inner_f64_kernel(InnerArgs A, const
   }
 }
 
+// One element per block row (E <= 2, e.g. BSGS giant steps of a single
+// ciphertext): no key reuse to amortise, so nothing is held across elements --
+// the digit and key words of a (limb, coefficient) are all loaded up front
+// (3 dnum loads in flight per thread) and consumed at once, with the register
+// budget of 3 CTAs / SM instead of 2.
+template <int MAXD>
+__global__ void __launch_bounds__(256, 3) ks_inner_f64_one_kernel(InnerArgs A, const int* limbs) {
+  const int N = 1 << A.logn;
+  const int ext = A.n_q + A.n_special, full = A.n_chain + A.n_special;
+  const int j = limbs[blockIdx.y];
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int kl = j < A.n_q ? j : A.n_chain + (j - A.n_q);
+  const int E = A.batch;
+  const int r = blockIdx.z / E, b = blockIdx.z % E;
+  const u64* key = A.keys[r];
+  const PrimeConst& P = A.pc[kl];
+  const bool comp = (A.cmask >> r) & 1ull;
+  const u64 ta = (!comp || A.kg[r] <= 1) ? (u64)t : (u64)ntt_auto_index((u32)t, A.kg[r], A.logn);
+  const int src = (A.g == 1) ? t : (int)ntt_auto_index((u32)t, A.g, A.logn);
+  const long long dstride = (long long)A.dnum * ext * N;
+  const long long e = (A.shared ? 0 : (long long)r * E) + b;
+  const int down = (A.c1 && j < A.n_q) ? j / A.alpha : -1;
+  const u64* Db = A.digits + e * dstride + (long long)j * N + src;
+  const u64* Cb = down >= 0 ? A.c1 + e * A.c1_stride + (long long)j * N + src : nullptr;
+  u64 v[MAXD], k0[MAXD], k1[MAXD];
+#pragma unroll
+  for (int d = 0; d < MAXD; ++d) {
+    if (d < A.dnum) {
+      v[d] = __ldcs(d == down ? Cb : Db + (long long)d * ext * N);
+      if (comp) {
+        k0[d] = __ldg(key + ((long long)d * full + kl) * N + t);
+        k1[d] = uniform_word(A.kseed[r], ((u64)d * full + kl) * N + ta, P.q);
+      } else {
+        k0[d] = __ldg(key + (((long long)d * 2 + 0) * full + kl) * N + t);
+        k1[d] = __ldg(key + (((long long)d * 2 + 1) * full + kl) * N + t);
+      }
+    } else {
+      v[d] = k0[d] = k1[d] = 0;
+    }
+  }
+  double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+  for (int d = 0; d < MAXD; ++d) {
+    double xh, xl, ah, al, bh, bl;
+    split20_d(v[d], xh, xl);
+    split20_d(k0[d], ah, al);
+    split20_d(k1[d], bh, bl);
+    s[0][0] = __fma_rn(xh, ah, s[0][0]);
+    s[0][1] = __fma_rn(xh, al, s[0][1]);
+    s[0][1] = __fma_rn(xl, ah, s[0][1]);
+    s[0][2] = __fma_rn(xl, al, s[0][2]);
+    s[1][0] = __fma_rn(xh, bh, s[1][0]);
+    s[1][1] = __fma_rn(xh, bl, s[1][1]);
+    s[1][1] = __fma_rn(xl, bh, s[1][1]);
+    s[1][2] = __fma_rn(xl, bl, s[1][2]);
+  }
+  u64* ub = A.u + ((long long)r * E + b) * 2 * ext * N + (long long)j * N + t;
+  ub[0] = combine_split(s[0], P);
+  ub[(long long)ext * N] = combine_split(s[1], P);
+}
+
 template <int MAXD>
 __global__ void __launch_bounds__(256, 2) ks_inner_kernel(InnerArgs A, const int* limbs) {
   const int N = 1 << A.logn;

@@ -440,7 +440,15 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
   const int nf = A.dnum <= 8 ? c->ks_nf64[n_q] : 0;
   const int ni = A.dnum <= 8 ? c->ks_nint[n_q] : n_q + c->n_special;
   const int* il = A.dnum <= 8 ? lists + c->n_total() : nullptr;
-  if (nf > 0) {
+  static const bool one_off = getenv("HX_KS_ONE") && atoi(getenv("HX_KS_ONE")) == 0;
+  if (nf > 0 && E <= 2 && !one_off) {  // no key reuse across elements: one element per block row
+    dim3 grid((unsigned)(c->N() / th), (unsigned)nf, (unsigned)(A.n_keys * E));
+    if (A.dnum <= 4)
+      hx::ks_inner_f64_one_kernel<4><<<grid, th, 0, s>>>(A, lists);
+    else
+      hx::ks_inner_f64_one_kernel<8><<<grid, th, 0, s>>>(A, lists);
+    launched(c, "ks_inner_f64_one_kernel");
+  } else if (nf > 0) {
     dim3 grid((unsigned)(c->N() / th), (unsigned)nf, gz);
     if (A.dnum <= 4)
       hx::ks_inner_f64_kernel<4><<<grid, th, 0, s>>>(A, lists);
