@@ -51,6 +51,10 @@ struct ModUpColArgs {
   // icnt[d] integer-class targets (conversion only, coefficient domain out)
   int toff[kMaxDigits], tcnt[kMaxDigits], icnt[kMaxDigits];
   int alpha, n_q, n_chain, ext, dnum, logn;
+  // target split: blockIdx.z = element * tsplit + part; part p converts the
+  // p-th share of the digit's target list (small batches still fill the GPU;
+  // each part re-reads the alpha source tiles, from L2)
+  int tsplit;
 };
 
 // bconv of one tile word (sources at src[i * stride]) into the working
@@ -174,12 +178,15 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
   u64* src = dyn_smem + TILE;    // [alpha][TILE] x_i of the tile
   const int t = threadIdx.x;
   const int tile = blockIdx.x, d = blockIdx.y;
-  const long long b = blockIdx.z;
+  const long long b = blockIdx.z / A.tsplit;
+  const int part = blockIdx.z % A.tsplit;
   const int logn = A.logn;
   const long long N = 1ll << logn;
   const int lo = d * A.alpha, cnt = min(A.alpha, A.n_q - lo);
-  const int nt = A.tcnt[d], ni = A.icnt[d];
-  if (nt + ni == 0) return;
+  const int nt_all = A.tcnt[d], ni_all = A.icnt[d], tot = nt_all + ni_all;
+  // this part's slice [k_lo, k_hi) of the (FP64 targets, integer targets) list
+  const int k_lo = (int)((long long)tot * part / A.tsplit), k_hi = (int)((long long)tot * (part + 1) / A.tsplit);
+  if (k_lo >= k_hi) return;
 
   // ---- sources: x_i = [a_i Qhat_i^-1]_{q_i} (canonical); FP64-class sources
   // stored as double bits, the wide ones as integers
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
   const BconvC* bcd = A.bc + A.bc_off[d];
   u64* dout = A.out + (b * A.dnum + d) * (long long)A.ext * N;
 #pragma unroll 1
-  for (int k = 0; k < nt; ++k) {
+  for (int k = k_lo; k < min(k_hi, nt_all); ++k) {
     const int j = tl[k];
     const int pj = j < A.n_q ? j : A.n_chain + (j - A.n_q);
     const PrimeConst P = A.pc[pj];
@@ -239,7 +246,7 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
       modup_target<S, OB, true, MAXA, 2>(src, sm, cnt, sf64, C, P, base, tile, logn);
   }
 #pragma unroll 1
-  for (int k = nt; k < nt + ni; ++k) {
+  for (int k = max(k_lo, nt_all); k < k_hi; ++k) {
     const int j = tl[k];
     const int pj = j < A.n_q ? j : A.n_chain + (j - A.n_q);
     const PrimeConst& P = A.pc[pj];

@@ -251,8 +251,14 @@ void launch_modup_col_t(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, c
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * TILE * (1 + MAXA));
     configured = true;
   }
-  dim3 grid((unsigned)(c->N() / TILE), (unsigned)A.dnum, (unsigned)batch);
-  kern<<<grid, TILE / 16, hx::modup_col_smem_bytes(S, OB, c->alpha), s>>>(A);
+  // enough CTAs for ~3 waves of resident CTAs even for one ciphertext
+  hx::ModUpColArgs B = A;
+  const long long base = (c->N() / TILE) * (long long)A.dnum * batch;
+  int maxt = 1;
+  for (int d = 0; d < A.dnum; ++d) maxt = std::max(maxt, A.tcnt[d] + A.icnt[d]);
+  B.tsplit = (int)std::max(1ll, std::min<long long>(maxt, (148ll * 3 * 3 + base - 1) / base));
+  dim3 grid((unsigned)(c->N() / TILE), (unsigned)A.dnum, (unsigned)(batch * B.tsplit));
+  kern<<<grid, TILE / 16, hx::modup_col_smem_bytes(S, OB, c->alpha), s>>>(B);
   launched(c, "modup_col_kernel");
 }
 
