@@ -69,6 +69,7 @@ struct hx_ctx {
   // ModDown constants
   hx::SC* d_phinv = nullptr;   // [K]
   hx::SC* d_pconv = nullptr;   // [K][n_chain]
+  double* d_pconvf = nullptr;  // [K][n_chain][4]: FP64 form (w, w/q, [2^30 w]_q, /q)
   hx::u64* d_pmodq = nullptr;  // [n_chain]
   hx::SC* d_pinv = nullptr;    // [n_chain]
   // Rescale constants: [l][i] for i < l

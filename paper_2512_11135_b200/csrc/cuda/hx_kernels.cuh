@@ -482,6 +482,7 @@ struct ModDownArgs {
   const PrimeConst* pc;
   const SC* phinv;   // [K]
   const SC* pconv;   // [K][n_chain]  ([P/p_k]_{q_i})
+  const double* pconvf;  // [K][n_chain][4] FP64 form for q_i < 2^47 targets
   const u64* pmodq;  // [n_chain]     ([P]_{q_i})
   int n_q, n_chain, n_special, logn;
 };
@@ -503,8 +504,33 @@ __global__ void moddown_bconv_kernel(ModDownArgs A) {
     }
   }
   u64* cb = A.conv + b * (long long)A.n_q * N;
+  // FP64 pipe for the q_i < 2^47 targets: x_k (< 2^60) as two exact 30-bit
+  // halves, v = sum_k xh_k [2^30 w_k]_q + xl_k w_k - nneg [P]_q, all exact
+  double xh[MAXK], xl[MAXK];
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k) {
+    xh[k] = xl[k] = 0.0;
+    if (k < A.n_special) {
+      xh[k] = __dsub_rn(__longlong_as_double((long long)((x[k] >> 30) | 0x4330000000000000ull)), kTwo52);
+      xl[k] = __dsub_rn(__longlong_as_double((long long)((x[k] & 0x3FFFFFFFull) | 0x4330000000000000ull)), kTwo52);
+    }
+  }
   for (int i = 0; i < A.n_q; ++i) {
     const PrimeConst& P = A.pc[i];
+    if (P.f64) {
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < MAXK; ++k) {
+        if (k < A.n_special) {
+          const double* w = A.pconvf + ((long long)k * A.n_chain + i) * 4;
+          acc = __dadd_rn(acc, mulmod_f64(xh[k], w[2], w[3], P.qd));
+          acc = __dadd_rn(acc, mulmod_f64(xl[k], w[0], w[1], P.qd));
+        }
+      }
+      acc = __fma_rn(-(double)nneg, __longlong_as_double((long long)u64_to_f64bits(A.pmodq[i])), acc);
+      cb[(long long)i * N + t] = f64bits_to_residue((u64)__double_as_longlong(acc), P.qd, P.qinv_d);
+      continue;
+    }
     u64 v = 0;
 #pragma unroll
     for (int k = 0; k < MAXK; ++k) {

@@ -509,6 +509,7 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
   M.pc = c->d_pc;
   M.phinv = c->d_phinv;
   M.pconv = c->d_pconv;
+  M.pconvf = c->d_pconvf;
   M.pmodq = c->d_pmodq;
   M.n_q = n_q;
   M.n_chain = c->n_chain;
@@ -957,6 +958,21 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
     c->d_phinv = upload(phinv);
     c->d_pconv = upload(pconv);
     c->d_pmodq = upload(pmodq);
+    // FP64 form of the P -> Q conversion constants: [k][i] -> (w, w/q, w30, w30/q)
+    {
+      std::vector<double> pf((size_t)n_special * n_chain * 4);
+      for (int k = 0; k < n_special; ++k)
+        for (int i = 0; i < n_chain; ++i) {
+          const u64 q = c->primes[i], w = pconv[(size_t)k * n_chain + i].w;
+          const u64 w30 = hmul(w, (1ull << 30) % q, q);
+          double* e = pf.data() + ((size_t)k * n_chain + i) * 4;
+          e[0] = (double)w;
+          e[1] = (double)w / (double)q;
+          e[2] = (double)w30;
+          e[3] = (double)w30 / (double)q;
+        }
+      c->d_pconvf = upload(pf);
+    }
     c->d_pinv = upload(pinv);
     // Rescale constants
     std::vector<SC> qlinv((size_t)n_chain * n_chain, SC{0, 0});
@@ -1006,6 +1022,7 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
 void hx_ctx_destroy(hx_ctx* c) {
   if (!c) return;
   for (void* p : {(void*)c->d_pc, (void*)c->d_tw, (void*)c->d_twf, (void*)c->d_modup, (void*)c->d_phinv,
+                  (void*)c->d_pconvf,
                   (void*)c->d_pconv, (void*)c->d_pmodq, (void*)c->d_pinv, (void*)c->d_qlinv,
                   (void*)c->d_qlmod, (void*)c->d_maclimbs, (void*)c->d_kslimbs, (void*)c->d_bconv,
                   (void*)c->d_tlist})
