@@ -94,4 +94,19 @@ std::vector<std::int64_t> diag_rotations(int d);
 std::vector<std::int64_t> row_rotations(const PackedMatrix& M);
 std::vector<std::int64_t> matmul_rotations(int d, std::size_t slots);
 
+// polyeval: slot-wise p(x) = sum_i c_i x^i (Power) or
+// sum_i c_i T_i(y), y = (2x - (a + b)) / (b - a) (Chebyshev on [a, b]).
+// Depth-optimal baby-step / giant-step split p = lo + X_h hi, h = 2^(m-1),
+// X_h = x^h (Power) or T_h(y) (Chebyshev, division by T_h via
+// T_h T_j = (T_(h+j) + T_|h-j|) / 2).  Every coefficient multiplication is a
+// plaintext product whose encoding scale is chosen so that each partial
+// result lands on an exact target scale: the output scale is exactly Delta.
+// Levels consumed: ceil(log2(#coeffs)) (min 1), +1 for the Chebyshev domain
+// map.  LevelUnderflowError when the input level is too low.
+enum class PolyBasis { Power, Chebyshev };
+Ciphertext polyeval(SlotOps& ops, const Ciphertext& x, const std::vector<double>& coeffs, PolyBasis basis,
+                    double a = -1.0, double b = 1.0, KernelReport* report = nullptr);
+// levels polyeval consumes for `n_coeffs` coefficients
+int polyeval_depth(std::size_t n_coeffs, PolyBasis basis);
+
 }  // namespace helix

@@ -103,6 +103,10 @@ hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_
 /* rotation count a dense rows x cols matvec records at `slots` slots (counters
  * only, no device work; helix::predicted_rotations; SPEC criterion 4) */
 long long hxc_predicted_rotations(int method, int rows, int cols, int64_t slots);
+/* polyeval: n coefficients, power basis (chebyshev = 0) or
+ * Chebyshev on [lo, hi]; output scale exactly Delta (helix::polyeval) */
+hxc_ct* hxc_polyeval(hxc_backend* b, const hxc_ct* x, const double* coeffs, int n, int chebyshev, double lo,
+                     double hi, hxc_report* rep);
 int hxc_matmul_rotations(int d, int64_t* out, int cap);
 
 /* ---- raw device words, for the bit-exact parity tests ----

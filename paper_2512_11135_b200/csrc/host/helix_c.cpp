@@ -254,6 +254,17 @@ long long hxc_predicted_rotations(int method, int rows, int cols, int64_t slots)
   });
 }
 
+hxc_ct* hxc_polyeval(hxc_backend* b, const hxc_ct* x, const double* coeffs, int n, int chebyshev, double lo,
+                     double hi, hxc_report* rep) {
+  return guard<hxc_ct*>(nullptr, [&] {
+    KernelReport k;
+    auto c = polyeval(*b->b, x->c, std::vector<double>(coeffs, coeffs + n),
+                      chebyshev ? PolyBasis::Chebyshev : PolyBasis::Power, lo, hi, &k);
+    fill(rep, k);
+    return wrap(c);
+  });
+}
+
 int hxc_matmul_rotations(int d, int64_t* out, int cap) {
   const auto r = matmul_rotations(d, 0);
   for (int i = 0; i < (int)r.size() && i < cap; ++i) out[i] = r[i];

@@ -377,6 +377,93 @@ std::int64_t predicted_rotations(Layout layout, int rows, int cols, std::size_t 
   }
 }
 
+// ------------------------------------------------------------------- polyeval
+int polyeval_depth(std::size_t n, PolyBasis basis) {
+  int m = 0;
+  while ((std::size_t(1) << m) < n) ++m;
+  return std::max(1, m) + (basis == PolyBasis::Chebyshev ? 1 : 0);
+}
+
+namespace {
+struct PolyCtx {
+  SlotOps& ops;
+  PolyBasis basis;
+  Ciphertext x;                      // the variable (y for Chebyshev), level L0
+  std::vector<Ciphertext> pw;        // pw[k] = X_{2^k}
+  std::vector<double> constv(double c) const { return std::vector<double>(ops.slots(), c); }
+
+  // X_{2^k}: x^(2^k) by squaring, or T_(2^k) = 2 T_(2^(k-1))^2 - 1
+  const Ciphertext& power(int k) {
+    while ((int)pw.size() <= k) {
+      const Ciphertext& p = pw.back();
+      Ciphertext sq = ops.rescale(ops.mul(p, p));
+      if (basis == PolyBasis::Chebyshev) {
+        sq = ops.add(sq, sq);
+        sq = ops.add_plain(sq, ops.encode(constv(-1.0), sq.level, sq.scale));
+      }
+      pw.push_back(sq);
+    }
+    return pw[k];
+  }
+
+  // c[0..n) evaluated to (level, scale) exactly; level <= L0 - depth(n)
+  Ciphertext eval(const std::vector<double>& c, int level, const Scale& target) {
+    const std::size_t n = c.size();
+    if (n <= 2) {  // c0 + c1 X: one plaintext product at level + 1, scale chosen to land on `target`
+      const int l1 = level + 1;
+      const Ciphertext xl = x.level == l1 ? x : ops.mod_down(x, l1);
+      const Scale s = target * Scale::prime(ops.modulus_at(l1)) / x.scale;
+      Ciphertext y = ops.rescale(ops.mul_plain(xl, ops.encode(constv(n > 1 ? c[1] : 0.0), l1, s)));
+      if (c[0] != 0.0) y = ops.add_plain(y, ops.encode(constv(c[0]), level, target));
+      return y;
+    }
+    int m = 0;
+    while ((std::size_t(1) << m) < n) ++m;
+    const std::size_t h = std::size_t(1) << (m - 1);
+    std::vector<double> lo(c.begin(), c.begin() + (std::ptrdiff_t)h), hi(c.begin() + (std::ptrdiff_t)h, c.end());
+    if (basis == PolyBasis::Chebyshev) {  // p = lo + T_h hi (Chebyshev division by T_h)
+      for (std::size_t j = 1; j < hi.size(); ++j) {
+        lo[h - j] -= c[h + j];
+        hi[j] = 2.0 * c[h + j];
+      }
+    }
+    const Ciphertext& P = power(m - 1);
+    const int lp = P.level;
+    // hi at (lp, T q_lp / S_P): the product's rescale lands exactly on `target`
+    const Scale th = target * Scale::prime(ops.modulus_at(lp)) / P.scale;
+    Ciphertext prod;
+    if (hi.size() == 1) {  // constant quotient: a plaintext product instead of a ciphertext one
+      prod = ops.rescale(ops.mul_plain(P, ops.encode(constv(hi[0]), lp, th)));
+    } else {
+      prod = ops.rescale(ops.mul(P, eval(hi, lp, th)));
+    }
+    if (prod.level != level) prod = ops.mod_down(prod, level);
+    return ops.add(eval(lo, level, target), prod);
+  }
+};
+}  // namespace
+
+Ciphertext polyeval(SlotOps& ops, const Ciphertext& x, const std::vector<double>& coeffs, PolyBasis basis,
+                    double a, double b, KernelReport* report) {
+  if (coeffs.empty()) throw std::invalid_argument("polyeval: no coefficients");
+  if (basis == PolyBasis::Chebyshev && !(b > a)) throw std::invalid_argument("polyeval: empty interval");
+  const int depth = polyeval_depth(coeffs.size(), basis);
+  if (x.level < depth) throw LevelUnderflowError("polyeval: insufficient level");
+  const auto snap = TraceSnapshot::take(ops.trace());
+  Ciphertext v = x;
+  if (basis == PolyBasis::Chebyshev) {  // y = alpha x + beta at level L - 1, scale Delta
+    const double alpha = 2.0 / (b - a), beta = -(a + b) / (b - a);
+    const Scale s = ops.params().delta() * Scale::prime(ops.modulus_at(x.level)) / x.scale;
+    v = ops.rescale(ops.mul_plain(x, ops.encode(std::vector<double>(ops.slots(), alpha), x.level, s)));
+    if (beta != 0.0) v = ops.add_plain(v, ops.encode(std::vector<double>(ops.slots(), beta), v.level, v.scale));
+  }
+  PolyCtx P{ops, basis, v, {v}};
+  const int out_level = v.level - polyeval_depth(coeffs.size(), PolyBasis::Power);
+  Ciphertext out = P.eval(coeffs, out_level, ops.params().delta());
+  if (report) *report = report_since(ops.trace(), snap, x.level, out);
+  return out;
+}
+
 // ------------------------------------------------------------------- keys
 std::vector<std::int64_t> bsgs_rotations(const BsgsPlan& plan) {
   std::vector<std::int64_t> r;

@@ -69,6 +69,7 @@ def lib():
         "hxc_matvec_shard": (i32, [v, v, v, C.POINTER(v), i32, rp]),
         "hxc_ct_like": (v, [v, v, v]),
         "hxc_matmul_rotations": (i32, [i32, C.POINTER(C.c_int64), i32]),
+        "hxc_polyeval": (v, [v, v, f64p, i32, i32, C.c_double, C.c_double, rp]),
         "hxc_predicted_rotations": (C.c_longlong, [i32, i32, i32, i64]),
         "hxc_secret_key_ptr": (v, [v]),
         "hxc_relin_key_ptr": (v, [v]),
@@ -289,6 +290,14 @@ class Backend:
     def matmul(self, A, B, d):
         r = Report()
         c = Ct(self, self.L.hxc_matmul(self.h, A.h, B.h, d, C.byref(r)))
+        return c, r.as_dict()
+
+    def polyeval(self, x, coeffs, basis="power", lo=-1.0, hi=1.0):
+        """slot-wise polynomial (SPEC polyeval): basis "power" or "chebyshev" on [lo, hi]"""
+        r = Report()
+        a, ap = _dp(coeffs)
+        c = Ct(self, self.L.hxc_polyeval(self.h, x.h, ap, len(a), 1 if basis == "chebyshev" else 0, lo, hi,
+                                         C.byref(r)))
         return c, r.as_dict()
 
     @staticmethod

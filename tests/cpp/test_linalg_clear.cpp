@@ -269,6 +269,41 @@ int main() {
     rotate_and_sum(be, c, 1, 1, &r1);
     CHECK(r1.rotations == 0, "span 1 -> 0 rotations");
   }
+  // ---------------------------------------------------------- polyeval
+  {
+    ClearBackend be(params(1024, 8));
+    std::mt19937_64 g(11);
+    std::uniform_real_distribution<double> U(-1.0, 1.0);
+    std::vector<double> xs(be.slots());
+    for (auto& v : xs) v = U(g);
+    const auto ct = be.encrypt(be.encode(xs, 8, be.params().delta()));
+    std::vector<double> c(8);
+    for (auto& v : c) v = U(g);
+    KernelReport rep;
+    const auto out = polyeval(be, ct, c, PolyBasis::Power, -1, 1, &rep);
+    const auto y = be.decrypt(out);
+    double err = 0;
+    for (std::size_t i = 0; i < xs.size(); ++i) {
+      double h = 0;
+      for (int k = 7; k >= 0; --k) h = h * xs[i] + c[k];
+      err = std::max(err, std::abs(y[i] - h));
+    }
+    CHECK(err < 1e-9, "polyeval degree 7 == Horner (SPEC.md:411)");
+    CHECK(rep.levels_consumed == 3 && out.scale == be.params().delta(), "polyeval: 3 levels, scale exactly Delta");
+    const auto sq = polyeval(be, be.encrypt(be.encode(std::vector<double>{1, 2, 3}, 8, be.params().delta())),
+                             std::vector<double>{0, 0, 1}, PolyBasis::Power);
+    const auto s3 = be.decrypt(sq);
+    CHECK(std::abs(s3[0] - 1) + std::abs(s3[1] - 4) + std::abs(s3[2] - 9) < 1e-9, "x^2 on [1,2,3] -> [1,4,9] (SPEC.md:410)");
+    // Chebyshev on [-8, 8]: T_3(y) at y = x / 8
+    std::vector<double> ch{0, 0, 0, 1};
+    const auto t3 = be.decrypt(polyeval(be, be.encrypt(be.encode(std::vector<double>{4.0}, 8, be.params().delta())), ch,
+                                        PolyBasis::Chebyshev, -8, 8, &rep));
+    CHECK(std::abs(t3[0] - (4 * 0.125 - 3 * 0.5)) < 1e-9 && rep.levels_consumed == 3, "Chebyshev T_3 + domain map level");
+    CHECK(throws<LevelUnderflowError>([&] {
+            polyeval(be, be.encrypt(be.encode(xs, 2, be.params().delta())), c, PolyBasis::Power);
+          }),
+          "polyeval: insufficient level");
+  }
   // ---------------------------------------------------------- the 4x4 example
   {
     const Matrix A = from_rows({{1, 2, 3, 4}, {5, 6, 7, 8}, {9, 10, 11, 12}, {13, 14, 15, 16}});

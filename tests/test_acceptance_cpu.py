@@ -35,3 +35,16 @@ def test_predicted_rotation_closed_forms():
     assert predicted_rotations(BSGS, 512, 256, n) == 15 + 2 * 15  # 2 row blocks share the baby steps
     with pytest.raises(Exception):
         predicted_rotations(BSGS, 4, 8192, n)  # wider than the slot count
+
+
+def test_criterion_8_gelu_fit():
+    """SPEC criterion 8 (cleartext part): a degree-127 Chebyshev fit of GeLU on
+    [-8, 8] is within 1e-2 of exact GeLU on a 10^4-point grid (the coefficients
+    polyeval takes for the paper's GeLU(degree=127))."""
+    import numpy as np
+    from scipy.special import erf
+
+    gelu = lambda t: 0.5 * t * (1 + erf(t / np.sqrt(2)))  # noqa: E731
+    fit = np.polynomial.chebyshev.Chebyshev.interpolate(gelu, 127, domain=[-8, 8])
+    grid = np.linspace(-8, 8, 10_000)
+    assert np.abs(fit(grid) - gelu(grid)).max() < 1e-2

@@ -138,3 +138,34 @@ def test_criterion_6_fidelity():
         cw = be.mod_down(cw, c.level)
         ref = ref * w
     assert np.abs(be.decrypt(c) - ref).max() < 1e-2
+
+
+def test_criterion_8_polyeval():
+    """SPEC criterion 8 (encrypted part) and polyeval's contract: degree-7
+    random coefficients vs cleartext Horner < 1e-3 on the lattice backend;
+    levels = ceil(log2(#coeffs)) (+1 for the Chebyshev domain map); output
+    scale exactly Delta; a degree-15 Chebyshev fit of GeLU on [-8, 8]
+    evaluated encrypted matches its cleartext Chebyshev evaluation."""
+    be = toy_backend()
+    n = be.slots
+    rng = np.random.default_rng(8)
+    xs = rng.uniform(-1, 1, n)
+    ct = be.encrypt(xs)
+    for deg in (1, 2, 3, 7):
+        c = rng.uniform(-1, 1, deg + 1)
+        out, rep = be.polyeval(ct, c)
+        exp = np.polynomial.polynomial.polyval(xs, c)
+        assert np.abs(be.decrypt(out) - exp).max() < 1e-3, deg
+        assert rep["levels_consumed"] == max(1, int(np.ceil(np.log2(deg + 1))))
+        assert abs(rep["output_scale_log2"] - 30.0) < 1e-9 and out.level == be.max_level - rep["levels_consumed"]
+    # x^2 on [1, 2, 3] -> [1, 4, 9]
+    c2 = be.encrypt(np.resize([1.0, 2.0, 3.0], n) / 4)  # inputs scaled into [-1, 1]
+    out, _ = be.polyeval(c2, [0.0, 0.0, 16.0])
+    assert np.allclose(be.decrypt(out)[:3], [1.0, 4.0, 9.0], atol=1e-3)
+    # Chebyshev: GeLU on [-8, 8], degree 15 (depth 4 + 1 for the domain map)
+    x8 = rng.uniform(-8, 8, n)
+    cheb = np.polynomial.chebyshev.Chebyshev.interpolate(
+        lambda t: 0.5 * t * (1 + np.tanh(np.sqrt(2 / np.pi) * (t + 0.044715 * t ** 3))), 15, domain=[-8, 8])
+    out, rep = be.polyeval(be.encrypt(x8), cheb.coef, "chebyshev", -8.0, 8.0)
+    assert rep["levels_consumed"] == 5
+    assert np.abs(be.decrypt(out) - cheb(x8)).max() < 1e-2
