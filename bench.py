@@ -40,8 +40,10 @@ HOIST_R = 32
 HOIST_CHUNK = 8
 
 
-def primes():
-    """config-2 primes: reference find_ntt_primes (modmath.hpp:138-152)."""
+def primes(fp64_specials: bool = False):
+    """config-2 primes: reference find_ntt_primes (modmath.hpp:138-152).
+    fp64_specials: the special primes just below 2^47 instead of 3 x 60-bit
+    (parameter co-design for B200's FP64 datapath; an extra, not the headline)."""
     # a self-contained restatement (bench must not depend on the oracle for
     # the product path): first primes = 1 mod 2N at or above the starts.
     def is_prime(n):
@@ -78,7 +80,10 @@ def primes():
     two_n = 2 * N
     q0 = find(1 << 59, 1, two_n)
     rest = find(1 << 39, N_CHAIN - 1, two_n)
-    sp = find(1 << 59, 3, two_n, exclude=q0)
+    if fp64_specials:  # 3 primes just below 2^47 (FP64 class): P ~ 2^141 > max digit 2^140
+        sp = find((1 << 47) - (1 << 36), 3, two_n, exclude=q0 + rest)
+    else:
+        sp = find(1 << 59, 3, two_n, exclude=q0)
     return q0 + rest, sp
 
 
@@ -528,6 +533,19 @@ def main():
                         "limb once (profiles/); DESIGN.md section 5"}
 
     extras = {"limb_ntt_per_s": ntt_limbs / (ntt_secs / 3)}
+    if not args.no_extras:
+        # the same batch-256 key switch with 3 special primes < 2^47 (FP64 class):
+        # every limb but q0 on the FP64 pipe
+        chain47, special47 = primes(fp64_specials=True)
+        ctx47 = Context(LOGN, chain47, special47, ALPHA)
+        key47 = make_key(torch, ctx47, gen, chain47, special47, g1, dev)
+        ks47 = time_loop(torch, lambda: ctx47.rotate(out, cts, key47, BATCH, nq, g1, stream), 3, 2, stream)
+        extras["ks_per_s_fp64_specials"] = {"value": BATCH * 3 / ks47, "unit": "KS/s",
+                                            "special_bits": [p.bit_length() for p in special47],
+                                            "log2_P": sum(p.bit_length() - 1 for p in special47) + 3}
+        del key47
+        ctx47.trim()
+        del ctx47
     # the linear transform's HBM-bound kernel: the BSGS diagonal MAC at the
     # FFN W1 block shape (n1 = n2 = 32, 24 limbs), diagonals streamed once
     del ntt_buf

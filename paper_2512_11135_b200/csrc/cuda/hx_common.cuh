@@ -38,6 +38,8 @@ struct PrimeConst {
   double w1n_d, w1n_q;       // last-stage twiddle * N^-1, / q
   double r20_d, r20_q;       // 2^20 mod q (and / q): 20-bit split MAC combine
   double r40_d, r40_q;       // 2^40 mod q
+  double r24_d, r24_q;       // 2^24 mod q: 24-bit split key inner product (q < 2^47)
+  double r48_d, r48_q;       // 2^48 mod q
   const double* twf_fwd;     // w as double (w / q formed in-kernel)
   const double* twf_inv;
 };

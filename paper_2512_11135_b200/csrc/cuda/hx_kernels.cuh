@@ -290,6 +290,21 @@ __device__ __forceinline__ u64 combine_split(const double (&s)[3], const PrimeCo
   return f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);
 }
 
+// 24-bit split for the key inner product (q < 2^47, dnum <= 8): with
+// x = xh 2^24 + xl (xh < 2^23), S_hh < 8 2^46, S_hl < 8 2^48, S_ll < 8 2^48 --
+// every sum below 2^52, exact; value = S_hh 2^48 + S_hl 2^24 + S_ll mod q.
+__device__ __forceinline__ void split24_d(u64 v, double& hi, double& lo) {
+  hi = __dsub_rn(__longlong_as_double((long long)((v >> 24) | 0x4330000000000000ull)), kTwo52);
+  lo = __dsub_rn(__longlong_as_double((long long)((v & 0xFFFFFFull) | 0x4330000000000000ull)), kTwo52);
+}
+
+__device__ __forceinline__ u64 combine_split24(const double (&s)[3], const PrimeConst& P) {
+  const double v = __dadd_rn(__dadd_rn(mulmod_f64(s[0], P.r48_d, P.r48_q, P.qd),
+                                       mulmod_f64(s[1], P.r24_d, P.r24_q, P.qd)),
+                             centre_f64(s[2], P.qd, P.qinv_d));
+  return f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);
+}
+
 template <int MAXD>
 __global__ void __launch_bounds__(256, 2) ks_inner_f64_kernel(InnerArgs A, const int* limbs) {
   const int N = 1 << A.logn;
@@ -312,7 +327,7 @@ __global__ void __launch_bounds__(256, 2) ks_inner_f64_kernel(InnerArgs A, const
       if (d < A.dnum) kw = comp ? (c == 0 ? __ldg(key + ((long long)d * full + kl) * N + t)
                                            : uniform_word(A.kseed[r], ((u64)d * full + kl) * N + ta, P.q))
                                 : __ldg(key + (((long long)d * 2 + c) * full + kl) * N + t);
-      split20_d(kw, kh[d][c], klo[d][c]);
+      split24_d(kw, kh[d][c], klo[d][c]);
     }
   const int src = (A.g == 1) ? t : (int)ntt_auto_index((u32)t, A.g, A.logn);
   const int per = (E + A.slices - 1) / A.slices;
@@ -332,7 +347,7 @@ __global__ void __launch_bounds__(256, 2) ks_inner_f64_kernel(InnerArgs A, const
 #pragma unroll
     for (int d = 0; d < MAXD; ++d) {
       double xh, xl;
-      split20_d(v[d], xh, xl);
+      split24_d(v[d], xh, xl);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         s[c][0] = __fma_rn(xh, kh[d][c], s[c][0]);
@@ -342,8 +357,8 @@ __global__ void __launch_bounds__(256, 2) ks_inner_f64_kernel(InnerArgs A, const
       }
     }
     u64* ub = ubase + (long long)b * 2 * ext * N + (long long)j * N + t;
-    ub[0] = combine_split(s[0], P);
-    ub[(long long)ext * N] = combine_split(s[1], P);
+    ub[0] = combine_split24(s[0], P);
+    ub[(long long)ext * N] = combine_split24(s[1], P);
   }
 }
 
@@ -391,9 +406,9 @@ __global__ void __launch_bounds__(256, 3) ks_inner_f64_one_kernel(InnerArgs A, c
 #pragma unroll
   for (int d = 0; d < MAXD; ++d) {
     double xh, xl, ah, al, bh, bl;
-    split20_d(v[d], xh, xl);
-    split20_d(k0[d], ah, al);
-    split20_d(k1[d], bh, bl);
+    split24_d(v[d], xh, xl);
+    split24_d(k0[d], ah, al);
+    split24_d(k1[d], bh, bl);
     s[0][0] = __fma_rn(xh, ah, s[0][0]);
     s[0][1] = __fma_rn(xh, al, s[0][1]);
     s[0][1] = __fma_rn(xl, ah, s[0][1]);
@@ -404,8 +419,8 @@ __global__ void __launch_bounds__(256, 3) ks_inner_f64_one_kernel(InnerArgs A, c
     s[1][2] = __fma_rn(xl, bl, s[1][2]);
   }
   u64* ub = A.u + ((long long)r * E + b) * 2 * ext * N + (long long)j * N + t;
-  ub[0] = combine_split(s[0], P);
-  ub[(long long)ext * N] = combine_split(s[1], P);
+  ub[0] = combine_split24(s[0], P);
+  ub[(long long)ext * N] = combine_split24(s[1], P);
 }
 
 template <int MAXD>

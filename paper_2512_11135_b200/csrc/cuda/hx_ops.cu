@@ -839,6 +839,10 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
       P.r20_q = P.r20_d / qd;
       P.r40_d = (double)((1ull << 40) % q);
       P.r40_q = P.r40_d / qd;
+      P.r24_d = (double)((1ull << 24) % q);
+      P.r24_q = P.r24_d / qd;
+      P.r48_d = (double)((1ull << 48) % q);
+      P.r48_q = P.r48_d / qd;
       double* ff = twf.data() + (size_t)i * 2 * N;
       if (P.f64)
         for (u64 k = 0; k < 2 * N; ++k) ff[k] = (double)(k < N ? f[k] : g[k - N]).x;
@@ -1007,7 +1011,7 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
       int* f = kl.data() + (size_t)nq * 2 * T;
       int* g = f + T;
       for (int j = 0; j < nq + n_special; ++j) {
-        if (c->allow_f64 && c->primes[c->pidx(j, nq)] < (1ull << 43))
+        if (c->allow_f64 && c->primes[c->pidx(j, nq)] < (1ull << 47))  // 24-bit split inner product
           f[c->ks_nf64[nq]++] = j;
         else
           g[c->ks_nint[nq]++] = j;

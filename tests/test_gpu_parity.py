@@ -8,7 +8,7 @@ Sizes: config 1 (N=2^13, 3+1 primes, alpha=1), a reduced-N config-2 shape
 import numpy as np
 import pytest
 
-from configs import config1, config2
+from configs import config1, config2, config2_fp64_specials
 from oracle_bindings import Oracle, galois_elt, gaussian, ternary, uniform_limbs
 
 pytestmark = pytest.mark.gpu
@@ -17,6 +17,7 @@ CFGS = {
     "c1": lambda: config1(13),
     "c2s": lambda: config2(12, 24),
     "c2": lambda: config2(16, 24),
+    "c2s47": lambda: config2_fp64_specials(12, 24),  # FP64-class special primes
 }
 
 _cache = {}
@@ -209,7 +210,7 @@ def test_modup_inner_moddown_parity(cfg):
             assert np.array_equal(Vg[b], orc.moddown_ntt(Ug[b], lvl, 2)), f"moddown lvl={lvl}"
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2s", "c2"])
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c2", "c2s47"])
 def test_rotate_parity_and_decrypt(cfg):
     p, ctx, orc = env(cfg)
     rng = np.random.default_rng(7)
@@ -240,7 +241,7 @@ def test_rotate_parity_and_decrypt(cfg):
         assert np.abs(diff).max() < 2**16
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c2s47"])
 def test_keyswitch_and_hoisted_parity(cfg):
     p, ctx, orc = env(cfg)
     rng = np.random.default_rng(8)
@@ -265,7 +266,7 @@ def test_keyswitch_and_hoisted_parity(cfg):
         assert np.array_equal(exp[r], orc.rotate(ct, keys[r], nq, g))
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c2s47"])
 def test_rotate_multi_parity(cfg):
     """hx_rotate_multi: per-element keys / galois elements, one batched ModUp"""
     import ctypes as C
@@ -289,7 +290,7 @@ def test_rotate_multi_parity(cfg):
         assert np.array_equal(got[b], orc.rotate(cts[b], keys[b], nq, gs[b])), b
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2s"])
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c2s47"])
 def test_tensor_and_mul_relin_parity(cfg):
     p, ctx, orc = env(cfg)
     rng = np.random.default_rng(9)

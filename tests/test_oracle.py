@@ -10,7 +10,7 @@ import os
 import numpy as np
 import pytest
 
-from configs import config1, config2
+from configs import config1, config2, config2_fp64_specials
 from oracle_bindings import (
     Oracle,
     Ref,
@@ -124,11 +124,12 @@ def _centred_max(a, b, q):
     return int(np.abs(d).max())
 
 
-@pytest.mark.parametrize("logn,n_chain", [(11, 24), (12, 8)])
-def test_oracle_hybrid_ks_decrypts(logn, n_chain):
+@pytest.mark.parametrize("logn,n_chain,fp64sp", [(11, 24, False), (12, 8, False), (11, 24, True)])
+def test_oracle_hybrid_ks_decrypts(logn, n_chain, fp64sp):
     """K=3 / alpha=3 hybrid KS: rotations and relinearisation decrypt correctly
-    at every level (the builder's restatement has no reference code)."""
-    p = config2(logn, n_chain)
+    at every level (the builder's restatement has no reference code); also
+    with the FP64-class (< 2^47) special primes, P ~ 2^141 > max digit 2^140."""
+    p = config2_fp64_specials(logn, n_chain) if fp64sp else config2(logn, n_chain)
     orc = Oracle(p["logn"], p["chain"], p["special"], 3)
     nq, K, n = len(p["chain"]), 3, 1 << logn
     rng = np.random.default_rng(3)

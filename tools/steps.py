@@ -14,6 +14,15 @@ from paper_2512_11135_b200 import Context  # noqa: E402
 
 def main():
     chain, special = bench.primes()
+    sb = int(os.environ.get("HX_SPECIAL_BITS", "0"))
+    if sb:  # experiment: special primes just below 2^sb (FP64-class when sb <= 47)
+        two_n = 2 * bench.N
+        special, p = [], ((1 << sb) // two_n) * two_n + 1
+        while len(special) < 3:
+            p -= two_n
+            if p not in chain and pow(3, p - 1, p) == 1 and all(pow(a, p - 1, p) == 1 for a in (2, 5, 7, 11, 13)):
+                special.append(p)
+        print("specials", [x.bit_length() for x in special], flush=True)
     ctx = Context(bench.LOGN, chain, special, bench.ALPHA)
     dev = torch.device("cuda", 0)
     gen = torch.Generator(device=dev)
