@@ -281,7 +281,7 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=16, chunk=8):
     n1 = n2 = 32; W2 d = 4096, 1 block, n1 = n2 = 64; one token per ciphertext
     (T = 1), plus the 90%-diagonal-pruned variants.  Diagonals are encoded on
     the device (hx_encode); prepare_s is encode + rotation-key generation."""
-    from paper_2512_11135_b200.helix import BSGS, Backend, params_json
+    from paper_2512_11135_b200.helix import BSGS, BSGS_STACKED, Backend, params_json
 
     rng = np.random.default_rng(20251211 * 10 + 3)
     be = Backend(params_json(LOGN, chain, special, ALPHA, 40), seed=3)
@@ -290,24 +290,30 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=16, chunk=8):
     W2 = rng.normal(0.0, 0.02, (3072, 768))
     lvl = be.max_level
     prune_rng = np.random.default_rng(20251211 * 10 + 3 + 200)
-    jobs = [("ffn_w1", W1.T.copy(), 1024, False), ("ffn_w1_pruned90", W1.T.copy(), 1024, True)]
+    jobs = [("ffn_w1", W1.T.copy(), 1024, False, BSGS), ("ffn_w1_pruned90", W1.T.copy(), 1024, True, BSGS),
+            # the 3 row blocks stacked in one set of full-length diagonals: one
+            # output ciphertext, (n1-1)+(n2-1) = 62 key switches instead of 124
+            ("ffn_w1_stacked", W1.T.copy(), 1024, False, BSGS_STACKED)]
     if not getattr(args, "no_w2", False):
-        jobs += [("ffn_w2", W2.T.copy(), 4096, False), ("ffn_w2_pruned90", W2.T.copy(), 4096, True)]
-    for name, M, d, prune in jobs:  # y = x W  ->  M = W^T (out x in)
+        jobs += [("ffn_w2", W2.T.copy(), 4096, False, BSGS), ("ffn_w2_pruned90", W2.T.copy(), 4096, True, BSGS)]
+    for name, M, d, prune, method in jobs:  # y = x W  ->  M = W^T (out x in)
         if prune:
             M = _prune_diagonals(M, d, prune_rng)
         x = rng.uniform(-1, 1, M.shape[1])
         xs = np.tile(np.concatenate([x, np.zeros(d - M.shape[1])]), be.slots // d)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        mat = be.prepare(BSGS, M, lvl)
+        mat = be.prepare(method, M, lvl)
         be.gen_rotation_keys(mat.rotations())
         torch.cuda.synchronize()
         prep = time.perf_counter() - t0
         ct = be.encrypt(xs, lvl)
         for _ in range(3):  # warm-up (pool growth, first-launch setup) + correctness
             outs, rep = be.matvec(mat, ct)
-        y = np.concatenate([be.decrypt(o)[:d] for o in outs])[:M.shape[0]]
+        if method == BSGS_STACKED:
+            y = be.decrypt(outs[0])[:M.shape[0]]
+        else:
+            y = np.concatenate([be.decrypt(o)[:d] for o in outs])[:M.shape[0]]
         err = float(np.abs(y - M @ x).max())
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -323,7 +329,7 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=16, chunk=8):
                      "rotations": rep["rotations"], "pt_muls": rep["pt_muls"], "nonzero_diagonals": info["nonzero"],
                      "diag_bytes": info["nonzero"] * 24 * N * 8, "prepare_s": prep}
         del outs
-        if not prune and tokens > 0:
+        if not prune and tokens > 0 and method == BSGS:
             chunk = max(1, 8 // info["blocks"]) if d < 4096 else 8  # bound the grouped-rotation working set
             # T tokens through the same matrix, key switches batched over a chunk
             # of `chunk` tokens (hxc_matvec_tokens); per-token throughput

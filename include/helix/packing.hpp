@@ -25,7 +25,7 @@ struct Matrix {
   double at(int r, int c) const { return data[(std::size_t)r * cols + c]; }
 };
 
-enum class Layout { PackedRow, Diagonal, BsgsDiagonal, RowMajor };
+enum class Layout { PackedRow, Diagonal, BsgsDiagonal, RowMajor, BsgsStacked };
 
 // n1 * n2 = d, powers of two
 struct BsgsPlan {
@@ -41,7 +41,8 @@ struct PackedMatrix {
   int d = 0;                       // block dimension (matvec layouts) / matrix dim (RowMajor)
   int row_blocks = 1;              // output blocks of d rows (matvec layouts)
   int rows_per_payload = 0;        // PackedRow only
-  BsgsPlan plan;                   // BsgsDiagonal only
+  BsgsPlan plan;                   // BsgsDiagonal / BsgsStacked
+  int stacked_blocks = 0;          // BsgsStacked: row blocks stacked in the slots
   std::size_t slots = 0;
   // Diagonal / BsgsDiagonal: payloads[b * d + i] (empty vector = all-zero payload)
   // PackedRow: payloads[g]; RowMajor: payloads[0]
@@ -56,6 +57,16 @@ PackedMatrix pack_diagonals(const Matrix& A, std::size_t slots);
 // diagonal n1 j + k stored rotated right by n1 j
 PackedMatrix pack_bsgs(const Matrix& A, const BsgsPlan& plan, std::size_t slots);
 PackedMatrix pack_bsgs(const Matrix& A, std::size_t slots);
+// Stacked-block BSGS (an extension beyond the SPEC layouts): the row blocks of
+// a tall matrix are stacked in ONE set of d full-length diagonals,
+// D_i[b d + r] = A[b d + r][(r + i) mod d] for blocks b < B = ceil(rows / d)
+// (B d <= n), each pre-rotated right by n1 (i / n1) over all n slots.  With x
+// replicated at period d the BSGS identity holds on the whole slot vector, so
+// one matvec yields every block at once -- y[row] in slot `row` -- with
+// (n1 - 1) + (n2 - 1) rotations and d plaintext products instead of
+// (n1 - 1) + B (n2 - 1) and B d (config 3 W1: 62 key switches instead of 124).
+PackedMatrix pack_bsgs_stacked(const Matrix& A, const BsgsPlan& plan, std::size_t slots);
+PackedMatrix pack_bsgs_stacked(const Matrix& A, std::size_t slots);
 // rows_per_payload = min(n / pad_cols, R); payload g holds rows [g p, (g+1) p)
 // at stride pad_cols
 PackedMatrix pack_rows(const Matrix& A, std::size_t slots);

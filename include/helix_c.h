@@ -34,7 +34,9 @@ typedef struct {
   double output_scale_log2;
 } hxc_report;
 
-enum { HXC_ROW = 0, HXC_DIAG = 1, HXC_BSGS = 2 };
+/* HXC_BSGS_STACKED: row blocks stacked in one set of full-length diagonals
+ * (helix::pack_bsgs_stacked); one output ciphertext, y[row] in slot `row` */
+enum { HXC_ROW = 0, HXC_DIAG = 1, HXC_BSGS = 2, HXC_BSGS_STACKED = 3 };
 
 const char* hxc_last_error(void);
 

@@ -136,7 +136,10 @@ hxc_mat* hxc_matrix_prepare(hxc_backend* b, int method, const double* A, int row
     const std::size_t n = b->b->slots();
     static const bool trace = getenv("HX_PREP_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
-    PackedMatrix P = method == HXC_ROW ? pack_rows(M, n) : method == HXC_DIAG ? pack_diagonals(M, n) : pack_bsgs(M, n);
+    PackedMatrix P = method == HXC_ROW              ? pack_rows(M, n)
+                     : method == HXC_DIAG           ? pack_diagonals(M, n)
+                     : method == HXC_BSGS_STACKED   ? pack_bsgs_stacked(M, n)
+                                                    : pack_bsgs(M, n);
     const auto t1 = std::chrono::steady_clock::now();
     auto* h = new hxc_mat;
     h->method = method;
@@ -188,7 +191,8 @@ int hxc_matvec(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, 
 int hxc_matvec_tokens(hxc_backend* b, const hxc_mat* m, const hxc_ct* const* xs, int T, hxc_ct** out, int cap,
                       hxc_report* rep) {
   return guard(-1, [&] {
-    if (m->method != HXC_BSGS) throw std::invalid_argument("hxc_matvec_tokens: BSGS matrices only");
+    if (m->method != HXC_BSGS && m->method != HXC_BSGS_STACKED)
+      throw std::invalid_argument("hxc_matvec_tokens: BSGS matrices only");
     std::vector<Ciphertext> in;
     for (int t = 0; t < T; ++t) in.push_back(xs[t]->c);
     const auto rs = matvec_bsgs_tokens(*b->b, m->m, in);
@@ -249,7 +253,10 @@ hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_
 
 long long hxc_predicted_rotations(int method, int rows, int cols, int64_t slots) {
   return guard<long long>(-1, [&] {
-    const Layout l = method == HXC_ROW ? Layout::PackedRow : method == HXC_DIAG ? Layout::Diagonal : Layout::BsgsDiagonal;
+    const Layout l = method == HXC_ROW    ? Layout::PackedRow
+                     : method == HXC_DIAG ? Layout::Diagonal
+                     : method == HXC_BSGS_STACKED ? Layout::BsgsStacked
+                                                  : Layout::BsgsDiagonal;
     return (long long)predicted_rotations(l, rows, cols, (std::size_t)slots);
   });
 }

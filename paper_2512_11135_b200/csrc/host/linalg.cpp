@@ -36,7 +36,8 @@ Ciphertext add_opt(SlotOps& ops, std::optional<Ciphertext>& acc, const Ciphertex
 }
 
 void require_matvec_input(const EncodedMatrix& M, const Ciphertext& x, Layout want) {
-  if (M.meta.layout != want) throw std::invalid_argument("matvec: wrong matrix layout");
+  const bool ok = M.meta.layout == want || (want == Layout::BsgsDiagonal && M.meta.layout == Layout::BsgsStacked);
+  if (!ok) throw std::invalid_argument("matvec: wrong matrix layout");
   detail::require_same_level(x.level, M.level, "matvec");
   if (x.level < 1) throw LevelUnderflowError("matvec: level budget < 1");
 }
@@ -371,6 +372,10 @@ std::int64_t predicted_rotations(Layout layout, int rows, int cols, std::size_t 
       const BsgsPlan plan = BsgsPlan::for_dim(pc);
       const std::int64_t blocks = (rows + pc - 1) / pc;
       return (plan.n1 - 1) + blocks * (plan.n2 - 1);
+    }
+    case Layout::BsgsStacked: {
+      const BsgsPlan plan = BsgsPlan::for_dim(pc);
+      return (plan.n1 - 1) + (plan.n2 - 1);
     }
     default:
       throw std::invalid_argument("predicted_rotations: not a matvec layout");

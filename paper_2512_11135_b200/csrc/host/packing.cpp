@@ -101,6 +101,42 @@ PackedMatrix pack_bsgs(const Matrix& A, std::size_t n) {
   return pack_bsgs(A, BsgsPlan::for_dim(next_pow2(std::max(A.cols, 1))), n);
 }
 
+PackedMatrix pack_bsgs_stacked(const Matrix& A, const BsgsPlan& plan, std::size_t n) {
+  PackedMatrix M = diag_common(A, n, Layout::BsgsStacked);
+  if (plan.n1 * plan.n2 != M.d) throw std::invalid_argument("pack_bsgs_stacked: plan inconsistent with padded dim");
+  if ((std::size_t)M.row_blocks * M.d > n) throw std::invalid_argument("pack_bsgs_stacked: blocks x d exceeds the slot count");
+  M.plan = plan;
+  const int B = M.row_blocks, d = M.d;
+  M.row_blocks = 1;  // one stacked output ciphertext
+  for (int i = 0; i < d; ++i) {
+    std::vector<double> D(n, 0.0);
+    bool any = false;
+    for (int b = 0; b < B; ++b)
+      for (int r = 0; r < d; ++r) {
+        const int row = b * d + r, col = (r + i) % d;
+        if (row < A.rows && col < A.cols) {
+          const double v = A.at(row, col);
+          D[(std::size_t)row] = v;
+          any = any || v != 0.0;
+        }
+      }
+    if (!any) {
+      M.payloads.emplace_back();
+      continue;
+    }
+    const std::size_t shift = (std::size_t)(i / plan.n1) * plan.n1;  // rotate right by n1 j over all n slots
+    std::vector<double> R(n);
+    for (std::size_t s = 0; s < n; ++s) R[s] = D[(s + n - shift) % n];
+    M.payloads.push_back(std::move(R));
+  }
+  M.stacked_blocks = B;
+  return M;
+}
+
+PackedMatrix pack_bsgs_stacked(const Matrix& A, std::size_t n) {
+  return pack_bsgs_stacked(A, BsgsPlan::for_dim(next_pow2(std::max(A.cols, 1))), n);
+}
+
 PackedMatrix pack_rows(const Matrix& A, std::size_t n) {
   PackedMatrix M;
   M.layout = Layout::PackedRow;
@@ -168,6 +204,17 @@ Matrix unpack(const PackedMatrix& M) {
     case Layout::RowMajor:
       for (int r = 0; r < M.rows; ++r)
         for (int c = 0; c < M.cols; ++c) A.at(r, c) = M.payloads[0][(std::size_t)r * M.d + c];
+      break;
+    case Layout::BsgsStacked:
+      for (int i = 0; i < M.d; ++i) {
+        const auto& p = M.payloads[i];
+        if (p.empty()) continue;
+        const std::size_t shift = (std::size_t)(i / M.plan.n1) * M.plan.n1, n = p.size();
+        for (int row = 0; row < M.rows; ++row) {
+          const int c = (row % M.d + i) % M.d;
+          if (c < M.cols) A.at(row, c) = p[((std::size_t)row + shift) % n];
+        }
+      }
       break;
   }
   return A;

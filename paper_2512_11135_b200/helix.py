@@ -14,7 +14,7 @@ import numpy as np
 from . import hx as _hx
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhelix_b200.so")
-ROW, DIAG, BSGS = 0, 1, 2
+ROW, DIAG, BSGS, BSGS_STACKED = 0, 1, 2, 3
 
 _lib = None
 

@@ -269,6 +269,34 @@ int main() {
     rotate_and_sum(be, c, 1, 1, &r1);
     CHECK(r1.rotations == 0, "span 1 -> 0 rotations");
   }
+  // ---------------------------------------------------------- stacked-block BSGS
+  {
+    std::mt19937_64 g(21);
+    for (auto [r, c] : std::vector<std::pair<int, int>>{{40, 16}, {64, 32}, {5, 8}, {48, 12}}) {
+      ClearBackend be(params(1024, 6));
+      const Matrix A = random_matrix(g, r, c);
+      const PackedMatrix P = pack_bsgs_stacked(A, be.slots());
+      CHECK(unpack(P).data == A.data, "unpack o pack_bsgs_stacked = identity");
+      std::vector<double> x(c);
+      std::uniform_real_distribution<double> U(-1, 1);
+      for (auto& v : x) v = U(g);
+      be.generate_rotation_keys(bsgs_rotations(P.plan));
+      std::vector<double> xp((std::size_t)P.d, 0.0);
+      std::copy(x.begin(), x.end(), xp.begin());
+      const auto ct = be.encrypt(be.encode(replicate(xp, P.d, be.slots()), 5, be.params().delta()));
+      const auto R = matvec_bsgs(be, encode_matrix(be, P, 5), ct);
+      const auto y = be.decrypt(R.outputs[0]);
+      double err = 0;
+      for (int i = 0; i < r; ++i) {
+        double acc = 0;
+        for (int k = 0; k < c; ++k) acc += A.at(i, k) * x[k];
+        err = std::max(err, std::abs(y[i] - acc));
+      }
+      CHECK(R.outputs.size() == 1 && err < 1e-9, "stacked BSGS = cleartext product, one output");
+      CHECK((int64_t)R.report.rotations == predicted_rotations(Layout::BsgsStacked, r, c, be.slots()),
+            "stacked BSGS rotations = (n1 - 1) + (n2 - 1)");
+    }
+  }
   // ---------------------------------------------------------- polyeval
   {
     ClearBackend be(params(1024, 8));

@@ -279,3 +279,44 @@ def test_bsgs_token_batch_matches_single(name, shape):
             assert np.array_equal(d2h(a.device_ptr(), 2 * nq * N), d2h(b.device_ptr(), 2 * nq * N))
         y = np.concatenate([be.decrypt(o)[:cols] for o in outs_t[t]])[:rows]
         assert np.abs(y - A @ xs[t]).max() < 1e-5
+
+
+@pytest.mark.parametrize("prune", [False, True])
+def test_bsgs_stacked_blocks(prune):
+    """Stacked-block BSGS (helix::pack_bsgs_stacked): the 2 row blocks of a
+    512 x 256 matrix in one set of full-length diagonals -> one output
+    ciphertext with y[row] in slot row, (n1 - 1) + (n2 - 1) rotations and d
+    plaintext products; matches the cleartext product and the per-block
+    BSGS method."""
+    from paper_2512_11135_b200.helix import BSGS, BSGS_STACKED, predicted_rotations
+
+    p, be = backend("c2s")
+    rng = np.random.default_rng(512 + prune)
+    A = rng.normal(0, 0.02, (512, 256))
+    if prune:
+        for b in range(2):
+            for i in rng.choice(256, 230, replace=False):
+                for j in range(256):
+                    A[b * 256 + j, (i + j) % 256] = 0
+    x = rng.uniform(-1, 1, 256)
+    lvl = be.max_level
+    M = be.prepare(BSGS_STACKED, A, lvl)
+    be.gen_rotation_keys(M.rotations())
+    ct = be.encrypt(np.tile(x, be.slots // 256), lvl)
+    be.trace_reset()
+    outs, rep = be.matvec(M, ct)
+    assert len(outs) == 1
+    y = be.decrypt(outs[0])[:512]
+    assert np.abs(y - A @ x).max() < 1e-5
+    info = M.info()
+    if not prune:
+        assert rep["rotations"] == 15 + 15 == predicted_rotations(BSGS_STACKED, 512, 256, be.slots)
+        assert rep["pt_muls"] == 256
+    assert rep["levels_consumed"] == 1 and abs(rep["output_scale_log2"] - 40.0) < 1e-12
+    # the per-block method agrees
+    M2 = be.prepare(BSGS, A, lvl)
+    be.gen_rotation_keys(M2.rotations())
+    outs2, rep2 = be.matvec(M2, ct)
+    y2 = np.concatenate([be.decrypt(o)[:256] for o in outs2])
+    assert np.abs(y - y2).max() < 1e-6
+    assert rep["rotations"] <= rep2["rotations"]
