@@ -407,6 +407,47 @@ def sharded_bsgs_bench(torch, dist, chain, special, rank, world, rows=11008, col
                                      "rotations_local": rep["rotations"], "prepare_s": prep}}
 
 
+def config5_stacked_bench(torch, chain, special, rows=11008, cols=4096, iters=3):
+    """BASELINE configs[4] on ONE GPU: W (11008 x 4096, N(0, 0.02^2)), x (4096,
+    U[-1,1]) replicated 8x, as a stacked-block BSGS (the 3 row blocks in one
+    set of 4096 full-length diagonals: 51.5 GB of diagonals + 126 keys instead
+    of 154.6 GB + 126 keys per-block, which does not fit next to the keys on
+    one B200)."""
+    from paper_2512_11135_b200.helix import BSGS_STACKED, Backend, params_json
+
+    rng = np.random.default_rng(20251211 * 10 + 5)
+    be = Backend(params_json(LOGN, chain, special, ALPHA, 40), seed=5)
+    W = rng.normal(0.0, 0.02, (rows, cols))
+    x = rng.uniform(-1, 1, cols)
+    lvl = be.max_level
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    M = be.prepare(BSGS_STACKED, W, lvl)
+    be.gen_rotation_keys(M.rotations())
+    torch.cuda.synchronize()
+    prep = time.perf_counter() - t0
+    ct = be.encrypt(np.tile(x, be.slots // cols), lvl)
+    for _ in range(2):
+        outs, rep = be.matvec(M, ct)
+    err = float(np.abs(be.decrypt(outs[0])[:rows] - W @ x).max())
+    del outs
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        outs, rep = be.matvec(M, ct)
+        del outs
+    e1.record()
+    torch.cuda.synchronize()
+    secs = e0.elapsed_time(e1) / 1e3 / iters
+    info = M.info()
+    be.close()
+    return {"config5_stacked_1gpu": {"matvec_per_s": 1.0 / secs, "ms_per_matvec": 1e3 * secs, "max_abs_err": err,
+                                     "rows": rows, "cols": cols, "d": info["d"], "rotations": rep["rotations"],
+                                     "pt_muls": rep["pt_muls"], "diag_bytes": info["nonzero"] * 24 * N * 8,
+                                     "prepare_s": prep}}
+
+
 def matmul_bench(torch, chain, special, d=128, n_q=4, iters=2):
     """BASELINE configs[3]: ct x ct matmul Q K^T of one head (128 x 64 padded to
     d = 128, N(0, 1)) through hxc_matmul (SPEC square-padded schedule), at a
@@ -634,7 +675,12 @@ def main():
             extras.update(matmul_bench(torch, chain, special))
         except Exception as exc:  # reported, never fatal for the headline line
             extras["matmul_d128"] = {"error": str(exc)[:200]}
-        if world > 1:  # config 5 needs >= 2 GPUs of memory (183 GB of diagonals + keys)
+        torch.cuda.empty_cache()
+        try:
+            extras.update(config5_stacked_bench(torch, chain, special))
+        except Exception as exc:
+            extras["config5_stacked_1gpu"] = {"error": str(exc)[:200]}
+        if world > 1:  # per-block config 5 needs >= 2 GPUs of memory (183 GB of diagonals + keys)
             torch.cuda.empty_cache()
             try:
                 extras.update(sharded_bsgs_bench(torch, dist, chain, special, rank, world))
