@@ -296,7 +296,11 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=16, chunk=8):
             ("ffn_w1_stacked", W1.T.copy(), 1024, False, BSGS_STACKED)]
     if not getattr(args, "no_w2", False):
         jobs += [("ffn_w2", W2.T.copy(), 4096, False, BSGS), ("ffn_w2_pruned90", W2.T.copy(), 4096, True, BSGS)]
+    only = getattr(args, "only", None)
+    if only:
+        jobs = [j for j in jobs if j[0] in only]
     for name, M, d, prune, method in jobs:  # y = x W  ->  M = W^T (out x in)
+        be.trim()  # workload switch: drop the previous job's scratch (a fragmented pool slows W2 by ~20%)
         if prune:
             M = _prune_diagonals(M, d, prune_rng)
         x = rng.uniform(-1, 1, M.shape[1])
@@ -323,6 +327,14 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=16, chunk=8):
         e1.record()
         torch.cuda.synchronize()
         secs = e0.elapsed_time(e1) / 1e3 / iters
+        if getattr(args, "verbose", False):
+            per = []
+            for _ in range(iters):
+                t0 = time.perf_counter()
+                outs, rep = be.matvec(mat, ct)
+                torch.cuda.synchronize()
+                per.append(round(1e3 * (time.perf_counter() - t0), 2))
+            print(name, "per-iteration wall ms:", per, file=sys.stderr)
         info = mat.info()
         out[name] = {"matvec_per_s": 1.0 / secs, "ms_per_matvec": 1e3 * secs, "max_abs_err": err,
                      "d": d, "n1": info["n1"], "n2": info["n2"], "row_blocks": info["blocks"],
@@ -374,14 +386,14 @@ def sharded_bsgs_bench(torch, dist, chain, special, rank, world, rows=11008, col
     x = rng.uniform(-1, 1, cols)
     lvl = be.max_level
     t0 = time.perf_counter()
-    M = be.prepare_shard(W, lvl, rank, world)
+    M = be.prepare_shard(W, lvl, rank, world, stacked=True)  # 4096 stacked diagonals split by giant group
     be.gen_rotation_keys(M.rotations())
     torch.cuda.synchronize()
     prep = time.perf_counter() - t0
     ct = be.encrypt(np.tile(x, be.slots // cols), lvl)
     allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else (lambda t: None)
     outs, rep = sharded_matvec(be, M, ct, lvl + 1, N, allreduce, torch)  # warm-up + correctness
-    y = np.concatenate([be.decrypt(o)[:cols] for o in outs])[:rows]
+    y = be.decrypt(outs[0])[:rows]  # stacked: one output, y[row] in slot row
     err = float(np.abs(y - W @ x).max())
     del outs
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -47,6 +47,9 @@ int64_t hxc_slots(hxc_backend* b);
 int hxc_max_level(hxc_backend* b);
 /* the underlying hx_ctx* (libhx_b200 C-ABI) for device-level pipelines */
 void* hxc_device_context(hxc_backend* b);
+/* release the device scratch arena and the stream-ordered pool's cached
+   memory (hx_ctx_trim); call between workloads of different shapes */
+int hxc_trim(hxc_backend* b);
 int hxc_gen_rotation_keys(hxc_backend* b, const int64_t* amounts, int count);
 
 /* encode(m, level, Delta) + encrypt; m has len <= slots entries (zero-padded) */
@@ -93,7 +96,7 @@ int hxc_matvec_tokens(hxc_backend* b, const hxc_mat* m, const hxc_ct* const* xs,
  * ranks (e.g. NCCL all-reduce of int64 = wrapping uint64 sum), reduces mod q
  * (hx_reduce_mod_q), wraps the words (hxc_ct_like) and rescales once. */
 hxc_mat* hxc_matrix_prepare_shard(hxc_backend* b, const double* A, int rows, int cols, int level,
-                                  int rank, int world);
+                                  int rank, int world, int stacked);
 int hxc_matvec_shard(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, int cap,
                      hxc_report* rep);
 /* a new ciphertext with the level / scale of `like` and words copied from the

@@ -11,6 +11,7 @@
 #include <string>
 
 #include "helix/gpu_backend.hpp"
+#include "hx_b200.h"
 #include "helix/linalg.hpp"
 
 using namespace helix;
@@ -70,6 +71,13 @@ void hxc_backend_destroy(hxc_backend* b) { delete b; }
 int64_t hxc_slots(hxc_backend* b) { return (int64_t)b->b->slots(); }
 int hxc_max_level(hxc_backend* b) { return b->b->params().max_level; }
 void* hxc_device_context(hxc_backend* b) { return b->b->device_context(); }
+
+int hxc_trim(hxc_backend* b) {
+  return guard(-1, [&] {
+    if (hx_ctx_trim((hx_ctx*)b->b->device_context()) != HX_OK) throw std::runtime_error(hx_last_error());
+    return 0;
+  });
+}
 
 int hxc_gen_rotation_keys(hxc_backend* b, const int64_t* a, int n) {
   return guard(-1, [&] {
@@ -208,13 +216,13 @@ int hxc_matvec_tokens(hxc_backend* b, const hxc_mat* m, const hxc_ct* const* xs,
 }
 
 hxc_mat* hxc_matrix_prepare_shard(hxc_backend* b, const double* A, int rows, int cols, int level, int rank,
-                                  int world) {
+                                  int world, int stacked) {
   return guard<hxc_mat*>(nullptr, [&] {
     Matrix M(rows, cols);
     std::memcpy(M.data.data(), A, sizeof(double) * (std::size_t)rows * cols);
-    const PackedMatrix P = pack_bsgs(M, b->b->slots());
+    const PackedMatrix P = stacked ? pack_bsgs_stacked(M, b->b->slots()) : pack_bsgs(M, b->b->slots());
     auto* h = new hxc_mat;
-    h->method = HXC_BSGS;
+    h->method = stacked ? HXC_BSGS_STACKED : HXC_BSGS;
     h->shard = bsgs_shard(P.plan, rank, world);
     h->m = encode_matrix(*b->b, P, level, h->shard);
     return h;

@@ -106,7 +106,8 @@ BsgsShard bsgs_shard(const BsgsPlan& plan, int rank, int world) {
 }
 
 EncodedMatrix encode_matrix(SlotOps& ops, const PackedMatrix& M, int level, const BsgsShard& shard) {
-  if (M.layout != Layout::BsgsDiagonal) throw std::invalid_argument("encode_matrix: shards apply to BSGS layouts");
+  if (M.layout != Layout::BsgsDiagonal && M.layout != Layout::BsgsStacked)
+    throw std::invalid_argument("encode_matrix: shards apply to BSGS layouts");
   PackedMatrix S = M;
   const int n1 = M.plan.n1, ge = shard.giant_end < 0 ? M.plan.n2 : shard.giant_end;
   for (int b = 0; b < M.row_blocks; ++b)

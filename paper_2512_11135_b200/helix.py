@@ -44,6 +44,7 @@ def lib():
         "hxc_slots": (i64, [v]),
         "hxc_max_level": (i32, [v]),
         "hxc_device_context": (v, [v]),
+        "hxc_trim": (i32, [v]),
         "hxc_gen_rotation_keys": (i32, [v, C.POINTER(C.c_int64), i32]),
         "hxc_encrypt": (v, [v, f64p, i32, i32]),
         "hxc_decrypt": (i32, [v, v, f64p]),
@@ -64,7 +65,7 @@ def lib():
         "hxc_matrix_rotations": (i32, [v, C.POINTER(C.c_int64), i32]),
         "hxc_matvec": (i32, [v, v, v, C.POINTER(v), i32, rp]),
         "hxc_matmul": (v, [v, v, v, i32, rp]),
-        "hxc_matrix_prepare_shard": (v, [v, f64p, i32, i32, i32, i32, i32]),
+        "hxc_matrix_prepare_shard": (v, [v, f64p, i32, i32, i32, i32, i32, i32]),
         "hxc_matvec_tokens": (i32, [v, v, C.POINTER(v), i32, C.POINTER(v), i32, rp]),
         "hxc_matvec_shard": (i32, [v, v, v, C.POINTER(v), i32, rp]),
         "hxc_ct_like": (v, [v, v, v]),
@@ -269,11 +270,13 @@ class Backend:
         cts = [Ct(self, outs[i]) for i in range(k)]
         return [cts[t * blocks:(t + 1) * blocks] for t in range(T)], r.as_dict()
 
-    def prepare_shard(self, A, level, rank, world):
-        """BSGS matrix restricted to this rank's giant groups (helix::bsgs_shard)"""
+    def prepare_shard(self, A, level, rank, world, stacked=False):
+        """BSGS (or stacked-block BSGS) matrix restricted to this rank's giant groups (helix::bsgs_shard)"""
         A = np.ascontiguousarray(A, dtype=np.float64)
         return Mat(self, self.L.hxc_matrix_prepare_shard(self.h, A.ctypes.data_as(C.POINTER(C.c_double)),
-                                                         A.shape[0], A.shape[1], level, rank, world), BSGS)
+                                                         A.shape[0], A.shape[1], level, rank, world,
+                                                         1 if stacked else 0),
+                   BSGS_STACKED if stacked else BSGS)
 
     def matvec_shard(self, mat, x):
         """pre-rescale partial outputs of this rank's giant groups"""
@@ -327,6 +330,11 @@ class Backend:
 
     def device_context(self):
         return self.L.hxc_device_context(self.h)
+
+    def trim(self):
+        """release cached device scratch (hx_ctx_trim)"""
+        if self.L.hxc_trim(self.h) != 0:
+            raise _err()
 
     def secret_key_ptr(self):
         return self.L.hxc_secret_key_ptr(self.h)

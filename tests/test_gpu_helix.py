@@ -205,16 +205,17 @@ def test_matmul_ctct(d):
     assert np.abs(out - A @ Bm).max() < 1e-3 * d
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
-def test_giant_step_shards_bit_exact(world):
+@pytest.mark.parametrize("world,stacked", [(2, False), (3, False), (4, False), (2, True), (3, True)])
+def test_giant_step_shards_bit_exact(world, stacked):
     """the G rank shards of a multi-block BSGS matvec (each rank
     its giant groups, pre-rescale partials), summed as int64 words (what the
     NCCL all-reduce does), reduced mod q on the device (hx_reduce_mod_q) and
     rescaled once, equal the single-GPU matvec word for word.  The ranks run
-    one after another on this GPU; nothing waits on another rank."""
+    one after another on this GPU; nothing waits on another rank.  Stacked:
+    the same over the stacked-block layout (one output ciphertext)."""
     import torch
 
-    from paper_2512_11135_b200.helix import BSGS
+    from paper_2512_11135_b200.helix import BSGS, BSGS_STACKED
     from paper_2512_11135_b200.shard import gather_words, reduce_partials, shard_range
 
     p, be = backend("c2s")
@@ -224,31 +225,36 @@ def test_giant_step_shards_bit_exact(world):
     x = rng.uniform(-1, 1, 256)
     lvl = 6
     nq = lvl + 1
-    M = be.prepare(BSGS, A, lvl)
+    M = be.prepare(BSGS_STACKED if stacked else BSGS, A, lvl)
     be.gen_rotation_keys(M.rotations())
     ct = be.encrypt(np.tile(x, be.slots // 256), lvl)
     ref, rep_full = be.matvec(M, ct)
+    nout = len(ref)
+    assert nout == (1 if stacked else 2)
     n2 = M.info()["n2"]
     total = None
     rots = 0
     for r in range(world):
-        Ms = be.prepare_shard(A, lvl, r, world)
+        Ms = be.prepare_shard(A, lvl, r, world, stacked=stacked)
         gb, ge = shard_range(n2, r, world)
         parts, rep = be.matvec_shard(Ms, ct)
-        assert len(parts) == 2 and rep["levels_consumed"] == 0
+        assert len(parts) == nout and rep["levels_consumed"] == 0
         rots += rep["rotations"] - (M.info()["n1"] - 1)  # baby steps are replicated per rank
         w = gather_words(parts, nq, N, torch)
         total = w if total is None else total + w  # int64 wrap == u64 sum
         like = parts
     torch.cuda.synchronize()
-    reduce_partials(be.device_context(), total, 2, nq, lambda t: None)
-    outs = [be.rescale(be.ct_like(like[i], total[i].data_ptr())) for i in range(2)]
-    for i in range(2):
+    reduce_partials(be.device_context(), total, nout, nq, lambda t: None)
+    outs = [be.rescale(be.ct_like(like[i], total[i].data_ptr())) for i in range(nout)]
+    for i in range(nout):
         got = d2h(outs[i].device_ptr(), 2 * lvl * N)
         exp = d2h(ref[i].device_ptr(), 2 * lvl * N)
         assert np.array_equal(got, exp)
     assert rots == rep_full["rotations"] - (M.info()["n1"] - 1)
-    y = np.concatenate([be.decrypt(o)[:256] for o in outs])
+    if stacked:
+        y = be.decrypt(outs[0])[:512]
+    else:
+        y = np.concatenate([be.decrypt(o)[:256] for o in outs])
     assert np.abs(y - A @ x).max() < 1e-5
 
 

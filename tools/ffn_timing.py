@@ -11,6 +11,8 @@ import bench  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--no-w2", action="store_true")
+ap.add_argument("--only", nargs="*", default=None)
+ap.add_argument("--verbose", action="store_true")
 args = ap.parse_args()
 chain, special = bench.primes()
 print(json.dumps(bench.ffn_bsgs_bench(torch, chain, special, args), indent=1))
