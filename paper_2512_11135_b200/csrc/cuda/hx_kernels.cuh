@@ -502,62 +502,100 @@ struct ModDownArgs {
   int n_q, n_chain, n_special, logn;
 };
 
+constexpr int kModDownEpt = 2;  // coefficient positions per thread
+
+// per-target constants staged in shared memory once per block: for target i,
+// [k][w, w/q, w30, w30/q] (FP64 form), then q, 1/q, [P]_q as doubles (q = 0
+// marks an integer-class target)
+inline int moddown_smem_bytes(int n_q, int K) { return 8 * n_q * (4 * K + 3); }
+
 template <int MAXK>
-__global__ void moddown_bconv_kernel(ModDownArgs A) {
+__global__ void __launch_bounds__(256) moddown_bconv_kernel(ModDownArgs A) {
+  extern __shared__ double mds[];
   const int N = 1 << A.logn;
   const long long b = blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  u64 x[MAXK];
-  int nneg = 0;
+  const int K = A.n_special, stride = 4 * K + 3;
+  for (int idx = threadIdx.x; idx < A.n_q * stride; idx += blockDim.x) {
+    const int i = idx / stride, m = idx % stride;
+    const PrimeConst& P = A.pc[i];
+    double v;
+    if (m < 4 * K)
+      v = P.f64 ? A.pconvf[((long long)(m >> 2) * A.n_chain + i) * 4 + (m & 3)] : 0.0;
+    else if (m == 4 * K)
+      v = P.f64 ? P.qd : 0.0;
+    else if (m == 4 * K + 1)
+      v = P.qinv_d;
+    else
+      v = P.f64 ? __longlong_as_double((long long)u64_to_f64bits(A.pmodq[i])) : 0.0;
+    mds[idx] = v;
+  }
+  __syncthreads();
+  const int t0 = blockIdx.x * blockDim.x * kModDownEpt + threadIdx.x;
+  u64 x[kModDownEpt][MAXK];
+  int nneg[kModDownEpt];
+  double xh[kModDownEpt][MAXK], xl[kModDownEpt][MAXK];
 #pragma unroll
-  for (int k = 0; k < MAXK; ++k) {
-    if (k < A.n_special) {
-      const PrimeConst& P = A.pc[A.n_chain + k];
-      const SC c = A.phinv[k];
-      x[k] = csub(shoup_lazy(A.sp[(b * A.n_special + k) * N + t], c.w, c.wp, P.q), P.q);
-      nneg += x[k] > (P.q >> 1);
+  for (int e = 0; e < kModDownEpt; ++e) {
+    const int t = t0 + e * blockDim.x;
+    nneg[e] = 0;
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) {
+      x[e][k] = 0;
+      xh[e][k] = xl[e][k] = 0.0;
+      if (k < K) {
+        const PrimeConst& P = A.pc[A.n_chain + k];
+        const SC c = A.phinv[k];
+        x[e][k] = csub(shoup_lazy(__ldcs(A.sp + (b * K + k) * N + t), c.w, c.wp, P.q), P.q);
+        nneg[e] += x[e][k] > (P.q >> 1);
+        // FP64 pipe for the q_i < 2^47 targets: x_k (< 2^60) as two exact 30-bit
+        // halves, v = sum_k xh_k [2^30 w_k]_q + xl_k w_k - nneg [P]_q, all exact
+        xh[e][k] = __dsub_rn(__longlong_as_double((long long)((x[e][k] >> 30) | 0x4330000000000000ull)), kTwo52);
+        xl[e][k] = __dsub_rn(__longlong_as_double((long long)((x[e][k] & 0x3FFFFFFFull) | 0x4330000000000000ull)), kTwo52);
+      }
     }
   }
   u64* cb = A.conv + b * (long long)A.n_q * N;
-  // FP64 pipe for the q_i < 2^47 targets: x_k (< 2^60) as two exact 30-bit
-  // halves, v = sum_k xh_k [2^30 w_k]_q + xl_k w_k - nneg [P]_q, all exact
-  double xh[MAXK], xl[MAXK];
-#pragma unroll
-  for (int k = 0; k < MAXK; ++k) {
-    xh[k] = xl[k] = 0.0;
-    if (k < A.n_special) {
-      xh[k] = __dsub_rn(__longlong_as_double((long long)((x[k] >> 30) | 0x4330000000000000ull)), kTwo52);
-      xl[k] = __dsub_rn(__longlong_as_double((long long)((x[k] & 0x3FFFFFFFull) | 0x4330000000000000ull)), kTwo52);
-    }
-  }
   for (int i = 0; i < A.n_q; ++i) {
-    const PrimeConst& P = A.pc[i];
-    if (P.f64) {
-      double acc = 0.0;
+    const double* cst = mds + i * stride;
+    const double qd = cst[4 * K];
+    if (qd != 0.0) {
+      const double qinv = cst[4 * K + 1], pm = cst[4 * K + 2];
+      double acc[kModDownEpt];
+#pragma unroll
+      for (int e = 0; e < kModDownEpt; ++e) acc[e] = __fma_rn(-(double)nneg[e], pm, 0.0);
 #pragma unroll
       for (int k = 0; k < MAXK; ++k) {
-        if (k < A.n_special) {
-          const double* w = A.pconvf + ((long long)k * A.n_chain + i) * 4;
-          acc = __dadd_rn(acc, mulmod_f64(xh[k], w[2], w[3], P.qd));
-          acc = __dadd_rn(acc, mulmod_f64(xl[k], w[0], w[1], P.qd));
+        if (k < K) {
+          const double w = cst[4 * k], wq = cst[4 * k + 1], w30 = cst[4 * k + 2], w30q = cst[4 * k + 3];
+#pragma unroll
+          for (int e = 0; e < kModDownEpt; ++e) {
+            acc[e] = __dadd_rn(acc[e], mulmod_f64(xh[e][k], w30, w30q, qd));
+            acc[e] = __dadd_rn(acc[e], mulmod_f64(xl[e][k], w, wq, qd));
+          }
         }
       }
-      acc = __fma_rn(-(double)nneg, __longlong_as_double((long long)u64_to_f64bits(A.pmodq[i])), acc);
-      cb[(long long)i * N + t] = f64bits_to_residue((u64)__double_as_longlong(acc), P.qd, P.qinv_d);
+#pragma unroll
+      for (int e = 0; e < kModDownEpt; ++e)
+        __stcs(cb + (long long)i * N + t0 + e * blockDim.x,
+               f64bits_to_residue((u64)__double_as_longlong(acc[e]), qd, qinv));
       continue;
     }
-    u64 v = 0;
+    const PrimeConst& P = A.pc[i];
 #pragma unroll
-    for (int k = 0; k < MAXK; ++k) {
-      if (k < A.n_special) {
-        const SC c = A.pconv[k * A.n_chain + i];
-        v = csub(v + shoup_lazy(x[k], c.w, c.wp, P.q), P.two_q);
+    for (int e = 0; e < kModDownEpt; ++e) {
+      u64 v = 0;
+#pragma unroll
+      for (int k = 0; k < MAXK; ++k) {
+        if (k < K) {
+          const SC c = A.pconv[k * A.n_chain + i];
+          v = csub(v + shoup_lazy(x[e][k], c.w, c.wp, P.q), P.two_q);
+        }
       }
+      v = csub(v, P.q);
+      const u64 pm = A.pmodq[i];
+      for (int m = 0; m < nneg[e]; ++m) v = submod(v, pm, P.q);
+      cb[(long long)i * N + t0 + e * blockDim.x] = v;
     }
-    v = csub(v, P.q);
-    const u64 pm = A.pmodq[i];
-    for (int m = 0; m < nneg; ++m) v = submod(v, pm, P.q);
-    cb[(long long)i * N + t] = v;
   }
 }
 
@@ -586,33 +624,57 @@ struct CombineArgs {
   u32 pg[64];
 };
 
-__global__ void combine_kernel(CombineArgs A) {
+constexpr int kCombineEpt = 8;  // elements per thread (amortises the per-poly setup)
+
+__global__ void __launch_bounds__(256) combine_kernel(CombineArgs A) {
   const int N = 1 << A.logn;
   const long long b = blockIdx.z;
   long long ba = b / A.add_every;
   if (A.add_period) ba %= A.add_period;
   const bool do_add = A.add && (b % A.add_every) == 0;
   const int i = blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const PrimeConst& P = A.pc[i];
   const SC c = A.pinv[i];
-  int src = t;
+  u32 g = 1;
   long long ob = b * A.out_stride;
   if (A.perm) {
     const long long q = b >> 1;
     const long long rr = q / A.per, e = q % A.per;
-    const u32 g = A.pg[rr];
-    if (g != 1) src = (int)ntt_auto_index((u32)t, g, A.logn);
+    g = A.pg[rr];
     ob = rr * A.out_rstride + e * A.out_estride + (b & 1) * (long long)A.n_q * N;
   }
-  const u64 uu = __ldg(A.u + b * A.u_stride + (long long)i * N + src);
-  const u64 cv = __ldg(A.conv + b * A.conv_stride + (long long)i * N + src);
-  u64 r = csub(shoup_lazy(uu + P.q - cv, c.w, c.wp, P.q), P.q);
-  if (do_add) {
-    const int asrc = A.perm ? src : (A.add_g == 1 ? t : (int)ntt_auto_index((u32)t, A.add_g, A.logn));
-    r = addmod(r, __ldg(A.add + ba * A.add_stride + (long long)i * N + asrc), P.q);
+  const u32 ag = A.perm ? g : A.add_g;
+  const u64* ub = A.u + b * A.u_stride + (long long)i * N;
+  const u64* cb = A.conv + b * A.conv_stride + (long long)i * N;
+  const u64* abase = do_add ? A.add + ba * A.add_stride + (long long)i * N : nullptr;
+  u64* outb = A.out + ob + (long long)i * N;
+  const double wd = __longlong_as_double((long long)u64_to_f64bits(c.w));
+  const int t0 = blockIdx.x * blockDim.x * kCombineEpt + threadIdx.x;
+  u64 uu[kCombineEpt], cv[kCombineEpt], ad[kCombineEpt];
+#pragma unroll
+  for (int k = 0; k < kCombineEpt; ++k) {  // all loads in flight first
+    const int t = t0 + k * blockDim.x;
+    const int src = g != 1 ? (int)ntt_auto_index((u32)t, g, A.logn) : t;
+    const int asrc = ag != 1 ? (int)ntt_auto_index((u32)t, ag, A.logn) : t;
+    uu[k] = __ldg(ub + src);
+    cv[k] = __ldg(cb + src);
+    ad[k] = do_add ? __ldg(abase + asrc) : 0ull;
   }
-  A.out[ob + (long long)i * N + t] = r;
+#pragma unroll
+  for (int k = 0; k < kCombineEpt; ++k) {
+    u64 r;
+    if (P.f64) {  // q < 2^47: (u - conv) P^-1 (+ add) on the FP64 pipe, exact
+      const double du = __longlong_as_double((long long)u64_to_f64bits(uu[k]));
+      const double dc = __longlong_as_double((long long)u64_to_f64bits(cv[k]));
+      double v = mulmod_f64h(__dsub_rn(du, dc), wd, P.qinv_d, P.qd);
+      v = __dadd_rn(v, __longlong_as_double((long long)u64_to_f64bits(ad[k])));  // |v| < 2q
+      r = f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);
+    } else {
+      r = csub(shoup_lazy(uu[k] + P.q - cv[k], c.w, c.wp, P.q), P.q);
+      if (do_add) r = addmod(r, ad[k], P.q);
+    }
+    __stcs(outb + t0 + k * blockDim.x, r);
+  }
 }
 
 // Rescale helper (rns_poly.cpp:144-162): from the coefficient-domain last limb

@@ -217,6 +217,8 @@ void copy2d(u64* dst, long long dpitch, const u64* src, long long spitch, long l
 
 int ew_threads(const hx_ctx* c) { return (int)std::min<long long>(256, c->N() / 2); }
 int pt_threads(const hx_ctx* c) { return (int)std::min<long long>(256, c->N()); }
+// combine_kernel: kCombineEpt elements per thread (N >= kCombineEpt)
+int combine_threads(const hx_ctx* c) { return (int)std::min<long long>(256, c->N() / hx::kCombineEpt); }
 
 template <hx::EwOp OP>
 void ew(hx_ctx* c, u64* out, const u64* a, const u64* b, long long batch, const LimbTable& lt,
@@ -515,14 +517,16 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
   M.n_chain = c->n_chain;
   M.n_special = K;
   M.logn = c->logn;
-  const int th = pt_threads(c);
-  dim3 grid((unsigned)(N / th), (unsigned)polys);
+  const int th = (int)std::min<long long>(256, N / hx::kModDownEpt);
+  dim3 grid((unsigned)(N / th / hx::kModDownEpt), (unsigned)polys);
+  const int smem = hx::moddown_smem_bytes(n_q, K);
+  HX_REQUIRE(smem <= 48 * 1024, "moddown: too many limbs for the constant stage");
   if (K <= 1)
-    hx::moddown_bconv_kernel<1><<<grid, th, 0, s>>>(M);
+    hx::moddown_bconv_kernel<1><<<grid, th, smem, s>>>(M);
   else if (K <= 4)
-    hx::moddown_bconv_kernel<4><<<grid, th, 0, s>>>(M);
+    hx::moddown_bconv_kernel<4><<<grid, th, smem, s>>>(M);
   else
-    hx::moddown_bconv_kernel<8><<<grid, th, 0, s>>>(M);
+    hx::moddown_bconv_kernel<8><<<grid, th, smem, s>>>(M);
   launched(c, "moddown_bconv_kernel");
   hx::ntt_forward(c, conv.p, polys, hx::make_table(c, n_q, 0), s);
   hx::CombineArgs C;
@@ -550,8 +554,9 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
     C.out_estride = perm->estride;
     for (std::size_t r = 0; r < perm->g.size(); ++r) C.pg[r] = (hx::u32)perm->g[r];
   }
-  dim3 g3((unsigned)(N / th), (unsigned)n_q, (unsigned)polys);
-  hx::combine_kernel<<<g3, th, 0, s>>>(C);
+  const int cth = combine_threads(c);
+  dim3 g3((unsigned)(N / cth / hx::kCombineEpt), (unsigned)n_q, (unsigned)polys);
+  hx::combine_kernel<<<g3, cth, 0, s>>>(C);
   launched(c, "combine_kernel");
 }
 
@@ -592,7 +597,9 @@ void rescale(hx_ctx* c, u64* out, const u64* in, long long polys, int n_q, cudaS
   C.add_period = 0;
   C.add_g = 1;
   C.logn = c->logn;
-  hx::combine_kernel<<<dim3((unsigned)(N / th), (unsigned)(n_q - 1), (unsigned)polys), th, 0, s>>>(C);
+  const int cth = combine_threads(c);
+  hx::combine_kernel<<<dim3((unsigned)(N / cth / hx::kCombineEpt), (unsigned)(n_q - 1), (unsigned)polys), cth, 0,
+                       s>>>(C);
   launched(c, "combine_kernel");
 }
 
