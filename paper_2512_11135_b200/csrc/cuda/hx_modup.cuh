@@ -104,6 +104,48 @@ __device__ __forceinline__ u64 bconv_word(const u64* src, int stride, int cnt, c
   }
 }
 
+// bconv of the 16 words a thread owns in the first COL group (tile elements
+// e_r = eb[r >> W] | (r mod 2^W) << lowbits), sources outer / words inner: the
+// source tests are uniform, so the 16 products of a source are independent
+// FP64 chains the scheduler interleaves (a per-word bconv_word puts a branch
+// between every product and leaves one dependent chain in flight).
+template <int WW, int MAXA, int SRC, int TILE>
+__device__ __forceinline__ void bconv_tile_f64(u64 (&x)[16], const u64* src, const int (&eb)[16 >> WW],
+                                               int lowbits, int cnt, const bool (&sf64)[MAXA],
+                                               const BconvC (&C)[MAXA], const PrimeConst& P) {
+  double acc[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+  // no `i < cnt` test: sources i >= cnt are zero tiles with zero constants
+  // (a per-source branch makes the compiler serialise the words)
+#pragma unroll
+  for (int i = 0; i < MAXA; ++i) {
+    {
+      const u64* si = src + i * TILE;
+      if (src_is_f64<SRC, MAXA>(sf64, i)) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
+          acc[r] = __dadd_rn(acc[r], mulmod_f64(__longlong_as_double((long long)si[e]), C[i].w, C[i].wq, P.qd));
+        }
+      } else {  // 60-bit source: x = xh 2^30 + xl
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
+          const u64 v = si[e];
+          const double xh = __dsub_rn(__longlong_as_double((long long)((v >> 30) | 0x4330000000000000ull)), kTwo52);
+          const double xl =
+              __dsub_rn(__longlong_as_double((long long)((v & 0x3FFFFFFFull) | 0x4330000000000000ull)), kTwo52);
+          acc[r] = __dadd_rn(acc[r], mulmod_f64(xh, C[i].w30, C[i].w30q, P.qd));
+          acc[r] = __dadd_rn(acc[r], mulmod_f64(xl, C[i].w, C[i].wq, P.qd));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r) x[r] = (u64)__double_as_longlong(acc[r]);
+}
+
 // one target limb of the tile: conversion into registers, forward COL stages,
 // store (FP64 or integer butterflies by the target's prime class)
 template <int S, int OB, bool F64, int MAXA, int SRC>
@@ -135,8 +177,10 @@ __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, c
     const int lowbits = OB + g0;                                                             \
     _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                         \
       const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                       \
-      x[r] = firstg ? bconv_word<F64, MAXA, SRC>(src + e, TILE, cnt, sf64, C, P) : sm[swz<false>(e)]; \
+      if (!(F64 && firstg)) x[r] = firstg ? bconv_word<F64, MAXA, SRC>(src + e, TILE, cnt, sf64, C, P) \
+                                          : sm[swz<false>(e)];                               \
     }                                                                                        \
+    if (F64 && firstg) bconv_tile_f64<WW, MAXA, SRC, TILE>(x, src, eb, lowbits, cnt, sf64, C, P); \
     if (F64)                                                                                 \
       ntt_group_f64<true, false, S, OB, WW>(x, jb, g0, logn, twf, nullptr, P, false);         \
     else                                                                                     \
@@ -209,6 +253,10 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
         if (sf64[i]) x = u64_to_f64bits(x);
         src[i * TILE + r * T + t] = x;
       }
+    } else {  // padding source of a short last digit: zeros (bconv_tile_f64)
+      sf64[i] = true;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) src[i * TILE + r * T + t] = 0ull;
     }
   }
   __syncthreads();
@@ -234,8 +282,12 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
     const PrimeConst P = A.pc[pj];
     BconvC C[MAXA];
 #pragma unroll
-    for (int i = 0; i < MAXA; ++i)
-      if (i < cnt) C[i] = bcd[(long long)j * A.alpha + i];
+    for (int i = 0; i < MAXA; ++i) {
+      if (i < cnt)
+        C[i] = bcd[(long long)j * A.alpha + i];
+      else
+        C[i] = BconvC{0.0, 0.0, 0.0, 0.0, 0ull, 0ull};
+    }
     u64* base = dout + (long long)j * N;
     __syncthreads();  // the previous target's last exchange reads are done
     if (mode == 0)
@@ -255,11 +307,24 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
     for (int i = 0; i < MAXA; ++i)
       if (i < cnt) C[i] = bcd[(long long)j * A.alpha + i];
     u64* base = dout + (long long)j * N;
+    u64 y[16];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const int e = r * T + t;
-      base[tile_gofs<false, S, OB>(e, tile, logn)] = csub(bconv_word<false, MAXA>(src + e, TILE, cnt, sf64, C, P), P.q);
+    for (int r = 0; r < 16; ++r) y[r] = 0;
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) {  // sources outer (uniform tests), words inner
+      if (i < cnt) {
+        const bool f = sf64[i];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          u64 v = src[i * TILE + r * T + t];
+          if (f)  // exact double -> integer
+            v = (u64)__double_as_longlong(__dadd_rn(__longlong_as_double((long long)v), kTwo52)) & 0xFFFFFFFFFFFFFull;
+          y[r] = csub(y[r] + shoup_lazy(v, C[i].sw, C[i].swp, P.q), P.two_q);
+        }
+      }
     }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) base[tile_gofs<false, S, OB>(r * T + t, tile, logn)] = csub(y[r], P.q);
   }
 }
 
