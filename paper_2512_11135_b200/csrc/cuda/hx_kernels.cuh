@@ -336,13 +336,23 @@ __global__ void __launch_bounds__(256, 2) ks_inner_f64_kernel(InnerArgs A, const
   const long long ebase = A.shared ? 0 : (long long)r * E;
   u64* ubase = A.u + (long long)r * E * 2 * ext * N;
   const int down = (A.c1 && j < A.n_q) ? j / A.alpha : -1;  // digit owning limb j
-  for (int b = b_lo; b < b_hi; ++b) {
+  // software pipeline over the batch slice: element b + 1's digit words are
+  // in flight while element b's products run (HBM latency x bandwidth needs
+  // more bytes in flight per SM than one element's 8 words per thread)
+  u64 vn[MAXD];
+  auto load = [&](int b, u64 (&v)[MAXD]) {
     const u64* Db = A.digits + (ebase + b) * dstride + (long long)j * N + src;
     const u64* Cb = down >= 0 ? A.c1 + (ebase + b) * A.c1_stride + (long long)j * N + src : nullptr;
-    u64 v[MAXD];
 #pragma unroll
     for (int d = 0; d < MAXD; ++d)
       v[d] = d < A.dnum ? __ldcs(d == down ? Cb : Db + (long long)d * ext * N) : 0ull;
+  };
+  if (b_lo < b_hi) load(b_lo, vn);
+  for (int b = b_lo; b < b_hi; ++b) {
+    u64 v[MAXD];
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) v[d] = vn[d];
+    if (b + 1 < b_hi) load(b + 1, vn);
     double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
 #pragma unroll
     for (int d = 0; d < MAXD; ++d) {
