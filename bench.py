@@ -591,6 +591,19 @@ def main():
                 "note": "traffic = 2 x algorithmic: the two-pass N = 256 x 256 split re-reads each "
                         "limb once (profiles/); DESIGN.md section 5"}
 
+    # the pipe that actually bounds the transform: FP64 (profiles/: DRAM ~50-64 %,
+    # FP64 pipe 50-70 % active).  Algorithmic FP64 lane-ops of the FP64-class
+    # limbs: 8 per butterfly (h, l, quotient x2, remainder, sum, X +- T), N/2
+    # log2 N butterflies per limb; peak = DFMA 62.6 lanes/clk/SM measured
+    # (tools/microbench/pipes.cu) x 148 SMs x the max SM clock
+    f64_limbs = 2 * BATCH * sum(1 for q in chain if q < (1 << 47))
+    f64_ops = f64_limbs * (N // 2) * LOGN * 8
+    f64_peak = 62.6 * 148 * 1965e6
+    roofline_fp64 = {"kernel": roofline["kernel"], "bound": "fp64", "achieved": f64_ops / ntt_transform_s / 1e12,
+                     "peak": f64_peak / 1e12, "unit": "T lane-op/s",
+                     "frac": f64_ops / ntt_transform_s / f64_peak, "lane_ops_per_launch": f64_ops,
+                     "peak_kind": "measured DFMA rate (62.6 lanes/clk/SM) x 148 SMs x 1965 MHz"}
+
     extras = {"limb_ntt_per_s": ntt_limbs / (ntt_secs / 3)}
     if not args.no_extras:
         # the same batch-256 key switch with 3 special primes < 2^47 (FP64 class):
@@ -716,7 +729,7 @@ def main():
                        "N": N, "chain_primes": nq, "special_primes": K, "alpha": ALPHA,
                        "batch_per_gpu": BATCH, "parallelism": f"replicas x{world}",
                        "l2": "inputs larger than L2 (6.4 GB of ciphertexts per step)"},
-            "roofline": roofline, "roofline_bsgs_mac": roofline_mac, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "roofline_fp64": roofline_fp64, "roofline_bsgs_mac": roofline_mac, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks, "extras": extras,
         }

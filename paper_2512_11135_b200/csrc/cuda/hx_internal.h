@@ -94,6 +94,8 @@ LimbTable make_table(const hx_ctx* c, int n_q, int n_p, int stride = -1, int fir
 void ntt_forward(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
 void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
 // forward ROW pass only (the COL pass done by a fused producer, hx_modup.cuh)
+void ntt_forward_combine(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, const EpiArgs& ep,
+                         cudaStream_t s);
 void ntt_forward_rows(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
 int ntt_split_a(int logn);
 

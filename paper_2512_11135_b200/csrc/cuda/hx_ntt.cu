@@ -44,6 +44,45 @@ void launch_pass(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cud
   ++c->launches;
 }
 
+template <int S, bool F64>
+void launch_row_combine(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, const EpiArgs& ep,
+                        cudaStream_t s) {
+  constexpr int OB = HX_NTT_OB;
+  constexpr int TILE = 1 << (S + OB);
+  NttArgs a;
+  a.data = data;
+  a.pc = c->d_pc;
+  a.lt = lt;
+  a.logn = c->logn;
+  a.instances = batch * lt.count;
+  a.batch = batch;
+  a.bper = 1;
+  const long long blocks = a.instances * (c->N() / TILE);
+  if (blocks <= 0) return;
+  constexpr int smem = ntt_smem_bytes<true, S, OB, F64>();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(ntt_row_combine_kernel<S, OB, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  ntt_row_combine_kernel<S, OB, F64><<<(unsigned)blocks, TILE / 16, smem, s>>>(a, ep);
+  ++c->launches;
+}
+
+template <bool F64>
+void dispatch_row_combine(hx_ctx* c, int S, u64* data, long long batch, const LimbTable& lt, const EpiArgs& ep,
+                          cudaStream_t s) {
+  switch (S) {
+    case 3: launch_row_combine<3, F64>(c, data, batch, lt, ep, s); break;
+    case 4: launch_row_combine<4, F64>(c, data, batch, lt, ep, s); break;
+    case 5: launch_row_combine<5, F64>(c, data, batch, lt, ep, s); break;
+    case 6: launch_row_combine<6, F64>(c, data, batch, lt, ep, s); break;
+    case 7: launch_row_combine<7, F64>(c, data, batch, lt, ep, s); break;
+    case 8: launch_row_combine<8, F64>(c, data, batch, lt, ep, s); break;
+    default: set_error("ntt: unsupported sub-transform size");
+  }
+}
+
 template <bool FWD, bool ROW, bool F64>
 void dispatch(hx_ctx* c, int S, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
   switch (S) {
@@ -82,6 +121,19 @@ void ntt_forward(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cud
   if (tf.count) dispatch<true, false, true>(c, a, data, batch, tf, s);
   if (ti.count) dispatch<true, true, false>(c, b, data, batch, ti, s);   // last b stages (ROW)
   if (tf.count) dispatch<true, true, true>(c, b, data, batch, tf, s);
+}
+
+// forward NTT of ModDown's converted term whose ROW pass writes the key-switch
+// combine instead of the transform (EpiArgs); `data` is left after the COL pass
+void ntt_forward_combine(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, const EpiArgs& ep,
+                         cudaStream_t s) {
+  const int a = split_a(c->logn), b = c->logn - a;
+  LimbTable ti, tf;
+  split(c, lt, ti, tf);
+  if (ti.count) dispatch<true, false, false>(c, a, data, batch, ti, s);
+  if (tf.count) dispatch<true, false, true>(c, a, data, batch, tf, s);
+  if (ti.count) dispatch_row_combine<false>(c, b, data, batch, ti, ep, s);
+  if (tf.count) dispatch_row_combine<true>(c, b, data, batch, tf, ep, s);
 }
 
 void ntt_forward_rows(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {

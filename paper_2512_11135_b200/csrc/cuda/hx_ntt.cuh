@@ -280,15 +280,101 @@ struct Sched {
   static constexpr int G = S / 4;          // number of full groups
 };
 
+// Key-switch combine fused into the last (ROW) pass of ModDown's forward NTT:
+// for poly b, limb i of the converted ModDown term v (this transform's
+// output), out = (u - v) [P^-1]_{q_i} (+ add), written at tau^-1 of the
+// coefficient index when a rotation's automorphism is fused (perm).  tau maps
+// aligned 2^j blocks of NTT indices onto aligned 2^j blocks, so a warp's 32
+// consecutive source words land in one aligned 32-word block: the permuted
+// store stays coalesced.  Same semantics as combine_kernel (hx_kernels.cuh).
+struct EpiArgs {
+  const u64* u;
+  const u64* add;  // may be null
+  u64* out;
+  const SC* pinv;  // [n_chain]
+  long long u_stride, out_stride, add_stride, add_every, add_period;
+  u32 add_g;
+  int n_q;
+  int perm, per;
+  long long out_rstride, out_estride;
+  u32 pginv[64];  // g^-1 mod 2N per rotation r (perm)
+};
+
+// combine epilogue of the forward ROW pass (see EpiArgs): the tile's
+// transformed words sit in smem (ROW swizzle, residues in [0, q)); thread t
+// handles tile words e = r T + t, i.e. coalesced runs of T.
+template <int S, int OB, bool F64>
+__device__ __forceinline__ void row_combine_epilogue(const u64* sm, int t, int tile, long long b, int i, int logn,
+                                                     const PrimeConst& P, const EpiArgs& E) {
+  constexpr int TILE = 1 << (S + OB);
+  constexpr int T = TILE / 16;
+  const long long N = 1ll << logn;
+  long long ba = b / E.add_every;
+  if (E.add_period) ba %= E.add_period;
+  const bool do_add = E.add && (b % E.add_every) == 0;
+  u32 ginv = 1;
+  long long ob = b * E.out_stride;
+  if (E.perm) {
+    const long long qq = b >> 1;
+    const long long rr = qq / E.per, e = qq % E.per;
+    ginv = E.pginv[rr];
+    ob = rr * E.out_rstride + e * E.out_estride + (b & 1) * (long long)E.n_q * N;
+  }
+  const SC c = E.pinv[i];
+  const u64* ub = E.u + b * E.u_stride + (long long)i * N;
+  const u64* abase = do_add ? E.add + ba * E.add_stride + (long long)i * N : nullptr;
+  u64* outb = E.out + ob + (long long)i * N;
+  const double wd = __longlong_as_double((long long)u64_to_f64bits(c.w));
+#pragma unroll 4
+  for (int r = 0; r < 16; ++r) {
+    const int e = r * T + t;
+    const int sidx = (tile << (S + OB)) + e;  // coefficient (NTT) index of the word
+    const u64 v = sm[swz<true>(e)];
+    // output index: tau^-1 (perm); the add operand is gathered at tau_{add_g}
+    // when no permutation is fused (combine_kernel's asrc)
+    const int oidx = ginv != 1 ? (int)ntt_auto_index((u32)sidx, ginv, logn) : sidx;
+    const int aidx = E.perm ? sidx : (E.add_g == 1 ? sidx : (int)ntt_auto_index((u32)sidx, E.add_g, logn));
+    const u64 uu = __ldcs(ub + sidx);
+    const u64 ad = do_add ? __ldg(abase + aidx) : 0ull;
+    u64 res;
+    if (F64) {
+      const double du = __longlong_as_double((long long)u64_to_f64bits(uu));
+      const double dv = __longlong_as_double((long long)u64_to_f64bits(v));
+      double w = mulmod_f64h(__dsub_rn(du, dv), wd, P.qinv_d, P.qd);
+      w = __dadd_rn(w, __longlong_as_double((long long)u64_to_f64bits(ad)));
+      res = f64bits_to_residue((u64)__double_as_longlong(w), P.qd, P.qinv_d);
+    } else {
+      res = csub(shoup_lazy(uu + P.q - v, c.w, c.wp, P.q), P.q);
+      if (do_add) res = csub(res + ad, P.q);
+    }
+    __stcs(outb + oidx, res);
+  }
+}
+
 // dynamic shared memory of a pass kernel (bytes)
 template <bool ROW, int S, int OB, bool F64>
 constexpr int ntt_smem_bytes() {
   return 8 * ((1 << (S + OB)) + ((ROW && F64) ? 17 * (1 << OB) * ((1 << S) - 1) / 16 + 16 : 0));
 }
 
+template <bool FWD, bool ROW, int S, int OB, bool F64, bool EPI>
+__device__ __forceinline__ void ntt_pass_body(const NttArgs& a, const EpiArgs* ep);
+
 template <bool FWD, bool ROW, int S, int OB, bool F64>
 __global__ void __launch_bounds__((1 << (S + OB)) / 16)
     ntt_pass_kernel(NttArgs a) {
+  ntt_pass_body<FWD, ROW, S, OB, F64, false>(a, nullptr);
+}
+
+// forward ROW pass + combine epilogue (ModDown)
+template <int S, int OB, bool F64>
+__global__ void __launch_bounds__((1 << (S + OB)) / 16)
+    ntt_row_combine_kernel(NttArgs a, EpiArgs ep) {
+  ntt_pass_body<true, true, S, OB, F64, true>(a, &ep);
+}
+
+template <bool FWD, bool ROW, int S, int OB, bool F64, bool EPI>
+__device__ __forceinline__ void ntt_pass_body(const NttArgs& a, const EpiArgs* ep) {
   constexpr int TILE = 1 << (S + OB);
   constexpr int T = TILE / 16;
   extern __shared__ u64 dyn_smem[];  // [TILE] data tile, then [kTw] staged twiddles
@@ -331,6 +417,18 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16)
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
 
+  if (EPI) {  // warm L2 with the epilogue's u (and add) tile lines while the transform runs
+    const long long N = 1ll << a.logn;
+    const int li = a.lt.off[ent];
+    const u64* ut = ep->u + bidx * ep->u_stride + (long long)li * N + ((long long)tile << (S + OB));
+    for (int l = t; l < TILE / 16; l += T) asm volatile("prefetch.global.L2 [%0];" ::"l"(ut + l * 16));
+    if (ep->add && (bidx % ep->add_every) == 0 && (ep->perm || ep->add_g == 1)) {
+      long long ba = bidx / ep->add_every;
+      if (ep->add_period) ba %= ep->add_period;
+      const u64* at = ep->add + ba * ep->add_stride + (long long)li * N + ((long long)tile << (S + OB));
+      for (int l = t; l < TILE / 16; l += T) asm volatile("prefetch.global.L2 [%0];" ::"l"(at + l * 16));
+    }
+  }
   u64 x[16];
   constexpr int NG = Sched<S>::G + (Sched<S>::R ? 1 : 0);
   // group g (in processing order) -> (g0, W)
@@ -419,10 +517,13 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16)
           sm[swz<ROW>(e)] = x[r];                                                              \
         }                                                                                      \
         __syncthreads();                                                                       \
-        _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
-          const int e = r * T + t;                                                             \
-          base[tile_gofs<ROW, S, OB>(e, tile, a.logn)] = sm[swz<ROW>(e)];                      \
-        }                                                                                      \
+        if (EPI)                                                                               \
+          row_combine_epilogue<S, OB, F64>(sm, t, tile, bidx, a.lt.off[ent], a.logn, P, *ep);  \
+        else                                                                                   \
+          _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                     \
+            const int e = r * T + t;                                                           \
+            base[tile_gofs<ROW, S, OB>(e, tile, a.logn)] = sm[swz<ROW>(e)];                    \
+          }                                                                                    \
       } else {                                                                                 \
         _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
           const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                     \

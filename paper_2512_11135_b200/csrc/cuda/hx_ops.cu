@@ -528,6 +528,41 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
   else
     hx::moddown_bconv_kernel<8><<<grid, th, smem, s>>>(M);
   launched(c, "moddown_bconv_kernel");
+  static const bool unfused = getenv("HX_MODDOWN_UNFUSED") != nullptr;
+  if (!unfused) {  // combine in the ROW pass epilogue of the conversion's NTT
+    hx::EpiArgs E{};
+    E.u = u;
+    E.add = add;
+    E.out = out;
+    E.pinv = c->d_pinv;
+    E.u_stride = u_stride;
+    E.out_stride = out_stride;
+    E.add_stride = add_stride;
+    E.add_every = add_every;
+    E.add_period = add_period;
+    E.add_g = (hx::u32)add_g;
+    E.n_q = n_q;
+    E.perm = 0;
+    if (perm) {
+      HX_REQUIRE(perm->g.size() <= 64 && add_g == 1 && add_every == 2, "fused output permutation");
+      E.perm = 1;
+      E.per = perm->per;
+      E.out_rstride = perm->rstride;
+      E.out_estride = perm->estride;
+      const u64 two_n = 2 * (u64)N;
+      for (std::size_t r = 0; r < perm->g.size(); ++r) {  // g^-1 mod 2N = g^(N-1) (g odd, |Z_2N^*| = N)
+        u64 g = perm->g[r] % two_n, inv = 1, e = (u64)N - 1;
+        while (e) {
+          if (e & 1) inv = inv * g % two_n;
+          g = g * g % two_n;
+          e >>= 1;
+        }
+        E.pginv[r] = (hx::u32)inv;
+      }
+    }
+    hx::ntt_forward_combine(c, conv.p, polys, hx::make_table(c, n_q, 0), E, s);
+    return;
+  }
   hx::ntt_forward(c, conv.p, polys, hx::make_table(c, n_q, 0), s);
   hx::CombineArgs C;
   C.u = u;
