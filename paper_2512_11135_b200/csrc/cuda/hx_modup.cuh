@@ -51,7 +51,7 @@ struct ModUpColArgs {
   // icnt[d] integer-class targets (conversion only, coefficient domain out)
   int toff[kMaxDigits], tcnt[kMaxDigits], icnt[kMaxDigits];
   int alpha, n_q, n_chain, ext, dnum, logn;
-  // target split: blockIdx.z = element * tsplit + part; part p converts the
+  // target split: blockIdx.y = element * tsplit + part; part p converts the
   // p-th share of the digit's target list (small batches still fill the GPU;
   // each part re-reads the alpha source tiles, from L2)
   int tsplit;
@@ -221,9 +221,12 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
   u64* sm = dyn_smem;            // [TILE] group exchange
   u64* src = dyn_smem + TILE;    // [alpha][TILE] x_i of the tile
   const int t = threadIdx.x;
-  const int tile = blockIdx.x, d = blockIdx.y;
-  const long long b = blockIdx.z / A.tsplit;
-  const int part = blockIdx.z % A.tsplit;
+  // digit slowest: the CTAs resident at a time run one source-class mode, so
+  // the instruction cache holds one loop body (mode 1 -- config 2's digit 0
+  // with the 60-bit q_0 -- is a larger body than mode 0)
+  const int tile = blockIdx.x, d = blockIdx.z;
+  const long long b = blockIdx.y / A.tsplit;
+  const int part = blockIdx.y % A.tsplit;
   const int logn = A.logn;
   const long long N = 1ll << logn;
   const int lo = d * A.alpha, cnt = min(A.alpha, A.n_q - lo);

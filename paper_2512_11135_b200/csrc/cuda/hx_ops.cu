@@ -259,7 +259,8 @@ void launch_modup_col_t(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, c
   int maxt = 1;
   for (int d = 0; d < A.dnum; ++d) maxt = std::max(maxt, A.tcnt[d] + A.icnt[d]);
   B.tsplit = (int)std::max(1ll, std::min<long long>(maxt, (148ll * 3 * 3 + base - 1) / base));
-  dim3 grid((unsigned)(c->N() / TILE), (unsigned)A.dnum, (unsigned)(batch * B.tsplit));
+  HX_REQUIRE(batch * B.tsplit <= 65535, "modup_col: batch too large for one launch");
+  dim3 grid((unsigned)(c->N() / TILE), (unsigned)(batch * B.tsplit), (unsigned)A.dnum);
   kern<<<grid, TILE / 16, hx::modup_col_smem_bytes(S, OB, c->alpha), s>>>(B);
   launched(c, "modup_col_kernel");
 }
