@@ -70,6 +70,13 @@ struct hx_ctx {
   hx::SC* d_phinv = nullptr;   // [K]
   hx::SC* d_pconv = nullptr;   // [K][n_chain]
   double* d_pconvf = nullptr;  // [K][n_chain][4]: FP64 form (w, w/q, [2^30 w]_q, /q)
+  // ModDown through modup_col_kernel (centred): BconvC [n_chain][K] with
+  // w = [P / p_k]_{q_j}; target lists per n_q (FP64 class first); [P]_{q_j}
+  // as double
+  hx::BconvC* d_mdbc = nullptr;
+  int* d_mdtl = nullptr;
+  std::vector<int> md_tl_off, md_tl_cnt, md_tl_icnt;
+  double* d_pmodqf = nullptr;
   hx::u64* d_pmodq = nullptr;  // [n_chain]
   hx::SC* d_pinv = nullptr;    // [n_chain]
   // Rescale constants: [l][i] for i < l
@@ -94,8 +101,10 @@ LimbTable make_table(const hx_ctx* c, int n_q, int n_p, int stride = -1, int fir
 void ntt_forward(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
 void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
 // forward ROW pass only (the COL pass done by a fused producer, hx_modup.cuh)
+// f64_col_done: the FP64-class limbs already had their COL pass (fused ModDown
+// conversion); the integer-class limbs still get theirs
 void ntt_forward_combine(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, const EpiArgs& ep,
-                         cudaStream_t s);
+                         cudaStream_t s, bool f64_col_done = false);
 void ntt_forward_rows(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
 int ntt_split_a(int logn);
 

@@ -51,6 +51,14 @@ struct ModUpColArgs {
   // icnt[d] integer-class targets (conversion only, coefficient domain out)
   int toff[kMaxDigits], tcnt[kMaxDigits], icnt[kMaxDigits];
   int alpha, n_q, n_chain, ext, dnum, logn;
+  // sources: src_n limbs per element in `coef`, digit d's limb i has prime
+  // index src_pbase + d alpha + i (ModUp: n_q, 0; ModDown: K, n_chain)
+  int src_n, src_pbase;
+  // ModDown (centred conversion, rns_poly.cpp:164-180 with K specials):
+  // subtract nneg [P]_{q_j}, nneg = #{k : x_k > p_k / 2} per word
+  int centred;
+  const double* pmf;  // [n_chain] [P]_{q_j} as double (FP64-class targets)
+  const u64* pmu;     // [n_chain] [P]_{q_j}
   // target split: blockIdx.y = element * tsplit + part; part p converts the
   // p-th share of the digit's target list (small batches still fill the GPU;
   // each part re-reads the alpha source tiles, from L2)
@@ -62,10 +70,11 @@ struct ModUpColArgs {
 // Source-class modes (fixed per digit, so a CTA runs one straight-line body and
 // the instruction cache holds one variant): 0 every source limb < 2^47,
 // 1 source 0 is the wide q_0 and the rest < 2^47 (config 2's digit 0),
-// 2 any mix (runtime test per source).
+// 2 any mix (runtime test per source), 3 every source wide (ModDown from
+// 60-bit special primes).
 template <int SRC, int MAXA>
 __device__ __forceinline__ bool src_is_f64(const bool (&sf64)[MAXA], int i) {
-  return SRC == 0 ? true : SRC == 1 ? (i != 0) : sf64[i];
+  return SRC == 0 ? true : SRC == 1 ? (i != 0) : SRC == 3 ? false : sf64[i];
 }
 
 template <bool F64, int MAXA, int SRC = 2>
@@ -109,13 +118,20 @@ __device__ __forceinline__ u64 bconv_word(const u64* src, int stride, int cnt, c
 // source tests are uniform, so the 16 products of a source are independent
 // FP64 chains the scheduler interleaves (a per-word bconv_word puts a branch
 // between every product and leaves one dependent chain in flight).
-template <int WW, int MAXA, int SRC, int TILE>
+template <int WW, int MAXA, int SRC, int TILE, bool CEN>
 __device__ __forceinline__ void bconv_tile_f64(u64 (&x)[16], const u64* src, const int (&eb)[16 >> WW],
                                                int lowbits, int cnt, const bool (&sf64)[MAXA],
-                                               const BconvC (&C)[MAXA], const PrimeConst& P) {
+                                               const BconvC (&C)[MAXA], const PrimeConst& P,
+                                               const unsigned char* nn, double pm) {
   double acc[16];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) acc[r] = 0.0;
+  for (int r = 0; r < 16; ++r) {
+    acc[r] = 0.0;
+    if (CEN) {  // - nneg [P]_q (exact: nneg <= K, [P]_q < 2^47)
+      const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
+      acc[r] = -(double)nn[e] * pm;
+    }
+  }
   // no `i < cnt` test: sources i >= cnt are zero tiles with zero constants
   // (a per-source branch makes the compiler serialise the words)
 #pragma unroll
@@ -148,10 +164,11 @@ __device__ __forceinline__ void bconv_tile_f64(u64 (&x)[16], const u64* src, con
 
 // one target limb of the tile: conversion into registers, forward COL stages,
 // store (FP64 or integer butterflies by the target's prime class)
-template <int S, int OB, bool F64, int MAXA, int SRC>
+template <int S, int OB, bool F64, int MAXA, int SRC, bool CEN = false>
 __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, const bool (&sf64)[MAXA],
                                              const BconvC (&C)[MAXA], const PrimeConst& P, u64* base,
-                                             int tile, int logn) {
+                                             int tile, int logn, const unsigned char* nn = nullptr,
+                                             double pm = 0.0) {
   constexpr int TILE = 1 << (S + OB);
   constexpr int NG = Sched<S>::G + (Sched<S>::R ? 1 : 0);
   const int t = threadIdx.x;
@@ -180,7 +197,7 @@ __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, c
       if (!(F64 && firstg)) x[r] = firstg ? bconv_word<F64, MAXA, SRC>(src + e, TILE, cnt, sf64, C, P) \
                                           : sm[swz<false>(e)];                               \
     }                                                                                        \
-    if (F64 && firstg) bconv_tile_f64<WW, MAXA, SRC, TILE>(x, src, eb, lowbits, cnt, sf64, C, P); \
+    if (F64 && firstg) bconv_tile_f64<WW, MAXA, SRC, TILE, CEN>(x, src, eb, lowbits, cnt, sf64, C, P, nn, pm); \
     if (F64)                                                                                 \
       ntt_group_f64<true, false, S, OB, WW>(x, jb, g0, logn, twf, nullptr, P, false);         \
     else                                                                                     \
@@ -213,7 +230,7 @@ __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, c
 // written in the coefficient domain for an ordinary integer NTT -- their
 // 64-bit Shoup butterflies need more registers and latency hiding than this
 // kernel's occupancy (3 CTAs of 128 threads per SM) gives them.
-template <int S, int OB, int MAXA>
+template <int S, int OB, int MAXA, bool CEN = false>
 __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup_col_kernel(ModUpColArgs A) {
   constexpr int TILE = 1 << (S + OB);
   constexpr int T = TILE / 16;
@@ -229,7 +246,7 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
   const int part = blockIdx.y % A.tsplit;
   const int logn = A.logn;
   const long long N = 1ll << logn;
-  const int lo = d * A.alpha, cnt = min(A.alpha, A.n_q - lo);
+  const int lo = d * A.alpha, cnt = min(A.alpha, A.src_n - lo);
   const int nt_all = A.tcnt[d], ni_all = A.icnt[d], tot = nt_all + ni_all;
   // this part's slice [k_lo, k_hi) of the (FP64 targets, integer targets) list
   const int k_lo = (int)((long long)tot * part / A.tsplit), k_hi = (int)((long long)tot * (part + 1) / A.tsplit);
@@ -238,12 +255,16 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
   // ---- sources: x_i = [a_i Qhat_i^-1]_{q_i} (canonical); FP64-class sources
   // stored as double bits, the wide ones as integers
   bool sf64[MAXA];
-  const u64* cb = A.coef + b * (long long)A.n_q * N;
+  const u64* cb = A.coef + b * (long long)A.src_n * N;
+  unsigned char* nn = reinterpret_cast<unsigned char*>(dyn_smem + TILE * (1 + MAXA));  // [TILE] nneg (ModDown)
+  int nneg[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) nneg[r] = 0;
 #pragma unroll
   for (int i = 0; i < MAXA; ++i) {
     sf64[i] = false;
     if (i < cnt) {
-      const PrimeConst& Q = A.pc[lo + i];
+      const PrimeConst& Q = A.pc[A.src_pbase + lo + i];
       sf64[i] = Q.f64;
       const SC h = A.qhinv[A.qh_off[d] + i];
       const u64* ci = cb + (long long)(lo + i) * N;
@@ -253,6 +274,7 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         u64 x = csub(shoup_lazy(a[r], h.w, h.wp, Q.q), Q.q);
+        if (CEN) nneg[r] += x > (Q.q >> 1);
         if (sf64[i]) x = u64_to_f64bits(x);
         src[i * TILE + r * T + t] = x;
       }
@@ -262,17 +284,22 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
       for (int r = 0; r < 16; ++r) src[i * TILE + r * T + t] = 0ull;
     }
   }
+  if (CEN) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) nn[r * T + t] = (unsigned char)nneg[r];
+  }
   __syncthreads();
   int mode = 0;  // source-class mode of this digit (see src_is_f64)
   {
-    bool all = true, first_only = cnt > 0 && !sf64[0];
+    bool all = true, none = true, first_only = cnt > 0 && !sf64[0];
 #pragma unroll
     for (int i = 0; i < MAXA; ++i)
       if (i < cnt) {
         all = all && sf64[i];
+        none = none && !sf64[i];
         if (i > 0) first_only = first_only && sf64[i];
       }
-    mode = all ? 0 : first_only ? 1 : 2;
+    mode = all ? 0 : (CEN && none) ? 3 : first_only ? 1 : 2;
   }
 
   const int* tl = A.tlist + A.toff[d];
@@ -293,12 +320,21 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
     }
     u64* base = dout + (long long)j * N;
     __syncthreads();  // the previous target's last exchange reads are done
-    if (mode == 0)
+    if (CEN) {  // ModDown
+      const double pm = A.pmf[pj];
+      if (mode == 0)
+        modup_target<S, OB, true, MAXA, 0, true>(src, sm, cnt, sf64, C, P, base, tile, logn, nn, pm);
+      else if (mode == 3)
+        modup_target<S, OB, true, MAXA, 3, true>(src, sm, cnt, sf64, C, P, base, tile, logn, nn, pm);
+      else
+        modup_target<S, OB, true, MAXA, 2, true>(src, sm, cnt, sf64, C, P, base, tile, logn, nn, pm);
+    } else if (mode == 0) {
       modup_target<S, OB, true, MAXA, 0>(src, sm, cnt, sf64, C, P, base, tile, logn);
-    else if (mode == 1)
+    } else if (mode == 1) {
       modup_target<S, OB, true, MAXA, 1>(src, sm, cnt, sf64, C, P, base, tile, logn);
-    else
+    } else {
       modup_target<S, OB, true, MAXA, 2>(src, sm, cnt, sf64, C, P, base, tile, logn);
+    }
   }
 #pragma unroll 1
   for (int k = max(k_lo, nt_all); k < k_hi; ++k) {
@@ -326,11 +362,25 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup
         }
       }
     }
+    if (CEN) {
+      const u64 pm = A.pmu[pj];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) base[tile_gofs<false, S, OB>(r * T + t, tile, logn)] = csub(y[r], P.q);
+      for (int r = 0; r < 16; ++r) {
+        u64 v = csub(y[r], P.q);
+        const int ng = nn[r * T + t];
+        for (int m = 0; m < ng; ++m) v = submod(v, pm, P.q);
+        base[tile_gofs<false, S, OB>(r * T + t, tile, logn)] = v;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) base[tile_gofs<false, S, OB>(r * T + t, tile, logn)] = csub(y[r], P.q);
+    }
   }
 }
 
-inline int modup_col_smem_bytes(int S, int OB, int alpha) { return 8 * (1 << (S + OB)) * (1 + alpha); }
+// data tile + alpha source tiles (+ the [TILE] nneg bytes of ModDown)
+inline int modup_col_smem_bytes(int S, int OB, int alpha, bool centred = false) {
+  return 8 * (1 << (S + OB)) * (1 + alpha) + (centred ? (1 << (S + OB)) : 0);
+}
 
 }  // namespace hx

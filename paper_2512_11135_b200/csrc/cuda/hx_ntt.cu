@@ -126,12 +126,12 @@ void ntt_forward(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cud
 // forward NTT of ModDown's converted term whose ROW pass writes the key-switch
 // combine instead of the transform (EpiArgs); `data` is left after the COL pass
 void ntt_forward_combine(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, const EpiArgs& ep,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool f64_col_done) {
   const int a = split_a(c->logn), b = c->logn - a;
   LimbTable ti, tf;
   split(c, lt, ti, tf);
   if (ti.count) dispatch<true, false, false>(c, a, data, batch, ti, s);
-  if (tf.count) dispatch<true, false, true>(c, a, data, batch, tf, s);
+  if (tf.count && !f64_col_done) dispatch<true, false, true>(c, a, data, batch, tf, s);
   if (ti.count) dispatch_row_combine<false>(c, b, data, batch, ti, ep, s);
   if (tf.count) dispatch_row_combine<true>(c, b, data, batch, tf, ep, s);
 }

@@ -244,13 +244,14 @@ void automorphism(hx_ctx* c, u64* out, const u64* in, long long batch, const Lim
 // ---- key-switch building blocks ----
 
 // ---- fused ModUp bconv + forward COL pass (hx_modup.cuh) ----
-template <int S, int MAXA>
+template <int S, int MAXA, bool CEN>
 void launch_modup_col_t(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, cudaStream_t s) {
   constexpr int OB = 3, TILE = 1 << (S + OB);
-  auto kern = hx::modup_col_kernel<S, OB, MAXA>;
+  auto kern = hx::modup_col_kernel<S, OB, MAXA, CEN>;
+  const int smem = hx::modup_col_smem_bytes(S, OB, MAXA, CEN);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * TILE * (1 + MAXA));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
   // enough CTAs for ~3 waves of resident CTAs even for one ciphertext
@@ -261,29 +262,36 @@ void launch_modup_col_t(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, c
   B.tsplit = (int)std::max(1ll, std::min<long long>(maxt, (148ll * 3 * 3 + base - 1) / base));
   HX_REQUIRE(batch * B.tsplit <= 65535, "modup_col: batch too large for one launch");
   dim3 grid((unsigned)(c->N() / TILE), (unsigned)(batch * B.tsplit), (unsigned)A.dnum);
-  kern<<<grid, TILE / 16, hx::modup_col_smem_bytes(S, OB, c->alpha), s>>>(B);
+  kern<<<grid, TILE / 16, smem, s>>>(B);
   launched(c, "modup_col_kernel");
 }
 
-template <int S>
+template <int S, bool CEN>
 bool launch_modup_col_a(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, cudaStream_t s) {
-  switch (c->alpha) {
-    case 1: launch_modup_col_t<S, 1>(c, A, batch, s); return true;
-    case 2: launch_modup_col_t<S, 2>(c, A, batch, s); return true;
-    case 3: launch_modup_col_t<S, 3>(c, A, batch, s); return true;
-    case 4: launch_modup_col_t<S, 4>(c, A, batch, s); return true;
+  switch (A.alpha) {
+    case 1: launch_modup_col_t<S, 1, CEN>(c, A, batch, s); return true;
+    case 2: launch_modup_col_t<S, 2, CEN>(c, A, batch, s); return true;
+    case 3: launch_modup_col_t<S, 3, CEN>(c, A, batch, s); return true;
+    case 4: launch_modup_col_t<S, 4, CEN>(c, A, batch, s); return true;
     default: return false;
   }
 }
 
-bool launch_modup_col(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, cudaStream_t s) {
+template <bool CEN>
+bool launch_modup_col_c(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, cudaStream_t s) {
   switch (hx::ntt_split_a(c->logn)) {
-    case 5: return launch_modup_col_a<5>(c, A, batch, s);
-    case 6: return launch_modup_col_a<6>(c, A, batch, s);
-    case 7: return launch_modup_col_a<7>(c, A, batch, s);
-    case 8: return launch_modup_col_a<8>(c, A, batch, s);
+    case 5: return launch_modup_col_a<5, CEN>(c, A, batch, s);
+    case 6: return launch_modup_col_a<6, CEN>(c, A, batch, s);
+    case 7: return launch_modup_col_a<7, CEN>(c, A, batch, s);
+    case 8: return launch_modup_col_a<8, CEN>(c, A, batch, s);
     default: return false;
   }
+}
+
+// A.centred selects the ModDown instantiation (its own kernel, so ModUp's
+// loop body and shared-memory footprint are untouched)
+bool launch_modup_col(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, cudaStream_t s) {
+  return A.centred ? launch_modup_col_c<true>(c, A, batch, s) : launch_modup_col_c<false>(c, A, batch, s);
 }
 
 bool modup_fused_ok(const hx_ctx* c, int n_q) {
@@ -318,6 +326,9 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
     A.ext = ext;
     A.dnum = dnum;
     A.logn = c->logn;
+    A.src_n = n_q;
+    A.src_pbase = 0;
+    A.centred = 0;
     LimbTable lt{};
     lt.stride = dnum * ext;
     for (int d = 0; d < dnum; ++d) {
@@ -506,6 +517,41 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
   DBuf sp(polys * K * N, s, c), conv(polys * n_q * N, s, c);
   copy2d(sp.p, K * N, u + (long long)n_q * N, u_stride, K * N, polys, s);
   hx::ntt_inverse(c, sp.p, polys, hx::make_table(c, 0, K), s);
+  static const bool unfused = getenv("HX_MODDOWN_UNFUSED") != nullptr;
+  static const bool col_off = getenv("HX_MODDOWN_COL_OFF") != nullptr;
+  const int sa = hx::ntt_split_a(c->logn);
+  bool col_done = false;
+  if (!unfused && !col_off && K >= 1 && K <= 4 && sa >= 5 && sa <= 8) {
+    // conversion P -> Q fused into the forward COL pass of the FP64-class
+    // targets (modup_col_kernel, centred mode); integer-class targets are
+    // written in the coefficient domain for their ordinary passes
+    hx::ModUpColArgs A{};
+    A.coef = sp.p;
+    A.out = conv.p;
+    A.pc = c->d_pc;
+    A.qhinv = c->d_phinv;
+    A.bc = c->d_mdbc;
+    A.tlist = c->d_mdtl;
+    A.qh_off[0] = 0;
+    A.bc_off[0] = 0;
+    A.toff[0] = c->md_tl_off[n_q];
+    A.tcnt[0] = c->md_tl_cnt[n_q];
+    A.icnt[0] = c->md_tl_icnt[n_q];
+    A.alpha = K;
+    A.n_q = n_q;
+    A.n_chain = c->n_chain;
+    A.ext = n_q;
+    A.dnum = 1;
+    A.logn = c->logn;
+    A.src_n = K;
+    A.src_pbase = c->n_chain;
+    A.centred = 1;
+    A.pmf = c->d_pmodqf;
+    A.pmu = c->d_pmodq;
+    HX_REQUIRE(launch_modup_col(c, A, polys, s), "moddown: fused conversion unavailable");
+    col_done = true;
+  }
+  if (!col_done) {
   hx::ModDownArgs M;
   M.sp = sp.p;
   M.conv = conv.p;
@@ -529,7 +575,7 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
   else
     hx::moddown_bconv_kernel<8><<<grid, th, smem, s>>>(M);
   launched(c, "moddown_bconv_kernel");
-  static const bool unfused = getenv("HX_MODDOWN_UNFUSED") != nullptr;
+  }
   if (!unfused) {  // combine in the ROW pass epilogue of the conversion's NTT
     hx::EpiArgs E{};
     E.u = u;
@@ -561,7 +607,7 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
         E.pginv[r] = (hx::u32)inv;
       }
     }
-    hx::ntt_forward_combine(c, conv.p, polys, hx::make_table(c, n_q, 0), E, s);
+    hx::ntt_forward_combine(c, conv.p, polys, hx::make_table(c, n_q, 0), E, s, col_done);
     return;
   }
   hx::ntt_forward(c, conv.p, polys, hx::make_table(c, n_q, 0), s);
@@ -1020,6 +1066,41 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
         }
       c->d_pconvf = upload(pf);
     }
+    {  // fused ModDown conversion + COL pass tables (modup_col_kernel, centred)
+      std::vector<hx::BconvC> mb((size_t)n_chain * n_special);
+      std::vector<double> pmf(n_chain);
+      for (int j = 0; j < n_chain; ++j) {
+        const u64 q = c->primes[j];
+        pmf[j] = (double)pmodq[j];
+        for (int k = 0; k < n_special; ++k) {
+          const SC w = pconv[(size_t)k * n_chain + j];
+          const u64 w30 = hmul(w.w, (1ull << 30) % q, q);
+          hx::BconvC& e = mb[(size_t)j * n_special + k];
+          e.w = (double)w.w;
+          e.wq = (double)w.w / (double)q;
+          e.w30 = (double)w30;
+          e.w30q = (double)w30 / (double)q;
+          e.sw = w.w;
+          e.swp = w.wp;
+        }
+      }
+      std::vector<int> tl;
+      c->md_tl_off.assign(n_chain + 1, 0);
+      c->md_tl_cnt.assign(n_chain + 1, 0);
+      c->md_tl_icnt.assign(n_chain + 1, 0);
+      for (int nq = 1; nq <= n_chain; ++nq) {
+        c->md_tl_off[nq] = (int)tl.size();
+        for (int cls = 0; cls < 2; ++cls)
+          for (int j = 0; j < nq; ++j) {
+            if ((c->f64[j] != 0) != (cls == 0)) continue;
+            tl.push_back(j);
+            ++(cls == 0 ? c->md_tl_cnt : c->md_tl_icnt)[nq];
+          }
+      }
+      c->d_mdbc = upload(mb);
+      c->d_mdtl = upload(tl);
+      c->d_pmodqf = upload(pmf);
+    }
     c->d_pinv = upload(pinv);
     // Rescale constants
     std::vector<SC> qlinv((size_t)n_chain * n_chain, SC{0, 0});
@@ -1072,7 +1153,7 @@ void hx_ctx_destroy(hx_ctx* c) {
                   (void*)c->d_pconvf,
                   (void*)c->d_pconv, (void*)c->d_pmodq, (void*)c->d_pinv, (void*)c->d_qlinv,
                   (void*)c->d_qlmod, (void*)c->d_maclimbs, (void*)c->d_kslimbs, (void*)c->d_bconv,
-                  (void*)c->d_tlist})
+                  (void*)c->d_tlist, (void*)c->d_mdbc, (void*)c->d_mdtl, (void*)c->d_pmodqf})
     if (p) cudaFree(p);
   if (c->arena.base) {
     cudaDeviceSynchronize();

@@ -17,10 +17,11 @@ def main(path):
         e = L.setdefault(d["ID"], {"name": d["Kernel Name"]})
         e[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
     hx = [v for v in L.values() if "hx::" in v["name"]]
-    # the last rotate starts after the last ntt inverse ROW pass that precedes modup_col's last launch
-    last_mc = max(i for i, v in enumerate(hx) if "modup_col" in v["name"])
-    start = max(i for i, v in enumerate(hx[:last_mc]) if "modup_col" in v["name"] or "combine" in v["name"]) + 1 \
-        if any("combine" in v["name"] for v in hx[:last_mc]) else 0
+    # the last rotate: everything after the combine (fused or not) that ends
+    # the previous key switch, i.e. the last combine before the last inner product
+    last_in = max(i for i, v in enumerate(hx) if "ks_inner" in v["name"])
+    prev = [i for i, v in enumerate(hx[:last_in]) if "combine" in v["name"]]
+    start = prev[-1] + 1 if prev else 0
     seq = hx[start:]
     tot = sum(v["gpu__time_duration.sum"] for v in seq)
     print(f"{'kernel':58s} {'ms':>7s} {'share':>6s} {'GB':>6s} {'TB/s':>5s} {'fp64%':>6s} {'issue%':>6s}")
