@@ -144,6 +144,8 @@ struct DBuf {
   bool from_arena = false;
   DBuf(size_t words, cudaStream_t st, hx_ctx* ctx = nullptr) : s(st), c(ctx), bytes(((words * 8) + 255) & ~size_t(255)) {
     if (!words) return;
+    static const bool no_arena = getenv("HX_NO_ARENA") != nullptr;  // debugging: pool allocations only
+    if (no_arena) c = nullptr;
     if (c) {
       HxArena& A = c->arena;
       if (A.stream_set && A.stream != st) {  // hand the arena over to stream st

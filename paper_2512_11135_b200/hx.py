@@ -64,6 +64,8 @@ def lib() -> C.CDLL:
         "hx_keyswitch": [v, v, v, v, i32, i32, v],
         "hx_rotate": [v, v, v, v, i32, i32, u64, v],
         "hx_rotate_hoisted": [v, v, v, C.POINTER(v), u64p, i32, i32, i32, v],
+        "hx_rotate_multi": [v, v, v, C.POINTER(v), u64p, i32, i32, v],
+        "hx_rotate_grouped": [v, v, v, C.POINTER(v), u64p, i32, i32, i32, v],
         "hx_tensor": [v, v, v, v, i32, i32, v],
         "hx_mul_relin": [v, v, v, v, v, i32, i32, v],
         "hx_bsgs_mac": [v, v, v, v, i32, i32, i32, i32, v],
@@ -209,6 +211,21 @@ class Context:
         ga = (C.c_uint64 * R)(*gs)
         _check(self.L.hx_rotate_hoisted(self.h, _p(out), _p(ct), kp, ga, R, batch, n_q, _stream(stream)),
                "hx_rotate_hoisted")
+
+    def rotate_multi(self, out, ct, keys, gs, n_q, stream=None):
+        """ciphertext b rotated with its own key keys[b] / Galois element gs[b]"""
+        B = len(keys)
+        kp = (C.c_void_p * B)(*[_p(k) for k in keys])
+        ga = (C.c_uint64 * B)(*gs)
+        _check(self.L.hx_rotate_multi(self.h, _p(out), _p(ct), kp, ga, B, n_q, _stream(stream)), "hx_rotate_multi")
+
+    def rotate_grouped(self, out, ct, keys, gs, E, n_q, stream=None):
+        """group r (E ciphertexts) rotated with keys[r] / gs[r]"""
+        R = len(keys)
+        kp = (C.c_void_p * R)(*[_p(k) for k in keys])
+        ga = (C.c_uint64 * R)(*gs)
+        _check(self.L.hx_rotate_grouped(self.h, _p(out), _p(ct), kp, ga, R, E, n_q, _stream(stream)),
+               "hx_rotate_grouped")
 
     def tensor(self, out3, a, b, batch, n_q, stream=None):
         _check(self.L.hx_tensor(self.h, _p(out3), _p(a), _p(b), batch, n_q, _stream(stream)), "hx_tensor")

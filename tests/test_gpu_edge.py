@@ -159,3 +159,58 @@ def test_bsgs_more_than_64_baby_steps():
         assert np.abs(be.decrypt(outs[0]) - B @ x).max() < 1e-4
         assert rep["rotations"] == 127 + 63 or prune
     be.close()
+
+
+@pytest.mark.parametrize("cfg", ["toy", "c2"])
+def test_batched_rotation_paths_agree_and_repeat(cfg):
+    """hx_rotate (one key over a batch), hx_rotate_multi (a key per
+    ciphertext) and hx_rotate_grouped (a key per group) are the same key
+    switch launched with different grid shapes (E = batch / E = 1 per key):
+    their words must agree, and repeated calls must return identical words --
+    a cross-CTA race in an in-place pass shows up here as a few differing
+    tiles of the last ciphertexts (a packed-digit experiment failed exactly
+    so, only at batch >= 15)."""
+    import torch
+
+    from paper_2512_11135_b200 import Context
+
+    if cfg == "toy":  # alpha = 1, dnum = n_q (FP64-class specials)
+        from oracle_bindings import find_ntt_primes
+
+        logn = 12
+        n = 1 << logn
+        chain = find_ntt_primes(1 << 34, 1, 2 * n) + find_ntt_primes(1 << 30, 8, 2 * n)
+        special = find_ntt_primes(1 << 36, 1, 2 * n)
+        alpha = 1
+    else:
+        p = config2(12, 12)
+        logn, chain, special, alpha = p["logn"], p["chain"], p["special"], p["alpha"]
+    n = 1 << logn
+    ctx = Context(logn, chain, special, alpha)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7)
+    nq = len(chain) - 1
+    ext = nq + len(special)
+    g = pow(5, 3, 2 * n)
+    # a structurally valid rotation-layout key (values uniform): the paths
+    # must agree word for word whatever the key is
+    full = len(chain) + len(special)
+    dmax = ctx.key_words() // (2 * full * n)  # key layout [dnum_max][2][full][N]
+    key = torch.zeros((dmax, 2, full, n), dtype=torch.int64, device="cuda")
+    for k, q in enumerate(list(chain) + list(special)):
+        key[:, :, k, :] = torch.randint(0, q, (dmax, 2, n), generator=gen, device="cuda")
+    del ext
+    for B in (1, 3, 15, 16):
+        cts = torch.empty((B, 2, nq, n), dtype=torch.int64, device="cuda")
+        for k, q in enumerate(chain[:nq]):
+            cts[:, :, k, :] = torch.randint(0, q, (B, 2, n), generator=gen, device="cuda")
+        outs = []
+        for rep in range(2):
+            o1, o2, o3 = (torch.empty_like(cts) for _ in range(3))
+            ctx.rotate(o1, cts, key, B, nq, g)
+            ctx.rotate_multi(o2, cts, [key] * B, [g] * B, nq)
+            ctx.rotate_grouped(o3, cts, [key], [g], B, nq)
+            torch.cuda.synchronize()
+            assert torch.equal(o1, o2) and torch.equal(o1, o3), (cfg, B, rep)
+            outs.append(o1.clone())
+        assert torch.equal(outs[0], outs[1]), (cfg, B)
