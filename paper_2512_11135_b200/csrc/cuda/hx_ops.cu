@@ -23,6 +23,7 @@
 #include "hx_internal.h"
 #include "hx_kernels.cuh"
 #include "hx_modup.cuh"
+#include "hx_rowinner.cuh"
 
 using hx::LimbTable;
 using hx::PrimeConst;
@@ -305,8 +306,11 @@ bool modup_fused_ok(const hx_ctx* c, int n_q) {
 // c1: [batch] polys of n_q limbs at stride c1_stride words.
 // copy_own = false: the digits' own limbs are left out of `digits` (the key
 // inner product reads them from c1, InnerArgs::c1)
+// defer_rows: the FP64-class limbs are left after their COL pass (the fused
+// ROW + inner-product kernel finishes them, ks_inner_multi rows_deferred);
+// only valid when modup_fused_ok
 void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long batch, int n_q,
-           cudaStream_t s, bool copy_own = true) {
+           cudaStream_t s, bool copy_own = true, bool defer_rows = false) {
   const long long N = c->N();
   const int K = c->n_special, ext = n_q + K, dnum = c->dnum(n_q);
   DBuf coef(batch * n_q * N, s, c);
@@ -366,9 +370,10 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
       ++x.count;
     }
     if (li.count) hx::ntt_forward(c, digits, batch, li, s);
-    if (lf.count) hx::ntt_forward_rows(c, digits, batch, lf, s);
+    if (lf.count && !defer_rows) hx::ntt_forward_rows(c, digits, batch, lf, s);
     return;
   }
+  HX_REQUIRE(!defer_rows, "modup: deferred ROW pass needs the fused path");
   // basis conversion per digit (coefficient domain), own limbs copied (NTT)
   LimbTable lt{};
   lt.stride = dnum * ext;
@@ -418,9 +423,47 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
 //   shared: keys[r] applies to digit elements 0..E-1 (hoisting);
 //   !shared: keys[r] applies to digit elements r E .. r E + E - 1.
 // Output element (r, e) at u + (r E + e) 2 ext N.
+template <int S>
+void launch_row_inner_t(hx_ctx* c, const hx::RowInnerArgs& A, cudaStream_t s) {
+  constexpr int OB = 3, TILE = 1 << (S + OB);  // the ROW tile of hx_ntt.cu (HX_NTT_OB)
+  auto kern = hx::ks_row_inner_f64_kernel<S, OB, 8>;
+  constexpr int smem = hx::ntt_smem_bytes<true, S, OB, true>();
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  const long long blocks = (long long)A.batch * (c->N() / TILE) * A.n_limbs;
+  if (blocks <= 0) return;
+  kern<<<(unsigned)blocks, TILE / 16, smem, s>>>(A);
+  launched(c, "ks_row_inner_f64_kernel");
+}
+
+void launch_row_inner(hx_ctx* c, const hx::RowInnerArgs& A, cudaStream_t s) {
+  switch (c->logn - hx::ntt_split_a(c->logn)) {
+    case 3: launch_row_inner_t<3>(c, A, s); break;
+    case 4: launch_row_inner_t<4>(c, A, s); break;
+    case 5: launch_row_inner_t<5>(c, A, s); break;
+    case 6: launch_row_inner_t<6>(c, A, s); break;
+    case 7: launch_row_inner_t<7>(c, A, s); break;
+    case 8: launch_row_inner_t<8>(c, A, s); break;
+    default: throw std::runtime_error("row_inner: unsupported sub-transform size");
+  }
+}
+
+// The fused ModUp ROW pass + key inner product applies to one uncompressed
+// key on the FP64-class limbs (hx_rowinner.cuh); HX_ROWINNER_OFF=1 disables it.
+bool row_inner_ok(const hx_ctx* c, int n_q, const u64* key) {
+  static const bool off = getenv("HX_ROWINNER_OFF") && atoi(getenv("HX_ROWINNER_OFF")) != 0;
+  return !off && modup_fused_ok(c, n_q) && c->dnum(n_q) <= 8 && c->ks_nf64[n_q] > 0 &&
+         c->ckeys.find(key) == c->ckeys.end();
+}
+
+// rows_deferred: `digits` holds the FP64-class ModUp limbs after their COL
+// pass only (modup defer_rows); one key, identity g, own limbs from c1.
 void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<const u64*>& keys,
                     bool shared, long long E, int n_q, u64 g, cudaStream_t s, const u64* c1 = nullptr,
-                    long long c1_stride = 0) {
+                    long long c1_stride = 0, bool rows_deferred = false) {
   HX_REQUIRE(!keys.empty() && (int)keys.size() <= hx::kMaxKeys, "ks_inner: 1..64 keys per launch");
   hx::InnerArgs A;
   A.digits = digits;
@@ -463,7 +506,27 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
   const int ni = A.dnum <= 8 ? c->ks_nint[n_q] : n_q + c->n_special;
   const int* il = A.dnum <= 8 ? lists + c->n_total() : nullptr;
   static const bool one_off = getenv("HX_KS_ONE") && atoi(getenv("HX_KS_ONE")) == 0;
-  if (nf > 0 && E <= 2 && !one_off) {  // no key reuse across elements: one element per block row
+  if (rows_deferred) {
+    HX_REQUIRE(A.n_keys == 1 && A.cmask == 0 && g == 1 && c1 && A.dnum <= 8 && nf > 0,
+               "ks_inner: deferred ROW pass needs one uncompressed key, g = 1, own limbs from c1");
+    hx::RowInnerArgs R;
+    R.digits = digits;
+    R.c1 = c1;
+    R.c1_stride = c1_stride;
+    R.key = keys[0];
+    R.u = u;
+    R.pc = c->d_pc;
+    R.limbs = lists;
+    R.n_limbs = nf;
+    R.n_q = n_q;
+    R.n_chain = c->n_chain;
+    R.n_special = c->n_special;
+    R.dnum = A.dnum;
+    R.alpha = c->alpha;
+    R.batch = (int)E;
+    R.logn = c->logn;
+    launch_row_inner(c, R, s);
+  } else if (nf > 0 && E <= 2 && !one_off) {  // no key reuse across elements: one element per block row
     dim3 grid((unsigned)(c->N() / th), (unsigned)nf, (unsigned)(A.n_keys * E));
     if (A.dnum <= 4)
       hx::ks_inner_f64_one_kernel<4><<<grid, th, 0, s>>>(A, lists);
@@ -495,8 +558,9 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
 }
 
 void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long batch, int n_q,
-              u64 g, cudaStream_t s, const u64* c1 = nullptr, long long c1_stride = 0) {
-  ks_inner_multi(c, u, digits, {key}, true, batch, n_q, g, s, c1, c1_stride);
+              u64 g, cudaStream_t s, const u64* c1 = nullptr, long long c1_stride = 0,
+              bool rows_deferred = false) {
+  ks_inner_multi(c, u, digits, {key}, true, batch, n_q, g, s, c1, c1_stride, rows_deferred);
 }
 
 // Centred ModDown of `polys` PQ-basis polys u (stride u_stride words) into
@@ -720,8 +784,10 @@ u64 galois_inverse(u64 g, u64 two_n) {
 // output), one permutation launch (per 64 keys).
 void rotate_batch_from_digits(hx_ctx* c, u64* out, const u64* in, const u64* digits,
                               const std::vector<const u64*>& keys, const std::vector<u64>& galois,
-                              bool shared, long long E, int n_q, cudaStream_t s) {
+                              bool shared, long long E, int n_q, cudaStream_t s,
+                              bool rows_deferred = false) {
   const long long N = c->N(), ct = 2ll * n_q * N;
+  HX_REQUIRE(!rows_deferred || keys.size() == 1, "rotate: deferred ROW pass needs one key");
   const int ext = n_q + c->n_special;
   const long long R = (long long)keys.size();
   const long long dstride = (long long)c->dnum(n_q) * ext * N;
@@ -731,7 +797,7 @@ void rotate_batch_from_digits(hx_ctx* c, u64* out, const u64* in, const u64* dig
     const std::vector<const u64*> kk(keys.begin() + r0, keys.begin() + r0 + nr);
     const u64* dg = shared ? digits : digits + r0 * E * dstride;
     const u64* c1 = (shared ? in : in + r0 * E * ct) + (long long)n_q * N;  // own limbs (not copied by ModUp)
-    ks_inner_multi(c, U.p + r0 * E * 2 * ext * N, dg, kk, shared, E, n_q, 1, s, c1, ct);
+    ks_inner_multi(c, U.p + r0 * E * 2 * ext * N, dg, kk, shared, E, n_q, 1, s, c1, ct, rows_deferred);
   }
   // polys p = (r E + e) 2 + c; the c0 polys add input ct (shared ? e : r E + e);
   // the output automorphism tau_{g_r} is fused into the combine (64 keys per call)
@@ -1357,8 +1423,9 @@ int hx_keyswitch(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* k
     const long long N = c->N();
     const int ext = n_q + c->n_special;
     DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s), c), U((long long)batch * 2 * ext * N, S(s), c);
-    modup(c, D.p, (const u64*)in, (long long)n_q * N, batch, n_q, S(s), false);
-    ks_inner(c, U.p, D.p, (const u64*)key, batch, n_q, 1, S(s), (const u64*)in, (long long)n_q * N);
+    const bool fuse = row_inner_ok(c, n_q, (const u64*)key);
+    modup(c, D.p, (const u64*)in, (long long)n_q * N, batch, n_q, S(s), false, fuse);
+    ks_inner(c, U.p, D.p, (const u64*)key, batch, n_q, 1, S(s), (const u64*)in, (long long)n_q * N, fuse);
     moddown(c, (u64*)out, (long long)n_q * N, U.p, (long long)ext * N, 2ll * batch, n_q, nullptr,
             0, 1, S(s));
   });
@@ -1375,9 +1442,10 @@ int hx_rotate(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t* key,
     const long long N = c->N();
     const int ext = n_q + c->n_special;
     DBuf D((long long)batch * c->dnum(n_q) * ext * N, S(s), c);
-    modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s), false);
+    const bool fuse = row_inner_ok(c, n_q, (const u64*)key);
+    modup(c, D.p, (const u64*)in + (long long)n_q * N, 2ll * n_q * N, batch, n_q, S(s), false, fuse);
     rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, {(const u64*)key}, {g}, true, batch,
-                             n_q, S(s));
+                             n_q, S(s), fuse);
   });
 }
 
@@ -1486,8 +1554,9 @@ int hx_mul_relin(hx_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b,
     hx::tensor_kernel<<<dim3((unsigned)(N / th), (unsigned)n_q, (unsigned)batch), th, 0, S(s)>>>(
         d3.p, (const u64*)a, (const u64*)b, c->d_pc, n_q, c->logn);
     launched(c, "tensor_kernel");
-    modup(c, D.p, d3.p + 2 * L, 3 * L, batch, n_q, S(s), false);
-    ks_inner(c, U.p, D.p, (const u64*)rlk, batch, n_q, 1, S(s), d3.p + 2 * L, 3 * L);
+    const bool fuse = row_inner_ok(c, n_q, (const u64*)rlk);
+    modup(c, D.p, d3.p + 2 * L, 3 * L, batch, n_q, S(s), false, fuse);
+    ks_inner(c, U.p, D.p, (const u64*)rlk, batch, n_q, 1, S(s), d3.p + 2 * L, 3 * L, fuse);
     moddown(c, (u64*)out, 2 * L, U.p, 2ll * ext * N, batch, n_q, d3.p, 3 * L, 1, S(s));
     moddown(c, (u64*)out + L, 2 * L, U.p + (long long)ext * N, 2ll * ext * N, batch, n_q,
             d3.p + L, 3 * L, 1, S(s));

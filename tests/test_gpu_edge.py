@@ -161,7 +161,7 @@ def test_bsgs_more_than_64_baby_steps():
     be.close()
 
 
-@pytest.mark.parametrize("cfg", ["toy", "c2"])
+@pytest.mark.parametrize("cfg", ["toy", "c2", "c2n16"])
 def test_batched_rotation_paths_agree_and_repeat(cfg):
     """hx_rotate (one key over a batch), hx_rotate_multi (a key per
     ciphertext) and hx_rotate_grouped (a key per group) are the same key
@@ -169,7 +169,9 @@ def test_batched_rotation_paths_agree_and_repeat(cfg):
     their words must agree, and repeated calls must return identical words --
     a cross-CTA race in an in-place pass shows up here as a few differing
     tiles of the last ciphertexts (a packed-digit experiment failed exactly
-    so, only at batch >= 15)."""
+    so, only at batch >= 15).  hx_rotate takes the fused ROW-pass + key
+    inner-product kernel (one key), the other two the separate ROW pass and
+    inner-product kernels: "c2n16" checks the N = 2^16 tile shape of both."""
     import torch
 
     from paper_2512_11135_b200 import Context
@@ -182,6 +184,9 @@ def test_batched_rotation_paths_agree_and_repeat(cfg):
         chain = find_ntt_primes(1 << 34, 1, 2 * n) + find_ntt_primes(1 << 30, 8, 2 * n)
         special = find_ntt_primes(1 << 36, 1, 2 * n)
         alpha = 1
+    elif cfg == "c2n16":
+        p = config2(16, 24)
+        logn, chain, special, alpha = p["logn"], p["chain"], p["special"], p["alpha"]
     else:
         p = config2(12, 12)
         logn, chain, special, alpha = p["logn"], p["chain"], p["special"], p["alpha"]
@@ -200,7 +205,7 @@ def test_batched_rotation_paths_agree_and_repeat(cfg):
     for k, q in enumerate(list(chain) + list(special)):
         key[:, :, k, :] = torch.randint(0, q, (dmax, 2, n), generator=gen, device="cuda")
     del ext
-    for B in (1, 3, 15, 16):
+    for B in ((1, 3) if cfg == "c2n16" else (1, 3, 15, 16)):
         cts = torch.empty((B, 2, nq, n), dtype=torch.int64, device="cuda")
         for k, q in enumerate(chain[:nq]):
             cts[:, :, k, :] = torch.randint(0, q, (B, 2, n), generator=gen, device="cuda")
