@@ -453,14 +453,20 @@ void launch_row_inner(hx_ctx* c, const hx::RowInnerArgs& A, cudaStream_t s) {
 
 // The fused ModUp ROW pass + key inner product applies to one uncompressed
 // key on the FP64-class limbs (hx_rowinner.cuh); HX_ROWINNER_OFF=1 disables it.
-bool row_inner_ok(const hx_ctx* c, int n_q, const u64* key) {
+bool row_inner_ok(const hx_ctx* c, int n_q, const std::vector<const u64*>& keys) {
   static const bool off = getenv("HX_ROWINNER_OFF") && atoi(getenv("HX_ROWINNER_OFF")) != 0;
-  return !off && modup_fused_ok(c, n_q) && c->dnum(n_q) <= 8 && c->ks_nf64[n_q] > 0 &&
-         c->ckeys.find(key) == c->ckeys.end();
+  if (off || !modup_fused_ok(c, n_q) || c->dnum(n_q) > 8 || c->ks_nf64[n_q] == 0) return false;
+  for (const u64* k : keys)
+    if (c->ckeys.find(k) != c->ckeys.end()) return false;
+  return true;
+}
+bool row_inner_ok(const hx_ctx* c, int n_q, const u64* key) {
+  return row_inner_ok(c, n_q, std::vector<const u64*>{key});
 }
 
 // rows_deferred: `digits` holds the FP64-class ModUp limbs after their COL
-// pass only (modup defer_rows); one key, identity g, own limbs from c1.
+// pass only (modup defer_rows); one key over the batch or one key per E
+// elements (!shared), uncompressed keys, identity g, own limbs from c1.
 void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<const u64*>& keys,
                     bool shared, long long E, int n_q, u64 g, cudaStream_t s, const u64* c1 = nullptr,
                     long long c1_stride = 0, bool rows_deferred = false) {
@@ -507,13 +513,15 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
   const int* il = A.dnum <= 8 ? lists + c->n_total() : nullptr;
   static const bool one_off = getenv("HX_KS_ONE") && atoi(getenv("HX_KS_ONE")) == 0;
   if (rows_deferred) {
-    HX_REQUIRE(A.n_keys == 1 && A.cmask == 0 && g == 1 && c1 && A.dnum <= 8 && nf > 0,
-               "ks_inner: deferred ROW pass needs one uncompressed key, g = 1, own limbs from c1");
+    static_assert(hx::kRowInnerMaxKeys == hx::kMaxKeys, "key table sizes");
+    HX_REQUIRE((A.n_keys == 1 || !shared) && A.cmask == 0 && g == 1 && c1 && A.dnum <= 8 && nf > 0,
+               "ks_inner: deferred ROW pass needs unshared uncompressed keys, g = 1, own limbs from c1");
     hx::RowInnerArgs R;
     R.digits = digits;
     R.c1 = c1;
     R.c1_stride = c1_stride;
-    R.key = keys[0];
+    for (int r = 0; r < A.n_keys; ++r) R.keys[r] = keys[r];
+    R.per_key = (int)E;
     R.u = u;
     R.pc = c->d_pc;
     R.limbs = lists;
@@ -523,7 +531,7 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
     R.n_special = c->n_special;
     R.dnum = A.dnum;
     R.alpha = c->alpha;
-    R.batch = (int)E;
+    R.batch = (int)(E * (shared ? 1 : A.n_keys));
     R.logn = c->logn;
     launch_row_inner(c, R, s);
   } else if (nf > 0 && E <= 2 && !one_off) {  // no key reuse across elements: one element per block row
@@ -787,7 +795,7 @@ void rotate_batch_from_digits(hx_ctx* c, u64* out, const u64* in, const u64* dig
                               bool shared, long long E, int n_q, cudaStream_t s,
                               bool rows_deferred = false) {
   const long long N = c->N(), ct = 2ll * n_q * N;
-  HX_REQUIRE(!rows_deferred || keys.size() == 1, "rotate: deferred ROW pass needs one key");
+  HX_REQUIRE(!rows_deferred || !shared || keys.size() == 1, "rotate: deferred ROW pass with shared digits needs one key");
   const int ext = n_q + c->n_special;
   const long long R = (long long)keys.size();
   const long long dstride = (long long)c->dnum(n_q) * ext * N;
@@ -1483,14 +1491,15 @@ int hx_rotate_multi(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64_t
     for (int b = 0; b < batch; ++b)
       HX_REQUIRE((galois[b] & 1) && galois[b] < 2 * (u64)N, "galois element");
     DBuf D((long long)batch * dstride, S(s), c);
-    modup(c, D.p, (const u64*)in + (long long)n_q * N, ct, batch, n_q, S(s), false);
     std::vector<const u64*> kk;
     std::vector<u64> gg;
     for (int b = 0; b < batch; ++b) {
       kk.push_back((const u64*)keys[b]);
       gg.push_back((u64)galois[b]);
     }
-    rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, kk, gg, false, 1, n_q, S(s));
+    const bool fuse = batch > 0 && row_inner_ok(c, n_q, kk);
+    modup(c, D.p, (const u64*)in + (long long)n_q * N, ct, batch, n_q, S(s), false, fuse);
+    rotate_batch_from_digits(c, (u64*)out, (const u64*)in, D.p, kk, gg, false, 1, n_q, S(s), fuse);
   });
 }
 
@@ -1519,10 +1528,12 @@ int hx_rotate_grouped(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
       const int nr = std::min(Rc, R - r0);
       const u64* ip = (const u64*)in + (long long)r0 * E * ct;
       DBuf D((long long)nr * E * c->dnum(n_q) * ext * N, S(s), c);
-      modup(c, D.p, ip + (long long)n_q * N, ct, (long long)nr * E, n_q, S(s), false);
       const std::vector<const u64*> kc(kk.begin() + r0, kk.begin() + r0 + nr);
       const std::vector<u64> gc(gg.begin() + r0, gg.begin() + r0 + nr);
-      rotate_batch_from_digits(c, (u64*)out + (long long)r0 * E * ct, ip, D.p, kc, gc, false, E, n_q, S(s));
+      const bool fuse = row_inner_ok(c, n_q, kc);
+      modup(c, D.p, ip + (long long)n_q * N, ct, (long long)nr * E, n_q, S(s), false, fuse);
+      rotate_batch_from_digits(c, (u64*)out + (long long)r0 * E * ct, ip, D.p, kc, gc, false, E, n_q, S(s),
+                               fuse);
     }
   });
 }

@@ -1,5 +1,5 @@
 // hx_rowinner.cuh -- ModUp's last (ROW) NTT pass fused with the key inner
-// product, FP64-class limbs, one rotation / relinearisation key.
+// product, FP64-class limbs, one uncompressed key per group of elements.
 //
 // Replaces, for every FP64-class extended limb j of a key switch,
 //   ntt_pass_kernel<FWD, ROW, ..., F64>  on the 8 ModUp digits of limb j
@@ -31,11 +31,17 @@
 
 namespace hx {
 
+constexpr int kRowInnerMaxKeys = 64;
+
 struct RowInnerArgs {
   const u64* digits;  // [E][dnum][ext][N]: COL-pass output (FP64 bits) of the ModUp limbs
   const u64* c1;      // own limbs, NTT form residues: element e limb j at c1 + e c1_stride + j N
   long long c1_stride;
-  const u64* key;     // [dnum][2][full][N]
+  // element b uses keys[b / per_key] ([dnum][2][full][N]): one key over the
+  // whole batch, or R keys of per_key consecutive elements each (grouped
+  // rotations); the elements of one key run back to back along the grid
+  const u64* keys[kRowInnerMaxKeys];
+  int per_key;
   u64* u;             // [E][2][ext][N]
   const PrimeConst* pc;
   const int* limbs;   // FP64-class extended limbs j (blockIdx order)
@@ -86,7 +92,7 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, 3) ks_row_inner_f64_kern
   const u64* Db = A.digits + (long long)b * dstride + (long long)j * N + tofs;
   const int down = j < A.n_q ? j / A.alpha : -1;
   const u64* Cb = A.c1 + (long long)b * A.c1_stride + (long long)j * N + tofs;
-  const u64* K0 = A.key + (long long)kl * N + tofs;  // digit d, poly c at + (d 2 + c) full N
+  const u64* K0 = A.keys[b / A.per_key] + (long long)kl * N + tofs;  // digit d, poly c at + (d 2 + c) full N
 
   double acc0[16], acc1[16];
 #pragma unroll
