@@ -16,10 +16,13 @@
 // overlaps the NTT's.  The ROW pass of those limbs is the ordinary ROW launch.
 //
 // Exactness: FP64-class targets (p < 2^47): x_i < 2^47 sources enter as exact
-// doubles, the 60-bit q_0 source as x = xh 2^30 + xl (two exact doubles, the
-// constant [2^30 Qhat_i]_p precomputed), each product by mulmod_f64 (exact),
-// the sum kept lazily in (-(alpha+1) p, (alpha+1) p): the forward FP64 NTT
-// grows values by < p per stage, so |v| < (alpha + 1 + logn) p < 2^52.  Integer
+// doubles, each product by mulmod_f64 (exact); a 60-bit source (q_0, the
+// ModDown specials) either by an integer Shoup product in [0, 2p) converted
+// exactly (HX_WIDE_INT, every third wide source: all of them on the integer
+// pipe measured slower, 5.23 vs 5.05 ms for ModDown's conversion) or as
+// x = xh 2^30 + xl, two exact doubles and the constant [2^30 Qhat_i]_p; the sum kept lazily in (-(2 alpha + K) p,
+// 2 alpha p): the forward FP64 NTT grows values by < p per stage, so
+// |v| < (2 alpha + K + logn) p < 2^52 and |v w| < 2^99.  Integer
 // targets (60-bit q_0 and special primes): Shoup products, sum in [0, 2p).
 #pragma once
 
@@ -118,6 +121,14 @@ __device__ __forceinline__ u64 bconv_word(const u64* src, int stride, int cnt, c
 // source tests are uniform, so the 16 products of a source are independent
 // FP64 chains the scheduler interleaves (a per-word bconv_word puts a branch
 // between every product and leaves one dependent chain in flight).
+#ifndef HX_WIDE_INT
+#define HX_WIDE_INT 1
+#endif
+constexpr bool kWideInt = HX_WIDE_INT != 0;
+#ifndef HX_MODUP_MINB
+#define HX_MODUP_MINB 3
+#endif
+
 template <int WW, int MAXA, int SRC, int TILE, bool CEN>
 __device__ __forceinline__ void bconv_tile_f64(u64 (&x)[16], const u64* src, const int (&eb)[16 >> WW],
                                                int lowbits, int cnt, const bool (&sf64)[MAXA],
@@ -143,6 +154,16 @@ __device__ __forceinline__ void bconv_tile_f64(u64 (&x)[16], const u64* src, con
         for (int r = 0; r < 16; ++r) {
           const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
           acc[r] = __dadd_rn(acc[r], mulmod_f64(__longlong_as_double((long long)si[e]), C[i].w, C[i].wq, P.qd));
+        }
+      } else if (kWideInt && i % 3 == 0) {  // one wide source in three: the pipes balance
+        // 60-bit source on the integer pipe (idle in this FP64-bound kernel):
+        // Shoup product [x w]_p in [0, 2p), exact in a double (p < 2^47) --
+        // 2 FP64 ops instead of the two 30-bit-half mulmods' 16
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
+          const u64 y = shoup_lazy(si[e], C[i].sw, C[i].swp, P.q);
+          acc[r] = __dadd_rn(acc[r], __longlong_as_double((long long)u64_to_f64bits(y)));
         }
       } else {  // 60-bit source: x = xh 2^30 + xl
 #pragma unroll
@@ -231,7 +252,7 @@ __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, c
 // 64-bit Shoup butterflies need more registers and latency hiding than this
 // kernel's occupancy (3 CTAs of 128 threads per SM) gives them.
 template <int S, int OB, int MAXA, bool CEN = false>
-__global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? 3 : 6)) modup_col_kernel(ModUpColArgs A) {
+__global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? HX_MODUP_MINB : 6)) modup_col_kernel(ModUpColArgs A) {
   constexpr int TILE = 1 << (S + OB);
   constexpr int T = TILE / 16;
   extern __shared__ u64 dyn_smem[];

@@ -31,6 +31,9 @@
 
 namespace hx {
 
+#ifndef HX_ROWINNER_MINB
+#define HX_ROWINNER_MINB 3
+#endif
 constexpr int kRowInnerMaxKeys = 64;
 
 struct RowInnerArgs {
@@ -49,7 +52,7 @@ struct RowInnerArgs {
 };
 
 template <int S, int OB, int MAXD>
-__global__ void __launch_bounds__((1 << (S + OB)) / 16, 3) ks_row_inner_f64_kernel(RowInnerArgs A) {
+__global__ void __launch_bounds__((1 << (S + OB)) / 16, HX_ROWINNER_MINB) ks_row_inner_f64_kernel(RowInnerArgs A) {
   constexpr int TILE = 1 << (S + OB);
   constexpr int T = TILE / 16;
   extern __shared__ u64 dyn_smem[];

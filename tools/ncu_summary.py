@@ -1,7 +1,7 @@
 """Summarise ncu outputs for profiles/ (run here, no GPU needed).
 
   python tools/ncu_summary.py launches <launches.csv>   per-kernel share of device time
-  python tools/ncu_summary.py full <report.ncu-rep>      key metrics per captured launch
+  python tools/ncu_summary.py full <report.ncu-rep|raw.csv>  key metrics per captured launch
 """
 import collections
 import csv
@@ -58,7 +58,10 @@ METRICS = [
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv"):  # `ncu -i rep --page raw --csv` exported on the GPU box
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units = rows[0], rows[1]
     idx = {n: i for i, n in enumerate(h)}

@@ -9,4 +9,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,
     --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python tools/prof.py ks 256 > /dev/null 2>&1
 python tools/ks_breakdown.py gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_breakdown.txt
 ncu --set full --clock-control none --import-source on -k regex:"${KREGEX:-row_inner|modup_col}" -s ${KSKIP:-2} -c ${KCOUNT:-2} \
-    -o gpurun_out/${TAG}_full -f python tools/prof.py ks 64 > gpurun_out/${TAG}_full.log 2>&1
+    -o /tmp/${TAG}_full -f python tools/prof.py ks 64 > gpurun_out/${TAG}_full.log 2>&1
+ncu -i /tmp/${TAG}_full.ncu-rep --page raw --csv > gpurun_out/${TAG}_full_raw.csv
+ncu -i /tmp/${TAG}_full.ncu-rep --page source --csv --print-source sass > /tmp/${TAG}_sass.csv && gzip -c /tmp/${TAG}_sass.csv > gpurun_out/${TAG}_sass.csv.gz
