@@ -99,7 +99,10 @@ LimbTable make_table(const hx_ctx* c, int n_q, int n_p, int stride = -1, int fir
 
 // NTT launchers (hx_ntt.cu)
 void ntt_forward(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
-void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
+// src: read the input from src (element b, limb entry e at src + b src_estride
+// + off[e] N) and leave the result in data -- an out-of-place transform
+void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s,
+                 const u64* src = nullptr, long long src_estride = 0);
 // forward ROW pass only (the COL pass done by a fused producer, hx_modup.cuh)
 // f64_col_done: the FP64-class limbs already had their COL pass (fused ModDown
 // conversion); the integer-class limbs still get theirs

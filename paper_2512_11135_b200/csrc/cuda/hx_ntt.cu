@@ -19,7 +19,8 @@ namespace hx {
 namespace {
 
 template <bool FWD, bool ROW, int S, bool F64>
-void launch_pass(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
+void launch_pass(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s,
+                 const u64* src = nullptr, long long src_estride = 0) {
   constexpr int OB = HX_NTT_OB;
   constexpr int TILE = 1 << (S + OB);
   NttArgs a;
@@ -30,6 +31,8 @@ void launch_pass(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cud
   a.instances = batch * lt.count;
   a.batch = batch;
   a.bper = 1;
+  a.src = src;
+  a.src_estride = src_estride;
   const long long tiles = c->N() / TILE;
   const long long blocks = a.instances * tiles;
   if (blocks <= 0) return;
@@ -84,14 +87,15 @@ void dispatch_row_combine(hx_ctx* c, int S, u64* data, long long batch, const Li
 }
 
 template <bool FWD, bool ROW, bool F64>
-void dispatch(hx_ctx* c, int S, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
+void dispatch(hx_ctx* c, int S, u64* data, long long batch, const LimbTable& lt, cudaStream_t s,
+              const u64* src = nullptr, long long src_estride = 0) {
   switch (S) {
-    case 3: launch_pass<FWD, ROW, 3, F64>(c, data, batch, lt, s); break;
-    case 4: launch_pass<FWD, ROW, 4, F64>(c, data, batch, lt, s); break;
-    case 5: launch_pass<FWD, ROW, 5, F64>(c, data, batch, lt, s); break;
-    case 6: launch_pass<FWD, ROW, 6, F64>(c, data, batch, lt, s); break;
-    case 7: launch_pass<FWD, ROW, 7, F64>(c, data, batch, lt, s); break;
-    case 8: launch_pass<FWD, ROW, 8, F64>(c, data, batch, lt, s); break;
+    case 3: launch_pass<FWD, ROW, 3, F64>(c, data, batch, lt, s, src, src_estride); break;
+    case 4: launch_pass<FWD, ROW, 4, F64>(c, data, batch, lt, s, src, src_estride); break;
+    case 5: launch_pass<FWD, ROW, 5, F64>(c, data, batch, lt, s, src, src_estride); break;
+    case 6: launch_pass<FWD, ROW, 6, F64>(c, data, batch, lt, s, src, src_estride); break;
+    case 7: launch_pass<FWD, ROW, 7, F64>(c, data, batch, lt, s, src, src_estride); break;
+    case 8: launch_pass<FWD, ROW, 8, F64>(c, data, batch, lt, s, src, src_estride); break;
     default: set_error("ntt: unsupported sub-transform size");
   }
 }
@@ -146,12 +150,14 @@ void ntt_forward_rows(hx_ctx* c, u64* data, long long batch, const LimbTable& lt
 
 int ntt_split_a(int logn) { return split_a(logn); }
 
-void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s) {
+void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s, const u64* src,
+                 long long src_estride) {
   const int a = split_a(c->logn), b = c->logn - a;
   LimbTable ti, tf;
   split(c, lt, ti, tf);
-  if (ti.count) dispatch<false, true, false>(c, b, data, batch, ti, s);   // low-bit stages (ROW)
-  if (tf.count) dispatch<false, true, true>(c, b, data, batch, tf, s);
+  // low-bit stages (ROW); with src, out of place (saves copying the input first)
+  if (ti.count) dispatch<false, true, false>(c, b, data, batch, ti, s, src, src_estride);
+  if (tf.count) dispatch<false, true, true>(c, b, data, batch, tf, s, src, src_estride);
   if (ti.count) dispatch<false, false, false>(c, a, data, batch, ti, s);  // high-bit stages (COL), x N^-1
   if (tf.count) dispatch<false, false, true>(c, a, data, batch, tf, s);
 }

@@ -45,6 +45,10 @@ struct NttArgs {
   long long instances;  // batch * lt.count
   long long batch;      // batch elements
   int bper;             // batch elements per CTA (the grid is pairs x chunks)
+  // out-of-place first pass: read instance (b, e) from src + b src_estride +
+  // off[e] N instead of `data` (null: in place)
+  const u64* src = nullptr;
+  long long src_estride = 0;
 };
 
 // Deposit free index f around the w group bits starting at bit lowbits.
@@ -387,6 +391,8 @@ __device__ __forceinline__ void ntt_pass_body(const NttArgs& a, const EpiArgs* e
   const long long bidx = inst / per;
   const int ent = (int)(inst % per);
   u64* base = a.data + ((long long)bidx * a.lt.stride + a.lt.off[ent]) * (1ll << a.logn);
+  const u64* lbase = a.src ? a.src + (long long)bidx * a.src_estride + (long long)a.lt.off[ent] * (1ll << a.logn)
+                           : base;  // first group's loads
   const PrimeConst P = a.pc[a.lt.prime[ent]];
   const ulonglong2* tw = FWD ? P.tw_fwd : P.tw_inv;
   const double* twf = FWD ? P.twf_fwd : P.twf_inv;
@@ -468,13 +474,13 @@ __device__ __forceinline__ void ntt_pass_body(const NttArgs& a, const EpiArgs* e
         /* direct coalesced global load */                                                     \
         _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
           const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);                     \
-          x[r] = base[tile_gofs<ROW, S, OB>(e, tile, a.logn)];                                 \
+          x[r] = lbase[tile_gofs<ROW, S, OB>(e, tile, a.logn)];                                \
         }                                                                                      \
       } else {                                                                                 \
         /* inverse ROW pass: stage through smem for coalescing */                              \
         _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \
           const int e = r * T + t;                                                             \
-          sm[swz<ROW>(e)] = base[tile_gofs<ROW, S, OB>(e, tile, a.logn)];                      \
+          sm[swz<ROW>(e)] = lbase[tile_gofs<ROW, S, OB>(e, tile, a.logn)];                     \
         }                                                                                      \
         __syncthreads();                                                                       \
         _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                       \

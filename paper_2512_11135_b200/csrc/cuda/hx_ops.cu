@@ -314,8 +314,7 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
   const long long N = c->N();
   const int K = c->n_special, ext = n_q + K, dnum = c->dnum(n_q);
   DBuf coef(batch * n_q * N, s, c);
-  copy2d(coef.p, n_q * N, c1, c1_stride, n_q * N, batch, s);
-  hx::ntt_inverse(c, coef.p, batch, hx::make_table(c, n_q, 0), s);
+  hx::ntt_inverse(c, coef.p, batch, hx::make_table(c, n_q, 0), s, c1, c1_stride);  // out of place
   if (modup_fused_ok(c, n_q)) {
     // conversion fused into the COL pass (one launch per prime class), the
     // digits' own limbs copied from the NTT-domain input, then the ROW pass
@@ -589,8 +588,7 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
   const long long N = c->N();
   const int K = c->n_special;
   DBuf sp(polys * K * N, s, c), conv(polys * n_q * N, s, c);
-  copy2d(sp.p, K * N, u + (long long)n_q * N, u_stride, K * N, polys, s);
-  hx::ntt_inverse(c, sp.p, polys, hx::make_table(c, 0, K), s);
+  hx::ntt_inverse(c, sp.p, polys, hx::make_table(c, 0, K), s, u + (long long)n_q * N, u_stride);  // out of place
   static const bool unfused = getenv("HX_MODDOWN_UNFUSED") != nullptr;
   static const bool col_off = getenv("HX_MODDOWN_COL_OFF") != nullptr;
   const int sa = hx::ntt_split_a(c->logn);
@@ -719,13 +717,12 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
 void rescale(hx_ctx* c, u64* out, const u64* in, long long polys, int n_q, cudaStream_t s) {
   const long long N = c->N();
   DBuf last(polys * N, s, c), lift(polys * (n_q - 1) * N, s, c);
-  copy2d(last.p, N, in + (long long)(n_q - 1) * N, (long long)n_q * N, N, polys, s);
   LimbTable lt{};
   lt.count = 1;
   lt.stride = 1;
   lt.off[0] = 0;
   lt.prime[0] = (unsigned char)(n_q - 1);
-  hx::ntt_inverse(c, last.p, polys, lt, s);
+  hx::ntt_inverse(c, last.p, polys, lt, s, in + (long long)(n_q - 1) * N, (long long)n_q * N);  // out of place
   hx::RescaleArgs R;
   R.last = last.p;
   R.out = lift.p;
