@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "hx_internal.h"
+#include "hx_ntt_cluster.cuh"
 
 #ifndef HX_NTT_OB
 #define HX_NTT_OB 3
@@ -100,6 +101,76 @@ void dispatch(hx_ctx* c, int S, u64* data, long long batch, const LimbTable& lt,
   }
 }
 
+// Single-pass FP64-class transform of N = 2^16 limbs, one limb per cluster of
+// 16 CTAs (hx_ntt_cluster.cuh).  Opt-in (HX_NTT_CLUSTER=1): measured slower
+// than the two passes on B200 (1.31 M vs 2.09 M limb-NTT/s; 52.3 vs 50.1 ms
+// per 256 key switches) -- each CTA runs load / transform / cluster barrier /
+// DSMEM gather / transform / store in lockstep with its cluster, so nothing
+// overlaps the phases.  false when not selected or unavailable (other N, no
+// cluster of that shape fits the device).
+template <bool FWD>
+bool launch_cluster(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s,
+                    const u64* src = nullptr, long long src_estride = 0) {
+  constexpr int S = 8, OB = 4, TILE = 1 << (S + OB), C = 1 << (S - OB);
+  static const bool off = !(getenv("HX_NTT_CLUSTER") && atoi(getenv("HX_NTT_CLUSTER")) == 1);
+  if (off || c->logn != 2 * S || lt.count == 0) return false;
+  auto kern = ntt_cluster_kernel<FWD, S, OB>;
+  constexpr int smem = ntt_cluster_smem_bytes<S, OB>();
+  static int ok = -1;
+  if (ok < 0) {
+    ok = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(C * 64);
+      cfg.blockDim = dim3(TILE / 16);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) == cudaSuccess && n > 0) ok = 1;
+      if (getenv("HX_ALLOC_TRACE")) fprintf(stderr, "[hx] ntt cluster kernel: %d active clusters\n", n);
+    }
+    cudaGetLastError();
+  }
+  if (!ok) return false;
+  NttArgs a;
+  a.data = data;
+  a.pc = c->d_pc;
+  a.lt = lt;
+  a.logn = c->logn;
+  a.instances = batch * lt.count;
+  a.batch = batch;
+  a.bper = 1;
+  a.src = src;
+  a.src_estride = src_estride;
+  const long long blocks = a.instances * C;
+  if (blocks <= 0) return true;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(TILE / 16);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) {
+    set_error("ntt: cluster launch failed");
+    return true;
+  }
+  ++c->launches;
+  return true;
+}
+
 // N = 2^a (column / high bits) x 2^b (row / low bits), a = ceil(logn/2)
 inline int split_a(int logn) { return (logn + 1) / 2; }
 
@@ -121,10 +192,11 @@ void ntt_forward(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cud
   const int a = split_a(c->logn), b = c->logn - a;
   LimbTable ti, tf;
   split(c, lt, ti, tf);
+  const bool one = tf.count && launch_cluster<true>(c, data, batch, tf, s);  // FP64 limbs in one pass
   if (ti.count) dispatch<true, false, false>(c, a, data, batch, ti, s);  // first a stages (COL)
-  if (tf.count) dispatch<true, false, true>(c, a, data, batch, tf, s);
+  if (tf.count && !one) dispatch<true, false, true>(c, a, data, batch, tf, s);
   if (ti.count) dispatch<true, true, false>(c, b, data, batch, ti, s);   // last b stages (ROW)
-  if (tf.count) dispatch<true, true, true>(c, b, data, batch, tf, s);
+  if (tf.count && !one) dispatch<true, true, true>(c, b, data, batch, tf, s);
 }
 
 // forward NTT of ModDown's converted term whose ROW pass writes the key-switch
@@ -155,11 +227,13 @@ void ntt_inverse(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cud
   const int a = split_a(c->logn), b = c->logn - a;
   LimbTable ti, tf;
   split(c, lt, ti, tf);
+  // FP64 limbs in one pass (cluster kernel) when available
+  const bool one = tf.count && launch_cluster<false>(c, data, batch, tf, s, src, src_estride);
   // low-bit stages (ROW); with src, out of place (saves copying the input first)
   if (ti.count) dispatch<false, true, false>(c, b, data, batch, ti, s, src, src_estride);
-  if (tf.count) dispatch<false, true, true>(c, b, data, batch, tf, s, src, src_estride);
+  if (tf.count && !one) dispatch<false, true, true>(c, b, data, batch, tf, s, src, src_estride);
   if (ti.count) dispatch<false, false, false>(c, a, data, batch, ti, s);  // high-bit stages (COL), x N^-1
-  if (tf.count) dispatch<false, false, true>(c, a, data, batch, tf, s);
+  if (tf.count && !one) dispatch<false, false, true>(c, a, data, batch, tf, s);
 }
 
 }  // namespace hx

@@ -476,3 +476,22 @@ def test_compressed_keys(cfg):
     ctx.rotate(o2, ct, full, 2, nq, g)
     assert np.array_equal(host(o1), host(o2))
     assert L.hx_key_release(ctx.h, ck.data_ptr()) == 0
+
+
+def test_ntt_cluster_variant_parity():
+    """The opt-in single-pass cluster NTT (HX_NTT_CLUSTER=1, read once per
+    process, hence the subprocess) gives the same words as the oracle at
+    N = 2^16: forward, inverse, and the out-of-place inverse of ModUp inside a
+    key switch (via the full rotate parity test)."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env_ = dict(os.environ, HX_NTT_CLUSTER="1")
+    f = os.path.join(here, "test_gpu_parity.py")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        f + "::test_ntt_roundtrip_parity[c2]", f + "::test_rotate_parity_and_decrypt[c2]"],
+                       env=env_, capture_output=True, text=True, cwd=here, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert " passed" in r.stdout and "2 passed" in r.stdout, r.stdout[-2000:]
