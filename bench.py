@@ -701,6 +701,16 @@ def main():
         except Exception as exc:  # reported, never fatal for the headline line
             extras["matmul_d128"] = {"error": str(exc)[:200]}
         torch.cuda.empty_cache()
+        # the same matmul with FP64-class special primes (parameter co-design:
+        # at a 4-limb level the 60-bit specials' integer passes dominate)
+        try:
+            chain47, special47 = primes(fp64_specials=True)
+            mm = matmul_bench(torch, chain47, special47)["matmul_d128"]
+            mm["special_bits"] = [int(p).bit_length() for p in special47]
+            extras["matmul_d128_fp64_specials"] = mm
+        except Exception as exc:
+            extras["matmul_d128_fp64_specials"] = {"error": str(exc)[:200]}
+        torch.cuda.empty_cache()
         try:
             extras.update(config5_stacked_bench(torch, chain, special))
         except Exception as exc:

@@ -169,9 +169,10 @@ def test_batched_rotation_paths_agree_and_repeat(cfg):
     their words must agree, and repeated calls must return identical words --
     a cross-CTA race in an in-place pass shows up here as a few differing
     tiles of the last ciphertexts (a packed-digit experiment failed exactly
-    so, only at batch >= 15).  hx_rotate takes the fused ROW-pass + key
-    inner-product kernel (one key), the other two the separate ROW pass and
-    inner-product kernels: "c2n16" checks the N = 2^16 tile shape of both."""
+    so, only at batch >= 15).  The three take the fused ROW-pass + key
+    inner-product kernel; hx_rotate_hoisted (one digit set for all keys) the
+    separate ROW pass and inner-product kernels, and must give the same
+    words: "c2n16" checks the N = 2^16 tile shape of both."""
     import torch
 
     from paper_2512_11135_b200 import Context
@@ -211,11 +212,13 @@ def test_batched_rotation_paths_agree_and_repeat(cfg):
             cts[:, :, k, :] = torch.randint(0, q, (B, 2, n), generator=gen, device="cuda")
         outs = []
         for rep in range(2):
-            o1, o2, o3 = (torch.empty_like(cts) for _ in range(3))
+            o1, o2, o3, o4 = (torch.empty_like(cts) for _ in range(4))
             ctx.rotate(o1, cts, key, B, nq, g)
             ctx.rotate_multi(o2, cts, [key] * B, [g] * B, nq)
             ctx.rotate_grouped(o3, cts, [key], [g], B, nq)
+            ctx.rotate_hoisted(o4, cts, [key], [g], B, nq)  # unfused: ROW pass + inner product
             torch.cuda.synchronize()
             assert torch.equal(o1, o2) and torch.equal(o1, o3), (cfg, B, rep)
+            assert torch.equal(o1, o4), (cfg, B, rep, "fused vs unfused ROW / inner product")
             outs.append(o1.clone())
         assert torch.equal(outs[0], outs[1]), (cfg, B)
