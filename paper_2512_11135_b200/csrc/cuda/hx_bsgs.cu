@@ -92,8 +92,14 @@ __device__ __forceinline__ void split20(u64 v, double& hi, double& lo) {
   lo = __dsub_rn(__longlong_as_double((long long)((v & 0xFFFFFull) | 0x4330000000000000ull)), kTwo52);
 }
 
-template <int KPT>
-__global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_f64_kernel(MacArgs A, const int* limbs) {
+// NW warps per CTA; for KPT <= 4 at most 64 registers so that 32 warps / SM
+// are resident (HBM latency x bandwidth needs that many 256-B diagonal rows
+// in flight: n1 = n2 = 32 MAC 0.69 -> 0.75 of the HBM peak).  KPT = 8
+// (n1 = 64) keeps 126 registers at 2 CTAs / SM: 16 warps of 4 baby steps
+// each measured 2 ms slower per W2 matvec.
+template <int KPT, int NW = kMacWarps>
+__global__ void __launch_bounds__(32 * NW, (KPT <= 4 ? 32 / NW : 2)) bsgs_mac_f64_kernel(MacArgs A, const int* limbs) {
+  constexpr int kMacWarps = NW;
   __shared__ double part[2][kMacWarps][2][3][32];  // [buf][warp][poly][S11,S10,S00][lane]
   const long long N = 1ll << A.logn;
   const int i = limbs[blockIdx.y];

@@ -66,9 +66,14 @@ def ffn(prune=False):
     be.gen_rotation_keys(mat.rotations())
     x = np.tile(np.concatenate([rng.uniform(-1, 1, 768), np.zeros(256)]), be.slots // 1024)
     ct = be.encrypt(x)
-    for _ in range(2):
-        outs, rep = be.matvec(mat, ct)
+    outs, rep = be.matvec(mat, ct)
     torch.cuda.synchronize()
+    # the second matvec alone inside the profiler window
+    # (ncu --profile-from-start off captures only this one)
+    torch.cuda.profiler.start()
+    outs, rep = be.matvec(mat, ct)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
     print("ok ffn", rep)
 
 
