@@ -305,8 +305,14 @@ __device__ __forceinline__ u64 combine_split24(const double (&s)[3], const Prime
   return f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);
 }
 
+#ifndef HX_KSF_MINB
+#define HX_KSF_MINB 2
+#endif
+#ifndef HX_KSI_MINB
+#define HX_KSI_MINB 2
+#endif
 template <int MAXD>
-__global__ void __launch_bounds__(256, 2) ks_inner_f64_kernel(InnerArgs A, const int* limbs) {
+__global__ void __launch_bounds__(256, HX_KSF_MINB) ks_inner_f64_kernel(InnerArgs A, const int* limbs) {
   const int N = 1 << A.logn;
   const int ext = A.n_q + A.n_special, full = A.n_chain + A.n_special;
   const int j = limbs[blockIdx.y];
@@ -434,7 +440,7 @@ __global__ void __launch_bounds__(256, 3) ks_inner_f64_one_kernel(InnerArgs A, c
 }
 
 template <int MAXD>
-__global__ void __launch_bounds__(256, 2) ks_inner_kernel(InnerArgs A, const int* limbs) {
+__global__ void __launch_bounds__(256, HX_KSI_MINB) ks_inner_kernel(InnerArgs A, const int* limbs) {
   const int N = 1 << A.logn;
   const int ext = A.n_q + A.n_special, full = A.n_chain + A.n_special;
   const int j = limbs ? limbs[blockIdx.y] : blockIdx.y;

@@ -1,7 +1,7 @@
 """ms per hx_rotate over `batch` ciphertexts (N=2^16, 24+3 primes), CUDA
 events, median of 5 runs of 3 calls -- quick A/B of kernel variants.
 
-  python tools/ks_time.py [batch] [op]     op: rotate (default) | relin
+  python tools/ks_time.py [batch] [op]     op: rotate (default) | relin | hoisted
 """
 import os
 import statistics
@@ -29,8 +29,17 @@ def main():
     key = bench.make_key(torch, ctx, gen, chain, special, g, dev)
     cts = bench.rand_limbs(torch, gen, chain, (B, 2), dev)
     out = torch.empty_like(cts)
-    f = (lambda: ctx.rotate(out, cts, key, B, nq, g)) if op == "rotate" else \
-        (lambda: ctx.mul_relin(out, cts, cts, key, B, nq))
+    if op == "rotate":
+        f = lambda: ctx.rotate(out, cts, key, B, nq, g)  # noqa: E731
+    elif op == "relin":
+        f = lambda: ctx.mul_relin(out, cts, cts, key, B, nq)  # noqa: E731
+    else:  # hoisted: 32 rotations of chunks of 8 ciphertexts (the bench extra)
+        gs = [pow(5, k, 2 * N) for k in range(1, 33)]
+        hout = torch.empty((8, 32, 2, nq, N), dtype=torch.int64, device=dev)
+
+        def f():
+            for c0 in range(0, B, 8):
+                ctx.rotate_hoisted(hout, cts[c0:c0 + 8], [key] * 32, gs, 8, nq)
     for _ in range(3):
         f()
     torch.cuda.synchronize()
