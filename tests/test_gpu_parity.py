@@ -266,9 +266,11 @@ def test_keyswitch_and_hoisted_parity(cfg):
         assert np.array_equal(exp[r], orc.rotate(ct, keys[r], nq, g))
 
 
-@pytest.mark.parametrize("cfg", ["c1", "c2s", "c2s47"])
+@pytest.mark.parametrize("cfg", ["c1", "c2s", "c2s47", "c2"])
 def test_rotate_multi_parity(cfg):
-    """hx_rotate_multi: per-element keys / galois elements, one batched ModUp"""
+    """hx_rotate_multi: per-element keys / galois elements, one batched ModUp
+    (the fused ROW + inner-product kernel with a key per element; "c2" at
+    the N = 2^16 tile shape)"""
     import ctypes as C
 
     p, ctx, orc = env(cfg)
