@@ -134,6 +134,9 @@ int hxc_matrix_payload_count(const hxc_mat* m);
 int hxc_encode_words(hxc_backend* b, const double* m, int len, int level, double scale, uint64_t* out);
 int hxc_encode_coeffs(const char* params_json, const double* m, int len, int level, double scale,
                       int64_t* out);
+/* host-only: CkksEncoder::decode_coeffs (encoder.cpp:119-159 restated with a
+ * Garner CRT): coefficient-domain limbs [n_limbs][N] -> N/2 slots */
+int hxc_decode_coeffs(const char* params_json, const uint64_t* limbs, int n_limbs, double scale, double* out);
 
 /* OpTrace JSON (canonical names ct_add ... bootstrap); returns length */
 int hxc_trace_json(hxc_backend* b, char* buf, int cap);

@@ -10,8 +10,12 @@
 // pieces composed from the reference's NttTables::forward /
 // inverse (ntt.cpp:57-96) and Modulus::mul/add/sub (modmath.hpp:41-63), with
 // the same conventions as the oracle.
+#include <atomic>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <memory>
 #include <thread>
 #include <vector>
@@ -26,10 +30,84 @@ using helix::u64;
 
 namespace {
 
+// Persistent worker pool (created once per context by ref_set_threads): a
+// parallel_for hands out indices through an atomic counter to the parked
+// workers and the calling thread; nested parallel_for calls made from inside
+// a task run serially on that task's thread (the batched arm threads across
+// ciphertexts, each rotation single-threaded).
+class Pool {
+ public:
+  explicit Pool(int n) {
+    for (int i = 0; i + 1 < n; ++i) th_.emplace_back([this] { work(); });
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int size() const { return (int)th_.size() + 1; }
+  void run(int count, const std::function<void(int)>& f) {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      job_ = &f;
+      count_ = count;
+      next_.store(0);
+      busy_ = (int)th_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [this] { return busy_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void drain() {
+    in_task() = true;
+    for (int i; (i = next_.fetch_add(1)) < count_;) (*job_)(i);
+    in_task() = false;
+  }
+  void work() {
+    long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      drain();
+      std::lock_guard<std::mutex> lk(m_);
+      if (--busy_ == 0) done_.notify_one();
+    }
+  }
+
+ public:
+  static bool& in_task() {
+    static thread_local bool t = false;
+    return t;
+  }
+
+ private:
+  std::vector<std::thread> th_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  std::atomic<int> next_{0};
+  int count_ = 0, busy_ = 0;
+  long gen_ = 0;
+  bool stop_ = false;
+};
+
 struct RefCtx {
   int logn = 0;
   std::size_t n = 0;
   int n_chain = 0, n_special = 0, alpha = 1, threads = 1;
+  std::unique_ptr<Pool> pool;
   std::vector<helix::Modulus> mods;   // chain then special
   std::vector<helix::NttTables> ntt;  // same order
   std::unique_ptr<helix::LatticeContext> lc;
@@ -37,18 +115,13 @@ struct RefCtx {
 };
 
 template <class F>
-void parallel_for(int count, int threads, F f) {
-  if (threads <= 1 || count <= 1) {
+void parallel_for(Pool* pool, int count, F f) {
+  if (!pool || pool->size() <= 1 || count <= 1 || Pool::in_task()) {
     for (int i = 0; i < count; ++i) f(i);
     return;
   }
-  std::vector<std::thread> pool;
-  const int nt = threads < count ? threads : count;
-  for (int w = 0; w < nt; ++w)
-    pool.emplace_back([&, w] {
-      for (int i = w; i < count; i += nt) f(i);
-    });
-  for (auto& t : pool) t.join();
+  const std::function<void(int)> fn = f;
+  pool->run(count, fn);
 }
 
 int pidx(const RefCtx* c, int k, int n_q) { return k < n_q ? k : c->n_chain + (k - n_q); }
@@ -75,22 +148,23 @@ void modup(const RefCtx* c, u64* D, const u64* c1, int n_q) {
   const std::size_t n = c->n;
   const int K = c->n_special, ext = n_q + K, dnum = (n_q + c->alpha - 1) / c->alpha;
   std::vector<u64> coef(c1, c1 + (std::size_t)n_q * n);
-  parallel_for(n_q, c->threads, [&](int i) {
+  parallel_for(c->pool.get(), n_q, [&](int i) {
     c->ntt[i].inverse(std::span<u64>(coef.data() + (std::size_t)i * n, n));
   });
   for (int d = 0; d < dnum; ++d) {
     const int lo = d * c->alpha, hi = std::min(lo + c->alpha, n_q);
     std::vector<u64> x((std::size_t)(hi - lo) * n);
-    for (int i = lo; i < hi; ++i) {
+    parallel_for(c->pool.get(), hi - lo, [&](int ii) {
+      const int i = lo + ii;
       const auto& m = c->mods[i];
       u64 prod = 1;
       for (int i2 = lo; i2 < hi; ++i2)
         if (i2 != i) prod = m.mul(prod, c->mods[i2].q % m.q);
       const u64 inv = m.inv(prod);
       for (std::size_t t = 0; t < n; ++t) x[(i - lo) * n + t] = m.mul(coef[i * n + t], inv);
-    }
+    });
     u64* out = D + (std::size_t)d * ext * n;
-    parallel_for(ext, c->threads, [&](int j) {
+    parallel_for(c->pool.get(), ext, [&](int j) {
       u64* dst = out + (std::size_t)j * n;
       if (j >= lo && j < hi) {
         std::memcpy(dst, c1 + (std::size_t)j * n, n * 8);
@@ -144,7 +218,7 @@ void inner(const RefCtx* c, u64* U, const u64* D, const u64* key, int n_q, u64 g
   const int K = c->n_special, ext = n_q + K, full = c->n_chain + K;
   const int dnum = (n_q + c->alpha - 1) / c->alpha;
   const auto perm = perm_table(c, g);
-  parallel_for(2 * ext, c->threads, [&](int cj) {
+  parallel_for(c->pool.get(), 2 * ext, [&](int cj) {
     const int cc = cj / ext, j = cj % ext, kl = pidx(c, j, n_q);
     const auto& m = c->mods[kl];
     u64* dst = U + ((std::size_t)cc * ext + j) * n;
@@ -163,7 +237,7 @@ void moddown(const RefCtx* c, u64* out, const u64* U, int n_q) {
   const int K = c->n_special, ext = n_q + K;
   std::vector<u64> sp(U + (std::size_t)n_q * n, U + (std::size_t)ext * n);
   std::vector<u64> x((std::size_t)K * n);
-  parallel_for(K, c->threads, [&](int k) {
+  parallel_for(c->pool.get(), K, [&](int k) {
     const auto& m = c->mods[c->n_chain + k];
     c->ntt[c->n_chain + k].inverse(std::span<u64>(sp.data() + (std::size_t)k * n, n));
     u64 prod = 1;
@@ -172,7 +246,7 @@ void moddown(const RefCtx* c, u64* out, const u64* U, int n_q) {
     const u64 inv = m.inv(prod);
     for (std::size_t t = 0; t < n; ++t) x[k * n + t] = m.mul(sp[k * n + t], inv);
   });
-  parallel_for(n_q, c->threads, [&](int i) {
+  parallel_for(c->pool.get(), n_q, [&](int i) {
     const auto& m = c->mods[i];
     std::vector<u64> ph(K);
     u64 Pq = 1;
@@ -243,7 +317,14 @@ void ref_ctx_destroy(void* h) {
   delete c;
 }
 
-void ref_set_threads(void* h, int threads) { static_cast<RefCtx*>(h)->threads = threads; }
+void ref_set_threads(void* h, int threads) {
+  auto* c = static_cast<RefCtx*>(h);
+  if (threads < 1) threads = 1;
+  if (c->threads == threads && (threads == 1 || c->pool)) return;
+  c->pool.reset();
+  c->threads = threads;
+  if (threads > 1) c->pool = std::make_unique<Pool>(threads);
+}
 
 u64 ref_psi(void* h, int i) { return static_cast<RefCtx*>(h)->ntt[i].psi(); }
 
@@ -348,12 +429,23 @@ int ref_rotate(void* h, const u64* in_ct, const u64* key, u64* out_ct, int n_q, 
   moddown(c, V.data(), U.data(), n_q);
   moddown(c, V.data() + L, U.data() + (std::size_t)ext * n, n_q);
   const auto perm = perm_table(c, g);
-  parallel_for(n_q, c->threads, [&](int i) {
+  parallel_for(c->pool.get(), n_q, [&](int i) {
     const auto& m = c->mods[i];
     for (std::size_t t = 0; t < n; ++t)
       out_ct[i * n + t] = m.add(in_ct[i * n + perm[t]], V[i * n + t]);
   });
   std::memcpy(out_ct + L, V.data() + L, L * 8);
+  return 0;
+}
+
+// The CPU reference arm over a batch: ciphertexts spread over the context's
+// persistent pool, one whole (single-threaded) rotation per task -- the
+// parallel axis BASELINE.md section 3 plans (independent ciphertexts).
+int ref_rotate_batch(void* h, const u64* in_cts, const u64* key, u64* out_cts, int batch, int n_q, u64 g) {
+  auto* c = static_cast<RefCtx*>(h);
+  const std::size_t ct = (std::size_t)2 * n_q * c->n;
+  if (batch == 1) return ref_rotate(h, in_cts, key, out_cts, n_q, g);
+  parallel_for(c->pool.get(), batch, [&](int b) { ref_rotate(h, in_cts + b * ct, key, out_cts + b * ct, n_q, g); });
   return 0;
 }
 

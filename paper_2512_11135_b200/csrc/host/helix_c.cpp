@@ -324,6 +324,16 @@ int hxc_encode_coeffs(const char* json, const double* m, int len, int level, dou
   });
 }
 
+int hxc_decode_coeffs(const char* json, const uint64_t* limbs, int n_limbs, double scale, double* out) {
+  return guard(-1, [&] {
+    const CkksEncoder enc(CkksParams::from_json(json));
+    const std::size_t n = enc.ring_degree();
+    const auto v = enc.decode_coeffs(std::span<const std::uint64_t>(limbs, (std::size_t)n_limbs * n), n_limbs, scale);
+    std::memcpy(out, v.data(), v.size() * sizeof(double));
+    return 0;
+  });
+}
+
 int hxc_trace_json(hxc_backend* b, char* buf, int cap) {
   const auto s = b->b->trace().to_json();
   if (buf && cap > 0) {

@@ -79,6 +79,7 @@ def lib():
         "hxc_matrix_payload_ptr": (v, [v, i32]),
         "hxc_matrix_payload_count": (i32, [v]),
         "hxc_encode_coeffs": (i32, [C.c_char_p, f64p, i32, i32, C.c_double, C.POINTER(C.c_int64)]),
+        "hxc_decode_coeffs": (i32, [C.c_char_p, C.POINTER(C.c_uint64), i32, C.c_double, f64p]),
         "hxc_encode_words": (i32, [v, f64p, i32, i32, C.c_double, C.POINTER(C.c_uint64)]),
         "hxc_trace_json": (i32, [v, C.c_char_p, i32]),
         "hxc_trace_reset": (None, [v]),
@@ -122,6 +123,19 @@ def encode_coeffs(pjson: str, m, level: int, scale: float) -> np.ndarray:
     out = np.zeros(n, dtype=np.int64)
     a, ap = _dp(m)
     if L.hxc_encode_coeffs(pjson.encode(), ap, len(a), level, scale, out.ctypes.data_as(C.POINTER(C.c_int64))) != 0:
+        raise _err()
+    return out
+
+
+def decode_coeffs(pjson: str, limbs, n_limbs: int, scale: float) -> np.ndarray:
+    """host-only CkksEncoder::decode_coeffs (no device needed)"""
+    L = lib()
+    n = json.loads(pjson)["N"]
+    a = np.ascontiguousarray(limbs, dtype=np.uint64)
+    assert a.size == n_limbs * n
+    out = np.zeros(n // 2, dtype=np.float64)
+    if L.hxc_decode_coeffs(pjson.encode(), a.ctypes.data_as(C.POINTER(C.c_uint64)), n_limbs, scale,
+                           out.ctypes.data_as(C.POINTER(C.c_double))) != 0:
         raise _err()
     return out
 

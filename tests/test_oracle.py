@@ -187,3 +187,92 @@ def test_live_reference_config1():
     o = np.zeros_like(ct)
     ref.L.ref_rotate(ref.h, ptr(ct), ptr(key), ptr(o), 3, g)
     assert np.array_equal(orc.rotate(ct, key, 3, g), o)
+
+
+# ---------------------------------------------------------------- K = 3 pin
+# config 2's hybrid key-switch shape (24 chain primes, K = 3 special primes,
+# alpha = 3, dnum = 8) at N = 2^11: the oracle's hxo_rotate / hxo_keyswitch
+# vs the reference-primitive composition in oracle/_ref (ref_shim.cpp) --
+# the CPU reference arm bench.py --impl reference times.
+K3_LOGN = 11
+K3_SEED = 20251211 * 10 + 2
+
+
+def k3_inputs():
+    """deterministic inputs (numpy PCG64) + their SHA-256"""
+    import hashlib
+
+    p = config2(K3_LOGN, 24)
+    n, nq, K = 1 << K3_LOGN, 24, 3
+    orc = Oracle(K3_LOGN, p["chain"], p["special"], 3)
+    rng = np.random.default_rng(K3_SEED)
+    s_full = orc.ntt_fwd(orc.from_i64(ternary(rng, n), nq, K), nq, K)
+    g = galois_elt(7, n)
+    dn = orc.dnum(nq)
+    key = orc.keygen_ksk(s_full, orc.automorphism_ntt(s_full, nq, K, g),
+                         uniform_limbs(rng, p["chain"] + p["special"], n, (dn,)),
+                         np.stack([gaussian(rng, n) for _ in range(dn)]))
+    ct = uniform_limbs(rng, p["chain"], n, (2,))
+    h = hashlib.sha256(ct.tobytes() + key.tobytes()).hexdigest()
+    return p, ct, key, g, h
+
+
+def _sha(a):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_golden_k3_rotate_vs_reference_primitives():
+    """always runs: the committed digests of the reference-primitive K = 3
+    key switch (tests/golden/make_golden_k3.py) equal the oracle's words"""
+    import json
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "ref_k3_n2048.json")) as f:
+        gold = json.load(f)
+    p, ct, key, g, h = k3_inputs()
+    assert h == gold["inputs_sha256"], "input generator drifted"
+    assert g == gold["galois"]
+    orc = Oracle(K3_LOGN, p["chain"], p["special"], 3)
+    assert _sha(orc.rotate(ct, key, 24, g)) == gold["ref_rotate_sha256"]
+    assert _sha(orc.keyswitch(np.ascontiguousarray(ct[1]), key, 24)) == gold["ref_keyswitch_sha256"]
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("lvl", [24, 13, 1])
+def test_live_reference_k3_rotate(lvl):
+    """live: ref_rotate == hxo_rotate at K = 3, alpha = 3 at three levels
+    (full, a partial last digit, one limb), plus the batched reference arm"""
+    p, ct, key, g, _ = k3_inputs()
+    orc = Oracle(K3_LOGN, p["chain"], p["special"], 3)
+    ref = Ref(K3_LOGN, p["chain"], p["special"], 3)
+    c = np.ascontiguousarray(ct[:, :lvl])
+    o = np.zeros_like(c)
+    assert ref.L.ref_rotate(ref.h, ptr(c), ptr(key), ptr(o), lvl, g) == 0
+    exp = orc.rotate(c, key, lvl, g)
+    assert np.array_equal(o, exp)
+    if lvl == 24 and hasattr(ref.L, "ref_rotate_batch"):
+        import ctypes as C
+
+        cts = np.ascontiguousarray(np.stack([c, exp]))
+        ob = np.zeros_like(cts)
+        ref.L.ref_rotate_batch.argtypes = [C.c_void_p] * 4 + [C.c_int, C.c_int, C.c_uint64]
+        ref.L.ref_set_threads(ref.h, 4)  # the persistent pool, one ciphertext per task
+        assert ref.L.ref_rotate_batch(ref.h, cts.ctypes.data, key.ctypes.data, ob.ctypes.data, 2, lvl, g) == 0
+        assert np.array_equal(ob[0], exp)
+        assert np.array_equal(ob[1], orc.rotate(exp, key, lvl, g))
+
+
+def test_golden_decode_matches_reference_decode(gold):
+    """CkksEncoder::decode (encoder.cpp:119-159, GMP CRT) vs the product's
+    Garner-CRT decode on the same coefficient-domain limbs"""
+    from paper_2512_11135_b200.helix import decode_coeffs, params_json
+
+    chain = [int(x) for x in gold["chain"]]
+    special = [int(x) for x in gold["special"]]
+    pj = params_json(int(gold["logn"]), chain, special, 1, 40)
+    got = decode_coeffs(pj, gold["enc_out"], 3, float(2**40))
+    exp = gold["dec_out"]
+    # identical CRT integers; the FFT is the reference's operation order, so
+    # the slots agree to the last few ulps
+    assert np.abs(got - exp).max() <= 1e-12 * max(1.0, np.abs(exp).max())
