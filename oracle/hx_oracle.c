@@ -749,3 +749,220 @@ void hxo_encrypt_sk(const hxo_ctx* c, uint64_t* ct, const uint64_t* m_ntt, const
   }
   free(en);
 }
+
+/* ------------------------------------------------------------------------ */
+/* linear-algebra drivers (reference kernels.cpp is missing, */
+/* proj/CMakeLists.txt:22) -- the schedules the product runs                 */
+/* (paper_2512_11135_b200/csrc/host/linalg.cpp, gpu_backend.cpp), restated   */
+/* over the primitives above.  Modular sums are order independent, so only   */
+/* the set of terms, the rotations and the rescale / ModDown placement pin    */
+/* the output words.                                                          */
+/* ------------------------------------------------------------------------ */
+
+static u64 reduce_amount(int64_t r, u64 slots) {
+  const int64_t s = (int64_t)slots;
+  return (u64)(((r % s) + s) % s);
+}
+
+/* Rot_r(ct) with the standard-layout key keys[r]; r == 0 copies */
+static void rot_by(const hxo_ctx* c, u64* out, const u64* ct, int64_t amount, const uint64_t* const* keys,
+                   int n_q) {
+  const u64 slots = c->n / 2, r = reduce_amount(amount, slots);
+  if (r == 0) {
+    memcpy(out, ct, (u64)2 * n_q * c->n * 8);
+    return;
+  }
+  u64 g = 1;
+  for (u64 i = 0; i < r; ++i) g = (g * 5) % (2 * c->n);
+  hxo_rotate(c, out, ct, keys[r], n_q, g);
+}
+
+static void ct_add(const hxo_ctx* c, u64* acc, const u64* x, int n_q) {
+  hxo_add(c, acc, acc, x, n_q, 0);
+  hxo_add(c, acc + (u64)n_q * c->n, acc + (u64)n_q * c->n, x + (u64)n_q * c->n, n_q, 0);
+}
+
+static void ct_mul_plain(const hxo_ctx* c, u64* out, const u64* x, const u64* pt, int n_q) {
+  hxo_mul(c, out, x, pt, n_q, 0);
+  hxo_mul(c, out + (u64)n_q * c->n, x + (u64)n_q * c->n, pt, n_q, 0);
+}
+
+static void ct_rescale(const hxo_ctx* c, u64* out, const u64* x, int n_q) {
+  hxo_rescale_ntt(c, out, x, n_q);
+  hxo_rescale_ntt(c, out + (u64)(n_q - 1) * c->n, x + (u64)n_q * c->n, n_q);
+}
+
+static u64 galois_of(const hxo_ctx* c, u64 r) {
+  u64 g = 1;
+  for (u64 i = 0; i < r; ++i) g = (g * 5) % (2 * c->n);
+  return g;
+}
+
+void hxo_matvec_bsgs(const hxo_ctx* c, uint64_t* out, const uint64_t* x, int n_q, int n1, int n2, int blocks,
+                     const uint64_t* const* diags, const uint64_t* const* keys, int giant_begin, int giant_end,
+                     int rescale, int lazy) {
+  const u64 n = c->n, L = (u64)n_q * n, ct = 2 * L;
+  const int K = c->n_special, ext = n_q + K;
+  const int gb = giant_begin, ge = giant_end < 0 ? n2 : giant_end;
+  /* baby steps Rot_k(x), k < n1: one ModUp shared by all (hoisting convention) */
+  u64* baby = (u64*)malloc((u64)n1 * ct * 8);
+  memcpy(baby, x, ct * 8);
+  if (n1 > 1) {
+    const uint64_t** kk = (const uint64_t**)malloc(sizeof(void*) * (n1 - 1));
+    u64* gs = (u64*)malloc(8 * (n1 - 1));
+    for (int k = 1; k < n1; ++k) {
+      kk[k - 1] = keys[k];
+      gs[k - 1] = galois_of(c, (u64)k);
+    }
+    hxo_rotate_hoisted(c, baby + ct, x, kk, gs, n1 - 1, n_q);
+    free(kk);
+    free(gs);
+  }
+  u64* inner = (u64*)malloc(ct * 8);
+  u64* acc = (u64*)malloc(ct * 8);
+  u64* tmp = (u64*)malloc(ct * 8);
+  u64* S = (u64*)malloc((u64)2 * ext * n * 8);
+  u64* U = (u64*)malloc((u64)2 * ext * n * 8);
+  u64* D = (u64*)malloc((u64)hxo_ctx_dnum(c, n_q) * ext * n * 8);
+  const u64 slots = n / 2;
+  for (int b = 0; b < blocks; ++b) {
+    memset(acc, 0, ct * 8);
+    memset(S, 0, (u64)2 * ext * n * 8);
+    int any_giant = 0;
+    for (int j = gb; j < ge; ++j) {
+      int live = 0;
+      memset(inner, 0, ct * 8);
+      for (int k = 0; k < n1; ++k) {
+        const uint64_t* dg = diags[(u64)b * n1 * n2 + (u64)j * n1 + k];
+        if (!dg) continue;
+        live = 1;
+        hxo_mul_acc(c, inner, baby + (u64)k * ct, dg, n_q, 0);
+        hxo_mul_acc(c, inner + L, baby + (u64)k * ct + L, dg, n_q, 0);
+      }
+      if (!live) continue;
+      if (j == 0) {
+        ct_add(c, acc, inner, n_q);
+      } else if (!lazy) {
+        rot_by(c, tmp, inner, (int64_t)n1 * j, keys, n_q);
+        ct_add(c, acc, tmp, n_q);
+      } else { /* double hoisting: tau_j(c0) into acc, the PQ-basis key-switch sum into S */
+        const u64 r = reduce_amount((int64_t)n1 * j, slots), g = galois_of(c, r);
+        hxo_modup(c, D, inner + L, n_q);
+        hxo_ks_inner(c, U, D, keys[r], n_q, g);
+        hxo_add(c, S, S, U, n_q, K);
+        hxo_add(c, S + (u64)ext * n, S + (u64)ext * n, U + (u64)ext * n, n_q, K);
+        hxo_automorphism_ntt(c, tmp, inner, n_q, 0, g);
+        hxo_add(c, acc, acc, tmp, n_q, 0);
+        any_giant = 1;
+      }
+    }
+    if (any_giant) { /* one ModDown per output */
+      hxo_moddown_ntt(c, tmp, S, n_q, 2);
+      ct_add(c, acc, tmp, n_q);
+    }
+    if (rescale)
+      ct_rescale(c, out + (u64)b * 2 * (n_q - 1) * n, acc, n_q);
+    else
+      memcpy(out + (u64)b * ct, acc, ct * 8);
+  }
+  free(baby);
+  free(inner);
+  free(acc);
+  free(tmp);
+  free(S);
+  free(U);
+  free(D);
+}
+
+/* packed-row matvec with the assembly of DESIGN.md s3.9
+ * (SPEC.md:422 leaves it unpinned): per payload g, t = rescale(x (.) rows_g),
+ * t += Rot(t, s) for s = 1, 2, .., pad_cols / 2; for r < p (row = g p + r <
+ * rows): u = t (.) mask_r, u = Rot(u, r pad_cols - row) unless that is 0 mod
+ * slots, acc += u; out = rescale(acc). */
+void hxo_matvec_row(const hxo_ctx* c, uint64_t* out, const uint64_t* x, int n_q, int groups, int p, int rows,
+                    int pad_cols, const uint64_t* const* rows_pts, const uint64_t* const* masks,
+                    const uint64_t* const* keys) {
+  const u64 n = c->n, slots = n / 2;
+  const int n1q = n_q - 1;
+  const u64 ct = 2 * (u64)n_q * n, ct1 = 2 * (u64)n1q * n;
+  u64* m = (u64*)malloc(ct * 8);
+  u64* t = (u64*)malloc(ct1 * 8);
+  u64* r1 = (u64*)malloc(ct1 * 8);
+  u64* u = (u64*)malloc(ct1 * 8);
+  u64* acc = (u64*)calloc(ct1, 8);
+  for (int g = 0; g < groups; ++g) {
+    ct_mul_plain(c, m, x, rows_pts[g], n_q);
+    ct_rescale(c, t, m, n_q);
+    for (int s = 1; s < pad_cols; s <<= 1) {
+      rot_by(c, r1, t, s, keys, n1q);
+      ct_add(c, t, r1, n1q);
+    }
+    for (int r = 0; r < p; ++r) {
+      const int row = g * p + r;
+      if (row >= rows) break;
+      ct_mul_plain(c, u, t, masks[r], n1q);
+      const int64_t shift = (int64_t)r * pad_cols - row;
+      if (reduce_amount(shift, slots) != 0) {
+        rot_by(c, r1, u, shift, keys, n1q);
+        ct_add(c, acc, r1, n1q);
+      } else {
+        ct_add(c, acc, u, n1q);
+      }
+    }
+  }
+  ct_rescale(c, out, acc, n1q);
+  free(m);
+  free(t);
+  free(r1);
+  free(u);
+  free(acc);
+}
+
+/* ct-ct matmul as DESIGN.md s3.10 schedules
+ * it: a_j = rescale(A (.) colmask_j), b_j = rescale(B (.) rowmask_j), a_j =
+ * Rot(a_j, j), b_j = Rot(b_j, d j) for j >= 1; a_j += Rot(a_j, -2^i), b_j +=
+ * Rot(b_j, -d 2^i) for i < log2 d; out = rescale(sum_j mul_relin(a_j, b_j)). */
+void hxo_matmul_ctct(const hxo_ctx* c, uint64_t* out, const uint64_t* A, const uint64_t* B, int n_q, int d,
+                     const uint64_t* const* colmask, const uint64_t* const* rowmask, const uint64_t* rlk,
+                     const uint64_t* const* keys) {
+  const u64 n = c->n;
+  const int nb = n_q - 1;
+  const u64 ct = 2 * (u64)n_q * n, cb = 2 * (u64)nb * n;
+  int lg = 0;
+  while ((1 << lg) < d) ++lg;
+  u64* m = (u64*)malloc(ct * 8);
+  u64* a = (u64*)malloc(cb * 8);
+  u64* bb = (u64*)malloc(cb * 8);
+  u64* t = (u64*)malloc(cb * 8);
+  u64* pr = (u64*)malloc(cb * 8);
+  u64* C = (u64*)calloc(cb, 8);
+  for (int j = 0; j < d; ++j) {
+    ct_mul_plain(c, m, A, colmask[j], n_q);
+    ct_rescale(c, a, m, n_q);
+    ct_mul_plain(c, m, B, rowmask[j], n_q);
+    ct_rescale(c, bb, m, n_q);
+    if (j) {
+      rot_by(c, t, a, j, keys, nb);
+      memcpy(a, t, cb * 8);
+      rot_by(c, t, bb, (int64_t)d * j, keys, nb);
+      memcpy(bb, t, cb * 8);
+    }
+    for (int i = 0; i < lg; ++i) {
+      rot_by(c, t, a, -((int64_t)1 << i), keys, nb);
+      ct_add(c, a, t, nb);
+    }
+    for (int i = 0; i < lg; ++i) {
+      rot_by(c, t, bb, -((int64_t)d << i), keys, nb);
+      ct_add(c, bb, t, nb);
+    }
+    hxo_mul_relin(c, pr, a, bb, rlk, nb);
+    ct_add(c, C, pr, nb);
+  }
+  ct_rescale(c, out, C, nb);
+  free(m);
+  free(a);
+  free(bb);
+  free(t);
+  free(pr);
+  free(C);
+}

@@ -109,6 +109,29 @@ void hxo_mul_relin(const hxo_ctx* c, uint64_t* out_ct, const uint64_t* a, const 
 void hxo_bsgs_mac(const hxo_ctx* c, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,
                   int n1, int n2, int n_q);
 
+/* ---- linear-algebra drivers ----
+ * keys: indexed by rotation amount r in [0, N/2) -> standard-layout key
+ * (NULL where unused).  Plaintexts are NTT-form [n_q][N] words. */
+/* BSGS matvec: baby steps hoisted; per row block b the inner sums over the
+ * NON-NULL diagonals diags[b n1 n2 + j n1 + k]; giant groups j in
+ * [giant_begin, giant_end) (giant_end < 0: n2) rotated by n1 j and summed.
+ * lazy = 1: double hoisting -- the giant rotations' key-switch products are
+ * summed in the PQ basis and ModDown runs once per output.
+ * out [blocks][2][n_q - rescale][N]. */
+void hxo_matvec_bsgs(const hxo_ctx* c, uint64_t* out, const uint64_t* x, int n_q, int n1, int n2, int blocks,
+                     const uint64_t* const* diags, const uint64_t* const* keys, int giant_begin, int giant_end,
+                     int rescale, int lazy);
+/* packed-row matvec; rows_pts [groups] at n_q limbs, masks [p] at n_q - 1 limbs;
+ * out [2][n_q - 2][N] */
+void hxo_matvec_row(const hxo_ctx* c, uint64_t* out, const uint64_t* x, int n_q, int groups, int p, int rows,
+                    int pad_cols, const uint64_t* const* rows_pts, const uint64_t* const* masks,
+                    const uint64_t* const* keys);
+/* ct-ct matmul of d x d row-major operands; masks [d] at n_q limbs;
+ * rlk standard layout; out [2][n_q - 2][N] */
+void hxo_matmul_ctct(const hxo_ctx* c, uint64_t* out, const uint64_t* A, const uint64_t* B, int n_q, int d,
+                     const uint64_t* const* colmask, const uint64_t* const* rowmask, const uint64_t* rlk,
+                     const uint64_t* const* keys);
+
 /* ---- keys / encryption ---- */
 /* s_full, sp_full: NTT form over the full basis (n_chain + K limbs);
  * a_full: [dnum_max][n_chain+K][N] uniform residues (used as NTT-form values);

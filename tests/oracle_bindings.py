@@ -80,6 +80,12 @@ def oracle_lib():
             "hxo_keygen_ksk": [v, u64p, u64p, u64p, u64p, i64p],
             "hxo_decrypt": [v, u64p, u64p, u64p, C.c_int],
             "hxo_encrypt_sk": [v, u64p, u64p, u64p, u64p, i64p, C.c_int],
+            "hxo_matvec_bsgs": [v, u64p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(u64p),
+                                C.POINTER(u64p), C.c_int, C.c_int, C.c_int, C.c_int],
+            "hxo_matvec_row": [v, u64p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(u64p),
+                               C.POINTER(u64p), C.POINTER(u64p)],
+            "hxo_matmul_ctct": [v, u64p, u64p, u64p, C.c_int, C.c_int, C.POINTER(u64p), C.POINTER(u64p), u64p,
+                                C.POINTER(u64p)],
         }.items():
             f = getattr(L, name)
             f.argtypes = args
@@ -260,6 +266,41 @@ class Oracle:
     def bsgs_mac(self, baby, diags, n1, n2, n_q):
         o = self.zeros(n2, 2, n_q)
         self.L.hxo_bsgs_mac(self.h, ptr(o), ptr(np.ascontiguousarray(baby)), ptr(np.ascontiguousarray(diags)), n1, n2, n_q)
+        return o
+
+    # ---- linear-algebra drivers (keys: {amount: standard-layout key array}) ----
+    def _keytab(self, keys: dict):
+        slots = self.n // 2
+        tab = (u64p * slots)()
+        for r, k in keys.items():
+            tab[r % slots] = ptr(k)
+        return tab
+
+    @staticmethod
+    def _ptab(arrs):
+        tab = (u64p * max(1, len(arrs)))()
+        for i, a in enumerate(arrs):
+            tab[i] = ptr(a) if a is not None else None
+        return tab
+
+    def matvec_bsgs(self, x, n_q, n1, n2, blocks, diags, keys, giant=(0, -1), rescale=True, lazy=False):
+        """diags: list (blocks * n1 * n2) of [n_q][N] arrays or None"""
+        o = self.zeros(blocks, 2, n_q - (1 if rescale else 0))
+        dt, kt = self._ptab(diags), self._keytab(keys)
+        self.L.hxo_matvec_bsgs(self.h, ptr(o), ptr(np.ascontiguousarray(x)), n_q, n1, n2, blocks, dt, kt,
+                               giant[0], giant[1], 1 if rescale else 0, 1 if lazy else 0)
+        return o
+
+    def matvec_row(self, x, n_q, p, rows, pad_cols, rows_pts, masks, keys):
+        o = self.zeros(2, n_q - 2)
+        self.L.hxo_matvec_row(self.h, ptr(o), ptr(np.ascontiguousarray(x)), n_q, len(rows_pts), p, rows, pad_cols,
+                              self._ptab(rows_pts), self._ptab(masks), self._keytab(keys))
+        return o
+
+    def matmul_ctct(self, A, B, n_q, d, colmask, rowmask, rlk, keys):
+        o = self.zeros(2, n_q - 2)
+        self.L.hxo_matmul_ctct(self.h, ptr(o), ptr(np.ascontiguousarray(A)), ptr(np.ascontiguousarray(B)), n_q, d,
+                               self._ptab(colmask), self._ptab(rowmask), ptr(rlk), self._keytab(keys))
         return o
 
     def keygen_ksk(self, s_full, sp_full, a_full, e):
