@@ -392,7 +392,7 @@ def sharded_bsgs_bench(torch, dist, chain, special, rank, world, rows=11008, col
     prep = time.perf_counter() - t0
     ct = be.encrypt(np.tile(x, be.slots // cols), lvl)
     allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else (lambda t: None)
-    outs, rep = sharded_matvec(be, M, ct, lvl + 1, N, allreduce, torch)  # warm-up + correctness
+    outs, rep = sharded_matvec(be, M, ct, lvl + 1, len(special), allreduce, torch, world, chain + special)  # warm-up + correctness
     y = be.decrypt(outs[0])[:rows]  # stacked: one output, y[row] in slot row
     err = float(np.abs(y - W @ x).max())
     del outs
@@ -402,7 +402,7 @@ def sharded_bsgs_bench(torch, dist, chain, special, rank, world, rows=11008, col
     torch.cuda.synchronize()
     e0.record()
     for _ in range(iters):
-        outs, rep = sharded_matvec(be, M, ct, lvl + 1, N, allreduce, torch)
+        outs, rep = sharded_matvec(be, M, ct, lvl + 1, len(special), allreduce, torch, world, chain + special)
         del outs
     e1.record()
     torch.cuda.synchronize()

@@ -101,8 +101,12 @@ class GpuLatticeBackend final : public SlotBackend {
   // per-block MAC launches write inner sums in [n2][blocks] order, then giant
   // step j of every block is rotated with one read of key n1 j
   // (hx_rotate_grouped) and summed in one pass.  Same trace as per-block.
-  // allow_empty: a block without live diagonals yields a zero ciphertext
-  // (giant-step shards, linalg.hpp BsgsShard) instead of an error.
+  // The giant rotations share one ModDown per output (double hoisting,
+  // hx_rotate_grouped_sum).  allow_empty (giant-step shards, linalg.hpp
+  // BsgsShard): a block without live diagonals is no error, and each output
+  // is a PQ-BASIS PARTIAL -- its buffer holds T ([2][n_q][N], the ciphertext
+  // words the handle shows) followed by S ([2][n_q + K][N], the unreduced
+  // key-switch sum); ranks sum both, then shard_finish() applies the ModDown.
   std::vector<Ciphertext> bsgs_blocks(const std::vector<Ciphertext>& baby,
                                       const std::vector<Plaintext>& diags, int n1, int n2, int blocks,
                                       bool allow_empty = false);
@@ -125,6 +129,13 @@ class GpuLatticeBackend final : public SlotBackend {
   // operand, d ct-ct products + relinearisation in one launch, one strided sum
   // and the final rescale.  Same trace records as the SlotOps form.
   Ciphertext matmul(const Ciphertext& A, const Ciphertext& B, int d);
+
+  // y = T + (ModDown(S_0), ModDown(S_1)) of a summed PQ partial (words =
+  // [T][S] as bsgs_blocks(allow_empty) lays them out), at like's level / scale
+  Ciphertext shard_finish(const Ciphertext& like, const std::uint64_t* words);
+  std::size_t shard_partial_words(int level) const {
+    return (std::size_t)2 * (2 * nq(level) + params_.special_primes.size()) * params_.ring_degree;
+  }
 
   // ---- raw access ----
   hx_ctx* device_context() const { return ctx_; }

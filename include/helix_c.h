@@ -92,9 +92,12 @@ int hxc_matvec_tokens(hxc_backend* b, const hxc_mat* m, const hxc_ct* const* xs,
 
 /* ---- giant-step sharding of BSGS (multi-GPU, one process per GPU) ----
  * rank r of world G encodes only its giant groups (helix::bsgs_shard) and
- * returns PRE-RESCALE partial outputs; the caller sums the partial words of all
- * ranks (e.g. NCCL all-reduce of int64 = wrapping uint64 sum), reduces mod q
- * (hx_reduce_mod_q), wraps the words (hxc_ct_like) and rescales once. */
+ * returns PQ-BASIS PARTIAL outputs (double-hoisted giant steps: the ModDown
+ * waits for the sum of all ranks): each handle's device buffer holds
+ * hxc_shard_partial_words() words, T [2][n_q][N] then S [2][n_q + K][N].  The
+ * caller sums the partial words of all ranks (NCCL all-reduce of int64 =
+ * wrapping uint64 sum), reduces T and S mod q (hx_reduce_mod_q with n_p = 0 /
+ * K), finishes with hxc_shard_finish (T + ModDown(S)) and rescales once. */
 hxc_mat* hxc_matrix_prepare_shard(hxc_backend* b, const double* A, int rows, int cols, int level,
                                   int rank, int world, int stacked);
 int hxc_matvec_shard(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct** out, int cap,
@@ -102,6 +105,11 @@ int hxc_matvec_shard(hxc_backend* b, const hxc_mat* m, const hxc_ct* x, hxc_ct**
 /* a new ciphertext with the level / scale of `like` and words copied from the
  * device buffer `words` ([2][level+1][N]) */
 hxc_ct* hxc_ct_like(hxc_backend* b, const hxc_ct* like, const uint64_t* words);
+/* words of one shard partial (T and S) at like's level */
+long long hxc_shard_partial_words(hxc_backend* b, const hxc_ct* like);
+/* the pre-rescale output T + (ModDown(S_0), ModDown(S_1)) of a summed, reduced
+ * partial (device words laid out as hxc_matvec_shard returns them) */
+hxc_ct* hxc_shard_finish(hxc_backend* b, const hxc_ct* like, const uint64_t* words);
 
 /* ct-ct matmul of row-major d x d operands */
 hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_report* rep);

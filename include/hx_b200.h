@@ -140,6 +140,23 @@ int hx_rotate_multi(hx_ctx* ctx, uint64_t* out, const uint64_t* in, const uint64
  * out [R][E][2][n_q][N]. */
 int hx_rotate_grouped(hx_ctx* ctx, uint64_t* out, const uint64_t* in, const uint64_t* const* keys,
                       const uint64_t* galois, int R, int E, int n_q, void* stream);
+/* Double-hoisted giant-step sum (BSGS):
+ *   out[e] = base[e] + sum_{r < R} Rot_{g_r}(in[r][e])
+ * with ONE ModDown per output e instead of one per rotation: the key-switch
+ * products tau_r(U_r) are summed in the PQ basis (S_e = sum_r tau_r(U_r),
+ * [E][2][n_q + K][N]) together with T_e = base[e] + (sum_r tau_r(c0_r), 0),
+ * then out[e] = T_e + (ModDown(S_e,0), ModDown(S_e,1)).  in [R][E][2][n_q][N],
+ * base [E][2][n_q][N] or NULL, keys[r] rotation layout.  pq_partial != NULL:
+ * stop before the ModDown -- write S to pq_partial and T to out (the partial
+ * a giant-step shard exchanges; finish with hx_moddown_add after the sum of
+ * the ranks' S and T, each reduced mod q). */
+int hx_rotate_grouped_sum(hx_ctx* ctx, uint64_t* out, uint64_t* pq_partial, const uint64_t* in,
+                          const uint64_t* base, const uint64_t* const* keys, const uint64_t* galois, int R, int E,
+                          int n_q, void* stream);
+/* out[e] = add[e] + (ModDown(pq[e][0]), ModDown(pq[e][1])); pq [E][2][n_q+K][N],
+ * add [E][2][n_q][N] or NULL */
+int hx_moddown_add(hx_ctx* ctx, uint64_t* out, const uint64_t* pq, const uint64_t* add, int E, int n_q,
+                   void* stream);
 /* tensor (LatticeContext::mul x4): a, b [batch][2][n_q][N] -> [batch][3][n_q][N] */
 int hx_tensor(hx_ctx* ctx, uint64_t* out3, const uint64_t* a, const uint64_t* b, int batch,
               int n_q, void* stream);

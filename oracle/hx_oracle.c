@@ -800,8 +800,12 @@ static u64 galois_of(const hxo_ctx* c, u64 r) {
 
 void hxo_matvec_bsgs(const hxo_ctx* c, uint64_t* out, const uint64_t* x, int n_q, int n1, int n2, int blocks,
                      const uint64_t* const* diags, const uint64_t* const* keys, int giant_begin, int giant_end,
-                     int rescale, int lazy) {
+                     int rescale, int lazy, int partial) {
   const u64 n = c->n, L = (u64)n_q * n, ct = 2 * L;
+  if (partial) {
+    lazy = 1;
+    rescale = 0;
+  }
   const int K = c->n_special, ext = n_q + K;
   const int gb = giant_begin, ge = giant_end < 0 ? n2 : giant_end;
   /* baby steps Rot_k(x), k < n1: one ModUp shared by all (hoisting convention) */
@@ -855,6 +859,12 @@ void hxo_matvec_bsgs(const hxo_ctx* c, uint64_t* out, const uint64_t* x, int n_q
         hxo_add(c, acc, acc, tmp, n_q, 0);
         any_giant = 1;
       }
+    }
+    if (partial) { /* giant-step shard: [T][S], the ModDown after the ranks' sum */
+      u64* o = out + (u64)b * (ct + (u64)2 * ext * n);
+      memcpy(o, acc, ct * 8);
+      memcpy(o + ct, S, (u64)2 * ext * n * 8);
+      continue;
     }
     if (any_giant) { /* one ModDown per output */
       hxo_moddown_ntt(c, tmp, S, n_q, 2);

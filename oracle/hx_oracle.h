@@ -117,10 +117,12 @@ void hxo_bsgs_mac(const hxo_ctx* c, uint64_t* inner, const uint64_t* baby, const
  * [giant_begin, giant_end) (giant_end < 0: n2) rotated by n1 j and summed.
  * lazy = 1: double hoisting -- the giant rotations' key-switch products are
  * summed in the PQ basis and ModDown runs once per output.
- * out [blocks][2][n_q - rescale][N]. */
+ * out [blocks][2][n_q - rescale][N].  partial = 1 (giant-step shard, implies
+ * lazy, no rescale): out [blocks][T 2 n_q + S 2 (n_q + K)][N], the PQ-basis
+ * partial before the ModDown. */
 void hxo_matvec_bsgs(const hxo_ctx* c, uint64_t* out, const uint64_t* x, int n_q, int n1, int n2, int blocks,
                      const uint64_t* const* diags, const uint64_t* const* keys, int giant_begin, int giant_end,
-                     int rescale, int lazy);
+                     int rescale, int lazy, int partial);
 /* packed-row matvec; rows_pts [groups] at n_q limbs, masks [p] at n_q - 1 limbs;
  * out [2][n_q - 2][N] */
 void hxo_matvec_row(const hxo_ctx* c, uint64_t* out, const uint64_t* x, int n_q, int groups, int p, int rows,

@@ -125,6 +125,52 @@ __global__ void permute_multi_kernel(u64* out, const u64* in, PermuteMulti P) {
       __ldg(in + ((long long)r * P.per + e) * P.in_stride + l * N + src);
 }
 
+// Permuted sum (double-hoisted BSGS giant steps): for element e and limb l
+//   out[e][l][t] (+)= sum_{r < R} in[r][e][l][ntt_auto_index(t, g_r)]  mod q_l,
+// i.e. sum_r tau_{g_r}(in_r) in the NTT domain.  Limb l of an element is limb
+// l % lpoly of a poly whose first n_q limbs are chain primes and the rest
+// special primes (PQ-basis key-switch products or Q-basis c0 polys).  Four
+// terms' loads are issued before their adds (memory-level parallelism).
+constexpr int kPermSumMax = 64;
+struct PermSumArgs {
+  u64* out;
+  long long out_estride;
+  const u64* in;
+  long long in_rstride, in_estride;
+  const PrimeConst* pc;
+  int lpoly, n_q, n_chain, R, logn, accumulate;
+  u32 g[kPermSumMax];
+};
+__global__ void __launch_bounds__(256) perm_sum_kernel(PermSumArgs A) {
+  const long long N = 1ll << A.logn;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = blockIdx.y;
+  const long long e = blockIdx.z;
+  const int lp = l % A.lpoly;
+  const u64 q = A.pc[lp < A.n_q ? lp : A.n_chain + (lp - A.n_q)].q;
+  u64* o = A.out + e * A.out_estride + (long long)l * N + t;
+  const u64* base = A.in + e * A.in_estride + (long long)l * N;
+  u64 acc = A.accumulate ? *o : 0ull;
+  int r = 0;
+  for (; r + 4 <= A.R; r += 4) {
+    u64 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const u32 g = A.g[r + k];
+      const int src = g == 1 ? t : (int)ntt_auto_index((u32)t, g, A.logn);
+      v[k] = __ldcs(base + (long long)(r + k) * A.in_rstride + src);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc = addmod(acc, v[k], q);
+  }
+  for (; r < A.R; ++r) {
+    const u32 g = A.g[r];
+    const int src = g == 1 ? t : (int)ntt_auto_index((u32)t, g, A.logn);
+    acc = addmod(acc, __ldcs(base + (long long)r * A.in_rstride + src), q);
+  }
+  *o = acc;
+}
+
 // from_i64 (rns_poly.cpp:218-227): small signed ints -> every limb.
 // v is [batch][N] int64; out [batch][limbs][N].
 __global__ void from_i64_kernel(u64* out, const long long* v, const PrimeConst* pc, LimbTable lt,

@@ -819,6 +819,39 @@ void rotate_batch_from_digits(hx_ctx* c, u64* out, const u64* in, const u64* dig
   }
 }
 
+// sum_r tau_{g_r}(in_r) into out (accumulate: out += ...), elements e < E
+// of `limbs` limbs (polys of lpoly limbs, the first n_q chain primes)
+void perm_sum(hx_ctx* c, u64* out, long long out_estride, const u64* in, long long in_rstride,
+              long long in_estride, const std::vector<u64>& g, long long E, int limbs, int lpoly, int n_q,
+              bool accumulate, cudaStream_t s) {
+  const int th = pt_threads(c);
+  for (std::size_t r0 = 0; r0 < g.size(); r0 += hx::kPermSumMax) {
+    const int nr = (int)std::min<std::size_t>(hx::kPermSumMax, g.size() - r0);
+    hx::PermSumArgs A;
+    A.out = out;
+    A.out_estride = out_estride;
+    A.in = in + (long long)r0 * in_rstride;
+    A.in_rstride = in_rstride;
+    A.in_estride = in_estride;
+    A.pc = c->d_pc;
+    A.lpoly = lpoly;
+    A.n_q = n_q;
+    A.n_chain = c->n_chain;
+    A.R = nr;
+    A.logn = c->logn;
+    A.accumulate = (accumulate || r0) ? 1 : 0;
+    for (int r = 0; r < nr; ++r) A.g[r] = (hx::u32)g[r0 + r];
+    for (long long e0 = 0; e0 < E; e0 += 65535) {
+      const long long ne = std::min<long long>(65535, E - e0);
+      hx::PermSumArgs B = A;
+      B.out += e0 * out_estride;
+      B.in += e0 * in_estride;
+      hx::perm_sum_kernel<<<dim3((unsigned)(c->N() / th), (unsigned)limbs, (unsigned)ne), th, 0, s>>>(B);
+      launched(c, "perm_sum_kernel");
+    }
+  }
+}
+
 // Host-buffer round trip, pipelined: the batch is cut into chunks; chunk i's
 // host->device copy (stream h), compute (stream s) and device->host copy
 // (stream d) overlap with chunks i-1 / i+1 on double-buffered device slots.
@@ -1532,6 +1565,76 @@ int hx_rotate_grouped(hx_ctx* c, uint64_t* out, const uint64_t* in, const uint64
       rotate_batch_from_digits(c, (u64*)out + (long long)r0 * E * ct, ip, D.p, kc, gc, false, E, n_q, S(s),
                                fuse);
     }
+  });
+}
+
+int hx_rotate_grouped_sum(hx_ctx* c, uint64_t* out, uint64_t* pq_partial, const uint64_t* in,
+                          const uint64_t* base, const uint64_t* const* keys, const uint64_t* galois, int R, int E,
+                          int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_COUNT(R);
+    HX_COUNT(E);
+    check_nq(c, n_q);
+    HX_REQUIRE(R >= 0 && E >= 1, "R >= 0, E >= 1");
+    const long long N = c->N(), ct = 2ll * n_q * N;
+    const int K = c->n_special, ext = n_q + K;
+    const long long uw = 2ll * ext * N;  // one PQ-basis key-switch product (2 polys)
+    for (int r = 0; r < R; ++r)
+      HX_REQUIRE((galois[r] & 1) && galois[r] < 2 * (u64)N, "galois element");
+    // T = base + sum_r tau_r(c0_r) (c1 part: base's), S = sum_r tau_r(U'_r)
+    DBuf Tb(pq_partial ? 0 : E * ct, S(s), c), Sb(pq_partial ? 0 : E * uw, S(s), c);
+    u64* T = pq_partial ? (u64*)out : Tb.p;
+    u64* Sp = pq_partial ? (u64*)pq_partial : Sb.p;
+    if (base)
+      cuda_ok(cudaMemcpyAsync(T, base, (size_t)(E * ct) * 8, cudaMemcpyDeviceToDevice, S(s)), "d2d");
+    else
+      cuda_ok(cudaMemsetAsync(T, 0, (size_t)(E * ct) * 8, S(s)), "memset");
+    cuda_ok(cudaMemsetAsync(Sp, 0, (size_t)(E * uw) * 8, S(s)), "memset");
+    // keys in chunks so the ModUp digits + products of a chunk stay within ~16 GB
+    const long long per_key = (long long)E * (c->dnum(n_q) + 2) * ext * N * 8;
+    const int Rc = (int)std::max(1ll, std::min<long long>(std::max(R, 1), (16ll << 30) / per_key));
+    for (int r0 = 0; r0 < R; r0 += Rc) {
+      const int nr = std::min(Rc, R - r0);
+      const u64* ip = (const u64*)in + (long long)r0 * E * ct;
+      std::vector<const u64*> kc;
+      std::vector<u64> gc;
+      for (int r = r0; r < r0 + nr; ++r) {
+        kc.push_back((const u64*)keys[r]);
+        gc.push_back((u64)galois[r]);
+      }
+      DBuf D((long long)nr * E * c->dnum(n_q) * ext * N, S(s), c);
+      DBuf U((long long)nr * E * uw, S(s), c);
+      const bool fuse = row_inner_ok(c, n_q, kc);
+      modup(c, D.p, ip + (long long)n_q * N, ct, (long long)nr * E, n_q, S(s), false, fuse);
+      const long long dstride = (long long)c->dnum(n_q) * ext * N;
+      for (int k0 = 0; k0 < nr; k0 += hx::kMaxKeys) {
+        const int nk = std::min(hx::kMaxKeys, nr - k0);
+        const std::vector<const u64*> kk(kc.begin() + k0, kc.begin() + k0 + nk);
+        ks_inner_multi(c, U.p + (long long)k0 * E * uw, D.p + (long long)k0 * E * dstride, kk, false, E, n_q, 1,
+                       S(s), ip + (long long)k0 * E * ct + (long long)n_q * N, ct, fuse);
+      }
+      // rotation-layout keys: U' = tau_r^-1(U_r), so tau_r(U'_r) is the product of the rotation
+      perm_sum(c, Sp, uw, U.p, E * uw, uw, gc, E, 2 * ext, ext, n_q, true, S(s));
+      perm_sum(c, T, ct, ip, E * ct, ct, gc, E, n_q, n_q, n_q, true, S(s));
+    }
+    if (pq_partial) return;
+    // one ModDown per output ciphertext: out = T + (ModDown(S_0), ModDown(S_1))
+    moddown(c, (u64*)out, (long long)n_q * N, Sp, (long long)ext * N, 2 * E, n_q, T, (long long)n_q * N, 1,
+            S(s), 1, 0, nullptr);
+  });
+}
+
+int hx_moddown_add(hx_ctx* c, uint64_t* out, const uint64_t* pq, const uint64_t* add, int E, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_COUNT(E);
+    check_nq(c, n_q);
+    if (!E) return;
+    const long long N = c->N();
+    const int ext = n_q + c->n_special;
+    moddown(c, (u64*)out, (long long)n_q * N, (const u64*)pq, (long long)ext * N, 2ll * E, n_q, (const u64*)add,
+            add ? (long long)n_q * N : 0, 1, S(s), 1, 0, nullptr);
   });
 }
 

@@ -806,27 +806,41 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
     gs.push_back(galois(r));
     J.push_back(j);
   }
-  auto out = dev((std::size_t)E * ctw);
-  if (!J.empty()) {
+  // y = inner_0 + sum_j Rot(inner_j) with ONE ModDown per output (double
+  // hoisting): the giant rotations' key-switch products are
+  // summed in the PQ basis (hx_rotate_grouped_sum).  Giant-step shards
+  // (allow_empty) stop before the ModDown: each output is the PQ partial
+  // [T = 2 n_q limbs][S = 2 (n_q + K) limbs] that the ranks sum (shard.py).
+  const bool partial = allow_empty;
+  const std::size_t uw = (std::size_t)2 * (nqv + params_.special_primes.size()) * N;
+  const std::size_t pw = partial ? ctw + uw : ctw;
+  auto out = dev((std::size_t)E * pw);
+  if (J.empty() && !partial) {
+    cuda_ck(cudaMemcpyAsync(out->ptr, inner->ptr, jstride * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
+  } else {
     std::shared_ptr<DeviceBuffer> src;
     const u64* srcp = inner->ptr + jstride;  // groups 1..n2-1 are contiguous
-    if ((int)J.size() != n2 - 1) {
+    if (!J.empty() && (int)J.size() != n2 - 1) {
       src = dev(J.size() * jstride);
       for (std::size_t i = 0; i < J.size(); ++i)
         cuda_ck(cudaMemcpyAsync(src->ptr + i * jstride, inner->ptr + J[i] * jstride, jstride * 8,
                                 cudaMemcpyDeviceToDevice, nullptr), "d2d");
       srcp = src->ptr;
     }
-    auto rotated = dev(J.size() * jstride);
-    ck(hx_rotate_grouped(ctx_, rotated->ptr, srcp, keys.data(), gs.data(), (int)J.size(), E, nqv, nullptr),
-       "rotate_grouped");
-    // y = inner_0 + sum_j Rot(inner_j): rotated terms summed in one pass
-    ck(hx_sum_strided(ctx_, out->ptr, rotated->ptr, (int)J.size(), (long long)jstride, 2 * E, (long long)ptw,
-                      (long long)ptw, nqv, nullptr),
-       "sum");
-    ck(hx_add(ctx_, out->ptr, out->ptr, inner->ptr, 2 * E, nqv, 0, nullptr), "add");
-  } else {
-    cuda_ck(cudaMemcpyAsync(out->ptr, inner->ptr, jstride * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
+    if (!partial) {
+      ck(hx_rotate_grouped_sum(ctx_, out->ptr, nullptr, srcp, inner->ptr, keys.data(), gs.data(), (int)J.size(), E,
+                               nqv, nullptr),
+         "rotate_grouped_sum");
+    } else {
+      auto tb = dev((std::size_t)E * ctw), sb = dev((std::size_t)E * uw);
+      ck(hx_rotate_grouped_sum(ctx_, tb->ptr, sb->ptr, srcp, inner->ptr, keys.data(), gs.data(), (int)J.size(), E,
+                               nqv, nullptr),
+         "rotate_grouped_sum");
+      cuda_ck(cudaMemcpy2DAsync(out->ptr, pw * 8, tb->ptr, ctw * 8, ctw * 8, E, cudaMemcpyDeviceToDevice, nullptr),
+              "memcpy2d");
+      cuda_ck(cudaMemcpy2DAsync(out->ptr + ctw, pw * 8, sb->ptr, uw * 8, uw * 8, E, cudaMemcpyDeviceToDevice, nullptr),
+              "memcpy2d");
+    }
   }
   std::vector<std::vector<Ciphertext>> res(T);
   for (int b = 0; b < blocks; ++b) {
@@ -840,8 +854,16 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
   }
   for (int t = 0; t < T; ++t)
     for (int b = 0; b < blocks; ++b)
-      res[t].push_back(wrap(out, ((std::size_t)t * blocks + b) * ctw, level, out_scale));
+      res[t].push_back(wrap(out, ((std::size_t)t * blocks + b) * pw, level, out_scale));
   return res;
+}
+
+Ciphertext GpuLatticeBackend::shard_finish(const Ciphertext& like, const std::uint64_t* words) {
+  const int n = nq(like.level);
+  const std::size_t N = params_.ring_degree, ctw = (std::size_t)2 * n * N;
+  auto buf = dev(ctw);
+  ck(hx_moddown_add(ctx_, buf->ptr, words + ctw, words, 1, n, nullptr), "moddown_add");
+  return wrap(buf, 0, like.level, like.scale);
 }
 
 std::vector<std::vector<Ciphertext>> GpuLatticeBackend::rotate_many_tokens(const std::vector<Ciphertext>& xs,

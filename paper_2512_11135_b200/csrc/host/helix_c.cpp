@@ -251,6 +251,14 @@ hxc_ct* hxc_ct_like(hxc_backend* b, const hxc_ct* like, const uint64_t* words) {
   });
 }
 
+long long hxc_shard_partial_words(hxc_backend* b, const hxc_ct* like) {
+  return (long long)b->b->shard_partial_words(like->c.level);
+}
+
+hxc_ct* hxc_shard_finish(hxc_backend* b, const hxc_ct* like, const uint64_t* words) {
+  return guard<hxc_ct*>(nullptr, [&] { return wrap(b->b->shard_finish(like->c, words)); });
+}
+
 hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_report* rep) {
   return guard<hxc_ct*>(nullptr, [&] {
     auto r = matmul_ctct(*b->b, A->c, B->c, d);

@@ -69,6 +69,8 @@ def lib():
         "hxc_matvec_tokens": (i32, [v, v, C.POINTER(v), i32, C.POINTER(v), i32, rp]),
         "hxc_matvec_shard": (i32, [v, v, v, C.POINTER(v), i32, rp]),
         "hxc_ct_like": (v, [v, v, v]),
+        "hxc_shard_partial_words": (C.c_longlong, [v, v]),
+        "hxc_shard_finish": (v, [v, v, v]),
         "hxc_matmul_rotations": (i32, [i32, C.POINTER(C.c_int64), i32]),
         "hxc_polyeval": (v, [v, v, f64p, i32, i32, C.c_double, C.c_double, rp]),
         "hxc_predicted_rotations": (C.c_longlong, [i32, i32, i32, i64]),
@@ -300,6 +302,13 @@ class Backend:
         if k < 0:
             raise _err()
         return [Ct(self, outs[i]) for i in range(k)], r.as_dict()
+
+    def shard_partial_words(self, like):
+        return int(self.L.hxc_shard_partial_words(self.h, like.h))
+
+    def shard_finish(self, like, words_ptr):
+        """pre-rescale output of a summed, reduced shard partial (T + ModDown(S))"""
+        return Ct(self, self.L.hxc_shard_finish(self.h, like.h, words_ptr))
 
     def ct_like(self, like, words_ptr):
         return Ct(self, self.L.hxc_ct_like(self.h, like.h, words_ptr))

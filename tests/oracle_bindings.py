@@ -81,7 +81,7 @@ def oracle_lib():
             "hxo_decrypt": [v, u64p, u64p, u64p, C.c_int],
             "hxo_encrypt_sk": [v, u64p, u64p, u64p, u64p, i64p, C.c_int],
             "hxo_matvec_bsgs": [v, u64p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(u64p),
-                                C.POINTER(u64p), C.c_int, C.c_int, C.c_int, C.c_int],
+                                C.POINTER(u64p), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int],
             "hxo_matvec_row": [v, u64p, u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(u64p),
                                C.POINTER(u64p), C.POINTER(u64p)],
             "hxo_matmul_ctct": [v, u64p, u64p, u64p, C.c_int, C.c_int, C.POINTER(u64p), C.POINTER(u64p), u64p,
@@ -283,12 +283,17 @@ class Oracle:
             tab[i] = ptr(a) if a is not None else None
         return tab
 
-    def matvec_bsgs(self, x, n_q, n1, n2, blocks, diags, keys, giant=(0, -1), rescale=True, lazy=False):
-        """diags: list (blocks * n1 * n2) of [n_q][N] arrays or None"""
-        o = self.zeros(blocks, 2, n_q - (1 if rescale else 0))
+    def matvec_bsgs(self, x, n_q, n1, n2, blocks, diags, keys, giant=(0, -1), rescale=True, lazy=False,
+                    partial=False):
+        """diags: list (blocks * n1 * n2) of [n_q][N] arrays or None.  partial:
+        giant-step shard PQ partials [blocks][(2 n_q + 2 (n_q + K)) N] words"""
+        if partial:
+            o = np.zeros((blocks, (4 * n_q + 2 * len(self.special)) * self.n), dtype=np.uint64)
+        else:
+            o = self.zeros(blocks, 2, n_q - (1 if rescale else 0))
         dt, kt = self._ptab(diags), self._keytab(keys)
         self.L.hxo_matvec_bsgs(self.h, ptr(o), ptr(np.ascontiguousarray(x)), n_q, n1, n2, blocks, dt, kt,
-                               giant[0], giant[1], 1 if rescale else 0, 1 if lazy else 0)
+                               giant[0], giant[1], 1 if rescale else 0, 1 if lazy else 0, 1 if partial else 0)
         return o
 
     def matvec_row(self, x, n_q, p, rows, pad_cols, rows_pts, masks, keys):

@@ -115,8 +115,9 @@ def test_config1_matvec_64x64(method):
 @pytest.mark.parametrize("keys", ["full", "compressed"])
 def test_bsgs_matvec_bit_exact_vs_oracle(keys):
     """The fused BSGS pipeline (hoisted baby steps, streaming MAC, batched giant
-    rotations, rescale) reproduces the oracle's ciphertext word for word, with
-    full and with compressed (seeded) key storage."""
+    rotations with one lazy ModDown, rescale) reproduces the oracle's
+    ciphertext word for word, with full and with compressed (seeded) key
+    storage."""
     from paper_2512_11135_b200.helix import BSGS
 
     p, be = backend("c1" if keys == "full" else "c1+ck")
@@ -146,15 +147,10 @@ def test_bsgs_matvec_bit_exact_vs_oracle(keys):
         # rotation layout = tau_{g^-1}(standard)  =>  standard = tau_g(rotation layout)
         return np.ascontiguousarray(orc.automorphism_ntt(rot, rot.shape[0], 0, g).reshape(orc.dnum(nq), 2, nq + K, N))
 
-    diags = np.stack([d2h(M.payload_ptr(i), nq * N).reshape(nq, N) for i in range(64)])
-    keys = [std_key(k) for k in range(1, n1)]
-    baby = np.concatenate([xw[None], orc.rotate_hoisted(xw, keys, [galois_elt(k, N) for k in range(1, n1)], nq)])
-    inner = orc.bsgs_mac(np.ascontiguousarray(baby), diags, n1, n2, nq)
-    acc = inner[0].copy()
-    for j in range(1, n2):
-        r = orc.rotate(np.ascontiguousarray(inner[j]), std_key(n1 * j), nq, galois_elt(n1 * j, N))
-        acc = np.stack([orc.binop("hxo_add", acc[c], r[c], nq) for c in range(2)])
-    exp = np.stack([orc.rescale_ntt(np.ascontiguousarray(acc[c]), nq) for c in range(2)])
+    diags = [d2h(M.payload_ptr(i), nq * N).reshape(nq, N) for i in range(64)]
+    keys = {k: std_key(k) for k in list(range(1, n1)) + [n1 * j for j in range(1, n2)]}
+    # baby steps hoisted, MAC, giant steps double hoisted (one ModDown), rescale
+    exp = orc.matvec_bsgs(xw, nq, n1, n2, 1, diags, keys, lazy=True)[0]
     assert np.array_equal(got, exp)
 
 
@@ -216,7 +212,7 @@ def test_giant_step_shards_bit_exact(world, stacked):
     import torch
 
     from paper_2512_11135_b200.helix import BSGS, BSGS_STACKED
-    from paper_2512_11135_b200.shard import gather_words, reduce_partials, shard_range
+    from paper_2512_11135_b200.shard import finish, gather_words, reduce_partials, shard_range
 
     p, be = backend("c2s")
     N = 1 << p["logn"]
@@ -240,12 +236,13 @@ def test_giant_step_shards_bit_exact(world, stacked):
         parts, rep = be.matvec_shard(Ms, ct)
         assert len(parts) == nout and rep["levels_consumed"] == 0
         rots += rep["rotations"] - (M.info()["n1"] - 1)  # baby steps are replicated per rank
-        w = gather_words(parts, nq, N, torch)
+        w = gather_words(parts, be.shard_partial_words(parts[0]), torch)
         total = w if total is None else total + w  # int64 wrap == u64 sum
         like = parts
     torch.cuda.synchronize()
-    reduce_partials(be.device_context(), total, nout, nq, lambda t: None)
-    outs = [be.rescale(be.ct_like(like[i], total[i].data_ptr())) for i in range(nout)]
+    reduce_partials(be.device_context(), total, nout, nq, lambda t: None, len(p["special"]), world,
+                    p["chain"] + p["special"])
+    outs = finish(be, like, total)
     for i in range(nout):
         got = d2h(outs[i].device_ptr(), 2 * lvl * N)
         exp = d2h(ref[i].device_ptr(), 2 * lvl * N)

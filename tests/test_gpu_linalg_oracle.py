@@ -24,7 +24,7 @@ from oracle_pipeline import (OracleView, d2h, make_mask, pack_bsgs, pack_bsgs_st
 
 pytestmark = pytest.mark.gpu
 
-LAZY = False  # flipped when the product BSGS uses the lazy ModDown
+LAZY = True  # the product's BSGS giant steps: one (lazy) ModDown per output
 
 _cache = {}
 
@@ -189,7 +189,7 @@ def test_c2s_giant_step_shards_words_vs_oracle(world):
     import torch
 
     from paper_2512_11135_b200.helix import BSGS
-    from paper_2512_11135_b200.shard import gather_words, reduce_partials, shard_range
+    from paper_2512_11135_b200.shard import finish, gather_words, reduce_partials, shard_range
 
     ov = view("c2s")
     be, N = ov.be, ov.N
@@ -210,15 +210,16 @@ def test_c2s_giant_step_shards_words_vs_oracle(world):
         Ms = be.prepare_shard(A, lvl, r, world)
         parts, rep = be.matvec_shard(Ms, ct)
         gb, ge = shard_range(n2, r, world)
-        exp = ov.orc.matvec_bsgs(xw, nq, n1, n2, blocks, diags, keys, giant=(gb, ge), rescale=False, lazy=LAZY)
-        got = np.stack([d2h(p_.device_ptr(), 2 * nq * N).reshape(2, nq, N) for p_ in parts])
+        exp = ov.orc.matvec_bsgs(xw, nq, n1, n2, blocks, diags, keys, giant=(gb, ge), partial=True)
+        pw = be.shard_partial_words(parts[0])
+        got = np.stack([d2h(p_.device_ptr(), pw) for p_ in parts])
         assert np.array_equal(got, exp), f"rank {r} partials"
-        w = gather_words(parts, nq, N, torch)
+        w = gather_words(parts, pw, torch)
         total = w if total is None else total + w
         like = parts
     torch.cuda.synchronize()
-    reduce_partials(be.device_context(), total, blocks, nq, lambda t: None)
-    outs = [be.rescale(be.ct_like(like[i], total[i].data_ptr())) for i in range(blocks)]
+    reduce_partials(be.device_context(), total, blocks, nq, lambda t: None, ov.K, world, ov.chain + ov.special)
+    outs = finish(be, like, total)
     exp = ov.orc.matvec_bsgs(xw, nq, n1, n2, blocks, diags, keys, lazy=LAZY)
     assert np.array_equal(out_words(ov, outs, lvl), exp)
 
@@ -249,7 +250,7 @@ def test_n16_config5_slice_shards_words_vs_oracle():
     import torch
 
     from paper_2512_11135_b200.helix import BSGS
-    from paper_2512_11135_b200.shard import gather_words, reduce_partials, shard_range
+    from paper_2512_11135_b200.shard import finish, gather_words, reduce_partials, shard_range
 
     ov = view("c2q3")
     be, N = ov.be, ov.N
@@ -276,16 +277,17 @@ def test_n16_config5_slice_shards_words_vs_oracle():
         parts, rep = be.matvec_shard(Ms, ct)
         gb, ge = shard_range(n2, r, world)
         dl = [diags.get(i) for i in range(blocks * n1 * n2)]
-        exp = ov.orc.matvec_bsgs(xw, nq, n1, n2, blocks, dl, keys, giant=(gb, ge), rescale=False, lazy=LAZY)
-        got = np.stack([d2h(p_.device_ptr(), 2 * nq * N).reshape(2, nq, N) for p_ in parts])
+        exp = ov.orc.matvec_bsgs(xw, nq, n1, n2, blocks, dl, keys, giant=(gb, ge), partial=True)
+        pw = be.shard_partial_words(parts[0])
+        got = np.stack([d2h(p_.device_ptr(), pw) for p_ in parts])
         assert np.array_equal(got, exp), f"rank {r}"
-        w = gather_words(parts, nq, N, torch)
+        w = gather_words(parts, pw, torch)
         total = w if total is None else total + w
         like = parts
         del Ms
     torch.cuda.synchronize()
-    reduce_partials(be.device_context(), total, blocks, nq, lambda t: None)
-    outs = [be.rescale(be.ct_like(like[i], total[i].data_ptr())) for i in range(blocks)]
+    reduce_partials(be.device_context(), total, blocks, nq, lambda t: None, ov.K, world, ov.chain + ov.special)
+    outs = finish(be, like, total)
     dl = [diags.get(i) for i in range(blocks * n1 * n2)]
     exp = ov.orc.matvec_bsgs(xw, nq, n1, n2, blocks, dl, keys, lazy=LAZY)
     assert np.array_equal(out_words(ov, outs, lvl), exp)

@@ -1,12 +1,15 @@
 """CPU (gloo, world_size 2) test of the multi-GPU giant-step sharding math
 (paper_2512_11135_b200/shard.py).
 
-Each rank runs the oracle's BSGS pipeline restricted to its giant groups
-(shard_range), produces PRE-RESCALE partials, all-reduces their words as
-int64 (the same call bench/sharded_matvec makes over NCCL), reduces mod q and
-rescales once.  The result must equal the unsharded oracle pipeline word for
-word.  Keys/diagonals are uniform random words: bit-exactness of the
-combination does not depend on them being well formed.
+Each rank runs the oracle's BSGS driver (hxo_matvec_bsgs) restricted to its
+giant groups (shard_range) in PARTIAL mode: with double-hoisted giant steps a
+partial is T = [2][n_q][N] plus S = [2][n_q + K][N] (the key-switch products
+before their single ModDown).  The ranks all-reduce those words as int64
+(the same call shard.sharded_matvec makes over NCCL), reduce T and S mod q,
+finish with T + ModDown(S) and rescale once.  The result must equal the
+unsharded oracle pipeline word for word.  Keys / diagonals are uniform random
+words: bit-exactness of the combination does not depend on them being well
+formed.  (The product's own shard path over gloo is tests/test_gpu_shard_mp.py.)
 """
 import os
 import socket
@@ -14,66 +17,83 @@ import socket
 import numpy as np
 import pytest
 
-from configs import config1
-from oracle_bindings import Oracle, galois_elt, uniform_limbs
+from configs import config1, config2
+from oracle_bindings import Oracle, uniform_limbs
 
-from paper_2512_11135_b200.shard import shard_range
+from paper_2512_11135_b200.shard import check_exact_sum, shard_range
+
+CASES = {"c1": dict(logn=10, nq=3, n1=4, n2=4, blocks=2, seed=11),
+         "c2": dict(logn=10, nq=6, n1=4, n2=8, blocks=1, seed=12)}
 
 
-def _bsgs_partial(orc, p, nq, n1, n2, gb, ge, seed):
-    """oracle BSGS over giant groups [gb, ge) -> (2, nq, N) pre-rescale sum"""
+def _params(name):
+    c = CASES[name]
+    return config1(c["logn"]) if name == "c1" else config2(c["logn"], 8)
+
+
+def _inputs(orc, p, c):
     N = 1 << p["logn"]
+    nq = c["nq"]
     chain = p["chain"][:nq]
+    full = p["chain"] + p["special"]
     K = len(p["special"])
-    full = chain + p["special"]
-    rng = np.random.default_rng(seed)  # identical on every rank
+    rng = np.random.default_rng(c["seed"])  # identical on every rank
     xw = uniform_limbs(rng, chain, N, (2,))
-    dn = orc.dnum(nq)
-
-    def key():
-        return np.ascontiguousarray(uniform_limbs(rng, full, N, (dn, 2)).reshape(dn, 2, nq + K, N))
-
-    baby_keys = [key() for _ in range(1, n1)]
-    giant_keys = [key() for _ in range(1, n2)]
-    diags = uniform_limbs(rng, chain, N, (n1 * n2,))
-    baby = np.concatenate([xw[None], orc.rotate_hoisted(xw, baby_keys, [galois_elt(k, N) for k in range(1, n1)], nq)])
-    inner = orc.bsgs_mac(np.ascontiguousarray(baby), diags, n1, n2, nq)
-    acc = np.zeros((2, nq, N), dtype=np.uint64)
-    for j in range(gb, ge):
-        r = inner[j] if j == 0 else orc.rotate(np.ascontiguousarray(inner[j]), giant_keys[j - 1], nq,
-                                               galois_elt(n1 * j, N))
-        acc = np.stack([orc.binop("hxo_add", acc[c], r[c], nq) for c in range(2)])
-    return acc
+    dn = orc.dnum(len(p["chain"]))
+    keys = {}
+    for r in list(range(1, c["n1"])) + [c["n1"] * j for j in range(1, c["n2"])]:
+        keys[r] = np.ascontiguousarray(uniform_limbs(rng, full, N, (dn, 2)).reshape(dn, 2, len(full), N))
+    diags = [uniform_limbs(rng, chain, N) for _ in range(c["blocks"] * c["n1"] * c["n2"])]
+    diags[3] = None  # a zero diagonal
+    return xw, keys, diags, K
 
 
-def _rescale(orc, acc, nq):
-    return np.stack([orc.rescale_ntt(np.ascontiguousarray(acc[c]), nq) for c in range(2)])
+def _finish(orc, words, p, nq, K, blocks):
+    """T + ModDown(S) per block, then rescale (reduced words in)"""
+    N = 1 << p["logn"]
+    out = []
+    for b in range(blocks):
+        w = words[b]
+        T = w[: 2 * nq * N].reshape(2, nq, N)
+        S = np.ascontiguousarray(w[2 * nq * N:].reshape(2, nq + K, N))
+        md = orc.moddown_ntt(S, nq, 2)
+        y = np.stack([orc.binop("hxo_add", np.ascontiguousarray(T[i]), md[i], nq) for i in range(2)])
+        out.append(np.stack([orc.rescale_ntt(np.ascontiguousarray(y[i]), nq) for i in range(2)]))
+    return np.stack(out)
 
 
-def _mod_q(words, chain):
-    q = np.array(chain, dtype=np.uint64)[None, :, None]
-    return (words.view(np.uint64) % q).astype(np.uint64)
+def _reduce(words, p, nq, K):
+    N = 1 << p["logn"]
+    qT = np.array(p["chain"][:nq], dtype=np.uint64)
+    qS = np.array(p["chain"][:nq] + p["special"], dtype=np.uint64)
+    out = words.view(np.uint64).copy()
+    for b in range(out.shape[0]):
+        T = out[b, : 2 * nq * N].reshape(2, nq, N)
+        S = out[b, 2 * nq * N:].reshape(2, nq + K, N)
+        T %= qT[None, :, None]
+        S %= qS[None, :, None]
+    return out
 
 
-CASE = dict(logn=10, nq=3, n1=4, n2=4, seed=11)
-
-
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, name):
     import torch
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        p = config1(CASE["logn"])
+        c = CASES[name]
+        p = _params(name)
         orc = Oracle(p["logn"], p["chain"], p["special"], p["alpha"])
-        nq = CASE["nq"]
-        gb, ge = shard_range(CASE["n2"], rank, world)
-        part = _bsgs_partial(orc, p, nq, CASE["n1"], CASE["n2"], gb, ge, CASE["seed"])
+        nq = c["nq"]
+        xw, keys, diags, K = _inputs(orc, p, c)
+        gb, ge = shard_range(c["n2"], rank, world)
+        part = orc.matvec_bsgs(xw, nq, c["n1"], c["n2"], c["blocks"], diags, keys, giant=(gb, ge), partial=True)
+        check_exact_sum(world, p["chain"] + p["special"])
         t = torch.from_numpy(part.view(np.int64).copy())
         dist.all_reduce(t)  # int64 wrap sum == exact u64 sum (world * q < 2^64)
-        summed = _mod_q(t.numpy(), p["chain"][:nq])
-        out = _rescale(orc, summed, nq)
+        summed = _reduce(t.numpy(), p, nq, K)
+        out = _finish(orc, summed, p, nq, K, c["blocks"])
         np.save(os.path.join(out_dir, f"rank{rank}.npy"), out)
     finally:
         dist.destroy_process_group()
@@ -95,15 +115,23 @@ def test_shard_range_partitions():
         shard_range(4, 2, 2)
 
 
-def test_giant_step_shards_gloo_world2(tmp_path):
+def test_exact_sum_guard():
+    check_exact_sum(8, [(1 << 60) - 1])
+    with pytest.raises(ValueError):
+        check_exact_sum(8, [(1 << 62) - 57])  # 8 (q - 1) >= 2^64 would wrap silently
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_giant_step_shards_gloo_world2(tmp_path, name):
     import torch.multiprocessing as mp
 
     world = 2
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, start_method="spawn")
-    p = config1(CASE["logn"])
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), name), nprocs=world, start_method="spawn")
+    c = CASES[name]
+    p = _params(name)
     orc = Oracle(p["logn"], p["chain"], p["special"], p["alpha"])
-    nq = CASE["nq"]
-    ref = _rescale(orc, _bsgs_partial(orc, p, nq, CASE["n1"], CASE["n2"], 0, CASE["n2"], CASE["seed"]), nq)
+    xw, keys, diags, K = _inputs(orc, p, c)
+    ref = orc.matvec_bsgs(xw, c["nq"], c["n1"], c["n2"], c["blocks"], diags, keys, lazy=True)
     for r in range(world):
         got = np.load(tmp_path / f"rank{r}.npy")
         assert np.array_equal(got, ref), f"rank {r} differs from the unsharded pipeline"
