@@ -129,6 +129,10 @@ class GpuLatticeBackend final : public SlotBackend {
   // operand, d ct-ct products + relinearisation in one launch, one strided sum
   // and the final rescale.  Same trace records as the SlotOps form.
   Ciphertext matmul(const Ciphertext& A, const Ciphertext& B, int d);
+  // H independent products (config 4's attention heads) in one schedule:
+  // each rotation / relinearisation launch covers every head, so a key is
+  // read once per H heads.  outs[h] = matmul(As[h], Bs[h], d) word for word.
+  std::vector<Ciphertext> matmul_heads(const std::vector<Ciphertext>& As, const std::vector<Ciphertext>& Bs, int d);
 
   // y = T + (ModDown(S_0), ModDown(S_1)) of a summed PQ partial (words =
   // [T][S] as bsgs_blocks(allow_empty) lays them out), at like's level / scale

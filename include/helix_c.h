@@ -113,6 +113,10 @@ hxc_ct* hxc_shard_finish(hxc_backend* b, const hxc_ct* like, const uint64_t* wor
 
 /* ct-ct matmul of row-major d x d operands */
 hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_report* rep);
+/* H heads in one batched schedule (keys read once per H heads); out[h] gets
+ * matmul(As[h], Bs[h]); rep = per-head counters; returns H or -1 */
+int hxc_matmul_heads(hxc_backend* b, const hxc_ct* const* As, const hxc_ct* const* Bs, int H, int d, hxc_ct** out,
+                     hxc_report* rep);
 /* rotation count a dense rows x cols matvec records at `slots` slots (counters
  * only, no device work; helix::predicted_rotations; SPEC criterion 4) */
 long long hxc_predicted_rotations(int method, int rows, int cols, int64_t slots);

@@ -65,6 +65,15 @@ int hx_ctx_trim(hx_ctx* ctx);
 /* number of kernels this context has launched so far (bench evidence) */
 unsigned long long hx_ctx_launches(const hx_ctx* ctx);
 
+/* live per-kernel timing for the roofline of a timed step: while `name` is
+ * set ("modup_col_kernel", "moddown_col_kernel", "ks_row_inner_f64_kernel",
+ * "ntt_pass_kernel", "ntt_row_combine_kernel"; NULL or "" = off) every launch
+ * of that kernel family records a CUDA event pair on its launching stream;
+ * hx_ctx_kernel_time synchronises them and returns the summed device time
+ * and the launch count since the last call (and clears them). */
+int hx_ctx_time_kernel(hx_ctx* ctx, const char* name);
+int hx_ctx_kernel_time(hx_ctx* ctx, double* total_ms, long long* launches);
+
 /* ---- memory / streams ---- */
 int hx_malloc(void** ptr, size_t bytes);
 int hx_free(void* ptr);
@@ -90,6 +99,11 @@ int hx_mul(hx_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int
            int n_p, void* stream);
 int hx_mul_acc(hx_ctx* ctx, uint64_t* acc, const uint64_t* a, const uint64_t* b, int batch,
                int n_q, int n_p, void* stream);
+/* broadcast product over [batch][n_q][N] polys: out[i] = a[a_mod ? i % a_mod : i]
+ * (.) b[i / b_div] -- e.g. d masks applied to every poly of H ciphertexts
+ * (a_mod = 2H, b_div = 2H) without replicating either operand */
+int hx_mul_bcast(hx_ctx* ctx, uint64_t* out, const uint64_t* a, const uint64_t* b, int batch, int a_mod,
+                 int b_div, int n_q, void* stream);
 /* LatticeContext::automorphism (rns_poly.cpp:124-142), X -> X^g, applied in
  * the NTT domain as a permutation. */
 int hx_automorphism(hx_ctx* ctx, uint64_t* out, const uint64_t* in, int batch, int n_q, int n_p,
@@ -188,6 +202,15 @@ int hx_bsgs_mac_tokens(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, lo
  * chunk a launch with n1 = chunk and diag_jstride = the block's n1.) */
 int hx_bsgs_mac(hx_ctx* ctx, uint64_t* inner, const uint64_t* baby, const uint64_t* diags,
                 int diag_limbs, int n1, int n2, int n_q, void* stream);
+/* pruned matrices: the live diagonals of one row block as an index list --
+ * group j owns entries [group_ptr[j], group_ptr[j+1]) (host ints, n2 + 1),
+ * entry e multiplies baby step ks[e] (host ints) by the [n_q][N] words at
+ * the DEVICE address diags[e] (a host array of device pointers); inner_j is
+ * written only for groups with entries.  n1 <= 128; T tokens as
+ * hx_bsgs_mac_tokens.  No gathers: diagonals and baby steps are read in place. */
+int hx_bsgs_mac_sparse(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, long long inner_tstride,
+                       const uint64_t* baby, long long baby_tstride, const int* group_ptr, const int* ks,
+                       const uint64_t* const* diags, int n1, int n2, int n_q, int tokens, void* stream);
 
 /* ---- keys / encryption ------------------------ */
 /* Device samplers (counter-based: splitmix64 of (seed, index)), used for key

@@ -213,7 +213,7 @@ std::vector<u64> perm_table(const RefCtx* c, u64 g) {
   return perm;
 }
 
-void inner(const RefCtx* c, u64* U, const u64* D, const u64* key, int n_q, u64 g) {
+void inner_(const RefCtx* c, u64* U, const u64* D, const u64* key, int n_q, u64 g) {
   const std::size_t n = c->n;
   const int K = c->n_special, ext = n_q + K, full = c->n_chain + K;
   const int dnum = (n_q + c->alpha - 1) / c->alpha;
@@ -413,7 +413,7 @@ int ref_keyswitch(void* h, const u64* in_ntt, const u64* key, u64* out, int n_q)
   const int ext = n_q + c->n_special, dnum = (n_q + c->alpha - 1) / c->alpha;
   std::vector<u64> D((std::size_t)dnum * ext * n), U((std::size_t)2 * ext * n);
   modup(c, D.data(), in_ntt, n_q);
-  inner(c, U.data(), D.data(), key, n_q, 1);
+  inner_(c, U.data(), D.data(), key, n_q, 1);
   moddown(c, out, U.data(), n_q);
   moddown(c, out + (std::size_t)n_q * n, U.data() + (std::size_t)ext * n, n_q);
   return 0;
@@ -425,7 +425,7 @@ int ref_rotate(void* h, const u64* in_ct, const u64* key, u64* out_ct, int n_q, 
   const int ext = n_q + c->n_special, dnum = (n_q + c->alpha - 1) / c->alpha;
   std::vector<u64> D((std::size_t)dnum * ext * n), U((std::size_t)2 * ext * n), V(2 * L);
   modup(c, D.data(), in_ct + L, n_q);
-  inner(c, U.data(), D.data(), key, n_q, g);
+  inner_(c, U.data(), D.data(), key, n_q, g);
   moddown(c, V.data(), U.data(), n_q);
   moddown(c, V.data() + L, U.data() + (std::size_t)ext * n, n_q);
   const auto perm = perm_table(c, g);
@@ -435,6 +435,122 @@ int ref_rotate(void* h, const u64* in_ct, const u64* key, u64* out_ct, int n_q, 
       out_ct[i * n + t] = m.add(in_ct[i * n + perm[t]], V[i * n + t]);
   });
   std::memcpy(out_ct + L, V.data() + L, L * 8);
+  return 0;
+}
+
+// ---- BSGS matvec over the reference primitives (the matvec CPU arm) --------
+// The same schedule as hxo_matvec_bsgs (lazy = 1, the product's double-hoisted
+// giant steps): hoisted baby steps, the diagonal MAC with Modulus::mul/add
+// (LatticeContext::mul_acc, rns_poly.cpp:102-110), giant key-switch products
+// summed in the PQ basis with one ModDown per output, then the rescale of
+// rns_poly.cpp:144-162 in the NTT domain (NttTables::inverse/forward).
+// Limb loops run on the context's pool.
+static u64 galois_of(const RefCtx* c, u64 r) {
+  u64 g = 1;
+  for (u64 i = 0; i < r; ++i) g = (g * 5) % (2 * c->n);
+  return g;
+}
+
+static void ref_rescale_ntt(RefCtx* c, u64* out, const u64* in, int n_q) {
+  const std::size_t n = c->n;
+  std::vector<u64> last(in + (std::size_t)(n_q - 1) * n, in + (std::size_t)n_q * n);
+  c->ntt[n_q - 1].inverse(std::span<u64>(last.data(), n));
+  const auto& ql = c->mods[n_q - 1];
+  parallel_for(c->pool.get(), n_q - 1, [&](int i) {
+    const auto& m = c->mods[i];
+    const u64 qinv = m.inv(ql.q % m.q);
+    std::vector<u64> v(in + (std::size_t)i * n, in + (std::size_t)(i + 1) * n);
+    c->ntt[i].inverse(std::span<u64>(v.data(), n));
+    for (std::size_t t = 0; t < n; ++t) v[t] = m.mul(m.sub(v[t], m.reduce_i64(ql.centered(last[t]))), qinv);
+    c->ntt[i].forward(std::span<u64>(v.data(), n));
+    std::memcpy(out + (std::size_t)i * n, v.data(), n * 8);
+  });
+}
+
+extern "C" int ref_matvec_bsgs(void* h, u64* out, const u64* x, int n_q, int n1, int n2, int blocks,
+                               const u64* const* diags, const u64* const* keys, int gb, int ge, int rescale) {
+  auto* c = static_cast<RefCtx*>(h);
+  const std::size_t n = c->n, L = (std::size_t)n_q * n, ct = 2 * L;
+  const int K = c->n_special, ext = n_q + K, dnum = (n_q + c->alpha - 1) / c->alpha;
+  const u64 slots = n / 2;
+  if (ge < 0) ge = n2;
+  std::vector<u64> baby((std::size_t)n1 * ct), D((std::size_t)dnum * ext * n), U((std::size_t)2 * ext * n),
+      S((std::size_t)2 * ext * n), V(ct), inner(ct), acc(ct);
+  std::memcpy(baby.data(), x, ct * 8);
+  if (n1 > 1) modup(c, D.data(), x + L, n_q);  // hoisted: one ModUp for every baby step
+  for (int k = 1; k < n1; ++k) {
+    const u64 g = galois_of(c, (u64)k);
+    inner_(c, U.data(), D.data(), keys[k], n_q, g);
+    moddown(c, V.data(), U.data(), n_q);
+    moddown(c, V.data() + L, U.data() + (std::size_t)ext * n, n_q);
+    const auto perm = perm_table(c, g);
+    u64* bk = baby.data() + (std::size_t)k * ct;
+    parallel_for(c->pool.get(), n_q, [&](int i) {
+      const auto& m = c->mods[i];
+      for (std::size_t t = 0; t < n; ++t) bk[i * n + t] = m.add(x[i * n + perm[t]], V[i * n + t]);
+    });
+    std::memcpy(bk + L, V.data() + L, L * 8);
+  }
+  for (int b = 0; b < blocks; ++b) {
+    std::fill(acc.begin(), acc.end(), 0);
+    std::fill(S.begin(), S.end(), 0);
+    bool any_giant = false;
+    for (int j = gb; j < ge; ++j) {
+      bool live = false;
+      std::fill(inner.begin(), inner.end(), 0);
+      for (int k = 0; k < n1; ++k) {
+        const u64* dg = diags[(std::size_t)b * n1 * n2 + (std::size_t)j * n1 + k];
+        if (!dg) continue;
+        live = true;
+        const u64* bk = baby.data() + (std::size_t)k * ct;
+        parallel_for(c->pool.get(), 2 * n_q, [&](int ci) {
+          const int cc = ci / n_q, i = ci % n_q;
+          const auto& m = c->mods[i];
+          u64* o = inner.data() + cc * L + (std::size_t)i * n;
+          const u64* a = bk + cc * L + (std::size_t)i * n;
+          const u64* d = dg + (std::size_t)i * n;
+          for (std::size_t t = 0; t < n; ++t) o[t] = m.add(o[t], m.mul(a[t], d[t]));
+        });
+      }
+      if (!live) continue;
+      if (j == 0) {
+        parallel_for(c->pool.get(), 2 * n_q, [&](int ci) {
+          const auto& m = c->mods[ci % n_q];
+          for (std::size_t t = 0; t < n; ++t) acc[ci * n + t] = m.add(acc[ci * n + t], inner[ci * n + t]);
+        });
+        continue;
+      }
+      const u64 r = (u64)(((long long)n1 * j) % (long long)slots), g = galois_of(c, r);
+      modup(c, D.data(), inner.data() + L, n_q);
+      inner_(c, U.data(), D.data(), keys[r], n_q, g);
+      const auto perm = perm_table(c, g);
+      parallel_for(c->pool.get(), 2 * ext, [&](int cj) {
+        const int j2 = cj % ext;
+        const auto& m = c->mods[pidx(c, j2, n_q)];
+        for (std::size_t t = 0; t < n; ++t) S[cj * n + t] = m.add(S[cj * n + t], U[cj * n + t]);
+      });
+      parallel_for(c->pool.get(), n_q, [&](int i) {
+        const auto& m = c->mods[i];
+        for (std::size_t t = 0; t < n; ++t) acc[i * n + t] = m.add(acc[i * n + t], inner[i * n + perm[t]]);
+      });
+      any_giant = true;
+    }
+    if (any_giant) {
+      moddown(c, V.data(), S.data(), n_q);
+      moddown(c, V.data() + L, S.data() + (std::size_t)ext * n, n_q);
+      parallel_for(c->pool.get(), 2 * n_q, [&](int ci) {
+        const auto& m = c->mods[ci % n_q];
+        for (std::size_t t = 0; t < n; ++t) acc[ci * n + t] = m.add(acc[ci * n + t], V[ci * n + t]);
+      });
+    }
+    if (rescale) {
+      u64* o = out + (std::size_t)b * 2 * (n_q - 1) * n;
+      ref_rescale_ntt(c, o, acc.data(), n_q);
+      ref_rescale_ntt(c, o + (std::size_t)(n_q - 1) * n, acc.data() + L, n_q);
+    } else {
+      std::memcpy(out + (std::size_t)b * ct, acc.data(), ct * 8);
+    }
+  }
   return 0;
 }
 

@@ -228,6 +228,74 @@ __global__ void __launch_bounds__(32 * kMacWarps) bsgs_mac_int_kernel(MacArgs A,
   }
 }
 
+// Sparse index-list MAC (pruned matrices): a CTA owns TT coefficients of one
+// limb for one token; the baby tile [n1][2][TT] is staged in shared memory
+// once, then the live (j, k) entries of the block are streamed group by
+// group straight from their plaintexts (no gather copies of diagonals or
+// baby steps), each diagonal word read once per token tile, 128-bit lazy
+// accumulation, one reduction per live output word.
+template <int TT>
+__global__ void __launch_bounds__(TT) bsgs_mac_sparse_kernel(SparseMacArgs A) {
+  extern __shared__ u64 smb[];  // [n1][2][TT]
+  const long long N = 1ll << A.logn;
+  const int i = blockIdx.y;
+  const int tid = threadIdx.x;
+  const int tok = blockIdx.x % A.tokens;
+  const long long t = (long long)(blockIdx.x / A.tokens) * TT + tid;
+  const u64* baby = A.baby + tok * A.baby_tstride;
+  u64* inner = A.inner + tok * A.inner_tstride;
+  const PrimeConst& P = A.pc[i];
+  const long long L = (long long)A.n_q * N;
+  for (int k = 0; k < A.n1; ++k) {
+    smb[(2 * k) * TT + tid] = __ldg(baby + (2ll * k) * L + i * N + t);
+    smb[(2 * k + 1) * TT + tid] = __ldg(baby + (2ll * k + 1) * L + i * N + t);
+  }
+  __syncthreads();
+  const long long off = i * N + t;
+  for (int j = 0; j < A.n2; ++j) {
+    const int e0 = A.gptr[j], e1 = A.gptr[j + 1];
+    if (e0 == e1) continue;
+    U128 z0{0, 0}, z1{0, 0};
+    int e = e0;
+    for (; e + 4 <= e1; e += 4) {
+      u64 d[4];
+      int k[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        d[u] = __ldcs(A.dptr[e + u] + off);
+        k[u] = A.ks[e + u];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        mac128(z0, d[u], smb[(2 * k[u]) * TT + tid]);
+        mac128(z1, d[u], smb[(2 * k[u] + 1) * TT + tid]);
+      }
+    }
+    for (; e < e1; ++e) {
+      const u64 d = __ldcs(A.dptr[e] + off);
+      const int k = A.ks[e];
+      mac128(z0, d, smb[(2 * k) * TT + tid]);
+      mac128(z1, d, smb[(2 * k + 1) * TT + tid]);
+    }
+    u64* o = inner + (long long)j * A.out_jstride + off;
+    o[0] = reduce128(z0, P);
+    o[L] = reduce128(z1, P);
+  }
+}
+
+void launch_bsgs_mac_sparse(const SparseMacArgs& A, long long N, cudaStream_t s) {
+  constexpr int TT = 64;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(bsgs_mac_sparse_kernel<TT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         128 * 2 * TT * (int)sizeof(u64));
+    configured = true;
+  }
+  const size_t smem = (size_t)A.n1 * 2 * TT * sizeof(u64);
+  dim3 grid((unsigned)(N / TT * A.tokens), (unsigned)A.n_q);
+  bsgs_mac_sparse_kernel<TT><<<grid, TT, smem, s>>>(A);
+}
+
 namespace {
 template <class K>
 void set_max_smem(K kernel, int bytes) {

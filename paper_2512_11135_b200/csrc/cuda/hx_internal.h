@@ -84,6 +84,11 @@ struct hx_ctx {
   hx::u64* d_qlmod = nullptr;  // [n_chain][n_chain]
   // launch counter (kernels issued through this context)
   unsigned long long launches = 0;
+  // live per-kernel timing (hx_ctx_time_kernel): CUDA events recorded on the
+  // launching stream around every launch of the kernel family `ktime_name`
+  bool ktime_on = false;
+  std::string ktime_name;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ktime_ev;
 
   int n_total() const { return n_chain + n_special; }
   long long N() const { return 1ll << logn; }
@@ -92,6 +97,25 @@ struct hx_ctx {
 };
 
 namespace hx {
+
+// RAII: events around one launch when its kernel family is being timed
+struct KTimer {
+  hx_ctx* c;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  KTimer(hx_ctx* c_, const char* name, cudaStream_t s_) : c(c_), s(s_) {
+    if (c->ktime_on && c->ktime_name == name && cudaEventCreate(&a) == cudaSuccess) cudaEventRecord(a, s);
+  }
+  ~KTimer() {
+    cudaEvent_t b = nullptr;
+    if (a && cudaEventCreate(&b) == cudaSuccess) {
+      cudaEventRecord(b, s);
+      c->ktime_ev.emplace_back(a, b);
+    }
+  }
+  KTimer(const KTimer&) = delete;
+  KTimer& operator=(const KTimer&) = delete;
+};
 
 // limb table for an (n_q chain, n_p special) poly batch element with `stride`
 // limbs per element starting at limb offset `first`
@@ -110,6 +134,8 @@ void ntt_forward_combine(hx_ctx* c, u64* data, long long batch, const LimbTable&
                          cudaStream_t s, bool f64_col_done = false);
 void ntt_forward_rows(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cudaStream_t s);
 int ntt_split_a(int logn);
+
+void launch_bsgs_mac_sparse(const SparseMacArgs& A, long long N, cudaStream_t s);
 
 void set_error(const std::string& msg);
 // record `msg` as hx_last_error() and return `code` (C-ABI entry points outside hx_ops.cu)

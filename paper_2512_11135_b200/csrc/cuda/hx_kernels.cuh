@@ -38,6 +38,9 @@ struct EwArgs {
   LimbTable lt;   // limbs of one batch element
   int logn;
   long long instances;
+  // broadcast operands: element b reads a element (a_mod ? b % a_mod : b) and
+  // b element b / b_div (a mask applied to every ciphertext poly of a batch)
+  long long a_mod = 0, b_div = 1;
 };
 
 // add / sub / negate / mul / mul_acc (rns_poly.cpp:62-110), 2 words per thread
@@ -50,11 +53,13 @@ __global__ void ew_kernel(EwArgs A) {
   const int e = (int)(inst % A.lt.count);
   const PrimeConst& P = A.pc[A.lt.prime[e]];
   const u64 q = P.q;
-  const long long ofs = (b * A.lt.stride + A.lt.off[e]) * (1ll << A.logn) +
-                        2ll * (chunk * blockDim.x + threadIdx.x);
-  const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(A.a + ofs);
+  const long long in_limb = (long long)A.lt.off[e] * (1ll << A.logn) + 2ll * (chunk * blockDim.x + threadIdx.x);
+  const long long ofs = b * A.lt.stride * (1ll << A.logn) + in_limb;
+  const long long ba = A.a_mod ? b % A.a_mod : b, bb = b / A.b_div;
+  const ulonglong2 x = *reinterpret_cast<const ulonglong2*>(A.a + ba * A.lt.stride * (1ll << A.logn) + in_limb);
   ulonglong2 y = make_ulonglong2(0, 0), r;
-  if (OP != EwOp::Neg && OP != EwOp::Copy) y = *reinterpret_cast<const ulonglong2*>(A.b + ofs);
+  if (OP != EwOp::Neg && OP != EwOp::Copy)
+    y = *reinterpret_cast<const ulonglong2*>(A.b + bb * A.lt.stride * (1ll << A.logn) + in_limb);
   if (OP == EwOp::Add) {
     r.x = addmod(x.x, y.x, q);
     r.y = addmod(x.y, y.y, q);

@@ -44,6 +44,7 @@ void launch_pass(hx_ctx* c, u64* data, long long batch, const LimbTable& lt, cud
                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
+  KTimer kt(c, "ntt_pass_kernel", s);
   ntt_pass_kernel<FWD, ROW, S, OB, F64><<<(unsigned)blocks, TILE / 16, smem, s>>>(a);
   ++c->launches;
 }
@@ -69,6 +70,7 @@ void launch_row_combine(hx_ctx* c, u64* data, long long batch, const LimbTable& 
     cudaFuncSetAttribute(ntt_row_combine_kernel<S, OB, F64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
+  KTimer kt(c, "ntt_row_combine_kernel", s);
   ntt_row_combine_kernel<S, OB, F64><<<(unsigned)blocks, TILE / 16, smem, s>>>(a, ep);
   ++c->launches;
 }

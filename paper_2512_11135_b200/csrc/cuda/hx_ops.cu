@@ -225,8 +225,10 @@ int combine_threads(const hx_ctx* c) { return (int)std::min<long long>(256, c->N
 
 template <hx::EwOp OP>
 void ew(hx_ctx* c, u64* out, const u64* a, const u64* b, long long batch, const LimbTable& lt,
-        cudaStream_t s) {
+        cudaStream_t s, long long a_mod = 0, long long b_div = 1) {
   hx::EwArgs A{out, a, b, c->d_pc, lt, c->logn, batch * lt.count};
+  A.a_mod = a_mod;
+  A.b_div = b_div;
   const int th = ew_threads(c);
   const long long blocks = A.instances * (c->N() / (2 * th));
   if (blocks <= 0) return;
@@ -265,7 +267,10 @@ void launch_modup_col_t(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, c
   B.tsplit = (int)std::max(1ll, std::min<long long>(maxt, (148ll * 3 * 3 + base - 1) / base));
   HX_REQUIRE(batch * B.tsplit <= 65535, "modup_col: batch too large for one launch");
   dim3 grid((unsigned)(c->N() / TILE), (unsigned)(batch * B.tsplit), (unsigned)A.dnum);
-  kern<<<grid, TILE / 16, smem, s>>>(B);
+  {
+    hx::KTimer kt(c, A.centred ? "moddown_col_kernel" : "modup_col_kernel", s);
+    kern<<<grid, TILE / 16, smem, s>>>(B);
+  }
   launched(c, "modup_col_kernel");
 }
 
@@ -434,7 +439,10 @@ void launch_row_inner_t(hx_ctx* c, const hx::RowInnerArgs& A, cudaStream_t s) {
   }
   const long long blocks = (long long)A.batch * (c->N() / TILE) * A.n_limbs;
   if (blocks <= 0) return;
-  kern<<<(unsigned)blocks, TILE / 16, smem, s>>>(A);
+  {
+    hx::KTimer kt(c, "ks_row_inner_f64_kernel", s);
+    kern<<<(unsigned)blocks, TILE / 16, smem, s>>>(A);
+  }
   launched(c, "ks_row_inner_f64_kernel");
 }
 
@@ -1352,6 +1360,17 @@ HX_EW_ENTRY(hx_sub, hx::EwOp::Sub)
 HX_EW_ENTRY(hx_mul, hx::EwOp::Mul)
 #undef HX_EW_ENTRY
 
+int hx_mul_bcast(hx_ctx* c, uint64_t* out, const uint64_t* a, const uint64_t* b, int batch, int a_mod,
+                 int b_div, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_COUNT(batch);
+    HX_REQUIRE(a_mod >= 0 && b_div >= 1, "mul_bcast: a_mod >= 0, b_div >= 1");
+    ew<hx::EwOp::Mul>(c, (u64*)out, (const u64*)a, (const u64*)b, batch, hx::make_table(c, n_q, 0), S(s), a_mod,
+                      b_div);
+  });
+}
+
 int hx_mul_acc(hx_ctx* c, uint64_t* acc, const uint64_t* a, const uint64_t* b, int batch, int n_q,
                int n_p, void* s) {
   return guarded([&] {
@@ -1705,6 +1724,47 @@ int hx_bsgs_mac_tokens(hx_ctx* c, uint64_t* inner, long long inner_jstride, long
   });
 }
 
+int hx_bsgs_mac_sparse(hx_ctx* c, uint64_t* inner, long long inner_jstride, long long inner_tstride,
+                       const uint64_t* baby, long long baby_tstride, const int* group_ptr, const int* ks,
+                       const uint64_t* const* diags, int n1, int n2, int n_q, int tokens, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    HX_REQUIRE(n1 >= 1 && n1 <= 128 && n2 >= 1 && tokens >= 1, "bsgs_mac_sparse: bad shape");
+    HX_REQUIRE(c->N() >= 64 && (long long)tokens * (c->N() / 64) < (1ll << 31), "bsgs_mac_sparse: shape");
+    HX_REQUIRE(group_ptr[0] == 0, "bsgs_mac_sparse: group_ptr[0] != 0");
+    for (int j = 0; j < n2; ++j) HX_REQUIRE(group_ptr[j + 1] >= group_ptr[j], "bsgs_mac_sparse: group_ptr not monotone");
+    const int nnz = group_ptr[n2];
+    if (nnz <= 0) return;
+    for (int e = 0; e < nnz; ++e) HX_REQUIRE(ks[e] >= 0 && ks[e] < n1 && diags[e], "bsgs_mac_sparse: bad entry");
+    // one device table: gptr [n2 + 1] | ks [nnz] (ints) | dptr [nnz] (pointers)
+    const size_t ib = ((size_t)(n2 + 1 + nnz) * sizeof(int) + 15) & ~(size_t)15;
+    std::vector<char> host(ib + (size_t)nnz * sizeof(void*));
+    std::memcpy(host.data(), group_ptr, (size_t)(n2 + 1) * sizeof(int));
+    std::memcpy(host.data() + (size_t)(n2 + 1) * sizeof(int), ks, (size_t)nnz * sizeof(int));
+    std::memcpy(host.data() + ib, diags, (size_t)nnz * sizeof(void*));
+    DBuf tab((host.size() + 7) / 8, S(s), c);
+    cuda_ok(cudaMemcpyAsync(tab.p, host.data(), host.size(), cudaMemcpyHostToDevice, S(s)), "h2d");
+    hx::SparseMacArgs A;
+    A.inner = (u64*)inner;
+    A.baby = (const u64*)baby;
+    A.gptr = (const int*)tab.p;
+    A.ks = A.gptr + (n2 + 1);
+    A.dptr = (const u64* const*)((const char*)tab.p + ib);
+    A.pc = c->d_pc;
+    A.n1 = n1;
+    A.n2 = n2;
+    A.n_q = n_q;
+    A.logn = c->logn;
+    A.tokens = tokens;
+    A.out_jstride = inner_jstride;
+    A.baby_tstride = baby_tstride;
+    A.inner_tstride = inner_tstride;
+    hx::launch_bsgs_mac_sparse(A, c->N(), S(s));
+    launched(c, "bsgs_mac_sparse_kernel");  // (pageable H2D: `host` may go once the call returns)
+  });
+}
+
 int hx_bsgs_mac_ex(hx_ctx* c, uint64_t* inner, long long inner_jstride, const uint64_t* baby,
                    const uint64_t* diags, int diag_limbs, int n1, int n2, int n_q, void* s) {
   return hx_bsgs_mac_tokens(c, inner, inner_jstride, 0, baby, 0, diags, diag_limbs, n1, n2, n_q, 1, 0, s);
@@ -1734,6 +1794,37 @@ int hx_sum_strided(hx_ctx* c, uint64_t* out, const uint64_t* in, int terms, long
     A.out_poly_stride = out_poly_stride;
     hx::launch_sum(A, polys, c->N(), S(s));
     launched(c, "sum_kernel");
+  });
+}
+
+int hx_ctx_time_kernel(hx_ctx* c, const char* name) {
+  return guarded([&] {
+    check_ctx(c);
+    for (auto& e : c->ktime_ev) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    c->ktime_ev.clear();
+    c->ktime_on = name && *name;
+    c->ktime_name = name ? name : "";
+  });
+}
+
+int hx_ctx_kernel_time(hx_ctx* c, double* total_ms, long long* launches) {
+  return guarded([&] {
+    check_ctx(c);
+    double tot = 0.0;
+    for (auto& e : c->ktime_ev) {
+      cuda_ok(cudaEventSynchronize(e.second), "event sync");
+      float ms = 0.f;
+      cuda_ok(cudaEventElapsedTime(&ms, e.first, e.second), "event elapsed");
+      tot += ms;
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    if (launches) *launches = (long long)c->ktime_ev.size();
+    if (total_ms) *total_ms = tot;
+    c->ktime_ev.clear();
   });
 }
 

@@ -36,6 +36,22 @@ struct MacArgs {
   int diag_jstride;
 };
 
+// Sparse (pruned) BSGS MAC: the live diagonals of one row block as an index
+// list grouped by giant step (CSR: group j owns entries [gptr[j], gptr[j+1])),
+// entry e = baby index ks[e] and the device address dptr[e] of its [n_q][N]
+// words.  inner_j is written for live groups only (dead ones keep the
+// caller's zeros).
+struct SparseMacArgs {
+  u64* inner;
+  const u64* baby;
+  const int* gptr;
+  const int* ks;
+  const u64* const* dptr;
+  const PrimeConst* pc;
+  int n1, n2, n_q, logn, tokens;
+  long long out_jstride, baby_tstride, inner_tstride;
+};
+
 // out = sum_{r < terms} in + r * term_stride, per (poly, limb) of `polys`
 // polys of n_q limbs (ciphertext sums of the BSGS giant steps)
 struct SumArgs {

@@ -531,10 +531,27 @@ std::vector<Ciphertext> GpuLatticeBackend::rotate_many(const Ciphertext& a,
 }
 
 Ciphertext GpuLatticeBackend::matmul(const Ciphertext& A, const Ciphertext& B, int d) {
+  return matmul_heads({A}, {B}, d).front();
+}
+
+// H independent products (attention heads) through one schedule: every
+// buffer is laid out [j][h][ct], so each rotation launch covers all heads and
+// reads its key once (the multi-key rotation groups the H heads of column j
+// under key j), the d x H ct-ct products share one relinearisation-key read,
+// and the d masks are applied by broadcast (hx_mul_bcast) without replicas.
+// Heads are processed in chunks bounded by device memory.
+std::vector<Ciphertext> GpuLatticeBackend::matmul_heads(const std::vector<Ciphertext>& As,
+                                                        const std::vector<Ciphertext>& Bs, int d) {
   const std::size_t N = params_.ring_degree, n = slots();
-  detail::require_same_level(A.level, B.level, "matmul_ctct");
-  if (A.level < 2) throw LevelUnderflowError("matmul_ctct: requires a multiplicative level of 2");
-  const int lv = A.level, nqa = nq(lv), nqb = nqa - 1, lg = __builtin_ctz((unsigned)d);
+  if (As.empty() || As.size() != Bs.size()) throw std::invalid_argument("matmul_heads: operand count");
+  const Ciphertext& A0 = As[0];
+  for (std::size_t h = 0; h < As.size(); ++h) {
+    detail::require_same_level(As[h].level, Bs[h].level, "matmul_ctct");
+    detail::require_same_level(As[h].level, A0.level, "matmul_heads");
+    if (As[h].scale != A0.scale || Bs[h].scale != Bs[0].scale) throw ScaleMismatchError("matmul_heads: scales differ");
+  }
+  if (A0.level < 2) throw LevelUnderflowError("matmul_ctct: requires a multiplicative level of 2");
+  const int lv = A0.level, nqa = nq(lv), nqb = nqa - 1, lg = __builtin_ctz((unsigned)d);
   const std::size_t cw = (std::size_t)2 * nqa * N, cwb = (std::size_t)2 * nqb * N;
   const Scale ms = Scale::prime(modulus_at(lv));
   const Scale ms_b = ms * Scale::prime(modulus_at(lv - 1)) / params_.delta();
@@ -544,74 +561,89 @@ Ciphertext GpuLatticeBackend::matmul(const Ciphertext& A, const Ciphertext& B, i
     if (!rot_set_.contains(r) || !key) throw MissingRotationKeyError("rotate: no key for amount " + std::to_string(r));
     return std::pair<const u64*, u64>{key, galois(r)};
   };
-  // masks, each twice ([j][poly]) so one elementwise launch covers both polys;
-  // encoded once per (d, level) and cached (plaintexts are immutable)
+  // the d column / row extraction masks, encoded once per (d, level) and cached
   auto it = matmul_masks_.find({d, lv});
   if (it == matmul_masks_.end()) {
     std::vector<std::vector<double>> cmv, rmv;
     for (int j = 0; j < d; ++j) {
-      auto c = make_mask(MaskKind::ColumnExtractor, j, d, n);
-      auto r = make_mask(MaskKind::RowExtractor, j, d, n);
-      cmv.push_back(c);
-      cmv.push_back(std::move(c));
-      rmv.push_back(r);
-      rmv.push_back(std::move(r));
+      cmv.push_back(make_mask(MaskKind::ColumnExtractor, j, d, n));
+      rmv.push_back(make_mask(MaskKind::RowExtractor, j, d, n));
     }
     it = matmul_masks_.emplace(std::make_pair(d, lv), std::make_pair(encode_many(cmv, lv, ms), encode_many(rmv, lv, ms_b)))
              .first;
   }
   const auto& cm = it->second.first;
   const auto& rm = it->second.second;
-  // operand replicas [j][2][nqa][N] and the masked / rescaled / rotated sets
-  auto rep = dev((std::size_t)d * cw), prod = dev((std::size_t)d * cw);
-  auto sa = dev((std::size_t)d * cwb), sb = dev((std::size_t)d * cwb), tmp = dev((std::size_t)d * cwb);
-  const auto side = [&](const Ciphertext& X, const std::vector<Plaintext>& masks, const std::shared_ptr<DeviceBuffer>& out,
-                        std::int64_t unit) {
-    for (int j = 0; j < d; ++j)
-      cuda_ck(cudaMemcpyAsync(rep->ptr + j * cw, payload(X).data(), cw * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
-    const u64* mk = payload(masks[0]).data();  // encode_many: contiguous [2d][nqa][N]
-    ck(hx_mul(ctx_, prod->ptr, rep->ptr, mk, 2 * d, nqa, 0, nullptr), "mul");
-    ck(hx_rescale(ctx_, out->ptr, prod->ptr, 2 * d, nqa, nullptr), "rescale");
-    // element j -> Rot_{unit j}, j >= 1 (element 0 stays)
-    std::vector<const u64*> keys;
-    std::vector<u64> gal;
-    for (int j = 1; j < d; ++j) {
-      const auto kg = need(unit * j);
-      keys.push_back(kg.first);
-      gal.push_back(kg.second);
+  // heads per chunk: ~6 buffers of d x (level ct) plus the rotations' ModUp digits
+  const int H_all = (int)As.size();
+  const std::size_t dnum = (std::size_t)hx_ctx_dnum(ctx_, nqb), ext = nqb + params_.special_primes.size();
+  const std::size_t per_head = (std::size_t)d * 8 * (3 * cw + 4 * cwb + dnum * ext * N);
+  std::size_t free_b = 0, total_b = 0;
+  cuda_ck(cudaMemGetInfo(&free_b, &total_b), "mem info");
+  const int Hc = (int)std::max<std::size_t>(1, std::min<std::size_t>(H_all, (free_b * 6 / 10) / std::max<std::size_t>(per_head, 1)));
+  std::vector<Ciphertext> outs;
+  for (int h0 = 0; h0 < H_all; h0 += Hc) {
+    const int H = std::min(Hc, H_all - h0);
+    auto in = dev((std::size_t)H * cw), prod = dev((std::size_t)d * H * cw);
+    auto sa = dev((std::size_t)d * H * cwb), sb = dev((std::size_t)d * H * cwb), tmp = dev((std::size_t)d * H * cwb);
+    const auto side = [&](const std::vector<Ciphertext>& X, const std::vector<Plaintext>& masks,
+                          const std::shared_ptr<DeviceBuffer>& out, std::int64_t unit) {
+      for (int h = 0; h < H; ++h)
+        cuda_ck(cudaMemcpyAsync(in->ptr + h * cw, payload(X[h0 + h]).data(), cw * 8, cudaMemcpyDeviceToDevice,
+                                nullptr), "d2d");
+      // prod[j][h][c] = X_h[c] (.) mask_j  (encode_many: masks contiguous [d][nqa][N])
+      ck(hx_mul_bcast(ctx_, prod->ptr, in->ptr, payload(masks[0]).data(), 2 * d * H, 2 * H, 2 * H, nqa, nullptr),
+         "mul_bcast");
+      ck(hx_rescale(ctx_, out->ptr, prod->ptr, 2 * d * H, nqa, nullptr), "rescale");
+      // column / row j -> 0 for j >= 1: key j applied to the H heads of column j
+      if (d > 1) {
+        std::vector<const u64*> keys;
+        std::vector<u64> gal;
+        for (int j = 1; j < d; ++j) {
+          const auto kg = need(unit * j);
+          keys.push_back(kg.first);
+          gal.push_back(kg.second);
+        }
+        ck(hx_rotate_grouped(ctx_, tmp->ptr, out->ptr + (std::size_t)H * cwb, keys.data(), gal.data(), d - 1, H, nqb,
+                             nullptr),
+           "rotate_grouped");
+        cuda_ck(cudaMemcpyAsync(out->ptr + (std::size_t)H * cwb, tmp->ptr, (std::size_t)(d - 1) * H * cwb * 8,
+                                cudaMemcpyDeviceToDevice, nullptr), "d2d");
+      }
+      // replicate: x += Rot_{-unit 2^i}(x), i < log2 d, all d x H at once (one key read)
+      for (int i = 0; i < lg; ++i) {
+        const auto kg = need(-(unit << i));
+        ck(hx_rotate(ctx_, tmp->ptr, out->ptr, kg.first, d * H, nqb, kg.second, nullptr), "rotate");
+        ck(hx_add(ctx_, out->ptr, out->ptr, tmp->ptr, 2 * d * H, nqb, 0, nullptr), "add");
+      }
+    };
+    side(As, cm, sa, 1);
+    side(Bs, rm, sb, d);
+    // d x H ct-ct products + relinearisation, summed over j per head, one rescale
+    ck(hx_mul_relin(ctx_, tmp->ptr, sa->ptr, sb->ptr, rlk_->ptr, d * H, nqb, nullptr), "mul_relin");
+    auto acc = dev((std::size_t)H * cwb);
+    ck(hx_sum_strided(ctx_, acc->ptr, tmp->ptr, d, (long long)H * cwb, 2 * H, (long long)nqb * N, (long long)nqb * N,
+                      nqb, nullptr),
+       "sum");
+    auto outb = dev((std::size_t)H * 2 * (nqb - 1) * N);
+    ck(hx_rescale(ctx_, outb->ptr, acc->ptr, 2 * H, nqb, nullptr), "rescale");
+    cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+    for (int h = 0; h < H; ++h) {
+      const Ciphertext& A = As[h0 + h];
+      const Ciphertext& B = Bs[h0 + h];
+      // trace: exactly the SlotOps schedule of linalg.cpp matmul_ctct, per head
+      trace_.record(OpKind::PtMul, lv, 2 * d);
+      trace_.record(OpKind::Rescale, lv, 2 * d);
+      trace_.record(OpKind::Rotate, lv - 1, 2 * (d - 1) + 2 * (std::size_t)d * lg);
+      trace_.record(OpKind::CtAdd, lv - 1, 2 * (std::size_t)d * lg + (d - 1));
+      trace_.record(OpKind::CtMul, lv - 1, d);
+      trace_.record(OpKind::Rescale, lv - 1);
+      const Scale s_a = A.scale * ms / Scale::prime(modulus_at(lv));
+      const Scale s_b = B.scale * ms_b / Scale::prime(modulus_at(lv));
+      outs.push_back(wrap(outb, (std::size_t)h * 2 * (nqb - 1) * N, lv - 2, s_a * s_b / Scale::prime(modulus_at(lv - 1))));
     }
-    if (d > 1) {
-      ck(hx_rotate_multi(ctx_, tmp->ptr, out->ptr + cwb, keys.data(), gal.data(), d - 1, nqb, nullptr), "rotate_multi");
-      cuda_ck(cudaMemcpyAsync(out->ptr + cwb, tmp->ptr, (std::size_t)(d - 1) * cwb * 8, cudaMemcpyDeviceToDevice,
-                              nullptr), "d2d");
-    }
-    // replicate: x += Rot_{-unit 2^i}(x), i < log2 d, for all d at once
-    for (int i = 0; i < lg; ++i) {
-      const auto kg = need(-(unit << i));
-      ck(hx_rotate(ctx_, tmp->ptr, out->ptr, kg.first, d, nqb, kg.second, nullptr), "rotate");
-      ck(hx_add(ctx_, out->ptr, out->ptr, tmp->ptr, 2 * d, nqb, 0, nullptr), "add");
-    }
-  };
-  side(A, cm, sa, 1);
-  side(B, rm, sb, d);
-  // d ct-ct products + relinearisation, summed over j, one rescale
-  ck(hx_mul_relin(ctx_, tmp->ptr, sa->ptr, sb->ptr, rlk_->ptr, d, nqb, nullptr), "mul_relin");
-  auto acc = dev(cwb);
-  ck(hx_sum_strided(ctx_, acc->ptr, tmp->ptr, d, (long long)cwb, 2, (long long)nqb * N, (long long)nqb * N, nqb, nullptr),
-     "sum");
-  auto outb = dev((std::size_t)2 * (nqb - 1) * N);
-  ck(hx_rescale(ctx_, outb->ptr, acc->ptr, 2, nqb, nullptr), "rescale");
-  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
-  // trace: exactly the SlotOps schedule of linalg.cpp matmul_ctct
-  trace_.record(OpKind::PtMul, lv, 2 * d);
-  trace_.record(OpKind::Rescale, lv, 2 * d);
-  trace_.record(OpKind::Rotate, lv - 1, 2 * (d - 1) + 2 * (std::size_t)d * lg);
-  trace_.record(OpKind::CtAdd, lv - 1, 2 * (std::size_t)d * lg + (d - 1));
-  trace_.record(OpKind::CtMul, lv - 1, d);
-  trace_.record(OpKind::Rescale, lv - 1);
-  const Scale s_a = A.scale * ms / Scale::prime(modulus_at(lv));
-  const Scale s_b = B.scale * ms_b / Scale::prime(modulus_at(lv));
-  return wrap(outb, 0, lv - 2, s_a * s_b / Scale::prime(modulus_at(lv - 1)));
+  }
+  return outs;
 }
 
 Ciphertext GpuLatticeBackend::bsgs_block(const std::vector<Ciphertext>& baby,
@@ -735,6 +767,48 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       ptmuls = d;
       adds = (std::uint64_t)(n1 - 1) * n2;
       for (int j = 0; j < n2; ++j) live[b][j] = 1;
+    } else if (n1 <= 128) {
+      // pruned / scattered block: one index-list MAC over its live (j, k)
+      // entries for all tokens, plaintexts and baby steps read in place
+      std::vector<int> gptr(n2 + 1, 0), ks;
+      std::vector<const u64*> dp;
+      for (int j = 0; j < n2; ++j) {
+        for (int k = 0; k < n1; ++k) {
+          const Plaintext& pt = D[(std::size_t)j * n1 + k];
+          if (!pt.payload) continue;
+          if (pt.level != level) throw LevelMismatchError("bsgs: diagonal level mismatch");
+          if (!have_scale) {
+            dscale = pt.scale;
+            have_scale = true;
+          } else if (pt.scale != dscale) {
+            throw ScaleMismatchError("bsgs: diagonal scales differ");
+          }
+          ks.push_back(k);
+          dp.push_back(payload(pt).data());
+        }
+        gptr[j + 1] = (int)ks.size();
+        const int cnt = gptr[j + 1] - gptr[j];
+        if (cnt) {
+          ptmuls += cnt;
+          adds += cnt - 1;
+          live[b][j] = 1;
+        }
+      }
+      bool uniform = true;
+      const long long bstride = T > 1 ? (long long)(baby_ptr[1] - baby_ptr[0]) : 0;
+      for (int t = 1; t < T && uniform; ++t) uniform = (long long)(baby_ptr[t] - baby_ptr[t - 1]) == bstride;
+      if (!ks.empty()) {
+        if (uniform) {
+          ck(hx_bsgs_mac_sparse(ctx_, inner->ptr + (std::size_t)b * ctw, (long long)jstride, (long long)(blocks * ctw),
+                                baby_ptr[0], bstride, gptr.data(), ks.data(), dp.data(), n1, n2, nqv, T, nullptr),
+             "bsgs_mac_sparse");
+        } else {
+          for (int t = 0; t < T; ++t)
+            ck(hx_bsgs_mac_sparse(ctx_, inner->ptr + ((std::size_t)t * blocks + b) * ctw, (long long)jstride, 0,
+                                  baby_ptr[t], 0, gptr.data(), ks.data(), dp.data(), n1, n2, nqv, 1, nullptr),
+               "bsgs_mac_sparse");
+        }
+      }
     } else {
       for (int j = 0; j < n2; ++j) {
         std::vector<int> ks;

@@ -267,6 +267,30 @@ hxc_ct* hxc_matmul(hxc_backend* b, const hxc_ct* A, const hxc_ct* B, int d, hxc_
   });
 }
 
+int hxc_matmul_heads(hxc_backend* b, const hxc_ct* const* As, const hxc_ct* const* Bs, int H, int d, hxc_ct** out,
+                     hxc_report* rep) {
+  return guard(-1, [&] {
+    auto* g = b->b.get();
+    std::vector<Ciphertext> A, B;
+    for (int h = 0; h < H; ++h) {
+      A.push_back(As[h]->c);
+      B.push_back(Bs[h]->c);
+    }
+    const auto snap = TraceSnapshot::take(g->trace());
+    const auto outs = g->matmul_heads(A, B, d);
+    KernelReport r;
+    r.rotations = snap.delta(g->trace(), OpKind::Rotate) / (std::uint64_t)H;
+    r.pt_muls = snap.delta(g->trace(), OpKind::PtMul) / (std::uint64_t)H;
+    r.ct_muls = snap.delta(g->trace(), OpKind::CtMul) / (std::uint64_t)H;
+    r.adds = snap.delta(g->trace(), OpKind::CtAdd) / (std::uint64_t)H;
+    r.levels_consumed = A[0].level - outs[0].level;
+    r.output_scale = outs[0].scale;
+    fill(rep, r);
+    for (int h = 0; h < H; ++h) out[h] = wrap(outs[h]);
+    return H;
+  });
+}
+
 long long hxc_predicted_rotations(int method, int rows, int cols, int64_t slots) {
   return guard<long long>(-1, [&] {
     const Layout l = method == HXC_ROW    ? Layout::PackedRow

@@ -65,6 +65,7 @@ def lib():
         "hxc_matrix_rotations": (i32, [v, C.POINTER(C.c_int64), i32]),
         "hxc_matvec": (i32, [v, v, v, C.POINTER(v), i32, rp]),
         "hxc_matmul": (v, [v, v, v, i32, rp]),
+        "hxc_matmul_heads": (i32, [v, C.POINTER(v), C.POINTER(v), i32, i32, C.POINTER(v), rp]),
         "hxc_matrix_prepare_shard": (v, [v, f64p, i32, i32, i32, i32, i32, i32]),
         "hxc_matvec_tokens": (i32, [v, v, C.POINTER(v), i32, C.POINTER(v), i32, rp]),
         "hxc_matvec_shard": (i32, [v, v, v, C.POINTER(v), i32, rp]),
@@ -317,6 +318,18 @@ class Backend:
         r = Report()
         c = Ct(self, self.L.hxc_matmul(self.h, A.h, B.h, d, C.byref(r)))
         return c, r.as_dict()
+
+    def matmul_heads(self, As, Bs, d):
+        """H heads batched (keys read once per H heads): ([Ct], per-head report)"""
+        r = Report()
+        H = len(As)
+        a = (C.c_void_p * H)(*[x.h for x in As])
+        b = (C.c_void_p * H)(*[x.h for x in Bs])
+        outs = (C.c_void_p * H)()
+        k = self.L.hxc_matmul_heads(self.h, a, b, H, d, outs, C.byref(r))
+        if k < 0:
+            raise _err()
+        return [Ct(self, outs[i]) for i in range(k)], r.as_dict()
 
     def polyeval(self, x, coeffs, basis="power", lo=-1.0, hi=1.0):
         """slot-wise polynomial (SPEC polyeval): basis "power" or "chebyshev" on [lo, hi]"""

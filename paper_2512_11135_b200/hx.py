@@ -160,6 +160,18 @@ class Context:
     def launches(self) -> int:
         return int(self.L.hx_ctx_launches(self.h))
 
+    def time_kernel(self, name):
+        """record CUDA events around every launch of kernel family `name` (None: off)"""
+        self.L.hx_ctx_time_kernel.argtypes = [C.c_void_p, C.c_char_p]
+        _check(self.L.hx_ctx_time_kernel(self.h, name.encode() if name else None), "hx_ctx_time_kernel")
+
+    def kernel_time(self):
+        """(summed device ms, launches) of the timed kernel family since the last call"""
+        ms, n = C.c_double(), C.c_longlong()
+        self.L.hx_ctx_kernel_time.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
+        _check(self.L.hx_ctx_kernel_time(self.h, C.byref(ms), C.byref(n)), "hx_ctx_kernel_time")
+        return ms.value, n.value
+
     # ---- ops (torch int64 CUDA tensors) ----
     def ntt_fwd(self, x, batch, n_q, n_p=0, stream=None):
         _check(self.L.hx_ntt_fwd(self.h, _p(x), batch, n_q, n_p, _stream(stream)), "hx_ntt_fwd")
@@ -237,6 +249,20 @@ class Context:
     def bsgs_mac(self, inner, baby, diags, diag_limbs, n1, n2, n_q, stream=None):
         _check(self.L.hx_bsgs_mac(self.h, _p(inner), _p(baby), _p(diags), diag_limbs, n1, n2, n_q,
                                   _stream(stream)), "hx_bsgs_mac")
+
+    def bsgs_mac_sparse(self, inner, inner_jstride, baby, group_ptr, ks, diag_ptrs, n1, n2, n_q, tokens=1,
+                        inner_tstride=0, baby_tstride=0, stream=None):
+        """index-list MAC: group j = entries [group_ptr[j], group_ptr[j+1]), entry e
+        multiplies baby ks[e] by the device words at diag_ptrs[e]"""
+        gp = (C.c_int * len(group_ptr))(*group_ptr)
+        kk = (C.c_int * max(1, len(ks)))(*ks)
+        dp = (C.c_void_p * max(1, len(diag_ptrs)))(*diag_ptrs)
+        self.L.hx_bsgs_mac_sparse.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p,
+                                              C.c_longlong, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                              C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        self.L.hx_bsgs_mac_sparse.restype = C.c_int
+        _check(self.L.hx_bsgs_mac_sparse(self.h, _p(inner), inner_jstride, inner_tstride, _p(baby), baby_tstride, gp,
+                                         kk, dp, n1, n2, n_q, tokens, _stream(stream)), "hx_bsgs_mac_sparse")
 
     def keygen_ksk(self, key, s_full, sp_full, a_full, e, stream=None):
         _check(self.L.hx_keygen_ksk(self.h, _p(key), _p(s_full), _p(sp_full), _p(a_full), _p(e),

@@ -293,3 +293,36 @@ def test_n16_config5_slice_shards_words_vs_oracle():
     assert np.array_equal(out_words(ov, outs, lvl), exp)
     y = np.concatenate([be.decrypt(o)[:4096] for o in outs])
     assert np.abs(y - A @ x).max() < 1e-4
+
+
+@pytest.mark.parametrize("name,d,H", [("c1", 8, 3), ("c2s", 16, 4)])
+def test_matmul_heads_words_vs_oracle(name, d, H):
+    """config 4's head batch (hxc_matmul_heads): every head's output equals the
+    single-head product and the oracle's matmul word for word; per-head counters"""
+    ov = view(name)
+    be = ov.be
+    lvl = be.max_level
+    rng = np.random.default_rng(90 + d)
+    be.gen_rotation_keys(be.matmul_rotations(d))
+    As = [rng.normal(0, 1, (d, d)) for _ in range(H)]
+    Bs = [rng.normal(0, 1, (d, d)) for _ in range(H)]
+    ca = [be.encrypt(A.reshape(-1), lvl) for A in As]
+    cb = [be.encrypt(B.reshape(-1), lvl) for B in Bs]
+    outs, rep = be.matmul_heads(ca, cb, d)
+    lg = d.bit_length() - 1
+    assert rep["rotations"] == 2 * d * (1 + lg) - 2 and rep["ct_muls"] == d and rep["levels_consumed"] == 2
+    n = be.slots
+    qa, qb = ov.q(lvl), ov.q(lvl - 1)
+    cm = [ov.encode(make_mask("col", j, d, n), lvl, float(qa)) for j in range(d)]
+    rm = [ov.encode(make_mask("row", j, d, n), lvl, scale_double(-40, [qa, qb])) for j in range(d)]
+    keys = ov.keys(be.matmul_rotations(d))
+    rlk = ov.rlk()
+    for h in range(H):
+        single, _ = be.matmul(ca[h], cb[h], d)
+        got = ov.ct(outs[h], lvl - 2)
+        assert np.array_equal(got, ov.ct(single, lvl - 2)), h
+        if h in (0, H - 1):
+            exp = ov.orc.matmul_ctct(ov.ct(ca[h]), ov.ct(cb[h]), lvl + 1, d, cm, rm, rlk, keys)
+            assert np.array_equal(got, exp), h
+        dec = be.decrypt(outs[h])[: d * d].reshape(d, d)
+        assert np.abs(dec - As[h] @ Bs[h]).max() < 1e-3 * d

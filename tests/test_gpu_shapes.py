@@ -276,3 +276,39 @@ def test_large_batch_ks_inner_slices(name, B):
     for b in range(B):
         assert np.array_equal(Dh[b], orc.modup(c1h[b], nq)), f"modup {b}"
         assert np.array_equal(Uh[b], orc.ks_inner(Dh[b], kh, nq, g)), f"inner {b}"
+
+
+def test_bsgs_mac_sparse_pruned_w1_block_n16():
+    """the index-list MAC of a 90 %-pruned W1 block (n1 = n2 = 32, 24 limbs,
+    N = 2^16, 2 tokens) vs the oracle MAC with the dead diagonals zeroed"""
+    import torch
+
+    p, ctx, orc = env("c2")
+    nq, n1, n2, T = 24, 32, 32, 2
+    rng = np.random.default_rng(43)
+    live = sorted(rng.choice(n1 * n2, 102, replace=False).tolist())
+    baby = dev_uniform(ctx, nq, 0, T * n1 * 2, 44).view(T, n1, 2, nq, ctx.n)
+    diags = dev_uniform(ctx, nq, 0, len(live), 45).view(len(live), nq, ctx.n)
+    gptr, ks, ptrs = [0], [], []
+    for j in range(n2):
+        for e, idx in enumerate(live):
+            if idx // n1 == j:
+                ks.append(idx % n1)
+                ptrs.append(diags[e].data_ptr())
+        gptr.append(len(ks))
+    ctw = 2 * nq * ctx.n
+    inner = torch.zeros((T, n2, 2, nq, ctx.n), dtype=torch.int64, device="cuda")
+    ctx.bsgs_mac_sparse(inner, ctw, baby, gptr, ks, ptrs, n1, n2, nq, tokens=T,
+                        inner_tstride=n2 * ctw, baby_tstride=n1 * ctw)
+    torch.cuda.synchronize()
+    for k in (0, 5):
+        o1 = Oracle(p["logn"], [p["chain"][k]], [], 1)
+        dense = np.zeros((n1 * n2, 1, ctx.n), dtype=np.uint64)
+        dh = host(diags[:, k, :].contiguous())
+        for e, idx in enumerate(live):
+            dense[idx, 0] = dh[e]
+        for t in range(T):
+            bk = host(baby[t, :, :, k, :].contiguous()).reshape(n1, 2, 1, ctx.n)
+            exp = o1.bsgs_mac(bk, dense, n1, n2, 1)
+            got = host(inner[t, :, :, k, :].contiguous()).reshape(n2, 2, 1, ctx.n)
+            assert np.array_equal(got, exp), (k, t)

@@ -276,3 +276,40 @@ def test_golden_decode_matches_reference_decode(gold):
     # identical CRT integers; the FFT is the reference's operation order, so
     # the slots agree to the last few ulps
     assert np.abs(got - exp).max() <= 1e-12 * max(1.0, np.abs(exp).max())
+
+
+@pytest.mark.skipif(not ref_available(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_live_reference_bsgs_matvec(cfg):
+    """the matvec CPU arm (ref_matvec_bsgs over the reference primitives) ==
+    hxo_matvec_bsgs (lazy giant steps) word for word, 2 row blocks, one zero
+    diagonal, 4 threads"""
+    import ctypes as C
+
+    if cfg == "c1":
+        p, nq, n1, n2 = config1(11), 3, 4, 4
+    else:
+        p, nq, n1, n2 = config2(11, 24), 24, 4, 4
+    n, K = 1 << p["logn"], len(p["special"])
+    orc = Oracle(p["logn"], p["chain"], p["special"], p["alpha"])
+    ref = Ref(p["logn"], p["chain"], p["special"], p["alpha"])
+    ref.L.ref_set_threads(ref.h, 4)
+    rng = np.random.default_rng(77)
+    full = p["chain"] + p["special"]
+    dn = orc.dnum(len(p["chain"]))
+    keys = {r: np.ascontiguousarray(uniform_limbs(rng, full, n, (dn, 2)))
+            for r in list(range(1, n1)) + [n1 * j for j in range(1, n2)]}
+    blocks = 2
+    diags = [uniform_limbs(rng, p["chain"][:nq], n) for _ in range(blocks * n1 * n2)]
+    diags[5] = None
+    x = uniform_limbs(rng, p["chain"][:nq], n, (2,))
+    exp = orc.matvec_bsgs(x, nq, n1, n2, blocks, diags, keys, lazy=True)
+    got = np.zeros_like(exp)
+    u64p = C.POINTER(C.c_uint64)
+    dt = (u64p * len(diags))(*[ptr(d) if d is not None else None for d in diags])
+    kt = (u64p * (n // 2))()
+    for r, k in keys.items():
+        kt[r] = ptr(k)
+    ref.L.ref_matvec_bsgs.argtypes = [C.c_void_p, u64p, u64p] + [C.c_int] * 4 + [C.POINTER(u64p)] * 2 + [C.c_int] * 3
+    assert ref.L.ref_matvec_bsgs(ref.h, ptr(got), ptr(x), nq, n1, n2, blocks, dt, kt, 0, -1, 1) == 0
+    assert np.array_equal(got, exp)
