@@ -38,6 +38,11 @@ BATCH = 256
 ALPHA = 3
 HOIST_R = 32
 HOIST_CHUNK = 8
+DOMINANT = "modup_col_kernel"
+F64_LANES_PER_CLK = 62.6  # DFMA lanes / clk / SM, measured on the box (tools/microbench/pipes.cu)
+MODUP_CONV_OPS = 21       # FP64 ops per converted word (3 sources: split products + exact reduction)
+COL_PASS_OPS = 32         # 8 of the 16 radix-2 stages, 4 FP64 ops per element per stage
+DOM_TRAFFIC_NCU = None    # set from profiles/ when an ncu --set full capture of this build exists
 
 
 def primes(fp64_specials: bool = False):
@@ -200,36 +205,129 @@ def peaks():
 
 
 # ------------------------------------------------------------------ CPU arms
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def _ref_or_port(chain, special, alpha, logn=LOGN, threads=1):
+    """(kind, handle): the reference's compiled primitives (oracle/_ref) when
+    built, else the C oracle port; both thread over the host cores"""
+    from oracle_bindings import Oracle, Ref, oracle_lib, ref_available
+
+    if ref_available():
+        r = Ref(logn, chain, special, alpha)
+        r.L.ref_set_threads(r.h, threads)
+        return "reference", r
+    oracle_lib().hxo_set_threads(threads)
+    return "port", Oracle(logn, chain, special, alpha)
+
+
 def cpu_reference_ks(samples: int, threads: int):
     """The reference's own primitives (oracle/_ref: NttTables, Modulus with the
-    Barrett fix) composed into the SPEC key switch, timed on host cores."""
-    import numpy as np
+    Barrett fix) composed into the SPEC key switch over a batch of `samples`
+    ciphertexts spread over a persistent pool of `threads` host threads (one
+    whole rotation per task: the independent-ciphertext axis of BASELINE.md
+    section 3).  Returns (KS/s, kind, seconds)."""
+    import ctypes as C
 
-    from oracle_bindings import Oracle, Ref, galois_elt, ptr, ref_available, uniform_limbs
+    from oracle_bindings import galois_elt, uniform_limbs
 
     chain, special = primes()
     rng = np.random.default_rng(1)
-    kind = "reference" if ref_available() else "port"
     key = uniform_limbs(rng, chain + special, N, ((N_CHAIN + ALPHA - 1) // ALPHA, 2))
-    ct = uniform_limbs(rng, chain, N, (2,))
-    out = np.zeros_like(ct)
+    cts = uniform_limbs(rng, chain, N, (samples, 2))
+    out = np.zeros_like(cts)
     g = galois_elt(1, N)
+    kind, h = _ref_or_port(chain, special, ALPHA, threads=threads)
     if kind == "reference":
-        r = Ref(LOGN, chain, special, ALPHA)
-        r.L.ref_set_threads(r.h, threads)
-        run = lambda: r.L.ref_rotate(r.h, ptr(ct), ptr(key), ptr(out), N_CHAIN, g)  # noqa: E731
-    else:
-        from oracle_bindings import oracle_lib
+        h.L.ref_rotate_batch.argtypes = [C.c_void_p] * 4 + [C.c_int, C.c_int, C.c_uint64]
 
-        o = Oracle(LOGN, chain, special, ALPHA)
-        oracle_lib().hxo_set_threads(threads)
-        run = lambda: o.rotate(ct, key, N_CHAIN, g)  # noqa: E731
-    run()  # warm
+        def run():
+            assert h.L.ref_rotate_batch(h.h, cts.ctypes.data, key.ctypes.data, out.ctypes.data, samples, N_CHAIN, g) == 0
+    else:
+        def run():
+            for b in range(samples):
+                out[b] = h.rotate(cts[b], key, N_CHAIN, g)
     t = time.perf_counter()
-    for _ in range(samples):
-        run()
+    run()
     dt = time.perf_counter() - t
     return samples / dt, kind, dt
+
+
+def cpu_reference_matvec(threads: int):
+    """matvec half of the metric on the host cores:
+    config 1 in full (N = 2^13, 64 x 64 BSGS, n1 = n2 = 8), and config 3's
+    FFN W1 (d = 1024, 3 row blocks, n1 = n2 = 32, N = 2^16, 24 + 3 primes) for
+    one token on a stated slice -- the 31 hoisted baby steps in full, then
+    giant groups 0..7 of one block (256 diagonals), extrapolated to 3 blocks x
+    32 groups.  Same schedule as the product (ref_matvec_bsgs = hxo_matvec_bsgs
+    with lazy giant steps); synthetic words (timing does not depend on them)."""
+    import ctypes as C
+
+    from oracle_bindings import ptr, uniform_limbs
+    from configs import config1
+
+    res = {}
+    u64p = C.POINTER(C.c_uint64)
+
+    def run(kind, h, x, n_q, n1, n2, blocks, diags, keys, gb, ge):
+        slots = (1 << h.logn) // 2
+        if kind == "reference":
+            dt_ = (u64p * len(diags))(*[ptr(d_) if d_ is not None else None for d_ in diags])
+            kt = (u64p * slots)()
+            for r, k in keys.items():
+                kt[r] = ptr(k)
+            out = np.zeros((blocks, 2, n_q - 1, 1 << h.logn), dtype=np.uint64)
+            h.L.ref_matvec_bsgs.argtypes = [C.c_void_p, u64p, u64p] + [C.c_int] * 4 + [C.POINTER(u64p)] * 2 + \
+                [C.c_int] * 3
+            t = time.perf_counter()
+            assert h.L.ref_matvec_bsgs(h.h, ptr(out), ptr(x), n_q, n1, n2, blocks, dt_, kt, gb, ge, 1) == 0
+            return time.perf_counter() - t
+        t = time.perf_counter()
+        h.matvec_bsgs(x, n_q, n1, n2, blocks, diags, keys, giant=(gb, ge), lazy=True)
+        return time.perf_counter() - t
+
+    # config 1 in full
+    p = config1(13)
+    kind, h = _ref_or_port(p["chain"], p["special"], 1, logn=13, threads=threads)
+    rng = np.random.default_rng(20251211 * 10 + 1)
+    n1c = n2c = 8
+    full = p["chain"] + p["special"]
+    keys = {r: np.ascontiguousarray(uniform_limbs(rng, full, 1 << 13, (3, 2)))
+            for r in list(range(1, n1c)) + [n1c * j for j in range(1, n2c)]}
+    diags = [uniform_limbs(rng, p["chain"], 1 << 13) for _ in range(64)]
+    x = uniform_limbs(rng, p["chain"], 1 << 13, (2,))
+    run(kind, h, x, 3, n1c, n2c, 1, diags, keys, 0, -1)  # warm
+    reps = 5
+    t1 = sum(run(kind, h, x, 3, n1c, n2c, 1, diags, keys, 0, -1) for _ in range(reps)) / reps
+    res["config1_bsgs"] = {"matvec_per_s": 1.0 / t1, "ms_per_matvec": 1e3 * t1, "kind": kind, "cores": threads,
+                           "sample": f"{reps} full 64 x 64 BSGS matvecs (N = 2^13, 14 rotations)"}
+    del h
+    # FFN W1 slice at N = 2^16 (one key / one diagonal word set reused: timing only)
+    chain, special = primes()
+    kind, h = _ref_or_port(chain, special, ALPHA, threads=threads)
+    key = np.ascontiguousarray(uniform_limbs(rng, chain + special, N, ((N_CHAIN + ALPHA - 1) // ALPHA, 2)))
+    n1, n2, G = 32, 32, 8
+    keys = {r: key for r in list(range(1, n1)) + [n1 * j for j in range(1, n2)]}
+    dg = uniform_limbs(rng, chain, N)
+    diags = [dg] * (n1 * n2)
+    x = uniform_limbs(rng, chain, N, (2,))
+    t_baby = run(kind, h, x, N_CHAIN, n1, n2, 1, diags, keys, 0, 0)  # baby steps (+ rescale of a zero sum)
+    t_slice = run(kind, h, x, N_CHAIN, n1, n2, 1, diags, keys, 0, G)
+    per_group = (t_slice - t_baby) / G
+    t_w1 = t_baby + 3 * n2 * per_group
+    res["ffn_w1"] = {"matvec_per_s": 1.0 / t_w1, "ms_per_matvec": 1e3 * t_w1, "kind": kind, "cores": threads,
+                     "extrapolated": True, "baby_steps_s": t_baby, "per_giant_group_s": per_group,
+                     "sample": f"31 hoisted baby steps + giant groups 0..{G - 1} of one block (256 diagonals) "
+                               f"timed ({t_slice:.1f} s), extrapolated to 3 blocks x 32 groups"}
+    return res
 
 
 def run_reference_arm(args):
@@ -237,13 +335,12 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    per_step = 1
-    t_total, vals = 0.0, []
+    per_step = threads  # one ciphertext per host thread
+    t_total = 0.0
     kind = "port"
     for i in range(args.warmup + args.steps):
         v, kind, dt = cpu_reference_ks(per_step, threads)
         if i >= args.warmup:
-            vals.append(v)
             t_total += dt
     value = args.steps * per_step / t_total
     line = {
@@ -251,11 +348,13 @@ def run_reference_arm(args):
         "value": value, "unit": "KS/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": "config2 single-rotation KS (bounded sample: 1 ciphertext per step)",
+        "config": {"workload": f"config2 single-rotation KS (bounded sample: {per_step} ciphertexts per step, "
+                               "one per host thread)",
                    "batch_per_step": per_step, "N": N, "chain_primes": N_CHAIN, "special_primes": 3,
                    "alpha": ALPHA},
-        "cpu_baseline": {"value": value, "unit": "KS/s", "cores": threads, "kind": kind,
-                         "sample": f"{args.steps} x 1 ciphertext rotation key switch"},
+        "cpu_baseline": {"value": value, "unit": "KS/s", "cores": threads, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": f"{args.steps} x {per_step}-ciphertext rotation key switch batches "
+                                   "(persistent pool, one ciphertext per thread)"},
         "e2e": {"value": value, "unit": "KS/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -274,7 +373,7 @@ def _prune_diagonals(M, d, rng, frac=0.9):
     return M
 
 
-def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=16, chunk=8):
+def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=128):
     """BASELINE configs[2]: FFN up-projection W1 (768 x 3072) and down-projection
     W2 (3072 x 768), N(0, 0.02^2), as BSGS linear transforms at N=2^16 / 24+3
     primes through the helix C-ABI (hxc_matvec): W1 d = 1024, 3 row blocks,
@@ -341,8 +440,9 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=16, chunk=8):
                      "rotations": rep["rotations"], "pt_muls": rep["pt_muls"], "nonzero_diagonals": info["nonzero"],
                      "diag_bytes": info["nonzero"] * 24 * N * 8, "prepare_s": prep}
         del outs
-        if not prune and tokens > 0 and method == BSGS:
-            chunk = max(1, 8 // info["blocks"]) if d < 4096 else 8  # bound the grouped-rotation working set
+        if tokens > 0:
+            # token chunk bounded by the working set: inner sums [n2][chunk][blocks] + baby sets [chunk][n1]
+            chunk = 8 if d >= 4096 else (32 if method == BSGS_STACKED else 16)
             # T tokens through the same matrix, key switches batched over a chunk
             # of `chunk` tokens (hxc_matvec_tokens); per-token throughput
             xt = [be.encrypt(np.tile(np.concatenate([rng.uniform(-1, 1, M.shape[1]), np.zeros(d - M.shape[1])]),
@@ -460,39 +560,66 @@ def config5_stacked_bench(torch, chain, special, rows=11008, cols=4096, iters=3)
                                      "prepare_s": prep}}
 
 
-def matmul_bench(torch, chain, special, d=128, n_q=4, iters=2):
-    """BASELINE configs[3]: ct x ct matmul Q K^T of one head (128 x 64 padded to
-    d = 128, N(0, 1)) through hxc_matmul (SPEC square-padded schedule), at a
-    4-limb level of the config-2 chain (q0 + 3 x 40-bit, K = 3 specials)."""
+def matmul_bench(torch, chain, special, d=128, n_q=4, iters=2, heads=12):
+    """BASELINE configs[3]: ct x ct matmul Q K^T (128 x 64 padded to d = 128,
+    N(0, 1)) through the SPEC square-padded schedule, at a level of n_q limbs
+    of the config-2 chain (K = 3 specials): one head (hxc_matmul) and the
+    12-head batch (hxc_matmul_heads: each rotation / relinearisation launch
+    covers every head, so the 268 rotation keys are read once per batch)."""
     from paper_2512_11135_b200.helix import Backend, params_json
 
     rng = np.random.default_rng(20251211 * 10 + 4)
     be = Backend(params_json(LOGN, chain[:n_q], special, ALPHA, 40), seed=4)
-    Q = np.zeros((d, d))
-    Kt = np.zeros((d, d))
-    Q[:, :64] = rng.normal(0, 1, (128, 64))
-    Kt[:64, :] = rng.normal(0, 1, (128, 64)).T
+    lvl = n_q - 1
+
+    def head():
+        Q = np.zeros((d, d))
+        Kt = np.zeros((d, d))
+        Q[:, :64] = rng.normal(0, 1, (128, 64))
+        Kt[:64, :] = rng.normal(0, 1, (128, 64)).T
+        return Q / 8, Kt / 8
+
     t0 = time.perf_counter()
     rots = Backend.matmul_rotations(d)
     be.gen_rotation_keys(rots)
     torch.cuda.synchronize()
     prep = time.perf_counter() - t0
-    ca, cb = be.encrypt(Q.reshape(-1) / 8), be.encrypt(Kt.reshape(-1) / 8)
+    Q, Kt = head()
+    ca, cb = be.encrypt(Q.reshape(-1), lvl), be.encrypt(Kt.reshape(-1), lvl)
     c, rep = be.matmul(ca, cb, d)  # warm-up + correctness
-    got = be.decrypt(c)[: d * d].reshape(d, d)
-    err = float(np.abs(got - (Q / 8) @ (Kt / 8)).max())
+    err = float(np.abs(be.decrypt(c)[: d * d].reshape(d, d) - Q @ Kt).max())
+    del c
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(iters):
         c, rep = be.matmul(ca, cb, d)
+        del c
     e1.record()
     torch.cuda.synchronize()
     secs = e0.elapsed_time(e1) / 1e3 / iters
+    res = {"matmul_per_s": 1.0 / secs, "ms_per_matmul": 1e3 * secs, "max_abs_err": err, "level_limbs": n_q,
+           "rotations": rep["rotations"], "ct_muls": rep["ct_muls"], "pt_muls": rep["pt_muls"],
+           "distinct_keys": len(rots), "keygen_s": prep}
+    if heads > 1:
+        hs = [head() for _ in range(heads)]
+        cas = [be.encrypt(q.reshape(-1), lvl) for q, _ in hs]
+        cbs = [be.encrypt(k.reshape(-1), lvl) for _, k in hs]
+        outs, rep_h = be.matmul_heads(cas, cbs, d)  # warm-up + correctness
+        herr = max(float(np.abs(be.decrypt(o)[: d * d].reshape(d, d) - q @ k).max())
+                   for o, (q, k) in zip(outs[:2], hs[:2]))
+        del outs
+        torch.cuda.synchronize()
+        e0.record()
+        outs, rep_h = be.matmul_heads(cas, cbs, d)
+        e1.record()
+        torch.cuda.synchronize()
+        del outs
+        hsecs = e0.elapsed_time(e1) / 1e3
+        res.update({f"heads{heads}_ms": 1e3 * hsecs, f"heads{heads}_ms_per_head": 1e3 * hsecs / heads,
+                    f"heads{heads}_matmul_per_s": heads / hsecs, f"heads{heads}_max_abs_err": herr})
     be.close()
-    return {"matmul_d128": {"matmul_per_s": 1.0 / secs, "ms_per_matmul": 1e3 * secs, "max_abs_err": err,
-                            "level_limbs": n_q, "rotations": rep["rotations"], "ct_muls": rep["ct_muls"],
-                            "pt_muls": rep["pt_muls"], "distinct_keys": len(rots), "keygen_s": prep}}
+    return res
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -553,6 +680,9 @@ def main():
         step()
     barrier()
     sampler.rows.clear()  # clocks of the timed region only
+    # live CUDA-event timing of the step's dominant kernel (modup_col_kernel:
+    # ModUp basis conversion fused into the forward COL pass) on its stream
+    ctx.time_kernel(DOMINANT)
     l0 = ctx.launches()
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     t0, t1 = evs[0], evs[-1]
@@ -564,6 +694,8 @@ def main():
     print("step ms:", [round(evs[k].elapsed_time(evs[k + 1]), 2) for k in range(args.steps)], file=sys.stderr)
     launches = ctx.launches() - l0
     clocks = sampler.stop()
+    dom_ms, dom_launches = ctx.kernel_time()
+    ctx.time_kernel(None)
     secs = t0.elapsed_time(t1) / 1e3
     if world > 1:
         tt = torch.tensor([secs], device=dev)
@@ -572,38 +704,56 @@ def main():
     ks_total = BATCH * args.steps * world
     value = ks_total / secs
 
-    # ---- roofline of the dominant kernel family (the NTT) ----
-    # algorithmic bytes per limb-NTT = read + write one limb = 2 N 8 B.
-    # One KS at 24 limbs runs 24 INTT (ModUp) + 8*24 NTT (ModUp) + 2*3 INTT +
-    # 2*24 NTT (ModDown) = 270 limb transforms.
+    # ---- roofline of the step's dominant kernel, measured inside the timed region ----
     hbm_peak, peak_kind = peaks()
+    f64_peak = F64_LANES_PER_CLK * 148 * 1965e6  # measured DFMA rate x SMs x max SM clock
+    steps = args.steps
+    dom_s = dom_ms / 1e3 / max(1, dom_launches)  # average launch (one per step)
+    f64_t = sum(1 for q in chain[1:] if q < (1 << 47))  # FP64-class chain primes (all but q0)
+    # ModUp targets per ciphertext: every chain limb outside the digit + the K specials;
+    # FP64-class ones get conversion + COL pass here, integer-class (60-bit) only conversion
+    dn = (nq + ALPHA - 1) // ALPHA
+    f64_targets = sum(sum(1 for i in range(nq) if not (d * ALPHA <= i < (d + 1) * ALPHA) and chain[i] < (1 << 47))
+                      for d in range(dn))
+    all_targets = dn * (nq + K) - nq
+    dom_ops = BATCH * f64_targets * N * (MODUP_CONV_OPS + COL_PASS_OPS)
+    dom_bytes = BATCH * (nq + all_targets) * N * 8  # read the INTT'd digit limbs, write every target limb once
+    roofline = {"kernel": DOMINANT + "<S=8,OB=3,alpha=3> (ModUp FastBConv fused into the forward COL pass; "
+                          f"{dom_s * 1e3:.2f} ms of the {1e3 * secs / steps:.2f} ms step, CUDA events on its stream "
+                          "over the timed region)",
+                "bound": "fp64", "achieved": dom_ops / dom_s / 1e12, "peak": f64_peak / 1e12,
+                "unit": "T FP64 lane-op/s", "frac": dom_ops / dom_s / f64_peak,
+                "traffic": DOM_TRAFFIC_NCU, "peak_kind": "measured DFMA 62.6 lanes/clk/SM (tools/microbench/pipes.cu) "
+                                                         "x 148 SMs x 1965 MHz",
+                "lane_ops_per_launch": dom_ops, "kernel_ms": dom_s * 1e3, "launches": dom_launches,
+                "share_of_step": dom_s * steps / secs,
+                "ops_model": f"({MODUP_CONV_OPS} conversion + {COL_PASS_OPS} COL-pass) FP64 ops per FP64-class "
+                             f"target word, {f64_targets} such targets per ciphertext",
+                "hbm": {"achieved": dom_bytes / dom_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                        "frac": dom_bytes / dom_s / 1e9 / hbm_peak, "algorithmic_bytes_per_launch": dom_bytes,
+                        "peak_kind": peak_kind},
+                "note": "FP64-pipe bound (DESIGN.md section 5): the conversion and NTT butterflies run on "
+                        "B200's FP64 pipe; traffic = ncu dram bytes of one launch (profiles/)"}
+    # step level: SURVEY 8(d) algorithmic bytes of a 256-ciphertext KS step (key once + in + out)
+    step_bytes = BATCH * 2 * (2 * nq * N * 8) + dn * 2 * (nq + K) * N * 8
+    roofline_step = {"bound": "hbm", "achieved": step_bytes / (secs / steps) / 1e9, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": step_bytes / (secs / steps) / 1e9 / hbm_peak,
+                     "algorithmic_bytes_per_step": step_bytes,
+                     "note": "SURVEY 8(d): 256 ciphertexts in + out and one 226.5 MB key per step; the NTT-bearing "
+                             "key switch is FP64/INT-issue bound (SURVEY 7, hard part 1)"}
+    # per-kernel shares of the step (one extra untimed step per kernel family)
+    breakdown = {}
+    for fam in ("modup_col_kernel", "ks_row_inner_f64_kernel", "ntt_pass_kernel", "ntt_row_combine_kernel",
+                "moddown_col_kernel"):
+        ctx.time_kernel(fam)
+        step()
+        ms_, cnt = ctx.kernel_time()
+        breakdown[fam] = {"ms": ms_, "launches": cnt, "share": ms_ / (1e3 * secs / steps)}
+    ctx.time_kernel(None)
+    # standalone forward NTT (limb-NTT/s extra)
     ntt_buf = rand_limbs(torch, gen, chain, (BATCH, 2), dev)
     ntt_secs = time_loop(torch, lambda: ctx.ntt_fwd(ntt_buf, 2 * BATCH, nq, 0, stream), 3, 1, stream)
     ntt_limbs = 2 * BATCH * nq
-    ntt_transform_s = ntt_secs / 3  # one forward transform = COL + ROW pass launches
-    ntt_bytes = ntt_limbs * 2 * N * 8  # algorithmic: read + write each limb once
-    ntt_achieved = ntt_bytes / ntt_transform_s / 1e9
-    roofline = {"kernel": "ntt_pass_kernel (forward transform of 512 polys x 24 limbs: COL + ROW "
-                          "pass launches, FP64 pipe for the 40-bit limbs)",
-                "bound": "hbm", "achieved": ntt_achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": ntt_achieved / hbm_peak, "traffic": 2 * ntt_bytes, "peak_kind": peak_kind,
-                "algorithmic_bytes_per_launch": ntt_bytes,
-                "note": "traffic = 2 x algorithmic: the two-pass N = 256 x 256 split re-reads each "
-                        "limb once (profiles/); DESIGN.md section 5"}
-
-    # the pipe that actually bounds the transform: FP64 (profiles/: DRAM ~50-64 %,
-    # FP64 pipe 50-70 % active).  Algorithmic FP64 lane-ops of the FP64-class
-    # limbs: 8 per butterfly (h, l, quotient x2, remainder, sum, X +- T), N/2
-    # log2 N butterflies per limb; peak = DFMA 62.6 lanes/clk/SM measured
-    # (tools/microbench/pipes.cu) x 148 SMs x the max SM clock
-    f64_limbs = 2 * BATCH * sum(1 for q in chain if q < (1 << 47))
-    f64_ops = f64_limbs * (N // 2) * LOGN * 8
-    f64_peak = 62.6 * 148 * 1965e6
-    roofline_fp64 = {"kernel": roofline["kernel"], "bound": "fp64", "achieved": f64_ops / ntt_transform_s / 1e12,
-                     "peak": f64_peak / 1e12, "unit": "T lane-op/s",
-                     "frac": f64_ops / ntt_transform_s / f64_peak, "lane_ops_per_launch": f64_ops,
-                     "peak_kind": "measured DFMA rate (62.6 lanes/clk/SM) x 148 SMs x 1965 MHz"}
-
     extras = {"limb_ntt_per_s": ntt_limbs / (ntt_secs / 3)}
     if not args.no_extras:
         # the same batch-256 key switch with 3 special primes < 2^47 (FP64 class):
@@ -640,9 +790,10 @@ def main():
         hm = time_loop(torch, lambda: ctx.mul_relin(out, cts, b2, rlk, BATCH, nq, stream), 2, 2, stream)
         extras["hmult_relin_per_s"] = BATCH * 2 / hm
         del b2
-        # 32-rotation hoisted batch, in chunks of HOIST_CHUNK ciphertexts
+        # 32-rotation hoisted batch with 32 DISTINCT rotation keys (amounts
+        # 1..32, 7.2 GB), in chunks of HOIST_CHUNK ciphertexts
         gs = [pow(5, k, 2 * N) for k in range(1, HOIST_R + 1)]
-        keys = [key] * HOIST_R  # one resident key reused (key bytes identical in size)
+        keys = [key] + [make_key(torch, ctx, gen, chain, special, g_, dev) for g_ in gs[1:]]
         hout = torch.empty((HOIST_CHUNK, HOIST_R, 2, nq, N), dtype=torch.int64, device=dev)
 
         def hoist():
@@ -651,7 +802,8 @@ def main():
 
         hs = time_loop(torch, hoist, 1, 2, stream)
         extras["hoisted32_ks_per_s"] = BATCH * HOIST_R / hs
-        del hout
+        extras["hoisted32_keys"] = "32 distinct rotation keys (amounts 1..32)"
+        del hout, keys
 
     # ---- e2e through the host-buffer C-ABI entry point ----
     hin = torch.empty(cts.shape, dtype=torch.int64, pin_memory=True)
@@ -696,20 +848,23 @@ def main():
         torch.cuda.empty_cache()
         extras.update(ffn_bsgs_bench(torch, chain, special, args))
         torch.cuda.empty_cache()
-        try:
-            extras.update(matmul_bench(torch, chain, special))
-        except Exception as exc:  # reported, never fatal for the headline line
-            extras["matmul_d128"] = {"error": str(exc)[:200]}
-        torch.cuda.empty_cache()
+        # config 4: level sweep (3 / 4 / 24 limbs), one head and the 12-head batch
+        for nql in (3, 4, 24):
+            try:
+                extras[f"matmul_d128_l{nql}"] = matmul_bench(torch, chain, special, n_q=nql,
+                                                             iters=1 if nql == 24 else 2)
+            except Exception as exc:  # reported, never fatal for the headline line
+                extras[f"matmul_d128_l{nql}"] = {"error": str(exc)[:200]}
+            torch.cuda.empty_cache()
         # the same matmul with FP64-class special primes (parameter co-design:
         # at a 4-limb level the 60-bit specials' integer passes dominate)
         try:
             chain47, special47 = primes(fp64_specials=True)
-            mm = matmul_bench(torch, chain47, special47)["matmul_d128"]
+            mm = matmul_bench(torch, chain47, special47, heads=0)
             mm["special_bits"] = [int(p).bit_length() for p in special47]
-            extras["matmul_d128_fp64_specials"] = mm
+            extras["matmul_d128_l4_fp64_specials"] = mm
         except Exception as exc:
-            extras["matmul_d128_fp64_specials"] = {"error": str(exc)[:200]}
+            extras["matmul_d128_l4_fp64_specials"] = {"error": str(exc)[:200]}
         torch.cuda.empty_cache()
         try:
             extras.update(config5_stacked_bench(torch, chain, special))
@@ -724,10 +879,16 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        samples = 4
-        v, kind, dt = cpu_reference_ks(samples, os.cpu_count() or 1)
-        cpu = {"value": v, "unit": "KS/s", "cores": os.cpu_count(), "kind": kind,
-               "sample": f"{samples} single-rotation key switches of 1 ciphertext ({dt:.1f} s)"}
+        threads = os.cpu_count() or 1
+        v, kind, dt = cpu_reference_ks(threads, threads)
+        cpu = {"value": v, "unit": "KS/s", "cores": threads, "kind": kind, "cpu_model": cpu_model(),
+               "sample": f"one batch of {threads} single-rotation key switches, one ciphertext per host thread "
+                         f"({dt:.1f} s)"}
+        if not args.no_extras:
+            try:
+                cpu["matvec"] = cpu_reference_matvec(threads)
+            except Exception as exc:
+                cpu["matvec"] = {"error": str(exc)[:200]}
 
     if rank == 0:
         line = {
@@ -739,7 +900,8 @@ def main():
                        "N": N, "chain_primes": nq, "special_primes": K, "alpha": ALPHA,
                        "batch_per_gpu": BATCH, "parallelism": f"replicas x{world}",
                        "l2": "inputs larger than L2 (6.4 GB of ciphertexts per step)"},
-            "roofline": roofline, "roofline_fp64": roofline_fp64, "roofline_bsgs_mac": roofline_mac, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "roofline_step": roofline_step, "step_breakdown": breakdown,
+            "roofline_bsgs_mac": roofline_mac, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks, "extras": extras,
         }
