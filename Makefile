@@ -14,7 +14,7 @@ HOST_DIR  := $(PKG)/csrc/host
 CU_SRCS   := $(CU_DIR)/hx_ntt.cu $(CU_DIR)/hx_ops.cu $(CU_DIR)/hx_bsgs.cu $(CU_DIR)/hx_encode.cu
 CU_HDRS   := $(wildcard $(CU_DIR)/*.cuh) $(CU_DIR)/hx_internal.h include/hx_b200.h
 HOST_SRCS := $(HOST_DIR)/params.cpp $(HOST_DIR)/encoder.cpp $(HOST_DIR)/gpu_backend.cpp \
-             $(HOST_DIR)/packing.cpp $(HOST_DIR)/linalg.cpp $(HOST_DIR)/helix_c.cpp
+             $(HOST_DIR)/packing.cpp $(HOST_DIR)/linalg.cpp $(HOST_DIR)/helix_c.cpp $(HOST_DIR)/lattice.cpp
 HOST_HDRS := $(wildcard include/helix/*.hpp) include/helix_c.h include/hx_b200.h
 BUILD     := build
 CU_OBJS   := $(patsubst $(CU_DIR)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
@@ -23,8 +23,8 @@ LIB       := $(PKG)/libhx_b200.so
 HLIB      := $(PKG)/libhelix_b200.so
 TESTBIN   := $(BUILD)/test_linalg_clear
 
-.PHONY: all lib host oracle ref testbin clean
-all: lib host oracle testbin
+.PHONY: all lib host oracle ref testbin testgpu clean
+all: lib host oracle testbin testgpu
 
 lib: $(LIB)
 host: $(HLIB)
@@ -54,6 +54,17 @@ $(TESTBIN): tests/cpp/test_linalg_clear.cpp oracle/clear_backend.cpp oracle/clea
 	  $(HOST_DIR)/params.cpp $(HOST_DIR)/linalg.cpp -o $@
 
 testbin: $(TESTBIN)
+
+# C++ reference-style caller linked with the B200 library (run on the GPU by
+# tests/test_gpu_cpp_api.py); cross-compiles here, needs a B200 to run
+GPUTEST   := $(BUILD)/test_gpu_api
+$(GPUTEST): tests/cpp/test_gpu_api.cpp $(HLIB) $(HOST_HDRS)
+	@mkdir -p $(BUILD)
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -I$(CUDA_HOME)/include -I$(JSON_DIR) tests/cpp/test_gpu_api.cpp \
+	  -o $@ -L$(PKG) -lhelix_b200 -lhx_b200 -L$(CUDA_HOME)/lib64 -lcudart \
+	  -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,$(CUDA_HOME)/lib64
+
+testgpu: $(GPUTEST)
 
 oracle:
 	$(MAKE) -C oracle all

@@ -16,12 +16,22 @@
 #include <vector>
 
 #include "helix/params.hpp"
+#include "helix/rns_poly.hpp"
 
 namespace helix {
 
 class CkksEncoder {
  public:
   explicit CkksEncoder(const CkksParams& params);
+  // the reference's constructor (encoder.hpp:22): encode() then returns RNS
+  // limbs lifted on the context's device (LatticeContext::from_i64)
+  explicit CkksEncoder(const LatticeContext& ctx);
+
+  // the reference's encode / decode (encoder.cpp:97-159): coefficient-domain
+  // RnsPoly over q_0..q_level; decode needs a coefficient-domain poly without
+  // the special limb (std::invalid_argument otherwise)
+  RnsPoly encode(std::span<const double> m, int level, double scale) const;
+  std::vector<double> decode(const RnsPoly& pt, double scale) const;
 
   // round(scale * inverse-embedding(m)), m zero-padded to n slots.
   // std::invalid_argument: |m| > n, scale <= 0, level out of range;
@@ -59,6 +69,7 @@ class CkksEncoder {
   std::vector<std::complex<double>> embed(std::span<const double> m) const;
 
   CkksParams params_;
+  const LatticeContext* ctx_ = nullptr;
   std::size_t n_, n_slots_;
   int log_n_ = 0;
   std::vector<std::size_t> slot_to_eval_;

@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "helix/modmath.hpp"
 #include "helix/scale.hpp"
 
 namespace helix {
@@ -53,10 +54,6 @@ struct CkksParams {
   static CkksParams config2(std::uint64_t ring_degree = 1ull << 16, int chain_primes = 24);
 };
 
-// first `count` primes p = 1 (mod two_n) at or above `start`, skipping `exclude`
-std::vector<std::uint64_t> find_ntt_primes(std::uint64_t start, std::size_t count,
-                                           std::uint64_t two_n,
-                                           const std::vector<std::uint64_t>& exclude = {});
-bool is_prime_u64(std::uint64_t n);
+// find_ntt_primes / is_prime_u64: helix/modmath.hpp (as in the reference)
 
 }  // namespace helix
