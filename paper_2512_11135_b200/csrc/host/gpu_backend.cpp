@@ -797,6 +797,43 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       bool uniform = true;
       const long long bstride = T > 1 ? (long long)(baby_ptr[1] - baby_ptr[0]) : 0;
       for (int t = 1; t < T && uniform; ++t) uniform = (long long)(baby_ptr[t] - baby_ptr[t - 1]) == bstride;
+      // runs of consecutive groups whose n1 diagonals are all live and contiguous
+      // (mostly-dense matrices) take the streaming dense MAC; the rest the index list
+      const auto dense_at = [&](int j) {
+        if (gptr[j + 1] - gptr[j] != n1) return false;
+        for (int k = 1; k < n1; ++k)
+          if (dp[gptr[j] + k] != dp[gptr[j]] + (std::size_t)k * ptw) return false;
+        return true;
+      };
+      std::vector<int> sgptr(n2 + 1, 0), sks;
+      std::vector<const u64*> sdp;
+      for (int j = 0; j < n2;) {
+        if (dense_at(j)) {
+          int j1 = j + 1;
+          while (j1 < n2 && dense_at(j1) && dp[gptr[j1]] == dp[gptr[j1 - 1]] + (std::size_t)n1 * ptw) ++j1;
+          const std::size_t off = (std::size_t)j * jstride + (std::size_t)b * ctw;
+          if (uniform) {
+            mac_chunked(ctx_, inner->ptr, inner_polys, off, (long long)jstride, (long long)(blocks * ctw), baby_ptr[0],
+                        bstride, ctw, dp[gptr[j]], ptw, nqv, n1, j1 - j, n1, T);
+          } else {
+            for (int t = 0; t < T; ++t)
+              mac_chunked(ctx_, inner->ptr, inner_polys, off + (std::size_t)t * blocks * ctw, (long long)jstride, 0,
+                          baby_ptr[t], 0, ctw, dp[gptr[j]], ptw, nqv, n1, j1 - j, n1, 1);
+          }
+          for (int jj = j; jj < j1; ++jj) sgptr[jj + 1] = (int)sks.size();
+          j = j1;
+          continue;
+        }
+        for (int e = gptr[j]; e < gptr[j + 1]; ++e) {
+          sks.push_back(ks[e]);
+          sdp.push_back(dp[e]);
+        }
+        sgptr[j + 1] = (int)sks.size();
+        ++j;
+      }
+      gptr.swap(sgptr);
+      ks.swap(sks);
+      dp.swap(sdp);
       if (!ks.empty()) {
         if (uniform) {
           ck(hx_bsgs_mac_sparse(ctx_, inner->ptr + (std::size_t)b * ctw, (long long)jstride, (long long)(blocks * ctw),
