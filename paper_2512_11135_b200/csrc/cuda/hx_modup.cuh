@@ -3,7 +3,8 @@
 //
 // Replaces, for every digit d of c1 (coefficient domain after the INTT),
 //   bconv -> [P_d]-basis limb j (coefficient domain)      (FastBConv, non-centred:
-//            the hybrid ModUp of the reference's keyswitch, rns_poly.cpp:182-216)
+//            the hybrid ModUp of the SPEC key switch, SPEC.md:193-201 / :229 --
+//            the reference has no ModUp code; K = 1 lifts per limb, rns_poly.cpp:218-227)
 //   NTT COL pass on limb j                                 (ntt.cpp:57-74, first stages)
 // with one kernel: a CTA owns one COL tile (2^OB adjacent columns x 2^S rows)
 // of one digit of one ciphertext.  It loads the digit's alpha source limbs of

@@ -878,54 +878,68 @@ void pipelined_host(hx_ctx* c, int batch, std::vector<const uint64_t*> in_host,
   constexpr int NS = 3;
   const int chunk = std::max(1, std::min(batch, chunk_env > 0 ? chunk_env : 8));
   const int nchunks = (batch + chunk - 1) / chunk;
-  cudaStream_t h = nullptr, d = nullptr;
-  cuda_ok(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking), "stream");
-  cuda_ok(cudaStreamCreateWithFlags(&d, cudaStreamNonBlocking), "stream");
-  cudaEvent_t ev_in[NS], ev_cmp[NS], ev_out[NS];
+  // streams, events and the arena slots live in one guard: on every exit path
+  // (including a throw from `compute` after copies were queued) all three
+  // streams are drained BEFORE the slots return to the arena and the streams /
+  // events are destroyed, so no in-flight copy can land in reused memory
+  struct Pipe {
+    hx_ctx* c;
+    cudaStream_t s, h = nullptr, d = nullptr;
+    cudaEvent_t ev_in[NS] = {}, ev_cmp[NS] = {}, ev_out[NS] = {};
+    std::vector<std::unique_ptr<DBuf>> slots;
+    explicit Pipe(hx_ctx* c_, cudaStream_t s_) : c(c_), s(s_) {}
+    ~Pipe() {
+      if (h) cudaStreamSynchronize(h);
+      if (d) cudaStreamSynchronize(d);
+      cudaStreamSynchronize(s);
+      while (!slots.empty()) slots.pop_back();
+      for (int k = 0; k < NS; ++k) {
+        if (ev_in[k]) cudaEventDestroy(ev_in[k]);
+        if (ev_cmp[k]) cudaEventDestroy(ev_cmp[k]);
+        if (ev_out[k]) cudaEventDestroy(ev_out[k]);
+      }
+      if (h) cudaStreamDestroy(h);
+      if (d) cudaStreamDestroy(d);
+    }
+  } P(c, s);
+  cuda_ok(cudaStreamCreateWithFlags(&P.h, cudaStreamNonBlocking), "stream");
+  cuda_ok(cudaStreamCreateWithFlags(&P.d, cudaStreamNonBlocking), "stream");
   for (int k = 0; k < NS; ++k) {
-    cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_cmp[k], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming);
+    cuda_ok(cudaEventCreateWithFlags(&P.ev_in[k], cudaEventDisableTiming), "event");
+    cuda_ok(cudaEventCreateWithFlags(&P.ev_cmp[k], cudaEventDisableTiming), "event");
+    cuda_ok(cudaEventCreateWithFlags(&P.ev_out[k], cudaEventDisableTiming), "event");
   }
-  // chunk slots from the context arena (released in reverse order)
-  std::vector<std::unique_ptr<DBuf>> slots;
+  cudaStream_t h = P.h, d = P.d;
+  // chunk slots from the context arena (released in reverse order by the guard)
   std::vector<u64*> din[NS];
   u64* dout[NS] = {};
   for (int k = 0; k < NS && k < nchunks; ++k) {
     for (long long w : in_words) {
-      slots.push_back(std::make_unique<DBuf>((size_t)w * chunk, s, c));
-      din[k].push_back(slots.back()->p);
+      P.slots.push_back(std::make_unique<DBuf>((size_t)w * chunk, s, c));
+      din[k].push_back(P.slots.back()->p);
     }
-    slots.push_back(std::make_unique<DBuf>((size_t)out_words * chunk, s, c));
-    dout[k] = slots.back()->p;
+    P.slots.push_back(std::make_unique<DBuf>((size_t)out_words * chunk, s, c));
+    dout[k] = P.slots.back()->p;
   }
   cuda_ok(cudaStreamSynchronize(s), "sync");
   for (int i = 0; i < nchunks; ++i) {
     const int k = i % NS, b0 = i * chunk, n = std::min(chunk, batch - b0);
-    if (i >= NS) cuda_ok(cudaStreamWaitEvent(h, ev_cmp[k], 0), "wait");  // input slot consumed
+    if (i >= NS) cuda_ok(cudaStreamWaitEvent(h, P.ev_cmp[k], 0), "wait");  // input slot consumed
     for (std::size_t a = 0; a < in_host.size(); ++a)
       cuda_ok(cudaMemcpyAsync(din[k][a], in_host[a] + (long long)b0 * in_words[a], (size_t)n * in_words[a] * 8,
                               cudaMemcpyHostToDevice, h), "h2d");
-    cudaEventRecord(ev_in[k], h);
-    cuda_ok(cudaStreamWaitEvent(s, ev_in[k], 0), "wait");
-    if (i >= NS) cuda_ok(cudaStreamWaitEvent(s, ev_out[k], 0), "wait");  // output slot drained
+    cuda_ok(cudaEventRecord(P.ev_in[k], h), "event record");
+    cuda_ok(cudaStreamWaitEvent(s, P.ev_in[k], 0), "wait");
+    if (i >= NS) cuda_ok(cudaStreamWaitEvent(s, P.ev_out[k], 0), "wait");  // output slot drained
     compute(dout[k], din[k], n, s);
-    cudaEventRecord(ev_cmp[k], s);
-    cuda_ok(cudaStreamWaitEvent(d, ev_cmp[k], 0), "wait");
+    cuda_ok(cudaEventRecord(P.ev_cmp[k], s), "event record");
+    cuda_ok(cudaStreamWaitEvent(d, P.ev_cmp[k], 0), "wait");
     cuda_ok(cudaMemcpyAsync(out_host + (long long)b0 * out_words, dout[k], (size_t)n * out_words * 8,
                             cudaMemcpyDeviceToHost, d), "d2h");
-    cudaEventRecord(ev_out[k], d);
+    cuda_ok(cudaEventRecord(P.ev_out[k], d), "event record");
   }
   cuda_ok(cudaStreamSynchronize(d), "sync");
   cuda_ok(cudaStreamSynchronize(s), "sync");
-  for (int k = 0; k < NS; ++k) {
-    cudaEventDestroy(ev_in[k]);
-    cudaEventDestroy(ev_cmp[k]);
-    cudaEventDestroy(ev_out[k]);
-  }
-  cudaStreamDestroy(h);
-  cudaStreamDestroy(d);
-  while (!slots.empty()) slots.pop_back();
 }
 
 }  // namespace
@@ -1999,6 +2013,8 @@ int hx_rotate_host(hx_ctx* c, uint64_t* out_host, const uint64_t* in_host, const
     check_ctx(c);
     HX_COUNT(batch);
     check_nq(c, n_q);
+    HX_REQUIRE((g & 1) && g < 2 * (u64)c->N(), "galois element");  // before any copy is queued
+    HX_REQUIRE(key != nullptr && in_host != nullptr && out_host != nullptr, "null buffer");
     const long long ct = 2ll * n_q * c->N();
     pipelined_host(c, batch, {in_host}, {ct}, out_host, ct, S(s),
                    [&](u64* out, const std::vector<u64*>& in, int n, cudaStream_t st) {
@@ -2014,6 +2030,7 @@ int hx_mul_relin_host(hx_ctx* c, uint64_t* out_host, const uint64_t* a_host,
     check_ctx(c);
     HX_COUNT(batch);
     check_nq(c, n_q);
+    HX_REQUIRE(rlk != nullptr && a_host != nullptr && b_host != nullptr && out_host != nullptr, "null buffer");
     const long long ct = 2ll * n_q * c->N();
     pipelined_host(c, batch, {a_host, b_host}, {ct, ct}, out_host, ct, S(s),
                    [&](u64* out, const std::vector<u64*>& in, int n, cudaStream_t st) {
