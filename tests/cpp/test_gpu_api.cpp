@@ -199,7 +199,7 @@ static void test_backend_matvec_and_matmul() {
   for (int i = 0; i < 4; ++i) CHECK(std::abs(cv[i] - exp[i]) < 1e-3, "matmul known answer");
   CHECK(mrep.rotations == 6 && mrep.levels_consumed == 2, "matmul counts (SPEC.md:403)");
   // errors map to the reference's exception types (backend.hpp:66-81)
-  CHECK(throws<MissingRotationKeyError>([&] { be.rotate(ct, 7); }), "missing key");
+  CHECK(throws<MissingRotationKeyError>([&] { be.rotate(ct, 9); }), "missing key (9 is in neither key set)");
   CHECK(throws<LevelMismatchError>([&] { be.add(ct, be.mod_down(ct, 0)); }), "level mismatch");
 }
 
