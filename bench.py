@@ -42,7 +42,7 @@ DOMINANT = "modup_col_kernel"
 F64_LANES_PER_CLK = 62.6  # DFMA lanes / clk / SM, measured on the box (tools/microbench/pipes.cu)
 MODUP_CONV_OPS = 21       # FP64 ops per converted word (3 sources: split products + exact reduction)
 COL_PASS_OPS = 32         # 8 of the 16 radix-2 stages, 4 FP64 ops per element per stage
-DOM_TRAFFIC_NCU = None    # set from profiles/ when an ncu --set full capture of this build exists
+DOM_TRAFFIC_NCU = 28990165000  # dram rd + wr of one modup_col launch, profiles/r02_ncu_full_ks.md
 
 
 def primes(fp64_specials: bool = False):

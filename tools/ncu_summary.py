@@ -46,6 +46,7 @@ METRICS = [
     ("dram__bytes_read.sum", "dram rd"),
     ("dram__bytes_write.sum", "dram wr"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram %"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "fp64 pipe %"),
     ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", "fmaheavy %"),
     ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "alu %"),
     ("sm__issue_active.avg.pct_of_peak_sustained_elapsed", "issue %"),
@@ -54,6 +55,8 @@ METRICS = [
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem conflicts"),
     ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math"),
     ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall lsb"),
+    ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall wait"),
+    ("smsp__average_warps_issue_stalled_dispatch_stall_per_issue_active.ratio", "stall dispatch"),
 ]
 
 
