@@ -212,6 +212,25 @@ int hx_bsgs_mac_sparse(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, lo
                        const uint64_t* baby, long long baby_tstride, const int* group_ptr, const int* ks,
                        const uint64_t* const* diags, int n1, int n2, int n_q, int tokens, void* stream);
 
+/* Tensor-core BSGS MAC (tcgen05.mma kind::i8 on byte-sliced words, TMEM
+ * accumulators, bulk-copy-streamed diagonals; hx_bsgs_tc.cu).  The diagonals of
+ * up to 128 rows r = b * n2 + j (row block b, giant step j) are packed once into
+ * a device buffer of hx_bsgs_tc_bytes bytes: limbs with q < 2^40 as 5-byte
+ * sliced tcgen05 operand tiles (37.5 % fewer bytes than u64 words), wider limbs
+ * (q_0) as u64 copies.  diag_ptrs: host array [rows * n1] of DEVICE addresses of
+ * [>= n_q][N] plaintext words (NULL = zero diagonal).  n1 % 8 == 0, n1 <= 64,
+ * N >= 128.  Returns -1 on a bad shape. */
+long long hx_bsgs_tc_bytes(hx_ctx* ctx, int rows, int n1, int n_q);
+int hx_bsgs_tc_pack(hx_ctx* ctx, void* packed, const uint64_t* const* diag_ptrs, int rows, int n1, int n_q,
+                    void* stream);
+/* inner sums of all rows from one packed matrix: row (b, j) of token t at
+ * inner + j inner_jstride + b inner_bstride + t inner_tstride words ([2][n_q][N]);
+ * baby sets [n1][2][n_q][N] at baby + t baby_tstride.  Same words as
+ * hx_bsgs_mac_tokens over the unpacked diagonals. */
+int hx_bsgs_mac_tc(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, long long inner_bstride,
+                   long long inner_tstride, const uint64_t* baby, long long baby_tstride, const void* packed,
+                   int blocks, int n2, int n1, int n_q, int tokens, void* stream);
+
 /* ---- keys / encryption ------------------------ */
 /* Device samplers (counter-based: splitmix64 of (seed, index)), used for key
  * material so that key generation needs no host RNG stream or H2D copy:

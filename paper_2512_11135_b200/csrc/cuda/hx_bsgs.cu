@@ -312,8 +312,8 @@ void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s, const int* d
     configured = true;
   }
   const int kpt = A.n1 / kMacWarps;
-  const bool f64_ok = n_f64 > 0 && N >= 32 && A.n1 % kMacWarps == 0 && (kpt == 1 || kpt == 2 || kpt == 4 || kpt == 8);
-  if (f64_ok) {
+  const bool ksplit = N >= 32 && A.n1 % kMacWarps == 0 && (kpt == 1 || kpt == 2 || kpt == 4 || kpt == 8);
+  if (ksplit && n_f64 > 0) {
     dim3 grid((unsigned)(N / 32 * A.tokens), (unsigned)n_f64);
     switch (kpt) {
       case 1: bsgs_mac_f64_kernel<1><<<grid, 32 * kMacWarps, 0, s>>>(A, d_f64_limbs); break;
@@ -323,7 +323,7 @@ void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s, const int* d
     }
   }
   // integer k-split kernel for the wide primes
-  if (f64_ok && n_int > 0) {
+  if (ksplit && n_int > 0) {
     dim3 grid((unsigned)(N / 32 * A.tokens), (unsigned)n_int);
     switch (kpt) {
       case 1: bsgs_mac_int_kernel<1><<<grid, 32 * kMacWarps, 0, s>>>(A, d_int_limbs); break;
@@ -331,8 +331,8 @@ void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s, const int* d
       case 4: bsgs_mac_int_kernel<4><<<grid, 32 * kMacWarps, 0, s>>>(A, d_int_limbs); break;
       case 8: bsgs_mac_int_kernel<8><<<grid, 32 * kMacWarps, 0, s>>>(A, d_int_limbs); break;
     }
-    return;
   }
+  if (ksplit) return;
   // generic smem-tile kernel (n1 not a multiple of 8, tiny N): all limbs
   const int* il = nullptr;
   const int ni = A.n_q;

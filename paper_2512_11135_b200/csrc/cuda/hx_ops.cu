@@ -1779,6 +1779,159 @@ int hx_bsgs_mac_sparse(hx_ctx* c, uint64_t* inner, long long inner_jstride, long
   });
 }
 
+namespace {
+struct TcPlan {
+  int KC, RG;
+  std::vector<int> tc, wide;  // limb lists (q < 2^40: sliced operand tiles; else u64 copies)
+  size_t tc_bytes, wide_bytes;
+};
+bool tc_shape_ok(const hx_ctx* c, int rows, int n1, int n_q) {
+  return c && rows >= 1 && rows <= 128 && n1 >= 8 && n1 <= 64 && n1 % 8 == 0 && n_q >= 1 && n_q <= c->n_chain &&
+         c->N() >= 128;
+}
+TcPlan tc_plan(const hx_ctx* c, int rows, int n1, int n_q) {
+  TcPlan P;
+  P.KC = (5 * n1 + 31) / 32 * 2;
+  P.RG = (rows + 7) / 8;
+  for (int i = 0; i < n_q; ++i) (c->primes[i] < (1ull << 40) ? P.tc : P.wide).push_back(i);
+  P.tc_bytes = P.tc.size() * (size_t)c->N() * P.RG * P.KC * 128;
+  P.wide_bytes = P.wide.size() * (size_t)rows * n1 * c->N() * 8;
+  return P;
+}
+int sm_count() {
+  static const int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+}  // namespace
+
+long long hx_bsgs_tc_bytes(hx_ctx* c, int rows, int n1, int n_q) {
+  if (!tc_shape_ok(c, rows, n1, n_q)) return -1;
+  const TcPlan P = tc_plan(c, rows, n1, n_q);
+  return (long long)(P.tc_bytes + P.wide_bytes);
+}
+
+int hx_bsgs_tc_pack(hx_ctx* c, void* packed, const uint64_t* const* diag_ptrs, int rows, int n1, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_REQUIRE(tc_shape_ok(c, rows, n1, n_q), "bsgs_tc_pack: bad shape (rows <= 128, n1 % 8 == 0, n1 <= 64, N >= 128)");
+    HX_REQUIRE(packed && diag_ptrs, "bsgs_tc_pack: null buffer");
+    const TcPlan P = tc_plan(c, rows, n1, n_q);
+    const size_t np = (size_t)rows * n1;
+    const size_t pb = np * sizeof(void*);
+    std::vector<char> host(pb + (P.tc.size() + P.wide.size()) * sizeof(int));
+    std::memcpy(host.data(), diag_ptrs, pb);
+    int* hl = reinterpret_cast<int*>(host.data() + pb);
+    std::copy(P.tc.begin(), P.tc.end(), hl);
+    std::copy(P.wide.begin(), P.wide.end(), hl + P.tc.size());
+    DBuf tab((host.size() + 7) / 8, S(s), c);
+    cuda_ok(cudaMemcpyAsync(tab.p, host.data(), host.size(), cudaMemcpyHostToDevice, S(s)), "h2d");
+    const int* dl = reinterpret_cast<const int*>(reinterpret_cast<const char*>(tab.p) + pb);
+    hx::launch_tc_pack(static_cast<unsigned char*>(packed), reinterpret_cast<const u64* const*>(tab.p), dl,
+                       (int)P.tc.size(), dl + P.tc.size(), (int)P.wide.size(), rows, n1, P.KC, P.RG, c->logn,
+                       P.tc_bytes, S(s));
+    launched(c, "tc_pack_kernel", (P.tc.empty() ? 0 : 1) + (P.wide.empty() ? 0 : 1));
+  });
+}
+
+int hx_bsgs_mac_tc(hx_ctx* c, uint64_t* inner, long long inner_jstride, long long inner_bstride,
+                   long long inner_tstride, const uint64_t* baby, long long baby_tstride, const void* packed,
+                   int blocks, int n2, int n1, int n_q, int tokens, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    HX_REQUIRE(blocks >= 1 && n2 >= 1 && tokens >= 1, "bsgs_mac_tc: bad shape");
+    const int rows = blocks * n2;
+    HX_REQUIRE(tc_shape_ok(c, rows, n1, n_q), "bsgs_mac_tc: bad shape (rows <= 128, n1 % 8 == 0, n1 <= 64)");
+    HX_REQUIRE(inner && baby && packed, "bsgs_mac_tc: null buffer");
+    HX_REQUIRE((reinterpret_cast<uintptr_t>(inner) & 31) == 0 && inner_jstride % 4 == 0 && inner_bstride % 4 == 0 &&
+                   inner_tstride % 4 == 0,
+               "bsgs_mac_tc: inner sums must be 32-byte aligned (whole-sector stores)");
+    const TcPlan P = tc_plan(c, rows, n1, n_q);
+    const long long N = c->N();
+    // device table: row offsets [rows] | TC limbs | wide limbs | Barrett constants [n_tc][2]
+    const size_t lb = (size_t)rows * 8 + (P.tc.size() + P.wide.size()) * sizeof(int);
+    std::vector<char> host(lb + P.tc.size() * 2 * sizeof(hx::u32));
+    hx::u32* mu = reinterpret_cast<hx::u32*>(host.data() + lb);
+    for (size_t e = 0; e < P.tc.size(); ++e) {
+      const u64 q = c->primes[P.tc[e]];
+      mu[2 * e] = (hx::u32)((((unsigned __int128)1) << 56) / q);
+      mu[2 * e + 1] = (hx::u32)((1ull << 48) / q);
+    }
+    long long* ro = reinterpret_cast<long long*>(host.data());
+    for (int b = 0; b < blocks; ++b)
+      for (int j = 0; j < n2; ++j) ro[b * n2 + j] = j * inner_jstride + b * inner_bstride;
+    int* hl = reinterpret_cast<int*>(host.data() + (size_t)rows * 8);
+    std::copy(P.tc.begin(), P.tc.end(), hl);
+    std::copy(P.wide.begin(), P.wide.end(), hl + P.tc.size());
+    DBuf tab((host.size() + 7) / 8, S(s), c);
+    cuda_ok(cudaMemcpyAsync(tab.p, host.data(), host.size(), cudaMemcpyHostToDevice, S(s)), "h2d");
+    const int* dl = reinterpret_cast<const int*>(reinterpret_cast<const char*>(tab.p) + (size_t)rows * 8);
+    const long long L = (long long)n_q * N;
+    int launches = 0;
+    if (!P.tc.empty()) {
+      hx::TcArgs A;
+      A.row_off = reinterpret_cast<const long long*>(tab.p);
+      A.L = L;
+      A.packed = static_cast<const unsigned char*>(packed);
+      A.limbs = dl;
+      A.pc = c->d_pc;
+      A.mu = reinterpret_cast<const hx::u32*>(reinterpret_cast<const char*>(tab.p) + lb);
+      A.rows = rows;
+      A.n1 = n1;
+      A.n_tc = (int)P.tc.size();
+      A.logn = c->logn;
+      A.KC = P.KC;
+      A.RG = P.RG;
+      A.tstride = inner_tstride;
+      DBuf bt((size_t)std::min(tokens, hx::kTcMaxTokens) * n1 * 2 * P.tc.size() * N, S(s), c);
+      for (int t0 = 0; t0 < tokens;) {
+        int T = hx::kTcMaxTokens;
+        while (T > tokens - t0) T /= 2;
+        hx::launch_tc_baby(bt.p, (const u64*)baby + t0 * baby_tstride, baby_tstride, L, dl, (int)P.tc.size(), n1, T,
+                           c->logn, S(s));
+        A.inner = (u64*)inner + t0 * inner_tstride;
+        A.baby = bt.p;
+        hx::KTimer kt(c, "bsgs_mac_tc_kernel", S(s));
+        hx::launch_bsgs_mac_tc(A, T, sm_count(), S(s));
+        launches += 2;
+        t0 += T;
+      }
+    }
+    // limbs with q >= 2^40: the integer k-split MAC over the u64 copies
+    // ([w][r][k][N]; the kernel indexes diags + i N + (j n1 + k) N)
+    const u64* wide = reinterpret_cast<const u64*>(static_cast<const char*>(packed) + P.tc_bytes);
+    for (size_t w = 0; w < P.wide.size(); ++w) {
+      const int i = P.wide[w];
+      for (int b = 0; b < blocks; ++b) {
+        hx::MacArgs A;
+        A.inner = (u64*)inner + b * inner_bstride;
+        A.baby = (const u64*)baby;
+        A.diags = wide + ((long long)w * rows + (long long)b * n2) * n1 * N - (long long)i * N;
+        A.pc = c->d_pc;
+        A.n1 = n1;
+        A.n2 = n2;
+        A.n_q = n_q;
+        A.logn = c->logn;
+        A.diag_stride = N;
+        A.out_jstride = inner_jstride;
+        A.limbs = nullptr;
+        A.tokens = tokens;
+        A.baby_tstride = baby_tstride;
+        A.inner_tstride = inner_tstride;
+        A.diag_jstride = n1;
+        hx::launch_bsgs_mac(A, N, S(s), nullptr, 0, dl + P.tc.size() + w, 1);
+        ++launches;
+      }
+    }
+    launched(c, "bsgs_mac_tc_kernel", launches);
+  });
+}
+
 int hx_bsgs_mac_ex(hx_ctx* c, uint64_t* inner, long long inner_jstride, const uint64_t* baby,
                    const uint64_t* diags, int diag_limbs, int n1, int n2, int n_q, void* s) {
   return hx_bsgs_mac_tokens(c, inner, inner_jstride, 0, baby, 0, diags, diag_limbs, n1, n2, n_q, 1, 0, s);

@@ -68,4 +68,26 @@ void launch_sum(const SumArgs& A, int polys, long long N, cudaStream_t s);
 void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s, const int* d_f64_limbs, int n_f64,
                      const int* d_int_limbs, int n_int);
 
+// ------------------------------------------------- tensor-core BSGS MAC
+// (hx_bsgs_tc.cu): the TC-class limbs (q < 2^40) of up to 128 rows r = (block,
+// giant step) per launch, T in {1, 2, 4, 8} tokens
+constexpr int kTcMaxTokens = 8;
+struct TcArgs {
+  u64* inner;
+  const long long* row_off;  // [R] word offset of row r's inner sum (j jstride + b bstride)
+  long long tstride, L;      // token stride of the inner sums; words per poly (n_q N)
+  const u64* baby;           // transposed baby words [n_tc][N][n1][2][T] (launch_tc_baby)
+  const unsigned char* packed;  // TC section [n_tc][N][RG][KC][128]
+  const int* limbs;             // TC-class limb list (li -> chain limb i)
+  const PrimeConst* pc;
+  const u32* mu;  // [n_tc][2]: floor(2^56 / q), floor(2^48 / q) (Barrett estimates)
+  int rows, n1, n_tc, logn, KC, RG;
+};
+int tc_max_tokens();
+void launch_tc_baby(u64* out, const u64* baby, long long btstride, long long L, const int* limbs, int n_tc, int n1,
+                    int T, int logn, cudaStream_t s);
+void launch_bsgs_mac_tc(const TcArgs& A, int tokens, int sms, cudaStream_t s);
+void launch_tc_pack(unsigned char* dst, const u64* const* dptr, const int* tc_limbs, int n_tc, const int* wide_limbs,
+                    int n_wide, int rows, int n1, int KC, int RG, int logn, size_t tc_bytes, cudaStream_t s);
+
 }  // namespace hx

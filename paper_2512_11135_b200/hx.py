@@ -250,6 +250,45 @@ class Context:
         _check(self.L.hx_bsgs_mac(self.h, _p(inner), _p(baby), _p(diags), diag_limbs, n1, n2, n_q,
                                   _stream(stream)), "hx_bsgs_mac")
 
+    def bsgs_mac_tokens(self, inner, inner_jstride, inner_tstride, baby, baby_tstride, diags, diag_limbs, n1, n2,
+                        n_q, tokens=1, diag_jstride=0, stream=None):
+        L = self.L
+        L.hx_bsgs_mac_tokens.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.c_longlong, C.c_void_p,
+                                         C.c_longlong, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.c_int, C.c_void_p]
+        L.hx_bsgs_mac_tokens.restype = C.c_int
+        _check(L.hx_bsgs_mac_tokens(self.h, _p(inner), inner_jstride, inner_tstride, _p(baby), baby_tstride,
+                                    _p(diags), diag_limbs, n1, n2, n_q, tokens, diag_jstride, _stream(stream)),
+               "hx_bsgs_mac_tokens")
+
+    def bsgs_tc_pack(self, diag_ptrs, rows, n1, n_q, stream=None):
+        """packed tensor-core operand buffer (uint8 tensor) of rows x n1 diagonals;
+        diag_ptrs: row-major [rows * n1] device addresses (None = zero diagonal)"""
+        import torch
+
+        L = self.L
+        L.hx_bsgs_tc_bytes.restype = C.c_longlong
+        L.hx_bsgs_tc_bytes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+        nb = L.hx_bsgs_tc_bytes(self.h, rows, n1, n_q)
+        if nb < 0:
+            raise HxError(f"hx_bsgs_tc_bytes: bad shape rows={rows} n1={n1} n_q={n_q}")
+        buf = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        dp = (C.c_void_p * len(diag_ptrs))(*diag_ptrs)
+        L.hx_bsgs_tc_pack.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
+                                      C.c_void_p]
+        L.hx_bsgs_tc_pack.restype = C.c_int
+        _check(L.hx_bsgs_tc_pack(self.h, _p(buf), dp, rows, n1, n_q, _stream(stream)), "hx_bsgs_tc_pack")
+        return buf
+
+    def bsgs_mac_tc(self, inner, inner_jstride, inner_bstride, inner_tstride, baby, baby_tstride, packed, blocks, n2,
+                    n1, n_q, tokens=1, stream=None):
+        L = self.L
+        L.hx_bsgs_mac_tc.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.c_longlong, C.c_longlong, C.c_void_p,
+                                     C.c_longlong, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.hx_bsgs_mac_tc.restype = C.c_int
+        _check(L.hx_bsgs_mac_tc(self.h, _p(inner), inner_jstride, inner_bstride, inner_tstride, _p(baby), baby_tstride,
+                                _p(packed), blocks, n2, n1, n_q, tokens, _stream(stream)), "hx_bsgs_mac_tc")
+
     def bsgs_mac_sparse(self, inner, inner_jstride, baby, group_ptr, ks, diag_ptrs, n1, n2, n_q, tokens=1,
                         inner_tstride=0, baby_tstride=0, stream=None):
         """index-list MAC: group j = entries [group_ptr[j], group_ptr[j+1]), entry e

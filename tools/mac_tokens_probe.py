@@ -28,7 +28,8 @@ def main():
     s = torch.cuda.current_stream().cuda_stream
     res = {}
     ctw = 2 * nq * N
-    for T in (1, 2, 4, 8, 16):
+    Ts = [int(a) for a in sys.argv[1:]] or [1, 2, 4, 8, 16]
+    for T in Ts:
         baby = rand_limbs(torch, gen, chain, (T, n1, 2), "cuda")
         inner = torch.empty((T, n2, 2, nq, N), dtype=torch.int64, device="cuda")
 
@@ -36,7 +37,8 @@ def main():
             assert L.hx_bsgs_mac_tokens(ctx.h, inner.data_ptr(), ctw, n2 * ctw, baby.data_ptr(), n1 * ctw,
                                         diags.data_ptr(), nq, n1, n2, nq, T, 0, s) == 0
 
-        secs = time_loop(torch, run, 5, 2, s) / 5
+        reps = int(os.environ.get("PROBE_REPS", "5"))
+        secs = time_loop(torch, run, reps, 2, s) / reps
         res[f"T{T}"] = {"ms": 1e3 * secs, "ms_per_token": 1e3 * secs / T,
                         "diag_GBps": n1 * n2 * nq * N * 8 / secs / 1e9}
         del baby, inner
