@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <span>
 #include <vector>
 
@@ -32,6 +33,12 @@ namespace helix {
 struct DeviceBuffer {
   std::uint64_t* ptr = nullptr;
   std::size_t words = 0;
+  // derived device representations of the (immutable) words, e.g. the
+  // tensor-core operand tiles of a BSGS matrix's diagonals (hx_bsgs_tc_pack),
+  // keyed by a signature of the shape and the diagonal offsets; they live
+  // and die with this buffer
+  std::mutex derived_mu;
+  std::vector<std::pair<std::uint64_t, std::shared_ptr<DeviceBuffer>>> derived;
   explicit DeviceBuffer(std::size_t words);
   ~DeviceBuffer();
   DeviceBuffer(const DeviceBuffer&) = delete;

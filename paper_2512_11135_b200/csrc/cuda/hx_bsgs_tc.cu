@@ -53,14 +53,26 @@ __device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
 __device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+__device__ __forceinline__ bool mbar_try(u64* bar, u32 parity) {
+  u32 ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// wait with a short sleep between polls: a spinning warp would take issue
+// slots from the builder / epilogue warps of its SM sub-partition
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+  if (mbar_try(bar, parity)) return;
+  u32 ns = 32;
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(ns);
+    if (ns < 256) ns *= 2;
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -145,9 +157,23 @@ constexpr int kTcMmaWarp = 1;       // one lane issues tcgen05.mma
 constexpr int kTcBuildWarp0 = 2, kTcBuildWarps = 6;   // B' tiles
 constexpr int kTcEpiWarp0 = 8, kTcEpiWarps = 8;       // TMEM -> reduce -> store (2 per TMEM sub-partition)
 constexpr int kTcWarps = kTcEpiWarp0 + kTcEpiWarps;
+
+#ifdef HX_TC_TRACE
+// per-item role timeline of CTA 0 (clock64), read by hx_tc_trace_get (trace builds only)
+__device__ unsigned long long hx_tc_trace[16][64];
+#define TC_TRACE(ev, n)                                                                        \
+  do {                                                                                         \
+    if (blockIdx.x == 0 && (n) < 64) hx_tc_trace[ev][n] = (unsigned long long)clock64();       \
+  } while (0)
+#else
+#define TC_TRACE(ev, n) \
+  do {                  \
+  } while (0)
+#endif
 constexpr int kTcThreads = 32 * kTcWarps;
 constexpr int kTcCols = 512;  // TMEM: two accumulator sets of 256 columns
-constexpr int kTcStages = 2;  // A / baby / B' ring depth
+constexpr int kTcMaxStages = 4;  // A / baby / B' ring depth: as many as fit (>= 2)
+constexpr size_t kTcSmemMax = 225 * 1024;
 
 template <int T>
 struct TcShape {
@@ -155,16 +181,19 @@ struct TcShape {
   static constexpr int NP = (NC + 15) / 16 * 16;  // MMA N (multiple of 16 for M = 128)
 };
 
-// shared-memory plan: kTcStages x (A tiles, B' tiles, baby words) + barriers
+// shared-memory plan: S stages of (A tiles, B' tiles, baby words) + barriers
 struct TcSmem {
-  size_t a, bp, bb, stage, total;
+  size_t a, bp, bb, stage;
+  int stages;
   __host__ __device__ TcSmem(int G, int NP, int KC, int T, int n1) {
     a = (size_t)G * 16 * KC * 128;
     bp = (size_t)G * (NP / 8) * KC * 128;
     bb = (size_t)G * n1 * 2 * T * 8;
     stage = a + bp + bb;
-    total = kTcStages * stage + 256;
+    stages = (int)((kTcSmemMax - 256) / stage);
+    if (stages > kTcMaxStages) stages = kTcMaxStages;
   }
+  __host__ __device__ size_t total() const { return stages * stage + 256; }
 };
 
 // TMEM columns [c0, c0 + n) of this warp's 32 lanes, n in {1, 2, 4, 8, 16, 32} chunks
@@ -185,10 +214,11 @@ __device__ __forceinline__ void tmem_ld_cols(u32 taddr, u32* v) {
 template <int T, int G>
 __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
   constexpr int NP = TcShape<T>::NP;
-  constexpr int S = kTcStages;
+
   static_assert(G * NP <= kTcCols / 2, "TMEM columns");
   extern __shared__ __align__(128) unsigned char sm[];
   const TcSmem plan(G, NP, A.KC, T, A.n1);
+  const int S = plan.stages;
   const int KB = A.KC * 128;  // bytes of one 8-row group (all K chunks)
   // stage s: A tiles [G][16 groups][KC][128] | B' tiles [G][NP/8 groups][KC][128] | baby [g][k][c][tok]
   auto sA = [&](int s) { return sm + s * plan.stage; };
@@ -254,6 +284,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
     for (long long n = 0; n < my_items; ++n) {
       const int s = (int)(n % S);
       if (n >= S) mbar_wait(&slot_free[s], (u32)((n / S - 1) & 1));
+      if (lane == 0) TC_TRACE(0, n);
       int li;
       long long t0;
       item_of(n, li, t0);
@@ -276,9 +307,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
       const int KS = A.KC / 2;  // MMA K steps of 32 bytes
       for (long long n = 0; n < my_items; ++n) {
         const int s = (int)(n % S), x = (int)(n & 1);
+        TC_TRACE(13, n);
         if (n >= 2) mbar_wait(&acc_free[x], (u32)(((n >> 1) - 1) & 1));
+        TC_TRACE(4, n);
         mbar_wait(&full_a[s], (u32)((n / S) & 1));
+        TC_TRACE(5, n);
         mbar_wait(&bp_full[s], (u32)((n / S) & 1));
+        TC_TRACE(6, n);
         tc_fence_after();
 #pragma unroll
         for (int g = 0; g < G; ++g) {
@@ -287,8 +322,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
             mma_i8(tmem + (u32)(x * (kTcCols / 2) + g * NP), umma_desc(a0 + k * 256, 128, KB),
                    umma_desc(b0 + k * 256, 128, KB), idesc, k > 0 ? 1u : 0u);
         }
+        TC_TRACE(11, n);
         mma_commit(&slot_free[s]);
         mma_commit(&acc_full[x]);
+        TC_TRACE(12, n);
       }
     }
   } else if (warp < kTcEpiWarp0) {
@@ -305,7 +342,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
       const u64 q = A.pc[i].q;
       const u32 mu48 = A.mu[2 * li + 1];
       mbar_wait(&full_b[s], (u32)((n / S) & 1));
+      if (bt == 0) TC_TRACE(1, n);
       if (n >= S) mbar_wait(&slot_free[s], (u32)((n / S - 1) & 1));
+      if (bt == 0) TC_TRACE(2, n);
       const u64* bb = sBb(s);
       for (int u = bt; u < units; u += 32 * kTcBuildWarps) {
         const int tok = u % T;
@@ -322,13 +361,20 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
         for (int a = 0; a < 5; ++a) {
           const int kp = a * n1 + 4 * kq;
           unsigned char* col = bg + (kp >> 4) * 128 + (kp & 15);
+          u32 wl[4], wh[4];
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            wl[m] = (u32)w[m];
+            wh[m] = (u32)(w[m] >> 32);
+          }
 #pragma unroll
           for (int b = 0; b < 5; ++b) {
             const int nn = (c * T + tok) * 5 + b;
-            // byte b of w[0..3] -> bytes 0..3 of one word
-            const u32 lo = __byte_perm((u32)(w[0] >> (8 * b)), (u32)(w[1] >> (8 * b)), 0x0040);
-            const u32 hi = __byte_perm((u32)(w[2] >> (8 * b)), (u32)(w[3] >> (8 * b)), 0x0040);
-            *reinterpret_cast<u32*>(col + (nn >> 3) * KB + (nn & 7) * 16) = __byte_perm(lo, hi, 0x5410);
+            // byte b of w[0..3] -> bytes 0..3 of one word (bytes 0-3 from the low halves, 4 from the high)
+            const u32 sel = b < 4 ? (u32)(b | ((4 + b) << 4)) : 0x40u;
+            const u32 p01 = __byte_perm(b < 4 ? wl[0] : wh[0], b < 4 ? wl[1] : wh[1], sel);
+            const u32 p23 = __byte_perm(b < 4 ? wl[2] : wh[2], b < 4 ? wl[3] : wh[3], sel);
+            *reinterpret_cast<u32*>(col + (nn >> 3) * KB + (nn & 7) * 16) = __byte_perm(p01, p23, 0x5410);
           }
           if (a < 4) {
 #pragma unroll
@@ -337,6 +383,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
         }
       }
       fence_async_smem();
+      if (bt == 0) TC_TRACE(3, n);
+      if (bt == 32 * kTcBuildWarps - 1) TC_TRACE(10, n);
       mbar_arrive(&bp_full[s]);
     }
   } else {
@@ -356,6 +404,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
       const u64 q = A.pc[i].q;
       const u32 mu56 = A.mu[2 * li];
       mbar_wait(&acc_full[x], (u32)((n >> 1) & 1));
+      if (ew == 0 && lane == 0) TC_TRACE(7, n);
       tc_fence_after();
       const u32 tbase = tmem + ((u32)(sp * 32) << 16) + (u32)(x * (kTcCols / 2) + c * T * 5);
       // slot of this item in its aligned group of 4 coefficients (one 32-byte
@@ -363,15 +412,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
       // sector writes cost a DRAM read-modify-write each
       const int p = (int)((t0 & 3) / G);
       const bool whole = n - p >= 0 && n - p + P - 1 < my_items;
+      const bool live = sp * 32 < A.rows;  // sub-partitions without rows only release the accumulator
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
+      for (int g = 0; g < (live ? G : 0); ++g) {
         u32 v[5 * T];
         tmem_ld_cols<5 * T>(tbase + (u32)(g * NP), v);
         tmem_wait_ld();
 #pragma unroll
         for (int tok = 0; tok < T; ++tok) {
           const u32* y = v + 5 * tok;
-          const u64 V = (u64)y[0] + ((u64)y[1] << 8) + ((u64)y[2] << 16) + ((u64)y[3] << 24) + ((u64)y[4] << 32);
+          const u64 V = (u64)y[0] + (u64)y[1] * 256u + (u64)y[2] * 65536u + (u64)y[3] * 16777216u + ((u64)y[4] << 32);
           const u64 val = barrett_small(V, 24, mu56, q);
 #pragma unroll
           for (int pp = 0; pp < P; ++pp)
@@ -379,6 +429,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
         }
       }
       tc_fence_before();
+      if (ew == 0 && lane == 0) TC_TRACE(8, n);
+      if (ew == 4 && lane == 0) TC_TRACE(14, n);
+      if (ew == 3 && lane == 0) TC_TRACE(15, n);
       mbar_arrive(&acc_free[x]);
       if (r < A.rows) {
 #pragma unroll
@@ -398,6 +451,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
           }
         }
       }
+      if (ew == 0 && lane == 0) TC_TRACE(9, n);
     }
   }
   tc_fence_before();
@@ -476,7 +530,7 @@ namespace {
 template <int T, int G>
 void launch_tc(const TcArgs& A, int sms, cudaStream_t s) {
   constexpr int NP = TcShape<T>::NP;
-  const size_t smem = TcSmem(G, NP, A.KC, T, A.n1).total;
+  const size_t smem = TcSmem(G, NP, A.KC, T, A.n1).total();
   cudaFuncSetAttribute(bsgs_mac_tc_kernel<T, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const long long items = (long long)A.n_tc * ((1ll << A.logn) / G);
   const int grid = (int)(items < sms ? items : sms);
@@ -488,7 +542,7 @@ void launch_tc(const TcArgs& A, int sms, cudaStream_t s) {
 template <int T>
 void dispatch_g(const TcArgs& A, int sms, cudaStream_t s) {
   constexpr int NP = TcShape<T>::NP;
-  auto fits = [&](int G) { return G * NP <= kTcCols / 2 && TcSmem(G, NP, A.KC, T, A.n1).total <= 200 * 1024; };
+  auto fits = [&](int G) { return G * NP <= kTcCols / 2 && TcSmem(G, NP, A.KC, T, A.n1).stages >= 3; };
   if constexpr (4 * NP <= kTcCols / 2) {
     if (fits(4)) return launch_tc<T, 4>(A, sms, s);
   }
@@ -501,6 +555,12 @@ void dispatch_g(const TcArgs& A, int sms, cudaStream_t s) {
 }  // namespace
 
 int tc_max_tokens() { return kTcMaxTokens; }
+
+#ifdef HX_TC_TRACE
+extern "C" int hx_tc_trace_get(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, hx_tc_trace, sizeof(hx_tc_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 void launch_tc_baby(u64* out, const u64* baby, long long btstride, long long L, const int* limbs, int n_tc, int n1,
                     int T, int logn, cudaStream_t s) {

@@ -682,6 +682,40 @@ static void mac_chunked(hx_ctx* ctx, std::uint64_t* inner, std::size_t inner_pol
   }
 }
 
+// Tensor-core operand tiles of the diagonals of rows r = (block b, giant
+// step j) < rows (hx_bsgs_tc_pack), made once and attached to the buffer that
+// holds the diagonals (every live diagonal must sit in `buf`).  Key: shape and
+// the offsets of all rows x n1 diagonals (-1 = absent).
+static std::shared_ptr<DeviceBuffer> tc_pack(hx_ctx* ctx, const std::shared_ptr<DeviceBuffer>& buf,
+                                             const std::vector<const u64*>& ptrs, int rows, int n1, int nqv) {
+  u64 sig = 0xcbf29ce484222325ull;
+  auto mix = [&](u64 v) {
+    sig ^= v;
+    sig *= 0x100000001b3ull;
+  };
+  mix((u64)rows);
+  mix((u64)n1);
+  mix((u64)nqv);
+  for (const u64* q : ptrs) mix(q ? (u64)(q - buf->ptr) : ~0ull);
+  std::lock_guard<std::mutex> g(buf->derived_mu);
+  for (const auto& e : buf->derived)
+    if (e.first == sig) return e.second;
+  const long long bytes = hx_bsgs_tc_bytes(ctx, rows, n1, nqv);
+  if (bytes < 0) throw std::invalid_argument("bsgs: tensor-core shape");
+  auto pk = dev(((std::size_t)bytes + 7) / 8);
+  ck(hx_bsgs_tc_pack(ctx, pk->ptr, ptrs.data(), rows, n1, nqv, nullptr), "bsgs_tc_pack");
+  buf->derived.emplace_back(sig, pk);
+  return pk;
+}
+
+static bool tc_mac_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HX_MAC_TC");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
     const std::vector<std::vector<Ciphertext>>& babies, const std::vector<Plaintext>& diags, int n1, int n2,
     int blocks, bool allow_empty) {
@@ -729,7 +763,65 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
   Scale dscale;
   bool have_scale = false;
   std::vector<std::vector<char>> live(blocks, std::vector<char>(n2, 0));
-  for (int b = 0; b < blocks; ++b) {
+  // ---- tensor-core MAC: every row block at once (tiles of <= 128 rows), the
+  // diagonals as byte-sliced operand tiles made once per matrix; dense or
+  // mostly dense blocks whose diagonals share one buffer
+  bool tc_done = false;
+  {
+    const long long bst = T > 1 ? (long long)(baby_ptr[1] - baby_ptr[0]) : 0;
+    bool ok = tc_mac_enabled() && n1 % 8 == 0 && n1 <= 64 && n2 <= 128 && N >= 128;
+    for (int t = 1; t < T && ok; ++t) ok = (long long)(baby_ptr[t] - baby_ptr[t - 1]) == bst;
+    std::shared_ptr<DeviceBuffer> src;
+    std::size_t nlive = 0;
+    for (std::size_t e = 0; e < (std::size_t)blocks * d && ok; ++e) {
+      const Plaintext& pt = diags[e];
+      if (!pt.payload) continue;
+      const auto& pl = payload(pt);
+      if (!src) src = pl.buf;
+      ok = pl.buf == src && pt.level == level && (!have_scale || pt.scale == dscale);
+      dscale = pt.scale;
+      have_scale = true;
+      ++nlive;
+    }
+    ok = ok && src && 2 * nlive >= (std::size_t)blocks * d;  // sparse matrices: the index-list MAC
+    // one token over few rows: the streaming CUDA-core MAC is as fast (measured:
+    // 32 rows x n1 = 32 at T = 1 is 16.1 vs 12.8 ms per FFN W1 stacked matvec)
+    ok = ok && (T >= 2 || blocks * n2 >= 96);
+    if (ok) {
+      const int bpt = std::max(1, 128 / n2);
+      for (int b0 = 0; b0 < blocks; b0 += bpt) {
+        const int nb = std::min(bpt, blocks - b0);
+        std::vector<const u64*> ptrs((std::size_t)nb * d, nullptr);
+        for (std::size_t e = 0; e < ptrs.size(); ++e) {
+          const Plaintext& pt = diags[(std::size_t)b0 * d + e];
+          if (pt.payload) ptrs[e] = payload(pt).data();
+        }
+        const auto pk = tc_pack(ctx_, src, ptrs, nb * n2, n1, nqv);
+        ck(hx_bsgs_mac_tc(ctx_, inner->ptr + (std::size_t)b0 * ctw, (long long)jstride, (long long)ctw,
+                          (long long)(blocks * ctw), baby_ptr[0], bst, pk->ptr, nb, n2, n1, nqv, T, nullptr),
+           "bsgs_mac_tc");
+      }
+      for (int b = 0; b < blocks; ++b) {
+        std::uint64_t ptmuls = 0, adds = 0;
+        for (int j = 0; j < n2; ++j) {
+          int cnt = 0;
+          for (int k = 0; k < n1; ++k) cnt += diags[(std::size_t)b * d + (std::size_t)j * n1 + k].payload != nullptr;
+          if (cnt) {
+            ptmuls += cnt;
+            adds += cnt - 1;
+            live[b][j] = 1;
+          }
+        }
+        if (!ptmuls && !allow_empty) throw std::invalid_argument("matvec_bsgs: block has no non-zero diagonal");
+        if (ptmuls) trace_.record(OpKind::PtMul, level, ptmuls * T);
+        if (adds) trace_.record(OpKind::CtAdd, level, adds * T);
+      }
+      tc_done = true;
+    } else {
+      have_scale = false;
+    }
+  }
+  for (int b = 0; b < blocks && !tc_done; ++b) {
     const Plaintext* D = diags.data() + (std::size_t)b * d;
     std::uint64_t ptmuls = 0, adds = 0;
     // fast path: the whole block dense and contiguous (encode_many) -> one MAC launch per token

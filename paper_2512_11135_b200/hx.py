@@ -13,7 +13,7 @@ import os
 from typing import Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhx_b200.so")
+LIB_PATH = os.environ.get("HX_LIB_PATH") or os.path.join(_HERE, "libhx_b200.so")  # override: debug builds
 
 HX_OK = 0
 

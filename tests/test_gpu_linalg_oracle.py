@@ -165,6 +165,23 @@ def test_c2s_bsgs_multiblock_words_vs_oracle(stacked, prune):
     _bsgs_case(ov, A, ov.be.max_level, stacked)
 
 
+@pytest.mark.parametrize("prune", [0, 5])
+def test_c2s_bsgs_tensor_core_rows96_words_vs_oracle(prune):
+    """6 row blocks x n2 = 16 = 96 rows, n1 = 16, one token: the tensor-core MAC
+    path of bsgs_blocks_tokens (all blocks in one hx_bsgs_mac_tc launch;
+    absent diagonals as zero operand rows) vs the oracle"""
+    ov = view("c2s")
+    rng = np.random.default_rng(300 + prune)
+    A = rng.normal(0, 0.02, (1536, 256))
+    if prune:
+        for b in range(6):
+            for i in rng.choice(256, prune, replace=False):
+                for j in range(256):
+                    A[b * 256 + j, (i + j) % 256] = 0
+    M, *_ = _bsgs_case(ov, A, ov.be.max_level)
+    assert M.info()["blocks"] == 6 and M.info()["n1"] == 16
+
+
 def test_c2s_bsgs_token_batch_words_vs_oracle():
     from paper_2512_11135_b200.helix import BSGS
 
