@@ -14,7 +14,8 @@ HOST_DIR  := $(PKG)/csrc/host
 CU_SRCS   := $(CU_DIR)/hx_ntt.cu $(CU_DIR)/hx_ops.cu $(CU_DIR)/hx_bsgs.cu $(CU_DIR)/hx_bsgs_tc.cu $(CU_DIR)/hx_encode.cu
 CU_HDRS   := $(wildcard $(CU_DIR)/*.cuh) $(CU_DIR)/hx_internal.h include/hx_b200.h
 HOST_SRCS := $(HOST_DIR)/params.cpp $(HOST_DIR)/encoder.cpp $(HOST_DIR)/gpu_backend.cpp \
-             $(HOST_DIR)/packing.cpp $(HOST_DIR)/linalg.cpp $(HOST_DIR)/helix_c.cpp $(HOST_DIR)/lattice.cpp
+             $(HOST_DIR)/packing.cpp $(HOST_DIR)/linalg.cpp $(HOST_DIR)/helix_c.cpp $(HOST_DIR)/lattice.cpp \
+             $(HOST_DIR)/roofline.cpp
 HOST_HDRS := $(wildcard include/helix/*.hpp) include/helix_c.h include/hx_b200.h
 BUILD     := build
 CU_OBJS   := $(patsubst $(CU_DIR)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
@@ -23,8 +24,8 @@ LIB       := $(PKG)/libhx_b200.so
 HLIB      := $(PKG)/libhelix_b200.so
 TESTBIN   := $(BUILD)/test_linalg_clear
 
-.PHONY: all lib host oracle ref testbin testgpu clean
-all: lib host oracle testbin testgpu
+.PHONY: all lib host oracle ref testbin testgpu cli clean
+all: lib host oracle testbin testgpu cli
 
 lib: $(LIB)
 host: $(HLIB)
@@ -65,6 +66,16 @@ $(GPUTEST): tests/cpp/test_gpu_api.cpp $(HLIB) $(HOST_HDRS)
 	  -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,$(CUDA_HOME)/lib64
 
 testgpu: $(GPUTEST)
+
+# `helix` command line: roofline / matvec / matmul
+CLI       := $(BUILD)/helix
+$(CLI): $(HOST_DIR)/cli.cpp $(HLIB) $(HOST_HDRS)
+	@mkdir -p $(BUILD)
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude -I$(CUDA_HOME)/include -I$(JSON_DIR) $(HOST_DIR)/cli.cpp \
+	  -o $@ -L$(PKG) -lhelix_b200 -lhx_b200 -L$(CUDA_HOME)/lib64 -lcudart \
+	  -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,$(CUDA_HOME)/lib64
+
+cli: $(CLI)
 
 oracle:
 	$(MAKE) -C oracle all
