@@ -45,14 +45,18 @@ $(HLIB): $(HOST_OBJS) $(LIB)
 	$(CXX) -shared -o $@ $(HOST_OBJS) -L$(PKG) -lhx_b200 -L$(CUDA_HOME)/lib64 -lcudart \
 	  -Wl,-rpath,'$$ORIGIN' -Wl,-rpath,$(CUDA_HOME)/lib64
 
-# C++ test driver: the SPEC linear-algebra kernels on the cleartext oracle
-# backend (oracle/clear_backend.cpp) -- counts, levels, scales, results.
-$(TESTBIN): tests/cpp/test_linalg_clear.cpp oracle/clear_backend.cpp oracle/clear_backend.hpp \
-            $(HOST_DIR)/packing.cpp $(HOST_DIR)/params.cpp $(HOST_DIR)/linalg.cpp $(HOST_HDRS)
+# C++ test driver: the SPEC linear-algebra kernels on the reference's own
+# cleartext ReferenceBackend (its source compiled from the reference tree
+# against our API-compatible headers; only where /root/reference exists)
+REF_PROJ  ?= /root/reference/proj
+$(TESTBIN): tests/cpp/test_linalg_clear.cpp $(HOST_DIR)/packing.cpp $(HOST_DIR)/params.cpp $(HOST_DIR)/linalg.cpp \
+            $(HOST_HDRS)
 	@mkdir -p $(BUILD)
-	$(CXX) -std=c++20 -O2 -Wall -Iinclude -Ioracle -I$(JSON_DIR) -DHELIX_NO_GPU \
-	  tests/cpp/test_linalg_clear.cpp oracle/clear_backend.cpp $(HOST_DIR)/packing.cpp \
-	  $(HOST_DIR)/params.cpp $(HOST_DIR)/linalg.cpp -o $@
+	@if [ -f $(REF_PROJ)/src/reference_backend.cpp ]; then \
+	  $(CXX) -std=c++20 -O2 -Wall -Iinclude -I$(REF_PROJ)/include -I$(JSON_DIR) -DHELIX_NO_GPU \
+	    tests/cpp/test_linalg_clear.cpp $(REF_PROJ)/src/reference_backend.cpp $(HOST_DIR)/packing.cpp \
+	    $(HOST_DIR)/params.cpp $(HOST_DIR)/linalg.cpp -o $@; \
+	else echo "testbin: $(REF_PROJ) absent, skipped"; fi
 
 testbin: $(TESTBIN)
 

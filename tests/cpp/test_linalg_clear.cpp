@@ -1,7 +1,9 @@
 // test_linalg_clear.cpp -- SPEC acceptance tests for the linear-algebra entry
-// points (helix/linalg.hpp, helix/packing.hpp) on the cleartext semantic
-// oracle backend (oracle/clear_backend.*, restating the reference's
-// ReferenceBackend).  Known answers are the SPEC's own examples
+// points (helix/linalg.hpp, helix/packing.hpp) on the REFERENCE's own
+// cleartext backend: helix::ReferenceBackend compiled from
+// /root/reference/proj/src/reference_backend.cpp against this repository's
+// API-compatible headers (Makefile `testbin`; test infrastructure, built only
+// where the reference tree is present).  Known answers are the SPEC's own examples
 // (acceptance criteria :674-682).  Run by
 // tests/test_linalg_cpu.py; exits non-zero on the first failure.
 #include <cmath>
@@ -11,12 +13,12 @@
 #include <string>
 #include <vector>
 
-#include "clear_backend.hpp"
 #include "helix/linalg.hpp"
+#include "helix/reference_backend.hpp"
 #include "helix/packing.hpp"
 
 using namespace helix;
-using helix_oracle::ClearBackend;
+using helix::ReferenceBackend;
 
 static int g_checks = 0;
 #define CHECK(cond, msg)                                                                  \
@@ -70,7 +72,7 @@ static double maxdiff(const std::vector<double>& a, const std::vector<double>& b
 }
 
 // output slot of row r for each method (row: slot r; diag/bsgs: block r/d, slot r%d)
-static std::vector<double> matvec_result(ClearBackend& be, const MatvecResult& R, const PackedMatrix& M) {
+static std::vector<double> matvec_result(ReferenceBackend& be, const MatvecResult& R, const PackedMatrix& M) {
   std::vector<double> y(M.rows);
   if (M.layout == Layout::PackedRow) {
     const auto v = be.decrypt(R.outputs[0]);
@@ -81,12 +83,12 @@ static std::vector<double> matvec_result(ClearBackend& be, const MatvecResult& R
   return y;
 }
 
-static MatvecResult run(ClearBackend& be, const PackedMatrix& M, const std::vector<double>& x, int level) {
+static MatvecResult run(ReferenceBackend& be, const PackedMatrix& M, const std::vector<double>& x, int level) {
   std::vector<std::int64_t> keys = M.layout == Layout::PackedRow ? row_rotations(M)
                                    : M.layout == Layout::Diagonal ? diag_rotations(M.d)
                                                                   : bsgs_rotations(M.plan);
   be.generate_rotation_keys(keys);
-  const auto xs = replicate(x, M.d, be.slots());
+  const auto xs = replicate(x, M.d, be.params().slot_count());
   const auto ct = be.encrypt(be.encode(xs, level, be.params().delta()));
   const auto E = encode_matrix(be, M, level);
   return M.layout == Layout::PackedRow ? matvec_row(be, E, ct)
@@ -201,7 +203,7 @@ int main() {
   const double tol = 1e-9;
   // ---------------------------------------------------------- slot API
   {
-    ClearBackend be(params(8, 3));  // n = 4
+    ReferenceBackend be(params(8, 3));  // n = 4
     be.generate_rotation_keys(std::vector<std::int64_t>{1});
     const std::vector<double> v{1, 2, 3, 4};
     const auto r = be.decrypt(be.rotate(be.encrypt(be.encode(v, 3, be.params().delta())), 1));
@@ -210,7 +212,7 @@ int main() {
           "missing rotation key is an error");
   }
   {
-    ClearBackend be(params(32, 3));  // n = 16
+    ReferenceBackend be(params(32, 3));  // n = 16
     be.generate_rotation_keys(std::vector<std::int64_t>{3, 5, 8});
     std::vector<double> v(16);
     for (int i = 0; i < 16; ++i) v[i] = i * 1.5 - 3;
@@ -260,7 +262,7 @@ int main() {
   }
   // ---------------------------------------------------------- rotate_and_sum
   {
-    ClearBackend be(params(8, 3));
+    ReferenceBackend be(params(8, 3));
     be.generate_rotation_keys(std::vector<std::int64_t>{1, 2});
     KernelReport rep;
     const auto c = rotate_and_sum(be, be.encrypt(be.encode(std::vector<double>{1, 2, 3, 4}, 3, be.params().delta())), 4, 1, &rep);
@@ -273,9 +275,9 @@ int main() {
   {
     std::mt19937_64 g(21);
     for (auto [r, c] : std::vector<std::pair<int, int>>{{40, 16}, {64, 32}, {5, 8}, {48, 12}}) {
-      ClearBackend be(params(1024, 6));
+      ReferenceBackend be(params(1024, 6));
       const Matrix A = random_matrix(g, r, c);
-      const PackedMatrix P = pack_bsgs_stacked(A, be.slots());
+      const PackedMatrix P = pack_bsgs_stacked(A, be.params().slot_count());
       CHECK(unpack(P).data == A.data, "unpack o pack_bsgs_stacked = identity");
       std::vector<double> x(c);
       std::uniform_real_distribution<double> U(-1, 1);
@@ -283,7 +285,7 @@ int main() {
       be.generate_rotation_keys(bsgs_rotations(P.plan));
       std::vector<double> xp((std::size_t)P.d, 0.0);
       std::copy(x.begin(), x.end(), xp.begin());
-      const auto ct = be.encrypt(be.encode(replicate(xp, P.d, be.slots()), 5, be.params().delta()));
+      const auto ct = be.encrypt(be.encode(replicate(xp, P.d, be.params().slot_count()), 5, be.params().delta()));
       const auto R = matvec_bsgs(be, encode_matrix(be, P, 5), ct);
       const auto y = be.decrypt(R.outputs[0]);
       double err = 0;
@@ -293,16 +295,16 @@ int main() {
         err = std::max(err, std::abs(y[i] - acc));
       }
       CHECK(R.outputs.size() == 1 && err < 1e-9, "stacked BSGS = cleartext product, one output");
-      CHECK((int64_t)R.report.rotations == predicted_rotations(Layout::BsgsStacked, r, c, be.slots()),
+      CHECK((int64_t)R.report.rotations == predicted_rotations(Layout::BsgsStacked, r, c, be.params().slot_count()),
             "stacked BSGS rotations = (n1 - 1) + (n2 - 1)");
     }
   }
   // ---------------------------------------------------------- polyeval
   {
-    ClearBackend be(params(1024, 8));
+    ReferenceBackend be(params(1024, 8));
     std::mt19937_64 g(11);
     std::uniform_real_distribution<double> U(-1.0, 1.0);
-    std::vector<double> xs(be.slots());
+    std::vector<double> xs(be.params().slot_count());
     for (auto& v : xs) v = U(g);
     const auto ct = be.encrypt(be.encode(xs, 8, be.params().delta()));
     std::vector<double> c(8);
@@ -337,10 +339,10 @@ int main() {
     const Matrix A = from_rows({{1, 2, 3, 4}, {5, 6, 7, 8}, {9, 10, 11, 12}, {13, 14, 15, 16}});
     const std::vector<double> x{1, 2, 3, 4}, want{30, 70, 110, 150};
     for (Layout L : {Layout::PackedRow, Layout::Diagonal, Layout::BsgsDiagonal}) {
-      ClearBackend be(params(1024, 6));
-      const auto P = L == Layout::PackedRow ? pack_rows(A, be.slots())
-                     : L == Layout::Diagonal ? pack_diagonals(A, be.slots())
-                                             : pack_bsgs(A, BsgsPlan{2, 2}, be.slots());
+      ReferenceBackend be(params(1024, 6));
+      const auto P = L == Layout::PackedRow ? pack_rows(A, be.params().slot_count())
+                     : L == Layout::Diagonal ? pack_diagonals(A, be.params().slot_count())
+                                             : pack_bsgs(A, BsgsPlan{2, 2}, be.params().slot_count());
       const auto R = run(be, P, x, 5);
       CHECK(maxdiff(matvec_result(be, R, P), want, 4) < tol, "4x4 matvec = [30,70,110,150] (SPEC.md:374)");
       CHECK(R.report.output_scale == be.params().delta(), "output scale exactly Delta");
@@ -349,13 +351,13 @@ int main() {
       if (L == Layout::BsgsDiagonal) CHECK(R.report.levels_consumed == 1 && R.report.rotations == 2 && R.report.pt_muls == 4, "bsgs: 2 rotations, 1 level (SPEC.md:392)");
     }
     // bsgs 16x16 -> 6 rotations
-    ClearBackend be(params(1024, 6));
+    ReferenceBackend be(params(1024, 6));
     std::mt19937_64 g(3);
     const Matrix M = random_matrix(g, 16, 16);
-    const auto R = run(be, pack_bsgs(M, be.slots()), std::vector<double>(16, 0.5), 4);
+    const auto R = run(be, pack_bsgs(M, be.params().slot_count()), std::vector<double>(16, 0.5), 4);
     CHECK(R.report.rotations == 6, "bsgs 16x16 -> 6 rotations");
     // 1x1 trivial plan: 0 rotations
-    ClearBackend b1(params(1024, 6));
+    ReferenceBackend b1(params(1024, 6));
     const auto R1 = run(b1, pack_bsgs(from_rows({{3.0}}), b1.slots()), std::vector<double>{2.0}, 4);
     CHECK(R1.report.rotations == 0 && std::abs(b1.decrypt(R1.outputs[0])[0] - 6.0) < tol, "1x1 -> 0 rotations, pure pt-mul");
   }
@@ -373,10 +375,10 @@ int main() {
         for (auto& v : x) v = u(g);
         const auto want = cleartext(A, x);
         for (Layout L : {Layout::PackedRow, Layout::Diagonal, Layout::BsgsDiagonal}) {
-          ClearBackend be(params(2048, 4));
-          const auto P = L == Layout::PackedRow ? pack_rows(A, be.slots())
-                         : L == Layout::Diagonal ? pack_diagonals(A, be.slots())
-                                                 : pack_bsgs(A, be.slots());
+          ReferenceBackend be(params(2048, 4));
+          const auto P = L == Layout::PackedRow ? pack_rows(A, be.params().slot_count())
+                         : L == Layout::Diagonal ? pack_diagonals(A, be.params().slot_count())
+                                                 : pack_bsgs(A, be.params().slot_count());
           const auto Rr = run(be, P, x, 3);
           CHECK(maxdiff(matvec_result(be, Rr, P), want, R) < tol, "method equivalence vs cleartext (SPEC.md:674)");
           const int lv = L == Layout::PackedRow ? 2 : 1;
@@ -396,10 +398,10 @@ int main() {
   }
   // ---------------------------------------------------------- matmul
   {
-    ClearBackend be(params(64, 5));  // n = 32
-    be.generate_rotation_keys(matmul_rotations(2, be.slots()));
-    const auto A = be.encrypt(be.encode(pack_rowmajor(from_rows({{1, 2}, {3, 4}}), be.slots()).payloads[0], 5, be.params().delta()));
-    const auto B = be.encrypt(be.encode(pack_rowmajor(from_rows({{5, 6}, {7, 8}}), be.slots()).payloads[0], 5, be.params().delta()));
+    ReferenceBackend be(params(64, 5));  // n = 32
+    be.generate_rotation_keys(matmul_rotations(2, be.params().slot_count()));
+    const auto A = be.encrypt(be.encode(pack_rowmajor(from_rows({{1, 2}, {3, 4}}), be.params().slot_count()).payloads[0], 5, be.params().delta()));
+    const auto B = be.encrypt(be.encode(pack_rowmajor(from_rows({{5, 6}, {7, 8}}), be.params().slot_count()).payloads[0], 5, be.params().delta()));
     const auto [Cm, rep] = matmul_ctct(be, A, B, 2);
     const auto c = be.decrypt(Cm);
     CHECK(maxdiff(c, {19, 22, 43, 50}, 4) < tol, "matmul [[1,2],[3,4]][[5,6],[7,8]] (SPEC.md:401)");
@@ -409,12 +411,12 @@ int main() {
     CHECK(throws<LevelUnderflowError>([&] { matmul_ctct(be, be.mod_down(A, 1), be.mod_down(B, 1), 2); }), "level < 2 rejected");
   }
   for (int d : {2, 4, 8, 16}) {
-    ClearBackend be(params(1024, 5));
-    be.generate_rotation_keys(matmul_rotations(d, be.slots()));
+    ReferenceBackend be(params(1024, 5));
+    be.generate_rotation_keys(matmul_rotations(d, be.params().slot_count()));
     std::mt19937_64 g(d);
     const Matrix A = random_matrix(g, d, d), B = random_matrix(g, d, d), B2 = random_matrix(g, d, d);
     auto enc = [&](const Matrix& M) {
-      return be.encrypt(be.encode(pack_rowmajor(M, be.slots()).payloads[0], 5, be.params().delta()));
+      return be.encrypt(be.encode(pack_rowmajor(M, be.params().slot_count()).payloads[0], 5, be.params().delta()));
     };
     const auto [C, rep] = matmul_ctct(be, enc(A), enc(B), d);
     const int lg = d == 2 ? 1 : d == 4 ? 2 : d == 8 ? 3 : 4;
