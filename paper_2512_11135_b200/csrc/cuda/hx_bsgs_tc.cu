@@ -347,12 +347,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) bsgs_mac_tc_kernel(TcArgs A) {
       if (bt == 0) TC_TRACE(2, n);
       const u64* bb = sBb(s);
       for (int u = bt; u < units; u += 32 * kTcBuildWarps) {
+        // lane order (tok, kq mod 4, c, g, kq / 4): the 32 stores of a warp
+        // land on distinct (row nn mod 8, 4-byte column kq mod 4) words of
+        // the 128-byte core matrices -- one shared-memory wavefront each for
+        // T >= 4 (tok fastest alone put 4 lanes on every bank)
         const int tok = u % T;
         int rest = u / T;
-        const int c = rest & 1;
-        rest >>= 1;
-        const int g = rest % G;
-        const int kq = rest / G;
+        int kq, c, g;
+        if ((nkq & 3) == 0) {
+          const int klo = rest & 3;
+          rest >>= 2;
+          c = rest & 1;
+          rest >>= 1;
+          g = rest % G;
+          kq = klo + 4 * (rest / G);
+        } else {
+          c = rest & 1;
+          rest >>= 1;
+          g = rest % G;
+          kq = rest / G;
+        }
         u64 w[4];
 #pragma unroll
         for (int m = 0; m < 4; ++m) w[m] = bb[((size_t)(g * n1 + 4 * kq + m) * 2 + c) * T + tok];

@@ -53,6 +53,17 @@ __device__ __forceinline__ u64 shoup_lazy(u64 a, u64 w, u64 wp, u64 q) {
   return a * w - mulhi64(a, wp) * q;
 }
 
+// Same product with the Shoup quotient's lowest partial product dropped:
+// hi64(a wp) ~ ah wh + hi32(ah wl) + hi32(al wh) undershoots the exact
+// quotient by at most 2, so the result is in [0, 4q) (q < 2^61).  3 multiplies
+// instead of the 64x64 high product's 4 plus carry chain: the integer NTT
+// butterflies are IMAD-bound.
+__device__ __forceinline__ u64 shoup_lazy4(u64 a, u64 w, u64 wp, u64 q) {
+  const u32 al = (u32)a, ah = (u32)(a >> 32), wl = (u32)wp, wh = (u32)(wp >> 32);
+  const u64 qh = (u64)ah * wh + __umulhi(ah, wl) + __umulhi(al, wh);
+  return a * w - qh * q;
+}
+
 __device__ __forceinline__ u64 csub(u64 a, u64 m) { return a >= m ? a - m : a; }
 
 // [0, 4q) -> [0, q)

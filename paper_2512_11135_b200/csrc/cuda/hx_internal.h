@@ -82,6 +82,13 @@ struct hx_ctx {
   // Rescale constants: [l][i] for i < l
   hx::SC* d_qlinv = nullptr;   // [n_chain][n_chain]
   hx::u64* d_qlmod = nullptr;  // [n_chain][n_chain]
+  // side stream of the key switch (HX_KS_SIDE=1): the integer-class ModUp
+  // limbs (NTT + key inner product) run beside the FP64 ROW + inner kernel;
+  // fork / join events, `side_open` between the fork in modup and the join
+  // in the inner product
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool side_open = false;
   // launch counter (kernels issued through this context)
   unsigned long long launches = 0;
   // live per-kernel timing (hx_ctx_time_kernel): CUDA events recorded on the

@@ -126,6 +126,10 @@ __device__ __forceinline__ u64 bconv_word(const u64* src, int stride, int cnt, c
 #define HX_WIDE_INT 1
 #endif
 constexpr bool kWideInt = HX_WIDE_INT != 0;
+#ifndef HX_MODUP_INT0
+#define HX_MODUP_INT0 0
+#endif
+constexpr bool kModUpInt0 = HX_MODUP_INT0 != 0;
 #ifndef HX_MODUP_MINB
 #define HX_MODUP_MINB 3
 #endif
@@ -287,7 +291,9 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? HX_MODUP_MINB
     sf64[i] = false;
     if (i < cnt) {
       const PrimeConst& Q = A.pc[A.src_pbase + lo + i];
-      sf64[i] = Q.f64;
+      // HX_MODUP_INT0: source 0 of every ModUp digit kept as an integer, so its
+      // products run on the integer pipe (Shoup, mode 1) beside the FP64 ones
+      sf64[i] = Q.f64 && !(kModUpInt0 && !CEN && i == 0);
       const SC h = A.qhinv[A.qh_off[d] + i];
       const u64* ci = cb + (long long)(lo + i) * N;
       u64 a[16];

@@ -66,6 +66,16 @@ __device__ __forceinline__ int swz(int e) {
   return ROW ? (e ^ ((e >> 4) & 15)) : (e ^ (((e >> 7) & 1) << 3));
 }
 
+#ifndef HX_SHOUP_APPROX
+#define HX_SHOUP_APPROX 0
+#endif
+constexpr bool kShoupApprox = HX_SHOUP_APPROX != 0;
+__device__ __forceinline__ u64 shoup_ntt(u64 a, u64 w, u64 wp, u64 q) {
+  return kShoupApprox ? shoup_lazy4(a, w, wp, q) : shoup_lazy(a, w, wp, q);
+}
+// [0, 8q) -> [0, q)
+__device__ __forceinline__ u64 reduce8(u64 a, u64 q) { return csub(csub(csub(a, q << 2), q << 1), q); }
+
 // One radix-2^W group over sub-bits [g0, g0+W) of the tile index.
 // x[r], r = (r_out << W) | r_in ; element e_r = base[r_out] | (r_in << lowbits).
 template <bool FWD, bool ROW, int S, int W>
@@ -74,7 +84,9 @@ __device__ __forceinline__ void ntt_group(u64 (&x)[16], const int (&jb)[16 >> W]
                                           const PrimeConst& P, bool last_stage_inv) {
   constexpr int NO = 16 >> W;
   const int logb = ROW ? 0 : (logn - S);  // j-bit of sub-bit 0
-  const u64 q = P.q, q2 = P.two_q;
+  // lazy bound: products in [0, 2q) (exact Shoup) or [0, 4q) (shoup_lazy4);
+  // forward values stay below 2 q2, inverse values below q2
+  const u64 q = P.q, q2 = kShoupApprox ? (P.q << 2) : P.two_q;
   const u64 N = 1ull << logn;
 #pragma unroll
   for (int ii = 0; ii < W; ++ii) {
@@ -96,15 +108,15 @@ __device__ __forceinline__ void ntt_group(u64 (&x)[16], const int (&jb)[16 >> W]
           const u64 X = x[r0], Y = x[r1];
           if (FWD) {
             const u64 Xr = csub(X, q2);
-            const u64 T = shoup_lazy(Y, wt.x, wt.y, q);
+            const u64 T = shoup_ntt(Y, wt.x, wt.y, q);
             x[r0] = Xr + T;
             x[r1] = Xr - T + q2;
           } else if (fin) {
-            x[r0] = shoup_lazy(X + Y, P.ninv, P.ninvp, q);
-            x[r1] = shoup_lazy(X - Y + q2, P.w1n, P.w1np, q);
+            x[r0] = shoup_ntt(X + Y, P.ninv, P.ninvp, q);
+            x[r1] = shoup_ntt(X - Y + q2, P.w1n, P.w1np, q);
           } else {
             x[r0] = csub(X + Y, q2);
-            x[r1] = shoup_lazy(X - Y + q2, wt.x, wt.y, q);
+            x[r1] = shoup_ntt(X - Y + q2, wt.x, wt.y, q);
           }
         }
       }
@@ -513,7 +525,8 @@ __device__ __forceinline__ void ntt_pass_body(const NttArgs& a, const EpiArgs* e
         }                                                                                      \
       } else {                                                                                 \
         _Pragma("unroll") for (int r = 0; r < 16; ++r) x[r] =                                  \
-            (FWD ? (ROW ? reduce4(x[r], q, P.two_q) : x[r]) : (ROW ? x[r] : csub(x[r], q)));    \
+            (FWD ? (ROW ? (kShoupApprox ? reduce8(x[r], q) : reduce4(x[r], q, P.two_q)) : x[r])   \
+                 : (ROW ? x[r] : (kShoupApprox ? reduce4(x[r], q, P.two_q) : csub(x[r], q))));       \
       }                                                                                        \
       if (FWD && ROW) {                                                                        \
         /* stage through smem for a coalesced store */                                         \

@@ -314,6 +314,29 @@ bool modup_fused_ok(const hx_ctx* c, int n_q) {
 // defer_rows: the FP64-class limbs are left after their COL pass (the fused
 // ROW + inner-product kernel finishes them, ks_inner_multi rows_deferred);
 // only valid when modup_fused_ok
+bool side_stream_on() {
+  static const bool on = getenv("HX_KS_SIDE") && atoi(getenv("HX_KS_SIDE")) != 0;
+  return on;
+}
+// s -> c->side: the side stream starts after everything issued on s so far
+void fork_side(hx_ctx* c, cudaStream_t s) {
+  if (!c->side) {
+    cuda_ok(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking), "side stream");
+    cuda_ok(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming), "side event");
+    cuda_ok(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming), "side event");
+  }
+  cuda_ok(cudaEventRecord(c->ev_fork, s), "fork");
+  cuda_ok(cudaStreamWaitEvent(c->side, c->ev_fork, 0), "fork");
+  c->side_open = true;
+}
+// c->side -> s: work issued on s from now on waits for the side stream
+void join_side(hx_ctx* c, cudaStream_t s) {
+  if (!c->side_open) return;
+  cuda_ok(cudaEventRecord(c->ev_join, c->side), "join");
+  cuda_ok(cudaStreamWaitEvent(s, c->ev_join, 0), "join");
+  c->side_open = false;
+}
+
 void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long batch, int n_q,
            cudaStream_t s, bool copy_own = true, bool defer_rows = false) {
   const long long N = c->N();
@@ -373,7 +396,14 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
       x.prime[x.count] = lt.prime[e];
       ++x.count;
     }
-    if (li.count) hx::ntt_forward(c, digits, batch, li, s);
+    if (li.count && defer_rows && side_stream_on()) {
+      // the integer-class limbs (NTT here, inner product in ks_inner_multi)
+      // on the side stream, beside the fused FP64 ROW + inner kernel
+      fork_side(c, s);
+      hx::ntt_forward(c, digits, batch, li, c->side);
+    } else if (li.count) {
+      hx::ntt_forward(c, digits, batch, li, s);
+    }
     if (lf.count && !defer_rows) hx::ntt_forward_rows(c, digits, batch, lf, s);
     return;
   }
@@ -431,7 +461,10 @@ template <int S>
 void launch_row_inner_t(hx_ctx* c, const hx::RowInnerArgs& A, cudaStream_t s) {
   constexpr int OB = 3, TILE = 1 << (S + OB);  // the ROW tile of hx_ntt.cu (HX_NTT_OB)
   auto kern = hx::ks_row_inner_f64_kernel<S, OB, 8>;
-  constexpr int smem = hx::ntt_smem_bytes<true, S, OB, true>();
+  // HX_RI_2CTA=1: request enough shared memory that only 2 CTAs fit an SM,
+  // leaving registers for the side stream's integer kernels (HX_KS_SIDE)
+  static const bool two = getenv("HX_RI_2CTA") && atoi(getenv("HX_RI_2CTA")) != 0;
+  const int smem = two ? std::max(hx::row_inner_smem_bytes<S, OB>(), 78 * 1024) : hx::row_inner_smem_bytes<S, OB>();
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -475,8 +508,9 @@ bool row_inner_ok(const hx_ctx* c, int n_q, const u64* key) {
 // pass only (modup defer_rows); one key over the batch or one key per E
 // elements (!shared), uncompressed keys, identity g, own limbs from c1.
 void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<const u64*>& keys,
-                    bool shared, long long E, int n_q, u64 g, cudaStream_t s, const u64* c1 = nullptr,
+                    bool shared, long long E, int n_q, u64 g, cudaStream_t s_main, const u64* c1 = nullptr,
                     long long c1_stride = 0, bool rows_deferred = false) {
+  const cudaStream_t s = s_main;
   HX_REQUIRE(!keys.empty() && (int)keys.size() <= hx::kMaxKeys, "ks_inner: 1..64 keys per launch");
   hx::InnerArgs A;
   A.digits = digits;
@@ -557,6 +591,8 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
     launched(c, "ks_inner_f64_kernel");
   }
   if (ni > 0) {
+    // integer-class limbs: on the side stream when modup forked it
+    const cudaStream_t s = rows_deferred && c->side_open ? c->side : s_main;
     dim3 grid((unsigned)(c->N() / th), (unsigned)ni, gz);
     if (A.dnum <= 4)
       hx::ks_inner_kernel<4><<<grid, th, 0, s>>>(A, il);
@@ -570,6 +606,7 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
       hx::ks_inner_kernel<64><<<grid, th, 0, s>>>(A, il);
     launched(c, "ks_inner_kernel");
   }
+  join_side(c, s_main);
 }
 
 void ks_inner(hx_ctx* c, u64* u, const u64* digits, const u64* key, long long batch, int n_q,
@@ -1288,6 +1325,12 @@ void hx_ctx_destroy(hx_ctx* c) {
     cudaFree(c->arena.base);
   }
   if (c->arena.ev) cudaEventDestroy(c->arena.ev);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+    cudaEventDestroy(c->ev_fork);
+    cudaEventDestroy(c->ev_join);
+  }
   delete c;
 }
 

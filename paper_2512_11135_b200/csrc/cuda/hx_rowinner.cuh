@@ -35,6 +35,23 @@ namespace hx {
 #define HX_ROWINNER_MINB 3
 #endif
 constexpr int kRowInnerMaxKeys = 64;
+// HX_RI_PREFETCH: the next digit's COL-pass tile is copied into a second
+// shared-memory buffer (cp.async, 16 B per copy) while the current digit is
+// transformed, so the digit loop no longer waits on an HBM load per digit
+#ifndef HX_RI_PREFETCH
+#define HX_RI_PREFETCH 0
+#endif
+constexpr bool kRiPrefetch = HX_RI_PREFETCH != 0;
+// shared memory of ks_row_inner_f64_kernel: exchange tile + ROW twiddles
+// (ntt_smem_bytes<true, S, OB, true>) + two prefetch tiles
+template <int S, int OB>
+constexpr int row_inner_tw_words() {
+  return (17 * (1 << OB) * ((1 << S) - 1) / 16 + 16 + 1) & ~1;
+}
+template <int S, int OB>
+constexpr int row_inner_smem_bytes() {
+  return 8 * ((1 << (S + OB)) + row_inner_tw_words<S, OB>() + (kRiPrefetch ? 2 * (1 << (S + OB)) : 0));
+}
 
 struct RowInnerArgs {
   const u64* digits;  // [E][dnum][ext][N]: COL-pass output (FP64 bits) of the ModUp limbs
@@ -101,12 +118,39 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, HX_ROWINNER_MINB) ks_row
 #pragma unroll
   for (int r = 0; r < 16; ++r) acc0[r] = acc1[r] = 0.0;
 
+  u64* pbuf = dyn_smem + TILE + row_inner_tw_words<S, OB>();  // [2][TILE] (kRiPrefetch)
+  auto next_digit = [&](int d) {  // first transformed digit >= d, or dnum
+    while (d < A.dnum && d == down) ++d;
+    return d;
+  };
+  auto prefetch = [&](int d, int slot) {  // one commit group per call
+    if (d < A.dnum) {
+      const u64* src = Db + (long long)d * ext * N;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(pbuf + slot * TILE);
+#pragma unroll
+      for (int i = 0; i < TILE / (2 * T); ++i) {
+        const int c = t + i * T;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * c), "l"(src + 2 * c)
+                     : "memory");
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  int slot = 0;
+  if (kRiPrefetch) prefetch(next_digit(0), 0);
+
   bool tw_ready = false;
 #pragma unroll 1
   for (int d = 0; d < MAXD; ++d) {
     if (d >= A.dnum) break;
     const u64* kd0 = K0 + (long long)(2 * d) * full * N;
     const u64* kd1 = kd0 + (long long)full * N;
+    if (kRiPrefetch && d != down) {
+      prefetch(next_digit(d + 1), slot ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // twiddles + this digit's tile
+      __syncthreads();
+      tw_ready = true;
+    }
     if (d == down) {  // own limb: already in NTT form (residues)
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
@@ -132,9 +176,10 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, HX_ROWINNER_MINB) ks_row
     int eb[16 >> WW], jb[16 >> WW];                                                         \
     group_index<true, S, OB, WW>(t, g0, A.logn, tile, eb, jb);                              \
     if (gi == 0) {                                                                          \
+      const u64* pb = pbuf + slot * TILE;                                                   \
       _Pragma("unroll") for (int r = 0; r < 16; ++r) {                                      \
         const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << g0);                         \
-        x[r] = __ldcs(base + e);                                                            \
+        x[r] = kRiPrefetch ? pb[e] : __ldcs(base + e);                                      \
       }                                                                                     \
       if (!tw_ready) {                                                                      \
         asm volatile("cp.async.wait_all;\n" ::: "memory");                                 \
@@ -171,6 +216,7 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, HX_ROWINNER_MINB) ks_row
       else if (W == 1) HX_RI_GROUP(1)
 #undef HX_RI_GROUP
     }
+    slot ^= 1;
   }
   if (!tw_ready) asm volatile("cp.async.wait_all;\n" ::: "memory");
   u64* ub = A.u + (long long)b * 2 * ext * N + (long long)j * N + tofs;
