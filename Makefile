@@ -11,7 +11,7 @@ CXXFLAGS  := -std=c++20 -O2 -fPIC -Wall -Wextra -Wno-unused-parameter -Iinclude 
 PKG       := paper_2512_11135_b200
 CU_DIR    := $(PKG)/csrc/cuda
 HOST_DIR  := $(PKG)/csrc/host
-CU_SRCS   := $(CU_DIR)/hx_ntt.cu $(CU_DIR)/hx_ops.cu $(CU_DIR)/hx_bsgs.cu $(CU_DIR)/hx_bsgs_tc.cu $(CU_DIR)/hx_encode.cu
+CU_SRCS   := $(CU_DIR)/hx_ntt.cu $(CU_DIR)/hx_ops.cu $(CU_DIR)/hx_bsgs.cu $(CU_DIR)/hx_bsgs_tc.cu $(CU_DIR)/hx_bsgs_p40.cu $(CU_DIR)/hx_encode.cu
 CU_HDRS   := $(wildcard $(CU_DIR)/*.cuh) $(CU_DIR)/hx_internal.h include/hx_b200.h
 HOST_SRCS := $(HOST_DIR)/params.cpp $(HOST_DIR)/encoder.cpp $(HOST_DIR)/gpu_backend.cpp \
              $(HOST_DIR)/packing.cpp $(HOST_DIR)/linalg.cpp $(HOST_DIR)/helix_c.cpp $(HOST_DIR)/lattice.cpp \

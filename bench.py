@@ -782,7 +782,19 @@ def main():
                     "achieved": mac_bytes / mac_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                     "frac": mac_bytes / mac_s / 1e9 / hbm_peak, "algorithmic_bytes_per_launch": mac_bytes,
                     "peak_kind": peak_kind}
-    del baby, diags, inner
+    # the same block through the packed single-token MAC (5-byte words of the
+    # 40-bit limbs streamed by cp.async.bulk; q_0 on the integer MAC)
+    pk = ctx.bsgs_p40_pack(diags, nq, mn1, mn2, nq)
+    p40_s = time_loop(torch, lambda: ctx.bsgs_mac_p40(inner, 2 * nq * N, baby, pk, diags, nq, mn1, mn2, nq,
+                                                      stream=stream), 5, 2, stream) / 5
+    n40 = sum(1 for q in chain if q < (1 << 40))
+    p40_bytes = (mn1 * mn2 * (n40 * 5 + (nq - n40) * 8) + (2 * mn1 + 2 * mn2) * nq * 8) * N
+    roofline_mac["p40"] = {"kernel": "bsgs_mac_p40_kernel (+ bsgs_mac_int_kernel for q_0), same block",
+                           "ms": p40_s * 1e3, "achieved": p40_bytes / p40_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                           "frac": p40_bytes / p40_s / 1e9 / hbm_peak, "algorithmic_bytes_per_launch": p40_bytes,
+                           "u64_equivalent_GBps": mac_bytes / p40_s / 1e9,
+                           "speedup_vs_u64_mac": mac_s / p40_s}
+    del baby, diags, inner, pk
     if not args.no_extras:
         # HMult + relin over the batch
         rlk = make_key(torch, ctx, gen, chain, special, 0, dev)

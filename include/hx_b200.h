@@ -212,6 +212,19 @@ int hx_bsgs_mac_sparse(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, lo
                        const uint64_t* baby, long long baby_tstride, const int* group_ptr, const int* ks,
                        const uint64_t* const* diags, int n1, int n2, int n_q, int tokens, void* stream);
 
+/* Packed single-token BSGS MAC (hx_bsgs_p40.cu): the diagonals of one block
+ * (n2 giant rows, n1 baby steps, diagonal (j, k) at diags + (j diag_jstride +
+ * k) diag_limbs N words, diag_jstride 0 = n1) are packed once into 5-byte words
+ * for the limbs with q < 2^40 (hx_bsgs_p40_bytes bytes, -1 = unsupported
+ * shape or no such limb); the MAC streams them with bulk copies and runs the
+ * remaining (wide, e.g. 60-bit q_0) limbs on the integer MAC over the u64
+ * words at `diags`.  n1 in {32, 64}.  Same words as hx_bsgs_mac_ex. */
+long long hx_bsgs_p40_bytes(hx_ctx* ctx, int n1, int n2, int n_q);
+int hx_bsgs_p40_pack(hx_ctx* ctx, void* packed, const uint64_t* diags, int diag_limbs, int n1, int n2,
+                     int diag_jstride, int n_q, void* stream);
+int hx_bsgs_mac_p40(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, const uint64_t* baby, const void* packed,
+                    const uint64_t* diags, int diag_limbs, int n1, int n2, int diag_jstride, int n_q, void* stream);
+
 /* Tensor-core BSGS MAC (tcgen05.mma kind::i8 on byte-sliced words, TMEM
  * accumulators, bulk-copy-streamed diagonals; hx_bsgs_tc.cu).  The diagonals of
  * up to 128 rows r = b * n2 + j (row block b, giant step j) are packed once into

@@ -134,6 +134,18 @@ u64 find_psi(u64 q, u64 n) {
   throw HxError(HX_ERR_INVALID, "no primitive 2N-th root");
 }
 
+// An allocation that failed may succeed once the stream-ordered pool has
+// returned its cached (freed) blocks to the device: sync, trim, retry once.
+void trim_pool() {
+  cudaGetLastError();
+  cuda_ok(cudaDeviceSynchronize(), "sync");
+  int dev = 0;
+  cudaMemPool_t pool;
+  cuda_ok(cudaGetDevice(&dev), "device");
+  cuda_ok(cudaDeviceGetDefaultMemPool(&pool, dev), "mem pool");
+  cuda_ok(cudaMemPoolTrimTo(pool, 0), "mem pool trim");
+}
+
 // ---- stream-ordered scratch buffer ----
 // Scoped device temporary: from the context arena (HxArena, hx_internal.h)
 // when a context is given, else from the stream-ordered pool.
@@ -165,7 +177,11 @@ struct DBuf {
           cuda_ok(cudaFree(A.base), "cudaFree(arena)");
         }
         A.base = nullptr;
-        cuda_ok(cudaMalloc((void**)&A.base, A.high), "cudaMalloc(arena)");
+        if (cudaMalloc((void**)&A.base, A.high) != cudaSuccess) {
+          A.base = nullptr;
+          trim_pool();
+          cuda_ok(cudaMalloc((void**)&A.base, A.high), "cudaMalloc(arena)");
+        }
         A.cap = A.high;
         if (getenv("HX_ALLOC_TRACE")) fprintf(stderr, "[hx] arena regrown to %.2f GB\n", A.cap * 1e-9);
       }
@@ -179,7 +195,11 @@ struct DBuf {
       }
       A.top += bytes;  // keeps the LIFO accounting; memory from the pool
     }
-    cuda_ok(cudaMallocAsync((void**)&p, words * 8, st), "cudaMallocAsync");
+    if (cudaMallocAsync((void**)&p, words * 8, st) != cudaSuccess) {
+      p = nullptr;
+      trim_pool();
+      cuda_ok(cudaMallocAsync((void**)&p, words * 8, st), "cudaMallocAsync");
+    }
   }
   ~DBuf() {
     if (!p) return;
@@ -1778,6 +1798,102 @@ int hx_bsgs_mac_tokens(hx_ctx* c, uint64_t* inner, long long inner_jstride, long
     const int* lists = c->d_maclimbs + (size_t)n_q * 2 * c->n_chain;
     hx::launch_bsgs_mac(A, c->N(), S(s), lists, c->mac_nf64[n_q], lists + c->n_chain, c->mac_nint[n_q]);
     launched(c, "bsgs_mac_kernel", 2);
+  });
+}
+
+// ---- P40: 5-byte packed diagonals (limbs with q < 2^40), hx_bsgs_p40.cu
+namespace {
+struct P40Plan {
+  std::vector<int> p40, wide;  // limbs of 0..n_q-1 with q < 2^40 / the rest
+};
+P40Plan p40_plan(const hx_ctx* c, int n_q) {
+  P40Plan P;
+  for (int i = 0; i < n_q; ++i) (c->primes[i] < (1ull << 40) && c->f64[i] ? P.p40 : P.wide).push_back(i);
+  return P;
+}
+bool p40_shape_ok(const hx_ctx* c, int n1, int n2, int n_q) {
+  return c && (n1 == 32 || n1 == 64) && n2 >= 1 && n_q >= 1 && n_q <= c->n_chain && c->N() >= 32;
+}
+}  // namespace
+
+long long hx_bsgs_p40_bytes(hx_ctx* c, int n1, int n2, int n_q) {
+  if (!p40_shape_ok(c, n1, n2, n_q)) return -1;
+  const P40Plan P = p40_plan(c, n_q);
+  if (P.p40.empty()) return -1;
+  return (long long)P.p40.size() * c->N() * n2 * n1 * 5;
+}
+
+int hx_bsgs_p40_pack(hx_ctx* c, void* packed, const uint64_t* diags, int diag_limbs, int n1, int n2,
+                     int diag_jstride, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    HX_REQUIRE(p40_shape_ok(c, n1, n2, n_q) && diag_limbs >= n_q, "bsgs_p40_pack: bad shape (n1 in {32, 64})");
+    HX_REQUIRE(packed && diags, "bsgs_p40_pack: null buffer");
+    const int dj = diag_jstride ? diag_jstride : n1;
+    HX_REQUIRE(dj >= n1, "bsgs_p40_pack: diag_jstride < n1");
+    const P40Plan P = p40_plan(c, n_q);
+    HX_REQUIRE(!P.p40.empty(), "bsgs_p40_pack: no limb with q < 2^40");
+    DBuf tab((P.p40.size() * sizeof(int) + 7) / 8, S(s), c);
+    cuda_ok(cudaMemcpyAsync(tab.p, P.p40.data(), P.p40.size() * sizeof(int), cudaMemcpyHostToDevice, S(s)), "h2d");
+    hx::launch_p40_pack(static_cast<unsigned char*>(packed), (const u64*)diags, (long long)diag_limbs * c->N(),
+                        reinterpret_cast<const int*>(tab.p), (int)P.p40.size(), n1, n2, dj, c->logn, S(s));
+    launched(c, "p40_pack_kernel");
+  });
+}
+
+int hx_bsgs_mac_p40(hx_ctx* c, uint64_t* inner, long long inner_jstride, const uint64_t* baby, const void* packed,
+                    const uint64_t* diags, int diag_limbs, int n1, int n2, int diag_jstride, int n_q, void* s) {
+  return guarded([&] {
+    check_ctx(c);
+    check_nq(c, n_q);
+    HX_REQUIRE(p40_shape_ok(c, n1, n2, n_q) && diag_limbs >= n_q, "bsgs_mac_p40: bad shape (n1 in {32, 64})");
+    HX_REQUIRE(inner && baby && packed && diags, "bsgs_mac_p40: null buffer");
+    const int dj = diag_jstride ? diag_jstride : n1;
+    HX_REQUIRE(dj >= n1, "bsgs_mac_p40: diag_jstride < n1");
+    const P40Plan P = p40_plan(c, n_q);
+    HX_REQUIRE(!P.p40.empty(), "bsgs_mac_p40: no limb with q < 2^40");
+    std::vector<int> lists(P.p40);
+    lists.insert(lists.end(), P.wide.begin(), P.wide.end());
+    DBuf tab((lists.size() * sizeof(int) + 7) / 8, S(s), c);
+    cuda_ok(cudaMemcpyAsync(tab.p, lists.data(), lists.size() * sizeof(int), cudaMemcpyHostToDevice, S(s)), "h2d");
+    const int* dl = reinterpret_cast<const int*>(tab.p);
+    hx::P40Args A;
+    A.inner = (u64*)inner;
+    A.baby = (const u64*)baby;
+    A.packed = static_cast<const unsigned char*>(packed);
+    A.limbs = dl;
+    A.pc = c->d_pc;
+    A.out_jstride = inner_jstride;
+    A.n1 = n1;
+    A.n2 = n2;
+    A.n_q = n_q;
+    A.logn = c->logn;
+    A.stages = hx::p40_stages(n1);
+    {
+      hx::KTimer kt(c, "bsgs_mac_p40_kernel", S(s));
+      hx::launch_bsgs_mac_p40(A, (int)P.p40.size(), S(s));
+    }
+    launched(c, "bsgs_mac_p40_kernel");
+    if (!P.wide.empty()) {  // the wide limbs (60-bit q_0): 128-bit integer MAC over the u64 words
+      hx::MacArgs M;
+      M.inner = (u64*)inner;
+      M.baby = (const u64*)baby;
+      M.diags = (const u64*)diags;
+      M.pc = c->d_pc;
+      M.n1 = n1;
+      M.n2 = n2;
+      M.n_q = n_q;
+      M.logn = c->logn;
+      M.diag_stride = (long long)diag_limbs * c->N();
+      M.out_jstride = inner_jstride;
+      M.limbs = nullptr;
+      M.tokens = 1;
+      M.baby_tstride = 0;
+      M.inner_tstride = 0;
+      M.diag_jstride = dj;
+      hx::launch_bsgs_mac(M, c->N(), S(s), nullptr, 0, dl + P.p40.size(), (int)P.wide.size());
+      launched(c, "bsgs_mac_int_kernel");
+    }
   });
 }
 

@@ -68,6 +68,24 @@ void launch_sum(const SumArgs& A, int polys, long long N, cudaStream_t s);
 void launch_bsgs_mac(const MacArgs& A, long long N, cudaStream_t s, const int* d_f64_limbs, int n_f64,
                      const int* d_int_limbs, int n_int);
 
+// ------------------------------------------------- packed (5-byte) BSGS MAC
+// (hx_bsgs_p40.cu): limbs with q < 2^40 of one contiguous block of
+// diagonals, packed once into the P40 layout, streamed by cp.async.bulk
+constexpr int kP40MaxStages = 8;
+struct P40Args {
+  u64* inner;                   // inner_j at inner + j out_jstride ([2][n_q][N])
+  const u64* baby;              // [n1][2][n_q][N]
+  const unsigned char* packed;  // P40 layout [n_p40][N / 32][n2][5 n1 32 bytes]
+  const int* limbs;             // P40 limb list (p -> chain limb i)
+  const PrimeConst* pc;
+  long long out_jstride;
+  int n1, n2, n_q, logn, stages;
+};
+int p40_stages(int n1);
+void launch_bsgs_mac_p40(const P40Args& A, int n_p40, cudaStream_t s);
+void launch_p40_pack(unsigned char* dst, const u64* diags, long long diag_stride, const int* limbs, int n_p40,
+                     int n1, int n2, int dj, int logn, cudaStream_t s);
+
 // ------------------------------------------------- tensor-core BSGS MAC
 // (hx_bsgs_tc.cu): the TC-class limbs (q < 2^40) of up to 128 rows r = (block,
 // giant step) per launch, T in {1, 2, 4, 8} tokens

@@ -57,7 +57,20 @@ std::uint64_t GpuLatticeBackend::next_u64() {
 
 // ------------------------------------------------------------- DeviceBuffer
 DeviceBuffer::DeviceBuffer(std::size_t w) : words(w) {
-  if (w) cuda_ck(cudaMallocAsync((void**)&ptr, w * 8, nullptr), "cudaMallocAsync");
+  if (!w) return;
+  if (cudaMallocAsync((void**)&ptr, w * 8, nullptr) == cudaSuccess) return;
+  // the pool may hold freed blocks too small for this request (e.g. the
+  // packed forms of a matrix swapped for one another): release them to the
+  // device and try once more
+  cudaGetLastError();
+  ptr = nullptr;
+  cuda_ck(cudaDeviceSynchronize(), "sync");
+  int dev = 0;
+  cudaMemPool_t pool;
+  cuda_ck(cudaGetDevice(&dev), "device");
+  cuda_ck(cudaDeviceGetDefaultMemPool(&pool, dev), "mem pool");
+  cuda_ck(cudaMemPoolTrimTo(pool, 0), "mem pool trim");
+  cuda_ck(cudaMallocAsync((void**)&ptr, w * 8, nullptr), "cudaMallocAsync");
 }
 DeviceBuffer::~DeviceBuffer() {
   if (ptr) cudaFreeAsync(ptr, nullptr);
@@ -697,13 +710,49 @@ static std::shared_ptr<DeviceBuffer> tc_pack(hx_ctx* ctx, const std::shared_ptr<
   mix((u64)n1);
   mix((u64)nqv);
   for (const u64* q : ptrs) mix(q ? (u64)(q - buf->ptr) : ~0ull);
+  sig &= ~1ull;  // low bit 0: tensor-core tiles, 1: P40 packs
   std::lock_guard<std::mutex> g(buf->derived_mu);
   for (const auto& e : buf->derived)
     if (e.first == sig) return e.second;
+  // one packed form per matrix at a time (the P40 packs of single-token
+  // matvecs go when the token batches need tiles): u64 + one pack fits HBM
+  std::erase_if(buf->derived, [](const auto& e) { return (e.first & 1) != 0; });
   const long long bytes = hx_bsgs_tc_bytes(ctx, rows, n1, nqv);
   if (bytes < 0) throw std::invalid_argument("bsgs: tensor-core shape");
   auto pk = dev(((std::size_t)bytes + 7) / 8);
   ck(hx_bsgs_tc_pack(ctx, pk->ptr, ptrs.data(), rows, n1, nqv, nullptr), "bsgs_tc_pack");
+  buf->derived.emplace_back(sig, pk);
+  return pk;
+}
+
+// 5-byte packed diagonals (hx_bsgs_p40_pack) of n2 giant groups x n1 baby
+// steps starting at `diags` (group stride dj diagonals) inside `buf`, made
+// once and attached to the buffer; null when the shape / primes do not allow it
+static bool p40_mac_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("HX_MAC_P40");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+static std::shared_ptr<DeviceBuffer> p40_pack(hx_ctx* ctx, const std::shared_ptr<DeviceBuffer>& buf,
+                                              const u64* diags, int n1, int n2, int dj, int nqv) {
+  if (!p40_mac_enabled()) return nullptr;
+  const long long bytes = hx_bsgs_p40_bytes(ctx, n1, n2, nqv);
+  if (bytes < 0) return nullptr;
+  u64 sig = 0x9e3779b97f4a7c15ull;
+  const u64 key[] = {(u64)(diags - buf->ptr), (u64)n1, (u64)n2, (u64)dj, (u64)nqv, 0x7034300000000000ull};
+  for (u64 v : key) {
+    sig ^= v;
+    sig *= 0x100000001b3ull;
+  }
+  sig |= 1ull;
+  std::lock_guard<std::mutex> g(buf->derived_mu);
+  for (const auto& e : buf->derived)
+    if (e.first == sig) return e.second;
+  std::erase_if(buf->derived, [](const auto& e) { return (e.first & 1) == 0; });  // tensor-core tiles
+  auto pk = dev(((std::size_t)bytes + 7) / 8);
+  ck(hx_bsgs_p40_pack(ctx, pk->ptr, diags, nqv, n1, n2, dj, nqv, nullptr), "bsgs_p40_pack");
   buf->derived.emplace_back(sig, pk);
   return pk;
 }
@@ -785,8 +834,11 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
     }
     ok = ok && src && 2 * nlive >= (std::size_t)blocks * d;  // sparse matrices: the index-list MAC
     // one token over few rows: the streaming CUDA-core MAC is as fast (measured:
-    // 32 rows x n1 = 32 at T = 1 is 16.1 vs 12.8 ms per FFN W1 stacked matvec)
-    ok = ok && (T >= 2 || blocks * n2 >= 96);
+    // 32 rows x n1 = 32 at T = 1 is 16.1 vs 12.8 ms per FFN W1 stacked matvec);
+    // one token over dense blocks: the packed (P40) streaming MAC reads the same
+    // 5-byte words at a higher rate
+    const bool p40_ok = p40_mac_enabled() && n1 <= 64 && hx_bsgs_p40_bytes(ctx_, n1, n2, nqv) > 0;
+    ok = ok && (T >= 2 || (blocks * n2 >= 96 && !p40_ok));
     if (ok) {
       const int bpt = std::max(1, 128 / n2);
       for (int b0 = 0; b0 < blocks; b0 += bpt) {
@@ -848,7 +900,13 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       bool uniform = tok_mac;
       const long long bstride = T > 1 ? (long long)(baby_ptr[1] - baby_ptr[0]) : 0;
       for (int t = 1; t < T && uniform; ++t) uniform = (long long)(baby_ptr[t] - baby_ptr[t - 1]) == bstride;
-      if (uniform) {
+      std::shared_ptr<DeviceBuffer> pk;
+      if (T == 1 && n1 <= 64) pk = p40_pack(ctx_, p0->buf, p0->data(), n1, n2, n1, nqv);
+      if (pk) {
+        ck(hx_bsgs_mac_p40(ctx_, inner->ptr + (std::size_t)b * ctw, (long long)jstride, baby_ptr[0], pk->ptr,
+                           p0->data(), nqv, n1, n2, n1, nqv, nullptr),
+           "bsgs_mac_p40");
+      } else if (uniform) {
         mac_chunked(ctx_, inner->ptr, inner_polys, (std::size_t)b * ctw, (long long)jstride, (long long)(blocks * ctw),
                     baby_ptr[0], bstride, ctw, p0->data(), ptw, nqv, n1, n2, n1, T);
       } else {
@@ -904,7 +962,16 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
           int j1 = j + 1;
           while (j1 < n2 && dense_at(j1) && dp[gptr[j1]] == dp[gptr[j1 - 1]] + (std::size_t)n1 * ptw) ++j1;
           const std::size_t off = (std::size_t)j * jstride + (std::size_t)b * ctw;
-          if (uniform) {
+          std::shared_ptr<DeviceBuffer> pk;
+          if (T == 1 && n1 <= 64) {
+            const Plaintext& p0 = D[(std::size_t)j * n1];
+            pk = p40_pack(ctx_, payload(p0).buf, dp[gptr[j]], n1, j1 - j, n1, nqv);
+          }
+          if (pk) {
+            ck(hx_bsgs_mac_p40(ctx_, inner->ptr + off, (long long)jstride, baby_ptr[0], pk->ptr, dp[gptr[j]], nqv, n1,
+                               j1 - j, n1, nqv, nullptr),
+               "bsgs_mac_p40");
+          } else if (uniform) {
             mac_chunked(ctx_, inner->ptr, inner_polys, off, (long long)jstride, (long long)(blocks * ctw), baby_ptr[0],
                         bstride, ctw, dp[gptr[j]], ptw, nqv, n1, j1 - j, n1, T);
           } else {

@@ -289,6 +289,33 @@ class Context:
         _check(L.hx_bsgs_mac_tc(self.h, _p(inner), inner_jstride, inner_bstride, inner_tstride, _p(baby), baby_tstride,
                                 _p(packed), blocks, n2, n1, n_q, tokens, _stream(stream)), "hx_bsgs_mac_tc")
 
+    def bsgs_p40_pack(self, diags, diag_limbs, n1, n2, n_q, diag_jstride=0, stream=None):
+        """5-byte packed diagonals (uint8 tensor) of one block for hx_bsgs_mac_p40"""
+        import torch
+
+        L = self.L
+        L.hx_bsgs_p40_bytes.restype = C.c_longlong
+        L.hx_bsgs_p40_bytes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int]
+        nb = L.hx_bsgs_p40_bytes(self.h, n1, n2, n_q)
+        if nb < 0:
+            raise HxError(f"hx_bsgs_p40_bytes: unsupported shape n1={n1} n2={n2} n_q={n_q}")
+        buf = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        L.hx_bsgs_p40_pack.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_int, C.c_void_p]
+        L.hx_bsgs_p40_pack.restype = C.c_int
+        _check(L.hx_bsgs_p40_pack(self.h, _p(buf), _p(diags), diag_limbs, n1, n2, diag_jstride, n_q,
+                                  _stream(stream)), "hx_bsgs_p40_pack")
+        return buf
+
+    def bsgs_mac_p40(self, inner, inner_jstride, baby, packed, diags, diag_limbs, n1, n2, n_q, diag_jstride=0,
+                     stream=None):
+        L = self.L
+        L.hx_bsgs_mac_p40.argtypes = [C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p]
+        L.hx_bsgs_mac_p40.restype = C.c_int
+        _check(L.hx_bsgs_mac_p40(self.h, _p(inner), inner_jstride, _p(baby), _p(packed), _p(diags), diag_limbs, n1,
+                                 n2, diag_jstride, n_q, _stream(stream)), "hx_bsgs_mac_p40")
+
     def bsgs_mac_sparse(self, inner, inner_jstride, baby, group_ptr, ks, diag_ptrs, n1, n2, n_q, tokens=1,
                         inner_tstride=0, baby_tstride=0, stream=None):
         """index-list MAC: group j = entries [group_ptr[j], group_ptr[j+1]), entry e

@@ -40,6 +40,8 @@ def reduce_partials(hctx: int, words, n_cts: int, n_q: int, allreduce, n_special
     hctx is the hx_ctx* of the backend (Backend.device_context())."""
     from .hx import _check, lib
 
+    if world > 1 and not primes:
+        raise ValueError("reduce_partials: pass the context primes so the exact-sum bound can be checked")
     if primes:
         check_exact_sum(world, primes)
     allreduce(words)
