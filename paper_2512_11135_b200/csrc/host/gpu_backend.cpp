@@ -833,12 +833,10 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       ++nlive;
     }
     ok = ok && src && 2 * nlive >= (std::size_t)blocks * d;  // sparse matrices: the index-list MAC
-    // one token over few rows: the streaming CUDA-core MAC is as fast (measured:
-    // 32 rows x n1 = 32 at T = 1 is 16.1 vs 12.8 ms per FFN W1 stacked matvec);
-    // one token over dense blocks: the packed (P40) streaming MAC reads the same
-    // 5-byte words at a higher rate
-    const bool p40_ok = p40_mac_enabled() && n1 <= 64 && hx_bsgs_p40_bytes(ctx_, n1, n2, nqv) > 0;
-    ok = ok && (T >= 2 || (blocks * n2 >= 96 && !p40_ok));
+    // one token over few rows: the streaming CUDA-core MACs are faster (measured:
+    // 32 rows x n1 = 32 at T = 1 is 16.1 vs 12.8 ms per FFN W1 stacked matvec;
+    // at 96 rows the tensor cores win, 7.3 ms vs 3 x 2.7 ms of the P40 MAC)
+    ok = ok && (T >= 2 || blocks * n2 >= 96);
     if (ok) {
       const int bpt = std::max(1, 128 / n2);
       for (int b0 = 0; b0 < blocks; b0 += bpt) {
