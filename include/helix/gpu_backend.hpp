@@ -33,6 +33,11 @@ namespace helix {
 struct DeviceBuffer {
   std::uint64_t* ptr = nullptr;
   std::size_t words = 0;
+  // allocated and freed in the order of the CUDA stream of the backend whose
+  // operation created it (null: the legacy default stream); the reference
+  // keeps that stream alive while any of its buffers lives
+  void* stream = nullptr;
+  std::shared_ptr<void> stream_ref;
   // derived device representations of the (immutable) words, e.g. the
   // tensor-core operand tiles of a BSGS matrix's diagonals (hx_bsgs_tc_pack),
   // keyed by a signature of the shape and the diagonal offsets; they live
@@ -176,6 +181,16 @@ class GpuLatticeBackend final : public SlotBackend {
   // device encoder (hx_encode): n messages -> NTT-domain plaintext words at out
   void encode_device(const std::vector<const std::vector<double>*>& msgs, int level, const Scale& scale,
                      std::uint64_t* out);
+
+  // Concurrency model: every public operation holds mu_
+  // (operations on one backend serialise; handles stay value-like) and
+  // issues its work on this backend's own CUDA stream (blocking w.r.t. the
+  // legacy default stream, so callers that use it stay ordered), so
+  // operations of distinct backends run concurrently on the device
+  struct DeviceScope;
+  friend struct DeviceScope;
+  mutable std::recursive_mutex mu_;
+  std::shared_ptr<void> stream_;
 
   CkksParams params_;
   CkksEncoder enc_;

@@ -55,10 +55,36 @@ std::uint64_t GpuLatticeBackend::next_u64() {
   return r;
 }
 
+// ------------------------------------------------- backend stream / lock
+namespace {
+// the stream (and its owner) of the backend operation running on this thread
+thread_local cudaStream_t tl_stream = nullptr;
+thread_local const std::shared_ptr<void>* tl_owner = nullptr;
+cudaStream_t cur() { return tl_stream; }
+}  // namespace
+
+struct GpuLatticeBackend::DeviceScope {
+  std::unique_lock<std::recursive_mutex> lk;
+  cudaStream_t prev_s;
+  const std::shared_ptr<void>* prev_o;
+  explicit DeviceScope(const GpuLatticeBackend& b) : lk(b.mu_), prev_s(tl_stream), prev_o(tl_owner) {
+    tl_stream = static_cast<cudaStream_t>(b.stream_.get());
+    tl_owner = &b.stream_;
+  }
+  ~DeviceScope() {
+    tl_stream = prev_s;
+    tl_owner = prev_o;
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+};
+
 // ------------------------------------------------------------- DeviceBuffer
 DeviceBuffer::DeviceBuffer(std::size_t w) : words(w) {
   if (!w) return;
-  if (cudaMallocAsync((void**)&ptr, w * 8, nullptr) == cudaSuccess) return;
+  stream = cur();
+  if (tl_owner) stream_ref = *tl_owner;
+  if (cudaMallocAsync((void**)&ptr, w * 8, cur()) == cudaSuccess) return;
   // the pool may hold freed blocks too small for this request (e.g. the
   // packed forms of a matrix swapped for one another): release them to the
   // device and try once more
@@ -70,10 +96,10 @@ DeviceBuffer::DeviceBuffer(std::size_t w) : words(w) {
   cuda_ck(cudaGetDevice(&dev), "device");
   cuda_ck(cudaDeviceGetDefaultMemPool(&pool, dev), "mem pool");
   cuda_ck(cudaMemPoolTrimTo(pool, 0), "mem pool trim");
-  cuda_ck(cudaMallocAsync((void**)&ptr, w * 8, nullptr), "cudaMallocAsync");
+  cuda_ck(cudaMallocAsync((void**)&ptr, w * 8, cur()), "cudaMallocAsync");
 }
 DeviceBuffer::~DeviceBuffer() {
-  if (ptr) cudaFreeAsync(ptr, nullptr);
+  if (ptr) cudaFreeAsync(ptr, static_cast<cudaStream_t>(stream));
 }
 
 static std::shared_ptr<DeviceBuffer> dev(std::size_t words) {
@@ -94,6 +120,13 @@ GpuLatticeBackend::GpuLatticeBackend(CkksParams params, std::uint64_t seed)
                        params_.special_primes.data(), (int)params_.special_primes.size(),
                        params_.digit_size);
   if (!ctx_) throw std::runtime_error(std::string("hx_ctx_create: ") + hx_last_error());
+  cudaStream_t st = nullptr;
+  cuda_ck(cudaStreamCreate(&st), "backend stream");
+  stream_ = std::shared_ptr<void>(st, [](void* p) {
+    cudaStreamSynchronize(static_cast<cudaStream_t>(p));
+    cudaStreamDestroy(static_cast<cudaStream_t>(p));
+  });
+  DeviceScope ds(*this);
   u64 sm = seed;
   for (auto& w : rng_) w = splitmix(sm);
   const std::size_t N = params_.ring_degree;
@@ -107,22 +140,23 @@ GpuLatticeBackend::GpuLatticeBackend(CkksParams params, std::uint64_t seed)
     c = (std::int64_t)r - 1;
   }
   DeviceBuffer sv(N);
-  cuda_ck(cudaMemcpyAsync(sv.ptr, s.data(), N * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
+  cuda_ck(cudaMemcpyAsync(sv.ptr, s.data(), N * 8, cudaMemcpyHostToDevice, cur()), "h2d");
   s_full_ = dev((std::size_t)(nc + K) * N);
-  ck(hx_from_i64(ctx_, s_full_->ptr, (const int64_t*)sv.ptr, 1, nc, K, nullptr), "from_i64");
-  ck(hx_ntt_fwd(ctx_, s_full_->ptr, 1, nc, K, nullptr), "ntt");
+  ck(hx_from_i64(ctx_, s_full_->ptr, (const int64_t*)sv.ptr, 1, nc, K, cur()), "from_i64");
+  ck(hx_ntt_fwd(ctx_, s_full_->ptr, 1, nc, K, cur()), "ntt");
   // relinearisation key (s' = s^2)
   auto s2 = dev((std::size_t)(nc + K) * N);
-  ck(hx_mul(ctx_, s2->ptr, s_full_->ptr, s_full_->ptr, 1, nc, K, nullptr), "mul");
+  ck(hx_mul(ctx_, s2->ptr, s_full_->ptr, s_full_->ptr, 1, nc, K, cur()), "mul");
   rlk_ = make_key(s2, 0);
-  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+  cuda_ck(cudaStreamSynchronize(cur()), "sync");
 }
 
 GpuLatticeBackend::~GpuLatticeBackend() {
   rot_keys_.clear();
   rlk_.reset();
   s_full_.reset();
-  cudaStreamSynchronize(nullptr);
+  matmul_masks_.clear();
+  cudaStreamSynchronize(static_cast<cudaStream_t>(stream_.get()));
   hx_encoder_destroy(henc_);
   hx_ctx_destroy(ctx_);  // forgets the compressed keys with the context
 }
@@ -168,36 +202,37 @@ std::shared_ptr<DeviceBuffer> GpuLatticeBackend::make_key(const std::shared_ptr<
   const std::size_t N = params_.ring_degree;
   DeviceBuffer de((std::size_t)dn * N);
   const std::uint64_t seed = next_u64();
-  ck(hx_sample_cbd(ctx_, (int64_t*)de.ptr, (long long)dn * N, next_u64(), nullptr), "sample_cbd");
+  ck(hx_sample_cbd(ctx_, (int64_t*)de.ptr, (long long)dn * N, next_u64(), cur()), "sample_cbd");
   std::shared_ptr<DeviceBuffer> key;
   if (params_.compress_keys) {
     key = dev(hx_ckey_words(ctx_));
     if (g == 0)
-      ck(hx_keygen_ksk_c(ctx_, key->ptr, s_full_->ptr, sp->ptr, seed, (const int64_t*)de.ptr, nullptr), "keygen");
+      ck(hx_keygen_ksk_c(ctx_, key->ptr, s_full_->ptr, sp->ptr, seed, (const int64_t*)de.ptr, cur()), "keygen");
     else
-      ck(hx_keygen_rotation_c(ctx_, key->ptr, s_full_->ptr, g, seed, (const int64_t*)de.ptr, nullptr),
+      ck(hx_keygen_rotation_c(ctx_, key->ptr, s_full_->ptr, g, seed, (const int64_t*)de.ptr, cur()),
          "keygen_rotation");
   } else {  // full keys: the same words, the uniform halves materialised
     const int K = (int)params_.special_primes.size();
     DeviceBuffer da((std::size_t)dn * (nc + K) * N);
-    ck(hx_sample_uniform(ctx_, da.ptr, nc, K, dn, seed, nullptr), "sample_uniform");
+    ck(hx_sample_uniform(ctx_, da.ptr, nc, K, dn, seed, cur()), "sample_uniform");
     key = dev(hx_key_words(ctx_));
     if (g == 0)
-      ck(hx_keygen_ksk(ctx_, key->ptr, s_full_->ptr, sp->ptr, da.ptr, (const int64_t*)de.ptr, nullptr), "keygen");
+      ck(hx_keygen_ksk(ctx_, key->ptr, s_full_->ptr, sp->ptr, da.ptr, (const int64_t*)de.ptr, cur()), "keygen");
     else
-      ck(hx_keygen_rotation(ctx_, key->ptr, s_full_->ptr, g, da.ptr, (const int64_t*)de.ptr, nullptr),
+      ck(hx_keygen_rotation(ctx_, key->ptr, s_full_->ptr, g, da.ptr, (const int64_t*)de.ptr, cur()),
          "keygen_rotation");
   }
-  cuda_ck(cudaStreamSynchronize(nullptr), "sync");  // da / de die here
+  cuda_ck(cudaStreamSynchronize(cur()), "sync");  // da / de die here
   return key;
 }
 
 void GpuLatticeBackend::expand_key(const std::uint64_t* key, std::uint64_t* full) const {
+  DeviceScope ds(*this);
   if (params_.compress_keys)
-    ck(hx_key_expand(ctx_, full, key, nullptr), "key_expand");
+    ck(hx_key_expand(ctx_, full, key, cur()), "key_expand");
   else
-    cuda_ck(cudaMemcpyAsync(full, key, hx_key_words(ctx_) * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
-  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+    cuda_ck(cudaMemcpyAsync(full, key, hx_key_words(ctx_) * 8, cudaMemcpyDeviceToDevice, cur()), "d2d");
+  cuda_ck(cudaStreamSynchronize(cur()), "sync");
 }
 
 std::uint64_t GpuLatticeBackend::galois(std::int64_t r) const {
@@ -211,6 +246,7 @@ std::uint64_t GpuLatticeBackend::galois(std::int64_t r) const {
 }
 
 void GpuLatticeBackend::generate_rotation_keys(std::span<const std::int64_t> amounts) {
+  DeviceScope ds(*this);
   const auto n = (std::int64_t)slots();
   for (std::int64_t a : amounts) {
     const std::int64_t r = detail::reduce_amount(a, n);
@@ -221,6 +257,7 @@ void GpuLatticeBackend::generate_rotation_keys(std::span<const std::int64_t> amo
 }
 
 const std::uint64_t* GpuLatticeBackend::rotation_key(std::int64_t r) const {
+  DeviceScope ds(*this);
   auto it = rot_keys_.find(r);
   return it == rot_keys_.end() ? nullptr : it->second->ptr;
 }
@@ -282,17 +319,18 @@ void GpuLatticeBackend::encode_device(const std::vector<const std::vector<double
       std::memcpy(host.data() + i * width, msgs[c0 + i]->data(), msgs[c0 + i]->size() * 8);
     cuda_ck(cudaMemcpy(dm.ptr, host.data(), k * width * 8, cudaMemcpyHostToDevice), "h2d");
     const int rc = hx_encode(henc_, (int64_t*)dc.ptr, (const double*)dm.ptr, (int)width, (long long)width, (int)k,
-                             scale.to_double(), cap, nullptr);
+                             scale.to_double(), cap, cur());
     if (rc == HX_ERR_OVERFLOW) throw std::overflow_error(hx_last_error());
     ck(rc, "encode");
     std::uint64_t* o = out + c0 * n * N;
-    ck(hx_from_i64(ctx_, o, (const int64_t*)dc.ptr, (int)k, n, 0, nullptr), "from_i64");
-    ck(hx_ntt_fwd(ctx_, o, (int)k, n, 0, nullptr), "ntt");
+    ck(hx_from_i64(ctx_, o, (const int64_t*)dc.ptr, (int)k, n, 0, cur()), "from_i64");
+    ck(hx_ntt_fwd(ctx_, o, (int)k, n, 0, cur()), "ntt");
   }
-  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+  cuda_ck(cudaStreamSynchronize(cur()), "sync");
 }
 
 Plaintext GpuLatticeBackend::encode(std::span<const double> m, int level, const Scale& scale) {
+  DeviceScope ds(*this);
   if (m.size() > slots()) throw std::invalid_argument("encode: vector longer than slot count");
   if (!scale.is_positive()) throw std::invalid_argument("encode: non-positive scale");
   if (level < 0 || level > params_.max_level) throw std::invalid_argument("encode: level out of range");
@@ -312,6 +350,7 @@ Plaintext GpuLatticeBackend::encode(std::span<const double> m, int level, const 
 
 std::vector<Plaintext> GpuLatticeBackend::encode_many(const std::vector<std::vector<double>>& msgs,
                                                       int level, const Scale& scale) {
+  DeviceScope ds(*this);
   if (level < 0 || level > params_.max_level) throw std::invalid_argument("encode: level out of range");
   const std::size_t N = params_.ring_degree;
   const int n = nq(level);
@@ -341,21 +380,23 @@ std::vector<Plaintext> GpuLatticeBackend::encode_many(const std::vector<std::vec
 }
 
 std::vector<double> GpuLatticeBackend::decode(const Plaintext& pt) {
+  DeviceScope ds(*this);
   const std::size_t N = params_.ring_degree;
   const int n = nq(pt.level);
   if (!pt.payload) return std::vector<double>(slots(), 0.0);
   const auto& p = payload(pt);
   DeviceBuffer tmp((std::size_t)n * N);
-  cuda_ck(cudaMemcpyAsync(tmp.ptr, p.data(), (std::size_t)n * N * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
-  ck(hx_ntt_inv(ctx_, tmp.ptr, 1, n, 0, nullptr), "intt");
+  cuda_ck(cudaMemcpyAsync(tmp.ptr, p.data(), (std::size_t)n * N * 8, cudaMemcpyDeviceToDevice, cur()), "d2d");
+  ck(hx_ntt_inv(ctx_, tmp.ptr, 1, n, 0, cur()), "intt");
   std::vector<u64> limbs((std::size_t)n * N);
-  cuda_ck(cudaMemcpyAsync(limbs.data(), tmp.ptr, limbs.size() * 8, cudaMemcpyDeviceToHost, nullptr), "d2h");
-  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+  cuda_ck(cudaMemcpyAsync(limbs.data(), tmp.ptr, limbs.size() * 8, cudaMemcpyDeviceToHost, cur()), "d2h");
+  cuda_ck(cudaStreamSynchronize(cur()), "sync");
   return enc_.decode_coeffs(limbs, n, pt.scale.to_double());
 }
 
 // ------------------------------------------------------------- encrypt / decrypt
 Ciphertext GpuLatticeBackend::encrypt(const Plaintext& pt) {
+  DeviceScope ds(*this);
   const std::size_t N = params_.ring_degree;
   const int n = nq(pt.level);
   std::vector<u64> a;
@@ -363,28 +404,29 @@ Ciphertext GpuLatticeBackend::encrypt(const Plaintext& pt) {
   sample_uniform(a, n, 0, 1);
   sample_error(e, 1);
   DeviceBuffer da(a.size()), de(e.size());
-  cuda_ck(cudaMemcpyAsync(da.ptr, a.data(), a.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
-  cuda_ck(cudaMemcpyAsync(de.ptr, e.data(), e.size() * 8, cudaMemcpyHostToDevice, nullptr), "h2d");
+  cuda_ck(cudaMemcpyAsync(da.ptr, a.data(), a.size() * 8, cudaMemcpyHostToDevice, cur()), "h2d");
+  cuda_ck(cudaMemcpyAsync(de.ptr, e.data(), e.size() * 8, cudaMemcpyHostToDevice, cur()), "h2d");
   std::shared_ptr<DeviceBuffer> zero;
   const u64* m;
   if (pt.payload) {
     m = payload(pt).data();
   } else {
     zero = dev((std::size_t)n * N);
-    cuda_ck(cudaMemsetAsync(zero->ptr, 0, (std::size_t)n * N * 8, nullptr), "memset");
+    cuda_ck(cudaMemsetAsync(zero->ptr, 0, (std::size_t)n * N * 8, cur()), "memset");
     m = zero->ptr;
   }
   auto buf = dev((std::size_t)2 * n * N);
-  ck(hx_encrypt_sk(ctx_, buf->ptr, m, s_full_->ptr, da.ptr, (const int64_t*)de.ptr, n, nullptr), "encrypt");
-  cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+  ck(hx_encrypt_sk(ctx_, buf->ptr, m, s_full_->ptr, da.ptr, (const int64_t*)de.ptr, n, cur()), "encrypt");
+  cuda_ck(cudaStreamSynchronize(cur()), "sync");
   return wrap(buf, 0, pt.level, pt.scale);
 }
 
 std::vector<double> GpuLatticeBackend::decrypt(const Ciphertext& ct) {
+  DeviceScope ds(*this);
   const std::size_t N = params_.ring_degree;
   const int n = nq(ct.level);
   auto buf = dev((std::size_t)n * N);
-  ck(hx_decrypt(ctx_, buf->ptr, payload(ct).data(), s_full_->ptr, 1, n, nullptr), "decrypt");
+  ck(hx_decrypt(ctx_, buf->ptr, payload(ct).data(), s_full_->ptr, 1, n, cur()), "decrypt");
   auto p = std::make_shared<GpuPlaintext>();
   p->buf = buf;
   p->n_q = n;
@@ -398,16 +440,18 @@ std::vector<double> GpuLatticeBackend::decrypt(const Ciphertext& ct) {
 
 // ------------------------------------------------------------- SlotOps
 Ciphertext GpuLatticeBackend::add(const Ciphertext& a, const Ciphertext& b) {
+  DeviceScope ds(*this);
   detail::require_same_level(a.level, b.level, "add");
   detail::require_same_scale(a.scale, b.scale, "add");
   const int n = nq(a.level);
   auto buf = dev((std::size_t)2 * n * params_.ring_degree);
-  ck(hx_add(ctx_, buf->ptr, payload(a).data(), payload(b).data(), 2, n, 0, nullptr), "add");
+  ck(hx_add(ctx_, buf->ptr, payload(a).data(), payload(b).data(), 2, n, 0, cur()), "add");
   trace_.record(OpKind::CtAdd, a.level);
   return wrap(buf, 0, a.level, a.scale);
 }
 
 Ciphertext GpuLatticeBackend::add_plain(const Ciphertext& a, const Plaintext& b) {
+  DeviceScope ds(*this);
   detail::require_same_level(a.level, b.level, "add_plain");
   detail::require_same_scale(a.scale, b.scale, "add_plain");
   const std::size_t N = params_.ring_degree;
@@ -415,44 +459,47 @@ Ciphertext GpuLatticeBackend::add_plain(const Ciphertext& a, const Plaintext& b)
   auto buf = dev((std::size_t)2 * n * N);
   const u64* ad = payload(a).data();
   if (b.payload)
-    ck(hx_add(ctx_, buf->ptr, ad, payload(b).data(), 1, n, 0, nullptr), "add");
+    ck(hx_add(ctx_, buf->ptr, ad, payload(b).data(), 1, n, 0, cur()), "add");
   else
-    cuda_ck(cudaMemcpyAsync(buf->ptr, ad, (std::size_t)n * N * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
+    cuda_ck(cudaMemcpyAsync(buf->ptr, ad, (std::size_t)n * N * 8, cudaMemcpyDeviceToDevice, cur()), "d2d");
   cuda_ck(cudaMemcpyAsync(buf->ptr + (std::size_t)n * N, ad + (std::size_t)n * N, (std::size_t)n * N * 8,
-                          cudaMemcpyDeviceToDevice, nullptr), "d2d");
+                          cudaMemcpyDeviceToDevice, cur()), "d2d");
   trace_.record(OpKind::PtAdd, a.level);
   return wrap(buf, 0, a.level, a.scale);
 }
 
 Ciphertext GpuLatticeBackend::mul(const Ciphertext& a, const Ciphertext& b) {
+  DeviceScope ds(*this);
   detail::require_same_level(a.level, b.level, "mul");
   if (a.level < 1) throw LevelUnderflowError("mul: no level left for a following rescale");
   const int n = nq(a.level);
   auto buf = dev((std::size_t)2 * n * params_.ring_degree);
-  ck(hx_mul_relin(ctx_, buf->ptr, payload(a).data(), payload(b).data(), rlk_->ptr, 1, n, nullptr), "mul_relin");
+  ck(hx_mul_relin(ctx_, buf->ptr, payload(a).data(), payload(b).data(), rlk_->ptr, 1, n, cur()), "mul_relin");
   trace_.record(OpKind::CtMul, a.level);
   return wrap(buf, 0, a.level, a.scale * b.scale);
 }
 
 Ciphertext GpuLatticeBackend::mul_plain(const Ciphertext& a, const Plaintext& b) {
+  DeviceScope ds(*this);
   detail::require_same_level(a.level, b.level, "mul_plain");
   if (a.level < 1) throw LevelUnderflowError("mul_plain: no level left for a following rescale");
   const std::size_t N = params_.ring_degree;
   const int n = nq(a.level);
   auto buf = dev((std::size_t)2 * n * N);
   if (!b.payload) {
-    cuda_ck(cudaMemsetAsync(buf->ptr, 0, (std::size_t)2 * n * N * 8, nullptr), "memset");
+    cuda_ck(cudaMemsetAsync(buf->ptr, 0, (std::size_t)2 * n * N * 8, cur()), "memset");
   } else {
     const u64* ad = payload(a).data();
     const u64* bd = payload(b).data();
-    ck(hx_mul(ctx_, buf->ptr, ad, bd, 1, n, 0, nullptr), "mul");
-    ck(hx_mul(ctx_, buf->ptr + (std::size_t)n * N, ad + (std::size_t)n * N, bd, 1, n, 0, nullptr), "mul");
+    ck(hx_mul(ctx_, buf->ptr, ad, bd, 1, n, 0, cur()), "mul");
+    ck(hx_mul(ctx_, buf->ptr + (std::size_t)n * N, ad + (std::size_t)n * N, bd, 1, n, 0, cur()), "mul");
   }
   trace_.record(OpKind::PtMul, a.level);
   return wrap(buf, 0, a.level, a.scale * b.scale);
 }
 
 Ciphertext GpuLatticeBackend::rotate(const Ciphertext& a, std::int64_t k) {
+  DeviceScope ds(*this);
   const auto n = (std::int64_t)slots();
   const std::int64_t r = detail::reduce_amount(k, n);
   const std::size_t N = params_.ring_degree;
@@ -460,42 +507,45 @@ Ciphertext GpuLatticeBackend::rotate(const Ciphertext& a, std::int64_t k) {
   if (r == 0) {
     auto buf = dev((std::size_t)2 * nqv * N);
     cuda_ck(cudaMemcpyAsync(buf->ptr, payload(a).data(), (std::size_t)2 * nqv * N * 8,
-                            cudaMemcpyDeviceToDevice, nullptr), "d2d");
+                            cudaMemcpyDeviceToDevice, cur()), "d2d");
     return wrap(buf, 0, a.level, a.scale);
   }
   const u64* key = rotation_key(r);
   if (!rot_set_.contains(r) || !key) throw MissingRotationKeyError("rotate: no key for amount " + std::to_string(r));
   auto buf = dev((std::size_t)2 * nqv * N);
-  ck(hx_rotate(ctx_, buf->ptr, payload(a).data(), key, 1, nqv, galois(r), nullptr), "rotate");
+  ck(hx_rotate(ctx_, buf->ptr, payload(a).data(), key, 1, nqv, galois(r), cur()), "rotate");
   trace_.record(OpKind::Rotate, a.level);
   return wrap(buf, 0, a.level, a.scale);
 }
 
 Ciphertext GpuLatticeBackend::rescale(const Ciphertext& a) {
+  DeviceScope ds(*this);
   if (a.level < 1) throw LevelUnderflowError("rescale: no levels remain");
   if (!(a.scale.log2() > params_.delta().log2()))
     throw std::invalid_argument("rescale: scale not above Delta (no multiplication preceded)");
   const int n = nq(a.level);
   auto buf = dev((std::size_t)2 * (n - 1) * params_.ring_degree);
-  ck(hx_rescale(ctx_, buf->ptr, payload(a).data(), 2, n, nullptr), "rescale");
+  ck(hx_rescale(ctx_, buf->ptr, payload(a).data(), 2, n, cur()), "rescale");
   trace_.record(OpKind::Rescale, a.level);
   return wrap(buf, 0, a.level - 1, a.scale / Scale::prime(modulus_at(a.level)));
 }
 
 Ciphertext GpuLatticeBackend::mod_down(const Ciphertext& a, int target) {
+  DeviceScope ds(*this);
   if (target > a.level) throw std::invalid_argument("mod_down: target level above current level");
   if (target < 0) throw std::invalid_argument("mod_down: negative target level");
   const std::size_t N = params_.ring_degree;
   const int n = nq(a.level), t = nq(target);
   auto buf = dev((std::size_t)2 * t * N);
   cuda_ck(cudaMemcpy2DAsync(buf->ptr, (std::size_t)t * N * 8, payload(a).data(), (std::size_t)n * N * 8,
-                            (std::size_t)t * N * 8, 2, cudaMemcpyDeviceToDevice, nullptr),
+                            (std::size_t)t * N * 8, 2, cudaMemcpyDeviceToDevice, cur()),
           "memcpy2d");
   if (target != a.level) trace_.record(OpKind::ModDown, a.level);
   return wrap(buf, 0, target, a.scale);
 }
 
 Ciphertext GpuLatticeBackend::bootstrap(const Ciphertext& a) {
+  DeviceScope ds(*this);
   if (!params_.mock_bootstrap)
     throw std::runtime_error("bootstrap: only the insecure mock refresh is implemented (mock_bootstrap=false)");
   trace_.record(OpKind::Bootstrap, a.level);
@@ -506,6 +556,7 @@ Ciphertext GpuLatticeBackend::bootstrap(const Ciphertext& a) {
 // ------------------------------------------------------------- fused pipelines
 std::vector<Ciphertext> GpuLatticeBackend::rotate_many(const Ciphertext& a,
                                                        std::span<const std::int64_t> amounts) {
+  DeviceScope ds(*this);
   const auto n = (std::int64_t)slots();
   const std::size_t N = params_.ring_degree;
   const int nqv = nq(a.level);
@@ -527,16 +578,16 @@ std::vector<Ciphertext> GpuLatticeBackend::rotate_many(const Ciphertext& a,
     // hoisted outputs land contiguously; identity rotations are copied after
     auto tmp = dev(keys.size() * ctw);
     ck(hx_rotate_hoisted(ctx_, tmp->ptr, payload(a).data(), keys.data(), gs.data(), (int)keys.size(), 1,
-                         nqv, nullptr), "rotate_hoisted");
+                         nqv, cur()), "rotate_hoisted");
     for (std::size_t j = 0; j < which.size(); ++j)
       cuda_ck(cudaMemcpyAsync(buf->ptr + which[j] * ctw, tmp->ptr + j * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
-                              nullptr), "d2d");
+                              cur()), "d2d");
     trace_.record(OpKind::Rotate, a.level, keys.size());
   }
   std::vector<Ciphertext> out;
   for (std::size_t i = 0; i < amounts.size(); ++i) {
     if (detail::reduce_amount(amounts[i], n) == 0)
-      cuda_ck(cudaMemcpyAsync(buf->ptr + i * ctw, payload(a).data(), ctw * 8, cudaMemcpyDeviceToDevice, nullptr),
+      cuda_ck(cudaMemcpyAsync(buf->ptr + i * ctw, payload(a).data(), ctw * 8, cudaMemcpyDeviceToDevice, cur()),
               "d2d");
     out.push_back(wrap(buf, i * ctw, a.level, a.scale));
   }
@@ -544,6 +595,7 @@ std::vector<Ciphertext> GpuLatticeBackend::rotate_many(const Ciphertext& a,
 }
 
 Ciphertext GpuLatticeBackend::matmul(const Ciphertext& A, const Ciphertext& B, int d) {
+  DeviceScope ds(*this);
   return matmul_heads({A}, {B}, d).front();
 }
 
@@ -555,6 +607,7 @@ Ciphertext GpuLatticeBackend::matmul(const Ciphertext& A, const Ciphertext& B, i
 // Heads are processed in chunks bounded by device memory.
 std::vector<Ciphertext> GpuLatticeBackend::matmul_heads(const std::vector<Ciphertext>& As,
                                                         const std::vector<Ciphertext>& Bs, int d) {
+  DeviceScope ds(*this);
   const std::size_t N = params_.ring_degree, n = slots();
   if (As.empty() || As.size() != Bs.size()) throw std::invalid_argument("matmul_heads: operand count");
   const Ciphertext& A0 = As[0];
@@ -603,11 +656,11 @@ std::vector<Ciphertext> GpuLatticeBackend::matmul_heads(const std::vector<Cipher
                           const std::shared_ptr<DeviceBuffer>& out, std::int64_t unit) {
       for (int h = 0; h < H; ++h)
         cuda_ck(cudaMemcpyAsync(in->ptr + h * cw, payload(X[h0 + h]).data(), cw * 8, cudaMemcpyDeviceToDevice,
-                                nullptr), "d2d");
+                                cur()), "d2d");
       // prod[j][h][c] = X_h[c] (.) mask_j  (encode_many: masks contiguous [d][nqa][N])
-      ck(hx_mul_bcast(ctx_, prod->ptr, in->ptr, payload(masks[0]).data(), 2 * d * H, 2 * H, 2 * H, nqa, nullptr),
+      ck(hx_mul_bcast(ctx_, prod->ptr, in->ptr, payload(masks[0]).data(), 2 * d * H, 2 * H, 2 * H, nqa, cur()),
          "mul_bcast");
-      ck(hx_rescale(ctx_, out->ptr, prod->ptr, 2 * d * H, nqa, nullptr), "rescale");
+      ck(hx_rescale(ctx_, out->ptr, prod->ptr, 2 * d * H, nqa, cur()), "rescale");
       // column / row j -> 0 for j >= 1: key j applied to the H heads of column j
       if (d > 1) {
         std::vector<const u64*> keys;
@@ -618,29 +671,29 @@ std::vector<Ciphertext> GpuLatticeBackend::matmul_heads(const std::vector<Cipher
           gal.push_back(kg.second);
         }
         ck(hx_rotate_grouped(ctx_, tmp->ptr, out->ptr + (std::size_t)H * cwb, keys.data(), gal.data(), d - 1, H, nqb,
-                             nullptr),
+                             cur()),
            "rotate_grouped");
         cuda_ck(cudaMemcpyAsync(out->ptr + (std::size_t)H * cwb, tmp->ptr, (std::size_t)(d - 1) * H * cwb * 8,
-                                cudaMemcpyDeviceToDevice, nullptr), "d2d");
+                                cudaMemcpyDeviceToDevice, cur()), "d2d");
       }
       // replicate: x += Rot_{-unit 2^i}(x), i < log2 d, all d x H at once (one key read)
       for (int i = 0; i < lg; ++i) {
         const auto kg = need(-(unit << i));
-        ck(hx_rotate(ctx_, tmp->ptr, out->ptr, kg.first, d * H, nqb, kg.second, nullptr), "rotate");
-        ck(hx_add(ctx_, out->ptr, out->ptr, tmp->ptr, 2 * d * H, nqb, 0, nullptr), "add");
+        ck(hx_rotate(ctx_, tmp->ptr, out->ptr, kg.first, d * H, nqb, kg.second, cur()), "rotate");
+        ck(hx_add(ctx_, out->ptr, out->ptr, tmp->ptr, 2 * d * H, nqb, 0, cur()), "add");
       }
     };
     side(As, cm, sa, 1);
     side(Bs, rm, sb, d);
     // d x H ct-ct products + relinearisation, summed over j per head, one rescale
-    ck(hx_mul_relin(ctx_, tmp->ptr, sa->ptr, sb->ptr, rlk_->ptr, d * H, nqb, nullptr), "mul_relin");
+    ck(hx_mul_relin(ctx_, tmp->ptr, sa->ptr, sb->ptr, rlk_->ptr, d * H, nqb, cur()), "mul_relin");
     auto acc = dev((std::size_t)H * cwb);
     ck(hx_sum_strided(ctx_, acc->ptr, tmp->ptr, d, (long long)H * cwb, 2 * H, (long long)nqb * N, (long long)nqb * N,
-                      nqb, nullptr),
+                      nqb, cur()),
        "sum");
     auto outb = dev((std::size_t)H * 2 * (nqb - 1) * N);
-    ck(hx_rescale(ctx_, outb->ptr, acc->ptr, 2 * H, nqb, nullptr), "rescale");
-    cuda_ck(cudaStreamSynchronize(nullptr), "sync");
+    ck(hx_rescale(ctx_, outb->ptr, acc->ptr, 2 * H, nqb, cur()), "rescale");
+    cuda_ck(cudaStreamSynchronize(cur()), "sync");
     for (int h = 0; h < H; ++h) {
       const Ciphertext& A = As[h0 + h];
       const Ciphertext& B = Bs[h0 + h];
@@ -661,12 +714,14 @@ std::vector<Ciphertext> GpuLatticeBackend::matmul_heads(const std::vector<Cipher
 
 Ciphertext GpuLatticeBackend::bsgs_block(const std::vector<Ciphertext>& baby,
                                          const std::vector<Plaintext>& diags, int n1, int n2) {
+  DeviceScope ds(*this);
   return bsgs_blocks(baby, diags, n1, n2, 1).front();
 }
 
 std::vector<Ciphertext> GpuLatticeBackend::bsgs_blocks(const std::vector<Ciphertext>& baby,
                                                        const std::vector<Plaintext>& diags, int n1, int n2,
                                                        int blocks, bool allow_empty) {
+  DeviceScope ds(*this);
   return bsgs_blocks_tokens({baby}, diags, n1, n2, blocks, allow_empty).front();
 }
 
@@ -685,13 +740,13 @@ static void mac_chunked(hx_ctx* ctx, std::uint64_t* inner, std::size_t inner_pol
     std::uint64_t* dst = inner;
     if (k0) {
       if (!tmp) tmp = std::make_unique<DeviceBuffer>(inner_polys * ptw);
-      cuda_ck(cudaMemsetAsync(tmp->ptr, 0, inner_polys * ptw * 8, nullptr), "memset");
+      cuda_ck(cudaMemsetAsync(tmp->ptr, 0, inner_polys * ptw * 8, cur()), "memset");
       dst = tmp->ptr;
     }
     ck(hx_bsgs_mac_tokens(ctx, dst + off, jstride, tstride, baby + (std::size_t)k0 * ctw, btstride,
-                          diags + (std::size_t)k0 * ptw, nqv, kc, n2, nqv, T, dj, nullptr),
+                          diags + (std::size_t)k0 * ptw, nqv, kc, n2, nqv, T, dj, cur()),
        "bsgs_mac");
-    if (k0) ck(hx_add(ctx, inner, inner, dst, (int)inner_polys, nqv, 0, nullptr), "add");
+    if (k0) ck(hx_add(ctx, inner, inner, dst, (int)inner_polys, nqv, 0, cur()), "add");
   }
 }
 
@@ -720,7 +775,7 @@ static std::shared_ptr<DeviceBuffer> tc_pack(hx_ctx* ctx, const std::shared_ptr<
   const long long bytes = hx_bsgs_tc_bytes(ctx, rows, n1, nqv);
   if (bytes < 0) throw std::invalid_argument("bsgs: tensor-core shape");
   auto pk = dev(((std::size_t)bytes + 7) / 8);
-  ck(hx_bsgs_tc_pack(ctx, pk->ptr, ptrs.data(), rows, n1, nqv, nullptr), "bsgs_tc_pack");
+  ck(hx_bsgs_tc_pack(ctx, pk->ptr, ptrs.data(), rows, n1, nqv, cur()), "bsgs_tc_pack");
   buf->derived.emplace_back(sig, pk);
   return pk;
 }
@@ -752,7 +807,7 @@ static std::shared_ptr<DeviceBuffer> p40_pack(hx_ctx* ctx, const std::shared_ptr
     if (e.first == sig) return e.second;
   std::erase_if(buf->derived, [](const auto& e) { return (e.first & 1) == 0; });  // tensor-core tiles
   auto pk = dev(((std::size_t)bytes + 7) / 8);
-  ck(hx_bsgs_p40_pack(ctx, pk->ptr, diags, nqv, n1, n2, dj, nqv, nullptr), "bsgs_p40_pack");
+  ck(hx_bsgs_p40_pack(ctx, pk->ptr, diags, nqv, n1, n2, dj, nqv, cur()), "bsgs_p40_pack");
   buf->derived.emplace_back(sig, pk);
   return pk;
 }
@@ -768,6 +823,7 @@ static bool tc_mac_enabled() {
 std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
     const std::vector<std::vector<Ciphertext>>& babies, const std::vector<Plaintext>& diags, int n1, int n2,
     int blocks, bool allow_empty) {
+  DeviceScope ds(*this);
   const int T = (int)babies.size();
   if (T < 1) throw std::invalid_argument("bsgs_blocks: no tokens");
   for (const auto& bb : babies)
@@ -796,7 +852,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       auto bb = dev(n1 * ctw);
       for (int k = 0; k < n1; ++k)
         cuda_ck(cudaMemcpyAsync(bb->ptr + k * ctw, payload(babies[t][k]).data(), ctw * 8, cudaMemcpyDeviceToDevice,
-                                nullptr), "d2d");
+                                cur()), "d2d");
       baby_ptr[t] = bb->ptr;
       keep.push_back(bb);
     }
@@ -808,7 +864,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
   const std::size_t jstride = (std::size_t)E * ctw;
   auto inner = dev((std::size_t)n2 * jstride);
   const std::size_t inner_polys = (std::size_t)n2 * E * 2;
-  cuda_ck(cudaMemsetAsync(inner->ptr, 0, inner->words * 8, nullptr), "memset");
+  cuda_ck(cudaMemsetAsync(inner->ptr, 0, inner->words * 8, cur()), "memset");
   Scale dscale;
   bool have_scale = false;
   std::vector<std::vector<char>> live(blocks, std::vector<char>(n2, 0));
@@ -848,7 +904,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
         }
         const auto pk = tc_pack(ctx_, src, ptrs, nb * n2, n1, nqv);
         ck(hx_bsgs_mac_tc(ctx_, inner->ptr + (std::size_t)b0 * ctw, (long long)jstride, (long long)ctw,
-                          (long long)(blocks * ctw), baby_ptr[0], bst, pk->ptr, nb, n2, n1, nqv, T, nullptr),
+                          (long long)(blocks * ctw), baby_ptr[0], bst, pk->ptr, nb, n2, n1, nqv, T, cur()),
            "bsgs_mac_tc");
       }
       for (int b = 0; b < blocks; ++b) {
@@ -902,7 +958,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       if (T == 1 && n1 <= 64) pk = p40_pack(ctx_, p0->buf, p0->data(), n1, n2, n1, nqv);
       if (pk) {
         ck(hx_bsgs_mac_p40(ctx_, inner->ptr + (std::size_t)b * ctw, (long long)jstride, baby_ptr[0], pk->ptr,
-                           p0->data(), nqv, n1, n2, n1, nqv, nullptr),
+                           p0->data(), nqv, n1, n2, n1, nqv, cur()),
            "bsgs_mac_p40");
       } else if (uniform) {
         mac_chunked(ctx_, inner->ptr, inner_polys, (std::size_t)b * ctw, (long long)jstride, (long long)(blocks * ctw),
@@ -967,7 +1023,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
           }
           if (pk) {
             ck(hx_bsgs_mac_p40(ctx_, inner->ptr + off, (long long)jstride, baby_ptr[0], pk->ptr, dp[gptr[j]], nqv, n1,
-                               j1 - j, n1, nqv, nullptr),
+                               j1 - j, n1, nqv, cur()),
                "bsgs_mac_p40");
           } else if (uniform) {
             mac_chunked(ctx_, inner->ptr, inner_polys, off, (long long)jstride, (long long)(blocks * ctw), baby_ptr[0],
@@ -994,12 +1050,12 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       if (!ks.empty()) {
         if (uniform) {
           ck(hx_bsgs_mac_sparse(ctx_, inner->ptr + (std::size_t)b * ctw, (long long)jstride, (long long)(blocks * ctw),
-                                baby_ptr[0], bstride, gptr.data(), ks.data(), dp.data(), n1, n2, nqv, T, nullptr),
+                                baby_ptr[0], bstride, gptr.data(), ks.data(), dp.data(), n1, n2, nqv, T, cur()),
              "bsgs_mac_sparse");
         } else {
           for (int t = 0; t < T; ++t)
             ck(hx_bsgs_mac_sparse(ctx_, inner->ptr + ((std::size_t)t * blocks + b) * ctw, (long long)jstride, 0,
-                                  baby_ptr[t], 0, gptr.data(), ks.data(), dp.data(), n1, n2, nqv, 1, nullptr),
+                                  baby_ptr[t], 0, gptr.data(), ks.data(), dp.data(), n1, n2, nqv, 1, cur()),
                "bsgs_mac_sparse");
         }
       }
@@ -1032,7 +1088,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
           dg = std::make_unique<DeviceBuffer>(ks.size() * ptw);
           for (std::size_t i = 0; i < ks.size(); ++i)
             cuda_ck(cudaMemcpyAsync(dg->ptr + i * ptw, payload(D[(std::size_t)j * n1 + ks[i]]).data(), ptw * 8,
-                                    cudaMemcpyDeviceToDevice, nullptr), "d2d");
+                                    cudaMemcpyDeviceToDevice, cur()), "d2d");
         }
         for (int t = 0; t < T; ++t) {
           const std::size_t off = j * jstride + ((std::size_t)t * blocks + b) * ctw;
@@ -1043,7 +1099,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
             DeviceBuffer bs(ks.size() * ctw);
             for (std::size_t i = 0; i < ks.size(); ++i)
               cuda_ck(cudaMemcpyAsync(bs.ptr + i * ctw, baby_ptr[t] + ks[i] * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
-                                      nullptr), "d2d");
+                                      cur()), "d2d");
             mac_chunked(ctx_, inner->ptr, inner_polys, off, (long long)ctw, 0, bs.ptr, 0, ctw, dg->ptr, ptw, nqv,
                         (int)ks.size(), 1, (int)ks.size(), 1);
           }
@@ -1084,7 +1140,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
   const std::size_t pw = partial ? ctw + uw : ctw;
   auto out = dev((std::size_t)E * pw);
   if (J.empty() && !partial) {
-    cuda_ck(cudaMemcpyAsync(out->ptr, inner->ptr, jstride * 8, cudaMemcpyDeviceToDevice, nullptr), "d2d");
+    cuda_ck(cudaMemcpyAsync(out->ptr, inner->ptr, jstride * 8, cudaMemcpyDeviceToDevice, cur()), "d2d");
   } else {
     std::shared_ptr<DeviceBuffer> src;
     const u64* srcp = inner->ptr + jstride;  // groups 1..n2-1 are contiguous
@@ -1092,21 +1148,21 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       src = dev(J.size() * jstride);
       for (std::size_t i = 0; i < J.size(); ++i)
         cuda_ck(cudaMemcpyAsync(src->ptr + i * jstride, inner->ptr + J[i] * jstride, jstride * 8,
-                                cudaMemcpyDeviceToDevice, nullptr), "d2d");
+                                cudaMemcpyDeviceToDevice, cur()), "d2d");
       srcp = src->ptr;
     }
     if (!partial) {
       ck(hx_rotate_grouped_sum(ctx_, out->ptr, nullptr, srcp, inner->ptr, keys.data(), gs.data(), (int)J.size(), E,
-                               nqv, nullptr),
+                               nqv, cur()),
          "rotate_grouped_sum");
     } else {
       auto tb = dev((std::size_t)E * ctw), sb = dev((std::size_t)E * uw);
       ck(hx_rotate_grouped_sum(ctx_, tb->ptr, sb->ptr, srcp, inner->ptr, keys.data(), gs.data(), (int)J.size(), E,
-                               nqv, nullptr),
+                               nqv, cur()),
          "rotate_grouped_sum");
-      cuda_ck(cudaMemcpy2DAsync(out->ptr, pw * 8, tb->ptr, ctw * 8, ctw * 8, E, cudaMemcpyDeviceToDevice, nullptr),
+      cuda_ck(cudaMemcpy2DAsync(out->ptr, pw * 8, tb->ptr, ctw * 8, ctw * 8, E, cudaMemcpyDeviceToDevice, cur()),
               "memcpy2d");
-      cuda_ck(cudaMemcpy2DAsync(out->ptr + ctw, pw * 8, sb->ptr, uw * 8, uw * 8, E, cudaMemcpyDeviceToDevice, nullptr),
+      cuda_ck(cudaMemcpy2DAsync(out->ptr + ctw, pw * 8, sb->ptr, uw * 8, uw * 8, E, cudaMemcpyDeviceToDevice, cur()),
               "memcpy2d");
     }
   }
@@ -1127,15 +1183,17 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
 }
 
 Ciphertext GpuLatticeBackend::shard_finish(const Ciphertext& like, const std::uint64_t* words) {
+  DeviceScope ds(*this);
   const int n = nq(like.level);
   const std::size_t N = params_.ring_degree, ctw = (std::size_t)2 * n * N;
   auto buf = dev(ctw);
-  ck(hx_moddown_add(ctx_, buf->ptr, words + ctw, words, 1, n, nullptr), "moddown_add");
+  ck(hx_moddown_add(ctx_, buf->ptr, words + ctw, words, 1, n, cur()), "moddown_add");
   return wrap(buf, 0, like.level, like.scale);
 }
 
 std::vector<std::vector<Ciphertext>> GpuLatticeBackend::rotate_many_tokens(const std::vector<Ciphertext>& xs,
                                                                            std::span<const std::int64_t> amounts) {
+  DeviceScope ds(*this);
   const int T = (int)xs.size();
   if (T < 1) throw std::invalid_argument("rotate_many: no ciphertexts");
   const auto n = (std::int64_t)slots();
@@ -1147,7 +1205,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::rotate_many_tokens(const
   auto in = dev((std::size_t)T * ctw);
   for (int t = 0; t < T; ++t) {
     if (xs[t].level != level) throw LevelMismatchError("rotate_many: token level mismatch");
-    cuda_ck(cudaMemcpyAsync(in->ptr + t * ctw, payload(xs[t]).data(), ctw * 8, cudaMemcpyDeviceToDevice, nullptr),
+    cuda_ck(cudaMemcpyAsync(in->ptr + t * ctw, payload(xs[t]).data(), ctw * 8, cudaMemcpyDeviceToDevice, cur()),
             "d2d");
   }
   std::vector<const u64*> keys;
@@ -1168,19 +1226,19 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::rotate_many_tokens(const
     const bool lead_identity = detail::reduce_amount(amounts[0], n) == 0 && which.size() == R - 1;
     if (lead_identity) {  // BSGS baby steps: write rotations straight after the identity slot
       auto tmp = dev((std::size_t)T * keys.size() * ctw);
-      ck(hx_rotate_hoisted(ctx_, tmp->ptr, in->ptr, keys.data(), gs.data(), (int)keys.size(), T, nqv, nullptr),
+      ck(hx_rotate_hoisted(ctx_, tmp->ptr, in->ptr, keys.data(), gs.data(), (int)keys.size(), T, nqv, cur()),
          "rotate_hoisted");
       cuda_ck(cudaMemcpy2DAsync(buf->ptr + ctw, R * ctw * 8, tmp->ptr, keys.size() * ctw * 8, keys.size() * ctw * 8,
-                                T, cudaMemcpyDeviceToDevice, nullptr),
+                                T, cudaMemcpyDeviceToDevice, cur()),
               "memcpy2d");
     } else {
       auto tmp = dev((std::size_t)T * keys.size() * ctw);
-      ck(hx_rotate_hoisted(ctx_, tmp->ptr, in->ptr, keys.data(), gs.data(), (int)keys.size(), T, nqv, nullptr),
+      ck(hx_rotate_hoisted(ctx_, tmp->ptr, in->ptr, keys.data(), gs.data(), (int)keys.size(), T, nqv, cur()),
          "rotate_hoisted");
       for (int t = 0; t < T; ++t)
         for (std::size_t j = 0; j < which.size(); ++j)
           cuda_ck(cudaMemcpyAsync(buf->ptr + (t * R + which[j]) * ctw, tmp->ptr + (t * keys.size() + j) * ctw, ctw * 8,
-                                  cudaMemcpyDeviceToDevice, nullptr), "d2d");
+                                  cudaMemcpyDeviceToDevice, cur()), "d2d");
     }
     trace_.record(OpKind::Rotate, level, keys.size() * T);
   }
@@ -1189,7 +1247,7 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::rotate_many_tokens(const
     for (std::size_t i = 0; i < R; ++i) {
       if (detail::reduce_amount(amounts[i], n) == 0)
         cuda_ck(cudaMemcpyAsync(buf->ptr + (t * R + i) * ctw, in->ptr + t * ctw, ctw * 8, cudaMemcpyDeviceToDevice,
-                                nullptr), "d2d");
+                                cur()), "d2d");
       out[t].push_back(wrap(buf, (t * R + i) * ctw, level, xs[t].scale));
     }
   return out;
