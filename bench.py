@@ -648,7 +648,11 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        import datetime
+
+        # a rank that fails inside a collective extra must not hang the others for
+        # the default 10 minutes: the NCCL watchdog aborts after 5
+        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(minutes=5))
 
     chain, special = primes()
     ctx = Context(LOGN, chain, special, ALPHA)
