@@ -745,6 +745,24 @@ def main():
                      "algorithmic_bytes_per_step": step_bytes,
                      "note": "SURVEY 8(d): 256 ciphertexts in + out and one 226.5 MB key per step; the NTT-bearing "
                              "key switch is FP64/INT-issue bound (SURVEY 7, hard part 1)"}
+    # step level, compute side: the FP64 lane-op model of one key switch over
+    # the kernels of the step against the FP64 pipe peak;
+    # the integer-class (60-bit) limbs' work comes on top of it
+    n_f = sum(1 for q in chain[:nq] if q < (1 << 47))  # FP64-class chain limbs (all but q_0)
+    n_fext = n_f + sum(1 for p in special if p < (1 << 47))  # FP64-class extended limbs
+    ks_f64 = N * (64 * n_f                                        # c1 INTT (16 stages x 4 per element)
+                  + (MODUP_CONV_OPS + COL_PASS_OPS) * f64_targets  # ModUp conversion + COL pass
+                  + n_fext * ((dn - 1) * COL_PASS_OPS + dn * 12)   # ROW pass of the digits + inner product
+                  + 2 * n_f * (31 + COL_PASS_OPS)                  # ModDown conversion + COL pass (2 polys)
+                  + 2 * n_f * (COL_PASS_OPS + 10))                 # ModDown ROW pass + combine
+    step_f64 = BATCH * ks_f64
+    roofline_step_fp64 = {"bound": "fp64", "achieved": step_f64 / (secs / steps) / 1e12, "peak": f64_peak / 1e12,
+                          "unit": "T FP64 lane-op/s", "frac": step_f64 / (secs / steps) / f64_peak,
+                          "lane_ops_per_step": step_f64,
+                          "note": "FP64 op model of every FP64-class kernel of the key switch (c1 INTT, ModUp "
+                                  "conversion + COL, ROW + inner product, ModDown conversion + COL, ROW + combine); "
+                                  "the 60-bit limbs' integer NTTs and inner product (~11 ms of the step) are not "
+                                  "in it"}
     # per-kernel shares of the step (one extra untimed step per kernel family)
     breakdown = {}
     for fam in ("modup_col_kernel", "ks_row_inner_f64_kernel", "ntt_pass_kernel", "ntt_row_combine_kernel",
@@ -916,7 +934,8 @@ def main():
                        "N": N, "chain_primes": nq, "special_primes": K, "alpha": ALPHA,
                        "batch_per_gpu": BATCH, "parallelism": f"replicas x{world}",
                        "l2": "inputs larger than L2 (6.4 GB of ciphertexts per step)"},
-            "roofline": roofline, "roofline_step": roofline_step, "step_breakdown": breakdown,
+            "roofline": roofline, "roofline_step": roofline_step, "roofline_step_fp64": roofline_step_fp64,
+            "step_breakdown": breakdown,
             "roofline_bsgs_mac": roofline_mac, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks, "extras": extras,
