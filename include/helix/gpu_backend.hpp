@@ -155,6 +155,9 @@ class GpuLatticeBackend final : public SlotBackend {
 
   // ---- raw access ----
   hx_ctx* device_context() const { return ctx_; }
+  // release the device scratch arena and the pool's cached blocks (between
+  // workloads of different shapes); serialised with the backend's operations
+  void trim();
   const CkksEncoder& encoder() const { return enc_; }
   static const GpuCiphertext& payload(const Ciphertext& ct);
   static const GpuPlaintext& payload(const Plaintext& pt);

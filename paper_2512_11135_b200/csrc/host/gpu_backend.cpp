@@ -262,6 +262,12 @@ const std::uint64_t* GpuLatticeBackend::rotation_key(std::int64_t r) const {
   return it == rot_keys_.end() ? nullptr : it->second->ptr;
 }
 
+void GpuLatticeBackend::trim() {
+  DeviceScope ds(*this);
+  cuda_ck(cudaStreamSynchronize(cur()), "sync");
+  ck(hx_ctx_trim(ctx_), "trim");
+}
+
 const GpuCiphertext& GpuLatticeBackend::payload(const Ciphertext& ct) {
   auto* p = dynamic_cast<const GpuCiphertext*>(ct.payload.get());
   if (!p) throw std::invalid_argument("ciphertext does not belong to the GPU backend");

@@ -74,7 +74,7 @@ void* hxc_device_context(hxc_backend* b) { return b->b->device_context(); }
 
 int hxc_trim(hxc_backend* b) {
   return guard(-1, [&] {
-    if (hx_ctx_trim((hx_ctx*)b->b->device_context()) != HX_OK) throw std::runtime_error(hx_last_error());
+    b->b->trim();
     return 0;
   });
 }
