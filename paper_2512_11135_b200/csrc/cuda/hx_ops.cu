@@ -138,6 +138,7 @@ u64 find_psi(u64 q, u64 n) {
 // returned its cached (freed) blocks to the device: sync, trim, retry once.
 void trim_pool() {
   cudaGetLastError();
+  if (getenv("HX_ALLOC_TRACE")) fprintf(stderr, "[hx] pool trim + retry\n");
   cuda_ok(cudaDeviceSynchronize(), "sync");
   int dev = 0;
   cudaMemPool_t pool;

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <exception>
+#include <cstdio>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -90,6 +91,7 @@ DeviceBuffer::DeviceBuffer(std::size_t w) : words(w) {
   // device and try once more
   cudaGetLastError();
   ptr = nullptr;
+  if (getenv("HX_ALLOC_TRACE")) fprintf(stderr, "[helix] pool trim + retry for %.2f GB\n", w * 8e-9);
   cuda_ck(cudaDeviceSynchronize(), "sync");
   int dev = 0;
   cudaMemPool_t pool;

@@ -33,13 +33,14 @@ def main():
         f = lambda: ctx.rotate(out, cts, key, B, nq, g)  # noqa: E731
     elif op == "relin":
         f = lambda: ctx.mul_relin(out, cts, cts, key, B, nq)  # noqa: E731
-    else:  # hoisted: 32 rotations of chunks of 8 ciphertexts (the bench extra)
+    else:  # hoisted: 32 rotations of chunks of HOIST_CHUNK (8) ciphertexts (the bench extra)
+        hc = int(os.environ.get("HOIST_CHUNK", "8"))
         gs = [pow(5, k, 2 * N) for k in range(1, 33)]
-        hout = torch.empty((8, 32, 2, nq, N), dtype=torch.int64, device=dev)
+        hout = torch.empty((hc, 32, 2, nq, N), dtype=torch.int64, device=dev)
 
         def f():
-            for c0 in range(0, B, 8):
-                ctx.rotate_hoisted(hout, cts[c0:c0 + 8], [key] * 32, gs, 8, nq)
+            for c0 in range(0, B, hc):
+                ctx.rotate_hoisted(hout, cts[c0:c0 + hc], [key] * 32, gs, hc, nq)
     for _ in range(3):
         f()
     torch.cuda.synchronize()
