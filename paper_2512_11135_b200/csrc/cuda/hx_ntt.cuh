@@ -23,6 +23,7 @@
 #pragma once
 
 #include "hx_common.cuh"
+#include "hx_types.cuh"
 
 namespace hx {
 
