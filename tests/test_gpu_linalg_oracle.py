@@ -124,7 +124,25 @@ def test_config1_matmul_words_vs_oracle(d):
 
 
 # ------------------------------------------------------------------ config-2 primes at N = 2^12
-def _bsgs_case(ov, A, lvl, method_stacked=False):
+def _launches(be, kernel, fn):
+    """fn() with the launches of kernel family `kernel` counted on the backend's context"""
+    import ctypes as C
+
+    from paper_2512_11135_b200.hx import lib
+
+    L = lib()
+    L.hx_ctx_time_kernel.argtypes = [C.c_void_p, C.c_char_p]
+    L.hx_ctx_kernel_time.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_longlong)]
+    h = be.device_context()
+    assert L.hx_ctx_time_kernel(h, kernel.encode()) == 0
+    out = fn()
+    ms, n = C.c_double(), C.c_longlong()
+    assert L.hx_ctx_kernel_time(h, C.byref(ms), C.byref(n)) == 0
+    assert L.hx_ctx_time_kernel(h, None) == 0
+    return out, n.value
+
+
+def _bsgs_case(ov, A, lvl, method_stacked=False, expect_kernel=None):
     from paper_2512_11135_b200.helix import BSGS, BSGS_STACKED
 
     be = ov.be
@@ -135,7 +153,11 @@ def _bsgs_case(ov, A, lvl, method_stacked=False):
     v = np.zeros(d)
     v[: A.shape[1]] = x
     ct = be.encrypt(np.tile(v, be.slots // d), lvl)
-    outs, rep = be.matvec(M, ct)
+    if expect_kernel:
+        (outs, rep), n = _launches(be, expect_kernel, lambda: be.matvec(M, ct))
+        assert n > 0, f"{expect_kernel} did not run"
+    else:
+        outs, rep = be.matvec(M, ct)
     if method_stacked:
         pl, d2, n1, n2 = pack_bsgs_stacked(A, be.slots)
         blocks = 1
@@ -166,6 +188,33 @@ def test_c2s_bsgs_multiblock_words_vs_oracle(stacked, prune):
 
 
 @pytest.mark.parametrize("prune", [0, 5])
+def test_c2s_bsgs_packed_p40_words_vs_oracle(prune):
+    """d = 1024 (n1 = n2 = 32), one block of 32 rows, one token: the packed
+    5-byte MAC (hx_bsgs_mac_p40) on the dense block, or on the dense giant-group
+    runs of a mostly dense block (5 zero diagonals; the rest on the index-list
+    MAC) vs the oracle"""
+    ov = view("c2s")
+    rng = np.random.default_rng(400 + prune)
+    A = rng.normal(0, 0.02, (1024, 1024))
+    if prune:
+        for i in rng.choice(1024, prune, replace=False):
+            for j in range(1024):
+                A[j, (i + j) % 1024] = 0
+    M, *_ = _bsgs_case(ov, A, ov.be.max_level, expect_kernel="bsgs_mac_p40_kernel")
+    assert M.info()["n1"] == 32 and M.info()["blocks"] == 1
+
+
+def test_config1_bsgs_packed_p40_n64_words_vs_oracle():
+    """d = 4096 (n1 = n2 = 64) at config 1 (N = 2^13, 3 limbs of 40 bits): the
+    packed MAC with 8 baby steps per warp vs the oracle"""
+    ov = view("c1")
+    rng = np.random.default_rng(401)
+    A = rng.normal(0, 0.02, (4096, 4096))
+    M, *_ = _bsgs_case(ov, A, ov.be.max_level, expect_kernel="bsgs_mac_p40_kernel")
+    assert M.info()["n1"] == 64
+
+
+@pytest.mark.parametrize("prune", [0, 5])
 def test_c2s_bsgs_tensor_core_rows96_words_vs_oracle(prune):
     """6 row blocks x n2 = 16 = 96 rows, n1 = 16, one token: the tensor-core MAC
     path of bsgs_blocks_tokens (all blocks in one hx_bsgs_mac_tc launch;
@@ -178,7 +227,7 @@ def test_c2s_bsgs_tensor_core_rows96_words_vs_oracle(prune):
             for i in rng.choice(256, prune, replace=False):
                 for j in range(256):
                     A[b * 256 + j, (i + j) % 256] = 0
-    M, *_ = _bsgs_case(ov, A, ov.be.max_level)
+    M, *_ = _bsgs_case(ov, A, ov.be.max_level, expect_kernel="bsgs_mac_tc_kernel")
     assert M.info()["blocks"] == 6 and M.info()["n1"] == 16
 
 
