@@ -317,6 +317,11 @@ struct EpiArgs {
   u32 pginv[64];  // g^-1 mod 2N per rotation r (perm)
 };
 
+#ifndef HX_COMBINE_UNROLL
+#define HX_COMBINE_UNROLL 8
+#endif
+constexpr int kCombineUnroll = HX_COMBINE_UNROLL;  // epilogue words in flight per thread (A/B)
+
 // combine epilogue of the forward ROW pass (see EpiArgs): the tile's
 // transformed words sit in smem (ROW swizzle, residues in [0, q)); thread t
 // handles tile words e = r T + t, i.e. coalesced runs of T.
@@ -342,17 +347,31 @@ __device__ __forceinline__ void row_combine_epilogue(const u64* sm, int t, int t
   const u64* abase = do_add ? E.add + ba * E.add_stride + (long long)i * N : nullptr;
   u64* outb = E.out + ob + (long long)i * N;
   const double wd = __longlong_as_double((long long)u64_to_f64bits(c.w));
-#pragma unroll 4
-  for (int r = 0; r < 16; ++r) {
+  // words in flight: KB at a time, all their loads issued before any store
+  // (the stores may alias the loads as far as the compiler knows, so a plain
+  // unrolled loop keeps one load pair in flight per store)
+  constexpr int KB = kCombineUnroll;
+#pragma unroll 1
+  for (int r0 = 0; r0 < 16; r0 += KB) {
+  u64 uus[KB], ads[KB];
+#pragma unroll
+  for (int rr = 0; rr < KB; ++rr) {
+    const int sidx = (tile << (S + OB)) + (r0 + rr) * T + t;
+    const int aidx = E.perm ? sidx : (E.add_g == 1 ? sidx : (int)ntt_auto_index((u32)sidx, E.add_g, logn));
+    uus[rr] = __ldcs(ub + sidx);
+    ads[rr] = do_add ? __ldg(abase + aidx) : 0ull;
+  }
+#pragma unroll
+  for (int rr = 0; rr < KB; ++rr) {
+    const int r = r0 + rr;
     const int e = r * T + t;
     const int sidx = (tile << (S + OB)) + e;  // coefficient (NTT) index of the word
     const u64 v = sm[swz<true>(e)];
     // output index: tau^-1 (perm); the add operand is gathered at tau_{add_g}
     // when no permutation is fused (combine_kernel's asrc)
     const int oidx = ginv != 1 ? (int)ntt_auto_index((u32)sidx, ginv, logn) : sidx;
-    const int aidx = E.perm ? sidx : (E.add_g == 1 ? sidx : (int)ntt_auto_index((u32)sidx, E.add_g, logn));
-    const u64 uu = __ldcs(ub + sidx);
-    const u64 ad = do_add ? __ldg(abase + aidx) : 0ull;
+    const u64 uu = uus[rr];
+    const u64 ad = ads[rr];
     u64 res;
     if (F64) {
       const double du = __longlong_as_double((long long)u64_to_f64bits(uu));
@@ -365,6 +384,7 @@ __device__ __forceinline__ void row_combine_epilogue(const u64* sm, int t, int t
       if (do_add) res = csub(res + ad, P.q);
     }
     __stcs(outb + oidx, res);
+  }
   }
 }
 
