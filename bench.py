@@ -383,7 +383,8 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=128):
     from paper_2512_11135_b200.helix import BSGS, BSGS_STACKED, Backend, params_json
 
     rng = np.random.default_rng(20251211 * 10 + 3)
-    be = Backend(params_json(LOGN, chain, special, ALPHA, 40), seed=3)
+    pj = params_json(LOGN, chain, special, ALPHA, 40)
+    be = None
     out = {}
     W1 = rng.normal(0.0, 0.02, (768, 3072))
     W2 = rng.normal(0.0, 0.02, (3072, 768))
@@ -399,7 +400,13 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=128):
     if only:
         jobs = [j for j in jobs if j[0] in only]
     for name, M, d, prune, method in jobs:  # y = x W  ->  M = W^T (out x in)
-        be.trim()  # workload switch: drop the previous job's scratch (a fragmented pool slows W2 by ~20%)
+        # each layer in its own backend (its own keys, matrix and scratch): the
+        # previous layer's 14-28 GB of rotation keys and pool blocks would
+        # otherwise crowd the token batches' working set (allocation retries)
+        if be is not None:
+            be.close()
+        torch.cuda.empty_cache()
+        be = Backend(pj, seed=3)
         if prune:
             M = _prune_diagonals(M, d, prune_rng)
         x = rng.uniform(-1, 1, M.shape[1])
@@ -465,7 +472,8 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=128):
             del xt
         del mat, ct
         torch.cuda.synchronize()
-    be.close()
+    if be is not None:
+        be.close()
     return out
 
 

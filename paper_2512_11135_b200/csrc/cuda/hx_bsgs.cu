@@ -353,7 +353,15 @@ __global__ void sum_kernel(SumArgs A) {
   const u64 q = A.pc[i].q;
   const u64* src = A.in + p * A.in_poly_stride + i * N + t;
   u64 acc = 0;
-  for (int r = 0; r < A.terms; ++r) acc = addmod(acc, __ldcs(src + r * A.term_stride), q);
+  int r = 0;
+  for (; r + 8 <= A.terms; r += 8) {  // 8 loads in flight per thread
+    u64 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcs(src + (r + k) * A.term_stride);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc = addmod(acc, v[k], q);
+  }
+  for (; r < A.terms; ++r) acc = addmod(acc, __ldcs(src + r * A.term_stride), q);
   A.out[p * A.out_poly_stride + i * N + t] = acc;
 }
 

@@ -157,16 +157,16 @@ __global__ void __launch_bounds__(256) perm_sum_kernel(PermSumArgs A) {
   const u64* base = A.in + e * A.in_estride + (long long)l * N;
   u64 acc = A.accumulate ? *o : 0ull;
   int r = 0;
-  for (; r + 4 <= A.R; r += 4) {
-    u64 v[4];
+  for (; r + 8 <= A.R; r += 8) {  // 8 gathered loads in flight per thread
+    u64 v[8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 8; ++k) {
       const u32 g = A.g[r + k];
       const int src = g == 1 ? t : (int)ntt_auto_index((u32)t, g, A.logn);
       v[k] = __ldcs(base + (long long)(r + k) * A.in_rstride + src);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) acc = addmod(acc, v[k], q);
+    for (int k = 0; k < 8; ++k) acc = addmod(acc, v[k], q);
   }
   for (; r < A.R; ++r) {
     const u32 g = A.g[r];
