@@ -388,7 +388,6 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=128):
     out = {}
     W1 = rng.normal(0.0, 0.02, (768, 3072))
     W2 = rng.normal(0.0, 0.02, (3072, 768))
-    lvl = be.max_level
     prune_rng = np.random.default_rng(20251211 * 10 + 3 + 200)
     jobs = [("ffn_w1", W1.T.copy(), 1024, False, BSGS), ("ffn_w1_pruned90", W1.T.copy(), 1024, True, BSGS),
             # the 3 row blocks stacked in one set of full-length diagonals: one
@@ -407,6 +406,7 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=128):
             be.close()
         torch.cuda.empty_cache()
         be = Backend(pj, seed=3)
+        lvl = be.max_level
         if prune:
             M = _prune_diagonals(M, d, prune_rng)
         x = rng.uniform(-1, 1, M.shape[1])
