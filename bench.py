@@ -40,8 +40,10 @@ HOIST_R = 32
 HOIST_CHUNK = 16  # ciphertexts per hoisted call (16: 5 % faster than 8, tools/gpu/r02_hoist.sh)
 DOMINANT = "modup_col_kernel"
 F64_LANES_PER_CLK = 62.6  # DFMA lanes / clk / SM, measured on the box (tools/microbench/pipes.cu)
-MODUP_CONV_OPS = 21       # FP64 ops per converted word (3 sources: split products + exact reduction)
+MODUP_CONV_OPS = 16       # FP64 ops per converted word (3 sources x 3 + one joint exact reduction, hx_modup.cuh)
 COL_PASS_OPS = 32         # 8 of the 16 radix-2 stages, 4 FP64 ops per element per stage
+FOLDED_COL_OPS = 29       # COL pass after a fused conversion: the first stage's twiddle product is folded into the constants
+MODDOWN_CONV_OPS = 28     # 3 wide sources (one on the integer pipe), centred correction, joint reduction
 DOM_TRAFFIC_NCU = 28990165000  # dram rd + wr of one modup_col launch, profiles/r02_ncu_full_ks.md
 
 
@@ -728,7 +730,7 @@ def main():
     f64_targets = sum(sum(1 for i in range(nq) if not (d * ALPHA <= i < (d + 1) * ALPHA) and chain[i] < (1 << 47))
                       for d in range(dn))
     all_targets = dn * (nq + K) - nq
-    dom_ops = BATCH * f64_targets * N * (MODUP_CONV_OPS + COL_PASS_OPS)
+    dom_ops = BATCH * f64_targets * N * (MODUP_CONV_OPS + FOLDED_COL_OPS)
     dom_bytes = BATCH * (nq + all_targets) * N * 8  # read the INTT'd digit limbs, write every target limb once
     roofline = {"kernel": DOMINANT + "<S=8,OB=3,alpha=3> (ModUp FastBConv fused into the forward COL pass; "
                           f"{dom_s * 1e3:.2f} ms of the {1e3 * secs / steps:.2f} ms step, CUDA events on its stream "
@@ -739,7 +741,7 @@ def main():
                                                          "x 148 SMs x 1965 MHz",
                 "lane_ops_per_launch": dom_ops, "kernel_ms": dom_s * 1e3, "launches": dom_launches,
                 "share_of_step": dom_s * steps / secs,
-                "ops_model": f"({MODUP_CONV_OPS} conversion + {COL_PASS_OPS} COL-pass) FP64 ops per FP64-class "
+                "ops_model": f"({MODUP_CONV_OPS} conversion + {FOLDED_COL_OPS} COL-pass) FP64 ops per FP64-class "
                              f"target word, {f64_targets} such targets per ciphertext",
                 "hbm": {"achieved": dom_bytes / dom_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                         "frac": dom_bytes / dom_s / 1e9 / hbm_peak, "algorithmic_bytes_per_launch": dom_bytes,
@@ -759,9 +761,9 @@ def main():
     n_f = sum(1 for q in chain[:nq] if q < (1 << 47))  # FP64-class chain limbs (all but q_0)
     n_fext = n_f + sum(1 for p in special if p < (1 << 47))  # FP64-class extended limbs
     ks_f64 = N * (64 * n_f                                        # c1 INTT (16 stages x 4 per element)
-                  + (MODUP_CONV_OPS + COL_PASS_OPS) * f64_targets  # ModUp conversion + COL pass
+                  + (MODUP_CONV_OPS + FOLDED_COL_OPS) * f64_targets  # ModUp conversion + COL pass
                   + n_fext * ((dn - 1) * COL_PASS_OPS + dn * 12)   # ROW pass of the digits + inner product
-                  + 2 * n_f * (31 + COL_PASS_OPS)                  # ModDown conversion + COL pass (2 polys)
+                  + 2 * n_f * (MODDOWN_CONV_OPS + FOLDED_COL_OPS)   # ModDown conversion + COL pass (2 polys)
                   + 2 * n_f * (COL_PASS_OPS + 10))                 # ModDown ROW pass + combine
     step_f64 = BATCH * ks_f64
     roofline_step_fp64 = {"bound": "fp64", "achieved": step_f64 / (secs / steps) / 1e12, "peak": f64_peak / 1e12,

@@ -77,6 +77,9 @@ struct hx_ctx {
   int* d_mdtl = nullptr;
   std::vector<int> md_tl_off, md_tl_cnt, md_tl_icnt;
   double* d_pmodqf = nullptr;
+  double* d_pmodqf1 = nullptr;  // [P psi^(N/2)]_{q_j}: the folded first stage
+  // joint-reduction rounding constants per n_q (0: bounds fail, unfused path)
+  std::vector<double> cs_up, cs_down;
   hx::u64* d_pmodq = nullptr;  // [n_chain]
   hx::SC* d_pinv = nullptr;    // [n_chain]
   // Rescale constants: [l][i] for i < l

@@ -36,9 +36,15 @@ namespace hx {
 // conversion constant of (source limb i of the digit, target limb j):
 // w = [Qhat_i]_{p_j}; FP64 form (w, w / p), (w30, w30 / p) with w30 = [2^30 w]_p;
 // integer form (w, Shoup w').
+// The *1 members are the same constants times the first forward twiddle
+// psi^(N/2) (tw[1]) of the target prime: the words of the upper half of the
+// first butterfly stage are converted with them, which IS that stage's
+// twiddle product (the stage has one twiddle), so the stage multiplies nothing.
 struct BconvC {
   double w, wq, w30, w30q;
   u64 sw, swp;
+  double w1, w301;
+  u64 sw1, swp1;
 };
 
 constexpr int kMaxDigits = 64;
@@ -62,6 +68,10 @@ struct ModUpColArgs {
   // subtract nneg [P]_{q_j}, nneg = #{k : x_k > p_k / 2} per word
   int centred;
   const double* pmf;  // [n_chain] [P]_{q_j} as double (FP64-class targets)
+  const double* pmf1; // [n_chain] [P tw1]_{q_j} (upper half of the folded first stage)
+  // joint reduction of a word's alpha products (bconv_tile_f64): 1.5 * 2^E with
+  // sum_i x_i w_i < 2^(E-1); the host checks E against the rint range
+  double cs_round;
   const u64* pmu;     // [n_chain] [P]_{q_j}
   // target split: blockIdx.y = element * tsplit + part; part p converts the
   // p-th share of the digit's target list (small batches still fill the GPU;
@@ -134,58 +144,92 @@ constexpr bool kModUpInt0 = HX_MODUP_INT0 != 0;
 #define HX_MODUP_MINB 3
 #endif
 
+// Joint reduction: the alpha (or 2 alpha, wide sources) products x_i w_i of a
+// word are summed EXACTLY before one reduction mod p.  A running sum S starts
+// at cs = 1.5 * 2^E and stays in the binade [2^E, 2^(E+1)) (sum < 2^(E-1)), so
+// every S' = fma(x, w, S) rounds x w to a multiple of G = 2^(E-52):
+//   d = S' - S       (exact: same binade)     = x w rounded to a multiple of G
+//   l = fma(x, w, -d)(exact: |l| <= G / 2, an integer below 2^53)
+// and sum_i x_i w_i = (S_last - cs) + sum_i l_i with both parts exact.  One
+// quotient, qf = rint(H / p) with H = S_last - cs (|H / p| < 2^51, checked on
+// the host), leaves r = H - qf p exactly (one FMA), and the word is r + L,
+// |r + L| < p + alpha G.  3 FP64 ops per product + 7 per word instead of 7
+// per product (mulmod_f64 + add): 16 instead of 21 for alpha = 3.
+// HB: the words r with bit WW-1 set are the lower inputs of the first
+// butterfly stage; they are converted with the constants premultiplied by
+// that stage's single twiddle (BconvC::w1 ...), so the stage adds / subtracts
+// only (ntt_group_f64 SKIP1).
 template <int WW, int MAXA, int SRC, int TILE, bool CEN>
 __device__ __forceinline__ void bconv_tile_f64(u64 (&x)[16], const u64* src, const int (&eb)[16 >> WW],
                                                int lowbits, int cnt, const bool (&sf64)[MAXA],
                                                const BconvC (&C)[MAXA], const PrimeConst& P,
-                                               const unsigned char* nn, double pm) {
-  double acc[16];
+                                               const unsigned char* nn, double pm, double pm1, double cs) {
+  constexpr int HB = 1 << (WW - 1);
+  double S[16], L[16];
+  bool lset = CEN;  // L holds a term already (compile-time in the fixed source modes)
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
-    acc[r] = 0.0;
+    S[r] = cs;
+    L[r] = 0.0;
     if (CEN) {  // - nneg [P]_q (exact: nneg <= K, [P]_q < 2^47)
       const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
-      acc[r] = -(double)nn[e] * pm;
+      L[r] = -(double)nn[e] * ((r & HB) ? pm1 : pm);
     }
   }
   // no `i < cnt` test: sources i >= cnt are zero tiles with zero constants
   // (a per-source branch makes the compiler serialise the words)
 #pragma unroll
   for (int i = 0; i < MAXA; ++i) {
-    {
-      const u64* si = src + i * TILE;
-      if (src_is_f64<SRC, MAXA>(sf64, i)) {
+    const u64* si = src + i * TILE;
+    if (src_is_f64<SRC, MAXA>(sf64, i)) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
-          acc[r] = __dadd_rn(acc[r], mulmod_f64(__longlong_as_double((long long)si[e]), C[i].w, C[i].wq, P.qd));
-        }
-      } else if (kWideInt && i % 3 == 0) {  // one wide source in three: the pipes balance
-        // 60-bit source on the integer pipe (idle in this FP64-bound kernel):
-        // Shoup product [x w]_p in [0, 2p), exact in a double (p < 2^47) --
-        // 2 FP64 ops instead of the two 30-bit-half mulmods' 16
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
-          const u64 y = shoup_lazy(si[e], C[i].sw, C[i].swp, P.q);
-          acc[r] = __dadd_rn(acc[r], __longlong_as_double((long long)u64_to_f64bits(y)));
-        }
-      } else {  // 60-bit source: x = xh 2^30 + xl
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
-          const u64 v = si[e];
-          const double xh = __dsub_rn(__longlong_as_double((long long)((v >> 30) | 0x4330000000000000ull)), kTwo52);
-          const double xl =
-              __dsub_rn(__longlong_as_double((long long)((v & 0x3FFFFFFFull) | 0x4330000000000000ull)), kTwo52);
-          acc[r] = __dadd_rn(acc[r], mulmod_f64(xh, C[i].w30, C[i].w30q, P.qd));
-          acc[r] = __dadd_rn(acc[r], mulmod_f64(xl, C[i].w, C[i].wq, P.qd));
-        }
+      for (int r = 0; r < 16; ++r) {
+        const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
+        const double xv = __longlong_as_double((long long)si[e]);
+        const double w = (r & HB) ? C[i].w1 : C[i].w;
+        const double sn = __fma_rn(xv, w, S[r]);
+        const double l = __fma_rn(xv, w, -__dsub_rn(sn, S[r]));
+        L[r] = lset ? __dadd_rn(L[r], l) : l;
+        S[r] = sn;
       }
+      lset = true;
+    } else if (kWideInt && i % 3 == 0) {  // one wide source in three: the pipes balance
+      // 60-bit source on the integer pipe (idle in this FP64-bound kernel):
+      // Shoup product [x w]_p in [0, 2p), exact in a double (p < 2^47)
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
+        const u64 y = (r & HB) ? shoup_lazy(si[e], C[i].sw1, C[i].swp1, P.q) : shoup_lazy(si[e], C[i].sw, C[i].swp, P.q);
+        const double yd = __longlong_as_double((long long)u64_to_f64bits(y));
+        L[r] = lset ? __dadd_rn(L[r], yd) : yd;
+      }
+      lset = true;
+    } else {  // 60-bit source: x = xh 2^30 + xl
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int e = eb[r >> WW] | ((r & ((1 << WW) - 1)) << lowbits);
+        const u64 v = si[e];
+        const double xh = __dsub_rn(__longlong_as_double((long long)((v >> 30) | 0x4330000000000000ull)), kTwo52);
+        const double xl =
+            __dsub_rn(__longlong_as_double((long long)((v & 0x3FFFFFFFull) | 0x4330000000000000ull)), kTwo52);
+        const double wa = (r & HB) ? C[i].w301 : C[i].w30, wb = (r & HB) ? C[i].w1 : C[i].w;
+        const double s1 = __fma_rn(xh, wa, S[r]);
+        const double l1 = __fma_rn(xh, wa, -__dsub_rn(s1, S[r]));
+        const double s2 = __fma_rn(xl, wb, s1);
+        const double l2 = __fma_rn(xl, wb, -__dsub_rn(s2, s1));
+        L[r] = lset ? __dadd_rn(L[r], __dadd_rn(l1, l2)) : __dadd_rn(l1, l2);
+        S[r] = s2;
+      }
+      lset = true;
     }
   }
 #pragma unroll
-  for (int r = 0; r < 16; ++r) x[r] = (u64)__double_as_longlong(acc[r]);
+  for (int r = 0; r < 16; ++r) {
+    const double H = __dsub_rn(S[r], cs);
+    const double qf = __dsub_rn(__fma_rn(H, P.qinv_d, kRound), kRound);
+    const double rr = __fma_rn(-qf, P.qd, H);
+    x[r] = (u64)__double_as_longlong(__dadd_rn(rr, L[r]));
+  }
 }
 
 // one target limb of the tile: conversion into registers, forward COL stages,
@@ -193,8 +237,8 @@ __device__ __forceinline__ void bconv_tile_f64(u64 (&x)[16], const u64* src, con
 template <int S, int OB, bool F64, int MAXA, int SRC, bool CEN = false>
 __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, const bool (&sf64)[MAXA],
                                              const BconvC (&C)[MAXA], const PrimeConst& P, u64* base,
-                                             int tile, int logn, const unsigned char* nn = nullptr,
-                                             double pm = 0.0) {
+                                             int tile, int logn, double cs, const unsigned char* nn = nullptr,
+                                             double pm = 0.0, double pm1 = 0.0) {
   constexpr int TILE = 1 << (S + OB);
   constexpr int NG = Sched<S>::G + (Sched<S>::R ? 1 : 0);
   const int t = threadIdx.x;
@@ -223,8 +267,11 @@ __device__ __forceinline__ void modup_target(const u64* src, u64* sm, int cnt, c
       if (!(F64 && firstg)) x[r] = firstg ? bconv_word<F64, MAXA, SRC>(src + e, TILE, cnt, sf64, C, P) \
                                           : sm[swz<false>(e)];                               \
     }                                                                                        \
-    if (F64 && firstg) bconv_tile_f64<WW, MAXA, SRC, TILE, CEN>(x, src, eb, lowbits, cnt, sf64, C, P, nn, pm); \
-    if (F64)                                                                                 \
+    if (F64 && firstg)                                                                       \
+      bconv_tile_f64<WW, MAXA, SRC, TILE, CEN>(x, src, eb, lowbits, cnt, sf64, C, P, nn, pm, pm1, cs); \
+    if (F64 && firstg)                                                                       \
+      ntt_group_f64<true, false, S, OB, WW, true>(x, jb, g0, logn, twf, nullptr, P, false);   \
+    else if (F64)                                                                            \
       ntt_group_f64<true, false, S, OB, WW>(x, jb, g0, logn, twf, nullptr, P, false);         \
     else                                                                                     \
       ntt_group<true, false, S, WW>(x, jb, g0, logn, tw, P, false);                          \
@@ -332,6 +379,7 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? HX_MODUP_MINB
 
   const int* tl = A.tlist + A.toff[d];
   const BconvC* bcd = A.bc + A.bc_off[d];
+  const double cs = A.cs_round;
   u64* dout = A.out + (b * A.dnum + d) * (long long)A.ext * N;
 #pragma unroll 1
   for (int k = k_lo; k < min(k_hi, nt_all); ++k) {
@@ -344,24 +392,24 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, (OB >= 3 ? HX_MODUP_MINB
       if (i < cnt)
         C[i] = bcd[(long long)j * A.alpha + i];
       else
-        C[i] = BconvC{0.0, 0.0, 0.0, 0.0, 0ull, 0ull};
+        C[i] = BconvC{0.0, 0.0, 0.0, 0.0, 0ull, 0ull, 0.0, 0.0, 0ull, 0ull};
     }
     u64* base = dout + (long long)j * N;
     __syncthreads();  // the previous target's last exchange reads are done
     if (CEN) {  // ModDown
-      const double pm = A.pmf[pj];
+      const double pm = A.pmf[pj], pm1 = A.pmf1[pj];
       if (mode == 0)
-        modup_target<S, OB, true, MAXA, 0, true>(src, sm, cnt, sf64, C, P, base, tile, logn, nn, pm);
+        modup_target<S, OB, true, MAXA, 0, true>(src, sm, cnt, sf64, C, P, base, tile, logn, cs, nn, pm, pm1);
       else if (mode == 3)
-        modup_target<S, OB, true, MAXA, 3, true>(src, sm, cnt, sf64, C, P, base, tile, logn, nn, pm);
+        modup_target<S, OB, true, MAXA, 3, true>(src, sm, cnt, sf64, C, P, base, tile, logn, cs, nn, pm, pm1);
       else
-        modup_target<S, OB, true, MAXA, 2, true>(src, sm, cnt, sf64, C, P, base, tile, logn, nn, pm);
+        modup_target<S, OB, true, MAXA, 2, true>(src, sm, cnt, sf64, C, P, base, tile, logn, cs, nn, pm, pm1);
     } else if (mode == 0) {
-      modup_target<S, OB, true, MAXA, 0>(src, sm, cnt, sf64, C, P, base, tile, logn);
+      modup_target<S, OB, true, MAXA, 0>(src, sm, cnt, sf64, C, P, base, tile, logn, cs);
     } else if (mode == 1) {
-      modup_target<S, OB, true, MAXA, 1>(src, sm, cnt, sf64, C, P, base, tile, logn);
+      modup_target<S, OB, true, MAXA, 1>(src, sm, cnt, sf64, C, P, base, tile, logn, cs);
     } else {
-      modup_target<S, OB, true, MAXA, 2>(src, sm, cnt, sf64, C, P, base, tile, logn);
+      modup_target<S, OB, true, MAXA, 2>(src, sm, cnt, sf64, C, P, base, tile, logn, cs);
     }
   }
 #pragma unroll 1

@@ -189,7 +189,10 @@ __device__ __forceinline__ int row_tw_offset(int beta) {
 }
 __device__ __forceinline__ int row_tw_pad(int k) { return k + (k >> 4); }
 
-template <bool FWD, bool ROW, int S, int OB, int W>
+// SKIP1 (forward only): the group's first stage (pair bit W-1) multiplies
+// nothing -- its lower inputs arrive premultiplied by the stage's twiddle
+// (the fused ModUp / ModDown conversion, hx_modup.cuh)
+template <bool FWD, bool ROW, int S, int OB, int W, bool SKIP1 = false>
 __device__ __forceinline__ void ntt_group_f64(u64 (&x)[16], const int (&jb)[16 >> W], int g0, int logn,
                                               const double* __restrict__ tw, const double* sm_tw,
                                               const PrimeConst& P, bool last_stage_inv) {
@@ -210,7 +213,7 @@ __device__ __forceinline__ void ntt_group_f64(u64 (&x)[16], const int (&jb)[16 >
         const unsigned j = (unsigned)jb[ro] + ((unsigned)(hp << (i + 1)) << (logb + g0));
         const bool fin = (!FWD) && last_stage_inv && (beta == logn - 1);
         double wt = 0.0;
-        if (!fin) {
+        if (!fin && !(SKIP1 && i == W - 1)) {
           if (ROW)
             wt = sm_tw[row_tw_offset<S, OB>(beta) + row_tw_pad((int)((j & ((1u << (S + OB)) - 1)) >> (beta + 1)))];
           else
@@ -241,7 +244,10 @@ __device__ __forceinline__ void ntt_group_f64(u64 (&x)[16], const int (&jb)[16 >
         for (int lp = 0; lp < (1 << i); ++lp) {
           const int r0 = rb | lp, r1 = r0 | (1 << i);
           const double X = v[r0], Y = v[r1];
-          if (FWD) {
+          if (FWD && SKIP1 && i == W - 1) {
+            v[r0] = __dadd_rn(X, Y);
+            v[r1] = __dsub_rn(X, Y);
+          } else if (FWD) {
             const double T = mulmod_f64h(Y, wt, P.qinv_d, q);
             v[r0] = __dadd_rn(X, T);
             v[r1] = __dsub_rn(X, T);

@@ -323,10 +323,48 @@ bool launch_modup_col(hx_ctx* c, const hx::ModUpColArgs& A, long long batch, cud
   return A.centred ? launch_modup_col_c<true>(c, A, batch, s) : launch_modup_col_c<false>(c, A, batch, s);
 }
 
+// Rounding constant 1.5 * 2^E of the fused conversion's joint reduction
+// (hx_modup.cuh bconv_tile_f64) for source primes `sr` and FP64-class target
+// primes `tg` (prime indices), `cen` centred-correction terms of up to p each;
+// 0.0 when an exactness bound fails (the caller then takes the unfused path):
+//   sum of the products  < 2^(E-1)           (the running sum keeps its binade)
+//   |H / p| < 2^50                            (the rint range of the one quotient)
+//   low parts + integer-pipe terms + centred terms, and the NTT's lazy growth
+//   on top of the converted words, stay below 2^52
+double bconv_round(const hx_ctx* c, const std::vector<int>& sr, const std::vector<int>& tg, int cen) {
+  long double pmax = 0, pmin = 0, per_p = 0;
+  int nprod = 0, nwide = 0;
+  for (int j : tg) {
+    const long double p = (long double)c->primes[j];
+    pmax = std::max(pmax, p);
+    pmin = pmin == 0 ? p : std::min(pmin, p);
+  }
+  for (int i : sr) {
+    if (c->f64[i]) {
+      per_p += (long double)c->primes[i];
+      nprod += 1;
+    } else {  // x = xh 2^30 + xl, q < 2^62 (or one Shoup product in [0, 2p) on the integer pipe)
+      per_p += 4294967296.0L + 1073741824.0L;
+      nprod += 2;
+      nwide += 1;
+    }
+  }
+  int E = 0;
+  std::frexp((double)(per_p * pmax), &E);  // per_p pmax < 2^E
+  E += 1;
+  int lmin = 0;
+  std::frexp((double)pmin, &lmin);         // pmin >= 2^(lmin - 1)
+  if (E - 1 - (lmin - 1) > 50 || E > 1000) return 0.0;
+  const long double lb = (long double)nprod * std::ldexp(1.0L, E - 53) + (2.0L * nwide + cen) * pmax;
+  const long double word = pmax + lb;  // |r| < p
+  if (2.0L * word + (long double)c->logn * pmax >= std::ldexp(1.0L, 52)) return 0.0;
+  return std::ldexp(1.5, E);
+}
+
 bool modup_fused_ok(const hx_ctx* c, int n_q) {
   static const bool off = getenv("HX_MODUP_UNFUSED") != nullptr;
   const int a = hx::ntt_split_a(c->logn);
-  return !off && a >= 5 && a <= 8 && c->alpha <= 4 && c->dnum(n_q) <= hx::kMaxDigits;
+  return !off && a >= 5 && a <= 8 && c->alpha <= 4 && c->dnum(n_q) <= hx::kMaxDigits && c->cs_up[n_q] != 0.0;
 }
 
 // c1: [batch] polys of n_q limbs at stride c1_stride words.
@@ -383,6 +421,7 @@ void modup(hx_ctx* c, u64* digits, const u64* c1, long long c1_stride, long long
     A.src_n = n_q;
     A.src_pbase = 0;
     A.centred = 0;
+    A.cs_round = c->cs_up[n_q];
     LimbTable lt{};
     lt.stride = dnum * ext;
     for (int d = 0; d < dnum; ++d) {
@@ -659,7 +698,7 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
   static const bool col_off = getenv("HX_MODDOWN_COL_OFF") != nullptr;
   const int sa = hx::ntt_split_a(c->logn);
   bool col_done = false;
-  if (!unfused && !col_off && K >= 1 && K <= 4 && sa >= 5 && sa <= 8) {
+  if (!unfused && !col_off && K >= 1 && K <= 4 && sa >= 5 && sa <= 8 && c->cs_down[n_q] != 0.0) {
     // conversion P -> Q fused into the forward COL pass of the FP64-class
     // targets (modup_col_kernel, centred mode); integer-class targets are
     // written in the coefficient domain for their ordinary passes
@@ -685,6 +724,8 @@ void moddown(hx_ctx* c, u64* out, long long out_stride, const u64* u, long long 
     A.src_pbase = c->n_chain;
     A.centred = 1;
     A.pmf = c->d_pmodqf;
+    A.pmf1 = c->d_pmodqf1;
+    A.cs_round = c->cs_down[n_q];
     A.pmu = c->d_pmodq;
     HX_REQUIRE(launch_modup_col(c, A, polys, s), "moddown: fused conversion unavailable");
     col_done = true;
@@ -1190,6 +1231,13 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
                 e.w30q = (double)w30 / (double)m;
                 e.sw = w.w;
                 e.swp = w.wp;
+                // premultiplied by the target's first forward twiddle psi^(N/2)
+                const u64 tw1 = hpow(c->psi[pj], N / 2, m);
+                const SC w1 = sc(hmul(prod, tw1, m), m);
+                e.w1 = (double)w1.w;
+                e.w301 = (double)hmul(w30, tw1, m);
+                e.sw1 = w1.w;
+                e.swp1 = w1.wp;
               }
               bc.push_back(e);
             }
@@ -1254,10 +1302,12 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
     }
     {  // fused ModDown conversion + COL pass tables (modup_col_kernel, centred)
       std::vector<hx::BconvC> mb((size_t)n_chain * n_special);
-      std::vector<double> pmf(n_chain);
+      std::vector<double> pmf(n_chain), pmf1(n_chain);
       for (int j = 0; j < n_chain; ++j) {
         const u64 q = c->primes[j];
         pmf[j] = (double)pmodq[j];
+        const u64 tw1 = hpow(c->psi[j], N / 2, q);  // first forward twiddle
+        pmf1[j] = (double)hmul(pmodq[j], tw1, q);
         for (int k = 0; k < n_special; ++k) {
           const SC w = pconv[(size_t)k * n_chain + j];
           const u64 w30 = hmul(w.w, (1ull << 30) % q, q);
@@ -1268,6 +1318,11 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
           e.w30q = (double)w30 / (double)q;
           e.sw = w.w;
           e.swp = w.wp;
+          const SC w1 = sc(hmul(w.w, tw1, q), q);
+          e.w1 = (double)w1.w;
+          e.w301 = (double)hmul(w30, tw1, q);
+          e.sw1 = w1.w;
+          e.swp1 = w1.wp;
         }
       }
       std::vector<int> tl;
@@ -1286,6 +1341,33 @@ hx_ctx* hx_ctx_create(int logn, const uint64_t* chain, int n_chain, const uint64
       c->d_mdbc = upload(mb);
       c->d_mdtl = upload(tl);
       c->d_pmodqf = upload(pmf);
+      c->d_pmodqf1 = upload(pmf1);
+      // rounding constants of the joint conversion (hx_modup.cuh bconv_tile_f64)
+      c->cs_up.assign(n_chain + 1, 0.0);
+      c->cs_down.assign(n_chain + 1, 0.0);
+      for (int nq = 1; nq <= n_chain; ++nq) {
+        std::vector<int> tg, sr;
+        const int dn = c->dnum(nq);
+        double up = -1.0;
+        for (int d = 0; d < dn && up != 0.0; ++d) {
+          const int lo = d * alpha, cnt = std::min(alpha, nq - lo);
+          tg.clear();
+          sr.clear();
+          for (int i = lo; i < lo + cnt; ++i) sr.push_back(i);
+          for (int j = 0; j < nq + n_special; ++j)
+            if (!(j >= lo && j < lo + cnt) && c->f64[c->pidx(j, nq)]) tg.push_back(c->pidx(j, nq));
+          if (tg.empty()) continue;
+          const double r = bconv_round(c.get(), sr, tg, 0);
+          up = (r == 0.0) ? 0.0 : std::max(up, r);
+        }
+        c->cs_up[nq] = up < 0.0 ? 1.0 : up;  // no FP64-class target at all: unused
+        tg.clear();
+        sr.clear();
+        for (int k = 0; k < n_special; ++k) sr.push_back(n_chain + k);
+        for (int j = 0; j < nq; ++j)
+          if (c->f64[j]) tg.push_back(j);
+        c->cs_down[nq] = tg.empty() ? 1.0 : bconv_round(c.get(), sr, tg, n_special);
+      }
     }
     c->d_pinv = upload(pinv);
     // Rescale constants
@@ -1339,7 +1421,8 @@ void hx_ctx_destroy(hx_ctx* c) {
                   (void*)c->d_pconvf,
                   (void*)c->d_pconv, (void*)c->d_pmodq, (void*)c->d_pinv, (void*)c->d_qlinv,
                   (void*)c->d_qlmod, (void*)c->d_maclimbs, (void*)c->d_kslimbs, (void*)c->d_bconv,
-                  (void*)c->d_tlist, (void*)c->d_mdbc, (void*)c->d_mdtl, (void*)c->d_pmodqf})
+                  (void*)c->d_tlist, (void*)c->d_mdbc, (void*)c->d_mdtl, (void*)c->d_pmodqf,
+                  (void*)c->d_pmodqf1})
     if (p) cudaFree(p);
   if (c->arena.base) {
     cudaDeviceSynchronize();
