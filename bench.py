@@ -392,6 +392,10 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=128):
     W2 = rng.normal(0.0, 0.02, (3072, 768))
     prune_rng = np.random.default_rng(20251211 * 10 + 3 + 200)
     jobs = [("ffn_w1", W1.T.copy(), 1024, False, BSGS), ("ffn_w1_pruned90", W1.T.copy(), 1024, True, BSGS),
+            # the same matrix on the cost-tuned split (BsgsPlan::for_cost: 3 row
+            # blocks share the baby steps, so n1 = 64, n2 = 16: 63 + 45 key
+            # switches instead of 31 + 93)
+            ("ffn_w1_cost_plan", W1.T.copy(), 1024, False, BSGS, -1),
             # the 3 row blocks stacked in one set of full-length diagonals: one
             # output ciphertext, (n1-1)+(n2-1) = 62 key switches instead of 124
             ("ffn_w1_stacked", W1.T.copy(), 1024, False, BSGS_STACKED)]
@@ -400,7 +404,8 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=128):
     only = getattr(args, "only", None)
     if only:
         jobs = [j for j in jobs if j[0] in only]
-    for name, M, d, prune, method in jobs:  # y = x W  ->  M = W^T (out x in)
+    for name, M, d, prune, method, *plan_n1 in jobs:  # y = x W  ->  M = W^T (out x in)
+        plan_n1 = plan_n1[0] if plan_n1 else int(os.environ.get("HX_BENCH_N1", "0"))
         # each layer in its own backend (its own keys, matrix and scratch): the
         # previous layer's 14-28 GB of rotation keys and pool blocks would
         # otherwise crowd the token batches' working set (allocation retries)
@@ -415,7 +420,7 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=128):
         xs = np.tile(np.concatenate([x, np.zeros(d - M.shape[1])]), be.slots // d)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        mat = be.prepare(method, M, lvl)
+        mat = be.prepare(method, M, lvl, plan_n1)
         be.gen_rotation_keys(mat.rotations())
         torch.cuda.synchronize()
         prep = time.perf_counter() - t0
@@ -491,16 +496,34 @@ def sharded_bsgs_bench(torch, dist, chain, special, rank, world, rows=11008, col
     from paper_2512_11135_b200.shard import sharded_matvec
 
     rng = np.random.default_rng(20251211 * 10 + 5)
-    be = Backend(params_json(LOGN, chain, special, ALPHA, 40), seed=5)  # same seed: same keys on every rank
-    W = rng.normal(0.0, 0.02, (rows, cols))
-    x = rng.uniform(-1, 1, cols)
-    lvl = be.max_level
-    t0 = time.perf_counter()
-    M = be.prepare_shard(W, lvl, rank, world, stacked=True)  # 4096 stacked diagonals split by giant group
-    be.gen_rotation_keys(M.rotations())
-    torch.cuda.synchronize()
-    prep = time.perf_counter() - t0
-    ct = be.encrypt(np.tile(x, be.slots // cols), lvl)
+    # every rank finishes its local set-up (diagonals, keys: ~25 GB) before any
+    # collective is entered, and the ranks agree that all of them did: a rank
+    # that failed locally (e.g. out of memory next to a neighbour's process)
+    # would otherwise leave the others waiting in the all-reduce until the
+    # NCCL watchdog aborts the job and the headline line is lost
+    be, fail = None, ""
+    try:
+        be = Backend(params_json(LOGN, chain, special, ALPHA, 40), seed=5)  # same seed: same keys on every rank
+        W = rng.normal(0.0, 0.02, (rows, cols))
+        x = rng.uniform(-1, 1, cols)
+        lvl = be.max_level
+        t0 = time.perf_counter()
+        M = be.prepare_shard(W, lvl, rank, world, stacked=True)  # 4096 stacked diagonals split by giant group
+        be.gen_rotation_keys(M.rotations())
+        torch.cuda.synchronize()
+        prep = time.perf_counter() - t0
+        ct = be.encrypt(np.tile(x, be.slots // cols), lvl)
+    except Exception as exc:  # noqa: BLE001 -- reported in the JSON line
+        fail = f"rank {rank}: {exc}"[:200]
+    if world > 1:
+        ok = torch.tensor([0 if fail else 1], device="cuda", dtype=torch.int32)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            if be is not None:
+                be.close()
+            return {"sharded_bsgs_config5": {"error": fail or "set-up failed on another rank"}}
+    elif fail:
+        raise RuntimeError(fail)
     allreduce = (lambda t: dist.all_reduce(t)) if world > 1 else (lambda t: None)
     outs, rep = sharded_matvec(be, M, ct, lvl + 1, len(special), allreduce, torch, world, chain + special)  # warm-up + correctness
     y = be.decrypt(outs[0])[:rows]  # stacked: one output, y[row] in slot row
@@ -654,7 +677,10 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HX_BENCH_DEVICE / HX_BENCH_DIST_BACKEND=gloo: run the multi-rank code path
+    # with every rank on one GPU (NCCL refuses two ranks per device) -- a check of
+    # the glue on a single-GPU box (tools/gpu/r02_world2.sh), never a reported number
+    local = int(os.environ.get("HX_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -662,7 +688,11 @@ def main():
 
         # a rank that fails inside a collective extra must not hang the others for
         # the default 10 minutes: the NCCL watchdog aborts after 5
-        dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(minutes=5))
+        backend = os.environ.get("HX_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev, timeout=datetime.timedelta(minutes=5))
+        else:
+            dist.init_process_group(backend, timeout=datetime.timedelta(minutes=5))
 
     chain, special = primes()
     ctx = Context(LOGN, chain, special, ALPHA)
@@ -787,19 +817,35 @@ def main():
     ntt_secs = time_loop(torch, lambda: ctx.ntt_fwd(ntt_buf, 2 * BATCH, nq, 0, stream), 3, 1, stream)
     ntt_limbs = 2 * BATCH * nq
     extras = {"limb_ntt_per_s": ntt_limbs / (ntt_secs / 3)}
-    if not args.no_extras:
+    # the key-switch extras need a second ~50 GB scratch arena: skipped when the
+    # ranks share one GPU (HX_BENCH_DEVICE, the single-GPU check of the multi-rank
+    # glue); an extra that fails is reported in its place and never costs the line
+    ks_extras = not args.no_extras and "HX_BENCH_DEVICE" not in os.environ
+
+    def guarded_extra(name, fn):
+        try:
+            fn()
+        except Exception as exc:  # noqa: BLE001
+            extras[name] = {"error": str(exc)[:200]}
+            torch.cuda.synchronize()
+
+    def extra_fp64_specials():
         # the same batch-256 key switch with 3 special primes < 2^47 (FP64 class):
         # every limb but q0 on the FP64 pipe
         chain47, special47 = primes(fp64_specials=True)
         ctx47 = Context(LOGN, chain47, special47, ALPHA)
-        key47 = make_key(torch, ctx47, gen, chain47, special47, g1, dev)
-        ks47 = time_loop(torch, lambda: ctx47.rotate(out, cts, key47, BATCH, nq, g1, stream), 3, 2, stream)
-        extras["ks_per_s_fp64_specials"] = {"value": BATCH * 3 / ks47, "unit": "KS/s",
-                                            "special_bits": [p.bit_length() for p in special47],
-                                            "log2_P": sum(p.bit_length() - 1 for p in special47) + 3}
-        del key47
-        ctx47.trim()
-        del ctx47
+        try:
+            key47 = make_key(torch, ctx47, gen, chain47, special47, g1, dev)
+            ks47 = time_loop(torch, lambda: ctx47.rotate(out, cts, key47, BATCH, nq, g1, stream), 3, 2, stream)
+            extras["ks_per_s_fp64_specials"] = {"value": BATCH * 3 / ks47, "unit": "KS/s",
+                                                "special_bits": [p.bit_length() for p in special47],
+                                                "log2_P": sum(p.bit_length() - 1 for p in special47) + 3}
+            del key47
+        finally:
+            ctx47.trim()
+
+    if ks_extras:
+        guarded_extra("ks_per_s_fp64_specials", extra_fp64_specials)
     # the linear transform's HBM-bound kernel: the BSGS diagonal MAC at the
     # FFN W1 block shape (n1 = n2 = 32, 24 limbs), diagonals streamed once
     del ntt_buf
@@ -827,13 +873,14 @@ def main():
                            "u64_equivalent_GBps": mac_bytes / p40_s / 1e9,
                            "speedup_vs_u64_mac": mac_s / p40_s}
     del baby, diags, inner, pk
-    if not args.no_extras:
+    def extra_hmult():
         # HMult + relin over the batch
         rlk = make_key(torch, ctx, gen, chain, special, 0, dev)
         b2 = rand_limbs(torch, gen, chain, (BATCH, 2), dev)
         hm = time_loop(torch, lambda: ctx.mul_relin(out, cts, b2, rlk, BATCH, nq, stream), 2, 2, stream)
         extras["hmult_relin_per_s"] = BATCH * 2 / hm
-        del b2
+
+    def extra_hoisted():
         # 32-rotation hoisted batch with 32 DISTINCT rotation keys (amounts
         # 1..32, 7.2 GB), in chunks of HOIST_CHUNK ciphertexts
         gs = [pow(5, k, 2 * N) for k in range(1, HOIST_R + 1)]
@@ -847,7 +894,10 @@ def main():
         hs = time_loop(torch, hoist, 1, 2, stream)
         extras["hoisted32_ks_per_s"] = BATCH * HOIST_R / hs
         extras["hoisted32_keys"] = "32 distinct rotation keys (amounts 1..32)"
-        del hout, keys
+
+    if ks_extras:
+        guarded_extra("hmult_relin_per_s", extra_hmult)
+        guarded_extra("hoisted32_ks_per_s", extra_hoisted)
 
     # ---- e2e through the host-buffer C-ABI entry point ----
     hin = torch.empty(cts.shape, dtype=torch.int64, pin_memory=True)
@@ -890,30 +940,36 @@ def main():
         torch.cuda.synchronize()
         ctx.trim()  # the headline's ~50 GB scratch arena is not needed by the extras
         torch.cuda.empty_cache()
-        extras.update(ffn_bsgs_bench(torch, chain, special, args))
-        torch.cuda.empty_cache()
-        # config 4: level sweep (3 / 4 / 24 limbs), one head and the 12-head batch
-        for nql in (3, 4, 24):
+        # the single-GPU workloads (configs 3 / 4 / 5-stacked) are reported by the
+        # N = 1 run; a multi-rank run keeps to the headline and the sharded transform
+        if world == 1:
             try:
-                extras[f"matmul_d128_l{nql}"] = matmul_bench(torch, chain, special, n_q=nql,
-                                                             iters=1 if nql == 24 else 2)
+                extras.update(ffn_bsgs_bench(torch, chain, special, args))
             except Exception as exc:  # reported, never fatal for the headline line
-                extras[f"matmul_d128_l{nql}"] = {"error": str(exc)[:200]}
+                extras["ffn_bsgs"] = {"error": str(exc)[:200]}
             torch.cuda.empty_cache()
-        # the same matmul with FP64-class special primes (parameter co-design:
-        # at a 4-limb level the 60-bit specials' integer passes dominate)
-        try:
-            chain47, special47 = primes(fp64_specials=True)
-            mm = matmul_bench(torch, chain47, special47, heads=0)
-            mm["special_bits"] = [int(p).bit_length() for p in special47]
-            extras["matmul_d128_l4_fp64_specials"] = mm
-        except Exception as exc:
-            extras["matmul_d128_l4_fp64_specials"] = {"error": str(exc)[:200]}
-        torch.cuda.empty_cache()
-        try:
-            extras.update(config5_stacked_bench(torch, chain, special))
-        except Exception as exc:
-            extras["config5_stacked_1gpu"] = {"error": str(exc)[:200]}
+            # config 4: level sweep (3 / 4 / 24 limbs), one head and the 12-head batch
+            for nql in (3, 4, 24):
+                try:
+                    extras[f"matmul_d128_l{nql}"] = matmul_bench(torch, chain, special, n_q=nql,
+                                                                 iters=1 if nql == 24 else 2)
+                except Exception as exc:  # reported, never fatal for the headline line
+                    extras[f"matmul_d128_l{nql}"] = {"error": str(exc)[:200]}
+                torch.cuda.empty_cache()
+            # the same matmul with FP64-class special primes (parameter co-design:
+            # at a 4-limb level the 60-bit specials' integer passes dominate)
+            try:
+                chain47, special47 = primes(fp64_specials=True)
+                mm = matmul_bench(torch, chain47, special47, heads=0)
+                mm["special_bits"] = [int(p).bit_length() for p in special47]
+                extras["matmul_d128_l4_fp64_specials"] = mm
+            except Exception as exc:
+                extras["matmul_d128_l4_fp64_specials"] = {"error": str(exc)[:200]}
+            torch.cuda.empty_cache()
+            try:
+                extras.update(config5_stacked_bench(torch, chain, special))
+            except Exception as exc:
+                extras["config5_stacked_1gpu"] = {"error": str(exc)[:200]}
         if world > 1:  # per-block config 5 needs >= 2 GPUs of memory (183 GB of diagonals + keys)
             torch.cuda.empty_cache()
             try:

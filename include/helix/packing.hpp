@@ -32,6 +32,17 @@ struct BsgsPlan {
   int n1 = 1, n2 = 1;
   // default: n1 = n2 = sqrt(d) for an even power of two, else n1 = sqrt(2d), n2 = d / n1
   static BsgsPlan for_dim(int d);
+  // Extension beyond the SPEC default: the split that minimises the key-switch
+  // cost (n1 - 1) baby + row_blocks (n2 - 1) giant of a matrix with
+  // `row_blocks` output blocks sharing the baby steps.  Hoisted baby steps
+  // share one ModUp and pay inner product + ModDown each; double-hoisted giant
+  // steps pay ModUp + inner product each, so with B > 1
+  // row blocks a longer baby side wins (config 3 W1, B = 3: n1 = 64, n2 = 16
+  // instead of 32 x 32).  The default cost ratio is the measured one on B200
+  // (hoisted rotation 88 us, ModUp + inner product 144 us at N = 2^16, 24
+  // limbs); n1 is capped at max_n1 (baby ciphertexts held in HBM at once).
+  static BsgsPlan for_cost(int d, int row_blocks, double baby_cost = 88.0, double giant_cost = 144.0,
+                           int max_n1 = 256);
 };
 
 struct PackedMatrix {

@@ -76,6 +76,12 @@ hxc_ct* hxc_rotate_and_sum(hxc_backend* b, const hxc_ct* x, int64_t span, int64_
  * rows x cols row-major matrix at `level` (encoding is not part of a matvec). */
 hxc_mat* hxc_matrix_prepare(hxc_backend* b, int method, const double* A, int rows, int cols,
                             int level);
+/* The same with an explicit BSGS split (helix::pack_bsgs(A, plan, n),
+ * linalg.hpp:82): n1 = 0 the SPEC default (BsgsPlan::for_dim), n1 > 0 that
+ * baby-step count (a power of two <= d, n2 = d / n1), n1 < 0 the
+ * cost-tuned split BsgsPlan::for_cost(d, row_blocks). */
+hxc_mat* hxc_matrix_prepare_plan(hxc_backend* b, int method, const double* A, int rows, int cols,
+                                 int level, int n1);
 void hxc_matrix_free(hxc_mat* m);
 /* d, n1, n2, row_blocks, nonzero payloads */
 int hxc_matrix_info(const hxc_mat* m, int* d, int* n1, int* n2, int* blocks, int* nonzero);

@@ -138,16 +138,37 @@ hxc_ct* hxc_rotate_and_sum(hxc_backend* b, const hxc_ct* x, int64_t span, int64_
 }
 
 hxc_mat* hxc_matrix_prepare(hxc_backend* b, int method, const double* A, int rows, int cols, int level) {
+  return hxc_matrix_prepare_plan(b, method, A, rows, cols, level, 0);
+}
+
+hxc_mat* hxc_matrix_prepare_plan(hxc_backend* b, int method, const double* A, int rows, int cols, int level,
+                                 int n1) {
   return guard<hxc_mat*>(nullptr, [&] {
     Matrix M(rows, cols);
     std::memcpy(M.data.data(), A, sizeof(double) * (std::size_t)rows * cols);
     const std::size_t n = b->b->slots();
     static const bool trace = getenv("HX_PREP_TRACE") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
+    const bool bsgs = method == HXC_BSGS || method == HXC_BSGS_STACKED;
+    if (n1 != 0 && !bsgs) throw std::invalid_argument("hxc_matrix_prepare_plan: n1 applies to the BSGS methods");
+    BsgsPlan plan;
+    if (bsgs) {
+      const int d = next_pow2(std::max(cols, 1));
+      const int blocks = method == HXC_BSGS_STACKED ? 1 : std::max(1, (rows + d - 1) / d);
+      if (n1 == 0) {
+        plan = BsgsPlan::for_dim(d);
+      } else if (n1 < 0) {
+        plan = BsgsPlan::for_cost(d, blocks);
+      } else {
+        if ((n1 & (n1 - 1)) || n1 > d) throw std::invalid_argument("hxc_matrix_prepare_plan: n1 must be a power of two <= d");
+        plan.n1 = n1;
+        plan.n2 = d / n1;
+      }
+    }
     PackedMatrix P = method == HXC_ROW              ? pack_rows(M, n)
                      : method == HXC_DIAG           ? pack_diagonals(M, n)
-                     : method == HXC_BSGS_STACKED   ? pack_bsgs_stacked(M, n)
-                                                    : pack_bsgs(M, n);
+                     : method == HXC_BSGS_STACKED   ? pack_bsgs_stacked(M, plan, n)
+                                                    : pack_bsgs(M, plan, n);
     const auto t1 = std::chrono::steady_clock::now();
     auto* h = new hxc_mat;
     h->method = method;

@@ -21,6 +21,28 @@ BsgsPlan BsgsPlan::for_dim(int d) {
   return p;
 }
 
+BsgsPlan BsgsPlan::for_cost(int d, int row_blocks, double baby_cost, double giant_cost, int max_n1) {
+  if (d < 1 || (d & (d - 1))) throw std::invalid_argument("BsgsPlan: d must be a power of two");
+  if (row_blocks < 1 || !(baby_cost > 0.0) || !(giant_cost > 0.0))
+    throw std::invalid_argument("BsgsPlan::for_cost: row_blocks and the costs must be positive");
+  BsgsPlan best = for_dim(d);
+  auto cost = [&](const BsgsPlan& p) {
+    return (p.n1 - 1) * baby_cost + (double)row_blocks * (p.n2 - 1) * giant_cost;
+  };
+  double bc = cost(best);
+  for (int n1 = 1; n1 <= d && n1 <= max_n1; n1 <<= 1) {
+    BsgsPlan p;
+    p.n1 = n1;
+    p.n2 = d / n1;
+    const double c = cost(p);
+    if (c < bc) {  // ties keep the SPEC default
+      bc = c;
+      best = p;
+    }
+  }
+  return best;
+}
+
 std::size_t PackedMatrix::nonzero_payloads() const {
   std::size_t c = 0;
   for (const auto& p : payloads) c += !p.empty();

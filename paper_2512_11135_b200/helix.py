@@ -60,6 +60,7 @@ def lib():
         "hxc_mod_down": (v, [v, v, i32]),
         "hxc_rotate_and_sum": (v, [v, v, i64, i64, rp]),
         "hxc_matrix_prepare": (v, [v, i32, f64p, i32, i32, i32]),
+        "hxc_matrix_prepare_plan": (v, [v, i32, f64p, i32, i32, i32, i32]),
         "hxc_matrix_free": (None, [v]),
         "hxc_matrix_info": (i32, [v] + [C.POINTER(C.c_int)] * 5),
         "hxc_matrix_rotations": (i32, [v, C.POINTER(C.c_int64), i32]),
@@ -260,10 +261,12 @@ class Backend:
         c = Ct(self, self.L.hxc_rotate_and_sum(self.h, a.h, span, stride, C.byref(r)))
         return c, r.as_dict()
 
-    def prepare(self, method, A, level):
+    def prepare(self, method, A, level, n1=0):
+        """n1 (BSGS methods): 0 = the SPEC split (BsgsPlan::for_dim), > 0 = that many
+        baby steps, < 0 = the cost-tuned split (BsgsPlan::for_cost)"""
         A = np.ascontiguousarray(A, dtype=np.float64)
-        return Mat(self, self.L.hxc_matrix_prepare(self.h, method, A.ctypes.data_as(C.POINTER(C.c_double)),
-                                                   A.shape[0], A.shape[1], level), method)
+        return Mat(self, self.L.hxc_matrix_prepare_plan(self.h, method, A.ctypes.data_as(C.POINTER(C.c_double)),
+                                                        A.shape[0], A.shape[1], level, n1), method)
 
     def matvec(self, mat, x):
         r = Report()

@@ -226,6 +226,27 @@ int main() {
     CHECK((D.payloads[1] == std::vector<double>{2, 7, 12, 13}), "diag[1] = [2,7,12,13] (SPEC.md:275)");
     const auto B = pack_bsgs(A, BsgsPlan{2, 2}, 4);
     CHECK(B.payloads.size() == 4, "d=4, n1=n2=2 -> 4 payloads (SPEC.md:284)");
+    // cost-tuned split (an extension; the SPEC default stays for_dim)
+    {
+      const BsgsPlan one = BsgsPlan::for_cost(1024, 1), w1 = BsgsPlan::for_cost(1024, 3), w2 = BsgsPlan::for_cost(4096, 1);
+      CHECK(one.n1 == 32 && one.n2 == 32, "for_cost: one row block keeps the square split");
+      CHECK(w1.n1 == 64 && w1.n2 == 16, "for_cost: 3 row blocks sharing the baby steps -> n1 = 64, n2 = 16");
+      CHECK(w2.n1 == 64 && w2.n2 == 64, "for_cost: d = 4096, one block keeps 64 x 64");
+      const BsgsPlan tie = BsgsPlan::for_cost(8, 1, 1.0, 1.0), def8 = BsgsPlan::for_dim(8);
+      CHECK(tie.n1 == def8.n1 && tie.n2 == def8.n2, "for_cost: ties keep the SPEC default");
+      CHECK(BsgsPlan::for_cost(1024, 64, 88.0, 144.0, 64).n1 == 64, "for_cost: n1 capped at max_n1");
+      bool threw = false;
+      try {
+        (void)BsgsPlan::for_cost(12, 1);
+      } catch (const std::invalid_argument&) {
+        threw = true;
+      }
+      CHECK(threw, "for_cost: d must be a power of two");
+      for (int B2 = 1; B2 <= 8; ++B2) {
+        const BsgsPlan p = BsgsPlan::for_cost(256, B2);
+        CHECK(p.n1 * p.n2 == 256, "for_cost: n1 n2 = d");
+      }
+    }
     CHECK(B.payloads[0] == D.payloads[0] && B.payloads[1] == D.payloads[1], "j=0 group = plain diagonals");
     // pre-rotation consistency: rotate stored payload left by n1 j -> plain diagonal
     for (int i = 2; i < 4; ++i) {

@@ -121,11 +121,12 @@ def block_diag(A, b, i, d):
     return v if np.any(v != 0) else None
 
 
-def pack_bsgs(A, n):
-    """diag'_{n1 j + k} of block b = diag_{n1 j + k} rotated right by n1 j, replicated"""
+def pack_bsgs(A, n, n1=None):
+    """diag'_{n1 j + k} of block b = diag_{n1 j + k} rotated right by n1 j, replicated (SPEC.md:278-286);
+    n1: an explicit baby-step count (default: the SPEC split)"""
     rows, cols = A.shape
     d = next_pow2(max(cols, 1))
-    n1, n2 = bsgs_plan(d)
+    n1, n2 = bsgs_plan(d) if n1 is None else (n1, d // n1)
     blocks = (rows + d - 1) // d
     out = []
     for b in range(blocks):

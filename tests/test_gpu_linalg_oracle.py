@@ -187,6 +187,31 @@ def test_c2s_bsgs_multiblock_words_vs_oracle(stacked, prune):
     _bsgs_case(ov, A, ov.be.max_level, stacked)
 
 
+@pytest.mark.parametrize("n1,expect", [(-1, (32, 8)), (64, (64, 4)), (8, (8, 32))])
+def test_c2s_bsgs_explicit_plan_words_vs_oracle(n1, expect):
+    """a non-default BSGS split (hxc_matrix_prepare_plan): the cost-tuned one
+    (BsgsPlan::for_cost, 3 row blocks of d = 256 -> 32 x 8) and two explicit
+    ones, against the oracle driver run with the same n1, n2"""
+    from paper_2512_11135_b200.helix import BSGS
+
+    ov = view("c2s")
+    be = ov.be
+    lvl = be.max_level
+    rng = np.random.default_rng(300 + n1)
+    A = rng.normal(0, 0.02, (768, 256))
+    M = be.prepare(BSGS, A, lvl, n1)
+    info = M.info()
+    assert (info["n1"], info["n2"], info["blocks"]) == (expect[0], expect[1], 3)
+    be.gen_rotation_keys(M.rotations())
+    ct = be.encrypt(np.tile(rng.uniform(-1, 1, 256), be.slots // 256), lvl)
+    outs, rep = be.matvec(M, ct)
+    assert rep["rotations"] == (expect[0] - 1) + 3 * (expect[1] - 1)
+    pl, d, p1, p2, blocks = pack_bsgs(A, be.slots, expect[0])
+    diags = encode_diags(ov, pl, lvl)
+    exp = ov.orc.matvec_bsgs(ov.ct(ct), lvl + 1, p1, p2, blocks, diags, ov.keys(M.rotations()), lazy=LAZY)
+    assert np.array_equal(out_words(ov, outs, lvl), exp)
+
+
 @pytest.mark.parametrize("prune", [0, 5])
 def test_c2s_bsgs_packed_p40_words_vs_oracle(prune):
     """d = 1024 (n1 = n2 = 32), one block of 32 rows, one token: the packed
