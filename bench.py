@@ -457,6 +457,9 @@ def ffn_bsgs_bench(torch, chain, special, args, iters=5, tokens=128):
         if tokens > 0:
             # token chunk bounded by the working set: inner sums [n2][chunk][blocks] + baby sets [chunk][n1]
             chunk = 8 if d >= 4096 else (32 if method == BSGS_STACKED else 16)
+            sq = 1 << ((d.bit_length()) // 2)  # the SPEC split's n1
+            if info["n1"] > sq:  # a longer baby side: proportionally fewer tokens per chunk
+                chunk = max(1, chunk * sq // info["n1"])
             # T tokens through the same matrix, key switches batched over a chunk
             # of `chunk` tokens (hxc_matvec_tokens); per-token throughput
             xt = [be.encrypt(np.tile(np.concatenate([rng.uniform(-1, 1, M.shape[1]), np.zeros(d - M.shape[1])]),
