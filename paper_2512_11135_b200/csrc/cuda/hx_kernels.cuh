@@ -518,8 +518,10 @@ __global__ void __launch_bounds__(256, HX_KSI_MINB) ks_inner_kernel(InnerArgs A,
   }
   const int src = (A.g == 1) ? t : (int)ntt_auto_index((u32)t, A.g, A.logn);
   // this CTA's slice of the elements; BB ciphertexts per iteration so that
-  // 8 x BB independent digit loads are in flight per thread
-  constexpr int BB = MAXD <= 8 ? 2 : 1;
+  // MAXD x BB (8-16) independent digit loads are in flight per thread -- at
+  // the low levels of the ct-ct matmul (dnum = 1 or 2) that is 8 / 4
+  // ciphertexts per iteration
+  constexpr int BB = MAXD <= 1 ? 8 : MAXD <= 2 ? 4 : MAXD <= 8 ? 2 : 1;
   const int per = (E + A.slices - 1) / A.slices;
   const int b_lo = slice * per, b_hi = min(E, b_lo + per);
   const long long dstride = (long long)A.dnum * ext * N;

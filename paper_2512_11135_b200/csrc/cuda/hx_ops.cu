@@ -654,7 +654,11 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
     // integer-class limbs: on the side stream when modup forked it
     const cudaStream_t s = rows_deferred && c->side_open ? c->side : s_main;
     dim3 grid((unsigned)(c->N() / th), (unsigned)ni, gz);
-    if (A.dnum <= 4)
+    if (A.dnum <= 1)
+      hx::ks_inner_kernel<1><<<grid, th, 0, s>>>(A, il);
+    else if (A.dnum <= 2)
+      hx::ks_inner_kernel<2><<<grid, th, 0, s>>>(A, il);
+    else if (A.dnum <= 4)
       hx::ks_inner_kernel<4><<<grid, th, 0, s>>>(A, il);
     else if (A.dnum <= 8)
       hx::ks_inner_kernel<8><<<grid, th, 0, s>>>(A, il);
