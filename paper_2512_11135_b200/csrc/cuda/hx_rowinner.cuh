@@ -42,6 +42,17 @@ constexpr int kRowInnerMaxKeys = 64;
 #define HX_RI_PREFETCH 0
 #endif
 constexpr bool kRiPrefetch = HX_RI_PREFETCH != 0;
+// HX_RI_KEYPF: at the top of a digit's iteration every thread asks L1 for one
+// 128-byte line of each of the digit's two key tiles (the tile is T lines), so
+// the 32 key loads at the end of the iteration -- after the ROW stages -- hit
+// L1 instead of waiting on L2 / HBM; 2: also the next digit's COL-pass tile
+#ifndef HX_RI_KEYPF
+#define HX_RI_KEYPF 0
+#endif
+constexpr int kRiKeyPf = HX_RI_KEYPF;
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p));
+}
 // shared memory of ks_row_inner_f64_kernel: exchange tile + ROW twiddles
 // (ntt_smem_bytes<true, S, OB, true>) + two prefetch tiles
 template <int S, int OB>
@@ -145,6 +156,14 @@ __global__ void __launch_bounds__((1 << (S + OB)) / 16, HX_ROWINNER_MINB) ks_row
     if (d >= A.dnum) break;
     const u64* kd0 = K0 + (long long)(2 * d) * full * N;
     const u64* kd1 = kd0 + (long long)full * N;
+    if (kRiKeyPf) {  // TILE words = T lines of 16 words: one line per thread and key poly
+      prefetch_l1(kd0 + 16 * t);
+      prefetch_l1(kd1 + 16 * t);
+      if (kRiKeyPf > 1) {
+        const int dn = next_digit(d + 1);
+        if (dn < A.dnum) prefetch_l1(Db + (long long)dn * ext * N + 16 * t);
+      }
+    }
     if (kRiPrefetch && d != down) {
       prefetch(next_digit(d + 1), slot ^ 1);
       asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // twiddles + this digit's tile
