@@ -900,7 +900,11 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
     // one token over few rows: the streaming CUDA-core MACs are faster (measured:
     // 32 rows x n1 = 32 at T = 1 is 16.1 vs 12.8 ms per FFN W1 stacked matvec;
     // at 96 rows the tensor cores win, 7.3 ms vs 3 x 2.7 ms of the P40 MAC)
-    ok = ok && (T >= 2 || blocks * n2 >= 96);
+    static const int tc_min_rows = [] {
+      const char* e = getenv("HX_TC_MIN_ROWS");  // A/B switch for the T = 1 threshold
+      return e ? atoi(e) : 96;
+    }();
+    ok = ok && (T >= 2 || blocks * n2 >= tc_min_rows);
     if (ok) {
       const int bpt = std::max(1, 128 / n2);
       for (int b0 = 0; b0 < blocks; b0 += bpt) {
