@@ -224,6 +224,14 @@ int hx_bsgs_p40_pack(hx_ctx* ctx, void* packed, const uint64_t* diags, int diag_
                      int diag_jstride, int n_q, void* stream);
 int hx_bsgs_mac_p40(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, const uint64_t* baby, const void* packed,
                     const uint64_t* diags, int diag_limbs, int n1, int n2, int diag_jstride, int n_q, void* stream);
+/* The same over `blocks` row blocks in one launch (the baby steps are read and
+ * split once for all of them): the diagonals of block b follow those of block
+ * b - 1 (diagonal (b, j, k) at diags + ((b n2 + j) n1 + k) diag_limbs N),
+ * `packed` was made by hx_bsgs_p40_pack with n2 * blocks rows, and the inner
+ * sum of (b, j) is written at inner + j inner_jstride + b inner_bstride. */
+int hx_bsgs_mac_p40_blocks(hx_ctx* ctx, uint64_t* inner, long long inner_jstride, long long inner_bstride,
+                           const uint64_t* baby, const void* packed, const uint64_t* diags, int diag_limbs, int n1,
+                           int n2, int blocks, int diag_jstride, int n_q, void* stream);
 
 /* Tensor-core BSGS MAC (tcgen05.mma kind::i8 on byte-sliced words, TMEM
  * accumulators, bulk-copy-streamed diagonals; hx_bsgs_tc.cu).  The diagonals of

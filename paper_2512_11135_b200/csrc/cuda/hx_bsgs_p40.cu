@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(32 * kP40Warps, (KPT <= 4 ? 4 : 2)) bsgs_mac_p
       const double v = __dadd_rn(__dadd_rn(mulmod_f64(Sm[0], P.r40_d, P.r40_q, P.qd),
                                            mulmod_f64(Sm[1], P.r20_d, P.r20_q, P.qd)),
                                  centre_f64(Sm[2], P.qd, P.qinv_d));
-      A.inner[(long long)j * A.out_jstride + c * L + i * N + t] =
+      const int jb = j / A.rpb, jj = j - jb * A.rpb;
+      A.inner[(long long)jj * A.out_jstride + (long long)jb * A.out_bstride + c * L + i * N + t] =
           f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);
     }
   }

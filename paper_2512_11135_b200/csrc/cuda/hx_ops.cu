@@ -1931,9 +1931,18 @@ int hx_bsgs_p40_pack(hx_ctx* c, void* packed, const uint64_t* diags, int diag_li
 
 int hx_bsgs_mac_p40(hx_ctx* c, uint64_t* inner, long long inner_jstride, const uint64_t* baby, const void* packed,
                     const uint64_t* diags, int diag_limbs, int n1, int n2, int diag_jstride, int n_q, void* s) {
+  return hx_bsgs_mac_p40_blocks(c, inner, inner_jstride, 0, baby, packed, diags, diag_limbs, n1, n2, 1, diag_jstride,
+                                n_q, s);
+}
+
+int hx_bsgs_mac_p40_blocks(hx_ctx* c, uint64_t* inner, long long inner_jstride, long long inner_bstride,
+                           const uint64_t* baby, const void* packed, const uint64_t* diags, int diag_limbs, int n1,
+                           int n2, int blocks, int diag_jstride, int n_q, void* s) {
   return guarded([&] {
     check_ctx(c);
     check_nq(c, n_q);
+    HX_REQUIRE(blocks >= 1 && (blocks == 1 || diag_jstride == 0 || diag_jstride == n1),
+               "bsgs_mac_p40: several blocks need contiguous diagonals (diag_jstride = n1)");
     HX_REQUIRE(p40_shape_ok(c, n1, n2, n_q) && diag_limbs >= n_q, "bsgs_mac_p40: bad shape (n1 in {32, 64})");
     HX_REQUIRE(inner && baby && packed && diags, "bsgs_mac_p40: null buffer");
     const int dj = diag_jstride ? diag_jstride : n1;
@@ -1952,8 +1961,10 @@ int hx_bsgs_mac_p40(hx_ctx* c, uint64_t* inner, long long inner_jstride, const u
     A.limbs = dl;
     A.pc = c->d_pc;
     A.out_jstride = inner_jstride;
+    A.out_bstride = inner_bstride;
+    A.rpb = n2;
     A.n1 = n1;
-    A.n2 = n2;
+    A.n2 = n2 * blocks;  // rows of one launch: every block's giant steps
     A.n_q = n_q;
     A.logn = c->logn;
     A.stages = hx::p40_stages(n1);
@@ -1962,11 +1973,11 @@ int hx_bsgs_mac_p40(hx_ctx* c, uint64_t* inner, long long inner_jstride, const u
       hx::launch_bsgs_mac_p40(A, (int)P.p40.size(), S(s));
     }
     launched(c, "bsgs_mac_p40_kernel");
-    if (!P.wide.empty()) {  // the wide limbs (60-bit q_0): 128-bit integer MAC over the u64 words
+    for (int b = 0; b < blocks && !P.wide.empty(); ++b) {  // the wide limbs (60-bit q_0): 128-bit integer MAC over the u64 words
       hx::MacArgs M;
-      M.inner = (u64*)inner;
+      M.inner = (u64*)inner + (long long)b * inner_bstride;
       M.baby = (const u64*)baby;
-      M.diags = (const u64*)diags;
+      M.diags = (const u64*)diags + (long long)b * n2 * dj * diag_limbs * c->N();
       M.pc = c->d_pc;
       M.n1 = n1;
       M.n2 = n2;

@@ -79,6 +79,10 @@ struct P40Args {
   const int* limbs;             // P40 limb list (p -> chain limb i)
   const PrimeConst* pc;
   long long out_jstride;
+  // rows r < n2 are (row block r / rpb, giant step r % rpb): inner sum at
+  // inner + (r % rpb) out_jstride + (r / rpb) out_bstride (one block: rpb = n2)
+  long long out_bstride;
+  int rpb;
   int n1, n2, n_q, logn, stages;
 };
 int p40_stages(int n1);

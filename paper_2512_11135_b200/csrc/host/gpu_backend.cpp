@@ -939,6 +939,36 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       have_scale = false;
     }
   }
+  // ---- one token, several dense row blocks whose diagonals follow one another
+  // in one buffer: ONE packed (P40) MAC launch over all blocks x n2 rows -- the
+  // baby steps are loaded and split once for every block and a CTA streams
+  // blocks x n2 stages instead of n2 (the cost-tuned W1 split has n2 = 16)
+  bool p40_merged = false;
+  if (!tc_done && T == 1 && blocks > 1 && n1 <= 64 && diags[0].payload) {
+    static const bool merge = [] {
+      const char* e = getenv("HX_P40_MERGE");
+      return !e || atoi(e) != 0;
+    }();
+    const GpuPlaintext* q0 = &payload(diags[0]);
+    bool ok = merge;
+    for (std::size_t i = 0; i < (std::size_t)blocks * d && ok; ++i) {
+      if (!diags[i].payload) {
+        ok = false;
+        break;
+      }
+      const auto& pi = payload(diags[i]);
+      ok = pi.buf == q0->buf && pi.offset == q0->offset + i * ptw && diags[i].level == level &&
+           diags[i].scale == diags[0].scale;
+    }
+    if (ok) {
+      if (auto pk = p40_pack(ctx_, q0->buf, q0->data(), n1, blocks * n2, n1, nqv)) {
+        ck(hx_bsgs_mac_p40_blocks(ctx_, inner->ptr, (long long)jstride, (long long)ctw, baby_ptr[0], pk->ptr,
+                                  q0->data(), nqv, n1, n2, blocks, n1, nqv, cur()),
+           "bsgs_mac_p40_blocks");
+        p40_merged = true;
+      }
+    }
+  }
   for (int b = 0; b < blocks && !tc_done; ++b) {
     const Plaintext* D = diags.data() + (std::size_t)b * d;
     std::uint64_t ptmuls = 0, adds = 0;
@@ -967,8 +997,10 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       const long long bstride = T > 1 ? (long long)(baby_ptr[1] - baby_ptr[0]) : 0;
       for (int t = 1; t < T && uniform; ++t) uniform = (long long)(baby_ptr[t] - baby_ptr[t - 1]) == bstride;
       std::shared_ptr<DeviceBuffer> pk;
-      if (T == 1 && n1 <= 64) pk = p40_pack(ctx_, p0->buf, p0->data(), n1, n2, n1, nqv);
-      if (pk) {
+      if (T == 1 && n1 <= 64 && !p40_merged) pk = p40_pack(ctx_, p0->buf, p0->data(), n1, n2, n1, nqv);
+      if (p40_merged) {
+        // this block's inner sums came from the merged launch above
+      } else if (pk) {
         ck(hx_bsgs_mac_p40(ctx_, inner->ptr + (std::size_t)b * ctw, (long long)jstride, baby_ptr[0], pk->ptr,
                            p0->data(), nqv, n1, n2, n1, nqv, cur()),
            "bsgs_mac_p40");

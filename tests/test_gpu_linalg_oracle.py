@@ -204,7 +204,10 @@ def test_c2s_bsgs_explicit_plan_words_vs_oracle(n1, expect):
     assert (info["n1"], info["n2"], info["blocks"]) == (expect[0], expect[1], 3)
     be.gen_rotation_keys(M.rotations())
     ct = be.encrypt(np.tile(rng.uniform(-1, 1, 256), be.slots // 256), lvl)
-    outs, rep = be.matvec(M, ct)
+    (outs, rep), n_p40 = _launches(be, "bsgs_mac_p40_kernel", lambda: be.matvec(M, ct))
+    # n1 in {32, 64}: the three dense blocks go through ONE packed MAC launch
+    # (hx_bsgs_mac_p40_blocks: 3 x n2 rows); n1 = 8 takes the streaming u64 MAC
+    assert n_p40 == (1 if expect[0] >= 32 else 0)
     assert rep["rotations"] == (expect[0] - 1) + 3 * (expect[1] - 1)
     pl, d, p1, p2, blocks = pack_bsgs(A, be.slots, expect[0])
     diags = encode_diags(ov, pl, lvl)
