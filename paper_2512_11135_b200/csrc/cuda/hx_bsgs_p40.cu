@@ -104,6 +104,8 @@ __global__ void __launch_bounds__(32 * kP40Warps, (KPT <= 4 ? 4 : 2)) bsgs_mac_p
       bl[kk][c] = p40_dbl((u32)(v & 0xFFFFFull));
     }
   }
+  int jj = 0;           // row j = (block jb, giant step jj), tracked without a division
+  long long boff = 0;   // jb out_bstride
   for (int j = 0; j < n2; ++j) {
     const int slot = j % S;
     p40_wait(&full[slot], (u32)((j / S) & 1));
@@ -153,9 +155,12 @@ __global__ void __launch_bounds__(32 * kP40Warps, (KPT <= 4 ? 4 : 2)) bsgs_mac_p
       const double v = __dadd_rn(__dadd_rn(mulmod_f64(Sm[0], P.r40_d, P.r40_q, P.qd),
                                            mulmod_f64(Sm[1], P.r20_d, P.r20_q, P.qd)),
                                  centre_f64(Sm[2], P.qd, P.qinv_d));
-      const int jb = j / A.rpb, jj = j - jb * A.rpb;
-      A.inner[(long long)jj * A.out_jstride + (long long)jb * A.out_bstride + c * L + i * N + t] =
+      A.inner[(long long)jj * A.out_jstride + boff + c * L + i * N + t] =
           f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);
+    }
+    if (++jj == A.rpb) {
+      jj = 0;
+      boff += A.out_bstride;
     }
   }
 }
