@@ -24,6 +24,8 @@
 // combine also releases the stage slot for the next copy.  Bytes in flight
 // come from shared memory, not registers, so the kernel keeps the 64-register
 // budget of 32 resident warps.
+#include <cstdlib>
+
 #include "hx_internal.h"
 
 namespace hx {
@@ -165,6 +167,120 @@ __global__ void __launch_bounds__(32 * kP40Warps, (KPT <= 4 ? 4 : 2)) bsgs_mac_p
   }
 }
 
+// RPS giant rows per step.  The per-row cross-warp combine of the kernel above
+// is its critical path (ncu: "barrier" is the top stall -- warps 0-1 reduce
+// every row on top of their own products while the other six wait at the next
+// row's barrier).  With RPS rows per barrier 2 RPS warps reduce one (row,
+// poly) each, so the combine costs every reducing warp one reduction per RPS
+// rows of products.  A stage is RPS consecutive rows (they are contiguous in
+// the P40 layout: one bulk copy), the partial sums live in dynamic shared
+// memory behind the stage ring.  Rows of one step never straddle row blocks
+// (host: rows per block % RPS == 0).  Same words as the kernel above.
+template <int KPT, int RPS>
+__global__ void __launch_bounds__(32 * kP40Warps, 2) bsgs_mac_p40x_kernel(P40Args A) {
+  __shared__ u64 full[kP40MaxStages];
+  extern __shared__ __align__(128) unsigned char stages[];
+  const long long N = 1ll << A.logn;
+  const int tile = blockIdx.x, p = blockIdx.y;
+  const int i = A.limbs[p];
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const long long t = (long long)tile * kP40TT + lane;
+  const PrimeConst& P = A.pc[i];
+  const long long L = (long long)A.n_q * N;
+  const u32 SB = 5u * A.n1 * kP40TT;  // bytes of one row
+  const u32 SS = RPS * SB;            // bytes of one stage
+  const int S = A.stages, steps = A.n2 / RPS;
+  // [buf][warp][row][poly][S11,S10,S00][lane]
+  double(*part)[kP40Warps][RPS][2][3][32] =
+      reinterpret_cast<double(*)[kP40Warps][RPS][2][3][32]>(stages + (size_t)S * SS);
+  const unsigned char* src = A.packed + (((size_t)p * (size_t)(N / kP40TT) + tile) * A.n2) * SB;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) p40_bar_init(&full[s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < S && s < steps; ++s) {
+      p40_expect(&full[s], SS);
+      p40_copy(stages + (size_t)s * SS, src + (size_t)s * SS, SS, &full[s]);
+    }
+  }
+  double bh[KPT][2], bl[KPT][2];
+#pragma unroll
+  for (int kk = 0; kk < KPT; ++kk) {
+    const int k = w * KPT + kk;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const u64 v = A.baby[(2ll * k + c) * L + i * N + t];
+      bh[kk][c] = p40_dbl((u32)(v >> 20));
+      bl[kk][c] = p40_dbl((u32)(v & 0xFFFFFull));
+    }
+  }
+  int jj = 0;          // giant step of the step's first row inside its row block
+  long long boff = 0;  // that block's output offset
+  for (int js = 0; js < steps; ++js) {
+    const int slot = js % S;
+    p40_wait(&full[slot], (u32)((js / S) & 1));
+    const int buf = js & 1;
+#pragma unroll
+    for (int rr = 0; rr < RPS; ++rr) {
+      const unsigned char* st = stages + (size_t)slot * SS + (size_t)rr * SB;
+      const uint2* lo = reinterpret_cast<const uint2*>(st);
+      const u32* hi = reinterpret_cast<const u32*>(st + 4 * A.n1 * kP40TT);
+      u32 lw[KPT], hw[KPT / 4];
+#pragma unroll
+      for (int q = 0; q < KPT / 2; ++q) {
+        const uint2 v = lo[(w * KPT / 2 + q) * kP40TT + lane];
+        lw[2 * q] = v.x;
+        lw[2 * q + 1] = v.y;
+      }
+#pragma unroll
+      for (int q = 0; q < KPT / 4; ++q) hw[q] = hi[(w * KPT / 4 + q) * kP40TT + lane];
+      double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
+#pragma unroll
+      for (int kk = 0; kk < KPT; ++kk) {
+        const u32 l = lw[kk], h = (hw[kk >> 2] >> (8 * (kk & 3))) & 0xFFu;
+        const double xh = p40_dbl((l >> 20) | (h << 12)), xl = p40_dbl(l & 0xFFFFFu);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          s[c][0] = __fma_rn(xh, bh[kk][c], s[c][0]);
+          s[c][1] = __fma_rn(xh, bl[kk][c], s[c][1]);
+          s[c][1] = __fma_rn(xl, bh[kk][c], s[c][1]);
+          s[c][2] = __fma_rn(xl, bl[kk][c], s[c][2]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int m = 0; m < 3; ++m) part[buf][w][rr][c][m][lane] = s[c][m];
+    }
+    __syncthreads();  // every warp is done with stage js: its slot takes stage js + S
+    if (tid == 0 && js + S < steps) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      p40_expect(&full[slot], SS);
+      p40_copy(stages + (size_t)slot * SS, src + (size_t)(js + S) * SS, SS, &full[slot]);
+    }
+    if (tid < 64 * RPS) {  // warps 0 .. 2 RPS - 1: one (row, poly) each
+      const int rr = tid >> 6, c = (tid >> 5) & 1;
+      double Sm[3] = {0, 0, 0};
+#pragma unroll
+      for (int ww = 0; ww < kP40Warps; ++ww)
+#pragma unroll
+        for (int m = 0; m < 3; ++m) Sm[m] = __dadd_rn(Sm[m], part[buf][ww][rr][c][m][lane]);
+      const double v = __dadd_rn(__dadd_rn(mulmod_f64(Sm[0], P.r40_d, P.r40_q, P.qd),
+                                           mulmod_f64(Sm[1], P.r20_d, P.r20_q, P.qd)),
+                                 centre_f64(Sm[2], P.qd, P.qinv_d));
+      A.inner[(long long)(jj + rr) * A.out_jstride + boff + c * L + i * N + t] =
+          f64bits_to_residue((u64)__double_as_longlong(v), P.qd, P.qinv_d);
+    }
+    jj += RPS;
+    if (jj == A.rpb) {
+      jj = 0;
+      boff += A.out_bstride;
+    }
+  }
+}
+
 // P40 packing: thread (lane = coefficient, k slice) of block (tile, j, p)
 __global__ void p40_pack_kernel(unsigned char* dst, const u64* diags, long long diag_stride, const int* limbs,
                                 int n1, int n2, int dj, int logn) {
@@ -193,11 +309,41 @@ void launch_p40_pack(unsigned char* dst, const u64* diags, long long diag_stride
 
 int p40_stages(int n1) { return n1 <= 32 ? 6 : 8; }
 
-void launch_bsgs_mac_p40(const P40Args& A, int n_p40, cudaStream_t s) {
+void launch_bsgs_mac_p40(const P40Args& A0, int n_p40, cudaStream_t s) {
+  P40Args A = A0;
   const long long N = 1ll << A.logn;
   const int kpt = A.n1 / kP40Warps;
-  const size_t smem = (size_t)A.stages * 5 * A.n1 * kP40TT;
   dim3 grid((unsigned)(N / kP40TT), (unsigned)n_p40);
+  // two giant rows per step (bsgs_mac_p40x_kernel) whenever the rows per block
+  // are even: 9.24 -> 7.72 ms at n1 = n2 = 64, 2.78 -> 2.61 ms at 32 (measured);
+  // HX_P40_RPS=1 / HX_P40_RPS4=1: the one-row kernel for n1 = 64 / 32 (A/B)
+  static const int rps_env = [] {
+    const char* e = getenv("HX_P40_RPS");
+    return e ? atoi(e) : 2;
+  }();
+  static const int rps4_env = [] {
+    const char* e = getenv("HX_P40_RPS4");
+    return e ? atoi(e) : 2;
+  }();
+  const int rps = kpt == 8 ? rps_env : rps4_env;
+  if (rps == 2 && A.rpb % 2 == 0) {
+    constexpr int RPS = 2;
+    A.stages = 3;  // 3 x 2 rows in flight
+    const size_t smem = (size_t)A.stages * RPS * 5 * A.n1 * kP40TT + sizeof(double) * 2 * kP40Warps * RPS * 2 * 3 * 32;
+    auto gox = [&](auto kern) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<grid, 32 * kP40Warps, smem, s>>>(A);
+    };
+    if (kpt == 8) {
+      gox(bsgs_mac_p40x_kernel<8, RPS>);
+      return;
+    }
+    if (kpt == 4) {
+      gox(bsgs_mac_p40x_kernel<4, RPS>);
+      return;
+    }
+  }
+  const size_t smem = (size_t)A.stages * 5 * A.n1 * kP40TT;
   auto go = [&](auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     kern<<<grid, 32 * kP40Warps, smem, s>>>(A);

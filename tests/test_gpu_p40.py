@@ -4,7 +4,9 @@ CUDA-core MAC over the u64 words (hx_bsgs_mac_tokens) and vs the CPU oracle's
 MAC (hxo_bsgs_mac, the mul_acc loop of matvec_bsgs), word for
 word: every n1 the kernel takes (32, 64), blocks whose giant groups
 are further apart than n1 (diag_jstride), n2 not a multiple of the stage
-ring, the 60-bit q_0 on the integer kernel, and the FFN shapes at N = 2^16."""
+ring, odd row counts (one row per step) and even ones (two rows per step,
+bsgs_mac_p40x_kernel), the 60-bit q_0 on the integer kernel, and the FFN
+shapes at N = 2^16."""
 import numpy as np
 import pytest
 
@@ -65,7 +67,10 @@ def run_case(name, n1, n2, dj, seed, oracle_limbs=None):
         assert np.array_equal(got[:, :, k:k + 1, :], exp), k
 
 
-@pytest.mark.parametrize("n1,n2,dj", [(32, 3, 32), (32, 32, 32), (64, 9, 64), (32, 5, 40), (64, 1, 64)])
+@pytest.mark.parametrize("n1,n2,dj", [(32, 3, 32), (32, 32, 32), (64, 9, 64), (32, 5, 40), (64, 1, 64),
+                                       # even row counts: the two-rows-per-step kernel (1 / 2 / 3 / 5 steps; a
+                                       # giant-group stride wider than n1)
+                                       (32, 2, 32), (64, 4, 64), (64, 6, 80), (32, 10, 32)])
 def test_p40_mac_n12_vs_oracle(n1, n2, dj):
     run_case("c2s", n1, n2, dj, 100 + n1 + n2)
 
