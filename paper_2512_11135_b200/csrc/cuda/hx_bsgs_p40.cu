@@ -175,9 +175,12 @@ __global__ void __launch_bounds__(32 * kP40Warps, (KPT <= 4 ? 4 : 2)) bsgs_mac_p
 // rows of products.  A stage is RPS consecutive rows (they are contiguous in
 // the P40 layout: one bulk copy), the partial sums live in dynamic shared
 // memory behind the stage ring.  Rows of one step never straddle row blocks
-// (host: rows per block % RPS == 0).  Same words as the kernel above.
-template <int KPT, int RPS>
-__global__ void __launch_bounds__(32 * kP40Warps, 2) bsgs_mac_p40x_kernel(P40Args A) {
+// (host: rows per block % RPS == 0).  NW warps split the n1 baby steps (KPT
+// each): n1 = 64 runs 8 warps x 8, n1 = 32 runs 4 warps x 8 so that with two
+// rows per step every warp reduces one (row, poly) -- the combine is then
+// balanced over the CTA.  Same words as the kernel above.
+template <int KPT, int RPS, int NW>
+__global__ void __launch_bounds__(32 * NW, (NW <= 4 ? 4 : 2)) bsgs_mac_p40x_kernel(P40Args A) {
   __shared__ u64 full[kP40MaxStages];
   extern __shared__ __align__(128) unsigned char stages[];
   const long long N = 1ll << A.logn;
@@ -191,8 +194,8 @@ __global__ void __launch_bounds__(32 * kP40Warps, 2) bsgs_mac_p40x_kernel(P40Arg
   const u32 SS = RPS * SB;            // bytes of one stage
   const int S = A.stages, steps = A.n2 / RPS;
   // [buf][warp][row][poly][S11,S10,S00][lane]
-  double(*part)[kP40Warps][RPS][2][3][32] =
-      reinterpret_cast<double(*)[kP40Warps][RPS][2][3][32]>(stages + (size_t)S * SS);
+  double(*part)[NW][RPS][2][3][32] =
+      reinterpret_cast<double(*)[NW][RPS][2][3][32]>(stages + (size_t)S * SS);
   const unsigned char* src = A.packed + (((size_t)p * (size_t)(N / kP40TT) + tile) * A.n2) * SB;
   if (tid == 0) {
     for (int s = 0; s < S; ++s) p40_bar_init(&full[s]);
@@ -260,11 +263,12 @@ __global__ void __launch_bounds__(32 * kP40Warps, 2) bsgs_mac_p40x_kernel(P40Arg
       p40_expect(&full[slot], SS);
       p40_copy(stages + (size_t)slot * SS, src + (size_t)(js + S) * SS, SS, &full[slot]);
     }
+    static_assert(2 * RPS <= NW, "one reducing warp per (row, poly)");
     if (tid < 64 * RPS) {  // warps 0 .. 2 RPS - 1: one (row, poly) each
       const int rr = tid >> 6, c = (tid >> 5) & 1;
       double Sm[3] = {0, 0, 0};
 #pragma unroll
-      for (int ww = 0; ww < kP40Warps; ++ww)
+      for (int ww = 0; ww < NW; ++ww)
 #pragma unroll
         for (int m = 0; m < 3; ++m) Sm[m] = __dadd_rn(Sm[m], part[buf][ww][rr][c][m][lane]);
       const double v = __dadd_rn(__dadd_rn(mulmod_f64(Sm[0], P.r40_d, P.r40_q, P.qd),
@@ -329,17 +333,24 @@ void launch_bsgs_mac_p40(const P40Args& A0, int n_p40, cudaStream_t s) {
   if (rps == 2 && A.rpb % 2 == 0) {
     constexpr int RPS = 2;
     A.stages = 3;  // 3 x 2 rows in flight
-    const size_t smem = (size_t)A.stages * RPS * 5 * A.n1 * kP40TT + sizeof(double) * 2 * kP40Warps * RPS * 2 * 3 * 32;
-    auto gox = [&](auto kern) {
+    auto gox = [&](auto kern, int nw) {
+      const size_t smem = (size_t)A.stages * RPS * 5 * A.n1 * kP40TT + sizeof(double) * 2 * nw * RPS * 2 * 3 * 32;
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kern<<<grid, 32 * kP40Warps, smem, s>>>(A);
+      kern<<<grid, 32 * nw, smem, s>>>(A);
     };
     if (kpt == 8) {
-      gox(bsgs_mac_p40x_kernel<8, RPS>);
+      gox(bsgs_mac_p40x_kernel<8, RPS, 8>, 8);
       return;
     }
-    if (kpt == 4) {
-      gox(bsgs_mac_p40x_kernel<4, RPS>);
+    if (kpt == 4) {  // n1 = 32
+      static const int nw4 = [] {  // HX_P40_NW4=8: 8 warps x 4 baby steps (A/B)
+        const char* e = getenv("HX_P40_NW4");
+        return e ? atoi(e) : 4;
+      }();
+      if (nw4 == 4)
+        gox(bsgs_mac_p40x_kernel<8, RPS, 4>, 4);
+      else
+        gox(bsgs_mac_p40x_kernel<4, RPS, 8>, 8);
       return;
     }
   }
