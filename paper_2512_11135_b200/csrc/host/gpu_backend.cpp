@@ -897,14 +897,17 @@ std::vector<std::vector<Ciphertext>> GpuLatticeBackend::bsgs_blocks_tokens(
       ++nlive;
     }
     ok = ok && src && 2 * nlive >= (std::size_t)blocks * d;  // sparse matrices: the index-list MAC
-    // one token over few rows: the streaming CUDA-core MACs are faster (measured:
-    // 32 rows x n1 = 32 at T = 1 is 16.1 vs 12.8 ms per FFN W1 stacked matvec;
-    // at 96 rows the tensor cores win, 7.3 ms vs 3 x 2.7 ms of the P40 MAC)
+    // one token: the packed (P40) MAC wherever it applies (n1 = 32 / 64; two rows
+    // per step, all row blocks in one launch: W1's 96 rows x n1 = 32 take 25.1 ms
+    // per matvec against 27.1 on the tensor cores), else the tensor cores from 96
+    // rows (below that the streaming CUDA-core MAC is faster)
     static const int tc_min_rows = [] {
       const char* e = getenv("HX_TC_MIN_ROWS");  // A/B switch for the T = 1 threshold
       return e ? atoi(e) : 96;
     }();
-    ok = ok && (T >= 2 || blocks * n2 >= tc_min_rows);
+    static const bool tc_over_p40 = getenv("HX_TC_OVER_P40") != nullptr;  // A/B: the round-2 choice
+    const bool p40_shape = p40_mac_enabled() && (n1 == 32 || n1 == 64) && !tc_over_p40;
+    ok = ok && (T >= 2 || (blocks * n2 >= tc_min_rows && !p40_shape));
     if (ok) {
       const int bpt = std::max(1, 128 / n2);
       for (int b0 = 0; b0 < blocks; b0 += bpt) {
