@@ -876,7 +876,7 @@ def main():
                                                       stream=stream), 5, 2, stream) / 5
     n40 = sum(1 for q in chain if q < (1 << 40))
     p40_bytes = (mn1 * mn2 * (n40 * 5 + (nq - n40) * 8) + (2 * mn1 + 2 * mn2) * nq * 8) * N
-    roofline_mac["p40"] = {"kernel": "bsgs_mac_p40_kernel (+ bsgs_mac_int_kernel for q_0), same block",
+    roofline_mac["p40"] = {"kernel": "bsgs_mac_p40x_kernel<8,2,4> (packed 5-byte diagonals, two rows per step, four warps; + bsgs_mac_int_kernel for q_0), same block",
                            "ms": p40_s * 1e3, "achieved": p40_bytes / p40_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
                            "frac": p40_bytes / p40_s / 1e9 / hbm_peak, "algorithmic_bytes_per_launch": p40_bytes,
                            "u64_equivalent_GBps": mac_bytes / p40_s / 1e9,
