@@ -366,14 +366,21 @@ template <int MAXD>
 __global__ void __launch_bounds__(256, HX_KSF_MINB) ks_inner_f64_kernel(InnerArgs A, const int* limbs) {
   const int N = 1 << A.logn;
   const int ext = A.n_q + A.n_special, full = A.n_chain + A.n_special;
+  // (key x slice) fastest, coefficient tile slowest: the CTAs in flight share one
+  // (limb, tile).  With hoisted rotations (shared digits, many keys) every key
+  // otherwise re-reads the chunk's digit limbs from HBM -- 58 GB of digit words
+  // against 7 GB of keys per 16-ciphertext chunk of the hoisted-32 batch; now
+  // the keys of a (limb, tile) run together and find the digits in L2 (default
+  // load policy when the digits are shared, evict-first when read once).
   const int j = limbs[blockIdx.y];
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.z * blockDim.x + threadIdx.x;
   const int kl = j < A.n_q ? j : A.n_chain + (j - A.n_q);
-  const int r = blockIdx.z / A.slices, slice = blockIdx.z % A.slices;
+  const int r = blockIdx.x / A.slices, slice = blockIdx.x % A.slices;
   const u64* key = A.keys[r];
   const int E = A.batch;
   const PrimeConst& P = A.pc[kl];
   const bool comp = (A.cmask >> r) & 1ull;
+  const bool reuse = A.shared && A.n_keys > 1;
   const u64 ta = (!comp || A.kg[r] <= 1) ? (u64)t : (u64)ntt_auto_index((u32)t, A.kg[r], A.logn);
   double kh[MAXD][2], klo[MAXD][2];
 #pragma unroll
@@ -402,7 +409,9 @@ __global__ void __launch_bounds__(256, HX_KSF_MINB) ks_inner_f64_kernel(InnerArg
     const u64* Cb = down >= 0 ? A.c1 + (ebase + b) * A.c1_stride + (long long)j * N + src : nullptr;
 #pragma unroll
     for (int d = 0; d < MAXD; ++d)
-      v[d] = d < A.dnum ? __ldcs(d == down ? Cb : Db + (long long)d * ext * N) : 0ull;
+      v[d] = d < A.dnum ? (reuse ? __ldg(d == down ? Cb : Db + (long long)d * ext * N)
+                                 : __ldcs(d == down ? Cb : Db + (long long)d * ext * N))
+                        : 0ull;
   };
   if (b_lo < b_hi) load(b_lo, vn);
   for (int b = b_lo; b < b_hi; ++b) {
@@ -434,15 +443,21 @@ __global__ void __launch_bounds__(256, HX_KSF_MINB) ks_inner_f64_kernel(InnerArg
 // the digit and key words of a (limb, coefficient) are all loaded up front
 // (3 dnum loads in flight per thread) and consumed at once, with the register
 // budget of 3 CTAs / SM instead of 2.
+// Grid: (key x element) runs FASTEST (blockIdx.x), the coefficient tile slowest
+// (blockIdx.z): the CTAs in flight then share one (limb, tile) digit slice --
+// with the tile fastest every key re-read all dnum digit limbs from HBM (ncu on
+// the 63 hoisted baby steps of a W1 matvec: 18.2 GB read for 12.2 GB of keys,
+// L2 hit rate 0.01 %).  The digits are loaded with the default policy, the
+// key words (used once) evict-first.
 template <int MAXD>
 __global__ void __launch_bounds__(256, 3) ks_inner_f64_one_kernel(InnerArgs A, const int* limbs) {
   const int N = 1 << A.logn;
   const int ext = A.n_q + A.n_special, full = A.n_chain + A.n_special;
   const int j = limbs[blockIdx.y];
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.z * blockDim.x + threadIdx.x;
   const int kl = j < A.n_q ? j : A.n_chain + (j - A.n_q);
   const int E = A.batch;
-  const int r = blockIdx.z / E, b = blockIdx.z % E;
+  const int r = blockIdx.x / E, b = blockIdx.x % E;
   const u64* key = A.keys[r];
   const PrimeConst& P = A.pc[kl];
   const bool comp = (A.cmask >> r) & 1ull;
@@ -457,51 +472,56 @@ __global__ void __launch_bounds__(256, 3) ks_inner_f64_one_kernel(InnerArgs A, c
 #pragma unroll
   for (int d = 0; d < MAXD; ++d) {
     if (d < A.dnum) {
-      v[d] = __ldcs(d == down ? Cb : Db + (long long)d * ext * N);
+      v[d] = __ldg(d == down ? Cb : Db + (long long)d * ext * N);
       if (comp) {
-        k0[d] = __ldg(key + ((long long)d * full + kl) * N + t);
+        k0[d] = __ldcs(key + ((long long)d * full + kl) * N + t);
         k1[d] = uniform_word(A.kseed[r], ((u64)d * full + kl) * N + ta, P.q);
       } else {
-        k0[d] = __ldg(key + (((long long)d * 2 + 0) * full + kl) * N + t);
-        k1[d] = __ldg(key + (((long long)d * 2 + 1) * full + kl) * N + t);
+        k0[d] = __ldcs(key + (((long long)d * 2 + 0) * full + kl) * N + t);
+        k1[d] = __ldcs(key + (((long long)d * 2 + 1) * full + kl) * N + t);
       }
     } else {
       v[d] = k0[d] = k1[d] = 0;
     }
   }
-  double s[2][3] = {{0, 0, 0}, {0, 0, 0}};
+  // one exact modular product per (digit, poly) (mulmod_f64h: 6 FP64
+  // instructions, no integer split) summed lazily (|acc| < dnum q) and
+  // normalised once -- as in ks_row_inner_f64_kernel.  With nothing to amortise
+  // over elements the 24-bit split MAC spent more instructions on splitting the
+  // 3 dnum words of every element (shift / mask / convert, 6 per word) than on
+  // its products: ncu showed the kernel issue-bound (70 % issue, DRAM 54 %).
+  double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
   for (int d = 0; d < MAXD; ++d) {
-    double xh, xl, ah, al, bh, bl;
-    split24_d(v[d], xh, xl);
-    split24_d(k0[d], ah, al);
-    split24_d(k1[d], bh, bl);
-    s[0][0] = __fma_rn(xh, ah, s[0][0]);
-    s[0][1] = __fma_rn(xh, al, s[0][1]);
-    s[0][1] = __fma_rn(xl, ah, s[0][1]);
-    s[0][2] = __fma_rn(xl, al, s[0][2]);
-    s[1][0] = __fma_rn(xh, bh, s[1][0]);
-    s[1][1] = __fma_rn(xh, bl, s[1][1]);
-    s[1][1] = __fma_rn(xl, bh, s[1][1]);
-    s[1][2] = __fma_rn(xl, bl, s[1][2]);
+    if (d < A.dnum) {
+      const double y = __longlong_as_double((long long)u64_to_f64bits(v[d]));
+      const double w0 = __longlong_as_double((long long)u64_to_f64bits(k0[d]));
+      const double w1 = __longlong_as_double((long long)u64_to_f64bits(k1[d]));
+      acc0 = __dadd_rn(acc0, mulmod_f64h(y, w0, P.qinv_d, P.qd));
+      acc1 = __dadd_rn(acc1, mulmod_f64h(y, w1, P.qinv_d, P.qd));
+    }
   }
   u64* ub = A.u + ((long long)r * E + b) * 2 * ext * N + (long long)j * N + t;
-  ub[0] = combine_split24(s[0], P);
-  ub[(long long)ext * N] = combine_split24(s[1], P);
+  ub[0] = f64bits_to_residue((u64)__double_as_longlong(acc0), P.qd, P.qinv_d);
+  ub[(long long)ext * N] = f64bits_to_residue((u64)__double_as_longlong(acc1), P.qd, P.qinv_d);
 }
 
 template <int MAXD>
 __global__ void __launch_bounds__(256, HX_KSI_MINB) ks_inner_kernel(InnerArgs A, const int* limbs) {
   const int N = 1 << A.logn;
   const int ext = A.n_q + A.n_special, full = A.n_chain + A.n_special;
+  // (key x slice) fastest, coefficient tile slowest: the CTAs in flight share one
+  // (limb, tile) -- its key words across the slices of a batch, its digit words
+  // across the keys of hoisted rotations (kept in L2: default load policy then)
   const int j = limbs ? limbs[blockIdx.y] : blockIdx.y;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.z * blockDim.x + threadIdx.x;
   const int kl = j < A.n_q ? j : A.n_chain + (j - A.n_q);
-  const int r = blockIdx.z / A.slices, slice = blockIdx.z % A.slices;
+  const int r = blockIdx.x / A.slices, slice = blockIdx.x % A.slices;
   const u64* key = A.keys[r];
   const int E = A.batch;
   const PrimeConst& P = A.pc[kl];
   const bool comp = (A.cmask >> r) & 1ull;
+  const bool reuse = A.shared && A.n_keys > 1;  // every key reads the same digits
   const u64 ta = (!comp || A.kg[r] <= 1) ? (u64)t : (u64)ntt_auto_index((u32)t, A.kg[r], A.logn);
   u64 k0[MAXD], k1[MAXD];
 #pragma unroll
@@ -536,7 +556,10 @@ __global__ void __launch_bounds__(256, HX_KSI_MINB) ks_inner_kernel(InnerArgs A,
       const u64* Cb = down >= 0 ? A.c1 + (ebase + b0 + bb) * A.c1_stride + (long long)j * N + src : nullptr;
 #pragma unroll
       for (int d = 0; d < MAXD; ++d)
-        v[bb][d] = (d < A.dnum && b0 + bb < b_hi) ? __ldcs(d == down ? Cb : Db + (long long)d * ext * N) : 0ull;
+        v[bb][d] = (d < A.dnum && b0 + bb < b_hi)
+                       ? (reuse ? __ldg(d == down ? Cb : Db + (long long)d * ext * N)
+                                : __ldcs(d == down ? Cb : Db + (long long)d * ext * N))
+                       : 0ull;
     }
 #pragma unroll
     for (int bb = 0; bb < BB; ++bb) {

@@ -636,14 +636,14 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
     R.logn = c->logn;
     launch_row_inner(c, R, s);
   } else if (nf > 0 && E <= 2 && !one_off) {  // no key reuse across elements: one element per block row
-    dim3 grid((unsigned)(c->N() / th), (unsigned)nf, (unsigned)(A.n_keys * E));
+    dim3 grid((unsigned)(A.n_keys * E), (unsigned)nf, (unsigned)(c->N() / th));  // keys fastest, tiles slowest
     if (A.dnum <= 4)
       hx::ks_inner_f64_one_kernel<4><<<grid, th, 0, s>>>(A, lists);
     else
       hx::ks_inner_f64_one_kernel<8><<<grid, th, 0, s>>>(A, lists);
     launched(c, "ks_inner_f64_one_kernel");
   } else if (nf > 0) {
-    dim3 grid((unsigned)(c->N() / th), (unsigned)nf, gz);
+    dim3 grid(gz, (unsigned)nf, (unsigned)(c->N() / th));  // (key, slice) fastest, tiles slowest
     if (A.dnum <= 4)
       hx::ks_inner_f64_kernel<4><<<grid, th, 0, s>>>(A, lists);
     else
@@ -653,7 +653,7 @@ void ks_inner_multi(hx_ctx* c, u64* u, const u64* digits, const std::vector<cons
   if (ni > 0) {
     // integer-class limbs: on the side stream when modup forked it
     const cudaStream_t s = rows_deferred && c->side_open ? c->side : s_main;
-    dim3 grid((unsigned)(c->N() / th), (unsigned)ni, gz);
+    dim3 grid(gz, (unsigned)ni, (unsigned)(c->N() / th));  // (key, slice) fastest, tiles slowest
     if (A.dnum <= 1)
       hx::ks_inner_kernel<1><<<grid, th, 0, s>>>(A, il);
     else if (A.dnum <= 2)
